@@ -1,0 +1,188 @@
+/* sim.h — C ABI of the B200-native vehicle-update hot path (arXiv 2406.10661).
+ *
+ * One simulation timestep of the paper's GPU microscopic traffic simulator
+ * (App. A2.2 "Execution Process"): per-lane ordering
+ * (P:130), leader / follower / side-neighbour lookup including the
+ * successor-lane substitution, IDM car following
+ * (P:156-167), randomized MOBIL lane changing, signal response
+ * (P:200), integration with hand-off into successor lanes,
+ * departure insertion, per-junction signal update (P:140-141,
+ * P:836-841) and travel / wait accounting.
+ * The exact model (incl. every reading of a silent passage) is DESIGN.md §1.
+ *
+ * Conventions (all entry points):
+ *   - every call returns sim_status; 0 = SIM_OK; nothing throws or aborts;
+ *   - input pointers are HOST pointers read during the call and copied; the
+ *     library never retains them; all device memory is owned by the library;
+ *   - sim_read_* write into CALLER-owned buffers (host memory unless stated);
+ *   - sim_step is asynchronous on the handle's stream; device faults and
+ *     capacity overflows surface at the next synchronising call
+ *     (sim_read_state / sim_read_metrics / sim_sync) and make the handle sticky
+ *     (SIM_E_STATE afterwards);
+ *   - setters take effect at the next step boundary (stream-ordered);
+ *     _batch variants equal the single calls applied in order;
+ *   - one controlling host thread per handle.
+ */
+#ifndef SIM_H
+#define SIM_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SIM_OK = 0,
+  SIM_E_INVALID = 1,   /* input violates a rule of DESIGN.md §1.1 (message via sim_last_error) */
+  SIM_E_RANGE = 2,     /* id / index out of range; nothing changed */
+  SIM_E_OOM = 3,       /* device allocation failed */
+  SIM_E_CUDA = 4,      /* CUDA runtime error (handle becomes sticky) */
+  SIM_E_NCCL = 5,      /* reserved: multi-GPU exchange failure */
+  SIM_E_STATE = 6,     /* destroyed / sticky handle */
+  SIM_E_CAPACITY = 7   /* a per-tile slot or inbox capacity overflowed (sticky) */
+} sim_status;
+
+typedef struct sim_s *sim_handle;   /* opaque, owned by the library */
+
+/* Lane graph (App. A2.1).  Host memory, caller-owned, CSR layout.
+ * Lanes are road lanes (lane_road >= 0, lane_junction == -1) or junction
+ * lanes (lane_road == -1, lane_junction >= 0).  A junction lane has exactly one
+ * predecessor and one successor, both road lanes.  Road lanes of a road have
+ * equal length and are listed leftmost first in road_lanes. */
+typedef struct {
+  int32_t n_lanes, n_roads, n_junctions;
+  const float *lane_length;          /* [n_lanes] metres, > 0 */
+  const float *lane_max_speed;       /* [n_lanes] m/s, > 0 */
+  const int32_t *lane_road;          /* [n_lanes] road id or -1 */
+  const int32_t *lane_junction;      /* [n_lanes] junction id or -1 */
+  const int32_t *lane_left, *lane_right; /* [n_lanes] neighbour lane or -1 (road lanes only) */
+  const int32_t *succ_offsets;       /* [n_lanes+1] CSR lane -> successor lanes */
+  const int32_t *succ_lanes;
+  const uint8_t *lane_turn;          /* [n_lanes] junction lanes: 0 STRAIGHT 1 LEFT 2 RIGHT */
+  const uint8_t *lane_kind;          /* [n_lanes] 0 NORMAL 1 DYNAMIC 2 TIDAL */
+  const int32_t *tidal_partner;      /* [n_lanes] partner lane of a TIDAL lane or -1 */
+  const uint8_t *lane_dir0;          /* [n_lanes] initial direction (DYNAMIC: 0 STRAIGHT 1 LEFT;
+                                        TIDAL: 0 FORWARD = usable, 1 BACKWARD) */
+  const int32_t *road_lane_offsets;  /* [n_roads+1] */
+  const int32_t *road_lanes;         /* leftmost first */
+  const int32_t *junc_lane_offsets;  /* [n_junctions+1] */
+  const int32_t *junc_lanes;         /* junction lane "slots" */
+  const int32_t *junc_phase_offsets; /* [n_junctions+1] CSR junction -> phases */
+  const uint8_t *phase_green;        /* for junction j, phase k: row of n_slots(j) bytes,
+                                        rows laid out junction by junction, phase by phase */
+  const int32_t *phase_green_steps;  /* [n_phases] FIXED_TIME green duration (steps) */
+  const uint8_t *junc_policy;        /* [n_junctions] 0 NONE 1 FIXED_TIME 2 MANUAL */
+  const int32_t *junc_offset_steps;  /* [n_junctions] FIXED_TIME cycle offset */
+} sim_graph;
+
+/* Trips (P:826 origin, destination, departure, route).  Host, caller-owned. */
+typedef struct {
+  int32_t n_trips;                   /* vehicle id = trip index */
+  const int32_t *depart_step;        /* [n] >= 0 */
+  const uint8_t *on_network_at_t0;   /* [n] 1: DRIVING at t = 0 at (start_lane, start_s, start_v) */
+  const int32_t *route_offsets;      /* [n+1] CSR trip -> roads */
+  const int32_t *route_roads;
+  const int32_t *start_lane;         /* [n] lane of route[0] */
+  const float *start_s, *start_v, *end_s; /* [n] metres, m/s, metres on the destination road */
+  const uint8_t *profile;            /* [n] index into params.profiles */
+} sim_trips;
+
+typedef struct { float a_max, a_comf, T, s0, v_max, length; } sim_profile;
+
+typedef struct {
+  uint64_t seed;                     /* Philox key (ledger L16) */
+  float dt;                          /* must be 1.0 */
+  int32_t n_profiles;                /* <= 256 */
+  const sim_profile *profiles;
+  float politeness, b_hard, b_safe, v_wait, queue_zone_m; /* 0.1, 8, 4, 0.1, 100 */
+  int32_t yellow_steps, lookahead_lanes;                  /* 3, 2 */
+  int32_t exact_mode;                /* 1: all per-vehicle math in fp64 (test mode) */
+  int32_t record_decisions;          /* 1: keep the last step's decisions for sim_read_decisions */
+  int32_t device;                    /* CUDA device ordinal */
+  void *stream;                      /* cudaStream_t to run on (NULL = library-created stream) */
+} sim_params;
+
+typedef struct {
+  int32_t n_vehicles, n_lanes, n_junctions, n_tiles;
+  int64_t device_bytes;              /* device memory held by the handle */
+} sim_sizes;
+
+/* Vehicle / junction / lane state, vid-, junction- and lane-indexed.
+ * All arrays caller-owned, sized from sim_sizes; any pointer may be NULL to
+ * skip that field on read (not on load). */
+typedef struct {
+  int32_t t;                         /* steps completed */
+  uint8_t *status;                   /* 0 PENDING 1 DRIVING 2 FINISHED */
+  int32_t *lane, *cursor, *wait_steps, *insert_time, *arrive_time;
+  float *s, *v;
+  uint8_t *junc_policy;
+  int32_t *junc_phase, *junc_elapsed, *junc_yellow_left, *junc_pending;
+  uint8_t *lane_dir;
+  uint8_t *lane_signal;              /* read only: signals seen in the last step */
+  int32_t *lane_offsets;             /* read only, optional: [n_lanes+1] per-lane order CSR */
+  int32_t *lane_order;               /* read only, optional: [n_vehicles] vids by (s, vid) */
+} sim_state;
+
+/* Decisions of the last step (record_decisions = 1), vid-indexed. */
+typedef struct {
+  int32_t *leader_vid;               /* -1 none */
+  int8_t *leader_hops;               /* 0 in-lane, h lanes ahead, -1 none */
+  int8_t *phantom;                   /* stop-line phantom active on the current lane */
+  int32_t *old_follower_vid;
+  int32_t *side_vid;                 /* [4*n] LF LB RF RB */
+  int8_t *lc;                        /* -1 left 0 stay +1 right */
+  int8_t *handoffs;
+  float *accel;
+  int8_t *finished, *inserted;
+  uint8_t *guard;                    /* 1: decided by the fp64 guard fallback */
+} sim_decisions;
+
+typedef struct {
+  int32_t t;
+  int64_t n_pending, n_driving, n_finished;
+  int64_t vehicle_steps;             /* sum over steps of vehicles moved */
+  int64_t sum_travel_steps, sum_wait_steps_finished, sum_depart_delay;
+  int64_t n_lane_changes, n_handoffs, n_inserted, n_guard_hits;
+  double att_finished;               /* sum_travel_steps / n_finished */
+  int32_t *lane_count;               /* optional caller buffer [n_lanes] or NULL */
+  int32_t *lane_waiting_at_end;      /* optional [n_lanes]: v < v_wait within queue_zone_m */
+} sim_metrics;
+
+/* Create a simulation.  Validates the graph and trips
+ * (SIM_E_INVALID names the first violated rule), builds road tiles, allocates
+ * device memory on params->device and uploads the t = 0 state. */
+sim_status sim_create(const sim_graph *g, const sim_trips *trips,
+                      const sim_params *params, sim_handle *out);
+/* Advance n >= 0 steps (next_step(n)), asynchronously. */
+sim_status sim_step(sim_handle h, int32_t n);
+/* Block until all enqueued work finished; reports deferred device errors. */
+sim_status sim_sync(sim_handle h);
+/* MANUAL phase request (set_tl_phase): junction switches to MANUAL,
+ * Y yellow steps then `phase`. */
+sim_status sim_set_signal_phase(sim_handle h, int32_t junction, int32_t phase);
+sim_status sim_set_signal_phase_batch(sim_handle h, int32_t m, const int32_t *junctions,
+                                      const int32_t *phases);
+/* Lane direction (set_road_lane_plan P:851 / set_lane_restriction P:846):
+ * DYNAMIC: 0 STRAIGHT 1 LEFT; TIDAL: 0 FORWARD (usable) 1 BACKWARD, the
+ * partner gets the complement.  SIM_E_INVALID for other lanes. */
+sim_status sim_set_lane_direction(sim_handle h, int32_t lane, int32_t dir);
+sim_status sim_set_lane_direction_batch(sim_handle h, int32_t m, const int32_t *lanes,
+                                        const int32_t *dirs);
+sim_status sim_query_sizes(sim_handle h, sim_sizes *out);
+/* Synchronising reads into caller-owned host buffers. */
+sim_status sim_read_state(sim_handle h, sim_state *out);
+sim_status sim_read_decisions(sim_handle h, sim_decisions *out);
+sim_status sim_read_metrics(sim_handle h, sim_metrics *out);
+/* Replace the whole state (checkpoint / parity hook).  Pending queues are
+ * rebuilt from status; all fields except lane_signal/lane_offsets/lane_order
+ * are required. */
+sim_status sim_load_state(sim_handle h, const sim_state *in);
+sim_status sim_destroy(sim_handle h);
+/* Last error message of h (NULL h: the calling thread's last create error). */
+const char *sim_last_error(sim_handle h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

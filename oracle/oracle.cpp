@@ -697,7 +697,7 @@ void or_read_state(void *h, or_state *o) {
     const Vehicle &v = S->V[k];
     o->status[k] = (uint8_t)v.status;
     o->lane[k] = v.status == DRIVING ? v.lane : -1;
-    o->cursor[k] = v.cursor; o->wait_steps[k] = v.wait;
+    o->cursor[k] = v.status == DRIVING ? v.cursor : 0; o->wait_steps[k] = v.wait;
     o->insert_time[k] = v.insert_time; o->arrive_time[k] = v.arrive_time;
     o->s[k] = v.s; o->v[k] = v.v;
   }

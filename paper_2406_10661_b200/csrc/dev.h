@@ -1,0 +1,138 @@
+// dev.h — device data layout of the B200 simulation store.
+//
+// Vehicles live in road TILES: one tile = one road's lanes + the junction
+// lanes leaving that road (their only predecessor is one of its lanes).  Every
+// vehicle is owned by exactly one tile; lane changes and road-lane -> junction
+// lane hand-offs stay inside the tile, only junction lane -> next road
+// hand-offs (and direct road -> road links) cross tiles.
+//
+// Between steps the state of a tile is
+//   * its STAYERS: a compacted SoA slab segment sorted by (lane_local, s, vid)
+//     (the paper's per-lane linked lists, as memory order), and
+//   * its INBOX: unsorted 32-byte records of vehicles that entered the tile or
+//     changed lane during the last step (the paper's per-lane addition
+//     buffers), merged into the order at the start of the next step.
+#pragma once
+#include <stdint.h>
+
+namespace sim {
+
+constexpr int kMaxTileLanes = 64;    // lanes per tile (road lanes + outgoing junction lanes)
+constexpr int kThreads = 128;        // k_step block size
+constexpr int kSmemVeh = 448;        // snapshot slots held in shared memory (larger tiles use global scratch)
+constexpr int kSmemInbox = 96;       // inbox keys sorted in shared memory
+constexpr int kNAcc = 12;            // per-tile int64 accumulators
+constexpr uint64_t kEmptyKey = ~0ull;
+
+enum Acc {
+  ACC_VEH_STEPS = 0, ACC_FINISHED, ACC_SUM_TRAVEL, ACC_SUM_WAIT_FIN, ACC_SUM_DELAY,
+  ACC_LANE_CHANGES, ACC_HANDOFFS, ACC_INSERTED, ACC_GUARD, ACC_OVERFLOW, ACC_R1, ACC_R2
+};
+enum { ST_PENDING = 0, ST_DRIVING = 1, ST_FINISHED = 2 };
+enum { SIG_GREEN = 0, SIG_YELLOW = 1, SIG_RED = 2 };
+enum { POL_NONE = 0, POL_FIXED = 1, POL_MANUAL = 2 };
+enum { KIND_NORMAL = 0, KIND_DYNAMIC = 1, KIND_TIDAL = 2 };
+constexpr int kLaneDest = -2, kLaneBlocked = -3;
+
+struct Prof {                       // one vehicle profile
+  float a_max, a_comf, T, s0, vmax, len, inv2sqrt_f, pad;
+  double a_max_d, a_comf_d, T_d, s0_d, vmax_d, len_d, inv2sqrt_d, pad_d;
+};
+
+struct InboxRec {                   // 32 B, one sector
+  float s, v;
+  int32_t vid, nxt, nxt2;
+  uint32_t meta;                    // lane_local:8 | profile:8 | cursor:16
+  int32_t wait, pad;
+};
+
+struct Slab {                       // SoA hot record, 28 B / vehicle
+  float *s, *v;
+  int32_t *vid, *nxt, *nxt2;        // route[c+1], route[c+2] (-1 past the end)
+  uint32_t *meta;
+  int32_t *wait;
+};
+
+__host__ __device__ inline uint32_t pack_meta(int lane_local, int prof, int cursor) {
+  return (uint32_t)lane_local | ((uint32_t)prof << 8) | ((uint32_t)cursor << 16);
+}
+
+struct StepArgs {
+  int32_t t, n_tiles, n_lanes, n_veh;
+  uint64_t seed;
+  // model constants (fp32 inputs; fp64 copies are their exact promotions)
+  float polite, b_hard, b_safe, v_wait;
+  double start_margin;              // v_cap + 0.5 * a_cap (ledger L17)
+  int32_t lookahead, exact_mode, record;
+  // lanes (global id)
+  const float *lane_len, *lane_vmax;
+  const int32_t *lane_road;         // -1 junction lane
+  const int32_t *lane_left, *lane_right;
+  const int32_t *succ_off, *succ;
+  const int32_t *target_road;       // road reached through lane j
+  const int32_t *exit_lane;         // junction lane: its successor; road lane: itself
+  const uint8_t *usable;
+  const uint8_t *lane_sig;
+  const int32_t *lane_tile;
+  const uint8_t *lane_local;
+  // tiles
+  const int32_t *tile_lane_off, *tile_lanes, *tile_nroad;
+  const int32_t *tile_base, *tile_cap, *tile_ibase, *tile_icap;
+  int32_t *cnt_in, *cnt_out;        // [n_tiles] stayer counts (read / write buffers)
+  int32_t *icnt_in, *icnt_out;      // [n_tiles] inbox counts
+  Slab in, out;                     // stayer slabs
+  const InboxRec *inbox_in;
+  InboxRec *inbox_out;
+  Slab scratch;                     // global fallback for large tiles ([base+ibase, +cap+icap))
+  int32_t *bsort_scratch;           // [Σ icap] inbox sort order for large inboxes
+  // lane summaries (first vehicle key) for t, t+1, t+2 (triple buffer)
+  const unsigned long long *summ_cur;
+  unsigned long long *summ_next, *summ_clear;
+  const float *pubv_cur;            // [n_veh] speed of summary vehicles at t
+  float *pubv_next;
+  // cold per-vehicle data
+  const int32_t *route_off, *route;
+  const float *end_s;
+  const uint8_t *veh_prof;
+  int32_t *insert_time, *arrive_time, *wait_fin;
+  uint8_t *status;
+  const int32_t *depart;
+  const float *start_s;
+  // pending queues (per lane, sorted by (depart, vid))
+  const int32_t *pend_off, *pend_vid;
+  int32_t *pend_head;
+  const Prof *prof;
+  long long *tacc;                  // [n_tiles][kNAcc]
+  // decision recording (vid-indexed), optional
+  int32_t *r_leader, *r_of, *r_side;
+  int8_t *r_hops, *r_phantom, *r_lc, *r_hand, *r_fin, *r_ins;
+  float *r_acc;
+  uint8_t *r_guard;
+};
+
+struct SignalArgs {
+  int32_t n_junctions, yellow;
+  uint8_t *policy;
+  int32_t *phase, *elapsed, *yellow_left, *pending, *request;
+  const int32_t *jl_off, *jl;       // junction -> lanes (slots)
+  const int32_t *ph_off;            // junction -> phases
+  const int64_t *green_off;         // junction -> first byte of its phase rows
+  const uint8_t *green;
+  const int32_t *green_steps;
+  uint8_t *lane_sig;
+};
+
+// kernel launchers (kernels.cu)
+void launch_signal(const SignalArgs &a, void *stream);
+void launch_step(const StepArgs &a, void *stream, int smem_bytes);
+int step_smem_bytes();
+void launch_set_i32(int32_t *dst, const int32_t *idx, const int32_t *val, int m, void *stream);
+void launch_apply_requests(int32_t *request, uint8_t *policy, const int32_t *junc,
+                           const int32_t *phase, int m, void *stream);
+void launch_reduce_acc(const long long *tacc, int n_tiles, const int32_t *cnt,
+                       const int32_t *icnt, long long *out, void *stream);
+void launch_lane_stats(const StepArgs &a, int32_t *lane_count, int32_t *lane_wait,
+                       float queue_zone, void *stream);
+void launch_fill_u64(unsigned long long *p, unsigned long long v, int64_t n, void *stream);
+
+}  // namespace sim

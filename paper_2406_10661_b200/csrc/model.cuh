@@ -1,0 +1,535 @@
+// model.cuh — the per-vehicle model of DESIGN.md §1.5 (O4-O9), templated on
+// the arithmetic type R:
+//   * R = double: the canonical operation sequence of DESIGN §1.7 (each op a
+//     separately rounded IEEE fp64 op via __dadd_rn/__dmul_rn/__ddiv_rn);
+//     used by exact_mode and by the guard fallback;
+//   * R = float: the fast path; every decision whose fp32 margin is inside the
+//     guard band sets Guard::hit and the vehicle is recomputed with R = double.
+// Paper: IDM P:156-167, randomized MOBIL P:171-198, signal P:200,
+// substitution of the next lane's first vehicle P:168-169 (App. A2.3).
+#pragma once
+#include <math.h>
+#include <stdint.h>
+
+#include "dev.h"
+
+namespace sim {
+
+template <typename R> struct Ar;
+template <> struct Ar<double> {
+  static constexpr bool fp64 = true;
+  __device__ __forceinline__ static double add(double a, double b) { return __dadd_rn(a, b); }
+  __device__ __forceinline__ static double sub(double a, double b) { return __dadd_rn(a, -b); }
+  __device__ __forceinline__ static double mul(double a, double b) { return __dmul_rn(a, b); }
+  __device__ __forceinline__ static double div(double a, double b) { return __ddiv_rn(a, b); }
+};
+template <> struct Ar<float> {
+  static constexpr bool fp64 = false;
+  __device__ __forceinline__ static float add(float a, float b) { return a + b; }
+  __device__ __forceinline__ static float sub(float a, float b) { return a - b; }
+  __device__ __forceinline__ static float mul(float a, float b) { return a * b; }
+  __device__ __forceinline__ static float div(float a, float b) { return __fdividef(a, b); }
+};
+
+// guard band of the fp32 path
+constexpr float kEpsPos = 4e-6f;    // relative to the magnitude of the positions involved
+constexpr float kEpsAcc = 2e-4f;    // m/s^2, accelerations / utilities
+constexpr float kEpsP = 2e-4f;      // draw vs p_LC
+constexpr float kEpsV = 2e-5f;      // relative, speed vs v_wait
+
+struct Guard { bool hit; };
+
+template <typename R> struct PV { R a_max, a_comf, T, s0, vmax, len, inv2; };
+__device__ __forceinline__ PV<double> pvals(const Prof &p, double) {
+  return {p.a_max_d, p.a_comf_d, p.T_d, p.s0_d, p.vmax_d, p.len_d, p.inv2sqrt_d};
+}
+__device__ __forceinline__ PV<float> pvals(const Prof &p, float) {
+  return {p.a_max, p.a_comf, p.T, p.s0, p.vmax, p.len, p.inv2sqrt_f};
+}
+
+// IDM (delta = 4) in canonical order; ledger L7 (no leader), L8.
+template <typename R, bool GUARD>
+__device__ __forceinline__ R idm(R v, R v0, bool lead, R gap, R dv, const PV<R> &p, R b_hard,
+                                 R gap_scale, Guard &g) {
+  using M = Ar<R>;
+  R x = M::div(v, v0);
+  R x2 = M::mul(x, x);
+  R x4 = M::mul(x2, x2);
+  R fr = M::sub((R)1, x4);
+  R a;
+  if (!lead) {
+    a = M::mul(p.a_max, fr);
+  } else {
+    if (GUARD && gap_scale > (R)0 && fabsf((float)gap) <= kEpsPos * (float)gap_scale) g.hit = true;
+    if (gap <= (R)0) {
+      a = -b_hard;
+    } else {
+      R z = M::add(M::mul(v, p.T), M::mul(M::mul(v, dv), p.inv2));
+      R zz = ((R)0 < z) ? z : (R)0;
+      R ss = M::add(p.s0, zz);
+      R q = M::div(ss, gap);
+      a = M::mul(p.a_max, M::sub(fr, M::mul(q, q)));
+    }
+  }
+  return (a < -b_hard) ? -b_hard : a;
+}
+
+// Tile-local lane metadata staged in shared memory.
+struct TileSh {
+  int nl, nroad, tile, base, ibase, cap, icap;
+  int glob[kMaxTileLanes];
+  float len[kMaxTileLanes], vmax[kMaxTileLanes];
+  int seg_start[kMaxTileLanes], seg_end[kMaxTileLanes];
+  int first_out[kMaxTileLanes];
+  int8_t left[kMaxTileLanes], right[kMaxTileLanes];
+  uint8_t isroad[kMaxTileLanes], usable[kMaxTileLanes];
+};
+
+// Snapshot of the tile at time t (shared memory or global scratch).
+struct View {
+  float *s, *v;
+  int32_t *vid, *nxt, *nxt2;
+  uint32_t *meta;
+  int32_t *wait;
+};
+
+__device__ __forceinline__ int m_lane(uint32_t m) { return (int)(m & 0xffu); }
+__device__ __forceinline__ int m_prof(uint32_t m) { return (int)((m >> 8) & 0xffu); }
+__device__ __forceinline__ int m_cursor(uint32_t m) { return (int)(m >> 16); }
+
+__device__ __forceinline__ int route_at(const StepArgs &A, int vid, int c, int nxt, int nxt2,
+                                        int idx) {
+  if (idx == c + 1) return nxt;
+  if (idx == c + 2) return nxt2;
+  int off = __ldg(A.route_off + vid);
+  int len = __ldg(A.route_off + vid + 1) - off;
+  return (idx >= 0 && idx < len) ? __ldg(A.route + off + idx) : -1;
+}
+
+// cand(b, R) != empty
+__device__ __forceinline__ bool has_outroad(const StepArgs &A, int b, int R) {
+  int e1 = __ldg(A.succ_off + b + 1);
+  for (int e = __ldg(A.succ_off + b); e < e1; ++e) {
+    int j = __ldg(A.succ + e);
+    if (A.usable[j] && __ldg(A.target_road + j) == R) return true;
+  }
+  return false;
+}
+
+// next lane from road lane m toward road R1 with preference toward R2 (ledger L24)
+__device__ __forceinline__ int next_from_road(const StepArgs &A, int m, int R1, int R2) {
+  if (R1 < 0) return kLaneDest;
+  int best_any = kLaneBlocked, best_pref = kLaneBlocked;
+  int e1 = __ldg(A.succ_off + m + 1);
+  for (int e = __ldg(A.succ_off + m); e < e1; ++e) {
+    int j = __ldg(A.succ + e);
+    if (!A.usable[j] || __ldg(A.target_road + j) != R1) continue;
+    if (best_any < 0 || j < best_any) best_any = j;
+    bool pref = (R2 < 0) || has_outroad(A, __ldg(A.exit_lane + j), R2);
+    if (pref && (best_pref < 0 || j < best_pref)) best_pref = j;
+  }
+  return best_pref >= 0 ? best_pref : best_any;
+}
+
+struct First { bool found; float s, v, len; int vid; };
+
+// first vehicle of lane m at time t: from the tile snapshot if m is ours, else
+// from the lane summary built race-free during step t-1
+__device__ __forceinline__ First first_of(const StepArgs &A, const TileSh &T, const View &C,
+                                          int m) {
+  First f;
+  f.found = false;
+  if (__ldg(A.lane_tile + m) == T.tile) {
+    int ll = A.lane_local[m];
+    int a = T.seg_start[ll];
+    if (a < T.seg_end[ll]) {
+      f.found = true;
+      f.s = C.s[a];
+      f.v = C.v[a];
+      f.vid = C.vid[a];
+      f.len = A.prof[m_prof(C.meta[a])].len;
+    }
+  } else {
+    unsigned long long key = A.summ_cur[m];
+    if (key != kEmptyKey) {
+      f.found = true;
+      f.s = __uint_as_float((unsigned)(key >> 32));
+      f.vid = (int)(unsigned)(key & 0xffffffffu);
+      f.v = A.pubv_cur[f.vid];
+      f.len = A.prof[A.veh_prof[f.vid]].len;
+    }
+  }
+  return f;
+}
+
+template <typename R> struct LEv {
+  R a, gap, vlead, lim, vlim;
+  R limrel;                          // lim - s computed without cancellation (fp32 path)
+  int leader, hops, next1;
+  bool has_leader, phantom, has_lim;
+};
+
+struct Me {                          // the ego vehicle's identity / route cache
+  int vid, cur, nxt, nxt2;
+};
+
+// O4-O6 for the ego placed on tile-local lane l (App. A2.3)
+template <typename R, bool GUARD>
+__device__ LEv<R> eval_lane(const StepArgs &A, const TileSh &T, const View &C, int l,
+                            int lead_idx, R s, R v, const PV<R> &p, const Me &me, Guard &g) {
+  using M = Ar<R>;
+  LEv<R> e;
+  const int lg = T.glob[l];
+  const bool road = T.isroad[l];
+  e.next1 = road ? (me.nxt < 0 ? kLaneDest : next_from_road(A, lg, me.nxt, me.nxt2))
+                 : __ldg(A.exit_lane + lg);
+  const R vmax_l = (R)T.vmax[l];
+  const R v0 = (p.vmax < vmax_l) ? p.vmax : vmax_l;
+  const R L = (R)T.len[l];
+  e.has_leader = false;
+  e.leader = -1;
+  e.hops = -1;
+  e.gap = (R)0;
+  e.vlead = (R)0;
+  R gscale = (R)0;
+  if (lead_idx >= 0) {                                   // main pointer
+    R sf = (R)C.s[lead_idx];
+    R lf = (R)A.prof[m_prof(C.meta[lead_idx])].len;
+    e.has_leader = true;
+    e.leader = C.vid[lead_idx];
+    e.hops = 0;
+    e.gap = M::sub(M::sub(sf, s), lf);
+    e.vlead = (R)C.v[lead_idx];
+    gscale = sf + s + lf;
+  } else {                                               // P:168-169 substitution
+    R d = M::sub(L, s);
+    int m = e.next1, rel = 0;
+    for (int h = 1; h <= A.lookahead; ++h) {
+      if (m < 0) break;
+      const bool mroad = __ldg(A.lane_road + m) >= 0;
+      if (mroad) rel += 1;
+      First f = first_of(A, T, C, m);
+      if (f.found) {
+        e.has_leader = true;
+        e.leader = f.vid;
+        e.hops = h;
+        e.gap = M::sub(M::add(d, (R)f.s), (R)f.len);
+        e.vlead = (R)f.v;
+        gscale = d + (R)f.s + (R)f.len;
+        break;
+      }
+      d = M::add(d, (R)__ldg(A.lane_len + m));
+      if (!mroad) {
+        m = __ldg(A.exit_lane + m);
+      } else {
+        int R1 = route_at(A, me.vid, me.cur, me.nxt, me.nxt2, me.cur + rel + 1);
+        int R2 = route_at(A, me.vid, me.cur, me.nxt, me.nxt2, me.cur + rel + 2);
+        m = next_from_road(A, m, R1, R2);
+      }
+    }
+  }
+  const R b_hard = (R)A.b_hard;
+  R a_lead = idm<R, GUARD>(v, v0, e.has_leader, e.gap, M::sub(v, e.vlead), p, b_hard, gscale, g);
+  e.a = a_lead;
+  e.phantom = false;
+  if (road && e.next1 != kLaneDest &&
+      (e.next1 == kLaneBlocked ||
+       (__ldg(A.lane_road + e.next1) < 0 && A.lane_sig[e.next1] != SIG_GREEN))) {
+    e.phantom = true;                                    // P:200 stationary vehicle at lane end
+    R gp = M::sub(L, s);                                 // sign exact: no guard needed
+    R a_ph = idm<R, GUARD>(v, v0, true, gp, M::sub(v, (R)0), p, b_hard, (R)0, g);
+    e.a = (a_ph < a_lead) ? a_ph : a_lead;
+  }
+  R lim_lead = M::add(s, e.gap);
+  e.has_lim = false;
+  e.lim = (R)0;
+  e.vlim = (R)0;
+  if (GUARD && e.phantom && e.has_leader &&
+      fabsf((float)(L - lim_lead)) <= kEpsPos * (float)(L + fabs(lim_lead)))
+    g.hit = true;
+  if (e.phantom && (!e.has_leader || L <= lim_lead)) {
+    e.has_lim = true;
+    e.lim = L;
+    e.limrel = M::sub(L, s);
+    e.vlim = (R)0;
+  } else if (e.has_leader) {
+    e.has_lim = true;
+    e.lim = lim_lead;
+    e.limrel = e.gap;
+    e.vlim = e.vlead;
+  }
+  return e;
+}
+
+struct Res {
+  float s1, v1, acc;
+  int lane_g, cursor;
+  int lc, hand;
+  bool fin;
+  int wait1;
+  // recorded decisions
+  int leader, hops, phantom, of_vid, side[4];
+};
+
+__device__ __forceinline__ int upper_bound_s(const View &C, int a, int b, float s) {
+  // first index in [a, b) with C.s > s   (side pointers; ties -> back, L11)
+  while (a < b) {
+    int mid = (a + b) >> 1;
+    if (C.s[mid] > s) b = mid; else a = mid + 1;
+  }
+  return a;
+}
+
+// One vehicle's update O4-O9 reading only state(t).
+template <typename R, bool GUARD>
+__device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, int i, Res &o,
+                           Guard &g) {
+  using M = Ar<R>;
+  const uint32_t meta = C.meta[i];
+  const int l = m_lane(meta), pr = m_prof(meta);
+  Me me;
+  me.vid = C.vid[i];
+  me.cur = m_cursor(meta);
+  me.nxt = C.nxt[i];
+  me.nxt2 = C.nxt2[i];
+  const PV<R> p = pvals(A.prof[pr], (R)0);
+  const R s = (R)C.s[i], v = (R)C.v[i];
+  const R L = (R)T.len[l];
+  const int lead = (i + 1 < T.seg_end[l]) ? i + 1 : -1;
+  const int of = (i > T.seg_start[l]) ? i - 1 : -1;
+  LEv<R> cur = eval_lane<R, GUARD>(A, T, C, l, lead, s, v, p, me, g);
+  o.leader = cur.leader;
+  o.hops = cur.hops;
+  o.phantom = cur.phantom;
+  o.of_vid = of >= 0 ? C.vid[of] : -1;
+  o.side[0] = o.side[1] = o.side[2] = o.side[3] = -1;
+  LEv<R> use = cur;
+  int lc = 0, new_l = l;
+  const R b_hard = (R)A.b_hard;
+  if (T.isroad[l]) {                                     // no LC in junction lanes
+    const bool dest = me.nxt < 0;
+    const bool inG = dest || cur.next1 != kLaneBlocked;
+    int mand = 0;
+    if (!inG) {                                          // ledger L18, L37
+      bool left_ok = false, right_ok = false;
+      for (int a = 0; a < T.nroad; ++a) {
+        if (!T.usable[a] || !has_outroad(A, T.glob[a], me.nxt)) continue;
+        if (a < l) left_ok = true;
+        if (a > l) right_ok = true;
+      }
+      mand = left_ok ? -1 : (right_ok ? 1 : 0);
+    }
+    const R rem = M::sub(L, s);
+    const R need = M::add(p.s0, M::mul(v, p.T));
+    const bool l19 = rem < need;                         // ledger L19
+    if (GUARD && inG && fabsf((float)(rem - need)) <= kEpsPos * (float)(L + need)) g.hit = true;
+    int sl[2] = {T.left[l], T.right[l]};
+    int front[2] = {-1, -1}, back[2] = {-1, -1};
+    for (int sd = 0; sd < 2; ++sd) {
+      if (sl[sd] < 0) continue;
+      int a = T.seg_start[sl[sd]], b = T.seg_end[sl[sd]];
+      int f = upper_bound_s(C, a, b, C.s[i]);
+      front[sd] = f < b ? f : -1;
+      back[sd] = f > a ? f - 1 : -1;
+      o.side[2 * sd] = front[sd] >= 0 ? C.vid[front[sd]] : -1;
+      o.side[2 * sd + 1] = back[sd] >= 0 ? C.vid[back[sd]] : -1;
+    }
+    const bool consider = inG ? !l19 : (mand != 0);
+    if (consider) {
+      R a_of = (R)0, a_of_new = (R)0;                    // old follower (L10)
+      if (of >= 0) {
+        const PV<R> po = pvals(A.prof[m_prof(C.meta[of])], (R)0);
+        const R so = (R)C.s[of], vo = (R)C.v[of];
+        const R v0o = (po.vmax < (R)T.vmax[l]) ? po.vmax : (R)T.vmax[l];
+        a_of = idm<R, GUARD>(vo, v0o, true, M::sub(M::sub(s, so), p.len), M::sub(vo, v), po,
+                             b_hard, s + so + p.len, g);
+        if (lead >= 0) {
+          const R sl_ = (R)C.s[lead];
+          const R ll_ = (R)A.prof[m_prof(C.meta[lead])].len;
+          a_of_new = idm<R, GUARD>(vo, v0o, true, M::sub(M::sub(sl_, so), ll_),
+                                   M::sub(vo, (R)C.v[lead]), po, b_hard, sl_ + so + ll_, g);
+        } else {
+          a_of_new = idm<R, GUARD>(vo, v0o, false, (R)0, (R)0, po, b_hard, (R)0, g);
+        }
+      }
+      bool adm[2] = {false, false};
+      R u[2] = {(R)0, (R)0};
+      LEv<R> ev[2];
+      for (int sd = 0; sd < 2; ++sd) {
+        const int ls = sl[sd];
+        const int sgn = sd == 0 ? -1 : 1;
+        if (ls < 0 || !T.usable[ls]) continue;
+        if (inG && !(dest || has_outroad(A, T.glob[ls], me.nxt))) continue;
+        if (!inG && sgn != mand) continue;
+        ev[sd] = eval_lane<R, GUARD>(A, T, C, ls, front[sd], s, v, p, me, g);
+        R a_nf = (R)0, a_nf_new = (R)0;
+        bool ok = true;
+        if (back[sd] >= 0) {
+          const int bi = back[sd];
+          const PV<R> pb = pvals(A.prof[m_prof(C.meta[bi])], (R)0);
+          const R sb = (R)C.s[bi], vb = (R)C.v[bi];
+          const R v0b = (pb.vmax < (R)T.vmax[ls]) ? pb.vmax : (R)T.vmax[ls];
+          if (front[sd] >= 0) {
+            const int fi = front[sd];
+            const R sf = (R)C.s[fi];
+            const R lf = (R)A.prof[m_prof(C.meta[fi])].len;
+            a_nf = idm<R, GUARD>(vb, v0b, true, M::sub(M::sub(sf, sb), lf),
+                                 M::sub(vb, (R)C.v[fi]), pb, b_hard, sf + sb + lf, g);
+          } else {
+            a_nf = idm<R, GUARD>(vb, v0b, false, (R)0, (R)0, pb, b_hard, (R)0, g);
+          }
+          const R gb = M::sub(M::sub(s, sb), p.len);
+          a_nf_new = idm<R, GUARD>(vb, v0b, true, gb, M::sub(vb, v), pb, b_hard, s + sb + p.len, g);
+          if (GUARD && fabsf((float)(a_nf_new + (R)A.b_safe)) <= kEpsAcc) g.hit = true;
+          if (!(a_nf_new >= -(R)A.b_safe)) ok = false;  // L17 (1)
+          if (!(gb >= (R)0)) ok = false;                 // L17 (2)
+        } else {
+          const R mrg = M::sub(s, p.len);
+          if (GUARD && fabs((double)mrg - A.start_margin) <= (double)kEpsPos * ((double)s + A.start_margin))
+            g.hit = true;
+          if (!(mrg >= (R)A.start_margin)) ok = false;  // L17 (3) lane-start rule
+        }
+        if (front[sd] >= 0) {
+          const int fi = front[sd];
+          const R sf = (R)C.s[fi];
+          const R lf = (R)A.prof[m_prof(C.meta[fi])].len;
+          const R gf = M::sub(M::sub(sf, s), lf);
+          if (GUARD && fabsf((float)gf) <= kEpsPos * (float)(sf + s + lf)) g.hit = true;
+          if (!(gf >= (R)0)) ok = false;                 // L17 (2)
+        }
+        // MOBIL utility (tilde = after the change, ledger L13)
+        u[sd] = M::add(M::sub(ev[sd].a, cur.a),
+                       M::mul((R)A.polite, M::add(M::sub(a_nf_new, a_nf), M::sub(a_of_new, a_of))));
+        adm[sd] = ok;
+      }
+      int choice = -1;
+      if (inG) {
+        if (adm[0] || adm[1]) {
+          R u0 = adm[0] ? (((R)0 < u[0]) ? u[0] : (R)0) : (R)0;
+          R u1 = adm[1] ? (((R)0 < u[1]) ? u[1] : (R)0) : (R)0;
+          R uT = M::add(u0, u1);
+          double pl;                                     // P:188-194, ledger L14
+          if (uT >= (R)1) pl = 0.9;
+          else if (uT > (R)0) pl = (double)M::mul((R)(0.9 - 2e-8), uT);
+          else pl = 2e-8;
+          // U53 of Philox4x32-10(seed; vid, t) (ledger L16)
+          uint32_t c0 = (uint32_t)me.vid, c1 = (uint32_t)A.t, c2 = 0u, c3 = 0u;
+          uint32_t k0 = (uint32_t)(A.seed & 0xffffffffull), k1 = (uint32_t)(A.seed >> 32);
+#pragma unroll
+          for (int r = 0; r < 10; ++r) {
+            uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+            uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+            uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+            c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+            k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+          }
+          const uint64_t mant = ((uint64_t)(c0 >> 5) << 26) + (uint64_t)(c1 >> 6);
+          const double r = (double)mant * (1.0 / 9007199254740992.0);
+          if (GUARD && fabs(r - pl) <= (double)kEpsP) g.hit = true;
+          if (r < pl) {                                  // P:196, ledger L15
+            if (adm[0] && adm[1]) {
+              if (GUARD && fabsf((float)(u[0] - u[1])) <= kEpsAcc) g.hit = true;
+              choice = (u[0] >= u[1]) ? 0 : 1;
+            } else {
+              choice = adm[0] ? 0 : 1;
+            }
+          }
+        }
+      } else {
+        const int sd = mand < 0 ? 0 : 1;
+        if (adm[sd]) choice = sd;                        // ledger L18
+      }
+      if (choice >= 0) {
+        use = ev[choice];
+        lc = choice == 0 ? -1 : 1;
+        new_l = sl[choice];
+      }
+    }
+  }
+  // O8 integrate (ledger L1) + clamp (L22, L23).  The fp64 path follows the
+  // canonical sequence (position s1); the fp32 path carries the position as
+  // base + advance so that stop-line / hand-off decisions and the residual
+  // after a hand-off are free of cancellation at large s.
+  const R a = use.a;
+  const R vr = M::add(v, a);
+  R s1, v1, adv;
+  const bool adv_zero = (v == (R)0) && (vr <= (R)0);     // exact in both precisions
+  if (vr < (R)0) {
+    const R q = M::div(M::mul(v, v), M::mul((R)2, a));
+    s1 = M::sub(s, q);
+    adv = -q;
+    v1 = (R)0;
+  } else {
+    adv = M::mul(M::add(v, vr), (R)0.5);
+    s1 = M::add(s, adv);
+    v1 = vr;
+  }
+  if (use.has_lim) {
+    bool bind;
+    if (M::fp64) {
+      bind = s1 > use.lim;
+    } else {
+      bind = adv > use.limrel;
+      if (GUARD && !adv_zero && fabsf((float)(adv - use.limrel)) <= kEpsPos * (float)(fabs(adv) + fabs(use.limrel) + (R)1e-3))
+        g.hit = true;
+    }
+    if (bind) {
+      if (GUARD && fabsf((float)use.limrel) <= kEpsPos * (float)(fabs(s) + fabs(use.lim)))
+        g.hit = true;
+      if (M::fp64 ? (use.lim < s) : (use.limrel < (R)0)) { s1 = s; adv = (R)0; v1 = (R)0; }
+      else { s1 = use.lim; adv = use.limrel; v1 = (use.vlim < v1) ? use.vlim : v1; }
+    }
+  }
+  // O9 hand-off and arrival (ledger L26, L31); position = pb + pa
+  R pb = M::fp64 ? s1 : s;
+  R pa = M::fp64 ? (R)0 : adv;
+  int curg = T.glob[new_l], ri = me.cur, n = use.next1, hand = 0;
+  bool fin = false;
+  for (;;) {
+    const bool croad = __ldg(A.lane_road + curg) >= 0;
+    const bool dest_road = croad && route_at(A, me.vid, me.cur, me.nxt, me.nxt2, ri + 1) < 0;
+    if (dest_road) {
+      const R es = (R)__ldg(A.end_s + me.vid);
+      const R rem = M::sub(es, pb);
+      if (GUARD && !(adv_zero && hand == 0) &&
+          fabsf((float)(pa - rem)) <= kEpsPos * (float)(fabs(pa) + fabs(rem) + (R)1e-3))
+        g.hit = true;
+      if (pa >= rem) { fin = true; break; }
+    }
+    const R Lc = (R)__ldg(A.lane_len + curg);
+    const R rem = M::sub(Lc, pb);
+    if (GUARD && n >= 0 && !(adv_zero && hand == 0) &&
+        fabsf((float)(pa - rem)) <= kEpsPos * (float)(fabs(pa) + fabs(rem) + (R)1e-3))
+      g.hit = true;
+    if (pa > rem && n >= 0) {
+      pb = M::sub(pb, Lc);
+      curg = n;
+      const bool nroad = __ldg(A.lane_road + curg) >= 0;
+      if (nroad) ri += 1;
+      hand += 1;
+      if (nroad) {
+        int R1 = route_at(A, me.vid, me.cur, me.nxt, me.nxt2, ri + 1);
+        int R2 = route_at(A, me.vid, me.cur, me.nxt, me.nxt2, ri + 2);
+        n = next_from_road(A, curg, R1, R2);
+      } else {
+        n = __ldg(A.exit_lane + curg);
+      }
+      continue;
+    }
+    break;
+  }
+  s1 = M::fp64 ? pb : (hand == 0 ? s1 : M::add(pb, pa));
+  const R vw = (R)A.v_wait;
+  if (GUARD && fabsf((float)(v1 - vw)) <= kEpsV * (float)(fabs(v) + fabs(a) + (R)1)) g.hit = true;
+  o.wait1 = C.wait[i] + ((v1 < vw) ? 1 : 0);             // ledger L28
+  o.s1 = (float)s1;
+  o.v1 = (float)v1;
+  o.acc = (float)a;
+  o.lane_g = curg;
+  o.cursor = ri;
+  o.lc = lc;
+  o.hand = hand;
+  o.fin = fin;
+}
+
+}  // namespace sim

@@ -1,0 +1,1012 @@
+// sim_api.cu — host runtime behind include/sim.h.
+//
+// Builds road tiles (dev.h), validates inputs, owns all device
+// memory, uploads canonical (per-lane sorted) state, enqueues steps
+// (k_signal + k_step per step on the handle's stream), and implements the
+// setters / readers.  Nothing here computes the model: every per-vehicle
+// decision is taken on the GPU (kernels.cu / model.cuh).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+#include <set>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sim.h"
+#include "dev.h"
+
+using namespace sim;
+
+namespace {
+thread_local std::string g_create_err;
+std::mutex g_live_mu;
+std::set<const void *> g_live;      // live handles: calls on destroyed handles fail
+bool is_live(const void *h) {
+  std::lock_guard<std::mutex> lk(g_live_mu);
+  return g_live.count(h) != 0;
+}
+
+struct HostState {                  // vid / junction / lane indexed state
+  int t = 0;
+  std::vector<uint8_t> status;
+  std::vector<int> lane, cursor, wait, insert_time, arrive_time;
+  std::vector<float> s, v;
+  std::vector<uint8_t> jpol;
+  std::vector<int> jphase, jel, jy, jpend;
+  std::vector<uint8_t> dir;
+};
+}  // namespace
+
+struct sim_s {
+  std::string err;
+  sim_status sticky = SIM_OK;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  // graph (host copies)
+  int nl = 0, nr = 0, nj = 0, nv = 0, nt = 0;
+  std::vector<float> L, vmax;
+  std::vector<int> road, junc, left, right, succ_off, succ, pred, target_road, exit_lane;
+  std::vector<uint8_t> kind, turn;
+  std::vector<int> partner;
+  std::vector<int> road_off, road_lanes, jl_off, jl, ph_off, green_steps;
+  std::vector<int64_t> green_off;
+  std::vector<uint8_t> green, pol0;
+  std::vector<int> offset0;
+  // tiles
+  std::vector<int> tile_lane_off, tile_lanes, tile_nroad, tile_base, tile_cap, tile_ibase, tile_icap;
+  std::vector<int> lane_tile;
+  std::vector<uint8_t> lane_local;
+  int64_t sum_cap = 0, sum_icap = 0;
+  // trips
+  std::vector<int> route_off, route, depart, start_lane;
+  std::vector<float> start_s, start_v, end_s;
+  std::vector<uint8_t> vprof, on0;
+  // params
+  sim_params P{};
+  std::vector<Prof> profs;
+  double start_margin = 0;
+  int Y = 3;
+  // state
+  int t = 0;
+  std::vector<uint8_t> dir, usable;
+  // device
+  std::vector<void *> allocs;
+  int64_t bytes = 0;
+  StepArgs A{};
+  SignalArgs SG{};
+  Slab slab[2]{};
+  InboxRec *inbox[2]{};
+  int32_t *cnt[2]{}, *icnt[2]{};
+  unsigned long long *summ[3]{};
+  float *pubv[2]{};
+  int32_t *pend_off_d = nullptr, *pend_vid_d = nullptr, *pend_head_d = nullptr;
+  uint8_t *usable_d = nullptr;
+  long long *red_d = nullptr;
+  int32_t *stage_d = nullptr;      // device staging for batch setters
+  int stage_cap = 0;
+  void *pinned = nullptr;
+  size_t pinned_cap = 0;
+  cudaEvent_t stage_ev = nullptr;
+  int smem = 0;
+};
+
+namespace {
+
+sim_status fail(sim_s *h, sim_status st, const std::string &m) {
+  if (h) h->err = m; else g_create_err = m;
+  return st;
+}
+
+#define CK(h, x)                                                                    \
+  do {                                                                              \
+    cudaError_t e_ = (x);                                                           \
+    if (e_ != cudaSuccess) {                                                        \
+      (h)->sticky = SIM_E_CUDA;                                                     \
+      return fail((h), SIM_E_CUDA, std::string("CUDA: ") + cudaGetErrorString(e_) + \
+                                       " at " + #x);                                \
+    }                                                                               \
+  } while (0)
+
+template <typename T>
+sim_status dalloc(sim_s *h, T **p, size_t n) {
+  *p = nullptr;
+  if (n == 0) n = 1;
+  cudaError_t e = cudaMalloc((void **)p, n * sizeof(T));
+  if (e != cudaSuccess) {
+    return fail(h, SIM_E_OOM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
+  }
+  h->allocs.push_back(*p);
+  h->bytes += (int64_t)(n * sizeof(T));
+  return SIM_OK;
+}
+
+template <typename T>
+sim_status upload(sim_s *h, T **p, const std::vector<T> &v) {
+  sim_status st = dalloc(h, p, v.size());
+  if (st) return st;
+  if (!v.empty()) CK(h, cudaMemcpy(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return SIM_OK;
+}
+
+bool is_road(const sim_s *h, int l) { return h->road[l] >= 0; }
+
+// usable(ℓ) (ledger L29, L30)
+void compute_usable(sim_s *h) {
+  h->usable.assign(h->nl, 1);
+  for (int l = 0; l < h->nl; ++l)
+    if (is_road(h, l)) h->usable[l] = !(h->kind[l] == KIND_TIDAL && h->dir[l] != 0);
+  for (int l = 0; l < h->nl; ++l) {
+    if (is_road(h, l)) continue;
+    int a = h->pred[l], b = h->succ[h->succ_off[l]];
+    bool u = h->usable[b];
+    if (u && h->kind[a] == KIND_DYNAMIC) {
+      if (h->turn[l] == 1) u = h->dir[a] == 1;
+      else if (h->turn[l] == 0) u = h->dir[a] == 0;
+    }
+    h->usable[l] = u;
+  }
+}
+
+sim_status validate_and_copy(sim_s *h, const sim_graph *g, const sim_trips *tr,
+                             const sim_params *p) {
+  if (!g || !tr || !p) return fail(h, SIM_E_INVALID, "null argument");
+  if (p->dt != 1.0f) return fail(h, SIM_E_INVALID, "params.dt must be 1.0 (P:768)");
+  if (p->n_profiles <= 0 || p->n_profiles > 256 || !p->profiles)
+    return fail(h, SIM_E_INVALID, "n_profiles must be in [1, 256]");
+  for (int i = 0; i < p->n_profiles; ++i) {
+    const sim_profile &q = p->profiles[i];
+    if (!(q.a_max > 0 && q.a_comf > 0 && q.T > 0 && q.s0 > 0 && q.v_max > 0 && q.length > 0))
+      return fail(h, SIM_E_INVALID, "profile " + std::to_string(i) + " has a non-positive field");
+  }
+  if (p->lookahead_lanes < 0 || p->yellow_steps < 0)
+    return fail(h, SIM_E_INVALID, "lookahead_lanes / yellow_steps must be >= 0");
+  const int nl = g->n_lanes, nr = g->n_roads, nj = g->n_junctions, nv = tr->n_trips;
+  if (nl <= 0 || nr <= 0 || nj < 0 || nv < 0) return fail(h, SIM_E_INVALID, "bad sizes");
+  h->nl = nl; h->nr = nr; h->nj = nj; h->nv = nv;
+  h->L.assign(g->lane_length, g->lane_length + nl);
+  h->vmax.assign(g->lane_max_speed, g->lane_max_speed + nl);
+  h->road.assign(g->lane_road, g->lane_road + nl);
+  h->junc.assign(g->lane_junction, g->lane_junction + nl);
+  h->left.assign(g->lane_left, g->lane_left + nl);
+  h->right.assign(g->lane_right, g->lane_right + nl);
+  h->succ_off.assign(g->succ_offsets, g->succ_offsets + nl + 1);
+  h->kind.assign(g->lane_kind, g->lane_kind + nl);
+  h->turn.assign(g->lane_turn, g->lane_turn + nl);
+  h->partner.assign(g->tidal_partner, g->tidal_partner + nl);
+  h->dir.assign(g->lane_dir0, g->lane_dir0 + nl);
+  if (h->succ_off[0] != 0) return fail(h, SIM_E_INVALID, "succ_offsets[0] != 0");
+  for (int l = 0; l < nl; ++l)
+    if (h->succ_off[l + 1] < h->succ_off[l]) return fail(h, SIM_E_INVALID, "succ_offsets not monotone");
+  h->succ.assign(g->succ_lanes, g->succ_lanes + h->succ_off[nl]);
+  for (int l = 0; l < nl; ++l) {
+    std::string id = " (lane " + std::to_string(l) + ")";
+    if (!(h->L[l] > 0 && std::isfinite(h->L[l]))) return fail(h, SIM_E_INVALID, "lane_length must be > 0" + id);
+    if (!(h->vmax[l] > 0 && std::isfinite(h->vmax[l]))) return fail(h, SIM_E_INVALID, "lane_max_speed must be > 0" + id);
+    if ((h->road[l] >= 0) == (h->junc[l] >= 0)) return fail(h, SIM_E_INVALID, "lane must belong to exactly one road or junction" + id);
+    if (h->road[l] >= nr || h->junc[l] >= nj) return fail(h, SIM_E_INVALID, "road/junction id out of range" + id);
+    if (h->kind[l] > 2) return fail(h, SIM_E_INVALID, "bad lane_kind" + id);
+    for (int e = h->succ_off[l]; e < h->succ_off[l + 1]; ++e)
+      if (h->succ[e] < 0 || h->succ[e] >= nl) return fail(h, SIM_E_INVALID, "successor out of range" + id);
+  }
+  std::vector<std::vector<int>> preds(nl);
+  for (int l = 0; l < nl; ++l)
+    for (int e = h->succ_off[l]; e < h->succ_off[l + 1]; ++e) preds[h->succ[e]].push_back(l);
+  h->pred.assign(nl, -1);
+  h->target_road.assign(nl, -1);
+  h->exit_lane.assign(nl, -1);
+  for (int l = 0; l < nl; ++l) {
+    std::string id = " (lane " + std::to_string(l) + ")";
+    if (!is_road(h, l)) {
+      if (h->succ_off[l + 1] - h->succ_off[l] != 1 || preds[l].size() != 1)
+        return fail(h, SIM_E_INVALID, "junction lane needs exactly one predecessor and one successor" + id);
+      int b = h->succ[h->succ_off[l]], a = preds[l][0];
+      if (!is_road(h, b) || !is_road(h, a))
+        return fail(h, SIM_E_INVALID, "junction lane must connect two road lanes" + id);
+      if (h->left[l] >= 0 || h->right[l] >= 0)
+        return fail(h, SIM_E_INVALID, "junction lanes have no left/right neighbours (P:95)" + id);
+      h->pred[l] = a;
+      h->target_road[l] = h->road[b];
+      h->exit_lane[l] = b;
+    } else {
+      h->target_road[l] = h->road[l];
+      h->exit_lane[l] = l;
+    }
+  }
+  h->road_off.assign(g->road_lane_offsets, g->road_lane_offsets + nr + 1);
+  if (h->road_off[0] != 0 || h->road_off[nr] < 0) return fail(h, SIM_E_INVALID, "bad road_lane_offsets");
+  h->road_lanes.assign(g->road_lanes, g->road_lanes + h->road_off[nr]);
+  std::vector<int> seen(nl, 0);
+  for (int r = 0; r < nr; ++r) {
+    std::string id = " (road " + std::to_string(r) + ")";
+    int a = h->road_off[r], b = h->road_off[r + 1];
+    if (b <= a) return fail(h, SIM_E_INVALID, "road without lanes" + id);
+    for (int e = a; e < b; ++e) {
+      int l = h->road_lanes[e];
+      if (l < 0 || l >= nl || h->road[l] != r) return fail(h, SIM_E_INVALID, "road_lanes inconsistent with lane_road" + id);
+      seen[l]++;
+      if (h->L[l] != h->L[h->road_lanes[a]]) return fail(h, SIM_E_INVALID, "lanes of a road must have equal length (L20)" + id);
+      int lf = e > a ? h->road_lanes[e - 1] : -1, rt = e + 1 < b ? h->road_lanes[e + 1] : -1;
+      if (h->left[l] != lf || h->right[l] != rt)
+        return fail(h, SIM_E_INVALID, "lane_left/lane_right must follow road_lanes order (leftmost first)" + id);
+    }
+  }
+  for (int l = 0; l < nl; ++l)
+    if (is_road(h, l) && seen[l] != 1) return fail(h, SIM_E_INVALID, "road lane missing from road_lanes");
+  for (int l = 0; l < nl; ++l)
+    if (h->kind[l] == KIND_TIDAL) {
+      int q = h->partner[l];
+      if (q >= 0 && (q >= nl || h->partner[q] != l || h->kind[q] != KIND_TIDAL))
+        return fail(h, SIM_E_INVALID, "tidal_partner must be mutual (lane " + std::to_string(l) + ")");
+    }
+  // junctions
+  h->jl_off.assign(g->junc_lane_offsets, g->junc_lane_offsets + nj + 1);
+  h->jl.assign(g->junc_lanes, g->junc_lanes + (nj ? h->jl_off[nj] : 0));
+  h->ph_off.assign(g->junc_phase_offsets, g->junc_phase_offsets + nj + 1);
+  int nph = nj ? h->ph_off[nj] : 0;
+  h->green_steps.assign(g->phase_green_steps, g->phase_green_steps + nph);
+  h->pol0.assign(g->junc_policy, g->junc_policy + nj);
+  h->offset0.assign(g->junc_offset_steps, g->junc_offset_steps + nj);
+  h->green_off.assign(nj + 1, 0);
+  for (int j = 0; j < nj; ++j) {
+    int ns = h->jl_off[j + 1] - h->jl_off[j], np = h->ph_off[j + 1] - h->ph_off[j];
+    if (ns < 0 || np < 0) return fail(h, SIM_E_INVALID, "bad junction CSR");
+    for (int e = h->jl_off[j]; e < h->jl_off[j + 1]; ++e)
+      if (h->jl[e] < 0 || h->jl[e] >= nl || h->junc[h->jl[e]] != j)
+        return fail(h, SIM_E_INVALID, "junc_lanes inconsistent with lane_junction (junction " + std::to_string(j) + ")");
+    if (h->pol0[j] > 2) return fail(h, SIM_E_INVALID, "bad junc_policy");
+    for (int k = h->ph_off[j]; k < h->ph_off[j + 1]; ++k)
+      if (h->pol0[j] == POL_FIXED && h->green_steps[k] < 1)
+        return fail(h, SIM_E_INVALID, "FIXED_TIME green durations must be >= 1");
+    h->green_off[j + 1] = h->green_off[j] + (int64_t)ns * np;
+  }
+  h->green.assign(g->phase_green, g->phase_green + h->green_off[nj]);
+  // trips
+  h->route_off.assign(tr->route_offsets, tr->route_offsets + nv + 1);
+  if (h->route_off[0] != 0) return fail(h, SIM_E_INVALID, "route_offsets[0] != 0");
+  h->route.assign(tr->route_roads, tr->route_roads + h->route_off[nv]);
+  h->depart.assign(tr->depart_step, tr->depart_step + nv);
+  h->start_lane.assign(tr->start_lane, tr->start_lane + nv);
+  h->start_s.assign(tr->start_s, tr->start_s + nv);
+  h->start_v.assign(tr->start_v, tr->start_v + nv);
+  h->end_s.assign(tr->end_s, tr->end_s + nv);
+  h->vprof.assign(tr->profile, tr->profile + nv);
+  h->on0.assign(tr->on_network_at_t0, tr->on_network_at_t0 + nv);
+  // road adjacency for route validation
+  std::vector<std::vector<int>> radj(nr);
+  for (int l = 0; l < nl; ++l)
+    if (is_road(h, l))
+      for (int e = h->succ_off[l]; e < h->succ_off[l + 1]; ++e) radj[h->road[l]].push_back(h->target_road[h->succ[e]]);
+  for (auto &v : radj) { std::sort(v.begin(), v.end()); v.erase(std::unique(v.begin(), v.end()), v.end()); }
+  for (int k = 0; k < nv; ++k) {
+    std::string id = " (trip " + std::to_string(k) + ")";
+    int a = h->route_off[k], b = h->route_off[k + 1];
+    if (b <= a || b - a > 65000) return fail(h, SIM_E_INVALID, "route length must be in [1, 65000]" + id);
+    for (int e = a; e < b; ++e) {
+      int r = h->route[e];
+      if (r < 0 || r >= nr) return fail(h, SIM_E_INVALID, "route road out of range" + id);
+      if (e + 1 < b && !std::binary_search(radj[r].begin(), radj[r].end(), h->route[e + 1]))
+        return fail(h, SIM_E_INVALID, "consecutive route roads are not connected" + id);
+    }
+    int sl = h->start_lane[k];
+    if (sl < 0 || sl >= nl || h->road[sl] != h->route[a]) return fail(h, SIM_E_INVALID, "start_lane must be a lane of route[0]" + id);
+    if (!(h->start_s[k] >= 0 && h->start_s[k] <= h->L[sl])) return fail(h, SIM_E_INVALID, "start_s outside [0, L]" + id);
+    if (h->start_s[k] == 0.0f) h->start_s[k] = 0.0f;          // canonical +0
+    if (!(h->start_v[k] >= 0 && std::isfinite(h->start_v[k]))) return fail(h, SIM_E_INVALID, "start_v must be >= 0" + id);
+    int dl = h->road_lanes[h->road_off[h->route[b - 1]]];
+    if (!(h->end_s[k] >= 0 && h->end_s[k] <= h->L[dl])) return fail(h, SIM_E_INVALID, "end_s outside [0, L]" + id);
+    if (h->vprof[k] >= p->n_profiles) return fail(h, SIM_E_INVALID, "profile index out of range" + id);
+    if (h->depart[k] < 0) return fail(h, SIM_E_INVALID, "depart_step must be >= 0" + id);
+  }
+  h->P = *p;
+  h->Y = p->yellow_steps;
+  h->profs.resize(p->n_profiles);
+  float acap = 0;
+  for (int i = 0; i < p->n_profiles; ++i) {
+    const sim_profile &q = p->profiles[i];
+    Prof &o = h->profs[i];
+    o.a_max = q.a_max; o.a_comf = q.a_comf; o.T = q.T; o.s0 = q.s0; o.vmax = q.v_max; o.len = q.length;
+    o.a_max_d = q.a_max; o.a_comf_d = q.a_comf; o.T_d = q.T; o.s0_d = q.s0; o.vmax_d = q.v_max; o.len_d = q.length;
+    o.inv2sqrt_d = 1.0 / (2.0 * std::sqrt(o.a_max_d * o.a_comf_d));
+    o.inv2sqrt_f = (float)o.inv2sqrt_d;
+    o.pad = 0; o.pad_d = 0;
+    acap = std::max(acap, q.a_max);
+  }
+  float vcap = 0;
+  for (int l = 0; l < nl; ++l) vcap = std::max(vcap, h->vmax[l]);
+  h->start_margin = (double)vcap + 0.5 * (double)acap;
+  return SIM_OK;
+}
+
+sim_status build_tiles(sim_s *h) {
+  // tile = road (leftmost lane first) + junction lanes whose predecessor is on it
+  const int nr = h->nr, nl = h->nl;
+  std::vector<std::vector<int>> jls(nr);
+  for (int l = 0; l < nl; ++l)
+    if (!is_road(h, l)) jls[h->road[h->pred[l]]].push_back(l);
+  float lmin = 1e30f;
+  for (auto &q : h->profs) lmin = std::min(lmin, q.len);
+  h->nt = nr;
+  h->tile_lane_off.assign(nr + 1, 0);
+  h->tile_nroad.assign(nr, 0);
+  h->lane_tile.assign(nl, -1);
+  h->lane_local.assign(nl, 0);
+  h->tile_lanes.clear();
+  h->tile_base.assign(nr, 0); h->tile_cap.assign(nr, 0);
+  h->tile_ibase.assign(nr, 0); h->tile_icap.assign(nr, 0);
+  auto lane_cap = [&](int l) { return (int)std::floor(h->L[l] / lmin) + 2; };
+  std::vector<int> feed(nr, 0);
+  for (int l = 0; l < nl; ++l)
+    for (int e = h->succ_off[l]; e < h->succ_off[l + 1]; ++e) {
+      int j = h->succ[e];
+      if (is_road(h, j) && h->lane_tile.size() && h->road[j] != (is_road(h, l) ? h->road[l] : h->road[h->pred[l]]))
+        feed[h->road[j]] += lane_cap(l);
+    }
+  int64_t base = 0, ibase = 0;
+  for (int r = 0; r < nr; ++r) {
+    std::vector<int> lanes(h->road_lanes.begin() + h->road_off[r], h->road_lanes.begin() + h->road_off[r + 1]);
+    h->tile_nroad[r] = (int)lanes.size();
+    std::sort(jls[r].begin(), jls[r].end());
+    lanes.insert(lanes.end(), jls[r].begin(), jls[r].end());
+    if ((int)lanes.size() > kMaxTileLanes)
+      return fail(h, SIM_E_INVALID, "road " + std::to_string(r) + " has more than 64 lanes incl. outgoing junction lanes");
+    int cap = 0;
+    for (size_t k = 0; k < lanes.size(); ++k) {
+      h->lane_tile[lanes[k]] = r;
+      h->lane_local[lanes[k]] = (uint8_t)k;
+      h->tile_lanes.push_back(lanes[k]);
+      cap += lane_cap(lanes[k]);
+    }
+    cap = cap + cap / 4 + 16;
+    int icap = cap + feed[r] + h->tile_nroad[r] + 16;
+    h->tile_lane_off[r + 1] = (int)h->tile_lanes.size();
+    h->tile_base[r] = (int)base; h->tile_cap[r] = cap;
+    h->tile_ibase[r] = (int)ibase; h->tile_icap[r] = icap;
+    base += cap; ibase += icap;
+    if (base + ibase > 2000000000LL) return fail(h, SIM_E_INVALID, "network too large for 32-bit slot indices");
+  }
+  h->sum_cap = base; h->sum_icap = ibase;
+  return SIM_OK;
+}
+
+// initial signal state: FIXED_TIME advanced `offset` steps
+void init_junctions(sim_s *h, HostState &S) {
+  S.jpol.assign(h->nj, 0); S.jphase.assign(h->nj, 0); S.jel.assign(h->nj, 0);
+  S.jy.assign(h->nj, 0); S.jpend.assign(h->nj, 0);
+  for (int j = 0; j < h->nj; ++j) {
+    int K = h->ph_off[j + 1] - h->ph_off[j];
+    int pol = K == 0 ? POL_NONE : h->pol0[j];
+    int ph = 0, el = 0, y = 0, q = 0;
+    if (pol == POL_FIXED)
+      for (int s = 0; s < h->offset0[j]; ++s) {
+        if (y > 0) { y -= 1; if (y == 0) { ph = q; el = 0; } }
+        else {
+          el += 1;
+          if (el >= h->green_steps[h->ph_off[j] + ph]) {
+            int nx = (ph + 1) % K;
+            if (h->Y > 0) { y = h->Y; q = nx; } else { ph = nx; q = nx; el = 0; }
+          }
+        }
+      }
+    S.jpol[j] = (uint8_t)pol; S.jphase[j] = ph; S.jel[j] = el; S.jy[j] = y; S.jpend[j] = q;
+  }
+}
+
+int route_at(const sim_s *h, int vid, int idx) {
+  int a = h->route_off[vid], n = h->route_off[vid + 1] - a;
+  return (idx >= 0 && idx < n) ? h->route[a + idx] : -1;
+}
+
+sim_status push_staging(sim_s *h, const void *src, size_t bytes, void *dst) {
+  if (bytes == 0) return SIM_OK;
+  if (h->pinned_cap < bytes) {
+    if (h->pinned) { CK(h, cudaEventSynchronize(h->stage_ev)); cudaFreeHost(h->pinned); }
+    h->pinned = nullptr;
+    CK(h, cudaHostAlloc(&h->pinned, bytes, cudaHostAllocDefault));
+    h->pinned_cap = bytes;
+  } else {
+    CK(h, cudaEventSynchronize(h->stage_ev));
+  }
+  std::memcpy(h->pinned, src, bytes);
+  CK(h, cudaMemcpyAsync(dst, h->pinned, bytes, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaEventRecord(h->stage_ev, h->stream));
+  return SIM_OK;
+}
+
+// Upload a full state (canonical: stayer slabs sorted per lane, empty inboxes).
+sim_status upload_state(sim_s *h, const HostState &S) {
+  const int nv = h->nv, nt = h->nt, t = S.t;
+  const int par = t & 1;
+  h->t = t;
+  h->dir = S.dir;
+  compute_usable(h);
+  CK(h, cudaMemcpyAsync(h->usable_d, h->usable.data(), h->nl, cudaMemcpyHostToDevice, h->stream));
+  // slabs
+  std::vector<std::vector<int>> per_tile(nt);
+  for (int k = 0; k < nv; ++k)
+    if (S.status[k] == ST_DRIVING) {
+      int l = S.lane[k];
+      if (l < 0 || l >= h->nl) return fail(h, SIM_E_RANGE, "lane out of range for driving vehicle " + std::to_string(k));
+      per_tile[h->lane_tile[l]].push_back(k);
+    }
+  std::vector<float> s(h->sum_cap), v(h->sum_cap);
+  std::vector<int> vid(h->sum_cap), nx(h->sum_cap), nx2(h->sum_cap), wt(h->sum_cap);
+  std::vector<uint32_t> meta(h->sum_cap);
+  std::vector<int> cnt(nt, 0);
+  std::vector<unsigned long long> summ(h->nl, kEmptyKey);
+  std::vector<float> pubv(nv, 0.f);
+  for (int T = 0; T < nt; ++T) {
+    auto &ks = per_tile[T];
+    std::sort(ks.begin(), ks.end(), [&](int a, int b) {
+      int la = h->lane_local[S.lane[a]], lb = h->lane_local[S.lane[b]];
+      if (la != lb) return la < lb;
+      if (S.s[a] != S.s[b]) return S.s[a] < S.s[b];
+      return a < b;
+    });
+    if ((int)ks.size() > h->tile_cap[T])
+      return fail(h, SIM_E_CAPACITY, "state exceeds the slot capacity of road tile " + std::to_string(T));
+    for (size_t i = 0; i < ks.size(); ++i) {
+      int k = ks[i], p = h->tile_base[T] + (int)i;
+      s[p] = S.s[k] == 0.0f ? 0.0f : S.s[k];
+      v[p] = S.v[k];
+      vid[p] = k;
+      nx[p] = route_at(h, k, S.cursor[k] + 1);
+      nx2[p] = route_at(h, k, S.cursor[k] + 2);
+      meta[p] = pack_meta(h->lane_local[S.lane[k]], h->vprof[k], S.cursor[k]);
+      wt[p] = S.wait[k];
+      unsigned long long key = ((unsigned long long)*(const uint32_t *)&s[p] << 32) | (unsigned)k;
+      int l = S.lane[k];
+      if (key < summ[l]) summ[l] = key;
+      pubv[k] = S.v[k];
+    }
+    cnt[T] = (int)ks.size();
+  }
+  Slab &o = h->slab[par];
+  CK(h, cudaMemcpyAsync(o.s, s.data(), s.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(o.v, v.data(), v.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(o.vid, vid.data(), vid.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(o.nxt, nx.data(), nx.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(o.nxt2, nx2.data(), nx2.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(o.meta, meta.data(), meta.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(o.wait, wt.data(), wt.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(h->cnt[par], cnt.data(), nt * 4, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemsetAsync(h->icnt[0], 0, nt * 4, h->stream));
+  CK(h, cudaMemsetAsync(h->icnt[1], 0, nt * 4, h->stream));
+  CK(h, cudaMemcpyAsync(h->summ[t % 3], summ.data(), h->nl * 8, cudaMemcpyHostToDevice, h->stream));
+  launch_fill_u64(h->summ[(t + 1) % 3], kEmptyKey, h->nl, h->stream);
+  launch_fill_u64(h->summ[(t + 2) % 3], kEmptyKey, h->nl, h->stream);
+  CK(h, cudaMemcpyAsync(h->pubv[par], pubv.data(), nv * 4, cudaMemcpyHostToDevice, h->stream));
+  // cold arrays
+  std::vector<int> wfin(nv, 0);
+  for (int k = 0; k < nv; ++k) wfin[k] = S.status[k] == ST_FINISHED ? S.wait[k] : 0;
+  CK(h, cudaMemcpyAsync(h->A.status, S.status.data(), nv, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(h->A.insert_time, S.insert_time.data(), nv * 4, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(h->A.arrive_time, S.arrive_time.data(), nv * 4, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(h->A.wait_fin, wfin.data(), nv * 4, cudaMemcpyHostToDevice, h->stream));
+  // pending queues per start lane sorted by (depart, vid) (ledger L25)
+  std::vector<std::vector<int>> pq(h->nl);
+  for (int k = 0; k < nv; ++k)
+    if (S.status[k] == ST_PENDING) pq[h->start_lane[k]].push_back(k);
+  std::vector<int> poff(h->nl + 1, 0), pvid;
+  for (int l = 0; l < h->nl; ++l) {
+    std::sort(pq[l].begin(), pq[l].end(), [&](int a, int b) {
+      return h->depart[a] != h->depart[b] ? h->depart[a] < h->depart[b] : a < b;
+    });
+    poff[l + 1] = poff[l] + (int)pq[l].size();
+    pvid.insert(pvid.end(), pq[l].begin(), pq[l].end());
+  }
+  std::vector<int> head(poff.begin(), poff.end() - 1);
+  CK(h, cudaMemcpyAsync(h->pend_off_d, poff.data(), poff.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  if (!pvid.empty())
+    CK(h, cudaMemcpyAsync(h->pend_vid_d, pvid.data(), pvid.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(h->pend_head_d, head.data(), head.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  // junctions
+  if (h->nj) {
+    std::vector<int> req(h->nj, -1);
+    CK(h, cudaMemcpyAsync(h->SG.policy, S.jpol.data(), h->nj, cudaMemcpyHostToDevice, h->stream));
+    CK(h, cudaMemcpyAsync(h->SG.phase, S.jphase.data(), h->nj * 4, cudaMemcpyHostToDevice, h->stream));
+    CK(h, cudaMemcpyAsync(h->SG.elapsed, S.jel.data(), h->nj * 4, cudaMemcpyHostToDevice, h->stream));
+    CK(h, cudaMemcpyAsync(h->SG.yellow_left, S.jy.data(), h->nj * 4, cudaMemcpyHostToDevice, h->stream));
+    CK(h, cudaMemcpyAsync(h->SG.pending, S.jpend.data(), h->nj * 4, cudaMemcpyHostToDevice, h->stream));
+    CK(h, cudaMemcpyAsync(h->SG.request, req.data(), h->nj * 4, cudaMemcpyHostToDevice, h->stream));
+  }
+  CK(h, cudaStreamSynchronize(h->stream));   // host vectors die at return
+  return SIM_OK;
+}
+
+sim_status alloc_all(sim_s *h) {
+  sim_status st;
+#define AL(p, n) if ((st = dalloc(h, &(p), (n)))) return st
+#define UP(p, v) if ((st = upload(h, &(p), (v)))) return st
+  StepArgs &A = h->A;
+  const int nl = h->nl, nv = h->nv, nt = h->nt;
+  float *f; int32_t *i32;
+  UP(f, h->L); A.lane_len = f;
+  UP(f, h->vmax); A.lane_vmax = f;
+  UP(i32, h->road); A.lane_road = i32;
+  UP(i32, h->left); A.lane_left = i32;
+  UP(i32, h->right); A.lane_right = i32;
+  UP(i32, h->succ_off); A.succ_off = i32;
+  UP(i32, h->succ); A.succ = i32;
+  UP(i32, h->target_road); A.target_road = i32;
+  UP(i32, h->exit_lane); A.exit_lane = i32;
+  AL(h->usable_d, nl); A.usable = h->usable_d;
+  uint8_t *sig; AL(sig, nl);
+  CK(h, cudaMemset(sig, 0, nl));
+  A.lane_sig = sig;
+  UP(i32, h->lane_tile); A.lane_tile = i32;
+  uint8_t *u8; UP(u8, h->lane_local); A.lane_local = u8;
+  UP(i32, h->tile_lane_off); A.tile_lane_off = i32;
+  UP(i32, h->tile_lanes); A.tile_lanes = i32;
+  UP(i32, h->tile_nroad); A.tile_nroad = i32;
+  UP(i32, h->tile_base); A.tile_base = i32;
+  UP(i32, h->tile_cap); A.tile_cap = i32;
+  UP(i32, h->tile_ibase); A.tile_ibase = i32;
+  UP(i32, h->tile_icap); A.tile_icap = i32;
+  for (int b = 0; b < 2; ++b) {
+    Slab &s = h->slab[b];
+    AL(s.s, h->sum_cap); AL(s.v, h->sum_cap); AL(s.vid, h->sum_cap); AL(s.nxt, h->sum_cap);
+    AL(s.nxt2, h->sum_cap); AL(s.meta, h->sum_cap); AL(s.wait, h->sum_cap);
+    AL(h->inbox[b], h->sum_icap);
+    AL(h->cnt[b], nt); AL(h->icnt[b], nt);
+    AL(h->pubv[b], nv);
+    CK(h, cudaMemset(h->cnt[b], 0, nt * 4));
+    CK(h, cudaMemset(h->icnt[b], 0, nt * 4));
+  }
+  const int64_t sc = h->sum_cap + h->sum_icap;
+  Slab &sc_ = A.scratch;
+  AL(sc_.s, sc); AL(sc_.v, sc); AL(sc_.vid, sc); AL(sc_.nxt, sc); AL(sc_.nxt2, sc);
+  AL(sc_.meta, sc); AL(sc_.wait, sc);
+  AL(A.bsort_scratch, h->sum_icap);
+  for (int b = 0; b < 3; ++b) AL(h->summ[b], nl);
+  UP(i32, h->route_off); A.route_off = i32;
+  UP(i32, h->route); A.route = i32;
+  UP(f, h->end_s); A.end_s = f;
+  UP(u8, h->vprof); A.veh_prof = u8;
+  AL(A.insert_time, nv); AL(A.arrive_time, nv); AL(A.wait_fin, nv); AL(A.status, nv);
+  UP(i32, h->depart); A.depart = i32;
+  UP(f, h->start_s); A.start_s = f;
+  AL(h->pend_off_d, nl + 1); AL(h->pend_vid_d, nv); AL(h->pend_head_d, nl);
+  A.pend_off = h->pend_off_d; A.pend_vid = h->pend_vid_d; A.pend_head = h->pend_head_d;
+  Prof *pr; UP(pr, h->profs); A.prof = pr;
+  AL(A.tacc, (size_t)nt * kNAcc);
+  CK(h, cudaMemset(A.tacc, 0, (size_t)nt * kNAcc * 8));
+  AL(h->red_d, kNAcc + 1);
+  if (h->P.record_decisions) {
+    AL(A.r_leader, nv); AL(A.r_of, nv); AL(A.r_side, 4 * (size_t)nv);
+    AL(A.r_hops, nv); AL(A.r_phantom, nv); AL(A.r_lc, nv); AL(A.r_hand, nv);
+    AL(A.r_fin, nv); AL(A.r_ins, nv); AL(A.r_acc, nv); AL(A.r_guard, nv);
+  }
+  // signals
+  SignalArgs &G = h->SG;
+  G.n_junctions = h->nj; G.yellow = h->Y;
+  AL(G.policy, h->nj); AL(G.phase, h->nj); AL(G.elapsed, h->nj); AL(G.yellow_left, h->nj);
+  AL(G.pending, h->nj); AL(G.request, h->nj);
+  UP(i32, h->jl_off); G.jl_off = i32;
+  UP(i32, h->jl); G.jl = i32;
+  UP(i32, h->ph_off); G.ph_off = i32;
+  int64_t *g64; UP(g64, h->green_off); G.green_off = g64;
+  const uint8_t *cu8; UP(u8, h->green); cu8 = u8; G.green = cu8;
+  UP(i32, h->green_steps); G.green_steps = i32;
+  G.lane_sig = sig;
+  // constants
+  A.n_tiles = nt; A.n_lanes = nl; A.n_veh = nv;
+  A.seed = h->P.seed;
+  A.polite = h->P.politeness; A.b_hard = h->P.b_hard; A.b_safe = h->P.b_safe; A.v_wait = h->P.v_wait;
+  A.start_margin = h->start_margin;
+  A.lookahead = h->P.lookahead_lanes;
+  A.exact_mode = h->P.exact_mode;
+  A.record = h->P.record_decisions;
+  CK(h, cudaEventCreateWithFlags(&h->stage_ev, cudaEventDisableTiming));
+  CK(h, cudaEventRecord(h->stage_ev, h->stream));
+  return SIM_OK;
+#undef AL
+#undef UP
+}
+
+StepArgs step_args(sim_s *h, int t) {
+  StepArgs a = h->A;
+  const int par = t & 1;
+  a.t = t;
+  a.in = h->slab[par];
+  a.out = h->slab[par ^ 1];
+  a.cnt_in = h->cnt[par];
+  a.cnt_out = h->cnt[par ^ 1];
+  a.icnt_in = h->icnt[par];
+  a.icnt_out = h->icnt[par ^ 1];
+  a.inbox_in = h->inbox[par];
+  a.inbox_out = h->inbox[par ^ 1];
+  a.summ_cur = h->summ[t % 3];
+  a.summ_next = h->summ[(t + 1) % 3];
+  a.summ_clear = h->summ[(t + 2) % 3];
+  a.pubv_cur = h->pubv[par];
+  a.pubv_next = h->pubv[par ^ 1];
+  return a;
+}
+
+sim_status check(sim_s *h) {
+  if (!h || !is_live(h)) return fail(nullptr, SIM_E_STATE, "null or destroyed handle");
+  if (h->sticky) return fail(h, SIM_E_STATE, "handle is in a sticky error state: " + h->err);
+  return SIM_OK;
+}
+
+sim_status device_check(sim_s *h) {
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) {
+    h->sticky = SIM_E_CUDA;
+    return fail(h, SIM_E_CUDA, std::string("CUDA (deferred): ") + cudaGetErrorString(e));
+  }
+  return SIM_OK;
+}
+
+sim_status read_counters(sim_s *h, std::vector<long long> &out) {
+  StepArgs a = step_args(h, h->t);
+  launch_reduce_acc(h->A.tacc, h->nt, a.cnt_in, a.icnt_in, h->red_d, h->stream);
+  out.assign(kNAcc + 1, 0);
+  CK(h, cudaMemcpyAsync(out.data(), h->red_d, (kNAcc + 1) * 8, cudaMemcpyDeviceToHost, h->stream));
+  sim_status st = device_check(h);
+  if (st) return st;
+  if (out[ACC_OVERFLOW] > 0) {
+    h->sticky = SIM_E_CAPACITY;
+    return fail(h, SIM_E_CAPACITY, "a road tile inbox overflowed its capacity");
+  }
+  return SIM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+static void destroy_impl(sim_s *h) {
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (void *p : h->allocs) cudaFree(p);
+  if (h->stage_d) cudaFree(h->stage_d);
+  if (h->pinned) cudaFreeHost(h->pinned);
+  if (h->stage_ev) cudaEventDestroy(h->stage_ev);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+sim_status sim_create(const sim_graph *g, const sim_trips *tr, const sim_params *p,
+                      sim_handle *out) {
+  if (!out) return fail(nullptr, SIM_E_INVALID, "out is NULL");
+  *out = nullptr;
+  sim_s *h = new sim_s();
+  sim_status st = validate_and_copy(h, g, tr, p);
+  if (!st) st = build_tiles(h);
+  if (st) { g_create_err = h->err; delete h; return st; }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    delete h;
+    return fail(nullptr, SIM_E_CUDA, "no CUDA device available (the library has no CPU fallback)");
+  }
+  h->device = p->device;
+  if (cudaSetDevice(h->device) != cudaSuccess) { delete h; return fail(nullptr, SIM_E_CUDA, "cudaSetDevice failed"); }
+  if (p->stream) h->stream = (cudaStream_t)p->stream;
+  else {
+    cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+    h->own_stream = true;
+  }
+  h->smem = step_smem_bytes();
+  st = alloc_all(h);
+  if (!st) {
+    HostState S;
+    S.t = 0;
+    const int nv = h->nv;
+    S.status.assign(nv, ST_PENDING); S.lane.assign(nv, -1); S.cursor.assign(nv, 0);
+    S.wait.assign(nv, 0); S.insert_time.assign(nv, -1); S.arrive_time.assign(nv, -1);
+    S.s.assign(nv, 0.f); S.v.assign(nv, 0.f);
+    for (int k = 0; k < nv; ++k)
+      if (h->on0[k]) {
+        S.status[k] = ST_DRIVING; S.lane[k] = h->start_lane[k]; S.s[k] = h->start_s[k];
+        S.v[k] = h->start_v[k]; S.insert_time[k] = 0;
+      }
+    init_junctions(h, S);
+    S.dir = h->dir;
+    st = upload_state(h, S);
+  }
+  if (st) {
+    g_create_err = h->err;
+    destroy_impl(h);
+    return st;
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_live_mu);
+    g_live.insert(h);
+  }
+  *out = h;
+  return SIM_OK;
+}
+
+sim_status sim_step(sim_handle h, int32_t n) {
+  sim_status st = check(h);
+  if (st) return st;
+  if (n < 0) return fail(h, SIM_E_RANGE, "n must be >= 0");
+  for (int i = 0; i < n; ++i) {
+    StepArgs a = step_args(h, h->t);
+    if (h->A.record) {
+      CK(h, cudaMemsetAsync(h->A.r_ins, 0, h->nv, h->stream));
+      CK(h, cudaMemsetAsync(h->A.r_leader, 0xff, h->nv * 4, h->stream));
+      CK(h, cudaMemsetAsync(h->A.r_lc, 0, h->nv, h->stream));
+    }
+    launch_signal(h->SG, h->stream);
+    launch_step(a, h->stream, h->smem);
+    h->t += 1;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    h->sticky = SIM_E_CUDA;
+    return fail(h, SIM_E_CUDA, std::string("launch: ") + cudaGetErrorString(e));
+  }
+  return SIM_OK;
+}
+
+sim_status sim_sync(sim_handle h) {
+  sim_status st = check(h);
+  if (st) return st;
+  return device_check(h);
+}
+
+sim_status sim_set_signal_phase_batch(sim_handle h, int32_t m, const int32_t *junctions,
+                                      const int32_t *phases) {
+  sim_status st = check(h);
+  if (st) return st;
+  if (m < 0 || (m > 0 && (!junctions || !phases))) return fail(h, SIM_E_INVALID, "bad batch");
+  for (int i = 0; i < m; ++i) {
+    int j = junctions[i];
+    if (j < 0 || j >= h->nj) return fail(h, SIM_E_RANGE, "junction out of range");
+    int K = h->ph_off[j + 1] - h->ph_off[j];
+    if (phases[i] < 0 || phases[i] >= K) return fail(h, SIM_E_RANGE, "phase out of range");
+  }
+  if (m == 0) return SIM_OK;
+  if (h->stage_cap < 2 * m) {
+    if (h->stage_d) { CK(h, cudaStreamSynchronize(h->stream)); cudaFree(h->stage_d); }
+    CK(h, cudaMalloc(&h->stage_d, 2 * (size_t)m * 4));
+    h->stage_cap = 2 * m;
+  }
+  std::vector<int32_t> buf(2 * (size_t)m);
+  std::memcpy(buf.data(), junctions, m * 4);
+  std::memcpy(buf.data() + m, phases, m * 4);
+  st = push_staging(h, buf.data(), buf.size() * 4, h->stage_d);
+  if (st) return st;
+  launch_apply_requests(h->SG.request, h->SG.policy, h->stage_d, h->stage_d + m, m, h->stream);
+  return SIM_OK;
+}
+
+sim_status sim_set_signal_phase(sim_handle h, int32_t j, int32_t p) {
+  return sim_set_signal_phase_batch(h, 1, &j, &p);
+}
+
+sim_status sim_set_lane_direction_batch(sim_handle h, int32_t m, const int32_t *lanes,
+                                        const int32_t *dirs) {
+  sim_status st = check(h);
+  if (st) return st;
+  if (m < 0 || (m > 0 && (!lanes || !dirs))) return fail(h, SIM_E_INVALID, "bad batch");
+  for (int i = 0; i < m; ++i) {
+    if (lanes[i] < 0 || lanes[i] >= h->nl || dirs[i] < 0 || dirs[i] > 1)
+      return fail(h, SIM_E_RANGE, "lane or direction out of range");
+    int k = h->kind[lanes[i]];
+    if (k != KIND_DYNAMIC && k != KIND_TIDAL)
+      return fail(h, SIM_E_INVALID, "lane " + std::to_string(lanes[i]) + " is neither DYNAMIC nor TIDAL");
+  }
+  for (int i = 0; i < m; ++i) {
+    int l = lanes[i];
+    h->dir[l] = (uint8_t)dirs[i];
+    if (h->kind[l] == KIND_TIDAL && h->partner[l] >= 0) h->dir[h->partner[l]] = (uint8_t)(1 - dirs[i]);
+  }
+  if (m == 0) return SIM_OK;
+  compute_usable(h);
+  return push_staging(h, h->usable.data(), h->nl, h->usable_d);
+}
+
+sim_status sim_set_lane_direction(sim_handle h, int32_t lane, int32_t dir) {
+  return sim_set_lane_direction_batch(h, 1, &lane, &dir);
+}
+
+sim_status sim_query_sizes(sim_handle h, sim_sizes *out) {
+  if (!h || !is_live(h)) return SIM_E_STATE;
+  if (!out) return SIM_E_INVALID;
+  out->n_vehicles = h->nv; out->n_lanes = h->nl; out->n_junctions = h->nj; out->n_tiles = h->nt;
+  out->device_bytes = h->bytes;
+  return SIM_OK;
+}
+
+sim_status sim_read_state(sim_handle h, sim_state *o) {
+  sim_status st = check(h);
+  if (st) return st;
+  if (!o) return fail(h, SIM_E_INVALID, "out is NULL");
+  std::vector<long long> cs;
+  st = read_counters(h, cs);
+  if (st) return st;
+  const int par = h->t & 1, nv = h->nv, nt = h->nt;
+  std::vector<int> cnt(nt), icnt(nt);
+  CK(h, cudaMemcpy(cnt.data(), h->cnt[par], nt * 4, cudaMemcpyDeviceToHost));
+  CK(h, cudaMemcpy(icnt.data(), h->icnt[par], nt * 4, cudaMemcpyDeviceToHost));
+  const Slab &sl = h->slab[par];
+  std::vector<float> s(h->sum_cap), v(h->sum_cap);
+  std::vector<int> vid(h->sum_cap), wt(h->sum_cap);
+  std::vector<uint32_t> meta(h->sum_cap);
+  CK(h, cudaMemcpy(s.data(), sl.s, s.size() * 4, cudaMemcpyDeviceToHost));
+  CK(h, cudaMemcpy(v.data(), sl.v, v.size() * 4, cudaMemcpyDeviceToHost));
+  CK(h, cudaMemcpy(vid.data(), sl.vid, vid.size() * 4, cudaMemcpyDeviceToHost));
+  CK(h, cudaMemcpy(wt.data(), sl.wait, wt.size() * 4, cudaMemcpyDeviceToHost));
+  CK(h, cudaMemcpy(meta.data(), sl.meta, meta.size() * 4, cudaMemcpyDeviceToHost));
+  std::vector<InboxRec> ib(h->sum_icap);
+  CK(h, cudaMemcpy(ib.data(), h->inbox[par], ib.size() * sizeof(InboxRec), cudaMemcpyDeviceToHost));
+  std::vector<uint8_t> status(nv);
+  std::vector<int> ins(nv), arr(nv), wfin(nv);
+  CK(h, cudaMemcpy(status.data(), h->A.status, nv, cudaMemcpyDeviceToHost));
+  CK(h, cudaMemcpy(ins.data(), h->A.insert_time, nv * 4, cudaMemcpyDeviceToHost));
+  CK(h, cudaMemcpy(arr.data(), h->A.arrive_time, nv * 4, cudaMemcpyDeviceToHost));
+  CK(h, cudaMemcpy(wfin.data(), h->A.wait_fin, nv * 4, cudaMemcpyDeviceToHost));
+  std::vector<int> lane(nv, -1), cur(nv, 0), wait(nv, 0);
+  std::vector<float> vs(nv, 0.f), vv(nv, 0.f);
+  for (int k = 0; k < nv; ++k) if (status[k] == ST_FINISHED) wait[k] = wfin[k];
+  auto put = [&](int T, int k, float ss, float v_, uint32_t m, int w) {
+    lane[k] = h->tile_lanes[h->tile_lane_off[T] + (m & 0xff)];
+    vs[k] = ss; vv[k] = v_; cur[k] = (int)(m >> 16); wait[k] = w;
+  };
+  for (int T = 0; T < nt; ++T) {
+    for (int i = 0; i < cnt[T]; ++i) { int p = h->tile_base[T] + i; put(T, vid[p], s[p], v[p], meta[p], wt[p]); }
+    for (int i = 0; i < icnt[T]; ++i) { const InboxRec &r = ib[h->tile_ibase[T] + i]; put(T, r.vid, r.s, r.v, r.meta, r.wait); }
+  }
+  o->t = h->t;
+  if (o->status) std::memcpy(o->status, status.data(), nv);
+  for (int k = 0; k < nv; ++k) {
+    bool d = status[k] == ST_DRIVING;
+    if (o->lane) o->lane[k] = d ? lane[k] : -1;
+    if (o->cursor) o->cursor[k] = d ? cur[k] : 0;
+    if (o->wait_steps) o->wait_steps[k] = wait[k];
+    if (o->insert_time) o->insert_time[k] = ins[k];
+    if (o->arrive_time) o->arrive_time[k] = arr[k];
+    if (o->s) o->s[k] = d ? vs[k] : 0.f;
+    if (o->v) o->v[k] = d ? vv[k] : 0.f;
+  }
+  if (h->nj) {
+    if (o->junc_policy) CK(h, cudaMemcpy(o->junc_policy, h->SG.policy, h->nj, cudaMemcpyDeviceToHost));
+    if (o->junc_phase) CK(h, cudaMemcpy(o->junc_phase, h->SG.phase, h->nj * 4, cudaMemcpyDeviceToHost));
+    if (o->junc_elapsed) CK(h, cudaMemcpy(o->junc_elapsed, h->SG.elapsed, h->nj * 4, cudaMemcpyDeviceToHost));
+    if (o->junc_yellow_left) CK(h, cudaMemcpy(o->junc_yellow_left, h->SG.yellow_left, h->nj * 4, cudaMemcpyDeviceToHost));
+    if (o->junc_pending) CK(h, cudaMemcpy(o->junc_pending, h->SG.pending, h->nj * 4, cudaMemcpyDeviceToHost));
+  }
+  if (o->lane_dir) std::memcpy(o->lane_dir, h->dir.data(), h->nl);
+  if (o->lane_signal) CK(h, cudaMemcpy(o->lane_signal, h->A.lane_sig, h->nl, cudaMemcpyDeviceToHost));
+  if (o->lane_offsets && o->lane_order) {
+    std::vector<std::vector<int>> per(h->nl);
+    for (int k = 0; k < nv; ++k) if (status[k] == ST_DRIVING) per[lane[k]].push_back(k);
+    int off = 0;
+    for (int l = 0; l < h->nl; ++l) {
+      std::sort(per[l].begin(), per[l].end(), [&](int a, int b) {
+        return vs[a] != vs[b] ? vs[a] < vs[b] : a < b;
+      });
+      o->lane_offsets[l] = off;
+      for (int k : per[l]) o->lane_order[off++] = k;
+    }
+    o->lane_offsets[h->nl] = off;
+  }
+  return SIM_OK;
+}
+
+sim_status sim_read_decisions(sim_handle h, sim_decisions *o) {
+  sim_status st = check(h);
+  if (st) return st;
+  if (!h->A.record) return fail(h, SIM_E_INVALID, "created without record_decisions");
+  st = device_check(h);
+  if (st) return st;
+  const size_t n = h->nv;
+  const StepArgs &A = h->A;
+  if (o->leader_vid) CK(h, cudaMemcpy(o->leader_vid, A.r_leader, n * 4, cudaMemcpyDeviceToHost));
+  if (o->leader_hops) CK(h, cudaMemcpy(o->leader_hops, A.r_hops, n, cudaMemcpyDeviceToHost));
+  if (o->phantom) CK(h, cudaMemcpy(o->phantom, A.r_phantom, n, cudaMemcpyDeviceToHost));
+  if (o->old_follower_vid) CK(h, cudaMemcpy(o->old_follower_vid, A.r_of, n * 4, cudaMemcpyDeviceToHost));
+  if (o->side_vid) CK(h, cudaMemcpy(o->side_vid, A.r_side, 4 * n * 4, cudaMemcpyDeviceToHost));
+  if (o->lc) CK(h, cudaMemcpy(o->lc, A.r_lc, n, cudaMemcpyDeviceToHost));
+  if (o->handoffs) CK(h, cudaMemcpy(o->handoffs, A.r_hand, n, cudaMemcpyDeviceToHost));
+  if (o->accel) CK(h, cudaMemcpy(o->accel, A.r_acc, n * 4, cudaMemcpyDeviceToHost));
+  if (o->finished) CK(h, cudaMemcpy(o->finished, A.r_fin, n, cudaMemcpyDeviceToHost));
+  if (o->inserted) CK(h, cudaMemcpy(o->inserted, A.r_ins, n, cudaMemcpyDeviceToHost));
+  if (o->guard) CK(h, cudaMemcpy(o->guard, A.r_guard, n, cudaMemcpyDeviceToHost));
+  return SIM_OK;
+}
+
+sim_status sim_read_metrics(sim_handle h, sim_metrics *m) {
+  sim_status st = check(h);
+  if (st) return st;
+  if (!m) return fail(h, SIM_E_INVALID, "out is NULL");
+  std::vector<long long> c;
+  st = read_counters(h, c);
+  if (st) return st;
+  m->t = h->t;
+  m->n_driving = c[kNAcc];
+  m->n_finished = c[ACC_FINISHED];
+  // pending = trips never inserted: total - on-network-at-t0 - inserted ... computed from status
+  std::vector<uint8_t> status(h->nv);
+  if (h->nv) CK(h, cudaMemcpy(status.data(), h->A.status, h->nv, cudaMemcpyDeviceToHost));
+  int64_t pend = 0, fin = 0;
+  for (uint8_t s : status) { pend += s == ST_PENDING; fin += s == ST_FINISHED; }
+  m->n_pending = pend;
+  m->n_finished = fin;
+  m->vehicle_steps = c[ACC_VEH_STEPS];
+  m->sum_travel_steps = c[ACC_SUM_TRAVEL];
+  m->sum_wait_steps_finished = c[ACC_SUM_WAIT_FIN];
+  m->sum_depart_delay = c[ACC_SUM_DELAY];
+  m->n_lane_changes = c[ACC_LANE_CHANGES];
+  m->n_handoffs = c[ACC_HANDOFFS];
+  m->n_inserted = c[ACC_INSERTED];
+  m->n_guard_hits = c[ACC_GUARD];
+  m->att_finished = c[ACC_FINISHED] ? (double)c[ACC_SUM_TRAVEL] / (double)c[ACC_FINISHED] : 0.0;
+  if (m->lane_count || m->lane_waiting_at_end) {
+    int32_t *d;
+    CK(h, cudaMalloc(&d, 2 * (size_t)h->nl * 4));
+    CK(h, cudaMemsetAsync(d, 0, 2 * (size_t)h->nl * 4, h->stream));
+    StepArgs a = step_args(h, h->t);
+    launch_lane_stats(a, d, d + h->nl, h->P.queue_zone_m, h->stream);
+    std::vector<int32_t> buf(2 * (size_t)h->nl);
+    CK(h, cudaMemcpyAsync(buf.data(), d, buf.size() * 4, cudaMemcpyDeviceToHost, h->stream));
+    st = device_check(h);
+    cudaFree(d);
+    if (st) return st;
+    if (m->lane_count) std::memcpy(m->lane_count, buf.data(), h->nl * 4);
+    if (m->lane_waiting_at_end) std::memcpy(m->lane_waiting_at_end, buf.data() + h->nl, h->nl * 4);
+  }
+  return SIM_OK;
+}
+
+sim_status sim_load_state(sim_handle h, const sim_state *in) {
+  sim_status st = check(h);
+  if (st) return st;
+  if (!in || !in->status || !in->lane || !in->cursor || !in->wait_steps || !in->insert_time ||
+      !in->arrive_time || !in->s || !in->v || !in->lane_dir ||
+      (h->nj && (!in->junc_policy || !in->junc_phase || !in->junc_elapsed ||
+                 !in->junc_yellow_left || !in->junc_pending)))
+    return fail(h, SIM_E_INVALID, "sim_load_state needs every state field");
+  st = device_check(h);
+  if (st) return st;
+  HostState S;
+  const int nv = h->nv;
+  S.t = in->t;
+  S.status.assign(in->status, in->status + nv);
+  S.lane.assign(in->lane, in->lane + nv);
+  S.cursor.assign(in->cursor, in->cursor + nv);
+  S.wait.assign(in->wait_steps, in->wait_steps + nv);
+  S.insert_time.assign(in->insert_time, in->insert_time + nv);
+  S.arrive_time.assign(in->arrive_time, in->arrive_time + nv);
+  S.s.assign(in->s, in->s + nv);
+  S.v.assign(in->v, in->v + nv);
+  for (int k = 0; k < nv; ++k) {
+    if (S.status[k] > 2) return fail(h, SIM_E_RANGE, "bad status");
+    if (S.status[k] != ST_DRIVING) continue;
+    int l = S.lane[k];
+    if (l < 0 || l >= h->nl) return fail(h, SIM_E_RANGE, "lane out of range");
+    int c = S.cursor[k];
+    if (c < 0 || c >= h->route_off[k + 1] - h->route_off[k]) return fail(h, SIM_E_RANGE, "cursor out of range");
+    if (!(S.s[k] >= 0 && S.s[k] <= h->L[l]) || !(S.v[k] >= 0))
+      return fail(h, SIM_E_RANGE, "s/v out of range for vehicle " + std::to_string(k));
+  }
+  S.jpol.assign(in->junc_policy, in->junc_policy + h->nj);
+  S.jphase.assign(in->junc_phase, in->junc_phase + h->nj);
+  S.jel.assign(in->junc_elapsed, in->junc_elapsed + h->nj);
+  S.jy.assign(in->junc_yellow_left, in->junc_yellow_left + h->nj);
+  S.jpend.assign(in->junc_pending, in->junc_pending + h->nj);
+  S.dir.assign(in->lane_dir, in->lane_dir + h->nl);
+  return upload_state(h, S);
+}
+
+sim_status sim_destroy(sim_handle h) {
+  {
+    std::lock_guard<std::mutex> lk(g_live_mu);
+    if (!h || !g_live.erase(h)) return SIM_E_STATE;     // destroyed twice / never created
+  }
+  destroy_impl(h);
+  return SIM_OK;
+}
+
+const char *sim_last_error(sim_handle h) {
+  return (h && is_live(h)) ? h->err.c_str() : g_create_err.c_str();
+}
+
+}  // extern "C"

@@ -1,0 +1,267 @@
+"""Thin ctypes binding of include/sim.h (argument marshalling only).
+
+Every step of the simulation runs in the CUDA kernels of libsim_b200.so; this
+module only converts numpy arrays / dicts to the C structs and back.  There is
+no CPU fallback: if the extension is missing or no GPU is present, the calls
+fail loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from .build import LIB
+
+SIM_OK, SIM_E_INVALID, SIM_E_RANGE, SIM_E_OOM, SIM_E_CUDA, SIM_E_NCCL, SIM_E_STATE, \
+    SIM_E_CAPACITY = range(8)
+STATUS_NAMES = ["SIM_OK", "SIM_E_INVALID", "SIM_E_RANGE", "SIM_E_OOM", "SIM_E_CUDA",
+                "SIM_E_NCCL", "SIM_E_STATE", "SIM_E_CAPACITY"]
+
+P = C.c_void_p
+
+
+class SimError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES[status] if 0 <= status < 8 else status}: {msg}")
+        self.status = status
+
+
+class sim_graph(C.Structure):
+    _fields_ = [("n_lanes", C.c_int32), ("n_roads", C.c_int32), ("n_junctions", C.c_int32)] + \
+        [(n, P) for n in ("lane_length", "lane_max_speed", "lane_road", "lane_junction",
+                          "lane_left", "lane_right", "succ_offsets", "succ_lanes", "lane_turn",
+                          "lane_kind", "tidal_partner", "lane_dir0", "road_lane_offsets",
+                          "road_lanes", "junc_lane_offsets", "junc_lanes", "junc_phase_offsets",
+                          "phase_green", "phase_green_steps", "junc_policy", "junc_offset_steps")]
+
+
+class sim_trips(C.Structure):
+    _fields_ = [("n_trips", C.c_int32)] + \
+        [(n, P) for n in ("depart_step", "on_network_at_t0", "route_offsets", "route_roads",
+                          "start_lane", "start_s", "start_v", "end_s", "profile")]
+
+
+class sim_params(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("dt", C.c_float), ("n_profiles", C.c_int32),
+                ("profiles", P), ("politeness", C.c_float), ("b_hard", C.c_float),
+                ("b_safe", C.c_float), ("v_wait", C.c_float), ("queue_zone_m", C.c_float),
+                ("yellow_steps", C.c_int32), ("lookahead_lanes", C.c_int32),
+                ("exact_mode", C.c_int32), ("record_decisions", C.c_int32),
+                ("device", C.c_int32), ("stream", P)]
+
+
+class sim_sizes(C.Structure):
+    _fields_ = [("n_vehicles", C.c_int32), ("n_lanes", C.c_int32), ("n_junctions", C.c_int32),
+                ("n_tiles", C.c_int32), ("device_bytes", C.c_int64)]
+
+
+class sim_state(C.Structure):
+    _fields_ = [("t", C.c_int32)] + [(n, P) for n in (
+        "status", "lane", "cursor", "wait_steps", "insert_time", "arrive_time", "s", "v",
+        "junc_policy", "junc_phase", "junc_elapsed", "junc_yellow_left", "junc_pending",
+        "lane_dir", "lane_signal", "lane_offsets", "lane_order")]
+
+
+class sim_decisions(C.Structure):
+    _fields_ = [(n, P) for n in ("leader_vid", "leader_hops", "phantom", "old_follower_vid",
+                                 "side_vid", "lc", "handoffs", "accel", "finished", "inserted",
+                                 "guard")]
+
+
+class sim_metrics(C.Structure):
+    _fields_ = [("t", C.c_int32)] + [(n, C.c_int64) for n in (
+        "n_pending", "n_driving", "n_finished", "vehicle_steps", "sum_travel_steps",
+        "sum_wait_steps_finished", "sum_depart_delay", "n_lane_changes", "n_handoffs",
+        "n_inserted", "n_guard_hits")] + [("att_finished", C.c_double), ("lane_count", P),
+                                          ("lane_waiting_at_end", P)]
+
+
+ABI_FUNCTIONS = ["sim_create", "sim_step", "sim_sync", "sim_set_signal_phase",
+                 "sim_set_signal_phase_batch", "sim_set_lane_direction",
+                 "sim_set_lane_direction_batch", "sim_query_sizes", "sim_read_state",
+                 "sim_read_decisions", "sim_read_metrics", "sim_load_state", "sim_destroy",
+                 "sim_last_error"]
+
+_lib = None
+
+
+def load_library(path=LIB):
+    """Load libsim_b200.so (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"CUDA extension {path} is missing; run "
+                          "`python -m paper_2406_10661_b200.build` (no CPU fallback exists)")
+    lib = C.CDLL(path)
+    i32, h = C.c_int32, C.c_void_p
+    sig = {
+        "sim_create": [P, P, P, C.POINTER(C.c_void_p)],
+        "sim_step": [h, i32], "sim_sync": [h],
+        "sim_set_signal_phase": [h, i32, i32], "sim_set_signal_phase_batch": [h, i32, P, P],
+        "sim_set_lane_direction": [h, i32, i32], "sim_set_lane_direction_batch": [h, i32, P, P],
+        "sim_query_sizes": [h, P], "sim_read_state": [h, P], "sim_read_decisions": [h, P],
+        "sim_read_metrics": [h, P], "sim_load_state": [h, P], "sim_destroy": [h],
+    }
+    for name, args in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = C.c_int32
+    lib.sim_last_error.argtypes = [h]
+    lib.sim_last_error.restype = C.c_char_p
+    _lib = lib
+    return lib
+
+
+def _ptr(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+_GRAPH_DT = dict(lane_length=np.float32, lane_max_speed=np.float32, lane_road=np.int32,
+                 lane_junction=np.int32, lane_left=np.int32, lane_right=np.int32,
+                 succ_offsets=np.int32, succ_lanes=np.int32, lane_turn=np.uint8,
+                 lane_kind=np.uint8, tidal_partner=np.int32, lane_dir0=np.uint8,
+                 road_lane_offsets=np.int32, road_lanes=np.int32, junc_lane_offsets=np.int32,
+                 junc_lanes=np.int32, junc_phase_offsets=np.int32, phase_green=np.uint8,
+                 phase_green_steps=np.int32, junc_policy=np.uint8, junc_offset_steps=np.int32)
+_TRIP_DT = dict(depart_step=np.int32, on_network_at_t0=np.uint8, route_offsets=np.int32,
+                route_roads=np.int32, start_lane=np.int32, start_s=np.float32,
+                start_v=np.float32, end_s=np.float32, profile=np.uint8)
+
+
+class Sim:
+    """One simulation handle (sim_create ... sim_destroy)."""
+
+    def __init__(self, graph, trips, profiles, params, device=0, stream=None,
+                 exact_mode=False, record_decisions=False):
+        lib = load_library()
+        self.lib = lib
+        g = {k: np.ascontiguousarray(graph[k], dtype=dt) for k, dt in _GRAPH_DT.items()}
+        tr = {k: np.ascontiguousarray(trips[k], dtype=dt) for k, dt in _TRIP_DT.items()}
+        prof = np.ascontiguousarray(profiles, dtype=np.float32).reshape(-1, 6)
+        self.n_lanes = int(g["lane_length"].shape[0])
+        self.n_junctions = int(g["junc_lane_offsets"].shape[0] - 1)
+        self.n = int(tr["depart_step"].shape[0])
+        G = sim_graph(self.n_lanes, int(g["road_lane_offsets"].shape[0] - 1), self.n_junctions,
+                      *[_ptr(g[n]) for n, _ in sim_graph._fields_[3:]])
+        T = sim_trips(self.n, *[_ptr(tr[n]) for n, _ in sim_trips._fields_[1:]])
+        Pm = sim_params(int(params["seed"]), float(params.get("dt", 1.0)), prof.shape[0],
+                        _ptr(prof), params["politeness"], params["b_hard"], params["b_safe"],
+                        params["v_wait"], params["queue_zone_m"], params["yellow_steps"],
+                        params["lookahead_lanes"], int(exact_mode), int(record_decisions),
+                        int(device), C.c_void_p(stream) if stream else None)
+        hh = C.c_void_p()
+        st = lib.sim_create(C.byref(G), C.byref(T), C.byref(Pm), C.byref(hh))
+        if st != SIM_OK:
+            raise SimError(st, (lib.sim_last_error(None) or b"").decode())
+        self.h = hh
+        self.record = bool(record_decisions)
+
+    @classmethod
+    def from_scenario(cls, scen, **kw):
+        return cls(scen.graph, scen.trips, scen.profiles, scen.params, **kw)
+
+    def _chk(self, st):
+        if st != SIM_OK:
+            raise SimError(st, (self.lib.sim_last_error(self.h) or b"").decode())
+
+    def step(self, n=1):
+        self._chk(self.lib.sim_step(self.h, int(n)))
+
+    def sync(self):
+        self._chk(self.lib.sim_sync(self.h))
+
+    def set_signal_phase(self, junction, phase):
+        self._chk(self.lib.sim_set_signal_phase(self.h, int(junction), int(phase)))
+
+    def set_signal_phase_batch(self, junctions, phases):
+        j = np.ascontiguousarray(junctions, np.int32)
+        p = np.ascontiguousarray(phases, np.int32)
+        self._chk(self.lib.sim_set_signal_phase_batch(self.h, len(j), _ptr(j), _ptr(p)))
+
+    def set_lane_direction(self, lane, d):
+        self._chk(self.lib.sim_set_lane_direction(self.h, int(lane), int(d)))
+
+    def set_lane_direction_batch(self, lanes, dirs):
+        l = np.ascontiguousarray(lanes, np.int32)
+        d = np.ascontiguousarray(dirs, np.int32)
+        self._chk(self.lib.sim_set_lane_direction_batch(self.h, len(l), _ptr(l), _ptr(d)))
+
+    def query_sizes(self):
+        s = sim_sizes()
+        self._chk(self.lib.sim_query_sizes(self.h, C.byref(s)))
+        return {n: getattr(s, n) for n, _ in sim_sizes._fields_}
+
+    def read_state(self, lane_order=False):
+        n, nj, nl = self.n, self.n_junctions, self.n_lanes
+        b = dict(status=np.zeros(n, np.uint8), lane=np.zeros(n, np.int32),
+                 cursor=np.zeros(n, np.int32), wait_steps=np.zeros(n, np.int32),
+                 insert_time=np.zeros(n, np.int32), arrive_time=np.zeros(n, np.int32),
+                 s=np.zeros(n, np.float32), v=np.zeros(n, np.float32),
+                 junc_policy=np.zeros(nj, np.uint8), junc_phase=np.zeros(nj, np.int32),
+                 junc_elapsed=np.zeros(nj, np.int32), junc_yellow_left=np.zeros(nj, np.int32),
+                 junc_pending=np.zeros(nj, np.int32), lane_dir=np.zeros(nl, np.uint8),
+                 lane_signal=np.zeros(nl, np.uint8))
+        if lane_order:
+            b["lane_offsets"] = np.zeros(nl + 1, np.int32)
+            b["lane_order"] = np.zeros(max(n, 1), np.int32)
+        st = sim_state(0, *[_ptr(b[nm]) if nm in b else None for nm, _ in sim_state._fields_[1:]])
+        self._chk(self.lib.sim_read_state(self.h, C.byref(st)))
+        b["t"] = st.t
+        if lane_order:
+            b["lane_order"] = b["lane_order"][:b["lane_offsets"][-1]]
+        return b
+
+    def load_state(self, state):
+        n, nj, nl = self.n, self.n_junctions, self.n_lanes
+        conv = dict(status=np.uint8, lane=np.int32, cursor=np.int32, wait_steps=np.int32,
+                    insert_time=np.int32, arrive_time=np.int32, s=np.float32, v=np.float32,
+                    junc_policy=np.uint8, junc_phase=np.int32, junc_elapsed=np.int32,
+                    junc_yellow_left=np.int32, junc_pending=np.int32, lane_dir=np.uint8)
+        b = {k: np.ascontiguousarray(state[k], dtype=dt) for k, dt in conv.items()}
+        st = sim_state(int(state["t"]), *[_ptr(b[nm]) if nm in b else None
+                                          for nm, _ in sim_state._fields_[1:]])
+        self._chk(self.lib.sim_load_state(self.h, C.byref(st)))
+
+    def read_decisions(self):
+        n = self.n
+        b = dict(leader_vid=np.zeros(n, np.int32), leader_hops=np.zeros(n, np.int8),
+                 phantom=np.zeros(n, np.int8), old_follower_vid=np.zeros(n, np.int32),
+                 side_vid=np.zeros(4 * n, np.int32), lc=np.zeros(n, np.int8),
+                 handoffs=np.zeros(n, np.int8), accel=np.zeros(n, np.float32),
+                 finished=np.zeros(n, np.int8), inserted=np.zeros(n, np.int8),
+                 guard=np.zeros(n, np.uint8))
+        d = sim_decisions(*[_ptr(b[nm]) for nm, _ in sim_decisions._fields_])
+        self._chk(self.lib.sim_read_decisions(self.h, C.byref(d)))
+        b["side_vid"] = b["side_vid"].reshape(n, 4)
+        return b
+
+    def read_metrics(self, lane_stats=False):
+        m = sim_metrics()
+        bufs = None
+        if lane_stats:
+            bufs = (np.zeros(self.n_lanes, np.int32), np.zeros(self.n_lanes, np.int32))
+            m.lane_count = _ptr(bufs[0])
+            m.lane_waiting_at_end = _ptr(bufs[1])
+        self._chk(self.lib.sim_read_metrics(self.h, C.byref(m)))
+        out = {n: getattr(m, n) for n, _ in sim_metrics._fields_[:-2]}
+        if bufs is not None:
+            out["lane_count"], out["lane_waiting_at_end"] = bufs
+        return out
+
+    def destroy(self):
+        if getattr(self, "h", None):
+            self.lib.sim_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def sim_create(graph, trips, profiles, params, **kw):
+    return Sim(graph, trips, profiles, params, **kw)

@@ -214,7 +214,7 @@ def ring(n_vehicles=20, length=1000.0, laps=40, vmax=16.667, seed=1,
     r = b.add_road(n_lanes, length, vmax)
     for l in b.road_lanes[r]:
         b.connect_direct(l, l)
-    spacing = length / n_vehicles if spacing is None else spacing
+    spacing = length * n_lanes / n_vehicles if spacing is None else spacing
     n = n_vehicles
     lanes = np.array([b.road_lanes[r][k % n_lanes] for k in range(n)], np.int32)
     s = np.array([(spacing * (k // n_lanes)) % length for k in range(n)],
@@ -336,12 +336,11 @@ def _grid_core(rows, cols, spacing, lane_fn, vmax_fn, rng, jitter=0.0,
             if deg[a] <= 2 or deg[c] <= 2:
                 continue
             keep.discard((a, c))
-            if not _connected(pos.keys(), keep):
-                keep.add((a, c))
-                continue
             deg[a] -= 1
             deg[c] -= 1
             removed += 1
+        if not _connected(pos.keys(), keep):
+            raise RuntimeError("removal disconnected the grid; use another seed")
     road_info = {}
     in_roads = {k: {} for k in pos}
     out_roads = {k: {} for k in pos}
@@ -523,24 +522,39 @@ def grid(rows=4, cols=4, road_len=300.0, lanes=2, n_trips=5000,
                     meta=dict(builder=b, sources=sources, sinks=sinks))
 
 
-def _random_walk(b, succ_roads, start_road, n_roads, rng):
-    route = [start_road]
+def _random_walks(b, succ_roads, start_roads, n_roads, rng):
+    """Vectorised biased random walks (straight 0.6, left 0.2, right 0.2, no
+    U-turn) of n_roads roads from each start road; a walk stops at a dead end."""
     meta = b.road_meta
-    for _ in range(n_roads - 1):
-        r = route[-1]
+    nr = len(meta)
+    cand = np.full((nr, 3), -1, np.int64)
+    w = np.zeros((nr, 3))
+    for r in range(nr):
         h = meta[r][2]
-        opts, w = [], []
+        k = 0
         for r2 in succ_roads[r]:
             h2 = meta[r2][2]
-            if h2 == (h + 2) % 4:
-                continue           # no U-turns
-            opts.append(r2)
-            w.append(0.6 if h2 == h else 0.2)
-        if not opts:
-            break
-        w = np.array(w) / np.sum(w)
-        route.append(opts[int(rng.choice(len(opts), p=w))])
-    return route
+            if h2 == (h + 2) % 4 or k >= 3:
+                continue
+            cand[r, k] = r2
+            w[r, k] = 0.6 if h2 == h else 0.2
+            k += 1
+    tot = w.sum(1, keepdims=True)
+    cw = np.cumsum(np.where(tot > 0, w / np.where(tot > 0, tot, 1), 0), axis=1)
+    n = len(start_roads)
+    routes = np.full((n, n_roads), -1, np.int64)
+    routes[:, 0] = start_roads
+    alive = np.ones(n, bool)
+    for s in range(1, n_roads):
+        cur = routes[:, s - 1]
+        u = rng.random(n)
+        pick = (u[:, None] >= cw[np.maximum(cur, 0)]).sum(1)
+        pick = np.minimum(pick, 2)
+        nxt = cand[np.maximum(cur, 0), pick]
+        alive &= (cur >= 0) & (tot[np.maximum(cur, 0), 0] > 0) & (nxt >= 0)
+        routes[:, s] = np.where(alive, nxt, -1)
+    lens = (routes >= 0).sum(1)
+    return routes, lens
 
 
 def _place_on_lanes(lane_ids, lane_len, n_vehicles, prof_len, profile_of, rng,
@@ -630,16 +644,20 @@ def city(G=72, spacing=900.0, n_vehicles=2_000_000, seed=4, route_len=40,
                                      profiles[:, 5], profile_of, rng)
     succ_roads = b.road_successors()
     idx = np.where(keep)[0]
-    routes = []
-    end_s = []
-    for vid in idx:
-        r0 = int(g["lane_road"][lanes[vid]])
-        rt = _random_walk(b, succ_roads, r0, route_len, rng)
-        routes.append(rt)
-        end_s.append(float(g["lane_length"][b.road_lanes[rt[-1]][0]]))
+    r0 = g["lane_road"][lanes[idx]]
+    rt, lens = _random_walks(b, succ_roads, r0, route_len, rng)
     n = len(idx)
-    trips = _trip_arrays(routes, lanes[idx], s[idx], np.zeros(n), end_s,
-                         np.zeros(n), np.ones(n), profile_of[idx])
+    off = np.zeros(n + 1, np.int64)
+    off[1:] = np.cumsum(lens)
+    flat = rt[rt >= 0]
+    last = rt[np.arange(n), lens - 1]
+    first_lane_of_road = g["road_lanes"][g["road_lane_offsets"][:-1]]
+    end_s = g["lane_length"][first_lane_of_road[last]]
+    trips = dict(depart_step=np.zeros(n, np.int32), on_network_at_t0=np.ones(n, np.uint8),
+                 route_offsets=off.astype(np.int32), route_roads=flat.astype(np.int32),
+                 start_lane=lanes[idx].astype(np.int32), start_s=s[idx].astype(np.float32),
+                 start_v=np.zeros(n, np.float32), end_s=end_s.astype(np.float32),
+                 profile=profile_of[idx].astype(np.uint8))
     return Scenario(f"city{G}", g, trips, profiles, default_params(seed),
                     meta=dict(builder=b, junc_xy=np.array(b.junc_xy)))
 
