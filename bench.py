@@ -1,0 +1,306 @@
+"""bench.py — vehicle-steps/s of the B200 hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Workload (N=1): SURVEY §8(d) C4, the city-like synthetic network (G = 72
+perturbed grid, ~133k lanes, 5,184 signalised junctions) with 2,000,000
+vehicles on the network, seeded.  A step is one call of sim_step(1): the
+signal kernel + the fused step kernel over all road tiles.  Each timed step is
+preceded (outside its events) by an L2 flush (a 512 MiB device write), so
+every step streams its state from HBM.  Device time: CUDA events on the
+simulation stream.  value = sum over the timed steps of vehicles moved / time.
+
+--impl reference times the fp64 CPU oracle (oracle/, the reference arm of
+this task) on the same workload on the host's cores.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "vehicle-steps/sec"
+UNIT = "vehicle-steps/s"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+NCU_TRAFFIC = os.path.join(ROOT, "profiles", "ncu_kstep_traffic.json")
+
+
+def algorithmic_bytes(n_veh, n_movers, n_lanes):
+    """Bytes one step must move: the 28 B hot record read + written
+    per vehicle, 8 B extra per mover (32 B inbox record written and read
+    instead of the slab record), and per lane 24 B of metadata + 24 B of
+    summary traffic (first-vehicle key write / clear / read)."""
+    return 56.0 * n_veh + 8.0 * n_movers + 48.0 * n_lanes
+
+
+def peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons via NVML while the timed region runs."""
+    REASONS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+               "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, device=0):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                fn = getattr(self.nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                    getattr(self.nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
+                r = fn(self.h)
+                for k, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def make_workload(rank=0):
+    import synth
+    scen = synth.city(G=72, n_vehicles=2_000_000, seed=4 + 1000 * rank)
+    return scen
+
+
+def workload_config(scen, extra=None):
+    cfg = {"workload": "C4 city-like synthetic network (SURVEY 8(d)): G=72 perturbed grid, "
+                       "2M vehicles on the network at t=0, fixed-time signals",
+           "n_vehicles": int(scen.n_trips), "n_lanes": int(scen.n_lanes),
+           "n_junctions": int(len(scen.graph["junc_lane_offsets"]) - 1),
+           "n_roads": int(len(scen.graph["road_lane_offsets"]) - 1),
+           "l2": "flushed (512 MiB write) before every timed step",
+           "seed": int(scen.params["seed"])}
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+def cpu_baseline(scen, budget_s=20.0, max_steps=10):
+    """The oracle as it stands, single-threaded, on a bounded sample (the
+    first steps of the same workload from the same initial state)."""
+    import oracle
+    oracle.build()
+    o = oracle.Oracle(scen)
+    done, veh, t0 = 0, 0, time.perf_counter()
+    while done < max_steps and (time.perf_counter() - t0) < budget_s:
+        before = o.metrics()["vehicle_steps"]
+        o.step(1)
+        veh += o.metrics()["vehicle_steps"] - before
+        done += 1
+    dt = time.perf_counter() - t0
+    return {"value": veh / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"first {done} steps of the same C4 workload ({veh} vehicle-steps, "
+                      f"{dt:.1f} s, serial fp64 C++ oracle)"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    scen = make_workload(0)
+    import oracle
+    oracle.build()
+    o = oracle.Oracle(scen)
+    for _ in range(args.warmup):
+        o.step(1)
+    budget = 150.0
+    done, veh, t0 = 0, 0, time.perf_counter()
+    while done < args.steps and (time.perf_counter() - t0) < budget:
+        before = o.metrics()["vehicle_steps"]
+        o.step(1)
+        veh += o.metrics()["vehicle_steps"] - before
+        done += 1
+    dt = time.perf_counter() - t0
+    value = veh / dt
+    sample = (f"{done} of {args.steps} timed steps (after {args.warmup} warm-up) of the C4 "
+              f"workload, {veh} vehicle-steps in {dt:.1f} s")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": done, "warmup": args.warmup,
+            "ms_per_step": 1e3 * dt / max(done, 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(scen),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_gpu(args, rank, world, local_rank):
+    import torch
+    import paper_2406_10661_b200 as p
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if rank == 0:
+        p.build()
+    if world > 1:
+        torch.distributed.barrier()
+    scen = make_workload(rank)
+    stream = torch.cuda.Stream(dev)          # the simulation stream (events recorded on it)
+    torch.cuda.set_stream(stream)
+    sim = p.Sim.from_scenario(scen, device=local_rank, stream=stream.cuda_stream)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    for _ in range(args.warmup):
+        sim.step(1)
+    m0 = sim.read_metrics()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    sim.enable_timing(True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            flush.fill_(k & 0xff)                      # L2 flush, outside the events
+            evs[k][0].record(stream)
+            sim.step(1)
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    step_ms = sum(a.elapsed_time(b) for a, b in evs)
+    kstep_ms, ksig_ms, launches = sim.read_timing()
+    sim.enable_timing(False)
+    m1 = sim.read_metrics()
+    vsteps = m1["vehicle_steps"] - m0["vehicle_steps"]
+    movers = (m1["n_lane_changes"] - m0["n_lane_changes"]) + (m1["n_handoffs"] - m0["n_handoffs"]) \
+        + (m1["n_finished"] - m0["n_finished"])
+    t_max = step_ms
+    tot_vsteps = vsteps
+    if world > 1:
+        t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        v = torch.tensor([vsteps], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(v)
+        t_max, tot_vsteps = float(t.item()), float(v.item())
+    value = tot_vsteps / (t_max / 1e3)
+    # roofline of the dominant kernel (k_step)
+    peak, peak_kind = peaks()
+    per_launch_bytes = algorithmic_bytes(vsteps / args.steps, movers / args.steps, scen.n_lanes)
+    kstep_avg_s = kstep_ms / 1e3 / args.steps
+    achieved = per_launch_bytes / kstep_avg_s / 1e9
+    traffic = None
+    try:
+        with open(NCU_TRAFFIC) as f:
+            tr = json.load(f)
+        if tr.get("workload") == "C4" and tr.get("n_vehicles") == scen.n_trips:
+            traffic = tr.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    # e2e: RL-style loop through the public API with host buffers
+    nj = len(scen.graph["junc_lane_offsets"]) - 1
+    jids = np.arange(nj, dtype=np.int32)
+    offs = scen.graph["junc_offset_steps"].astype(np.int64)
+    e2e_steps = max(10, min(args.steps, 50))
+    lane_bytes = 8 * scen.n_lanes
+    torch.cuda.synchronize()
+    me0 = sim.read_metrics()
+    t0 = time.perf_counter()
+    for k in range(e2e_steps):
+        tau = (me0["t"] + k + offs) % 102                 # host fixed-time controller
+        ph = np.where(tau < 33, 0, np.where(tau < 51, 1, np.where(tau < 84, 2, 3))).astype(np.int32)
+        sim.set_signal_phase_batch(jids, ph)              # H2D: the step's control input
+        sim.step(1)
+        obs = sim.read_metrics(lane_stats=True)           # D2H: counters + lane queues
+    e2e_dt = time.perf_counter() - t0
+    e2e_v = obs["vehicle_steps"] - me0["vehicle_steps"]
+    e2e_val = e2e_v / e2e_dt
+    if world > 1:
+        t = torch.tensor([e2e_dt], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        v = torch.tensor([e2e_v], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(v)
+        e2e_val = float(v.item()) / float(t.item())
+    if rank != 0:
+        return
+    cpu = cpu_baseline(scen) if world == 1 and not args.no_cpu else None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": workload_config(scen, {
+            "parallelism": "single GPU" if world == 1 else
+            f"{world} independent replicas (one C4 instance per GPU; spatial partition not yet built)",
+            "fp64_guard_hits_per_step": (m1["n_guard_hits"] - m0["n_guard_hits"]) / args.steps}),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": "k_step", "kernel_ms_avg": kstep_ms / args.steps,
+                     "signal_kernel_ms_avg": ksig_ms / args.steps,
+                     "alg_bytes_per_launch": per_launch_bytes},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * nj,
+                "d2h_bytes_per_step": lane_bytes + 8 * 15, "steps": e2e_steps},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl")
+    run_gpu(args, rank, world, local_rank)
+    if world > 1:
+        import torch
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -178,6 +178,14 @@ sim_status sim_read_metrics(sim_handle h, sim_metrics *out);
  * rebuilt from status; all fields except lane_signal/lane_offsets/lane_order
  * are required. */
 sim_status sim_load_state(sim_handle h, const sim_state *in);
+/* Device timing (measurement hook): enable = 1 opens a new window
+ * in which every sim_step launch is bracketed by CUDA events on the handle's
+ * stream (and resets the launch counter); sim_read_timing (synchronising)
+ * returns the summed device time of the step kernels and of the signal
+ * kernels in the window, and the number of library kernel launches. */
+sim_status sim_enable_timing(sim_handle h, int32_t enable);
+sim_status sim_read_timing(sim_handle h, double *step_kernel_ms, double *signal_kernel_ms,
+                           int64_t *n_launches);
 sim_status sim_destroy(sim_handle h);
 /* Last error message of h (NULL h: the calling thread's last create error). */
 const char *sim_last_error(sim_handle h);

@@ -22,6 +22,8 @@ constexpr int kThreads = 128;        // k_step block size
 constexpr int kSmemVeh = 448;        // snapshot slots held in shared memory (larger tiles use global scratch)
 constexpr int kSmemInbox = 96;       // inbox keys sorted in shared memory
 constexpr int kNAcc = 12;            // per-tile int64 accumulators
+constexpr int kMaxRoadLanes = 8;     // road lanes per tile cached in the successor table
+constexpr int kMaxSucc = 12;         // successors per road lane cached in the table
 constexpr uint64_t kEmptyKey = ~0ull;
 
 enum Acc {
@@ -72,6 +74,8 @@ struct StepArgs {
   const int32_t *target_road;       // road reached through lane j
   const int32_t *exit_lane;         // junction lane: its successor; road lane: itself
   const uint8_t *usable;
+  const int4 *outroads;             // per lane: <= 4 distinct roads reachable through usable
+                                    // successors (-1 pad; w == -2: more, scan the CSR)
   const uint8_t *lane_sig;
   const int32_t *lane_tile;
   const uint8_t *lane_local;
@@ -85,6 +89,9 @@ struct StepArgs {
   InboxRec *inbox_out;
   Slab scratch;                     // global fallback for large tiles ([base+ibase, +cap+icap))
   int32_t *bsort_scratch;           // [Σ icap] inbox sort order for large inboxes
+  float *rs_s1, *rs_v1;             // per-slot results for large tiles (scratch indexing)
+  int32_t *rs_lane, *rs_wait, *rs_cur, *rs_glist;
+  uint8_t *rs_flags;
   // lane summaries (first vehicle key) for t, t+1, t+2 (triple buffer)
   const unsigned long long *summ_cur;
   unsigned long long *summ_next, *summ_clear;
@@ -130,7 +137,8 @@ void launch_set_i32(int32_t *dst, const int32_t *idx, const int32_t *val, int m,
 void launch_apply_requests(int32_t *request, uint8_t *policy, const int32_t *junc,
                            const int32_t *phase, int m, void *stream);
 void launch_reduce_acc(const long long *tacc, int n_tiles, const int32_t *cnt,
-                       const int32_t *icnt, long long *out, void *stream);
+                       const int32_t *icnt, const uint8_t *status, int nv, long long *out,
+                       void *stream);
 void launch_lane_stats(const StepArgs &a, int32_t *lane_count, int32_t *lane_wait,
                        float queue_zone, void *stream);
 void launch_fill_u64(unsigned long long *p, unsigned long long v, int64_t n, void *stream);

@@ -30,16 +30,73 @@ __device__ __forceinline__ bool key_less(unsigned long long h1, int v1, unsigned
   return h1 < h2 || (h1 == h2 && v1 < v2);
 }
 
+// fp64 canonical path (exact_mode and guard fallback) kept out of line so the
+// hot fp32 path is register-allocated on its own
+#ifndef F64_NOINLINE
+#define F64_NOINLINE __forceinline__
+#endif
+#ifdef GUARD_STATS
+__device__ unsigned long long g_guard_stats[32];
+#endif
+__device__ F64_NOINLINE void veh_update_f64(const StepArgs &A, const TileSh &T, const View &C,
+                                            int i, Res &r) {
+  Guard g;
+  g.hit = false;
+  g.why = 0;
+  veh_update<double, false>(A, T, C, i, r, g);
+}
+
+struct ResView {                     // per-slot step results (shared or global scratch)
+  float *s1, *v1;
+  int32_t *lane, *wait, *cur;
+  uint8_t *flags;                    // lc+1 : 2 | fin : 1 | min(hand, 31) : 5
+};
+__device__ __forceinline__ void store_res(const ResView &R, int i, const Res &r) {
+  R.s1[i] = r.s1;
+  R.v1[i] = r.v1;
+  R.lane[i] = r.lane_g;
+  R.wait[i] = r.wait1;
+  R.cur[i] = r.cursor;
+  R.flags[i] = (uint8_t)((r.lc + 1) | (r.fin ? 4 : 0) | ((r.hand > 31 ? 31 : r.hand) << 3));
+}
+__device__ __forceinline__ void load_res(const ResView &R, int i, Res &r) {
+  r.s1 = R.s1[i];
+  r.v1 = R.v1[i];
+  r.lane_g = R.lane[i];
+  r.wait1 = R.wait[i];
+  r.cursor = R.cur[i];
+  const int f = R.flags[i];
+  r.lc = (f & 3) - 1;
+  r.fin = (f & 4) != 0;
+  r.hand = f >> 3;
+}
+__device__ __forceinline__ void record(const StepArgs &A, int vid, const Res &r, bool guard) {
+  A.r_leader[vid] = r.leader;
+  A.r_hops[vid] = (int8_t)r.hops;
+  A.r_phantom[vid] = (int8_t)r.phantom;
+  A.r_of[vid] = r.of_vid;
+  for (int q = 0; q < 4; ++q) A.r_side[4 * vid + q] = r.side[q];
+  A.r_lc[vid] = (int8_t)r.lc;
+  A.r_hand[vid] = (int8_t)(r.hand > 127 ? 127 : r.hand);
+  A.r_acc[vid] = r.acc;
+  A.r_fin[vid] = (int8_t)r.fin;
+  A.r_guard[vid] = (uint8_t)(guard ? 1 : 0);
+}
+
 struct StepShared {
   TileSh T;
   int warp_tot[kThreads / 32];
   int nst_out;
+  int nguard;
   unsigned long long bk_hi[kSmemInbox];
   int bk_vid[kSmemInbox];
   int bsort[kSmemInbox];
 };
 
-__global__ void __launch_bounds__(kThreads) k_step(StepArgs A) {
+#ifndef KSTEP_MINB
+#define KSTEP_MINB 4
+#endif
+__global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ StepShared S;
   TileSh &T = S.T;
@@ -58,6 +115,7 @@ __global__ void __launch_bounds__(kThreads) k_step(StepArgs A) {
     T.cap = A.tile_cap[tile];
     T.icap = A.tile_icap[tile];
     S.nst_out = 0;
+    S.nguard = 0;
   }
   for (int l = tid; l < nl; l += kThreads) {
     int g = A.tile_lanes[l0 + l];
@@ -72,6 +130,29 @@ __global__ void __launch_bounds__(kThreads) k_step(StepArgs A) {
     int lf = A.lane_left ? A.lane_left[g] : -1, rt = A.lane_right ? A.lane_right[g] : -1;
     T.left[l] = (lf >= 0 && A.lane_tile[lf] == tile) ? (int8_t)A.lane_local[lf] : (int8_t)-1;
     T.right[l] = (rt >= 0 && A.lane_tile[rt] == tile) ? (int8_t)A.lane_local[rt] : (int8_t)-1;
+  }
+  // successor table of the tile's road lanes (usable successors only)
+  const int nroad = A.tile_nroad[tile];
+  if (tid == 0) T.tab_ok = nroad <= kMaxRoadLanes ? 1 : 0;
+  if (nroad <= kMaxRoadLanes) {
+    for (int l = tid; l < nroad; l += kThreads) {
+      const int g = A.tile_lanes[l0 + l];
+      const int e0 = A.succ_off[g], e1 = A.succ_off[g + 1];
+      int k = 0;
+      bool ok = e1 - e0 <= kMaxSucc;
+      if (ok)
+        for (int e = e0; e < e1; ++e) {
+          const int j = A.succ[e];
+          if (!A.usable[j]) continue;
+          SuccEnt &s = T.se[l][k++];
+          s.j = j;
+          s.troad = A.target_road[j];
+          s.b = A.exit_lane[j];
+          s.outr = A.outroads[s.b];
+        }
+      T.sn[l] = (uint8_t)k;
+      if (!ok) T.tab_ok = 0;
+    }
   }
   const int n_st = A.cnt_in[tile];
   const int n_in = A.icnt_in[tile];
@@ -187,46 +268,77 @@ __global__ void __launch_bounds__(kThreads) k_step(StepArgs A) {
   }
   __syncthreads();
 
-  // ---- 2-3. per-vehicle update + outputs ------------------------------------
+  // ---- 2. per-vehicle update (a2-a4), results staged per snapshot slot ------
+  // Phase A: every vehicle on the fp32 fast path; vehicles whose decision
+  // margins fall inside the guard band are queued.  Phase B: the queue is
+  // recomputed with the canonical fp64 sequence, packed onto few lanes (so a
+  // rare fallback does not stall whole warps).  No barrier inside either loop.
+  ResView R;
+  int *glist;
+  if (smem_ok) {
+    unsigned char *rb = dyn + kSmemVeh * 7 * 4;
+    R.s1 = reinterpret_cast<float *>(rb);
+    R.v1 = R.s1 + kSmemVeh;
+    R.lane = reinterpret_cast<int32_t *>(R.v1 + kSmemVeh);
+    R.wait = R.lane + kSmemVeh;
+    R.cur = R.wait + kSmemVeh;
+    glist = R.cur + kSmemVeh;
+    R.flags = reinterpret_cast<uint8_t *>(glist + kSmemVeh);
+  } else {
+    const int sb = base + ibase;
+    R.s1 = A.rs_s1 + sb;
+    R.v1 = A.rs_v1 + sb;
+    R.lane = A.rs_lane + sb;
+    R.wait = A.rs_wait + sb;
+    R.cur = A.rs_cur + sb;
+    R.flags = A.rs_flags + sb;
+    glist = A.rs_glist + sb;
+  }
   long long acc_travel = 0, acc_waitfin = 0;
   int acc_fin = 0, acc_lc = 0, acc_hand = 0, acc_guard = 0, acc_ovf = 0;
+  for (int i = tid; i < n; i += kThreads) {
+    Res r;
+    Guard g;
+    g.hit = false;
+    g.why = 0;
+    if (A.exact_mode) {
+      veh_update_f64(A, T, C, i, r);
+    } else {
+      veh_update<float, true>(A, T, C, i, r, g);
+      if (g.hit) {
+        glist[atomicAdd(&S.nguard, 1)] = i;
+        acc_guard += 1;
+#ifdef GUARD_STATS
+        for (int b = 0; b < 32; ++b)
+          if (g.why & (1u << b)) atomicAdd(&g_guard_stats[b], 1ull);
+#endif
+      }
+    }
+    store_res(R, i, r);
+    if (A.record) record(A, C.vid[i], r, g.hit);
+  }
+  __syncthreads();
+  for (int q = tid; q < S.nguard; q += kThreads) {
+    const int i = glist[q];
+    Res r;
+    veh_update_f64(A, T, C, i, r);
+    store_res(R, i, r);
+    if (A.record) record(A, C.vid[i], r, true);
+  }
+  __syncthreads();
+
+  // ---- 3. outputs, in chunks of kThreads (order-preserving compaction) -------
   const int nchunks = (n + kThreads - 1) / kThreads;
   for (int ch = 0; ch < nchunks; ++ch) {
     const int i = ch * kThreads + tid;
-    const bool active = i < n;
-    Res r;
     int kind = 0;                      // 0 none, 1 stayer, 2 mover, 3 finished
-    if (active) {
-      Guard g;
-      g.hit = false;
-      if (A.exact_mode) {
-        veh_update<double, false>(A, T, C, i, r, g);
-      } else {
-        veh_update<float, true>(A, T, C, i, r, g);
-        if (g.hit) {
-          Guard g2;
-          g2.hit = false;
-          veh_update<double, false>(A, T, C, i, r, g2);
-          acc_guard += 1;
-        }
-      }
+    Res r;
+    if (i < n) {
+      load_res(R, i, r);
       const int l = m_lane(C.meta[i]);
       if (r.fin) kind = 3;
       else if (r.lc == 0 && r.hand == 0 && r.lane_g == T.glob[l]) kind = 1;
       else kind = 2;
-      if (A.record) {
-        const int vid = C.vid[i];
-        A.r_leader[vid] = r.leader;
-        A.r_hops[vid] = (int8_t)r.hops;
-        A.r_phantom[vid] = (int8_t)r.phantom;
-        A.r_of[vid] = r.of_vid;
-        for (int q = 0; q < 4; ++q) A.r_side[4 * vid + q] = r.side[q];
-        A.r_lc[vid] = (int8_t)r.lc;
-        A.r_hand[vid] = (int8_t)(r.hand > 127 ? 127 : r.hand);
-        A.r_acc[vid] = r.acc;
-        A.r_fin[vid] = (int8_t)r.fin;
-        A.r_guard[vid] = (uint8_t)(g.hit ? 1 : 0);
-      }
     }
     // order-preserving compaction of stayers (block scan)
     const unsigned ball = __ballot_sync(0xffffffffu, kind == 1);
@@ -447,18 +559,26 @@ __global__ void k_apply_requests(int32_t *request, uint8_t *policy, const int32_
 }
 
 __global__ void k_reduce_acc(const long long *tacc, int n_tiles, const int32_t *cnt,
-                             const int32_t *icnt, long long *out) {
-  __shared__ long long sh[kNAcc + 1][8];
-  const int c = blockIdx.x;                         // one block per counter (+1: driving)
+                             const int32_t *icnt, const uint8_t *status, int nv, long long *out) {
+  // blocks 0..kNAcc-1: per-tile counters; kNAcc: driving (stayers + inbox);
+  // kNAcc+1 / +2: PENDING / FINISHED vehicles from the status array
+  __shared__ long long sh[8];
+  const int c = blockIdx.x;
   long long x = 0;
-  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x)
-    x += (c < kNAcc) ? tacc[(size_t)t * kNAcc + c] : (long long)(cnt[t] + icnt[t]);
+  if (c < kNAcc) {
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) x += tacc[(size_t)t * kNAcc + c];
+  } else if (c == kNAcc) {
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) x += (long long)(cnt[t] + icnt[t]);
+  } else {
+    const uint8_t want = (c == kNAcc + 1) ? ST_PENDING : ST_FINISHED;
+    for (int k = threadIdx.x; k < nv; k += blockDim.x) x += status[k] == want;
+  }
   for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
-  if ((threadIdx.x & 31) == 0) sh[c][threadIdx.x >> 5] = x;
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = x;
   __syncthreads();
   if (threadIdx.x == 0) {
     long long s = 0;
-    for (int w = 0; w < (int)(blockDim.x / 32); ++w) s += sh[c][w];
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) s += sh[w];
     out[c] = s;
   }
 }
@@ -492,7 +612,7 @@ __global__ void k_fill_u64(unsigned long long *p, unsigned long long v, int64_t 
 }
 
 // ---- launchers ---------------------------------------------------------------
-int step_smem_bytes() { return kSmemVeh * 7 * 4; }
+int step_smem_bytes() { return kSmemVeh * (7 * 4 + 6 * 4 + 1); }
 
 void launch_step(const StepArgs &a, void *stream, int smem_bytes) {
   static bool attr = false;
@@ -515,8 +635,10 @@ void launch_apply_requests(int32_t *request, uint8_t *policy, const int32_t *jun
 }
 
 void launch_reduce_acc(const long long *tacc, int n_tiles, const int32_t *cnt,
-                       const int32_t *icnt, long long *out, void *stream) {
-  k_reduce_acc<<<kNAcc + 1, 256, 0, (cudaStream_t)stream>>>(tacc, n_tiles, cnt, icnt, out);
+                       const int32_t *icnt, const uint8_t *status, int nv, long long *out,
+                       void *stream) {
+  k_reduce_acc<<<kNAcc + 3, 256, 0, (cudaStream_t)stream>>>(tacc, n_tiles, cnt, icnt, status, nv,
+                                                            out);
 }
 
 void launch_lane_stats(const StepArgs &a, int32_t *lane_count, int32_t *lane_wait, float zone,
@@ -530,5 +652,19 @@ void launch_fill_u64(unsigned long long *p, unsigned long long v, int64_t n, voi
 }
 
 void launch_set_i32(int32_t *, const int32_t *, const int32_t *, int, void *) {}
+
+}  // namespace sim
+
+extern "C" int sim_debug_guard_stats(unsigned long long *out) {
+#ifdef GUARD_STATS
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(out, sim::g_guard_stats, 32 * 8) == cudaSuccess ? 32 : -1;
+#else
+  (void)out;
+  return 0;
+#endif
+}
+
+namespace sim {
 
 }  // namespace sim

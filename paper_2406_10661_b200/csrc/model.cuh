@@ -37,7 +37,7 @@ constexpr float kEpsAcc = 2e-4f;    // m/s^2, accelerations / utilities
 constexpr float kEpsP = 2e-4f;      // draw vs p_LC
 constexpr float kEpsV = 2e-5f;      // relative, speed vs v_wait
 
-struct Guard { bool hit; };
+struct Guard { bool hit; unsigned why; };   // why: guard reason bits (stats builds)
 
 template <typename R> struct PV { R a_max, a_comf, T, s0, vmax, len, inv2; };
 __device__ __forceinline__ PV<double> pvals(const Prof &p, double) {
@@ -60,7 +60,7 @@ __device__ __forceinline__ R idm(R v, R v0, bool lead, R gap, R dv, const PV<R> 
   if (!lead) {
     a = M::mul(p.a_max, fr);
   } else {
-    if (GUARD && gap_scale > (R)0 && fabsf((float)gap) <= kEpsPos * (float)gap_scale) g.hit = true;
+    if (GUARD && gap_scale > (R)0 && fabsf((float)gap) <= kEpsPos * (float)gap_scale) g.hit = true, g.why |= (1u << 0);
     if (gap <= (R)0) {
       a = -b_hard;
     } else {
@@ -74,9 +74,14 @@ __device__ __forceinline__ R idm(R v, R v0, bool lead, R gap, R dv, const PV<R> 
   return (a < -b_hard) ? -b_hard : a;
 }
 
+struct SuccEnt { int j, troad, b, pad; int4 outr; };   // usable successor of a tile road lane (b: exit lane)
+
 // Tile-local lane metadata staged in shared memory.
 struct TileSh {
   int nl, nroad, tile, base, ibase, cap, icap;
+  int tab_ok;                        // successor table valid for this tile
+  uint8_t sn[kMaxRoadLanes];
+  SuccEnt se[kMaxRoadLanes][kMaxSucc];
   int glob[kMaxTileLanes];
   float len[kMaxTileLanes], vmax[kMaxTileLanes];
   int seg_start[kMaxTileLanes], seg_end[kMaxTileLanes];
@@ -106,14 +111,24 @@ __device__ __forceinline__ int route_at(const StepArgs &A, int vid, int c, int n
   return (idx >= 0 && idx < len) ? __ldg(A.route + off + idx) : -1;
 }
 
-// cand(b, R) != empty
+__device__ __forceinline__ bool in4(const int4 &o, int R) {
+  return o.x == R || o.y == R || o.z == R || o.w == R;
+}
+
+// cand(b, R) != empty, global lane b
 __device__ __forceinline__ bool has_outroad(const StepArgs &A, int b, int R) {
+  const int4 o = __ldg(A.outroads + b);
+  if (o.w != -2) return in4(o, R);
   int e1 = __ldg(A.succ_off + b + 1);
   for (int e = __ldg(A.succ_off + b); e < e1; ++e) {
     int j = __ldg(A.succ + e);
     if (A.usable[j] && __ldg(A.target_road + j) == R) return true;
   }
   return false;
+}
+__device__ __forceinline__ bool pref_ok(const StepArgs &A, const int4 &outr, int b, int R2) {
+  if (R2 < 0) return true;
+  return outr.w != -2 ? in4(outr, R2) : has_outroad(A, b, R2);
 }
 
 // next lane from road lane m toward road R1 with preference toward R2 (ledger L24)
@@ -125,10 +140,41 @@ __device__ __forceinline__ int next_from_road(const StepArgs &A, int m, int R1, 
     int j = __ldg(A.succ + e);
     if (!A.usable[j] || __ldg(A.target_road + j) != R1) continue;
     if (best_any < 0 || j < best_any) best_any = j;
-    bool pref = (R2 < 0) || has_outroad(A, __ldg(A.exit_lane + j), R2);
-    if (pref && (best_pref < 0 || j < best_pref)) best_pref = j;
+    const int b = __ldg(A.exit_lane + j);
+    if (pref_ok(A, __ldg(A.outroads + b), b, R2) && (best_pref < 0 || j < best_pref)) best_pref = j;
   }
   return best_pref >= 0 ? best_pref : best_any;
+}
+// the same two predicates for a road lane of this tile, from the shared-memory
+// successor table (built per step; usable successors only)
+__device__ __forceinline__ bool has_outroad_t(const StepArgs &A, const TileSh &T, int a, int R) {
+  if (!T.tab_ok) return has_outroad(A, T.glob[a], R);
+  for (int k = 0; k < T.sn[a]; ++k)
+    if (T.se[a][k].troad == R) return true;
+  return false;
+}
+__device__ __forceinline__ int next_from_road_t(const StepArgs &A, const TileSh &T, int l, int R1,
+                                                int R2) {
+  if (!T.tab_ok) return next_from_road(A, T.glob[l], R1, R2);
+  if (R1 < 0) return kLaneDest;
+  int best_any = kLaneBlocked, best_pref = kLaneBlocked;
+  for (int k = 0; k < T.sn[l]; ++k) {
+    const SuccEnt &e = T.se[l][k];
+    if (e.troad != R1) continue;
+    if (best_any < 0 || e.j < best_any) best_any = e.j;
+    if (pref_ok(A, e.outr, e.b, R2) && (best_pref < 0 || e.j < best_pref))
+      best_pref = e.j;
+  }
+  return best_pref >= 0 ? best_pref : best_any;
+}
+// any road lane (global id g)
+__device__ __forceinline__ int next_from_road_any(const StepArgs &A, const TileSh &T, int g,
+                                                  int R1, int R2) {
+  if (__ldg(A.lane_tile + g) == T.tile) {
+    const int l = A.lane_local[g];
+    if (l < T.nroad) return next_from_road_t(A, T, l, R1, R2);
+  }
+  return next_from_road(A, g, R1, R2);
 }
 
 struct First { bool found; float s, v, len; int vid; };
@@ -181,7 +227,7 @@ __device__ LEv<R> eval_lane(const StepArgs &A, const TileSh &T, const View &C, i
   LEv<R> e;
   const int lg = T.glob[l];
   const bool road = T.isroad[l];
-  e.next1 = road ? (me.nxt < 0 ? kLaneDest : next_from_road(A, lg, me.nxt, me.nxt2))
+  e.next1 = road ? (me.nxt < 0 ? kLaneDest : next_from_road_t(A, T, l, me.nxt, me.nxt2))
                  : __ldg(A.exit_lane + lg);
   const R vmax_l = (R)T.vmax[l];
   const R v0 = (p.vmax < vmax_l) ? p.vmax : vmax_l;
@@ -200,7 +246,7 @@ __device__ LEv<R> eval_lane(const StepArgs &A, const TileSh &T, const View &C, i
     e.hops = 0;
     e.gap = M::sub(M::sub(sf, s), lf);
     e.vlead = (R)C.v[lead_idx];
-    gscale = sf + s + lf;
+    gscale = fabs(sf - s) + lf;
   } else {                                               // P:168-169 substitution
     R d = M::sub(L, s);
     int m = e.next1, rel = 0;
@@ -224,7 +270,7 @@ __device__ LEv<R> eval_lane(const StepArgs &A, const TileSh &T, const View &C, i
       } else {
         int R1 = route_at(A, me.vid, me.cur, me.nxt, me.nxt2, me.cur + rel + 1);
         int R2 = route_at(A, me.vid, me.cur, me.nxt, me.nxt2, me.cur + rel + 2);
-        m = next_from_road(A, m, R1, R2);
+        m = next_from_road_any(A, T, m, R1, R2);
       }
     }
   }
@@ -246,7 +292,7 @@ __device__ LEv<R> eval_lane(const StepArgs &A, const TileSh &T, const View &C, i
   e.vlim = (R)0;
   if (GUARD && e.phantom && e.has_leader &&
       fabsf((float)(L - lim_lead)) <= kEpsPos * (float)(L + fabs(lim_lead)))
-    g.hit = true;
+    g.hit = true, g.why |= (1u << 1);
   if (e.phantom && (!e.has_leader || L <= lim_lead)) {
     e.has_lim = true;
     e.lim = L;
@@ -313,7 +359,7 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
     if (!inG) {                                          // ledger L18, L37
       bool left_ok = false, right_ok = false;
       for (int a = 0; a < T.nroad; ++a) {
-        if (!T.usable[a] || !has_outroad(A, T.glob[a], me.nxt)) continue;
+        if (!T.usable[a] || !has_outroad_t(A, T, a, me.nxt)) continue;
         if (a < l) left_ok = true;
         if (a > l) right_ok = true;
       }
@@ -322,9 +368,10 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
     const R rem = M::sub(L, s);
     const R need = M::add(p.s0, M::mul(v, p.T));
     const bool l19 = rem < need;                         // ledger L19
-    if (GUARD && inG && fabsf((float)(rem - need)) <= kEpsPos * (float)(L + need)) g.hit = true;
+    if (GUARD && inG && v != (R)0 && fabsf((float)(rem - need)) <= kEpsPos * (float)(fabs(rem) + need)) g.hit = true, g.why |= (1u << 2);
     int sl[2] = {T.left[l], T.right[l]};
     int front[2] = {-1, -1}, back[2] = {-1, -1};
+#pragma unroll
     for (int sd = 0; sd < 2; ++sd) {
       if (sl[sd] < 0) continue;
       int a = T.seg_start[sl[sd]], b = T.seg_end[sl[sd]];
@@ -342,12 +389,12 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
         const R so = (R)C.s[of], vo = (R)C.v[of];
         const R v0o = (po.vmax < (R)T.vmax[l]) ? po.vmax : (R)T.vmax[l];
         a_of = idm<R, GUARD>(vo, v0o, true, M::sub(M::sub(s, so), p.len), M::sub(vo, v), po,
-                             b_hard, s + so + p.len, g);
+                             b_hard, fabs(s - so) + p.len, g);
         if (lead >= 0) {
           const R sl_ = (R)C.s[lead];
           const R ll_ = (R)A.prof[m_prof(C.meta[lead])].len;
           a_of_new = idm<R, GUARD>(vo, v0o, true, M::sub(M::sub(sl_, so), ll_),
-                                   M::sub(vo, (R)C.v[lead]), po, b_hard, sl_ + so + ll_, g);
+                                   M::sub(vo, (R)C.v[lead]), po, b_hard, fabs(sl_ - so) + ll_, g);
         } else {
           a_of_new = idm<R, GUARD>(vo, v0o, false, (R)0, (R)0, po, b_hard, (R)0, g);
         }
@@ -355,11 +402,12 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
       bool adm[2] = {false, false};
       R u[2] = {(R)0, (R)0};
       LEv<R> ev[2];
+#pragma unroll
       for (int sd = 0; sd < 2; ++sd) {
         const int ls = sl[sd];
         const int sgn = sd == 0 ? -1 : 1;
         if (ls < 0 || !T.usable[ls]) continue;
-        if (inG && !(dest || has_outroad(A, T.glob[ls], me.nxt))) continue;
+        if (inG && !(dest || has_outroad_t(A, T, ls, me.nxt))) continue;
         if (!inG && sgn != mand) continue;
         ev[sd] = eval_lane<R, GUARD>(A, T, C, ls, front[sd], s, v, p, me, g);
         R a_nf = (R)0, a_nf_new = (R)0;
@@ -374,19 +422,19 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
             const R sf = (R)C.s[fi];
             const R lf = (R)A.prof[m_prof(C.meta[fi])].len;
             a_nf = idm<R, GUARD>(vb, v0b, true, M::sub(M::sub(sf, sb), lf),
-                                 M::sub(vb, (R)C.v[fi]), pb, b_hard, sf + sb + lf, g);
+                                 M::sub(vb, (R)C.v[fi]), pb, b_hard, fabs(sf - sb) + lf, g);
           } else {
             a_nf = idm<R, GUARD>(vb, v0b, false, (R)0, (R)0, pb, b_hard, (R)0, g);
           }
           const R gb = M::sub(M::sub(s, sb), p.len);
-          a_nf_new = idm<R, GUARD>(vb, v0b, true, gb, M::sub(vb, v), pb, b_hard, s + sb + p.len, g);
-          if (GUARD && fabsf((float)(a_nf_new + (R)A.b_safe)) <= kEpsAcc) g.hit = true;
+          a_nf_new = idm<R, GUARD>(vb, v0b, true, gb, M::sub(vb, v), pb, b_hard, fabs(s - sb) + p.len, g);
+          if (GUARD && fabsf((float)(a_nf_new + (R)A.b_safe)) <= kEpsAcc) g.hit = true, g.why |= (1u << 3);
           if (!(a_nf_new >= -(R)A.b_safe)) ok = false;  // L17 (1)
           if (!(gb >= (R)0)) ok = false;                 // L17 (2)
         } else {
           const R mrg = M::sub(s, p.len);
           if (GUARD && fabs((double)mrg - A.start_margin) <= (double)kEpsPos * ((double)s + A.start_margin))
-            g.hit = true;
+            g.hit = true, g.why |= (1u << 4);
           if (!(mrg >= (R)A.start_margin)) ok = false;  // L17 (3) lane-start rule
         }
         if (front[sd] >= 0) {
@@ -394,7 +442,7 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
           const R sf = (R)C.s[fi];
           const R lf = (R)A.prof[m_prof(C.meta[fi])].len;
           const R gf = M::sub(M::sub(sf, s), lf);
-          if (GUARD && fabsf((float)gf) <= kEpsPos * (float)(sf + s + lf)) g.hit = true;
+          if (GUARD && fabsf((float)gf) <= kEpsPos * (float)(fabs(sf - s) + lf)) g.hit = true, g.why |= (1u << 5);
           if (!(gf >= (R)0)) ok = false;                 // L17 (2)
         }
         // MOBIL utility (tilde = after the change, ledger L13)
@@ -425,10 +473,10 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
           }
           const uint64_t mant = ((uint64_t)(c0 >> 5) << 26) + (uint64_t)(c1 >> 6);
           const double r = (double)mant * (1.0 / 9007199254740992.0);
-          if (GUARD && fabs(r - pl) <= (double)kEpsP) g.hit = true;
+          if (GUARD && fabs(r - pl) <= (double)kEpsP) g.hit = true, g.why |= (1u << 6);
           if (r < pl) {                                  // P:196, ledger L15
             if (adm[0] && adm[1]) {
-              if (GUARD && fabsf((float)(u[0] - u[1])) <= kEpsAcc) g.hit = true;
+              if (GUARD && fabsf((float)(u[0] - u[1])) <= kEpsAcc) g.hit = true, g.why |= (1u << 7);
               choice = (u[0] >= u[1]) ? 0 : 1;
             } else {
               choice = adm[0] ? 0 : 1;
@@ -440,9 +488,9 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
         if (adm[sd]) choice = sd;                        // ledger L18
       }
       if (choice >= 0) {
-        use = ev[choice];
+        use = choice == 0 ? ev[0] : ev[1];
         lc = choice == 0 ? -1 : 1;
-        new_l = sl[choice];
+        new_l = choice == 0 ? sl[0] : sl[1];
       }
     }
   }
@@ -471,11 +519,11 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
     } else {
       bind = adv > use.limrel;
       if (GUARD && !adv_zero && fabsf((float)(adv - use.limrel)) <= kEpsPos * (float)(fabs(adv) + fabs(use.limrel) + (R)1e-3))
-        g.hit = true;
+        g.hit = true, g.why |= (1u << 8);
     }
     if (bind) {
       if (GUARD && fabsf((float)use.limrel) <= kEpsPos * (float)(fabs(s) + fabs(use.lim)))
-        g.hit = true;
+        g.hit = true, g.why |= (1u << 9);
       if (M::fp64 ? (use.lim < s) : (use.limrel < (R)0)) { s1 = s; adv = (R)0; v1 = (R)0; }
       else { s1 = use.lim; adv = use.limrel; v1 = (use.vlim < v1) ? use.vlim : v1; }
     }
@@ -493,14 +541,14 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
       const R rem = M::sub(es, pb);
       if (GUARD && !(adv_zero && hand == 0) &&
           fabsf((float)(pa - rem)) <= kEpsPos * (float)(fabs(pa) + fabs(rem) + (R)1e-3))
-        g.hit = true;
+        g.hit = true, g.why |= (1u << 10);
       if (pa >= rem) { fin = true; break; }
     }
     const R Lc = (R)__ldg(A.lane_len + curg);
     const R rem = M::sub(Lc, pb);
     if (GUARD && n >= 0 && !(adv_zero && hand == 0) &&
         fabsf((float)(pa - rem)) <= kEpsPos * (float)(fabs(pa) + fabs(rem) + (R)1e-3))
-      g.hit = true;
+      g.hit = true, g.why |= (1u << 11);
     if (pa > rem && n >= 0) {
       pb = M::sub(pb, Lc);
       curg = n;
@@ -510,7 +558,7 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
       if (nroad) {
         int R1 = route_at(A, me.vid, me.cur, me.nxt, me.nxt2, ri + 1);
         int R2 = route_at(A, me.vid, me.cur, me.nxt, me.nxt2, ri + 2);
-        n = next_from_road(A, curg, R1, R2);
+        n = next_from_road_any(A, T, curg, R1, R2);
       } else {
         n = __ldg(A.exit_lane + curg);
       }
@@ -520,7 +568,7 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
   }
   s1 = M::fp64 ? pb : (hand == 0 ? s1 : M::add(pb, pa));
   const R vw = (R)A.v_wait;
-  if (GUARD && fabsf((float)(v1 - vw)) <= kEpsV * (float)(fabs(v) + fabs(a) + (R)1)) g.hit = true;
+  if (GUARD && fabsf((float)(v1 - vw)) <= kEpsV * (float)(fabs(v) + fabs(a) + (R)1)) g.hit = true, g.why |= (1u << 12);
   o.wait1 = C.wait[i] + ((v1 < vw) ? 1 : 0);             // ledger L28
   o.s1 = (float)s1;
   o.v1 = (float)v1;

@@ -74,6 +74,7 @@ struct sim_s {
   // state
   int t = 0;
   std::vector<uint8_t> dir, usable;
+  std::vector<int32_t> outroads;     // [4 * n_lanes]
   // device
   std::vector<void *> allocs;
   int64_t bytes = 0;
@@ -86,6 +87,8 @@ struct sim_s {
   float *pubv[2]{};
   int32_t *pend_off_d = nullptr, *pend_vid_d = nullptr, *pend_head_d = nullptr;
   uint8_t *usable_d = nullptr;
+  int32_t *outroads_d = nullptr;
+  uint8_t *stage_dir_d = nullptr;    // device staging for lane-direction setters
   long long *red_d = nullptr;
   int32_t *stage_d = nullptr;      // device staging for batch setters
   int stage_cap = 0;
@@ -93,6 +96,12 @@ struct sim_s {
   size_t pinned_cap = 0;
   cudaEvent_t stage_ev = nullptr;
   int smem = 0;
+  int32_t *lanestat_d = nullptr;
+  // device timing windows (sim_enable_timing / sim_read_timing)
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  int64_t n_launch = 0;
 };
 
 namespace {
@@ -149,6 +158,23 @@ void compute_usable(sim_s *h) {
       else if (h->turn[l] == 0) u = h->dir[a] == 0;
     }
     h->usable[l] = u;
+  }
+  // outroads: distinct roads reachable through usable successors (<= 4, else -2 marker)
+  h->outroads.assign(4 * (size_t)h->nl, -1);
+  for (int l = 0; l < h->nl; ++l) {
+    int k = 0;
+    int32_t *o = &h->outroads[4 * (size_t)l];
+    for (int e = h->succ_off[l]; e < h->succ_off[l + 1]; ++e) {
+      int j = h->succ[e];
+      if (!h->usable[j]) continue;
+      int r = h->target_road[j];
+      bool seen = false;
+      for (int q = 0; q < k && q < 4; ++q) seen |= o[q] == r;
+      if (seen) continue;
+      if (k < 4) o[k] = r;
+      ++k;
+    }
+    if (k > 4) o[3] = -2;
   }
 }
 
@@ -425,6 +451,8 @@ sim_status upload_state(sim_s *h, const HostState &S) {
   h->dir = S.dir;
   compute_usable(h);
   CK(h, cudaMemcpyAsync(h->usable_d, h->usable.data(), h->nl, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(h->outroads_d, h->outroads.data(), h->outroads.size() * 4,
+                        cudaMemcpyHostToDevice, h->stream));
   // slabs
   std::vector<std::vector<int>> per_tile(nt);
   for (int k = 0; k < nv; ++k)
@@ -535,6 +563,8 @@ sim_status alloc_all(sim_s *h) {
   UP(i32, h->target_road); A.target_road = i32;
   UP(i32, h->exit_lane); A.exit_lane = i32;
   AL(h->usable_d, nl); A.usable = h->usable_d;
+  AL(h->stage_dir_d, 17 * (size_t)nl);
+  AL(h->outroads_d, 4 * (size_t)nl); A.outroads = reinterpret_cast<const int4 *>(h->outroads_d);
   uint8_t *sig; AL(sig, nl);
   CK(h, cudaMemset(sig, 0, nl));
   A.lane_sig = sig;
@@ -562,6 +592,8 @@ sim_status alloc_all(sim_s *h) {
   AL(sc_.s, sc); AL(sc_.v, sc); AL(sc_.vid, sc); AL(sc_.nxt, sc); AL(sc_.nxt2, sc);
   AL(sc_.meta, sc); AL(sc_.wait, sc);
   AL(A.bsort_scratch, h->sum_icap);
+  AL(A.rs_s1, sc); AL(A.rs_v1, sc); AL(A.rs_lane, sc); AL(A.rs_wait, sc); AL(A.rs_cur, sc);
+  AL(A.rs_glist, sc); AL(A.rs_flags, sc);
   for (int b = 0; b < 3; ++b) AL(h->summ[b], nl);
   UP(i32, h->route_off); A.route_off = i32;
   UP(i32, h->route); A.route = i32;
@@ -575,7 +607,8 @@ sim_status alloc_all(sim_s *h) {
   Prof *pr; UP(pr, h->profs); A.prof = pr;
   AL(A.tacc, (size_t)nt * kNAcc);
   CK(h, cudaMemset(A.tacc, 0, (size_t)nt * kNAcc * 8));
-  AL(h->red_d, kNAcc + 1);
+  AL(h->red_d, kNAcc + 3);
+  AL(h->lanestat_d, 2 * (size_t)nl);
   if (h->P.record_decisions) {
     AL(A.r_leader, nv); AL(A.r_of, nv); AL(A.r_side, 4 * (size_t)nv);
     AL(A.r_hops, nv); AL(A.r_phantom, nv); AL(A.r_lc, nv); AL(A.r_hand, nv);
@@ -645,9 +678,10 @@ sim_status device_check(sim_s *h) {
 
 sim_status read_counters(sim_s *h, std::vector<long long> &out) {
   StepArgs a = step_args(h, h->t);
-  launch_reduce_acc(h->A.tacc, h->nt, a.cnt_in, a.icnt_in, h->red_d, h->stream);
-  out.assign(kNAcc + 1, 0);
-  CK(h, cudaMemcpyAsync(out.data(), h->red_d, (kNAcc + 1) * 8, cudaMemcpyDeviceToHost, h->stream));
+  launch_reduce_acc(h->A.tacc, h->nt, a.cnt_in, a.icnt_in, h->A.status, h->nv, h->red_d, h->stream);
+  h->n_launch += 1;
+  out.assign(kNAcc + 3, 0);
+  CK(h, cudaMemcpyAsync(out.data(), h->red_d, (kNAcc + 3) * 8, cudaMemcpyDeviceToHost, h->stream));
   sim_status st = device_check(h);
   if (st) return st;
   if (out[ACC_OVERFLOW] > 0) {
@@ -667,6 +701,7 @@ static void destroy_impl(sim_s *h) {
   if (h->stage_d) cudaFree(h->stage_d);
   if (h->pinned) cudaFreeHost(h->pinned);
   if (h->stage_ev) cudaEventDestroy(h->stage_ev);
+  for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
@@ -733,8 +768,22 @@ sim_status sim_step(sim_handle h, int32_t n) {
       CK(h, cudaMemsetAsync(h->A.r_leader, 0xff, h->nv * 4, h->stream));
       CK(h, cudaMemsetAsync(h->A.r_lc, 0, h->nv, h->stream));
     }
+    cudaEvent_t e[3] = {nullptr, nullptr, nullptr};
+    if (h->timing) {
+      while (h->ev_pool.size() < h->ev_used + 3) {
+        cudaEvent_t ev;
+        CK(h, cudaEventCreate(&ev));
+        h->ev_pool.push_back(ev);
+      }
+      for (int q = 0; q < 3; ++q) e[q] = h->ev_pool[h->ev_used + q];
+      h->ev_used += 3;
+      CK(h, cudaEventRecord(e[0], h->stream));
+    }
     launch_signal(h->SG, h->stream);
+    if (h->timing) CK(h, cudaEventRecord(e[1], h->stream));
     launch_step(a, h->stream, h->smem);
+    if (h->timing) CK(h, cudaEventRecord(e[2], h->stream));
+    h->n_launch += (h->nj > 0 ? 1 : 0) + (h->nt > 0 ? 1 : 0);
     h->t += 1;
   }
   cudaError_t e = cudaGetLastError();
@@ -800,7 +849,17 @@ sim_status sim_set_lane_direction_batch(sim_handle h, int32_t m, const int32_t *
   }
   if (m == 0) return SIM_OK;
   compute_usable(h);
-  return push_staging(h, h->usable.data(), h->nl, h->usable_d);
+  // one staging buffer: usable bytes followed by the outroads table
+  std::vector<uint8_t> buf((size_t)h->nl + h->outroads.size() * 4);
+  std::memcpy(buf.data(), h->outroads.data(), h->outroads.size() * 4);
+  std::memcpy(buf.data() + h->outroads.size() * 4, h->usable.data(), h->nl);
+  st = push_staging(h, buf.data(), buf.size(), h->stage_dir_d);
+  if (st) return st;
+  CK(h, cudaMemcpyAsync(h->outroads_d, h->stage_dir_d, h->outroads.size() * 4,
+                        cudaMemcpyDeviceToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(h->usable_d, h->stage_dir_d + h->outroads.size() * 4, h->nl,
+                        cudaMemcpyDeviceToDevice, h->stream));
+  return SIM_OK;
 }
 
 sim_status sim_set_lane_direction(sim_handle h, int32_t lane, int32_t dir) {
@@ -923,13 +982,8 @@ sim_status sim_read_metrics(sim_handle h, sim_metrics *m) {
   m->t = h->t;
   m->n_driving = c[kNAcc];
   m->n_finished = c[ACC_FINISHED];
-  // pending = trips never inserted: total - on-network-at-t0 - inserted ... computed from status
-  std::vector<uint8_t> status(h->nv);
-  if (h->nv) CK(h, cudaMemcpy(status.data(), h->A.status, h->nv, cudaMemcpyDeviceToHost));
-  int64_t pend = 0, fin = 0;
-  for (uint8_t s : status) { pend += s == ST_PENDING; fin += s == ST_FINISHED; }
-  m->n_pending = pend;
-  m->n_finished = fin;
+  m->n_pending = c[kNAcc + 1];
+  m->n_finished = c[kNAcc + 2];
   m->vehicle_steps = c[ACC_VEH_STEPS];
   m->sum_travel_steps = c[ACC_SUM_TRAVEL];
   m->sum_wait_steps_finished = c[ACC_SUM_WAIT_FIN];
@@ -940,19 +994,48 @@ sim_status sim_read_metrics(sim_handle h, sim_metrics *m) {
   m->n_guard_hits = c[ACC_GUARD];
   m->att_finished = c[ACC_FINISHED] ? (double)c[ACC_SUM_TRAVEL] / (double)c[ACC_FINISHED] : 0.0;
   if (m->lane_count || m->lane_waiting_at_end) {
-    int32_t *d;
-    CK(h, cudaMalloc(&d, 2 * (size_t)h->nl * 4));
+    int32_t *d = h->lanestat_d;
     CK(h, cudaMemsetAsync(d, 0, 2 * (size_t)h->nl * 4, h->stream));
     StepArgs a = step_args(h, h->t);
     launch_lane_stats(a, d, d + h->nl, h->P.queue_zone_m, h->stream);
-    std::vector<int32_t> buf(2 * (size_t)h->nl);
-    CK(h, cudaMemcpyAsync(buf.data(), d, buf.size() * 4, cudaMemcpyDeviceToHost, h->stream));
+    h->n_launch += 1;
+    if (m->lane_count)
+      CK(h, cudaMemcpyAsync(m->lane_count, d, h->nl * 4, cudaMemcpyDeviceToHost, h->stream));
+    if (m->lane_waiting_at_end)
+      CK(h, cudaMemcpyAsync(m->lane_waiting_at_end, d + h->nl, h->nl * 4, cudaMemcpyDeviceToHost, h->stream));
     st = device_check(h);
-    cudaFree(d);
     if (st) return st;
-    if (m->lane_count) std::memcpy(m->lane_count, buf.data(), h->nl * 4);
-    if (m->lane_waiting_at_end) std::memcpy(m->lane_waiting_at_end, buf.data() + h->nl, h->nl * 4);
   }
+  return SIM_OK;
+}
+
+sim_status sim_enable_timing(sim_handle h, int32_t enable) {
+  sim_status st = check(h);
+  if (st) return st;
+  st = device_check(h);
+  if (st) return st;
+  h->timing = enable != 0;
+  h->ev_used = 0;
+  h->n_launch = 0;
+  return SIM_OK;
+}
+
+sim_status sim_read_timing(sim_handle h, double *step_ms, double *signal_ms, int64_t *n_launches) {
+  sim_status st = check(h);
+  if (st) return st;
+  st = device_check(h);
+  if (st) return st;
+  double ks = 0, sg = 0;
+  for (size_t i = 0; i + 3 <= h->ev_used; i += 3) {
+    float a = 0, b = 0;
+    CK(h, cudaEventElapsedTime(&a, h->ev_pool[i], h->ev_pool[i + 1]));
+    CK(h, cudaEventElapsedTime(&b, h->ev_pool[i + 1], h->ev_pool[i + 2]));
+    sg += a;
+    ks += b;
+  }
+  if (step_ms) *step_ms = ks;
+  if (signal_ms) *signal_ms = sg;
+  if (n_launches) *n_launches = h->n_launch;
   return SIM_OK;
 }
 

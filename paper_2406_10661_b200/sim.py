@@ -81,8 +81,8 @@ class sim_metrics(C.Structure):
 ABI_FUNCTIONS = ["sim_create", "sim_step", "sim_sync", "sim_set_signal_phase",
                  "sim_set_signal_phase_batch", "sim_set_lane_direction",
                  "sim_set_lane_direction_batch", "sim_query_sizes", "sim_read_state",
-                 "sim_read_decisions", "sim_read_metrics", "sim_load_state", "sim_destroy",
-                 "sim_last_error"]
+                 "sim_read_decisions", "sim_read_metrics", "sim_load_state",
+                 "sim_enable_timing", "sim_read_timing", "sim_destroy", "sim_last_error"]
 
 _lib = None
 
@@ -104,6 +104,7 @@ def load_library(path=LIB):
         "sim_set_lane_direction": [h, i32, i32], "sim_set_lane_direction_batch": [h, i32, P, P],
         "sim_query_sizes": [h, P], "sim_read_state": [h, P], "sim_read_decisions": [h, P],
         "sim_read_metrics": [h, P], "sim_load_state": [h, P], "sim_destroy": [h],
+        "sim_enable_timing": [h, i32], "sim_read_timing": [h, P, P, P],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -250,6 +251,15 @@ class Sim:
         if bufs is not None:
             out["lane_count"], out["lane_waiting_at_end"] = bufs
         return out
+
+    def enable_timing(self, on=True):
+        self._chk(self.lib.sim_enable_timing(self.h, int(on)))
+
+    def read_timing(self):
+        """(step-kernel ms, signal-kernel ms, kernel launches) of the timing window."""
+        a, b, n = C.c_double(), C.c_double(), C.c_int64()
+        self._chk(self.lib.sim_read_timing(self.h, C.byref(a), C.byref(b), C.byref(n)))
+        return a.value, b.value, n.value
 
     def destroy(self):
         if getattr(self, "h", None):

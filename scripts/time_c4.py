@@ -1,0 +1,41 @@
+"""Quick device timing of k_step on C4 for a given library build (dev tool)."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import synth
+import paper_2406_10661_b200.sim as S
+lib = sys.argv[1] if len(sys.argv) > 1 else S.LIB
+cache = "/tmp/c4.npz"
+if os.path.exists(cache):
+    scen = synth.load_scenario(cache)
+else:
+    scen = synth.city(); synth.save_scenario(scen, cache)
+S.load_library(lib)
+st = torch.cuda.Stream()
+sim = S.Sim.from_scenario(scen, stream=st.cuda_stream)
+flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+sim.step(10); sim.sync()
+sim.enable_timing(True)
+n = 40
+m0 = sim.read_metrics()
+with torch.cuda.stream(st):
+    for k in range(n):
+        flush.fill_(k & 255)
+        sim.step(1)
+torch.cuda.synchronize()
+ks, sg, nl = sim.read_timing()
+m1 = sim.read_metrics()
+vs = m1["vehicle_steps"] - m0["vehicle_steps"]
+print(f"{os.path.basename(lib)}: k_step {ks/n*1e3:.1f} us  k_signal {sg/n*1e3:.1f} us  "
+      f"veh-steps/s(kstep) {vs/(ks/1e3):.3e}  guard/step {(m1['n_guard_hits']-m0['n_guard_hits'])/n:.0f}", flush=True)
+import ctypes
+L = S.load_library(lib)
+buf = (ctypes.c_ulonglong * 32)()
+try:
+    n = L.sim_debug_guard_stats(buf)
+    if n > 0:
+        names = ["idm_gap", "lim_select", "l19", "b_safe", "lane_start", "front_gap", "r_vs_p",
+                 "uL_vs_uR", "clamp_bind", "clamp_overlap", "arrival", "handoff", "wait"]
+        print({names[i]: buf[i] for i in range(len(names))})
+except AttributeError:
+    pass

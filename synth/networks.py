@@ -62,6 +62,25 @@ class Scenario:
         return int(self.trips["depart_step"].shape[0])
 
 
+def save_scenario(scen, path):
+    """Cache a scenario as .npz (graph / trips / profiles / params)."""
+    d = {f"g_{k}": v for k, v in scen.graph.items()}
+    d.update({f"t_{k}": v for k, v in scen.trips.items()})
+    d["profiles"] = scen.profiles
+    d["params_json"] = np.frombuffer(__import__("json").dumps(scen.params).encode(), np.uint8)
+    d["name"] = np.frombuffer(scen.name.encode(), np.uint8)
+    np.savez(path, **d)
+
+
+def load_scenario(path):
+    import json
+    z = np.load(path)
+    g = {k[2:]: z[k] for k in z.files if k.startswith("g_")}
+    t = {k[2:]: z[k] for k in z.files if k.startswith("t_")}
+    return Scenario(bytes(z["name"]).decode(), g, t, z["profiles"],
+                    json.loads(bytes(z["params_json"]).decode()))
+
+
 class NetBuilder:
     """Incremental lane-graph builder producing the sim_graph CSR arrays."""
 
