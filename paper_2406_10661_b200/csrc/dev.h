@@ -19,11 +19,12 @@ namespace sim {
 
 constexpr int kMaxTileLanes = 64;    // lanes per tile (road lanes + outgoing junction lanes)
 constexpr int kThreads = 128;        // k_step block size
-constexpr int kSmemVeh = 448;        // snapshot slots held in shared memory (larger tiles use global scratch)
+constexpr int kSmemVeh = 320;        // snapshot slots held in shared memory (larger tiles use global scratch)
 constexpr int kSmemInbox = 96;       // inbox keys sorted in shared memory
 constexpr int kNAcc = 12;            // per-tile int64 accumulators
 constexpr int kMaxRoadLanes = 8;     // road lanes per tile cached in the successor table
 constexpr int kMaxSucc = 12;         // successors per road lane cached in the table
+constexpr int kSmemProf = 8;         // profiles staged in shared memory
 constexpr uint64_t kEmptyKey = ~0ull;
 
 enum Acc {
@@ -65,7 +66,7 @@ struct StepArgs {
   // model constants (fp32 inputs; fp64 copies are their exact promotions)
   float polite, b_hard, b_safe, v_wait;
   double start_margin;              // v_cap + 0.5 * a_cap (ledger L17)
-  int32_t lookahead, exact_mode, record;
+  int32_t lookahead, exact_mode, record, n_prof;
   // lanes (global id)
   const float *lane_len, *lane_vmax;
   const int32_t *lane_road;         // -1 junction lane

@@ -91,10 +91,14 @@ struct StepShared {
   unsigned long long bk_hi[kSmemInbox];
   int bk_vid[kSmemInbox];
   int bsort[kSmemInbox];
+  unsigned long long sk_hi[kSmemInbox];   // inbox keys in sorted order
+  int sk_vid[kSmemInbox];
+  Prof prof[kSmemProf];
+  long long acc[kNAcc];
 };
 
 #ifndef KSTEP_MINB
-#define KSTEP_MINB 4
+#define KSTEP_MINB 8
 #endif
 __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -116,7 +120,11 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
     T.icap = A.tile_icap[tile];
     S.nst_out = 0;
     S.nguard = 0;
+    T.P = A.n_prof <= kSmemProf ? S.prof : A.prof;
   }
+  if (tid < kNAcc) S.acc[tid] = 0;
+  if (A.n_prof <= kSmemProf)
+    for (int q = tid; q < A.n_prof; q += kThreads) S.prof[q] = A.prof[q];
   for (int l = tid; l < nl; l += kThreads) {
     int g = A.tile_lanes[l0 + l];
     T.glob[l] = g;
@@ -149,6 +157,7 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
           s.troad = A.target_road[j];
           s.b = A.exit_lane[j];
           s.outr = A.outroads[s.b];
+          s.stop = (A.lane_road[j] < 0 && A.lane_sig[j] != SIG_GREEN) ? 1 : 0;
         }
       T.sn[l] = (uint8_t)k;
       if (!ok) T.tab_ok = 0;
@@ -199,6 +208,8 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
         int vj = S.bk_vid[j], rank = 0;
         for (int q = 0; q < n_in; ++q) rank += key_less(S.bk_hi[q], S.bk_vid[q], h, vj);
         bsort[rank] = j;
+        S.sk_hi[rank] = h;
+        S.sk_vid[rank] = vj;
       }
     } else {
       for (int j = tid; j < n_in; j += kThreads) {
@@ -224,10 +235,17 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
     if (n_in > 0) {
       unsigned long long h = hikey(m_lane(meta), s);
       int lo = 0, hi = n_in;
-      while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        InboxRec o = inb[bsort[mid]];
-        if (key_less(hikey(m_lane(o.meta), o.s), o.vid, h, vid)) lo = mid + 1; else hi = mid;
+      if (n_in <= kSmemInbox) {
+        while (lo < hi) {
+          int mid = (lo + hi) >> 1;
+          if (key_less(S.sk_hi[mid], S.sk_vid[mid], h, vid)) lo = mid + 1; else hi = mid;
+        }
+      } else {
+        while (lo < hi) {
+          int mid = (lo + hi) >> 1;
+          InboxRec o = inb[bsort[mid]];
+          if (key_less(hikey(m_lane(o.meta), o.s), o.vid, h, vid)) lo = mid + 1; else hi = mid;
+        }
       }
       pos += lo;
     }
@@ -428,17 +446,17 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
     const int k = A.pend_vid[h];
     if (A.depart[k] > A.t || !T.usable[l]) continue;
     const double ss = (double)A.start_s[k];
-    const Prof &pk = A.prof[A.veh_prof[k]];
+    const Prof &pk = T.P[A.veh_prof[k]];
     const int a0 = T.seg_start[l], b0 = T.seg_end[l];
     const int fa = upper_bound_s(C, a0, b0, (float)ss);
     bool ok = true;
     if (fa < b0) {
-      const double sa = C.s[fa], la = A.prof[m_prof(C.meta[fa])].len_d;
+      const double sa = C.s[fa], la = T.P[m_prof(C.meta[fa])].len_d;
       if (!(__dadd_rn(__dadd_rn(sa, -ss), -la) >= pk.s0_d)) ok = false;
     }
     if (fa > a0) {
       const int b = fa - 1;
-      const Prof &pb = A.prof[m_prof(C.meta[b])];
+      const Prof &pb = T.P[m_prof(C.meta[b])];
       const double need = __dadd_rn(__dadd_rn((double)C.v[b], __dmul_rn(0.5, pb.a_max_d)), pk.s0_d);
       if (!(__dadd_rn(__dadd_rn(ss, -(double)C.s[b]), -pk.len_d) >= need)) ok = false;
     } else {
@@ -473,25 +491,18 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
     acc_ins += 1;
     acc_delay += (long long)(A.t + 1 - A.depart[k]);
   }
-  // block reduction of the counters (int64, exact, order independent)
-  __shared__ long long red[kNAcc][kThreads / 32];
-  long long vals[kNAcc] = {0, acc_fin, acc_travel, acc_waitfin, acc_delay, acc_lc, acc_hand,
-                           acc_ins, acc_guard, acc_ovf, 0, 0};
+  // block reduction of the counters (int64 shared atomics, exact, order independent)
+  const long long vals[kNAcc] = {0, acc_fin, acc_travel, acc_waitfin, acc_delay, acc_lc, acc_hand,
+                                 acc_ins, acc_guard, acc_ovf, 0, 0};
 #pragma unroll
-  for (int c = 1; c < kNAcc; ++c) {
-    long long x = vals[c];
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
-    if (lane_id == 0) red[c][warp] = x;
-  }
+  for (int c = 1; c < kNAcc; ++c)
+    if (vals[c]) atomicAdd(reinterpret_cast<unsigned long long *>(&S.acc[c]),
+                           (unsigned long long)vals[c]);
   __syncthreads();
   if (tid == 0) {
     long long *ta = A.tacc + (size_t)tile * kNAcc;
     ta[ACC_VEH_STEPS] += n;
-    for (int c = 1; c < kNAcc; ++c) {
-      long long x = 0;
-      for (int w = 0; w < kThreads / 32; ++w) x += red[c][w];
-      ta[c] += x;
-    }
+    for (int c = 1; c < kNAcc; ++c) ta[c] += S.acc[c];
     A.cnt_out[tile] = S.nst_out;
     A.icnt_in[tile] = 0;
   }
@@ -560,27 +571,33 @@ __global__ void k_apply_requests(int32_t *request, uint8_t *policy, const int32_
 
 __global__ void k_reduce_acc(const long long *tacc, int n_tiles, const int32_t *cnt,
                              const int32_t *icnt, const uint8_t *status, int nv, long long *out) {
-  // blocks 0..kNAcc-1: per-tile counters; kNAcc: driving (stayers + inbox);
-  // kNAcc+1 / +2: PENDING / FINISHED vehicles from the status array
-  __shared__ long long sh[8];
-  const int c = blockIdx.x;
-  long long x = 0;
-  if (c < kNAcc) {
-    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) x += tacc[(size_t)t * kNAcc + c];
-  } else if (c == kNAcc) {
-    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) x += (long long)(cnt[t] + icnt[t]);
-  } else {
-    const uint8_t want = (c == kNAcc + 1) ? ST_PENDING : ST_FINISHED;
-    for (int k = threadIdx.x; k < nv; k += blockDim.x) x += status[k] == want;
-  }
-  for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = x;
+  // out (zeroed by the caller): [0, kNAcc) per-tile counters, kNAcc: driving
+  // (stayers + inbox), kNAcc+1 / +2: PENDING / FINISHED vehicles from status
+  __shared__ unsigned long long sh[kNAcc + 3];
+  if (threadIdx.x < kNAcc + 3) sh[threadIdx.x] = 0;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    long long s = 0;
-    for (int w = 0; w < (int)(blockDim.x / 32); ++w) s += sh[w];
-    out[c] = s;
+  const int stride = gridDim.x * blockDim.x;
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+  long long loc[kNAcc + 3] = {0};
+  for (int t = t0; t < n_tiles; t += stride) {
+#pragma unroll
+    for (int c = 0; c < kNAcc; ++c) loc[c] += tacc[(size_t)t * kNAcc + c];
+    loc[kNAcc] += cnt[t] + icnt[t];
   }
+  for (int k = t0; k < nv; k += stride) {
+    const uint8_t s = status[k];
+    loc[kNAcc + 1] += s == ST_PENDING;
+    loc[kNAcc + 2] += s == ST_FINISHED;
+  }
+#pragma unroll
+  for (int c = 0; c < kNAcc + 3; ++c) {
+    long long x = loc[c];
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0 && x) atomicAdd(&sh[c], (unsigned long long)x);
+  }
+  __syncthreads();
+  if (threadIdx.x < kNAcc + 3 && sh[threadIdx.x])
+    atomicAdd(reinterpret_cast<unsigned long long *>(&out[threadIdx.x]), sh[threadIdx.x]);
 }
 
 __global__ void k_lane_stats(StepArgs A, int32_t *cnt, int32_t *wt, float zone) {
@@ -637,8 +654,8 @@ void launch_apply_requests(int32_t *request, uint8_t *policy, const int32_t *jun
 void launch_reduce_acc(const long long *tacc, int n_tiles, const int32_t *cnt,
                        const int32_t *icnt, const uint8_t *status, int nv, long long *out,
                        void *stream) {
-  k_reduce_acc<<<kNAcc + 3, 256, 0, (cudaStream_t)stream>>>(tacc, n_tiles, cnt, icnt, status, nv,
-                                                            out);
+  cudaMemsetAsync(out, 0, (kNAcc + 3) * sizeof(long long), (cudaStream_t)stream);
+  k_reduce_acc<<<296, 256, 0, (cudaStream_t)stream>>>(tacc, n_tiles, cnt, icnt, status, nv, out);
 }
 
 void launch_lane_stats(const StepArgs &a, int32_t *lane_count, int32_t *lane_wait, float zone,

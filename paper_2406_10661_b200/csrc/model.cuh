@@ -74,11 +74,13 @@ __device__ __forceinline__ R idm(R v, R v0, bool lead, R gap, R dv, const PV<R> 
   return (a < -b_hard) ? -b_hard : a;
 }
 
-struct SuccEnt { int j, troad, b, pad; int4 outr; };   // usable successor of a tile road lane (b: exit lane)
+struct SuccEnt { int j, troad, b, stop; int4 outr; };  // usable successor of a tile road lane
+                                                          // (b: exit lane; stop: junction lane not GREEN)
 
 // Tile-local lane metadata staged in shared memory.
 struct TileSh {
   int nl, nroad, tile, base, ibase, cap, icap;
+  const Prof *P;                     // profile table (shared-memory copy when small)
   int tab_ok;                        // successor table valid for this tile
   uint8_t sn[kMaxRoadLanes];
   SuccEnt se[kMaxRoadLanes][kMaxSucc];
@@ -153,19 +155,35 @@ __device__ __forceinline__ bool has_outroad_t(const StepArgs &A, const TileSh &T
     if (T.se[a][k].troad == R) return true;
   return false;
 }
-__device__ __forceinline__ int next_from_road_t(const StepArgs &A, const TileSh &T, int l, int R1,
-                                                int R2) {
-  if (!T.tab_ok) return next_from_road(A, T.glob[l], R1, R2);
-  if (R1 < 0) return kLaneDest;
-  int best_any = kLaneBlocked, best_pref = kLaneBlocked;
+struct Next { int j; bool stop; };  // next lane and "stop line applies" (junction lane not GREEN)
+__device__ __forceinline__ Next next_stop_g(const StepArgs &A, int j) {
+  Next n;
+  n.j = j;
+  n.stop = j >= 0 && __ldg(A.lane_road + j) < 0 && A.lane_sig[j] != SIG_GREEN;
+  return n;
+}
+__device__ __forceinline__ Next next1_t(const StepArgs &A, const TileSh &T, int l, int R1, int R2) {
+  if (!T.tab_ok) return next_stop_g(A, next_from_road(A, T.glob[l], R1, R2));
+  Next n;
+  n.stop = false;
+  if (R1 < 0) { n.j = kLaneDest; return n; }
+  int best_any = kLaneBlocked, best_pref = kLaneBlocked, st_any = 0, st_pref = 0;
   for (int k = 0; k < T.sn[l]; ++k) {
     const SuccEnt &e = T.se[l][k];
     if (e.troad != R1) continue;
-    if (best_any < 0 || e.j < best_any) best_any = e.j;
-    if (pref_ok(A, e.outr, e.b, R2) && (best_pref < 0 || e.j < best_pref))
+    if (best_any < 0 || e.j < best_any) { best_any = e.j; st_any = e.stop; }
+    if (pref_ok(A, e.outr, e.b, R2) && (best_pref < 0 || e.j < best_pref)) {
       best_pref = e.j;
+      st_pref = e.stop;
+    }
   }
-  return best_pref >= 0 ? best_pref : best_any;
+  n.j = best_pref >= 0 ? best_pref : best_any;
+  n.stop = (best_pref >= 0 ? st_pref : st_any) != 0;
+  return n;
+}
+__device__ __forceinline__ int next_from_road_t(const StepArgs &A, const TileSh &T, int l, int R1,
+                                                int R2) {
+  return next1_t(A, T, l, R1, R2).j;
 }
 // any road lane (global id g)
 __device__ __forceinline__ int next_from_road_any(const StepArgs &A, const TileSh &T, int g,
@@ -193,7 +211,7 @@ __device__ __forceinline__ First first_of(const StepArgs &A, const TileSh &T, co
       f.s = C.s[a];
       f.v = C.v[a];
       f.vid = C.vid[a];
-      f.len = A.prof[m_prof(C.meta[a])].len;
+      f.len = T.P[m_prof(C.meta[a])].len;
     }
   } else {
     unsigned long long key = A.summ_cur[m];
@@ -202,7 +220,7 @@ __device__ __forceinline__ First first_of(const StepArgs &A, const TileSh &T, co
       f.s = __uint_as_float((unsigned)(key >> 32));
       f.vid = (int)(unsigned)(key & 0xffffffffu);
       f.v = A.pubv_cur[f.vid];
-      f.len = A.prof[A.veh_prof[f.vid]].len;
+      f.len = T.P[A.veh_prof[f.vid]].len;
     }
   }
   return f;
@@ -227,8 +245,10 @@ __device__ LEv<R> eval_lane(const StepArgs &A, const TileSh &T, const View &C, i
   LEv<R> e;
   const int lg = T.glob[l];
   const bool road = T.isroad[l];
-  e.next1 = road ? (me.nxt < 0 ? kLaneDest : next_from_road_t(A, T, l, me.nxt, me.nxt2))
-                 : __ldg(A.exit_lane + lg);
+  Next nx;
+  if (road) nx = me.nxt < 0 ? Next{kLaneDest, false} : next1_t(A, T, l, me.nxt, me.nxt2);
+  else nx = Next{__ldg(A.exit_lane + lg), false};
+  e.next1 = nx.j;
   const R vmax_l = (R)T.vmax[l];
   const R v0 = (p.vmax < vmax_l) ? p.vmax : vmax_l;
   const R L = (R)T.len[l];
@@ -240,7 +260,7 @@ __device__ LEv<R> eval_lane(const StepArgs &A, const TileSh &T, const View &C, i
   R gscale = (R)0;
   if (lead_idx >= 0) {                                   // main pointer
     R sf = (R)C.s[lead_idx];
-    R lf = (R)A.prof[m_prof(C.meta[lead_idx])].len;
+    R lf = (R)T.P[m_prof(C.meta[lead_idx])].len;
     e.has_leader = true;
     e.leader = C.vid[lead_idx];
     e.hops = 0;
@@ -278,9 +298,7 @@ __device__ LEv<R> eval_lane(const StepArgs &A, const TileSh &T, const View &C, i
   R a_lead = idm<R, GUARD>(v, v0, e.has_leader, e.gap, M::sub(v, e.vlead), p, b_hard, gscale, g);
   e.a = a_lead;
   e.phantom = false;
-  if (road && e.next1 != kLaneDest &&
-      (e.next1 == kLaneBlocked ||
-       (__ldg(A.lane_road + e.next1) < 0 && A.lane_sig[e.next1] != SIG_GREEN))) {
+  if (road && e.next1 != kLaneDest && (e.next1 == kLaneBlocked || nx.stop)) {
     e.phantom = true;                                    // P:200 stationary vehicle at lane end
     R gp = M::sub(L, s);                                 // sign exact: no guard needed
     R a_ph = idm<R, GUARD>(v, v0, true, gp, M::sub(v, (R)0), p, b_hard, (R)0, g);
@@ -338,7 +356,7 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
   me.cur = m_cursor(meta);
   me.nxt = C.nxt[i];
   me.nxt2 = C.nxt2[i];
-  const PV<R> p = pvals(A.prof[pr], (R)0);
+  const PV<R> p = pvals(T.P[pr], (R)0);
   const R s = (R)C.s[i], v = (R)C.v[i];
   const R L = (R)T.len[l];
   const int lead = (i + 1 < T.seg_end[l]) ? i + 1 : -1;
@@ -385,14 +403,14 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
     if (consider) {
       R a_of = (R)0, a_of_new = (R)0;                    // old follower (L10)
       if (of >= 0) {
-        const PV<R> po = pvals(A.prof[m_prof(C.meta[of])], (R)0);
+        const PV<R> po = pvals(T.P[m_prof(C.meta[of])], (R)0);
         const R so = (R)C.s[of], vo = (R)C.v[of];
         const R v0o = (po.vmax < (R)T.vmax[l]) ? po.vmax : (R)T.vmax[l];
         a_of = idm<R, GUARD>(vo, v0o, true, M::sub(M::sub(s, so), p.len), M::sub(vo, v), po,
                              b_hard, fabs(s - so) + p.len, g);
         if (lead >= 0) {
           const R sl_ = (R)C.s[lead];
-          const R ll_ = (R)A.prof[m_prof(C.meta[lead])].len;
+          const R ll_ = (R)T.P[m_prof(C.meta[lead])].len;
           a_of_new = idm<R, GUARD>(vo, v0o, true, M::sub(M::sub(sl_, so), ll_),
                                    M::sub(vo, (R)C.v[lead]), po, b_hard, fabs(sl_ - so) + ll_, g);
         } else {
@@ -414,13 +432,13 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
         bool ok = true;
         if (back[sd] >= 0) {
           const int bi = back[sd];
-          const PV<R> pb = pvals(A.prof[m_prof(C.meta[bi])], (R)0);
+          const PV<R> pb = pvals(T.P[m_prof(C.meta[bi])], (R)0);
           const R sb = (R)C.s[bi], vb = (R)C.v[bi];
           const R v0b = (pb.vmax < (R)T.vmax[ls]) ? pb.vmax : (R)T.vmax[ls];
           if (front[sd] >= 0) {
             const int fi = front[sd];
             const R sf = (R)C.s[fi];
-            const R lf = (R)A.prof[m_prof(C.meta[fi])].len;
+            const R lf = (R)T.P[m_prof(C.meta[fi])].len;
             a_nf = idm<R, GUARD>(vb, v0b, true, M::sub(M::sub(sf, sb), lf),
                                  M::sub(vb, (R)C.v[fi]), pb, b_hard, fabs(sf - sb) + lf, g);
           } else {
@@ -440,7 +458,7 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
         if (front[sd] >= 0) {
           const int fi = front[sd];
           const R sf = (R)C.s[fi];
-          const R lf = (R)A.prof[m_prof(C.meta[fi])].len;
+          const R lf = (R)T.P[m_prof(C.meta[fi])].len;
           const R gf = M::sub(M::sub(sf, s), lf);
           if (GUARD && fabsf((float)gf) <= kEpsPos * (float)(fabs(sf - s) + lf)) g.hit = true, g.why |= (1u << 5);
           if (!(gf >= (R)0)) ok = false;                 // L17 (2)

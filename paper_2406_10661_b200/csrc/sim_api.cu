@@ -634,6 +634,7 @@ sim_status alloc_all(sim_s *h) {
   A.lookahead = h->P.lookahead_lanes;
   A.exact_mode = h->P.exact_mode;
   A.record = h->P.record_decisions;
+  A.n_prof = (int)h->profs.size();
   CK(h, cudaEventCreateWithFlags(&h->stage_ev, cudaEventDisableTiming));
   CK(h, cudaEventRecord(h->stage_ev, h->stream));
   return SIM_OK;
