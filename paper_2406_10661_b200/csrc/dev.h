@@ -17,13 +17,15 @@
 
 namespace sim {
 
-constexpr int kMaxTileLanes = 64;    // lanes per tile (road lanes + outgoing junction lanes)
-constexpr int kThreads = 128;        // k_step block size
-constexpr int kSmemVeh = 320;        // snapshot slots held in shared memory (larger tiles use global scratch)
-constexpr int kSmemInbox = 96;       // inbox keys sorted in shared memory
+constexpr int kMaxTileLanes = 32;    // lanes per tile (road lanes + outgoing junction lanes)
+constexpr int kThreads = 32;         // k_step block size: one warp per road tile
+constexpr int kSmemVeh = 160;        // snapshot slots held in shared memory (larger tiles use global scratch)
+constexpr int kSmemInbox = 48;       // inbox keys sorted in shared memory
 constexpr int kNAcc = 12;            // per-tile int64 accumulators
-constexpr int kMaxRoadLanes = 8;     // road lanes per tile cached in the successor table
-constexpr int kMaxSucc = 12;         // successors per road lane cached in the table
+constexpr int kMaxRoadLanes = 4;     // road lanes per tile cached in the successor table
+constexpr int kMaxSucc = 8;          // successors per road lane cached in the table
+static_assert(kMaxRoadLanes * kMaxSucc == 32, "one warp builds the successor table");
+constexpr int kMaxGroups = 4;        // distinct target roads per road lane in the table
 constexpr int kSmemProf = 8;         // profiles staged in shared memory
 constexpr uint64_t kEmptyKey = ~0ull;
 

@@ -40,36 +40,15 @@ __device__ unsigned long long g_guard_stats[32];
 #endif
 __device__ F64_NOINLINE void veh_update_f64(const StepArgs &A, const TileSh &T, const View &C,
                                             int i, Res &r) {
+#ifdef NO_F64
+  return;
+#endif
   Guard g;
   g.hit = false;
   g.why = 0;
   veh_update<double, false>(A, T, C, i, r, g);
 }
 
-struct ResView {                     // per-slot step results (shared or global scratch)
-  float *s1, *v1;
-  int32_t *lane, *wait, *cur;
-  uint8_t *flags;                    // lc+1 : 2 | fin : 1 | min(hand, 31) : 5
-};
-__device__ __forceinline__ void store_res(const ResView &R, int i, const Res &r) {
-  R.s1[i] = r.s1;
-  R.v1[i] = r.v1;
-  R.lane[i] = r.lane_g;
-  R.wait[i] = r.wait1;
-  R.cur[i] = r.cursor;
-  R.flags[i] = (uint8_t)((r.lc + 1) | (r.fin ? 4 : 0) | ((r.hand > 31 ? 31 : r.hand) << 3));
-}
-__device__ __forceinline__ void load_res(const ResView &R, int i, Res &r) {
-  r.s1 = R.s1[i];
-  r.v1 = R.v1[i];
-  r.lane_g = R.lane[i];
-  r.wait1 = R.wait[i];
-  r.cursor = R.cur[i];
-  const int f = R.flags[i];
-  r.lc = (f & 3) - 1;
-  r.fin = (f & 4) != 0;
-  r.hand = f >> 3;
-}
 __device__ __forceinline__ void record(const StepArgs &A, int vid, const Res &r, bool guard) {
   A.r_leader[vid] = r.leader;
   A.r_hops[vid] = (int8_t)r.hops;
@@ -83,91 +62,134 @@ __device__ __forceinline__ void record(const StepArgs &A, int vid, const Res &r,
   A.r_guard[vid] = (uint8_t)(guard ? 1 : 0);
 }
 
+__device__ __forceinline__ void put_inbox(InboxRec *dst, const InboxRec &rec) {
+  int4 *d = reinterpret_cast<int4 *>(dst);
+  const int4 *s = reinterpret_cast<const int4 *>(&rec);
+  d[0] = s[0];
+  d[1] = s[1];
+}
+
 struct StepShared {
   TileSh T;
-  int warp_tot[kThreads / 32];
-  int nst_out;
-  int nguard;
-  unsigned long long bk_hi[kSmemInbox];
-  int bk_vid[kSmemInbox];
-  int bsort[kSmemInbox];
-  unsigned long long sk_hi[kSmemInbox];   // inbox keys in sorted order
-  int sk_vid[kSmemInbox];
+  union {
+    struct {
+      unsigned long long bk_hi[kSmemInbox];   // inbox keys (arrival order)
+      int bk_vid[kSmemInbox];
+      int bsort[kSmemInbox];
+      unsigned long long sk_hi[kSmemInbox];   // inbox keys in sorted order
+      int sk_vid[kSmemInbox];
+    };
+    SuccEnt stage[32];                        // successor-table staging (before the merge)
+  };
   Prof prof[kSmemProf];
-  long long acc[kNAcc];
 };
 
 #ifndef KSTEP_MINB
-#define KSTEP_MINB 8
+#define KSTEP_MINB 24
 #endif
+// One WARP per road tile: no block barriers, warps progress independently
+// (DESIGN §3.3).  All intra-tile synchronisation is __syncwarp().
 __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ StepShared S;
   TileSh &T = S.T;
-  const int tile = blockIdx.x, tid = threadIdx.x;
-  const int lane_id = tid & 31, warp = tid >> 5;
+  const int tile = blockIdx.x, lane_id = threadIdx.x;
 
   // ---- tile metadata -----------------------------------------------------
   const int l0 = A.tile_lane_off[tile];
   const int nl = A.tile_lane_off[tile + 1] - l0;
-  if (tid == 0) {
+  const int nroad = A.tile_nroad[tile];
+  const int n_st = A.cnt_in[tile];
+  const int n_in = A.icnt_in[tile];
+  const int n = n_st + n_in;
+  const int base = A.tile_base[tile];
+  const int ibase = A.tile_ibase[tile];
+  if (lane_id == 0) {
     T.nl = nl;
-    T.nroad = A.tile_nroad[tile];
+    T.nroad = nroad;
     T.tile = tile;
-    T.base = A.tile_base[tile];
-    T.ibase = A.tile_ibase[tile];
+    T.base = base;
+    T.ibase = ibase;
     T.cap = A.tile_cap[tile];
     T.icap = A.tile_icap[tile];
-    S.nst_out = 0;
-    S.nguard = 0;
     T.P = A.n_prof <= kSmemProf ? S.prof : A.prof;
+    T.tab_ok = nroad <= kMaxRoadLanes ? 1 : 0;
   }
-  if (tid < kNAcc) S.acc[tid] = 0;
+  __syncwarp();
   if (A.n_prof <= kSmemProf)
-    for (int q = tid; q < A.n_prof; q += kThreads) S.prof[q] = A.prof[q];
-  for (int l = tid; l < nl; l += kThreads) {
-    int g = A.tile_lanes[l0 + l];
+    for (int q = lane_id; q < A.n_prof; q += kThreads) S.prof[q] = A.prof[q];
+  for (int l = lane_id; l < nl; l += kThreads) {
+    const int g = A.tile_lanes[l0 + l];
     T.glob[l] = g;
     T.len[l] = A.lane_len[g];
     T.vmax[l] = A.lane_vmax[g];
-    T.isroad[l] = A.lane_road[g] >= 0;
+    T.isroad[l] = l < nroad;
     T.usable[l] = A.usable[g];
     T.seg_start[l] = 0;
     T.seg_end[l] = 0;
     T.first_out[l] = 0x7fffffff;
-    int lf = A.lane_left ? A.lane_left[g] : -1, rt = A.lane_right ? A.lane_right[g] : -1;
-    T.left[l] = (lf >= 0 && A.lane_tile[lf] == tile) ? (int8_t)A.lane_local[lf] : (int8_t)-1;
-    T.right[l] = (rt >= 0 && A.lane_tile[rt] == tile) ? (int8_t)A.lane_local[rt] : (int8_t)-1;
+    // road lanes are the first nroad local lanes, leftmost first (validated at create)
+    T.left[l] = (l < nroad && l > 0) ? (int8_t)(l - 1) : (int8_t)-1;
+    T.right[l] = (l < nroad - 1) ? (int8_t)(l + 1) : (int8_t)-1;
   }
-  // successor table of the tile's road lanes (usable successors only)
-  const int nroad = A.tile_nroad[tile];
-  if (tid == 0) T.tab_ok = nroad <= kMaxRoadLanes ? 1 : 0;
+  // successor table of the tile's road lanes: usable successors sorted by
+  // (target road, lane id) and grouped by target road (built in parallel, one
+  // warp lane per (road lane, successor) slot; staging reuses the inbox-key area)
+  SuccEnt *stage = S.stage;
   if (nroad <= kMaxRoadLanes) {
-    for (int l = tid; l < nroad; l += kThreads) {
+    const int x = lane_id;                          // kMaxRoadLanes * kMaxSucc == 32
+    const int l = x / kMaxSucc, k = x % kMaxSucc;
+    bool valid = false;
+    SuccEnt s;
+    if (l < nroad) {
       const int g = A.tile_lanes[l0 + l];
       const int e0 = A.succ_off[g], e1 = A.succ_off[g + 1];
-      int k = 0;
-      bool ok = e1 - e0 <= kMaxSucc;
-      if (ok)
-        for (int e = e0; e < e1; ++e) {
-          const int j = A.succ[e];
-          if (!A.usable[j]) continue;
-          SuccEnt &s = T.se[l][k++];
+      if (e1 - e0 > kMaxSucc) T.tab_ok = 0;
+      if (k < e1 - e0) {
+        const int j = A.succ[e0 + k];
+        if (A.usable[j]) {
+          valid = true;
           s.j = j;
           s.troad = A.target_road[j];
           s.b = A.exit_lane[j];
           s.outr = A.outroads[s.b];
           s.stop = (A.lane_road[j] < 0 && A.lane_sig[j] != SIG_GREEN) ? 1 : 0;
         }
-      T.sn[l] = (uint8_t)k;
-      if (!ok) T.tab_ok = 0;
+      }
     }
+    if (!valid) { s.j = 0x7fffffff; s.troad = 0x7fffffff; }
+    stage[x] = s;
+    __syncwarp();
+    int rank = 0, cnt = 0;
+    for (int q = 0; q < kMaxSucc; ++q) {
+      const SuccEnt &o = stage[l * kMaxSucc + q];
+      cnt += o.j != 0x7fffffff;
+      rank += (o.troad < s.troad) || (o.troad == s.troad && o.j < s.j);
+    }
+    if (valid) T.se[l][rank] = s;
+    if (l < nroad && k == 0) T.sn[l] = (uint8_t)cnt;
+    __syncwarp();
+    if (l < nroad && k < cnt) {
+      const bool start = k == 0 || T.se[l][k - 1].troad != T.se[l][k].troad;
+      int gid = 0;
+      for (int q = 1; q <= k; ++q) gid += T.se[l][q - 1].troad != T.se[l][q].troad;
+      if (start) {
+        if (gid < kMaxGroups) {
+          T.gtroad[l][gid] = T.se[l][k].troad;
+          T.gbeg[l][gid] = (uint8_t)k;
+        } else {
+          T.tab_ok = 0;
+        }
+      }
+      if (k == cnt - 1) {
+        const int ngr = min(gid + 1, kMaxGroups);
+        T.ng[l] = (uint8_t)ngr;
+        T.gbeg[l][ngr] = (uint8_t)cnt;
+      }
+    }
+    if (l < nroad && k == 0 && cnt == 0) T.ng[l] = 0;
   }
-  const int n_st = A.cnt_in[tile];
-  const int n_in = A.icnt_in[tile];
-  const int n = n_st + n_in;
-  const int base = A.tile_base[tile];
-  const int ibase = A.tile_ibase[tile];
+  __syncwarp();
 
   // snapshot view: shared memory, or this tile's global scratch if too large
   View C;
@@ -181,6 +203,8 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
     C.nxt2 = C.vid + 2 * kSmemVeh;
     C.meta = reinterpret_cast<uint32_t *>(C.vid + 3 * kSmemVeh);
     C.wait = C.vid + 4 * kSmemVeh;
+    C.ai = reinterpret_cast<float *>(C.vid + 5 * kSmemVeh);
+    C.gi = reinterpret_cast<uint8_t *>(C.ai + kSmemVeh);
   } else {
     const int sb = base + ibase;               // scratch is indexed by base + ibase (size cap + icap)
     C.s = A.scratch.s + sb;
@@ -190,60 +214,64 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
     C.nxt2 = A.scratch.nxt2 + sb;
     C.meta = A.scratch.meta + sb;
     C.wait = A.scratch.wait + sb;
+    C.ai = A.rs_s1 + sb;
+    C.gi = A.rs_flags + sb;
   }
   int *bsort = (n_in <= kSmemInbox) ? S.bsort : (A.bsort_scratch + ibase);
   const InboxRec *inb = A.inbox_in + ibase;
+  const bool small_in = n_in <= kSmemInbox;
 
   // ---- 1. merge stayers + sorted inbox (a1) ---------------------------------
   if (n_in > 0) {
-    if (n_in <= kSmemInbox) {
-      for (int j = tid; j < n_in; j += kThreads) {
-        InboxRec r = inb[j];
+    if (small_in) {
+      for (int j = lane_id; j < n_in; j += kThreads) {
+        const InboxRec r = inb[j];
         S.bk_hi[j] = hikey(m_lane(r.meta), r.s);
         S.bk_vid[j] = r.vid;
       }
-      __syncthreads();
-      for (int j = tid; j < n_in; j += kThreads) {
-        unsigned long long h = S.bk_hi[j];
-        int vj = S.bk_vid[j], rank = 0;
+      __syncwarp();
+      for (int j = lane_id; j < n_in; j += kThreads) {
+        const unsigned long long h = S.bk_hi[j];
+        const int vj = S.bk_vid[j];
+        int rank = 0;
         for (int q = 0; q < n_in; ++q) rank += key_less(S.bk_hi[q], S.bk_vid[q], h, vj);
         bsort[rank] = j;
         S.sk_hi[rank] = h;
         S.sk_vid[rank] = vj;
       }
     } else {
-      for (int j = tid; j < n_in; j += kThreads) {
-        InboxRec r = inb[j];
-        unsigned long long h = hikey(m_lane(r.meta), r.s);
+      for (int j = lane_id; j < n_in; j += kThreads) {
+        const InboxRec r = inb[j];
+        const unsigned long long h = hikey(m_lane(r.meta), r.s);
         int rank = 0;
         for (int q = 0; q < n_in; ++q) {
-          InboxRec o = inb[q];
+          const InboxRec o = inb[q];
           rank += key_less(hikey(m_lane(o.meta), o.s), o.vid, h, r.vid);
         }
         bsort[rank] = j;
       }
     }
   }
-  __syncthreads();
-  // stayers: position = own index + #inbox keys below (binary search in sorted inbox)
-  for (int i = tid; i < n_st; i += kThreads) {
+  __syncwarp();
+  // stayers: position = own index + #inbox keys below (binary search in the sorted inbox)
+  for (int i = lane_id; i < n_st; i += kThreads) {
     const int gi = base + i;
-    float s = A.in.s[gi];
-    uint32_t meta = A.in.meta[gi];
-    int vid = A.in.vid[gi];
+    const float s = A.in.s[gi];
+    const uint32_t meta = A.in.meta[gi];
+    const int vid = A.in.vid[gi];
     int pos = i;
     if (n_in > 0) {
-      unsigned long long h = hikey(m_lane(meta), s);
+      const unsigned long long h = hikey(m_lane(meta), s);
       int lo = 0, hi = n_in;
-      if (n_in <= kSmemInbox) {
+      if (small_in) {
         while (lo < hi) {
-          int mid = (lo + hi) >> 1;
+          const int mid = (lo + hi) >> 1;
           if (key_less(S.sk_hi[mid], S.sk_vid[mid], h, vid)) lo = mid + 1; else hi = mid;
         }
       } else {
         while (lo < hi) {
-          int mid = (lo + hi) >> 1;
-          InboxRec o = inb[bsort[mid]];
+          const int mid = (lo + hi) >> 1;
+          const InboxRec o = inb[bsort[mid]];
           if (key_less(hikey(m_lane(o.meta), o.s), o.vid, h, vid)) lo = mid + 1; else hi = mid;
         }
       }
@@ -257,18 +285,18 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
     C.meta[pos] = meta;
     C.wait[pos] = A.in.wait[gi];
   }
-  // inbox records: position = sorted rank + #stayers below (binary search in slab)
-  for (int r = tid; r < n_in; r += kThreads) {
-    InboxRec rec = inb[bsort[r]];
-    unsigned long long h = hikey(m_lane(rec.meta), rec.s);
+  // inbox records: position = sorted rank + #stayers below (binary search in the slab)
+  for (int r = lane_id; r < n_in; r += kThreads) {
+    const InboxRec rec = inb[bsort[r]];
+    const unsigned long long h = hikey(m_lane(rec.meta), rec.s);
     int lo = 0, hi = n_st;
     while (lo < hi) {
-      int mid = (lo + hi) >> 1;
-      int gi = base + mid;
+      const int mid = (lo + hi) >> 1;
+      const int gi = base + mid;
       if (key_less(hikey(m_lane(A.in.meta[gi]), A.in.s[gi]), A.in.vid[gi], h, rec.vid)) lo = mid + 1;
       else hi = mid;
     }
-    int pos = r + lo;
+    const int pos = r + lo;
     C.s[pos] = rec.s;
     C.v[pos] = rec.v;
     C.vid[pos] = rec.vid;
@@ -277,102 +305,79 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
     C.meta[pos] = rec.meta;
     C.wait[pos] = rec.wait;
   }
-  __syncthreads();
+  __syncwarp();
   // lane segments of the snapshot
-  for (int i = tid; i < n; i += kThreads) {
-    int l = m_lane(C.meta[i]);
+  for (int i = lane_id; i < n; i += kThreads) {
+    const int l = m_lane(C.meta[i]);
     if (i == 0 || m_lane(C.meta[i - 1]) != l) T.seg_start[l] = i;
     if (i == n - 1 || m_lane(C.meta[i + 1]) != l) T.seg_end[l] = i + 1;
   }
-  __syncthreads();
+  __syncwarp();
 
-  // ---- 2. per-vehicle update (a2-a4), results staged per snapshot slot ------
-  // Phase A: every vehicle on the fp32 fast path; vehicles whose decision
-  // margins fall inside the guard band are queued.  Phase B: the queue is
-  // recomputed with the canonical fp64 sequence, packed onto few lanes (so a
-  // rare fallback does not stall whole warps).  No barrier inside either loop.
-  ResView R;
-  int *glist;
-  if (smem_ok) {
-    unsigned char *rb = dyn + kSmemVeh * 7 * 4;
-    R.s1 = reinterpret_cast<float *>(rb);
-    R.v1 = R.s1 + kSmemVeh;
-    R.lane = reinterpret_cast<int32_t *>(R.v1 + kSmemVeh);
-    R.wait = R.lane + kSmemVeh;
-    R.cur = R.wait + kSmemVeh;
-    glist = R.cur + kSmemVeh;
-    R.flags = reinterpret_cast<uint8_t *>(glist + kSmemVeh);
-  } else {
-    const int sb = base + ibase;
-    R.s1 = A.rs_s1 + sb;
-    R.v1 = A.rs_v1 + sb;
-    R.lane = A.rs_lane + sb;
-    R.wait = A.rs_wait + sb;
-    R.cur = A.rs_cur + sb;
-    R.flags = A.rs_flags + sb;
-    glist = A.rs_glist + sb;
-  }
-  long long acc_travel = 0, acc_waitfin = 0;
-  int acc_fin = 0, acc_lc = 0, acc_hand = 0, acc_guard = 0, acc_ovf = 0;
-  for (int i = tid; i < n; i += kThreads) {
-    Res r;
-    Guard g;
-    g.hit = false;
-    g.why = 0;
-    if (A.exact_mode) {
-      veh_update_f64(A, T, C, i, r);
-    } else {
-      veh_update<float, true>(A, T, C, i, r, g);
-      if (g.hit) {
-        glist[atomicAdd(&S.nguard, 1)] = i;
-        acc_guard += 1;
-#ifdef GUARD_STATS
-        for (int b = 0; b < 32; ++b)
-          if (g.why & (1u << b)) atomicAdd(&g_guard_stats[b], 1ull);
+  // ---- pass 1: every vehicle's IDM vs its in-lane leader (free road if none);
+  // reused as its own a_lead, as a_of of its follower and as a_nf whenever it is
+  // the back neighbour of a lane changer
+#ifndef USE_PASS1
+#define USE_PASS1 0
 #endif
+  if (USE_PASS1 && !A.exact_mode) {
+    for (int i = lane_id; i < n; i += kThreads) {
+      const int l = m_lane(C.meta[i]);
+      const PV<float> p = pvals(T.P[m_prof(C.meta[i])], 0.f);
+      const float v = C.v[i];
+      const float v0 = (p.vmax < T.vmax[l]) ? p.vmax : T.vmax[l];
+      Guard g;
+      g.hit = false;
+      g.why = 0;
+      float a;
+      if (i + 1 < T.seg_end[l]) {
+        const float sf = C.s[i + 1], lf = T.P[m_prof(C.meta[i + 1])].len, s = C.s[i];
+        a = idm<float, true>(v, v0, true, (sf - s) - lf, v - C.v[i + 1], p, A.b_hard,
+                             fabsf(sf - s) + lf, g);
+      } else {
+        a = idm<float, true>(v, v0, false, 0.f, 0.f, p, A.b_hard, 0.f, g);
       }
+      C.ai[i] = a;
+      C.gi[i] = g.hit ? 1 : 0;
     }
-    store_res(R, i, r);
-    if (A.record) record(A, C.vid[i], r, g.hit);
+    __syncwarp();
   }
-  __syncthreads();
-  for (int q = tid; q < S.nguard; q += kThreads) {
-    const int i = glist[q];
-    Res r;
-    veh_update_f64(A, T, C, i, r);
-    store_res(R, i, r);
-    if (A.record) record(A, C.vid[i], r, true);
-  }
-  __syncthreads();
 
-  // ---- 3. outputs, in chunks of kThreads (order-preserving compaction) -------
-  const int nchunks = (n + kThreads - 1) / kThreads;
-  for (int ch = 0; ch < nchunks; ++ch) {
-    const int i = ch * kThreads + tid;
-    int kind = 0;                      // 0 none, 1 stayer, 2 mover, 3 finished
+  // ---- 2-3. per-vehicle update (a2-a4) and outputs, 32 vehicles at a time ----
+  long long acc_travel = 0, acc_waitfin = 0, acc_delay = 0;
+  int acc_fin = 0, acc_lc = 0, acc_hand = 0, acc_guard = 0, acc_ovf = 0, acc_ins = 0;
+  int run = 0;                                      // stayers written so far
+  for (int c0 = 0; c0 < n; c0 += kThreads) {
+    const int i = c0 + lane_id;
     Res r;
+    int kind = 0;                                   // 0 none, 1 stayer, 2 mover, 3 finished
     if (i < n) {
-      load_res(R, i, r);
+      Guard g;
+      g.hit = false;
+      g.why = 0;
+      if (A.exact_mode) {
+        veh_update_f64(A, T, C, i, r);
+      } else {
+        veh_update<float, true>(A, T, C, i, r, g);
+        if (g.hit) {                                // guard band: canonical fp64 recompute
+          veh_update_f64(A, T, C, i, r);
+          acc_guard += 1;
+#ifdef GUARD_STATS
+          for (int b = 0; b < 32; ++b)
+            if (g.why & (1u << b)) atomicAdd(&g_guard_stats[b], 1ull);
+#endif
+        }
+      }
+      if (A.record) record(A, C.vid[i], r, g.hit);
       const int l = m_lane(C.meta[i]);
       if (r.fin) kind = 3;
       else if (r.lc == 0 && r.hand == 0 && r.lane_g == T.glob[l]) kind = 1;
       else kind = 2;
     }
-    // order-preserving compaction of stayers (block scan)
+    // order-preserving compaction of stayers (warp ballot)
     const unsigned ball = __ballot_sync(0xffffffffu, kind == 1);
-    const int wprefix = __popc(ball & ((1u << lane_id) - 1u));
-    if (lane_id == 0) S.warp_tot[warp] = __popc(ball);
-    __syncthreads();
-    int woff = 0, tot = 0;
-#pragma unroll
-    for (int w = 0; w < kThreads / 32; ++w) {
-      const int x = S.warp_tot[w];
-      woff += (w < warp) ? x : 0;
-      tot += x;
-    }
-    const int run = S.nst_out;
     if (kind == 1) {
-      const int pos = base + run + woff + wprefix;
+      const int pos = base + run + __popc(ball & ((1u << lane_id) - 1u));
       const uint32_t meta = C.meta[i];
       A.out.s[pos] = r.s1;
       A.out.v[pos] = r.v1;
@@ -397,14 +402,8 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
       rec.pad = 0;
       const int dt = A.lane_tile[r.lane_g];
       const int slot = atomicAdd(&A.icnt_out[dt], 1);
-      if (slot < A.tile_icap[dt]) {
-        int4 *dst = reinterpret_cast<int4 *>(A.inbox_out + A.tile_ibase[dt] + slot);
-        const int4 *src = reinterpret_cast<const int4 *>(&rec);
-        dst[0] = src[0];
-        dst[1] = src[1];
-      } else {
-        acc_ovf += 1;
-      }
+      if (slot < A.tile_icap[dt]) put_inbox(A.inbox_out + A.tile_ibase[dt] + slot, rec);
+      else acc_ovf += 1;
       atomicMin(&A.summ_next[r.lane_g], vkey(r.s1, vid));
       A.pubv_next[vid] = r.v1;
       acc_lc += r.lc != 0;
@@ -420,13 +419,12 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
       acc_lc += r.lc != 0;
       acc_hand += r.hand;
     }
-    __syncthreads();
-    if (tid == 0) S.nst_out = run + tot;
-    __syncthreads();
+    run += __popc(ball);
   }
+  __syncwarp();
 
   // ---- 4. summaries, insertions, counters ------------------------------------
-  for (int l = tid; l < nl; l += kThreads) {
+  for (int l = lane_id; l < nl; l += kThreads) {
     const int g = T.glob[l];
     const int pos = T.first_out[l];
     if (pos != 0x7fffffff) {
@@ -437,9 +435,7 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
     }
     A.summ_clear[g] = kEmptyKey;
   }
-  int acc_ins = 0;
-  long long acc_delay = 0;
-  for (int l = tid; l < T.nroad; l += kThreads) {   // departures (K11; ledger L25)
+  for (int l = lane_id; l < nroad; l += kThreads) { // departures (K11; ledger L25)
     const int g = T.glob[l];
     const int h = A.pend_head[g];
     if (h >= A.pend_off[g + 1]) continue;
@@ -474,14 +470,8 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
     rec.wait = 0;
     rec.pad = 0;
     const int slot = atomicAdd(&A.icnt_out[tile], 1);
-    if (slot < T.icap) {
-      int4 *dst = reinterpret_cast<int4 *>(A.inbox_out + ibase + slot);
-      const int4 *src = reinterpret_cast<const int4 *>(&rec);
-      dst[0] = src[0];
-      dst[1] = src[1];
-    } else {
-      acc_ovf += 1;
-    }
+    if (slot < T.icap) put_inbox(A.inbox_out + ibase + slot, rec);
+    else acc_ovf += 1;
     atomicMin(&A.summ_next[g], vkey(rec.s, k));
     A.pubv_next[k] = 0.f;
     A.pend_head[g] = h + 1;
@@ -491,19 +481,22 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
     acc_ins += 1;
     acc_delay += (long long)(A.t + 1 - A.depart[k]);
   }
-  // block reduction of the counters (int64 shared atomics, exact, order independent)
-  const long long vals[kNAcc] = {0, acc_fin, acc_travel, acc_waitfin, acc_delay, acc_lc, acc_hand,
-                                 acc_ins, acc_guard, acc_ovf, 0, 0};
+  // warp reduction of the counters (int64, exact, order independent)
+  long long vals[kNAcc] = {0, acc_fin, acc_travel, acc_waitfin, acc_delay, acc_lc, acc_hand,
+                           acc_ins, acc_guard, acc_ovf, 0, 0};
+  const unsigned any = __ballot_sync(0xffffffffu, (acc_fin | acc_lc | acc_hand | acc_ins |
+                                                   acc_guard | acc_ovf) != 0);
+  if (any) {
 #pragma unroll
-  for (int c = 1; c < kNAcc; ++c)
-    if (vals[c]) atomicAdd(reinterpret_cast<unsigned long long *>(&S.acc[c]),
-                           (unsigned long long)vals[c]);
-  __syncthreads();
-  if (tid == 0) {
+    for (int c = 1; c < kNAcc - 2; ++c)
+      for (int o = 16; o > 0; o >>= 1) vals[c] += __shfl_down_sync(0xffffffffu, vals[c], o);
+  }
+  if (lane_id == 0) {
     long long *ta = A.tacc + (size_t)tile * kNAcc;
     ta[ACC_VEH_STEPS] += n;
-    for (int c = 1; c < kNAcc; ++c) ta[c] += S.acc[c];
-    A.cnt_out[tile] = S.nst_out;
+    if (any)
+      for (int c = 1; c < kNAcc - 2; ++c) ta[c] += vals[c];
+    A.cnt_out[tile] = run;
     A.icnt_in[tile] = 0;
   }
 }
@@ -629,7 +622,7 @@ __global__ void k_fill_u64(unsigned long long *p, unsigned long long v, int64_t 
 }
 
 // ---- launchers ---------------------------------------------------------------
-int step_smem_bytes() { return kSmemVeh * (7 * 4 + 6 * 4 + 1); }
+int step_smem_bytes() { return kSmemVeh * (7 * 4 + 4 + 1); }
 
 void launch_step(const StepArgs &a, void *stream, int smem_bytes) {
   static bool attr = false;

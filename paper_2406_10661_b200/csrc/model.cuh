@@ -13,6 +13,10 @@
 
 #include "dev.h"
 
+#ifndef USE_PASS1
+#define USE_PASS1 0
+#endif
+
 namespace sim {
 
 template <typename R> struct Ar;
@@ -82,8 +86,11 @@ struct TileSh {
   int nl, nroad, tile, base, ibase, cap, icap;
   const Prof *P;                     // profile table (shared-memory copy when small)
   int tab_ok;                        // successor table valid for this tile
-  uint8_t sn[kMaxRoadLanes];
-  SuccEnt se[kMaxRoadLanes][kMaxSucc];
+  uint8_t sn[kMaxRoadLanes];         // usable successors per road lane
+  uint8_t ng[kMaxRoadLanes];         // groups (distinct target roads) per road lane
+  uint8_t gbeg[kMaxRoadLanes][kMaxGroups + 1];
+  int gtroad[kMaxRoadLanes][kMaxGroups];
+  SuccEnt se[kMaxRoadLanes][kMaxSucc];   // sorted by (target road, lane id)
   int glob[kMaxTileLanes];
   float len[kMaxTileLanes], vmax[kMaxTileLanes];
   int seg_start[kMaxTileLanes], seg_end[kMaxTileLanes];
@@ -98,6 +105,8 @@ struct View {
   int32_t *vid, *nxt, *nxt2;
   uint32_t *meta;
   int32_t *wait;
+  float *ai;                         // fp32 IDM of each vehicle vs its in-lane leader (pass 1)
+  uint8_t *gi;                       // guard flag of that evaluation
 };
 
 __device__ __forceinline__ int m_lane(uint32_t m) { return (int)(m & 0xffu); }
@@ -151,8 +160,8 @@ __device__ __forceinline__ int next_from_road(const StepArgs &A, int m, int R1, 
 // successor table (built per step; usable successors only)
 __device__ __forceinline__ bool has_outroad_t(const StepArgs &A, const TileSh &T, int a, int R) {
   if (!T.tab_ok) return has_outroad(A, T.glob[a], R);
-  for (int k = 0; k < T.sn[a]; ++k)
-    if (T.se[a][k].troad == R) return true;
+  for (int g = 0; g < T.ng[a]; ++g)
+    if (T.gtroad[a][g] == R) return true;
   return false;
 }
 struct Next { int j; bool stop; };  // next lane and "stop line applies" (junction lane not GREEN)
@@ -164,22 +173,19 @@ __device__ __forceinline__ Next next_stop_g(const StepArgs &A, int j) {
 }
 __device__ __forceinline__ Next next1_t(const StepArgs &A, const TileSh &T, int l, int R1, int R2) {
   if (!T.tab_ok) return next_stop_g(A, next_from_road(A, T.glob[l], R1, R2));
-  Next n;
-  n.stop = false;
-  if (R1 < 0) { n.j = kLaneDest; return n; }
-  int best_any = kLaneBlocked, best_pref = kLaneBlocked, st_any = 0, st_pref = 0;
-  for (int k = 0; k < T.sn[l]; ++k) {
-    const SuccEnt &e = T.se[l][k];
-    if (e.troad != R1) continue;
-    if (best_any < 0 || e.j < best_any) { best_any = e.j; st_any = e.stop; }
-    if (pref_ok(A, e.outr, e.b, R2) && (best_pref < 0 || e.j < best_pref)) {
-      best_pref = e.j;
-      st_pref = e.stop;
+  if (R1 < 0) return Next{kLaneDest, false};
+  for (int g = 0; g < T.ng[l]; ++g) {
+    if (T.gtroad[l][g] != R1) continue;
+    const int b = T.gbeg[l][g], e = T.gbeg[l][g + 1];
+    // entries sorted by lane id: the first is the lowest candidate, the first
+    // whose exit lane continues toward R2 is the preferred one (ledger L24)
+    for (int k = b; k < e; ++k) {
+      const SuccEnt &x = T.se[l][k];
+      if (pref_ok(A, x.outr, x.b, R2)) return Next{x.j, x.stop != 0};
     }
+    return Next{T.se[l][b].j, T.se[l][b].stop != 0};
   }
-  n.j = best_pref >= 0 ? best_pref : best_any;
-  n.stop = (best_pref >= 0 ? st_pref : st_any) != 0;
-  return n;
+  return Next{kLaneBlocked, false};
 }
 __device__ __forceinline__ int next_from_road_t(const StepArgs &A, const TileSh &T, int l, int R1,
                                                 int R2) {
@@ -240,7 +246,8 @@ struct Me {                          // the ego vehicle's identity / route cache
 // O4-O6 for the ego placed on tile-local lane l (App. A2.3)
 template <typename R, bool GUARD>
 __device__ LEv<R> eval_lane(const StepArgs &A, const TileSh &T, const View &C, int l,
-                            int lead_idx, R s, R v, const PV<R> &p, const Me &me, Guard &g) {
+                            int lead_idx, R s, R v, const PV<R> &p, const Me &me, Guard &g,
+                            int self_idx = -1) {
   using M = Ar<R>;
   LEv<R> e;
   const int lg = T.glob[l];
@@ -295,7 +302,17 @@ __device__ LEv<R> eval_lane(const StepArgs &A, const TileSh &T, const View &C, i
     }
   }
   const R b_hard = (R)A.b_hard;
-  R a_lead = idm<R, GUARD>(v, v0, e.has_leader, e.gap, M::sub(v, e.vlead), p, b_hard, gscale, g);
+  R a_lead;
+  if constexpr (!M::fp64 && USE_PASS1) {
+    if (self_idx >= 0 && lead_idx >= 0) {          // own lane, in-lane leader: pass-1 value
+      a_lead = C.ai[self_idx];
+      if (GUARD && C.gi[self_idx]) g.hit = true, g.why |= (1u << 13);
+    } else {
+      a_lead = idm<R, GUARD>(v, v0, e.has_leader, e.gap, M::sub(v, e.vlead), p, b_hard, gscale, g);
+    }
+  } else {
+    a_lead = idm<R, GUARD>(v, v0, e.has_leader, e.gap, M::sub(v, e.vlead), p, b_hard, gscale, g);
+  }
   e.a = a_lead;
   e.phantom = false;
   if (road && e.next1 != kLaneDest && (e.next1 == kLaneBlocked || nx.stop)) {
@@ -361,7 +378,7 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
   const R L = (R)T.len[l];
   const int lead = (i + 1 < T.seg_end[l]) ? i + 1 : -1;
   const int of = (i > T.seg_start[l]) ? i - 1 : -1;
-  LEv<R> cur = eval_lane<R, GUARD>(A, T, C, l, lead, s, v, p, me, g);
+  LEv<R> cur = eval_lane<R, GUARD>(A, T, C, l, lead, s, v, p, me, g, i);
   o.leader = cur.leader;
   o.hops = cur.hops;
   o.phantom = cur.phantom;
@@ -406,8 +423,13 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
         const PV<R> po = pvals(T.P[m_prof(C.meta[of])], (R)0);
         const R so = (R)C.s[of], vo = (R)C.v[of];
         const R v0o = (po.vmax < (R)T.vmax[l]) ? po.vmax : (R)T.vmax[l];
-        a_of = idm<R, GUARD>(vo, v0o, true, M::sub(M::sub(s, so), p.len), M::sub(vo, v), po,
-                             b_hard, fabs(s - so) + p.len, g);
+        if constexpr (!M::fp64 && USE_PASS1) {           // of's in-lane leader is the ego
+          a_of = C.ai[of];
+          if (GUARD && C.gi[of]) g.hit = true, g.why |= (1u << 13);
+        } else {
+          a_of = idm<R, GUARD>(vo, v0o, true, M::sub(M::sub(s, so), p.len), M::sub(vo, v), po,
+                               b_hard, fabs(s - so) + p.len, g);
+        }
         if (lead >= 0) {
           const R sl_ = (R)C.s[lead];
           const R ll_ = (R)T.P[m_prof(C.meta[lead])].len;
@@ -435,7 +457,10 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
           const PV<R> pb = pvals(T.P[m_prof(C.meta[bi])], (R)0);
           const R sb = (R)C.s[bi], vb = (R)C.v[bi];
           const R v0b = (pb.vmax < (R)T.vmax[ls]) ? pb.vmax : (R)T.vmax[ls];
-          if (front[sd] >= 0) {
+          if constexpr (!M::fp64 && USE_PASS1) {         // back's in-lane leader is front
+            a_nf = C.ai[bi];
+            if (GUARD && C.gi[bi]) g.hit = true, g.why |= (1u << 13);
+          } else if (front[sd] >= 0) {
             const int fi = front[sd];
             const R sf = (R)C.s[fi];
             const R lf = (R)T.P[m_prof(C.meta[fi])].len;

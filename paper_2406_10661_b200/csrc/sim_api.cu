@@ -379,7 +379,7 @@ sim_status build_tiles(sim_s *h) {
     std::sort(jls[r].begin(), jls[r].end());
     lanes.insert(lanes.end(), jls[r].begin(), jls[r].end());
     if ((int)lanes.size() > kMaxTileLanes)
-      return fail(h, SIM_E_INVALID, "road " + std::to_string(r) + " has more than 64 lanes incl. outgoing junction lanes");
+      return fail(h, SIM_E_INVALID, "road " + std::to_string(r) + " has more than " + std::to_string(kMaxTileLanes) + " lanes incl. outgoing junction lanes");
     int cap = 0;
     for (size_t k = 0; k < lanes.size(); ++k) {
       h->lane_tile[lanes[k]] = r;
