@@ -101,6 +101,16 @@ typedef struct {
   int32_t record_decisions;          /* 1: keep the last step's decisions for sim_read_decisions */
   int32_t device;                    /* CUDA device ordinal */
   void *stream;                      /* cudaStream_t to run on (NULL = library-created stream) */
+  /* Spatial partition over `world` partitions.  world <= 1: one
+   * partition.  world > 1: either loopback = 1 (all partitions in this handle
+   * on `device`, exchanging by device copies; used to test partition
+   * invariance) or one process per GPU with the same nccl_id (from
+   * sim_get_nccl_unique_id on one rank) and rank in [0, world).  road_owner
+   * (optional, [n_roads]) fixes the partition of each road (with its outgoing
+   * junction lanes); NULL = the library's breadth-first partitioner. */
+  int32_t rank, world, loopback;
+  const uint8_t *nccl_id;            /* 128 bytes, NCCL mode only */
+  const int32_t *road_owner;
 } sim_params;
 
 typedef struct {
@@ -154,6 +164,15 @@ typedef struct {
  * device memory on params->device and uploads the t = 0 state. */
 sim_status sim_create(const sim_graph *g, const sim_trips *trips,
                       const sim_params *params, sim_handle *out);
+/* NCCL unique id for a partitioned run (call on one rank, broadcast the 128
+ * bytes to all ranks, e.g. with torch.distributed). */
+sim_status sim_get_nccl_unique_id(uint8_t out[128]);
+/* Host-only (no GPU): the partition sim_create would use for params->world,
+ * written to road_owner [n_roads] (may be NULL), and the exchange plan sizes
+ * plan_sizes [world*world*2] (may be NULL): for each (a, b) the migrant-buffer
+ * capacity a -> b and the number of lanes whose summary a reads from b. */
+sim_status sim_partition(const sim_graph *g, const sim_trips *trips, const sim_params *params,
+                         int32_t *road_owner, int32_t *plan_sizes);
 /* Advance n >= 0 steps (next_step(n)), asynchronously. */
 sim_status sim_step(sim_handle h, int32_t n);
 /* Block until all enqueued work finished; reports deferred device errors. */

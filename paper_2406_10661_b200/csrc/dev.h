@@ -51,6 +51,17 @@ struct InboxRec {                   // 32 B, one sector
   int32_t wait, pad;
 };
 
+struct MigRec {                     // 48 B: a vehicle migrating to another partition
+  InboxRec rec;                     // rec.meta holds the destination lane's tile-local index
+  int32_t tile, insert_time, pad0, pad1;
+};                                  // element 0 of every peer region is a header: rec.vid = count
+
+struct HaloRec {                    // 16 B: first-vehicle summary of one lane for a peer
+  unsigned long long key;
+  float v;
+  int32_t pad;
+};
+
 struct Slab {                       // SoA hot record, 28 B / vehicle
   float *s, *v;
   int32_t *vid, *nxt, *nxt2;        // route[c+1], route[c+2] (-1 past the end)
@@ -82,7 +93,9 @@ struct StepArgs {
   const uint8_t *lane_sig;
   const int32_t *lane_tile;
   const uint8_t *lane_local;
-  // tiles
+  // tiles (n_tiles global; this partition processes tiles[0 .. n_own))
+  int32_t rank, n_own;
+  const int32_t *tiles, *tile_owner;
   const int32_t *tile_lane_off, *tile_lanes, *tile_nroad;
   const int32_t *tile_base, *tile_cap, *tile_ibase, *tile_icap;
   int32_t *cnt_in, *cnt_out;        // [n_tiles] stayer counts (read / write buffers)
@@ -92,9 +105,12 @@ struct StepArgs {
   InboxRec *inbox_out;
   Slab scratch;                     // global fallback for large tiles ([base+ibase, +cap+icap))
   int32_t *bsort_scratch;           // [Σ icap] inbox sort order for large inboxes
-  float *rs_s1, *rs_v1;             // per-slot results for large tiles (scratch indexing)
-  int32_t *rs_lane, *rs_wait, *rs_cur, *rs_glist;
+  float *rs_s1;                     // per-slot in-lane IDM for large tiles (scratch indexing)
   uint8_t *rs_flags;
+  // migration to other partitions (world > 1): per-peer regions of MigRec
+  MigRec *out_buf;
+  const int32_t *out_off, *out_cap;
+  int32_t *out_cnt;
   // lane summaries (first vehicle key) for t, t+1, t+2 (triple buffer)
   const unsigned long long *summ_cur;
   unsigned long long *summ_next, *summ_clear;
@@ -117,7 +133,7 @@ struct StepArgs {
   int32_t *r_leader, *r_of, *r_side;
   int8_t *r_hops, *r_phantom, *r_lc, *r_hand, *r_fin, *r_ins;
   float *r_acc;
-  uint8_t *r_guard;
+  uint8_t *r_guard, *r_mark;        // r_mark: processed by this partition in the last step
 };
 
 struct SignalArgs {
@@ -145,5 +161,12 @@ void launch_reduce_acc(const long long *tacc, int n_tiles, const int32_t *cnt,
 void launch_lane_stats(const StepArgs &a, int32_t *lane_count, int32_t *lane_wait,
                        float queue_zone, void *stream);
 void launch_fill_u64(unsigned long long *p, unsigned long long v, int64_t n, void *stream);
+void launch_mig_header(MigRec *out_buf, const int32_t *out_off, const int32_t *out_cap,
+                       int32_t *out_cnt, int world, void *stream);
+void launch_absorb(const StepArgs &a, const MigRec *in_buf, const int32_t *in_off,
+                   const int32_t *in_cap, int world, void *stream);
+void launch_halo_pack(const StepArgs &a, const int32_t *lanes, HaloRec *buf, int64_t n, void *stream);
+void launch_halo_unpack(const StepArgs &a, const int32_t *lanes, const HaloRec *buf, int64_t n,
+                        void *stream);
 
 }  // namespace sim

@@ -13,6 +13,8 @@
 //      P:142), and per-tile int64 counters accumulate (a6).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "dev.h"
 #include "model.cuh"
 
@@ -60,6 +62,7 @@ __device__ __forceinline__ void record(const StepArgs &A, int vid, const Res &r,
   A.r_acc[vid] = r.acc;
   A.r_fin[vid] = (int8_t)r.fin;
   A.r_guard[vid] = (uint8_t)(guard ? 1 : 0);
+  A.r_mark[vid] = 1;
 }
 
 __device__ __forceinline__ void put_inbox(InboxRec *dst, const InboxRec &rec) {
@@ -93,7 +96,7 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ StepShared S;
   TileSh &T = S.T;
-  const int tile = blockIdx.x, lane_id = threadIdx.x;
+  const int tile = A.tiles[blockIdx.x], lane_id = threadIdx.x;
 
   // ---- tile metadata -----------------------------------------------------
   const int l0 = A.tile_lane_off[tile];
@@ -401,11 +404,24 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
       rec.wait = r.wait1;
       rec.pad = 0;
       const int dt = A.lane_tile[r.lane_g];
-      const int slot = atomicAdd(&A.icnt_out[dt], 1);
-      if (slot < A.tile_icap[dt]) put_inbox(A.inbox_out + A.tile_ibase[dt] + slot, rec);
-      else acc_ovf += 1;
-      atomicMin(&A.summ_next[r.lane_g], vkey(r.s1, vid));
-      A.pubv_next[vid] = r.v1;
+      const int owner = A.tile_owner[dt];
+      if (owner == A.rank) {
+        const int slot = atomicAdd(&A.icnt_out[dt], 1);
+        if (slot < A.tile_icap[dt]) put_inbox(A.inbox_out + A.tile_ibase[dt] + slot, rec);
+        else acc_ovf += 1;
+        atomicMin(&A.summ_next[r.lane_g], vkey(r.s1, vid));
+        A.pubv_next[vid] = r.v1;
+      } else {                                      // migrant to another partition
+        const int slot = atomicAdd(&A.out_cnt[owner], 1);
+        if (slot < A.out_cap[owner]) {
+          MigRec *m = A.out_buf + A.out_off[owner] + 1 + slot;
+          put_inbox(&m->rec, rec);
+          m->tile = dt;
+          m->insert_time = A.insert_time[vid];
+        } else {
+          acc_ovf += 1;
+        }
+      }
       acc_lc += r.lc != 0;
       acc_hand += r.hand;
     } else if (kind == 3) {
@@ -595,8 +611,8 @@ __global__ void k_reduce_acc(const long long *tacc, int n_tiles, const int32_t *
 
 __global__ void k_lane_stats(StepArgs A, int32_t *cnt, int32_t *wt, float zone) {
   // lane queue length: per lane, vehicles and those with v < v_wait
-  // within the last `zone` metres, over stayers + inbox of each tile
-  const int tile = blockIdx.x;
+  // within the last `zone` metres, over stayers + inbox of each own tile
+  const int tile = A.tiles[blockIdx.x];
   const int ns = A.cnt_in[tile], ni = A.icnt_in[tile];
   const int l0 = A.tile_lane_off[tile];
   for (int i = threadIdx.x; i < ns + ni; i += blockDim.x) {
@@ -621,6 +637,60 @@ __global__ void k_fill_u64(unsigned long long *p, unsigned long long v, int64_t 
     p[i] = v;
 }
 
+// ---- partition exchange -------------------------------------------
+__global__ void k_mig_header(MigRec *out_buf, const int32_t *out_off, const int32_t *out_cap,
+                             int32_t *out_cnt, int world) {
+  const int q = threadIdx.x;
+  if (q < world) {
+    if (out_cap[q] > 0) out_buf[out_off[q]].rec.vid = out_cnt[q];   // count header of region q
+    out_cnt[q] = 0;                                 // ready for the next step
+  }
+}
+
+// Received migrants join their tile's inbox for step t+1 exactly like local
+// movers (integer atomics: order independent, so results do not depend on the
+// partitioning, P-PART).  One block per peer region.
+__global__ void k_absorb(StepArgs A, const MigRec *in_buf, const int32_t *in_off,
+                         const int32_t *in_cap) {
+  const int q = blockIdx.x;
+  const int cap = in_cap[q];
+  if (cap == 0) return;
+  const MigRec *reg = in_buf + in_off[q];
+  const int cnt = min(reg[0].rec.vid, cap);
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const MigRec &m = reg[1 + i];
+    const int dt = m.tile, vid = m.rec.vid;
+    const int lane_g = A.tile_lanes[A.tile_lane_off[dt] + m_lane(m.rec.meta)];
+    const int slot = atomicAdd(&A.icnt_out[dt], 1);
+    if (slot < A.tile_icap[dt]) put_inbox(A.inbox_out + A.tile_ibase[dt] + slot, m.rec);
+    atomicMin(&A.summ_next[lane_g], vkey(m.rec.s, vid));
+    A.pubv_next[vid] = m.rec.v;
+    A.insert_time[vid] = m.insert_time;
+    A.status[vid] = ST_DRIVING;
+  }
+}
+
+__global__ void k_halo_pack(StepArgs A, const int32_t *lanes, HaloRec *buf, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long key = A.summ_next[lanes[i]];
+    HaloRec r;
+    r.key = key;
+    r.v = key != kEmptyKey ? A.pubv_next[(int)(unsigned)(key & 0xffffffffu)] : 0.f;
+    r.pad = 0;
+    buf[i] = r;
+  }
+}
+
+__global__ void k_halo_unpack(StepArgs A, const int32_t *lanes, const HaloRec *buf, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const HaloRec r = buf[i];
+    A.summ_next[lanes[i]] = r.key;
+    if (r.key != kEmptyKey) A.pubv_next[(int)(unsigned)(r.key & 0xffffffffu)] = r.v;
+  }
+}
+
 // ---- launchers ---------------------------------------------------------------
 int step_smem_bytes() { return kSmemVeh * (7 * 4 + 4 + 1); }
 
@@ -630,8 +700,8 @@ void launch_step(const StepArgs &a, void *stream, int smem_bytes) {
     cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     attr = true;
   }
-  if (a.n_tiles > 0)
-    k_step<<<a.n_tiles, kThreads, smem_bytes, (cudaStream_t)stream>>>(a);
+  if (a.n_own > 0)
+    k_step<<<a.n_own, kThreads, smem_bytes, (cudaStream_t)stream>>>(a);
 }
 
 void launch_signal(const SignalArgs &a, void *stream) {
@@ -653,8 +723,8 @@ void launch_reduce_acc(const long long *tacc, int n_tiles, const int32_t *cnt,
 
 void launch_lane_stats(const StepArgs &a, int32_t *lane_count, int32_t *lane_wait, float zone,
                        void *stream) {
-  if (a.n_tiles > 0)
-    k_lane_stats<<<a.n_tiles, 128, 0, (cudaStream_t)stream>>>(a, lane_count, lane_wait, zone);
+  if (a.n_own > 0)
+    k_lane_stats<<<a.n_own, 128, 0, (cudaStream_t)stream>>>(a, lane_count, lane_wait, zone);
 }
 
 void launch_fill_u64(unsigned long long *p, unsigned long long v, int64_t n, void *stream) {
@@ -662,6 +732,22 @@ void launch_fill_u64(unsigned long long *p, unsigned long long v, int64_t n, voi
 }
 
 void launch_set_i32(int32_t *, const int32_t *, const int32_t *, int, void *) {}
+
+void launch_mig_header(MigRec *out_buf, const int32_t *out_off, const int32_t *out_cap,
+                       int32_t *out_cnt, int world, void *stream) {
+  k_mig_header<<<1, 32, 0, (cudaStream_t)stream>>>(out_buf, out_off, out_cap, out_cnt, world);
+}
+void launch_absorb(const StepArgs &a, const MigRec *in_buf, const int32_t *in_off,
+                   const int32_t *in_cap, int world, void *stream) {
+  k_absorb<<<world, 256, 0, (cudaStream_t)stream>>>(a, in_buf, in_off, in_cap);
+}
+void launch_halo_pack(const StepArgs &a, const int32_t *lanes, HaloRec *buf, int64_t n, void *stream) {
+  if (n > 0) k_halo_pack<<<(int)std::min<int64_t>((n + 255) / 256, 1184), 256, 0, (cudaStream_t)stream>>>(a, lanes, buf, n);
+}
+void launch_halo_unpack(const StepArgs &a, const int32_t *lanes, const HaloRec *buf, int64_t n,
+                        void *stream) {
+  if (n > 0) k_halo_unpack<<<(int)std::min<int64_t>((n + 255) / 256, 1184), 256, 0, (cudaStream_t)stream>>>(a, lanes, buf, n);
+}
 
 }  // namespace sim
 

@@ -1,18 +1,29 @@
 // sim_api.cu — host runtime behind include/sim.h.
 //
-// Builds road tiles (dev.h), validates inputs, owns all device
-// memory, uploads canonical (per-lane sorted) state, enqueues steps
-// (k_signal + k_step per step on the handle's stream), and implements the
-// setters / readers.  Nothing here computes the model: every per-vehicle
-// decision is taken on the GPU (kernels.cu / model.cuh).
+// Builds road tiles (dev.h), validates inputs, partitions the
+// tiles over ranks, owns all device memory, uploads canonical
+// (per-lane sorted) state, enqueues steps (k_signal + k_step per partition,
+// then the migration and halo exchanges when partitioned) on the handle's
+// stream, and implements the setters / readers.  Nothing here computes the
+// model: every per-vehicle decision is taken on the GPU (kernels.cu, model.cuh).
+//
+// Partitioned modes (sim_params.world > 1):
+//   * NCCL: one process per GPU, one partition per handle; exchanges are
+//     grouped ncclSend / ncclRecv on the simulation stream; metrics are
+//     ncclAllReduce'd (NCCL is loaded with dlopen only in this mode);
+//   * loopback: all `world` partitions live in one handle on one device and
+//     exchange by device-to-device copies — the same kernels and exchange
+//     plan, used to test partition invariance (P-PART) on a single GPU.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cmath>
-#include <mutex>
-#include <set>
 #include <cstdio>
 #include <cstring>
+#include <deque>
+#include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -39,7 +50,69 @@ struct HostState {                  // vid / junction / lane indexed state
   std::vector<int> jphase, jel, jy, jpend;
   std::vector<uint8_t> dir;
 };
+
+// ---- minimal NCCL binding (dlopen; only the partitioned NCCL mode needs it) --
+typedef struct { char internal[128]; } NcclId;
+typedef void *NcclComm;
+struct Nccl {
+  void *lib = nullptr;
+  int (*GetUniqueId)(NcclId *) = nullptr;
+  int (*CommInitRank)(NcclComm *, int, NcclId, int) = nullptr;
+  int (*CommDestroy)(NcclComm) = nullptr;
+  int (*Send)(const void *, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+  int (*Recv)(void *, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+  int (*AllReduce)(const void *, void *, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
+  const char *(*GetErrorString)(int) = nullptr;
+  bool load(std::string &err) {
+    if (lib) return true;
+    const char *names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char *n : names)
+      if ((lib = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!lib) { err = "cannot dlopen libnccl.so.2 (needed for world > 1 without loopback)"; return false; }
+#define SYM(f, n) f = reinterpret_cast<decltype(f)>(dlsym(lib, n)); if (!f) { err = std::string("missing ") + n; return false; }
+    SYM(GetUniqueId, "ncclGetUniqueId"); SYM(CommInitRank, "ncclCommInitRank");
+    SYM(CommDestroy, "ncclCommDestroy"); SYM(Send, "ncclSend"); SYM(Recv, "ncclRecv");
+    SYM(AllReduce, "ncclAllReduce"); SYM(GroupStart, "ncclGroupStart"); SYM(GroupEnd, "ncclGroupEnd");
+    SYM(GetErrorString, "ncclGetErrorString");
+#undef SYM
+    return true;
+  }
+};
+Nccl g_nccl;
+constexpr int kNcclInt8 = 0, kNcclInt64 = 4, kNcclSum = 0;
 }  // namespace
+
+// One partition's device state (all partitions of a loopback handle share the
+// device and the stream; a NCCL handle has exactly one).
+struct Part {
+  int rank = 0;
+  StepArgs A{};
+  SignalArgs SG{};
+  Slab slab[2]{};
+  InboxRec *inbox[2]{};
+  int32_t *cnt[2]{}, *icnt[2]{};
+  unsigned long long *summ[3]{};
+  float *pubv[2]{};
+  int32_t *pend_off_d = nullptr, *pend_vid_d = nullptr, *pend_head_d = nullptr;
+  uint8_t *usable_d = nullptr;
+  int32_t *outroads_d = nullptr;
+  long long *red_d = nullptr;
+  int32_t *lanestat_d = nullptr;
+  std::vector<int> tiles;                       // own tiles
+  // exchange plan (world > 1): migrant regions per peer (header record + cap)
+  std::vector<int> out_off, out_cap, in_off, in_cap;
+  MigRec *out_buf = nullptr, *in_buf = nullptr;
+  int32_t *out_cnt = nullptr;
+  int32_t *in_off_d = nullptr, *in_cap_d = nullptr;
+  int64_t out_n = 0, in_n = 0;
+  // halo: summaries of lanes each peer reads from us / we read from each peer
+  std::vector<int> hs_off, hr_off;              // [world+1] offsets into the lists
+  int32_t *hs_lanes = nullptr, *hr_lanes = nullptr;
+  HaloRec *hs_buf = nullptr, *hr_buf = nullptr;
+  int64_t hs_n = 0, hr_n = 0;
+};
 
 struct sim_s {
   std::string err;
@@ -71,32 +144,28 @@ struct sim_s {
   std::vector<Prof> profs;
   double start_margin = 0;
   int Y = 3;
+  // partitioning
+  int world = 1, rank = 0;                      // rank: this process (NCCL mode)
+  bool loopback = false;
+  std::vector<int> tile_owner;
+  NcclComm comm = nullptr;
+  std::vector<Part> parts;
   // state
   int t = 0;
   std::vector<uint8_t> dir, usable;
   std::vector<int32_t> outroads;     // [4 * n_lanes]
+  int64_t fin0 = 0;                  // FINISHED vehicles in the last loaded state
+  long long acc_fin0 = 0;            // finished counter at the last load
   // device
   std::vector<void *> allocs;
   int64_t bytes = 0;
-  StepArgs A{};
-  SignalArgs SG{};
-  Slab slab[2]{};
-  InboxRec *inbox[2]{};
-  int32_t *cnt[2]{}, *icnt[2]{};
-  unsigned long long *summ[3]{};
-  float *pubv[2]{};
-  int32_t *pend_off_d = nullptr, *pend_vid_d = nullptr, *pend_head_d = nullptr;
-  uint8_t *usable_d = nullptr;
-  int32_t *outroads_d = nullptr;
-  uint8_t *stage_dir_d = nullptr;    // device staging for lane-direction setters
-  long long *red_d = nullptr;
-  int32_t *stage_d = nullptr;      // device staging for batch setters
+  int32_t *stage_d = nullptr;        // device staging for batch setters
   int stage_cap = 0;
+  uint8_t *stage_dir_d = nullptr;    // device staging for lane-direction setters
   void *pinned = nullptr;
   size_t pinned_cap = 0;
   cudaEvent_t stage_ev = nullptr;
   int smem = 0;
-  int32_t *lanestat_d = nullptr;
   // device timing windows (sim_enable_timing / sim_read_timing)
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -117,6 +186,16 @@ sim_status fail(sim_s *h, sim_status st, const std::string &m) {
     if (e_ != cudaSuccess) {                                                        \
       (h)->sticky = SIM_E_CUDA;                                                     \
       return fail((h), SIM_E_CUDA, std::string("CUDA: ") + cudaGetErrorString(e_) + \
+                                       " at " + #x);                                \
+    }                                                                               \
+  } while (0)
+
+#define NK(h, x)                                                                    \
+  do {                                                                              \
+    int r_ = (x);                                                                   \
+    if (r_ != 0) {                                                                  \
+      (h)->sticky = SIM_E_NCCL;                                                     \
+      return fail((h), SIM_E_NCCL, std::string("NCCL: ") + g_nccl.GetErrorString(r_) + \
                                        " at " + #x);                                \
     }                                                                               \
   } while (0)
@@ -422,9 +501,100 @@ void init_junctions(sim_s *h, HostState &S) {
   }
 }
 
+
 int route_at(const sim_s *h, int vid, int idx) {
   int a = h->route_off[vid], n = h->route_off[vid + 1] - a;
   return (idx >= 0 && idx < n) ? h->route[a + idx] : -1;
+}
+
+// ---- partitioning ---------------------------------------------
+// Default partitioner: breadth-first order of the roads over the undirected
+// road adjacency (deterministic, from road 0, ties by id), cut into `world`
+// contiguous chunks of equal slot capacity.  Callers with coordinates can pass
+// their own road_owner (bench.py uses recursive coordinate bisection).
+std::vector<int> default_partition(const sim_s *h, int world) {
+  std::vector<std::vector<int>> adj(h->nr);
+  for (int l = 0; l < h->nl; ++l) {
+    if (!is_road(h, l)) continue;
+    for (int e = h->succ_off[l]; e < h->succ_off[l + 1]; ++e) {
+      int r1 = h->road[l], r2 = h->target_road[h->succ[e]];
+      if (r1 != r2) { adj[r1].push_back(r2); adj[r2].push_back(r1); }
+    }
+  }
+  for (auto &a : adj) { std::sort(a.begin(), a.end()); a.erase(std::unique(a.begin(), a.end()), a.end()); }
+  std::vector<int> order;
+  std::vector<char> seen(h->nr, 0);
+  for (int s = 0; s < h->nr; ++s) {
+    if (seen[s]) continue;
+    std::deque<int> q{s};
+    seen[s] = 1;
+    while (!q.empty()) {
+      int r = q.front(); q.pop_front();
+      order.push_back(r);
+      for (int x : adj[r]) if (!seen[x]) { seen[x] = 1; q.push_back(x); }
+    }
+  }
+  int64_t tot = 0;
+  for (int r = 0; r < h->nr; ++r) tot += h->tile_cap[r];
+  std::vector<int> owner(h->nr, 0);
+  int64_t acc = 0;
+  for (int r : order) {
+    owner[r] = (int)std::min<int64_t>(world - 1, (acc * world) / std::max<int64_t>(tot, 1));
+    acc += h->tile_cap[r];
+  }
+  return owner;
+}
+
+// Exchange plan: migrant capacities and halo lane lists for every ordered pair.
+struct Plan {
+  std::vector<std::vector<int>> mig_cap;             // [from][to]
+  std::vector<std::vector<std::vector<int>>> halo;   // [reader][owner] sorted lanes
+};
+
+Plan make_plan(const sim_s *h) {
+  const int W = h->world;
+  Plan P;
+  P.mig_cap.assign(W, std::vector<int>(W, 0));
+  P.halo.assign(W, std::vector<std::vector<int>>(W));
+  float lmin = 1e30f, acap = 0, vcap = 0;
+  for (auto &q : h->profs) { lmin = std::min(lmin, q.len); acap = std::max(acap, q.a_max); }
+  for (int l = 0; l < h->nl; ++l) vcap = std::max(vcap, h->vmax[l]);
+  const int reach = (int)std::ceil((vcap + acap) / lmin) + 2;   // vehicles within one step of a lane end
+  auto owner_of = [&](int l) { return h->tile_owner[h->lane_tile[l]]; };
+  for (int l = 0; l < h->nl; ++l) {
+    const int a = owner_of(l);
+    for (int e = h->succ_off[l]; e < h->succ_off[l + 1]; ++e) {
+      const int y = h->succ[e], b = owner_of(y);
+      if (a == b) continue;
+      // a vehicle can leave through y only from l (or from l's predecessor road
+      // lane in the same step when l is a short junction lane)
+      int c = (int)std::floor(h->L[l] / lmin) + 2 + reach;
+      P.mig_cap[a][b] += c;
+    }
+  }
+  for (int a = 0; a < W; ++a)
+    for (int b = 0; b < W; ++b)
+      if (P.mig_cap[a][b]) P.mig_cap[a][b] = 2 * P.mig_cap[a][b] + 64;
+  // halo: lanes within `lookahead` successor hops of a lane owned by the reader
+  const int K = std::max(h->P.lookahead_lanes, 1);
+  std::vector<std::set<int>> need(W);
+  for (int l = 0; l < h->nl; ++l) {
+    const int a = owner_of(l);
+    std::vector<int> front{l};
+    for (int hop = 0; hop < K; ++hop) {
+      std::vector<int> nxt;
+      for (int x : front)
+        for (int e = h->succ_off[x]; e < h->succ_off[x + 1]; ++e) {
+          int y = h->succ[e];
+          nxt.push_back(y);
+          if (owner_of(y) != a) need[a].insert(y);
+        }
+      front.swap(nxt);
+    }
+  }
+  for (int a = 0; a < W; ++a)
+    for (int y : need[a]) P.halo[a][owner_of(y)].push_back(y);
+  return P;
 }
 
 sim_status push_staging(sim_s *h, const void *src, size_t bytes, void *dst) {
@@ -443,17 +613,15 @@ sim_status push_staging(sim_s *h, const void *src, size_t bytes, void *dst) {
   return SIM_OK;
 }
 
-// Upload a full state (canonical: stayer slabs sorted per lane, empty inboxes).
+// Upload a full state (canonical: stayer slabs sorted per lane, empty inboxes)
+// into every partition; each keeps the vehicles of its own tiles, all other
+// state (summaries, cold arrays, signals, queues) is replicated.
 sim_status upload_state(sim_s *h, const HostState &S) {
   const int nv = h->nv, nt = h->nt, t = S.t;
   const int par = t & 1;
   h->t = t;
   h->dir = S.dir;
   compute_usable(h);
-  CK(h, cudaMemcpyAsync(h->usable_d, h->usable.data(), h->nl, cudaMemcpyHostToDevice, h->stream));
-  CK(h, cudaMemcpyAsync(h->outroads_d, h->outroads.data(), h->outroads.size() * 4,
-                        cudaMemcpyHostToDevice, h->stream));
-  // slabs
   std::vector<std::vector<int>> per_tile(nt);
   for (int k = 0; k < nv; ++k)
     if (S.status[k] == ST_DRIVING) {
@@ -461,9 +629,9 @@ sim_status upload_state(sim_s *h, const HostState &S) {
       if (l < 0 || l >= h->nl) return fail(h, SIM_E_RANGE, "lane out of range for driving vehicle " + std::to_string(k));
       per_tile[h->lane_tile[l]].push_back(k);
     }
-  std::vector<float> s(h->sum_cap), v(h->sum_cap);
-  std::vector<int> vid(h->sum_cap), nx(h->sum_cap), nx2(h->sum_cap), wt(h->sum_cap);
-  std::vector<uint32_t> meta(h->sum_cap);
+  std::vector<float> s(h->sum_cap, 0.f), v(h->sum_cap, 0.f);
+  std::vector<int> vid(h->sum_cap, 0), nx(h->sum_cap, 0), nx2(h->sum_cap, 0), wt(h->sum_cap, 0);
+  std::vector<uint32_t> meta(h->sum_cap, 0);
   std::vector<int> cnt(nt, 0);
   std::vector<unsigned long long> summ(h->nl, kEmptyKey);
   std::vector<float> pubv(nv, 0.f);
@@ -493,28 +661,12 @@ sim_status upload_state(sim_s *h, const HostState &S) {
     }
     cnt[T] = (int)ks.size();
   }
-  Slab &o = h->slab[par];
-  CK(h, cudaMemcpyAsync(o.s, s.data(), s.size() * 4, cudaMemcpyHostToDevice, h->stream));
-  CK(h, cudaMemcpyAsync(o.v, v.data(), v.size() * 4, cudaMemcpyHostToDevice, h->stream));
-  CK(h, cudaMemcpyAsync(o.vid, vid.data(), vid.size() * 4, cudaMemcpyHostToDevice, h->stream));
-  CK(h, cudaMemcpyAsync(o.nxt, nx.data(), nx.size() * 4, cudaMemcpyHostToDevice, h->stream));
-  CK(h, cudaMemcpyAsync(o.nxt2, nx2.data(), nx2.size() * 4, cudaMemcpyHostToDevice, h->stream));
-  CK(h, cudaMemcpyAsync(o.meta, meta.data(), meta.size() * 4, cudaMemcpyHostToDevice, h->stream));
-  CK(h, cudaMemcpyAsync(o.wait, wt.data(), wt.size() * 4, cudaMemcpyHostToDevice, h->stream));
-  CK(h, cudaMemcpyAsync(h->cnt[par], cnt.data(), nt * 4, cudaMemcpyHostToDevice, h->stream));
-  CK(h, cudaMemsetAsync(h->icnt[0], 0, nt * 4, h->stream));
-  CK(h, cudaMemsetAsync(h->icnt[1], 0, nt * 4, h->stream));
-  CK(h, cudaMemcpyAsync(h->summ[t % 3], summ.data(), h->nl * 8, cudaMemcpyHostToDevice, h->stream));
-  launch_fill_u64(h->summ[(t + 1) % 3], kEmptyKey, h->nl, h->stream);
-  launch_fill_u64(h->summ[(t + 2) % 3], kEmptyKey, h->nl, h->stream);
-  CK(h, cudaMemcpyAsync(h->pubv[par], pubv.data(), nv * 4, cudaMemcpyHostToDevice, h->stream));
-  // cold arrays
   std::vector<int> wfin(nv, 0);
-  for (int k = 0; k < nv; ++k) wfin[k] = S.status[k] == ST_FINISHED ? S.wait[k] : 0;
-  CK(h, cudaMemcpyAsync(h->A.status, S.status.data(), nv, cudaMemcpyHostToDevice, h->stream));
-  CK(h, cudaMemcpyAsync(h->A.insert_time, S.insert_time.data(), nv * 4, cudaMemcpyHostToDevice, h->stream));
-  CK(h, cudaMemcpyAsync(h->A.arrive_time, S.arrive_time.data(), nv * 4, cudaMemcpyHostToDevice, h->stream));
-  CK(h, cudaMemcpyAsync(h->A.wait_fin, wfin.data(), nv * 4, cudaMemcpyHostToDevice, h->stream));
+  h->fin0 = 0;
+  for (int k = 0; k < nv; ++k) {
+    wfin[k] = S.status[k] == ST_FINISHED ? S.wait[k] : 0;
+    h->fin0 += S.status[k] == ST_FINISHED;
+  }
   // pending queues per start lane sorted by (depart, vid) (ledger L25)
   std::vector<std::vector<int>> pq(h->nl);
   for (int k = 0; k < nv; ++k)
@@ -528,29 +680,62 @@ sim_status upload_state(sim_s *h, const HostState &S) {
     pvid.insert(pvid.end(), pq[l].begin(), pq[l].end());
   }
   std::vector<int> head(poff.begin(), poff.end() - 1);
-  CK(h, cudaMemcpyAsync(h->pend_off_d, poff.data(), poff.size() * 4, cudaMemcpyHostToDevice, h->stream));
-  if (!pvid.empty())
-    CK(h, cudaMemcpyAsync(h->pend_vid_d, pvid.data(), pvid.size() * 4, cudaMemcpyHostToDevice, h->stream));
-  CK(h, cudaMemcpyAsync(h->pend_head_d, head.data(), head.size() * 4, cudaMemcpyHostToDevice, h->stream));
-  // junctions
-  if (h->nj) {
-    std::vector<int> req(h->nj, -1);
-    CK(h, cudaMemcpyAsync(h->SG.policy, S.jpol.data(), h->nj, cudaMemcpyHostToDevice, h->stream));
-    CK(h, cudaMemcpyAsync(h->SG.phase, S.jphase.data(), h->nj * 4, cudaMemcpyHostToDevice, h->stream));
-    CK(h, cudaMemcpyAsync(h->SG.elapsed, S.jel.data(), h->nj * 4, cudaMemcpyHostToDevice, h->stream));
-    CK(h, cudaMemcpyAsync(h->SG.yellow_left, S.jy.data(), h->nj * 4, cudaMemcpyHostToDevice, h->stream));
-    CK(h, cudaMemcpyAsync(h->SG.pending, S.jpend.data(), h->nj * 4, cudaMemcpyHostToDevice, h->stream));
-    CK(h, cudaMemcpyAsync(h->SG.request, req.data(), h->nj * 4, cudaMemcpyHostToDevice, h->stream));
+  std::vector<int> req(h->nj, -1);
+  for (Part &P : h->parts) {
+    cudaStream_t st = h->stream;
+    std::vector<int> pc(nt, 0);
+    for (int T : P.tiles) pc[T] = cnt[T];
+    CK(h, cudaMemcpyAsync(P.usable_d, h->usable.data(), h->nl, cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(P.outroads_d, h->outroads.data(), h->outroads.size() * 4, cudaMemcpyHostToDevice, st));
+    Slab &o = P.slab[par];
+    CK(h, cudaMemcpyAsync(o.s, s.data(), s.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(o.v, v.data(), v.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(o.vid, vid.data(), vid.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(o.nxt, nx.data(), nx.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(o.nxt2, nx2.data(), nx2.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(o.meta, meta.data(), meta.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(o.wait, wt.data(), wt.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(P.cnt[par], pc.data(), nt * 4, cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemsetAsync(P.icnt[0], 0, nt * 4, st));
+    CK(h, cudaMemsetAsync(P.icnt[1], 0, nt * 4, st));
+    CK(h, cudaMemcpyAsync(P.summ[t % 3], summ.data(), h->nl * 8, cudaMemcpyHostToDevice, st));
+    launch_fill_u64(P.summ[(t + 1) % 3], kEmptyKey, h->nl, st);
+    launch_fill_u64(P.summ[(t + 2) % 3], kEmptyKey, h->nl, st);
+    CK(h, cudaMemcpyAsync(P.pubv[par], pubv.data(), nv * 4, cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(P.A.status, S.status.data(), nv, cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(P.A.insert_time, S.insert_time.data(), nv * 4, cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(P.A.arrive_time, S.arrive_time.data(), nv * 4, cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(P.A.wait_fin, wfin.data(), nv * 4, cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(P.pend_off_d, poff.data(), poff.size() * 4, cudaMemcpyHostToDevice, st));
+    if (!pvid.empty())
+      CK(h, cudaMemcpyAsync(P.pend_vid_d, pvid.data(), pvid.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(P.pend_head_d, head.data(), head.size() * 4, cudaMemcpyHostToDevice, st));
+    if (h->nj) {
+      CK(h, cudaMemcpyAsync(P.SG.policy, S.jpol.data(), h->nj, cudaMemcpyHostToDevice, st));
+      CK(h, cudaMemcpyAsync(P.SG.phase, S.jphase.data(), h->nj * 4, cudaMemcpyHostToDevice, st));
+      CK(h, cudaMemcpyAsync(P.SG.elapsed, S.jel.data(), h->nj * 4, cudaMemcpyHostToDevice, st));
+      CK(h, cudaMemcpyAsync(P.SG.yellow_left, S.jy.data(), h->nj * 4, cudaMemcpyHostToDevice, st));
+      CK(h, cudaMemcpyAsync(P.SG.pending, S.jpend.data(), h->nj * 4, cudaMemcpyHostToDevice, st));
+      CK(h, cudaMemcpyAsync(P.SG.request, req.data(), h->nj * 4, cudaMemcpyHostToDevice, st));
+    }
+    if (P.out_cnt) CK(h, cudaMemsetAsync(P.out_cnt, 0, h->world * 4, st));
   }
   CK(h, cudaStreamSynchronize(h->stream));   // host vectors die at return
+  // counters keep accumulating across loads: remember the finished baseline
+  h->acc_fin0 = 0;
+  for (Part &P : h->parts) {
+    std::vector<long long> ta((size_t)nt * kNAcc);
+    CK(h, cudaMemcpy(ta.data(), P.A.tacc, ta.size() * 8, cudaMemcpyDeviceToHost));
+    for (int T = 0; T < nt; ++T) h->acc_fin0 += ta[(size_t)T * kNAcc + ACC_FINISHED];
+  }
   return SIM_OK;
 }
 
-sim_status alloc_all(sim_s *h) {
+sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   sim_status st;
 #define AL(p, n) if ((st = dalloc(h, &(p), (n)))) return st
 #define UP(p, v) if ((st = upload(h, &(p), (v)))) return st
-  StepArgs &A = h->A;
+  StepArgs &A = P.A;
   const int nl = h->nl, nv = h->nv, nt = h->nt;
   float *f; int32_t *i32;
   UP(f, h->L); A.lane_len = f;
@@ -562,9 +747,8 @@ sim_status alloc_all(sim_s *h) {
   UP(i32, h->succ); A.succ = i32;
   UP(i32, h->target_road); A.target_road = i32;
   UP(i32, h->exit_lane); A.exit_lane = i32;
-  AL(h->usable_d, nl); A.usable = h->usable_d;
-  AL(h->stage_dir_d, 17 * (size_t)nl);
-  AL(h->outroads_d, 4 * (size_t)nl); A.outroads = reinterpret_cast<const int4 *>(h->outroads_d);
+  AL(P.usable_d, nl); A.usable = P.usable_d;
+  AL(P.outroads_d, 4 * (size_t)nl); A.outroads = reinterpret_cast<const int4 *>(P.outroads_d);
   uint8_t *sig; AL(sig, nl);
   CK(h, cudaMemset(sig, 0, nl));
   A.lane_sig = sig;
@@ -577,24 +761,28 @@ sim_status alloc_all(sim_s *h) {
   UP(i32, h->tile_cap); A.tile_cap = i32;
   UP(i32, h->tile_ibase); A.tile_ibase = i32;
   UP(i32, h->tile_icap); A.tile_icap = i32;
+  UP(i32, h->tile_owner); A.tile_owner = i32;
+  UP(i32, P.tiles); A.tiles = i32;
+  A.n_own = (int)P.tiles.size();
+  A.rank = P.rank;
   for (int b = 0; b < 2; ++b) {
-    Slab &s = h->slab[b];
+    Slab &s = P.slab[b];
     AL(s.s, h->sum_cap); AL(s.v, h->sum_cap); AL(s.vid, h->sum_cap); AL(s.nxt, h->sum_cap);
     AL(s.nxt2, h->sum_cap); AL(s.meta, h->sum_cap); AL(s.wait, h->sum_cap);
-    AL(h->inbox[b], h->sum_icap);
-    AL(h->cnt[b], nt); AL(h->icnt[b], nt);
-    AL(h->pubv[b], nv);
-    CK(h, cudaMemset(h->cnt[b], 0, nt * 4));
-    CK(h, cudaMemset(h->icnt[b], 0, nt * 4));
+    AL(P.inbox[b], h->sum_icap);
+    AL(P.cnt[b], nt); AL(P.icnt[b], nt);
+    AL(P.pubv[b], nv);
+    CK(h, cudaMemset(P.cnt[b], 0, nt * 4));
+    CK(h, cudaMemset(P.icnt[b], 0, nt * 4));
+    CK(h, cudaMemset(P.pubv[b], 0, nv * 4));
   }
   const int64_t sc = h->sum_cap + h->sum_icap;
   Slab &sc_ = A.scratch;
   AL(sc_.s, sc); AL(sc_.v, sc); AL(sc_.vid, sc); AL(sc_.nxt, sc); AL(sc_.nxt2, sc);
   AL(sc_.meta, sc); AL(sc_.wait, sc);
   AL(A.bsort_scratch, h->sum_icap);
-  AL(A.rs_s1, sc); AL(A.rs_v1, sc); AL(A.rs_lane, sc); AL(A.rs_wait, sc); AL(A.rs_cur, sc);
-  AL(A.rs_glist, sc); AL(A.rs_flags, sc);
-  for (int b = 0; b < 3; ++b) AL(h->summ[b], nl);
+  AL(A.rs_s1, sc); AL(A.rs_flags, sc);
+  for (int b = 0; b < 3; ++b) AL(P.summ[b], nl);
   UP(i32, h->route_off); A.route_off = i32;
   UP(i32, h->route); A.route = i32;
   UP(f, h->end_s); A.end_s = f;
@@ -602,20 +790,56 @@ sim_status alloc_all(sim_s *h) {
   AL(A.insert_time, nv); AL(A.arrive_time, nv); AL(A.wait_fin, nv); AL(A.status, nv);
   UP(i32, h->depart); A.depart = i32;
   UP(f, h->start_s); A.start_s = f;
-  AL(h->pend_off_d, nl + 1); AL(h->pend_vid_d, nv); AL(h->pend_head_d, nl);
-  A.pend_off = h->pend_off_d; A.pend_vid = h->pend_vid_d; A.pend_head = h->pend_head_d;
+  AL(P.pend_off_d, nl + 1); AL(P.pend_vid_d, nv); AL(P.pend_head_d, nl);
+  A.pend_off = P.pend_off_d; A.pend_vid = P.pend_vid_d; A.pend_head = P.pend_head_d;
   Prof *pr; UP(pr, h->profs); A.prof = pr;
   AL(A.tacc, (size_t)nt * kNAcc);
   CK(h, cudaMemset(A.tacc, 0, (size_t)nt * kNAcc * 8));
-  AL(h->red_d, kNAcc + 3);
-  AL(h->lanestat_d, 2 * (size_t)nl);
+  AL(P.red_d, kNAcc + 3);
+  AL(P.lanestat_d, 2 * (size_t)nl);
   if (h->P.record_decisions) {
     AL(A.r_leader, nv); AL(A.r_of, nv); AL(A.r_side, 4 * (size_t)nv);
     AL(A.r_hops, nv); AL(A.r_phantom, nv); AL(A.r_lc, nv); AL(A.r_hand, nv);
-    AL(A.r_fin, nv); AL(A.r_ins, nv); AL(A.r_acc, nv); AL(A.r_guard, nv);
+    AL(A.r_fin, nv); AL(A.r_ins, nv); AL(A.r_acc, nv); AL(A.r_guard, nv); AL(A.r_mark, nv);
   }
-  // signals
-  SignalArgs &G = h->SG;
+  // exchange buffers
+  const int W = h->world;
+  if (W > 1 && plan) {
+    P.out_off.assign(W + 1, 0); P.out_cap.assign(W, 0);
+    P.in_off.assign(W + 1, 0); P.in_cap.assign(W, 0);
+    for (int q = 0; q < W; ++q) {
+      P.out_cap[q] = plan->mig_cap[P.rank][q];
+      P.in_cap[q] = plan->mig_cap[q][P.rank];
+      P.out_off[q + 1] = P.out_off[q] + (P.out_cap[q] ? P.out_cap[q] + 1 : 0);
+      P.in_off[q + 1] = P.in_off[q] + (P.in_cap[q] ? P.in_cap[q] + 1 : 0);
+    }
+    P.out_n = P.out_off[W]; P.in_n = P.in_off[W];
+    AL(P.out_buf, P.out_n); AL(P.in_buf, P.in_n); AL(P.out_cnt, W);
+    CK(h, cudaMemset(P.out_cnt, 0, W * 4));
+    CK(h, cudaMemset(P.in_buf, 0, std::max<int64_t>(P.in_n, 1) * sizeof(MigRec)));
+    std::vector<int> off(P.out_off.begin(), P.out_off.end() - 1);
+    UP(i32, off); A.out_off = i32;
+    UP(i32, P.out_cap); A.out_cap = i32;
+    std::vector<int> ioff(P.in_off.begin(), P.in_off.end() - 1);
+    UP(P.in_off_d, ioff);
+    UP(P.in_cap_d, P.in_cap);
+    A.out_buf = P.out_buf; A.out_cnt = P.out_cnt;
+    std::vector<int> hs, hr;
+    P.hs_off.assign(W + 1, 0); P.hr_off.assign(W + 1, 0);
+    for (int q = 0; q < W; ++q) {
+      const auto &snd = plan->halo[q][P.rank];      // lanes peer q reads from us
+      const auto &rcv = plan->halo[P.rank][q];      // lanes we read from q
+      hs.insert(hs.end(), snd.begin(), snd.end());
+      hr.insert(hr.end(), rcv.begin(), rcv.end());
+      P.hs_off[q + 1] = (int)hs.size();
+      P.hr_off[q + 1] = (int)hr.size();
+    }
+    P.hs_n = (int64_t)hs.size(); P.hr_n = (int64_t)hr.size();
+    UP(P.hs_lanes, hs); UP(P.hr_lanes, hr);
+    AL(P.hs_buf, P.hs_n); AL(P.hr_buf, P.hr_n);
+  }
+  // signals (replicated: every partition runs every junction's controller)
+  SignalArgs &G = P.SG;
   G.n_junctions = h->nj; G.yellow = h->Y;
   AL(G.policy, h->nj); AL(G.phase, h->nj); AL(G.elapsed, h->nj); AL(G.yellow_left, h->nj);
   AL(G.pending, h->nj); AL(G.request, h->nj);
@@ -623,7 +847,7 @@ sim_status alloc_all(sim_s *h) {
   UP(i32, h->jl); G.jl = i32;
   UP(i32, h->ph_off); G.ph_off = i32;
   int64_t *g64; UP(g64, h->green_off); G.green_off = g64;
-  const uint8_t *cu8; UP(u8, h->green); cu8 = u8; G.green = cu8;
+  UP(u8, h->green); G.green = u8;
   UP(i32, h->green_steps); G.green_steps = i32;
   G.lane_sig = sig;
   // constants
@@ -635,30 +859,28 @@ sim_status alloc_all(sim_s *h) {
   A.exact_mode = h->P.exact_mode;
   A.record = h->P.record_decisions;
   A.n_prof = (int)h->profs.size();
-  CK(h, cudaEventCreateWithFlags(&h->stage_ev, cudaEventDisableTiming));
-  CK(h, cudaEventRecord(h->stage_ev, h->stream));
   return SIM_OK;
 #undef AL
 #undef UP
 }
 
-StepArgs step_args(sim_s *h, int t) {
-  StepArgs a = h->A;
+StepArgs step_args(const Part &P, int t) {
+  StepArgs a = P.A;
   const int par = t & 1;
   a.t = t;
-  a.in = h->slab[par];
-  a.out = h->slab[par ^ 1];
-  a.cnt_in = h->cnt[par];
-  a.cnt_out = h->cnt[par ^ 1];
-  a.icnt_in = h->icnt[par];
-  a.icnt_out = h->icnt[par ^ 1];
-  a.inbox_in = h->inbox[par];
-  a.inbox_out = h->inbox[par ^ 1];
-  a.summ_cur = h->summ[t % 3];
-  a.summ_next = h->summ[(t + 1) % 3];
-  a.summ_clear = h->summ[(t + 2) % 3];
-  a.pubv_cur = h->pubv[par];
-  a.pubv_next = h->pubv[par ^ 1];
+  a.in = P.slab[par];
+  a.out = P.slab[par ^ 1];
+  a.cnt_in = P.cnt[par];
+  a.cnt_out = P.cnt[par ^ 1];
+  a.icnt_in = P.icnt[par];
+  a.icnt_out = P.icnt[par ^ 1];
+  a.inbox_in = P.inbox[par];
+  a.inbox_out = P.inbox[par ^ 1];
+  a.summ_cur = P.summ[t % 3];
+  a.summ_next = P.summ[(t + 1) % 3];
+  a.summ_clear = P.summ[(t + 2) % 3];
+  a.pubv_cur = P.pubv[par];
+  a.pubv_next = P.pubv[par ^ 1];
   return a;
 }
 
@@ -677,18 +899,123 @@ sim_status device_check(sim_s *h) {
   return SIM_OK;
 }
 
+// Global int64 counters: per-partition reduction, summed over loopback
+// partitions / ncclAllReduce'd over ranks.
 sim_status read_counters(sim_s *h, std::vector<long long> &out) {
-  StepArgs a = step_args(h, h->t);
-  launch_reduce_acc(h->A.tacc, h->nt, a.cnt_in, a.icnt_in, h->A.status, h->nv, h->red_d, h->stream);
-  h->n_launch += 1;
   out.assign(kNAcc + 3, 0);
-  CK(h, cudaMemcpyAsync(out.data(), h->red_d, (kNAcc + 3) * 8, cudaMemcpyDeviceToHost, h->stream));
-  sim_status st = device_check(h);
-  if (st) return st;
+  for (Part &P : h->parts) {
+    StepArgs a = step_args(P, h->t);
+    launch_reduce_acc(P.A.tacc, h->nt, a.cnt_in, a.icnt_in, P.A.status, 0, P.red_d, h->stream);
+    h->n_launch += 1;
+  }
+  if (h->comm) {
+    Part &P = h->parts[0];
+    NK(h, g_nccl.AllReduce(P.red_d, P.red_d, kNAcc + 3, kNcclInt64, kNcclSum, h->comm, h->stream));
+  }
+  std::vector<long long> tmp(kNAcc + 3);
+  for (Part &P : h->parts) {
+    CK(h, cudaMemcpyAsync(tmp.data(), P.red_d, (kNAcc + 3) * 8, cudaMemcpyDeviceToHost, h->stream));
+    sim_status st = device_check(h);
+    if (st) return st;
+    for (int c = 0; c < kNAcc + 3; ++c) out[c] += tmp[c];
+  }
   if (out[ACC_OVERFLOW] > 0) {
     h->sticky = SIM_E_CAPACITY;
-    return fail(h, SIM_E_CAPACITY, "a road tile inbox overflowed its capacity");
+    return fail(h, SIM_E_CAPACITY, "a road-tile inbox or a migration buffer overflowed its capacity");
   }
+  return SIM_OK;
+}
+
+// One step of every partition + the exchanges.
+sim_status step_once(sim_s *h) {
+  const int t = h->t, W = h->world;
+  cudaStream_t st = h->stream;
+  for (Part &P : h->parts) {
+    if (h->P.record_decisions) {
+      CK(h, cudaMemsetAsync(P.A.r_ins, 0, h->nv, st));
+      CK(h, cudaMemsetAsync(P.A.r_mark, 0, h->nv, st));
+      CK(h, cudaMemsetAsync(P.A.r_leader, 0xff, h->nv * 4, st));
+      CK(h, cudaMemsetAsync(P.A.r_lc, 0, h->nv, st));
+    }
+  }
+  cudaEvent_t e[3] = {nullptr, nullptr, nullptr};
+  if (h->timing) {
+    while (h->ev_pool.size() < h->ev_used + 3) {
+      cudaEvent_t ev;
+      CK(h, cudaEventCreate(&ev));
+      h->ev_pool.push_back(ev);
+    }
+    for (int q = 0; q < 3; ++q) e[q] = h->ev_pool[h->ev_used + q];
+    h->ev_used += 3;
+    CK(h, cudaEventRecord(e[0], st));
+  }
+  for (Part &P : h->parts) { launch_signal(P.SG, st); h->n_launch += h->nj > 0; }
+  if (h->timing) CK(h, cudaEventRecord(e[1], st));
+  for (Part &P : h->parts) {
+    StepArgs a = step_args(P, t);
+    launch_step(a, st, h->smem);
+    h->n_launch += a.n_own > 0;
+  }
+  if (h->timing) CK(h, cudaEventRecord(e[2], st));
+  if (W > 1) {
+    // 1. migration: headers carry the counts, whole regions are exchanged
+    for (Part &P : h->parts) { launch_mig_header(P.out_buf, P.A.out_off, P.A.out_cap, P.out_cnt, W, st); h->n_launch++; }
+    if (h->loopback) {
+      for (Part &P : h->parts)
+        for (int q = 0; q < W; ++q)
+          if (P.out_cap[q]) {
+            Part &Q = h->parts[q];
+            CK(h, cudaMemcpyAsync(Q.in_buf + Q.in_off[P.rank], P.out_buf + P.out_off[q],
+                                  (P.out_cap[q] + 1) * sizeof(MigRec), cudaMemcpyDeviceToDevice, st));
+          }
+    } else {
+      Part &P = h->parts[0];
+      NK(h, g_nccl.GroupStart());
+      for (int q = 0; q < W; ++q) {
+        if (P.out_cap[q])
+          NK(h, g_nccl.Send(P.out_buf + P.out_off[q], (P.out_cap[q] + 1) * sizeof(MigRec), kNcclInt8, q, h->comm, st));
+        if (P.in_cap[q])
+          NK(h, g_nccl.Recv(P.in_buf + P.in_off[q], (P.in_cap[q] + 1) * sizeof(MigRec), kNcclInt8, q, h->comm, st));
+      }
+      NK(h, g_nccl.GroupEnd());
+    }
+    for (Part &P : h->parts) {
+      StepArgs a = step_args(P, t);
+      launch_absorb(a, P.in_buf, P.in_off_d, P.in_cap_d, W, st);
+      h->n_launch++;
+    }
+    // 2. halo: the first-vehicle summaries of the lanes each peer reads
+    for (Part &P : h->parts) {
+      StepArgs a = step_args(P, t);
+      launch_halo_pack(a, P.hs_lanes, P.hs_buf, P.hs_n, st);
+      h->n_launch++;
+    }
+    if (h->loopback) {
+      for (Part &P : h->parts)
+        for (int q = 0; q < W; ++q) {
+          const int n = P.hs_off[q + 1] - P.hs_off[q];
+          if (!n) continue;
+          Part &Q = h->parts[q];
+          CK(h, cudaMemcpyAsync(Q.hr_buf + Q.hr_off[P.rank], P.hs_buf + P.hs_off[q], n * sizeof(HaloRec),
+                                cudaMemcpyDeviceToDevice, st));
+        }
+    } else {
+      Part &P = h->parts[0];
+      NK(h, g_nccl.GroupStart());
+      for (int q = 0; q < W; ++q) {
+        const int ns = P.hs_off[q + 1] - P.hs_off[q], nr = P.hr_off[q + 1] - P.hr_off[q];
+        if (ns) NK(h, g_nccl.Send(P.hs_buf + P.hs_off[q], ns * sizeof(HaloRec), kNcclInt8, q, h->comm, st));
+        if (nr) NK(h, g_nccl.Recv(P.hr_buf + P.hr_off[q], nr * sizeof(HaloRec), kNcclInt8, q, h->comm, st));
+      }
+      NK(h, g_nccl.GroupEnd());
+    }
+    for (Part &P : h->parts) {
+      StepArgs a = step_args(P, t);
+      launch_halo_unpack(a, P.hr_lanes, P.hr_buf, P.hr_n, st);
+      h->n_launch++;
+    }
+  }
+  h->t += 1;
   return SIM_OK;
 }
 
@@ -703,8 +1030,19 @@ static void destroy_impl(sim_s *h) {
   if (h->pinned) cudaFreeHost(h->pinned);
   if (h->stage_ev) cudaEventDestroy(h->stage_ev);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+  if (h->comm) g_nccl.CommDestroy(h->comm);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
+}
+
+sim_status sim_get_nccl_unique_id(uint8_t out[128]) {
+  std::string err;
+  if (!g_nccl.load(err)) return fail(nullptr, SIM_E_NCCL, err);
+  NcclId id;
+  int r = g_nccl.GetUniqueId(&id);
+  if (r) return fail(nullptr, SIM_E_NCCL, std::string("ncclGetUniqueId: ") + g_nccl.GetErrorString(r));
+  std::memcpy(out, id.internal, 128);
+  return SIM_OK;
 }
 
 sim_status sim_create(const sim_graph *g, const sim_trips *tr, const sim_params *p,
@@ -714,6 +1052,23 @@ sim_status sim_create(const sim_graph *g, const sim_trips *tr, const sim_params 
   sim_s *h = new sim_s();
   sim_status st = validate_and_copy(h, g, tr, p);
   if (!st) st = build_tiles(h);
+  if (!st) {
+    h->world = std::max(1, p->world);
+    h->rank = p->rank;
+    h->loopback = h->world > 1 && p->loopback;
+    if (h->world > 1 && !h->loopback && (!p->nccl_id || p->rank < 0 || p->rank >= h->world))
+      st = fail(h, SIM_E_INVALID, "world > 1 needs loopback = 1 or (nccl_id, 0 <= rank < world)");
+    if (h->world > 1 && h->nt < h->world) st = fail(h, SIM_E_INVALID, "fewer road tiles than partitions");
+  }
+  if (!st) {
+    if (p->road_owner) {
+      h->tile_owner.assign(p->road_owner, p->road_owner + h->nr);
+      for (int x : h->tile_owner)
+        if (x < 0 || x >= h->world) { st = fail(h, SIM_E_INVALID, "road_owner out of [0, world)"); break; }
+    } else {
+      h->tile_owner = h->world > 1 ? default_partition(h, h->world) : std::vector<int>(h->nr, 0);
+    }
+  }
   if (st) { g_create_err = h->err; delete h; return st; }
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -728,7 +1083,36 @@ sim_status sim_create(const sim_graph *g, const sim_trips *tr, const sim_params 
     h->own_stream = true;
   }
   h->smem = step_smem_bytes();
-  st = alloc_all(h);
+  Plan plan;
+  if (h->world > 1) plan = make_plan(h);
+  const int nparts = h->loopback ? h->world : 1;
+  h->parts.resize(nparts);
+  for (int i = 0; i < nparts && !st; ++i) {
+    Part &P = h->parts[i];
+    P.rank = h->loopback ? i : (h->world > 1 ? h->rank : 0);
+    for (int T = 0; T < h->nt; ++T) if (h->tile_owner[T] == P.rank) P.tiles.push_back(T);
+    st = alloc_part(h, P, h->world > 1 ? &plan : nullptr);
+  }
+  if (!st && h->world > 1 && !h->loopback) {
+    std::string err;
+    if (!g_nccl.load(err)) st = fail(h, SIM_E_NCCL, err);
+    else {
+      NcclId id;
+      std::memcpy(id.internal, p->nccl_id, 128);
+      int r = g_nccl.CommInitRank(&h->comm, h->world, id, h->rank);
+      if (r) st = fail(h, SIM_E_NCCL, std::string("ncclCommInitRank: ") + g_nccl.GetErrorString(r));
+    }
+  }
+  if (!st) {
+    cudaError_t e = cudaMalloc(&h->stage_dir_d, 17 * (size_t)h->nl);
+    if (e != cudaSuccess) st = fail(h, SIM_E_OOM, "cudaMalloc staging");
+    else h->allocs.push_back(h->stage_dir_d);
+  }
+  if (!st) {
+    if (cudaEventCreateWithFlags(&h->stage_ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventRecord(h->stage_ev, h->stream) != cudaSuccess)
+      st = fail(h, SIM_E_CUDA, "event creation failed");
+  }
   if (!st) {
     HostState S;
     S.t = 0;
@@ -763,29 +1147,8 @@ sim_status sim_step(sim_handle h, int32_t n) {
   if (st) return st;
   if (n < 0) return fail(h, SIM_E_RANGE, "n must be >= 0");
   for (int i = 0; i < n; ++i) {
-    StepArgs a = step_args(h, h->t);
-    if (h->A.record) {
-      CK(h, cudaMemsetAsync(h->A.r_ins, 0, h->nv, h->stream));
-      CK(h, cudaMemsetAsync(h->A.r_leader, 0xff, h->nv * 4, h->stream));
-      CK(h, cudaMemsetAsync(h->A.r_lc, 0, h->nv, h->stream));
-    }
-    cudaEvent_t e[3] = {nullptr, nullptr, nullptr};
-    if (h->timing) {
-      while (h->ev_pool.size() < h->ev_used + 3) {
-        cudaEvent_t ev;
-        CK(h, cudaEventCreate(&ev));
-        h->ev_pool.push_back(ev);
-      }
-      for (int q = 0; q < 3; ++q) e[q] = h->ev_pool[h->ev_used + q];
-      h->ev_used += 3;
-      CK(h, cudaEventRecord(e[0], h->stream));
-    }
-    launch_signal(h->SG, h->stream);
-    if (h->timing) CK(h, cudaEventRecord(e[1], h->stream));
-    launch_step(a, h->stream, h->smem);
-    if (h->timing) CK(h, cudaEventRecord(e[2], h->stream));
-    h->n_launch += (h->nj > 0 ? 1 : 0) + (h->nt > 0 ? 1 : 0);
-    h->t += 1;
+    st = step_once(h);
+    if (st) return st;
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -823,7 +1186,10 @@ sim_status sim_set_signal_phase_batch(sim_handle h, int32_t m, const int32_t *ju
   std::memcpy(buf.data() + m, phases, m * 4);
   st = push_staging(h, buf.data(), buf.size() * 4, h->stage_d);
   if (st) return st;
-  launch_apply_requests(h->SG.request, h->SG.policy, h->stage_d, h->stage_d + m, m, h->stream);
+  for (Part &P : h->parts) {           // replicated controllers: every partition applies it
+    launch_apply_requests(P.SG.request, P.SG.policy, h->stage_d, h->stage_d + m, m, h->stream);
+    h->n_launch++;
+  }
   return SIM_OK;
 }
 
@@ -850,16 +1216,18 @@ sim_status sim_set_lane_direction_batch(sim_handle h, int32_t m, const int32_t *
   }
   if (m == 0) return SIM_OK;
   compute_usable(h);
-  // one staging buffer: usable bytes followed by the outroads table
+  // one staging buffer: the outroads table followed by the usable bytes
   std::vector<uint8_t> buf((size_t)h->nl + h->outroads.size() * 4);
   std::memcpy(buf.data(), h->outroads.data(), h->outroads.size() * 4);
   std::memcpy(buf.data() + h->outroads.size() * 4, h->usable.data(), h->nl);
   st = push_staging(h, buf.data(), buf.size(), h->stage_dir_d);
   if (st) return st;
-  CK(h, cudaMemcpyAsync(h->outroads_d, h->stage_dir_d, h->outroads.size() * 4,
-                        cudaMemcpyDeviceToDevice, h->stream));
-  CK(h, cudaMemcpyAsync(h->usable_d, h->stage_dir_d + h->outroads.size() * 4, h->nl,
-                        cudaMemcpyDeviceToDevice, h->stream));
+  for (Part &P : h->parts) {
+    CK(h, cudaMemcpyAsync(P.outroads_d, h->stage_dir_d, h->outroads.size() * 4,
+                          cudaMemcpyDeviceToDevice, h->stream));
+    CK(h, cudaMemcpyAsync(P.usable_d, h->stage_dir_d + h->outroads.size() * 4, h->nl,
+                          cudaMemcpyDeviceToDevice, h->stream));
+  }
   return SIM_OK;
 }
 
@@ -875,6 +1243,9 @@ sim_status sim_query_sizes(sim_handle h, sim_sizes *out) {
   return SIM_OK;
 }
 
+// Vehicles on the tiles of the handle's partition(s) are read from the slabs /
+// inboxes; cold fields are merged over partitions (a vehicle's FINISHED record
+// lives on the partition where it arrived).
 sim_status sim_read_state(sim_handle h, sim_state *o) {
   sim_status st = check(h);
   if (st) return st;
@@ -883,58 +1254,67 @@ sim_status sim_read_state(sim_handle h, sim_state *o) {
   st = read_counters(h, cs);
   if (st) return st;
   const int par = h->t & 1, nv = h->nv, nt = h->nt;
-  std::vector<int> cnt(nt), icnt(nt);
-  CK(h, cudaMemcpy(cnt.data(), h->cnt[par], nt * 4, cudaMemcpyDeviceToHost));
-  CK(h, cudaMemcpy(icnt.data(), h->icnt[par], nt * 4, cudaMemcpyDeviceToHost));
-  const Slab &sl = h->slab[par];
-  std::vector<float> s(h->sum_cap), v(h->sum_cap);
-  std::vector<int> vid(h->sum_cap), wt(h->sum_cap);
-  std::vector<uint32_t> meta(h->sum_cap);
-  CK(h, cudaMemcpy(s.data(), sl.s, s.size() * 4, cudaMemcpyDeviceToHost));
-  CK(h, cudaMemcpy(v.data(), sl.v, v.size() * 4, cudaMemcpyDeviceToHost));
-  CK(h, cudaMemcpy(vid.data(), sl.vid, vid.size() * 4, cudaMemcpyDeviceToHost));
-  CK(h, cudaMemcpy(wt.data(), sl.wait, wt.size() * 4, cudaMemcpyDeviceToHost));
-  CK(h, cudaMemcpy(meta.data(), sl.meta, meta.size() * 4, cudaMemcpyDeviceToHost));
-  std::vector<InboxRec> ib(h->sum_icap);
-  CK(h, cudaMemcpy(ib.data(), h->inbox[par], ib.size() * sizeof(InboxRec), cudaMemcpyDeviceToHost));
-  std::vector<uint8_t> status(nv);
-  std::vector<int> ins(nv), arr(nv), wfin(nv);
-  CK(h, cudaMemcpy(status.data(), h->A.status, nv, cudaMemcpyDeviceToHost));
-  CK(h, cudaMemcpy(ins.data(), h->A.insert_time, nv * 4, cudaMemcpyDeviceToHost));
-  CK(h, cudaMemcpy(arr.data(), h->A.arrive_time, nv * 4, cudaMemcpyDeviceToHost));
-  CK(h, cudaMemcpy(wfin.data(), h->A.wait_fin, nv * 4, cudaMemcpyDeviceToHost));
-  std::vector<int> lane(nv, -1), cur(nv, 0), wait(nv, 0);
+  std::vector<int> lane(nv, -1), cur(nv, 0), wait(nv, 0), ins(nv, -1), arr(nv, -1);
   std::vector<float> vs(nv, 0.f), vv(nv, 0.f);
-  for (int k = 0; k < nv; ++k) if (status[k] == ST_FINISHED) wait[k] = wfin[k];
-  auto put = [&](int T, int k, float ss, float v_, uint32_t m, int w) {
-    lane[k] = h->tile_lanes[h->tile_lane_off[T] + (m & 0xff)];
-    vs[k] = ss; vv[k] = v_; cur[k] = (int)(m >> 16); wait[k] = w;
-  };
-  for (int T = 0; T < nt; ++T) {
-    for (int i = 0; i < cnt[T]; ++i) { int p = h->tile_base[T] + i; put(T, vid[p], s[p], v[p], meta[p], wt[p]); }
-    for (int i = 0; i < icnt[T]; ++i) { const InboxRec &r = ib[h->tile_ibase[T] + i]; put(T, r.vid, r.s, r.v, r.meta, r.wait); }
+  std::vector<uint8_t> status(nv, ST_PENDING);
+  std::vector<char> driving(nv, 0);
+  for (Part &P : h->parts) {
+    std::vector<int> cnt(nt), icnt(nt);
+    CK(h, cudaMemcpy(cnt.data(), P.cnt[par], nt * 4, cudaMemcpyDeviceToHost));
+    CK(h, cudaMemcpy(icnt.data(), P.icnt[par], nt * 4, cudaMemcpyDeviceToHost));
+    const Slab &sl = P.slab[par];
+    std::vector<float> s(h->sum_cap), v(h->sum_cap);
+    std::vector<int> vid(h->sum_cap), wt(h->sum_cap);
+    std::vector<uint32_t> meta(h->sum_cap);
+    CK(h, cudaMemcpy(s.data(), sl.s, s.size() * 4, cudaMemcpyDeviceToHost));
+    CK(h, cudaMemcpy(v.data(), sl.v, v.size() * 4, cudaMemcpyDeviceToHost));
+    CK(h, cudaMemcpy(vid.data(), sl.vid, vid.size() * 4, cudaMemcpyDeviceToHost));
+    CK(h, cudaMemcpy(wt.data(), sl.wait, wt.size() * 4, cudaMemcpyDeviceToHost));
+    CK(h, cudaMemcpy(meta.data(), sl.meta, meta.size() * 4, cudaMemcpyDeviceToHost));
+    std::vector<InboxRec> ib(h->sum_icap);
+    CK(h, cudaMemcpy(ib.data(), P.inbox[par], ib.size() * sizeof(InboxRec), cudaMemcpyDeviceToHost));
+    std::vector<uint8_t> pst(nv);
+    std::vector<int> pins(nv), parr(nv), pwf(nv);
+    CK(h, cudaMemcpy(pst.data(), P.A.status, nv, cudaMemcpyDeviceToHost));
+    CK(h, cudaMemcpy(pins.data(), P.A.insert_time, nv * 4, cudaMemcpyDeviceToHost));
+    CK(h, cudaMemcpy(parr.data(), P.A.arrive_time, nv * 4, cudaMemcpyDeviceToHost));
+    CK(h, cudaMemcpy(pwf.data(), P.A.wait_fin, nv * 4, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < nv; ++k) {
+      ins[k] = std::max(ins[k], pins[k]);
+      if (pst[k] == ST_FINISHED) { status[k] = ST_FINISHED; arr[k] = parr[k]; wait[k] = pwf[k]; }
+    }
+    auto put = [&](int T, int k, float ss, float v_, uint32_t m, int w) {
+      lane[k] = h->tile_lanes[h->tile_lane_off[T] + (m & 0xff)];
+      vs[k] = ss; vv[k] = v_; cur[k] = (int)(m >> 16); wait[k] = w; driving[k] = 1;
+    };
+    for (int T : P.tiles) {
+      for (int i = 0; i < cnt[T]; ++i) { int p = h->tile_base[T] + i; put(T, vid[p], s[p], v[p], meta[p], wt[p]); }
+      for (int i = 0; i < icnt[T]; ++i) { const InboxRec &r = ib[h->tile_ibase[T] + i]; put(T, r.vid, r.s, r.v, r.meta, r.wait); }
+    }
   }
+  for (int k = 0; k < nv; ++k) if (driving[k]) status[k] = ST_DRIVING;
   o->t = h->t;
   if (o->status) std::memcpy(o->status, status.data(), nv);
   for (int k = 0; k < nv; ++k) {
     bool d = status[k] == ST_DRIVING;
     if (o->lane) o->lane[k] = d ? lane[k] : -1;
     if (o->cursor) o->cursor[k] = d ? cur[k] : 0;
-    if (o->wait_steps) o->wait_steps[k] = wait[k];
+    if (o->wait_steps) o->wait_steps[k] = status[k] == ST_PENDING ? 0 : wait[k];
     if (o->insert_time) o->insert_time[k] = ins[k];
     if (o->arrive_time) o->arrive_time[k] = arr[k];
     if (o->s) o->s[k] = d ? vs[k] : 0.f;
     if (o->v) o->v[k] = d ? vv[k] : 0.f;
   }
+  Part &P0 = h->parts[0];
   if (h->nj) {
-    if (o->junc_policy) CK(h, cudaMemcpy(o->junc_policy, h->SG.policy, h->nj, cudaMemcpyDeviceToHost));
-    if (o->junc_phase) CK(h, cudaMemcpy(o->junc_phase, h->SG.phase, h->nj * 4, cudaMemcpyDeviceToHost));
-    if (o->junc_elapsed) CK(h, cudaMemcpy(o->junc_elapsed, h->SG.elapsed, h->nj * 4, cudaMemcpyDeviceToHost));
-    if (o->junc_yellow_left) CK(h, cudaMemcpy(o->junc_yellow_left, h->SG.yellow_left, h->nj * 4, cudaMemcpyDeviceToHost));
-    if (o->junc_pending) CK(h, cudaMemcpy(o->junc_pending, h->SG.pending, h->nj * 4, cudaMemcpyDeviceToHost));
+    if (o->junc_policy) CK(h, cudaMemcpy(o->junc_policy, P0.SG.policy, h->nj, cudaMemcpyDeviceToHost));
+    if (o->junc_phase) CK(h, cudaMemcpy(o->junc_phase, P0.SG.phase, h->nj * 4, cudaMemcpyDeviceToHost));
+    if (o->junc_elapsed) CK(h, cudaMemcpy(o->junc_elapsed, P0.SG.elapsed, h->nj * 4, cudaMemcpyDeviceToHost));
+    if (o->junc_yellow_left) CK(h, cudaMemcpy(o->junc_yellow_left, P0.SG.yellow_left, h->nj * 4, cudaMemcpyDeviceToHost));
+    if (o->junc_pending) CK(h, cudaMemcpy(o->junc_pending, P0.SG.pending, h->nj * 4, cudaMemcpyDeviceToHost));
   }
   if (o->lane_dir) std::memcpy(o->lane_dir, h->dir.data(), h->nl);
-  if (o->lane_signal) CK(h, cudaMemcpy(o->lane_signal, h->A.lane_sig, h->nl, cudaMemcpyDeviceToHost));
+  if (o->lane_signal) CK(h, cudaMemcpy(o->lane_signal, P0.A.lane_sig, h->nl, cudaMemcpyDeviceToHost));
   if (o->lane_offsets && o->lane_order) {
     std::vector<std::vector<int>> per(h->nl);
     for (int k = 0; k < nv; ++k) if (status[k] == ST_DRIVING) per[lane[k]].push_back(k);
@@ -954,22 +1334,52 @@ sim_status sim_read_state(sim_handle h, sim_state *o) {
 sim_status sim_read_decisions(sim_handle h, sim_decisions *o) {
   sim_status st = check(h);
   if (st) return st;
-  if (!h->A.record) return fail(h, SIM_E_INVALID, "created without record_decisions");
+  if (!h->P.record_decisions) return fail(h, SIM_E_INVALID, "created without record_decisions");
   st = device_check(h);
   if (st) return st;
   const size_t n = h->nv;
-  const StepArgs &A = h->A;
-  if (o->leader_vid) CK(h, cudaMemcpy(o->leader_vid, A.r_leader, n * 4, cudaMemcpyDeviceToHost));
-  if (o->leader_hops) CK(h, cudaMemcpy(o->leader_hops, A.r_hops, n, cudaMemcpyDeviceToHost));
-  if (o->phantom) CK(h, cudaMemcpy(o->phantom, A.r_phantom, n, cudaMemcpyDeviceToHost));
-  if (o->old_follower_vid) CK(h, cudaMemcpy(o->old_follower_vid, A.r_of, n * 4, cudaMemcpyDeviceToHost));
-  if (o->side_vid) CK(h, cudaMemcpy(o->side_vid, A.r_side, 4 * n * 4, cudaMemcpyDeviceToHost));
-  if (o->lc) CK(h, cudaMemcpy(o->lc, A.r_lc, n, cudaMemcpyDeviceToHost));
-  if (o->handoffs) CK(h, cudaMemcpy(o->handoffs, A.r_hand, n, cudaMemcpyDeviceToHost));
-  if (o->accel) CK(h, cudaMemcpy(o->accel, A.r_acc, n * 4, cudaMemcpyDeviceToHost));
-  if (o->finished) CK(h, cudaMemcpy(o->finished, A.r_fin, n, cudaMemcpyDeviceToHost));
-  if (o->inserted) CK(h, cudaMemcpy(o->inserted, A.r_ins, n, cudaMemcpyDeviceToHost));
-  if (o->guard) CK(h, cudaMemcpy(o->guard, A.r_guard, n, cudaMemcpyDeviceToHost));
+  std::vector<int32_t> lead(n), of(n), side(4 * n);
+  std::vector<int8_t> hops(n), ph(n), lc(n), hand(n), fin(n), ins(n);
+  std::vector<float> acc(n);
+  std::vector<uint8_t> guard(n), mark(n);
+  std::vector<int32_t> t32(4 * n);
+  std::vector<int8_t> t8(n);
+  std::vector<float> tf(n);
+  std::vector<uint8_t> tu(n), tm(n);
+  for (Part &P : h->parts) {
+    const StepArgs &A = P.A;
+    CK(h, cudaMemcpy(tm.data(), A.r_mark, n, cudaMemcpyDeviceToHost));
+    auto take32 = [&](const int32_t *src, std::vector<int32_t> &dst, size_t w) -> sim_status {
+      CK(h, cudaMemcpy(t32.data(), src, w * n * 4, cudaMemcpyDeviceToHost));
+      for (size_t k = 0; k < n; ++k) if (tm[k]) for (size_t q = 0; q < w; ++q) dst[w * k + q] = t32[w * k + q];
+      return SIM_OK;
+    };
+    auto take8 = [&](const int8_t *src, std::vector<int8_t> &dst) -> sim_status {
+      CK(h, cudaMemcpy(t8.data(), src, n, cudaMemcpyDeviceToHost));
+      for (size_t k = 0; k < n; ++k) if (tm[k]) dst[k] = t8[k];
+      return SIM_OK;
+    };
+    take32(A.r_leader, lead, 1); take32(A.r_of, of, 1); take32(A.r_side, side, 4);
+    take8(A.r_hops, hops); take8(A.r_phantom, ph); take8(A.r_lc, lc); take8(A.r_hand, hand);
+    take8(A.r_fin, fin);
+    CK(h, cudaMemcpy(t8.data(), A.r_ins, n, cudaMemcpyDeviceToHost));
+    for (size_t k = 0; k < n; ++k) ins[k] |= t8[k];
+    CK(h, cudaMemcpy(tf.data(), A.r_acc, n * 4, cudaMemcpyDeviceToHost));
+    for (size_t k = 0; k < n; ++k) if (tm[k]) acc[k] = tf[k];
+    CK(h, cudaMemcpy(tu.data(), A.r_guard, n, cudaMemcpyDeviceToHost));
+    for (size_t k = 0; k < n; ++k) if (tm[k]) guard[k] = tu[k];
+  }
+  if (o->leader_vid) std::memcpy(o->leader_vid, lead.data(), n * 4);
+  if (o->leader_hops) std::memcpy(o->leader_hops, hops.data(), n);
+  if (o->phantom) std::memcpy(o->phantom, ph.data(), n);
+  if (o->old_follower_vid) std::memcpy(o->old_follower_vid, of.data(), n * 4);
+  if (o->side_vid) std::memcpy(o->side_vid, side.data(), 4 * n * 4);
+  if (o->lc) std::memcpy(o->lc, lc.data(), n);
+  if (o->handoffs) std::memcpy(o->handoffs, hand.data(), n);
+  if (o->accel) std::memcpy(o->accel, acc.data(), n * 4);
+  if (o->finished) std::memcpy(o->finished, fin.data(), n);
+  if (o->inserted) std::memcpy(o->inserted, ins.data(), n);
+  if (o->guard) std::memcpy(o->guard, guard.data(), n);
   return SIM_OK;
 }
 
@@ -982,9 +1392,8 @@ sim_status sim_read_metrics(sim_handle h, sim_metrics *m) {
   if (st) return st;
   m->t = h->t;
   m->n_driving = c[kNAcc];
-  m->n_finished = c[ACC_FINISHED];
-  m->n_pending = c[kNAcc + 1];
-  m->n_finished = c[kNAcc + 2];
+  m->n_finished = h->fin0 + (c[ACC_FINISHED] - h->acc_fin0);
+  m->n_pending = h->nv - m->n_driving - m->n_finished;
   m->vehicle_steps = c[ACC_VEH_STEPS];
   m->sum_travel_steps = c[ACC_SUM_TRAVEL];
   m->sum_wait_steps_finished = c[ACC_SUM_WAIT_FIN];
@@ -995,11 +1404,15 @@ sim_status sim_read_metrics(sim_handle h, sim_metrics *m) {
   m->n_guard_hits = c[ACC_GUARD];
   m->att_finished = c[ACC_FINISHED] ? (double)c[ACC_SUM_TRAVEL] / (double)c[ACC_FINISHED] : 0.0;
   if (m->lane_count || m->lane_waiting_at_end) {
-    int32_t *d = h->lanestat_d;
+    Part &P0 = h->parts[0];
+    int32_t *d = P0.lanestat_d;
     CK(h, cudaMemsetAsync(d, 0, 2 * (size_t)h->nl * 4, h->stream));
-    StepArgs a = step_args(h, h->t);
-    launch_lane_stats(a, d, d + h->nl, h->P.queue_zone_m, h->stream);
-    h->n_launch += 1;
+    for (Part &P : h->parts) {          // every partition adds its own tiles' vehicles
+      StepArgs a = step_args(P, h->t);
+      launch_lane_stats(a, d, d + h->nl, h->P.queue_zone_m, h->stream);
+      h->n_launch += 1;
+    }
+    if (h->comm) NK(h, g_nccl.AllReduce(d, d, 2 * (size_t)h->nl, 2 /*ncclInt32*/, kNcclSum, h->comm, h->stream));
     if (m->lane_count)
       CK(h, cudaMemcpyAsync(m->lane_count, d, h->nl * 4, cudaMemcpyDeviceToHost, h->stream));
     if (m->lane_waiting_at_end)
@@ -1078,6 +1491,33 @@ sim_status sim_load_state(sim_handle h, const sim_state *in) {
   S.jpend.assign(in->junc_pending, in->junc_pending + h->nj);
   S.dir.assign(in->lane_dir, in->lane_dir + h->nl);
   return upload_state(h, S);
+}
+
+sim_status sim_partition(const sim_graph *g, const sim_trips *tr, const sim_params *p,
+                         int32_t *road_owner, int32_t *plan_sizes) {
+  // Host-only: the partition and exchange plan sim_create would use (no GPU needed).
+  sim_s *h = new sim_s();
+  sim_status st = validate_and_copy(h, g, tr, p);
+  if (!st) st = build_tiles(h);
+  if (!st) {
+    h->world = std::max(1, p->world);
+    if (p->road_owner) h->tile_owner.assign(p->road_owner, p->road_owner + h->nr);
+    else h->tile_owner = h->world > 1 ? default_partition(h, h->world) : std::vector<int>(h->nr, 0);
+    if (road_owner) std::memcpy(road_owner, h->tile_owner.data(), h->nr * 4);
+    if (plan_sizes && h->world > 1) {
+      Plan plan = make_plan(h);
+      const int W = h->world;
+      for (int a = 0; a < W; ++a)
+        for (int b = 0; b < W; ++b) {
+          plan_sizes[2 * (a * W + b)] = plan.mig_cap[a][b];
+          plan_sizes[2 * (a * W + b) + 1] = (int32_t)plan.halo[a][b].size();
+        }
+    }
+  } else {
+    g_create_err = h->err;
+  }
+  delete h;
+  return st;
 }
 
 sim_status sim_destroy(sim_handle h) {

@@ -49,7 +49,9 @@ class sim_params(C.Structure):
                 ("b_safe", C.c_float), ("v_wait", C.c_float), ("queue_zone_m", C.c_float),
                 ("yellow_steps", C.c_int32), ("lookahead_lanes", C.c_int32),
                 ("exact_mode", C.c_int32), ("record_decisions", C.c_int32),
-                ("device", C.c_int32), ("stream", P)]
+                ("device", C.c_int32), ("stream", P), ("rank", C.c_int32),
+                ("world", C.c_int32), ("loopback", C.c_int32), ("nccl_id", P),
+                ("road_owner", P)]
 
 
 class sim_sizes(C.Structure):
@@ -78,7 +80,7 @@ class sim_metrics(C.Structure):
                                           ("lane_waiting_at_end", P)]
 
 
-ABI_FUNCTIONS = ["sim_create", "sim_step", "sim_sync", "sim_set_signal_phase",
+ABI_FUNCTIONS = ["sim_create", "sim_get_nccl_unique_id", "sim_partition", "sim_step", "sim_sync", "sim_set_signal_phase",
                  "sim_set_signal_phase_batch", "sim_set_lane_direction",
                  "sim_set_lane_direction_batch", "sim_query_sizes", "sim_read_state",
                  "sim_read_decisions", "sim_read_metrics", "sim_load_state",
@@ -99,6 +101,7 @@ def load_library(path=LIB):
     i32, h = C.c_int32, C.c_void_p
     sig = {
         "sim_create": [P, P, P, C.POINTER(C.c_void_p)],
+        "sim_get_nccl_unique_id": [P], "sim_partition": [P, P, P, P, P],
         "sim_step": [h, i32], "sim_sync": [h],
         "sim_set_signal_phase": [h, i32, i32], "sim_set_signal_phase_batch": [h, i32, P, P],
         "sim_set_lane_direction": [h, i32, i32], "sim_set_lane_direction_batch": [h, i32, P, P],
@@ -132,27 +135,77 @@ _TRIP_DT = dict(depart_step=np.int32, on_network_at_t0=np.uint8, route_offsets=n
                 start_v=np.float32, end_s=np.float32, profile=np.uint8)
 
 
+def _marshal(graph, trips, profiles, params, device=0, stream=None, exact_mode=False,
+             record_decisions=False, world=1, rank=0, loopback=False, nccl_id=None,
+             road_owner=None):
+    g = {k: np.ascontiguousarray(graph[k], dtype=dt) for k, dt in _GRAPH_DT.items()}
+    tr = {k: np.ascontiguousarray(trips[k], dtype=dt) for k, dt in _TRIP_DT.items()}
+    prof = np.ascontiguousarray(profiles, dtype=np.float32).reshape(-1, 6)
+    keep = [g, tr, prof]
+    n_lanes = int(g["lane_length"].shape[0])
+    n_j = int(g["junc_lane_offsets"].shape[0] - 1)
+    n = int(tr["depart_step"].shape[0])
+    G = sim_graph(n_lanes, int(g["road_lane_offsets"].shape[0] - 1), n_j,
+                  *[_ptr(g[nm]) for nm, _ in sim_graph._fields_[3:]])
+    T = sim_trips(n, *[_ptr(tr[nm]) for nm, _ in sim_trips._fields_[1:]])
+    nid = None
+    if nccl_id is not None:
+        nid = np.frombuffer(bytes(nccl_id), dtype=np.uint8).copy()
+        keep.append(nid)
+    own = None
+    if road_owner is not None:
+        own = np.ascontiguousarray(road_owner, np.int32)
+        keep.append(own)
+    Pm = sim_params(int(params["seed"]), float(params.get("dt", 1.0)), prof.shape[0],
+                    _ptr(prof), params["politeness"], params["b_hard"], params["b_safe"],
+                    params["v_wait"], params["queue_zone_m"], params["yellow_steps"],
+                    params["lookahead_lanes"], int(exact_mode), int(record_decisions),
+                    int(device), C.c_void_p(stream) if stream else None, int(rank),
+                    int(world), int(bool(loopback)),
+                    _ptr(nid) if nid is not None else None,
+                    _ptr(own) if own is not None else None)
+    return G, T, Pm, keep
+
+
+def get_nccl_unique_id():
+    """128-byte NCCL unique id for a partitioned multi-process run."""
+    lib = load_library()
+    buf = np.zeros(128, np.uint8)
+    st = lib.sim_get_nccl_unique_id(_ptr(buf))
+    if st != SIM_OK:
+        raise SimError(st, (lib.sim_last_error(None) or b"").decode())
+    return bytes(buf)
+
+
+def partition(graph, trips, profiles, params, world, road_owner=None):
+    """Host-only partition + exchange-plan sizes (sim_partition; no GPU needed).
+
+    Returns (road_owner [n_roads], mig_cap [world, world], halo [world, world])."""
+    lib = load_library()
+    G, T, Pm, keep = _marshal(graph, trips, profiles, params, world=world,
+                              road_owner=road_owner)
+    nr = G.n_roads
+    own = np.zeros(nr, np.int32)
+    sizes = np.zeros(world * world * 2, np.int32)
+    st = lib.sim_partition(C.byref(G), C.byref(T), C.byref(Pm), _ptr(own), _ptr(sizes))
+    if st != SIM_OK:
+        raise SimError(st, (lib.sim_last_error(None) or b"").decode())
+    sizes = sizes.reshape(world, world, 2)
+    return own, sizes[:, :, 0].copy(), sizes[:, :, 1].copy()
+
+
 class Sim:
     """One simulation handle (sim_create ... sim_destroy)."""
 
     def __init__(self, graph, trips, profiles, params, device=0, stream=None,
-                 exact_mode=False, record_decisions=False):
+                 exact_mode=False, record_decisions=False, world=1, rank=0, loopback=False,
+                 nccl_id=None, road_owner=None):
         lib = load_library()
         self.lib = lib
-        g = {k: np.ascontiguousarray(graph[k], dtype=dt) for k, dt in _GRAPH_DT.items()}
-        tr = {k: np.ascontiguousarray(trips[k], dtype=dt) for k, dt in _TRIP_DT.items()}
-        prof = np.ascontiguousarray(profiles, dtype=np.float32).reshape(-1, 6)
-        self.n_lanes = int(g["lane_length"].shape[0])
-        self.n_junctions = int(g["junc_lane_offsets"].shape[0] - 1)
-        self.n = int(tr["depart_step"].shape[0])
-        G = sim_graph(self.n_lanes, int(g["road_lane_offsets"].shape[0] - 1), self.n_junctions,
-                      *[_ptr(g[n]) for n, _ in sim_graph._fields_[3:]])
-        T = sim_trips(self.n, *[_ptr(tr[n]) for n, _ in sim_trips._fields_[1:]])
-        Pm = sim_params(int(params["seed"]), float(params.get("dt", 1.0)), prof.shape[0],
-                        _ptr(prof), params["politeness"], params["b_hard"], params["b_safe"],
-                        params["v_wait"], params["queue_zone_m"], params["yellow_steps"],
-                        params["lookahead_lanes"], int(exact_mode), int(record_decisions),
-                        int(device), C.c_void_p(stream) if stream else None)
+        G, T, Pm, keep = _marshal(graph, trips, profiles, params, device, stream, exact_mode,
+                                  record_decisions, world, rank, loopback, nccl_id, road_owner)
+        self.n_lanes, self.n_junctions, self.n = G.n_lanes, G.n_junctions, T.n_trips
+        self.world, self.rank = max(1, int(world)), int(rank)
         hh = C.c_void_p()
         st = lib.sim_create(C.byref(G), C.byref(T), C.byref(Pm), C.byref(hh))
         if st != SIM_OK:

@@ -1,0 +1,87 @@
+"""P-PART on one GPU: the partitioned path (spatial partition of road tiles,
+migration of boundary vehicles, halo of lane summaries) run with
+the loopback transport gives bit-identical state and metrics for any number
+of partitions — decisions depend only on the snapshot and (seed, vid, t), and
+every reduction is integer."""
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def simlib():
+    import paper_2406_10661_b200 as p
+    p.build()
+    return p
+
+
+def _run(simlib, scen, steps, **kw):
+    g = simlib.Sim.from_scenario(scen, **kw)
+    g.step(steps)
+    return g.read_state(lane_order=True), g.read_metrics(lane_stats=True)
+
+
+KEYS = ("status", "lane", "cursor", "wait_steps", "insert_time", "arrive_time", "s", "v",
+        "lane_offsets", "lane_order")
+MKEYS = ("n_pending", "n_driving", "n_finished", "vehicle_steps", "sum_travel_steps",
+         "sum_wait_steps_finished", "sum_depart_delay", "n_lane_changes", "n_handoffs",
+         "n_inserted", "n_guard_hits")
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+@pytest.mark.parametrize("name", ["grid", "city"])
+def test_partition_invariance(simlib, name, world):
+    scen = (synth.grid(rows=4, cols=4, road_len=250.0, lanes=2, n_trips=3000, seed=12,
+                       depart_window=400) if name == "grid"
+            else synth.city(G=12, n_vehicles=20000, seed=13))
+    s1, m1 = _run(simlib, scen, 150)
+    sw, mw = _run(simlib, scen, 150, world=world, loopback=True)
+    for k in KEYS:
+        assert np.array_equal(s1[k], sw[k]), (k, world)
+    for k in MKEYS:
+        assert m1[k] == mw[k], (k, world, m1[k], mw[k])
+    assert np.array_equal(m1["lane_count"], mw["lane_count"])
+    assert np.array_equal(m1["lane_waiting_at_end"], mw["lane_waiting_at_end"])
+    assert m1["n_handoffs"] > 0
+
+
+def test_partitioned_exact_mode_matches_oracle(simlib, oracle_lib):
+    """The partitioned path is still the model: exact mode with 3 partitions
+    equals the oracle (store_fp32) bit for bit."""
+    scen = synth.grid(rows=3, cols=3, road_len=200.0, lanes=2, n_trips=1500, seed=21)
+    g = simlib.Sim.from_scenario(scen, exact_mode=True, world=3, loopback=True)
+    o = oracle_lib.Oracle(scen, store_fp32=True)
+    g.step(200)
+    o.step(200)
+    gs, os_ = g.read_state(), o.read_state()
+    for k in ("status", "lane", "cursor", "wait_steps", "insert_time", "arrive_time"):
+        assert np.array_equal(gs[k], os_[k]), k
+    d = os_["status"] == 1
+    assert np.array_equal(gs["s"][d].astype(np.float64), os_["s"][d])
+
+
+def test_partitioned_decisions_and_setters(simlib):
+    scen = synth.grid(rows=3, cols=3, road_len=250.0, lanes=3, n_trips=1500, seed=31,
+                      tidal=True, dynamic=True, depart_window=300)
+    a = simlib.Sim.from_scenario(scen, record_decisions=True)
+    b = simlib.Sim.from_scenario(scen, record_decisions=True, world=4, loopback=True)
+    rng = np.random.default_rng(1)
+    dyn = np.where(scen.graph["lane_kind"] == 1)[0]
+    for t in range(6):
+        ls = dyn[rng.random(len(dyn)) < 0.4]
+        ds = rng.integers(0, 2, len(ls))
+        js = rng.choice(len(scen.graph["junc_lane_offsets"]) - 1, 2, replace=False)
+        ps = rng.integers(0, 4, 2)
+        for sim in (a, b):
+            sim.set_lane_direction_batch(ls, ds)
+            sim.set_signal_phase_batch(js, ps)
+            sim.step(25)
+        da, db = a.read_decisions(), b.read_decisions()
+        for k in ("leader_vid", "lc", "handoffs", "inserted", "finished", "side_vid"):
+            assert np.array_equal(da[k], db[k]), (t, k)
+        sa, sb = a.read_state(), b.read_state()
+        for k in ("status", "lane", "s", "v", "junc_phase", "lane_signal"):
+            assert np.array_equal(sa[k], sb[k]), (t, k)
