@@ -97,15 +97,19 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def make_workload(rank=0):
+def make_workload(world=1):
+    """C4 at N=1; weak scaling for N > 1: the same city recipe grown to N times
+    the area (G = 72 * sqrt(N)) with 2M vehicles per GPU, spatially partitioned
+    over the N GPUs with boundary migration."""
     import synth
-    scen = synth.city(G=72, n_vehicles=2_000_000, seed=4 + 1000 * rank)
-    return scen
+    G = int(round(72 * np.sqrt(world)))
+    return synth.city(G=G, n_vehicles=2_000_000 * world, seed=4)
 
 
 def workload_config(scen, extra=None):
-    cfg = {"workload": "C4 city-like synthetic network (SURVEY 8(d)): G=72 perturbed grid, "
-                       "2M vehicles on the network at t=0, fixed-time signals",
+    G = int(np.sqrt(len(scen.graph["junc_lane_offsets"]) - 1))
+    cfg = {"workload": f"C4 city-like synthetic network (SURVEY 8(d)): G={G} perturbed grid, "
+                       f"{scen.n_trips / 1e6:.0f}M vehicles on the network at t=0, fixed-time signals",
            "n_vehicles": int(scen.n_trips), "n_lanes": int(scen.n_lanes),
            "n_junctions": int(len(scen.graph["junc_lane_offsets"]) - 1),
            "n_roads": int(len(scen.graph["road_lane_offsets"]) - 1),
@@ -137,7 +141,7 @@ def cpu_baseline(scen, budget_s=20.0, max_steps=10):
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    scen = make_workload(0)
+    scen = make_workload(1)
     import oracle
     oracle.build()
     o = oracle.Oracle(scen)
@@ -175,10 +179,20 @@ def run_gpu(args, rank, world, local_rank):
         p.build()
     if world > 1:
         torch.distributed.barrier()
-    scen = make_workload(rank)
+    scen = make_workload(world)
     stream = torch.cuda.Stream(dev)          # the simulation stream (events recorded on it)
     torch.cuda.set_stream(stream)
-    sim = p.Sim.from_scenario(scen, device=local_rank, stream=stream.cuda_stream)
+    if world > 1:
+        import synth
+        nid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            nid.copy_(torch.frombuffer(bytearray(p.get_nccl_unique_id()), dtype=torch.uint8))
+        torch.distributed.broadcast(nid, 0)
+        sim = p.Sim.from_scenario(scen, device=local_rank, stream=stream.cuda_stream, world=world,
+                                  rank=rank, nccl_id=bytes(nid.cpu().numpy()),
+                                  road_owner=synth.rcb_partition(scen, world))
+    else:
+        sim = p.Sim.from_scenario(scen, device=local_rank, stream=stream.cuda_stream)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
     for _ in range(args.warmup):
         sim.step(1)
@@ -202,22 +216,20 @@ def run_gpu(args, rank, world, local_rank):
     step_ms = sum(a.elapsed_time(b) for a, b in evs)
     kstep_ms, ksig_ms, launches = sim.read_timing()
     sim.enable_timing(False)
-    m1 = sim.read_metrics()
-    vsteps = m1["vehicle_steps"] - m0["vehicle_steps"]
+    m1 = sim.read_metrics()                  # global (allreduced over ranks when partitioned)
+    tot_vsteps = m1["vehicle_steps"] - m0["vehicle_steps"]
     movers = (m1["n_lane_changes"] - m0["n_lane_changes"]) + (m1["n_handoffs"] - m0["n_handoffs"]) \
         + (m1["n_finished"] - m0["n_finished"])
     t_max = step_ms
-    tot_vsteps = vsteps
     if world > 1:
         t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        v = torch.tensor([vsteps], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(v)
-        t_max, tot_vsteps = float(t.item()), float(v.item())
+        t_max = float(t.item())
     value = tot_vsteps / (t_max / 1e3)
-    # roofline of the dominant kernel (k_step)
+    # roofline of the dominant kernel (k_step), per GPU
     peak, peak_kind = peaks()
-    per_launch_bytes = algorithmic_bytes(vsteps / args.steps, movers / args.steps, scen.n_lanes)
+    per_launch_bytes = algorithmic_bytes(tot_vsteps / args.steps / world, movers / args.steps / world,
+                                         scen.n_lanes / world)
     kstep_avg_s = kstep_ms / 1e3 / args.steps
     achieved = per_launch_bytes / kstep_avg_s / 1e9
     traffic = None
@@ -244,14 +256,12 @@ def run_gpu(args, rank, world, local_rank):
         sim.step(1)
         obs = sim.read_metrics(lane_stats=True)           # D2H: counters + lane queues
     e2e_dt = time.perf_counter() - t0
-    e2e_v = obs["vehicle_steps"] - me0["vehicle_steps"]
+    e2e_v = obs["vehicle_steps"] - me0["vehicle_steps"]       # global
     e2e_val = e2e_v / e2e_dt
     if world > 1:
         t = torch.tensor([e2e_dt], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        v = torch.tensor([e2e_v], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(v)
-        e2e_val = float(v.item()) / float(t.item())
+        e2e_val = e2e_v / float(t.item())
     if rank != 0:
         return
     cpu = cpu_baseline(scen) if world == 1 and not args.no_cpu else None
@@ -261,7 +271,8 @@ def run_gpu(args, rank, world, local_rank):
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": workload_config(scen, {
             "parallelism": "single GPU" if world == 1 else
-            f"{world} independent replicas (one C4 instance per GPU; spatial partition not yet built)",
+            f"spatial partition over {world} GPUs (recursive coordinate bisection of road tiles), "
+            "boundary-vehicle migration + lane-summary halo per step via NCCL p2p",
             "fp64_guard_hits_per_step": (m1["n_guard_hits"] - m0["n_guard_hits"]) / args.steps}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,

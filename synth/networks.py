@@ -677,8 +677,38 @@ def city(G=72, spacing=900.0, n_vehicles=2_000_000, seed=4, route_len=40,
                  start_lane=lanes[idx].astype(np.int32), start_s=s[idx].astype(np.float32),
                  start_v=np.zeros(n, np.float32), end_s=end_s.astype(np.float32),
                  profile=profile_of[idx].astype(np.uint8))
+    road_dst = np.array([m[1] for m in b.road_meta], np.int64)
     return Scenario(f"city{G}", g, trips, profiles, default_params(seed),
-                    meta=dict(builder=b, junc_xy=np.array(b.junc_xy)))
+                    meta=dict(builder=b, junc_xy=np.array(b.junc_xy), road_dst=road_dst))
+
+
+def rcb_partition(scen, world):
+    """Recursive coordinate bisection of the roads into `world` parts by the
+    coordinates of their downstream junctions, weighted by lane-metres (a road
+    travels with its outgoing junction lanes: DESIGN §6).  Input preparation
+    for partitioned runs; the library has its own coordinate-free default."""
+    g = scen.graph
+    xy = np.asarray(scen.meta["junc_xy"], np.float64)[scen.meta["road_dst"]]
+    nl = np.diff(g["road_lane_offsets"])
+    L = g["lane_length"][g["road_lanes"][g["road_lane_offsets"][:-1]]]
+    w = nl * L
+    owner = np.zeros(len(nl), np.int32)
+
+    def split(idx, parts, base, depth):
+        if parts == 1:
+            owner[idx] = base
+            return
+        ext = xy[idx].max(0) - xy[idx].min(0)
+        ax = int(np.argmax(ext))
+        order = idx[np.lexsort((idx, xy[idx, ax]))]
+        left = parts // 2
+        cw = np.cumsum(w[order])
+        cut = int(np.searchsorted(cw, cw[-1] * left / parts))
+        split(order[:cut], left, base, depth + 1)
+        split(order[cut:], parts - left, base + left, depth + 1)
+
+    split(np.arange(len(nl)), world, 0, 0)
+    return owner
 
 
 def tiled_city(tiles_x=1, tiles_y=1, G=50, n_per_tile=1_000_000, seed=5, **kw):
