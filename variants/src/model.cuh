@@ -13,6 +13,9 @@
 
 #include "dev.h"
 
+#ifndef USE_PASS1
+#define USE_PASS1 0
+#endif
 
 namespace sim {
 
@@ -50,7 +53,7 @@ __device__ __forceinline__ PV<float> pvals(const Prof &p, float) {
 
 // IDM (delta = 4) in canonical order; ledger L7 (no leader), L8.
 template <typename R, bool GUARD>
-__device__ __forceinline__ R idm(R v, R v0, bool lead, R gap, R dv, const PV<R> &p, R b_hard,
+__device__ __noinline__ R idm(R v, R v0, bool lead, R gap, R dv, const PV<R> &p, R b_hard,
                                  R gap_scale, Guard &g) {
   using M = Ar<R>;
   R x = M::div(v, v0);
@@ -102,6 +105,8 @@ struct View {
   int32_t *vid, *nxt, *nxt2;
   uint32_t *meta;
   int32_t *wait;
+  float *ai;                         // fp32 IDM of each vehicle vs its in-lane leader (pass 1)
+  uint8_t *gi;                       // guard flag of that evaluation
 };
 
 __device__ __forceinline__ int m_lane(uint32_t m) { return (int)(m & 0xffu); }
@@ -240,8 +245,9 @@ struct Me {                          // the ego vehicle's identity / route cache
 
 // O4-O6 for the ego placed on tile-local lane l (App. A2.3)
 template <typename R, bool GUARD>
-__device__ LEv<R> eval_lane(const StepArgs &A, const TileSh &T, const View &C, int l,
-                            int lead_idx, R s, R v, const PV<R> &p, const Me &me, Guard &g) {
+__device__ __noinline__ LEv<R> eval_lane(const StepArgs &A, const TileSh &T, const View &C, int l,
+                            int lead_idx, R s, R v, const PV<R> &p, const Me &me, Guard &g,
+                            int self_idx = -1) {
   using M = Ar<R>;
   LEv<R> e;
   const int lg = T.glob[l];
@@ -296,7 +302,17 @@ __device__ LEv<R> eval_lane(const StepArgs &A, const TileSh &T, const View &C, i
     }
   }
   const R b_hard = (R)A.b_hard;
-  R a_lead = idm<R, GUARD>(v, v0, e.has_leader, e.gap, M::sub(v, e.vlead), p, b_hard, gscale, g);
+  R a_lead;
+  if constexpr (!M::fp64 && USE_PASS1) {
+    if (self_idx >= 0 && lead_idx >= 0) {          // own lane, in-lane leader: pass-1 value
+      a_lead = C.ai[self_idx];
+      if (GUARD && C.gi[self_idx]) g.hit = true, g.why |= (1u << 13);
+    } else {
+      a_lead = idm<R, GUARD>(v, v0, e.has_leader, e.gap, M::sub(v, e.vlead), p, b_hard, gscale, g);
+    }
+  } else {
+    a_lead = idm<R, GUARD>(v, v0, e.has_leader, e.gap, M::sub(v, e.vlead), p, b_hard, gscale, g);
+  }
   e.a = a_lead;
   e.phantom = false;
   if (road && e.next1 != kLaneDest && (e.next1 == kLaneBlocked || nx.stop)) {
@@ -362,7 +378,7 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
   const R L = (R)T.len[l];
   const int lead = (i + 1 < T.seg_end[l]) ? i + 1 : -1;
   const int of = (i > T.seg_start[l]) ? i - 1 : -1;
-  LEv<R> cur = eval_lane<R, GUARD>(A, T, C, l, lead, s, v, p, me, g);
+  LEv<R> cur = eval_lane<R, GUARD>(A, T, C, l, lead, s, v, p, me, g, i);
   o.leader = cur.leader;
   o.hops = cur.hops;
   o.phantom = cur.phantom;
@@ -390,7 +406,7 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
     if (GUARD && inG && v != (R)0 && fabsf((float)(rem - need)) <= kEpsPos * (float)(fabs(rem) + need)) g.hit = true, g.why |= (1u << 2);
     int sl[2] = {T.left[l], T.right[l]};
     int front[2] = {-1, -1}, back[2] = {-1, -1};
-#pragma unroll
+#pragma unroll 1
     for (int sd = 0; sd < 2; ++sd) {
       if (sl[sd] < 0) continue;
       int a = T.seg_start[sl[sd]], b = T.seg_end[sl[sd]];
@@ -407,8 +423,13 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
         const PV<R> po = pvals(T.P[m_prof(C.meta[of])], (R)0);
         const R so = (R)C.s[of], vo = (R)C.v[of];
         const R v0o = (po.vmax < (R)T.vmax[l]) ? po.vmax : (R)T.vmax[l];
-        a_of = idm<R, GUARD>(vo, v0o, true, M::sub(M::sub(s, so), p.len), M::sub(vo, v), po,
-                             b_hard, fabs(s - so) + p.len, g);
+        if constexpr (!M::fp64 && USE_PASS1) {           // of's in-lane leader is the ego
+          a_of = C.ai[of];
+          if (GUARD && C.gi[of]) g.hit = true, g.why |= (1u << 13);
+        } else {
+          a_of = idm<R, GUARD>(vo, v0o, true, M::sub(M::sub(s, so), p.len), M::sub(vo, v), po,
+                               b_hard, fabs(s - so) + p.len, g);
+        }
         if (lead >= 0) {
           const R sl_ = (R)C.s[lead];
           const R ll_ = (R)T.P[m_prof(C.meta[lead])].len;
@@ -421,7 +442,7 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
       bool adm[2] = {false, false};
       R u[2] = {(R)0, (R)0};
       LEv<R> ev[2];
-#pragma unroll
+#pragma unroll 1
       for (int sd = 0; sd < 2; ++sd) {
         const int ls = sl[sd];
         const int sgn = sd == 0 ? -1 : 1;
@@ -436,7 +457,10 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
           const PV<R> pb = pvals(T.P[m_prof(C.meta[bi])], (R)0);
           const R sb = (R)C.s[bi], vb = (R)C.v[bi];
           const R v0b = (pb.vmax < (R)T.vmax[ls]) ? pb.vmax : (R)T.vmax[ls];
-          if (front[sd] >= 0) {
+          if constexpr (!M::fp64 && USE_PASS1) {         // back's in-lane leader is front
+            a_nf = C.ai[bi];
+            if (GUARD && C.gi[bi]) g.hit = true, g.why |= (1u << 13);
+          } else if (front[sd] >= 0) {
             const int fi = front[sd];
             const R sf = (R)C.s[fi];
             const R lf = (R)T.P[m_prof(C.meta[fi])].len;
