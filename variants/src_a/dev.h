@@ -105,8 +105,7 @@ struct StepArgs {
   InboxRec *inbox_out;
   Slab scratch;                     // global fallback for large tiles ([base+ibase, +cap+icap))
   int32_t *bsort_scratch;           // [Σ icap] inbox sort order for large inboxes
-  float *rs_s1;                     // per-slot in-lane IDM for large tiles (scratch indexing)
-  uint8_t *rs_flags;
+  int32_t *dl_scratch;              // per-tile list of guard-deferred vehicles (scratch indexing)
   // migration to other partitions (world > 1): per-peer regions of MigRec
   MigRec *out_buf;
   const int32_t *out_off, *out_cap;

@@ -34,23 +34,6 @@ __device__ __forceinline__ bool key_less(unsigned long long h1, int v1, unsigned
 
 // fp64 canonical path (exact_mode and guard fallback) kept out of line so the
 // hot fp32 path is register-allocated on its own
-#ifndef F64_NOINLINE
-#define F64_NOINLINE __forceinline__
-#endif
-#ifdef GUARD_STATS
-__device__ unsigned long long g_guard_stats[32];
-#endif
-__device__ F64_NOINLINE void veh_update_f64(const StepArgs &A, const TileSh &T, const View &C,
-                                            int i, Res &r) {
-#ifdef NO_F64
-  return;
-#endif
-  Guard g;
-  g.hit = false;
-  g.why = 0;
-  veh_update<double, false>(A, T, C, i, r, g);
-}
-
 __device__ __forceinline__ void record(const StepArgs &A, int vid, const Res &r, bool guard) {
   A.r_leader[vid] = r.leader;
   A.r_hops[vid] = (int8_t)r.hops;
@@ -70,6 +53,59 @@ __device__ __forceinline__ void put_inbox(InboxRec *dst, const InboxRec &rec) {
   const int4 *s = reinterpret_cast<const int4 *>(&rec);
   d[0] = s[0];
   d[1] = s[1];
+}
+
+struct Acc8 {                        // per-thread counters of one tile
+  long long travel = 0, waitfin = 0, delay = 0;
+  int fin = 0, lc = 0, hand = 0, guard = 0, ovf = 0, ins = 0;
+};
+
+// a vehicle that leaves its slot: lane change / hand-off (kind 2, also every
+// guard-deferred vehicle) or arrival (kind 3)
+__device__ __forceinline__ void emit_moved(const StepArgs &A, const View &C, int i, const Res &r,
+                                           int kind, Acc8 &acc) {
+  const int vid = C.vid[i];
+  acc.lc += r.lc != 0;
+  acc.hand += r.hand;
+  if (kind == 3) {
+    A.status[vid] = ST_FINISHED;
+    A.arrive_time[vid] = A.t + 1;
+    A.wait_fin[vid] = r.wait1;
+    acc.fin += 1;
+    acc.travel += (long long)(A.t + 1 - A.insert_time[vid]);
+    acc.waitfin += r.wait1;
+    return;
+  }
+  const uint32_t meta = C.meta[i];
+  const int cur = m_cursor(meta);
+  InboxRec rec;
+  rec.s = r.s1;
+  rec.v = r.v1;
+  rec.vid = vid;
+  rec.nxt = route_at(A, vid, cur, C.nxt[i], C.nxt2[i], r.cursor + 1);
+  rec.nxt2 = route_at(A, vid, cur, C.nxt[i], C.nxt2[i], r.cursor + 2);
+  rec.meta = pack_meta(A.lane_local[r.lane_g], m_prof(meta), r.cursor);
+  rec.wait = r.wait1;
+  rec.pad = 0;
+  const int dt = A.lane_tile[r.lane_g];
+  const int owner = A.tile_owner[dt];
+  if (owner == A.rank) {
+    const int slot = atomicAdd(&A.icnt_out[dt], 1);
+    if (slot < A.tile_icap[dt]) put_inbox(A.inbox_out + A.tile_ibase[dt] + slot, rec);
+    else acc.ovf += 1;
+    atomicMin(&A.summ_next[r.lane_g], vkey(r.s1, vid));
+    A.pubv_next[vid] = r.v1;
+  } else {                                          // migrant to another partition
+    const int slot = atomicAdd(&A.out_cnt[owner], 1);
+    if (slot < A.out_cap[owner]) {
+      MigRec *m = A.out_buf + A.out_off[owner] + 1 + slot;
+      put_inbox(&m->rec, rec);
+      m->tile = dt;
+      m->insert_time = A.insert_time[vid];
+    } else {
+      acc.ovf += 1;
+    }
+  }
 }
 
 struct StepShared {
@@ -92,6 +128,7 @@ struct StepShared {
 #endif
 // One WARP per road tile: no block barriers, warps progress independently
 // (DESIGN §3.3).  All intra-tile synchronisation is __syncwarp().
+template <bool EXACT>
 __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ StepShared S;
@@ -206,8 +243,6 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
     C.nxt2 = C.vid + 2 * kSmemVeh;
     C.meta = reinterpret_cast<uint32_t *>(C.vid + 3 * kSmemVeh);
     C.wait = C.vid + 4 * kSmemVeh;
-    C.ai = reinterpret_cast<float *>(C.vid + 5 * kSmemVeh);
-    C.gi = reinterpret_cast<uint8_t *>(C.ai + kSmemVeh);
   } else {
     const int sb = base + ibase;               // scratch is indexed by base + ibase (size cap + icap)
     C.s = A.scratch.s + sb;
@@ -217,8 +252,6 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
     C.nxt2 = A.scratch.nxt2 + sb;
     C.meta = A.scratch.meta + sb;
     C.wait = A.scratch.wait + sb;
-    C.ai = A.rs_s1 + sb;
-    C.gi = A.rs_flags + sb;
   }
   int *bsort = (n_in <= kSmemInbox) ? S.bsort : (A.bsort_scratch + ibase);
   const InboxRec *inb = A.inbox_in + ibase;
@@ -317,65 +350,50 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
   }
   __syncwarp();
 
-  // ---- pass 1: every vehicle's IDM vs its in-lane leader (free road if none);
-  // reused as its own a_lead, as a_of of its follower and as a_nf whenever it is
-  // the back neighbour of a lane changer
-#ifndef USE_PASS1
-#define USE_PASS1 0
-#endif
-  if (USE_PASS1 && !A.exact_mode) {
-    for (int i = lane_id; i < n; i += kThreads) {
-      const int l = m_lane(C.meta[i]);
-      const PV<float> p = pvals(T.P[m_prof(C.meta[i])], 0.f);
-      const float v = C.v[i];
-      const float v0 = (p.vmax < T.vmax[l]) ? p.vmax : T.vmax[l];
-      Guard g;
-      g.hit = false;
-      g.why = 0;
-      float a;
-      if (i + 1 < T.seg_end[l]) {
-        const float sf = C.s[i + 1], lf = T.P[m_prof(C.meta[i + 1])].len, s = C.s[i];
-        a = idm<float, true>(v, v0, true, (sf - s) - lf, v - C.v[i + 1], p, A.b_hard,
-                             fabsf(sf - s) + lf, g);
-      } else {
-        a = idm<float, true>(v, v0, false, 0.f, 0.f, p, A.b_hard, 0.f, g);
-      }
-      C.ai[i] = a;
-      C.gi[i] = g.hit ? 1 : 0;
-    }
-    __syncwarp();
-  }
-
   // ---- 2-3. per-vehicle update (a2-a4) and outputs, 32 vehicles at a time ----
-  long long acc_travel = 0, acc_waitfin = 0, acc_delay = 0;
-  int acc_fin = 0, acc_lc = 0, acc_hand = 0, acc_guard = 0, acc_ovf = 0, acc_ins = 0;
+  // fp32 path: vehicles whose decision margins fall inside the guard band are
+  // deferred and recomputed after the loop with the canonical fp64 sequence;
+  // they leave through the inbox (as movers), so the in-order compaction of the
+  // stayers never waits for them and the fp64 code stays out of the hot loop.
+  Acc8 acc;
   int run = 0;                                      // stayers written so far
+  int ndef = 0;                                     // deferred vehicles (warp-uniform)
+  int *dlist = A.dl_scratch + base + ibase;
   for (int c0 = 0; c0 < n; c0 += kThreads) {
     const int i = c0 + lane_id;
     Res r;
     int kind = 0;                                   // 0 none, 1 stayer, 2 mover, 3 finished
+    bool defer = false;
     if (i < n) {
-      Guard g;
-      g.hit = false;
-      g.why = 0;
-      if (A.exact_mode) {
-        veh_update_f64(A, T, C, i, r);
+      if constexpr (EXACT) {
+        Guard g;
+        g.hit = false;
+        g.why = 0;
+        veh_update<double, false>(A, T, C, i, r, g);
       } else {
+        Guard g;
+        g.hit = false;
+        g.why = 0;
         veh_update<float, true>(A, T, C, i, r, g);
-        if (g.hit) {                                // guard band: canonical fp64 recompute
-          veh_update_f64(A, T, C, i, r);
-          acc_guard += 1;
+        defer = g.hit;
 #ifdef GUARD_STATS
+        if (g.hit)
           for (int b = 0; b < 32; ++b)
             if (g.why & (1u << b)) atomicAdd(&g_guard_stats[b], 1ull);
 #endif
-        }
       }
-      if (A.record) record(A, C.vid[i], r, g.hit);
-      const int l = m_lane(C.meta[i]);
-      if (r.fin) kind = 3;
-      else if (r.lc == 0 && r.hand == 0 && r.lane_g == T.glob[l]) kind = 1;
-      else kind = 2;
+      if (!defer) {
+        if (A.record) record(A, C.vid[i], r, false);
+        const int l = m_lane(C.meta[i]);
+        if (r.fin) kind = 3;
+        else if (r.lc == 0 && r.hand == 0 && r.lane_g == T.glob[l]) kind = 1;
+        else kind = 2;
+      }
+    }
+    if constexpr (!EXACT) {
+      const unsigned dball = __ballot_sync(0xffffffffu, defer);
+      if (defer) dlist[ndef + __popc(dball & ((1u << lane_id) - 1u))] = i;
+      ndef += __popc(dball);
     }
     // order-preserving compaction of stayers (warp ballot)
     const unsigned ball = __ballot_sync(0xffffffffu, kind == 1);
@@ -390,52 +408,24 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
       A.out.meta[pos] = meta;
       A.out.wait[pos] = r.wait1;
       atomicMin(&T.first_out[m_lane(meta)], pos);
-    } else if (kind == 2) {
-      const int vid = C.vid[i];
-      const uint32_t meta = C.meta[i];
-      const int cur = m_cursor(meta);
-      InboxRec rec;
-      rec.s = r.s1;
-      rec.v = r.v1;
-      rec.vid = vid;
-      rec.nxt = route_at(A, vid, cur, C.nxt[i], C.nxt2[i], r.cursor + 1);
-      rec.nxt2 = route_at(A, vid, cur, C.nxt[i], C.nxt2[i], r.cursor + 2);
-      rec.meta = pack_meta(A.lane_local[r.lane_g], m_prof(meta), r.cursor);
-      rec.wait = r.wait1;
-      rec.pad = 0;
-      const int dt = A.lane_tile[r.lane_g];
-      const int owner = A.tile_owner[dt];
-      if (owner == A.rank) {
-        const int slot = atomicAdd(&A.icnt_out[dt], 1);
-        if (slot < A.tile_icap[dt]) put_inbox(A.inbox_out + A.tile_ibase[dt] + slot, rec);
-        else acc_ovf += 1;
-        atomicMin(&A.summ_next[r.lane_g], vkey(r.s1, vid));
-        A.pubv_next[vid] = r.v1;
-      } else {                                      // migrant to another partition
-        const int slot = atomicAdd(&A.out_cnt[owner], 1);
-        if (slot < A.out_cap[owner]) {
-          MigRec *m = A.out_buf + A.out_off[owner] + 1 + slot;
-          put_inbox(&m->rec, rec);
-          m->tile = dt;
-          m->insert_time = A.insert_time[vid];
-        } else {
-          acc_ovf += 1;
-        }
-      }
-      acc_lc += r.lc != 0;
-      acc_hand += r.hand;
-    } else if (kind == 3) {
-      const int vid = C.vid[i];
-      A.status[vid] = ST_FINISHED;
-      A.arrive_time[vid] = A.t + 1;
-      A.wait_fin[vid] = r.wait1;
-      acc_fin += 1;
-      acc_travel += (long long)(A.t + 1 - A.insert_time[vid]);
-      acc_waitfin += r.wait1;
-      acc_lc += r.lc != 0;
-      acc_hand += r.hand;
+    } else if (kind >= 2) {
+      emit_moved(A, C, i, r, kind, acc);
     }
     run += __popc(ball);
+  }
+  if constexpr (!EXACT) {
+    __syncwarp();
+    for (int q = lane_id; q < ndef; q += kThreads) {
+      const int i = dlist[q];
+      Res r;
+      Guard g;
+      g.hit = false;
+      g.why = 0;
+      veh_update<double, false>(A, T, C, i, r, g);
+      if (A.record) record(A, C.vid[i], r, true);
+      emit_moved(A, C, i, r, r.fin ? 3 : 2, acc);
+      acc.guard += 1;
+    }
   }
   __syncwarp();
 
@@ -487,21 +477,21 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
     rec.pad = 0;
     const int slot = atomicAdd(&A.icnt_out[tile], 1);
     if (slot < T.icap) put_inbox(A.inbox_out + ibase + slot, rec);
-    else acc_ovf += 1;
+    else acc.ovf += 1;
     atomicMin(&A.summ_next[g], vkey(rec.s, k));
     A.pubv_next[k] = 0.f;
     A.pend_head[g] = h + 1;
     A.status[k] = ST_DRIVING;
     A.insert_time[k] = A.t + 1;
     if (A.record) A.r_ins[k] = 1;
-    acc_ins += 1;
-    acc_delay += (long long)(A.t + 1 - A.depart[k]);
+    acc.ins += 1;
+    acc.delay += (long long)(A.t + 1 - A.depart[k]);
   }
   // warp reduction of the counters (int64, exact, order independent)
-  long long vals[kNAcc] = {0, acc_fin, acc_travel, acc_waitfin, acc_delay, acc_lc, acc_hand,
-                           acc_ins, acc_guard, acc_ovf, 0, 0};
-  const unsigned any = __ballot_sync(0xffffffffu, (acc_fin | acc_lc | acc_hand | acc_ins |
-                                                   acc_guard | acc_ovf) != 0);
+  long long vals[kNAcc] = {0, acc.fin, acc.travel, acc.waitfin, acc.delay, acc.lc, acc.hand,
+                           acc.ins, acc.guard, acc.ovf, 0, 0};
+  const unsigned any = __ballot_sync(0xffffffffu, (acc.fin | acc.lc | acc.hand | acc.ins |
+                                                   acc.guard | acc.ovf) != 0);
   if (any) {
 #pragma unroll
     for (int c = 1; c < kNAcc - 2; ++c)
@@ -692,16 +682,18 @@ __global__ void k_halo_unpack(StepArgs A, const int32_t *lanes, const HaloRec *b
 }
 
 // ---- launchers ---------------------------------------------------------------
-int step_smem_bytes() { return kSmemVeh * (7 * 4 + 4 + 1); }
+int step_smem_bytes() { return kSmemVeh * 7 * 4; }
 
 void launch_step(const StepArgs &a, void *stream, int smem_bytes) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    cudaFuncSetAttribute(k_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    cudaFuncSetAttribute(k_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     attr = true;
   }
-  if (a.n_own > 0)
-    k_step<<<a.n_own, kThreads, smem_bytes, (cudaStream_t)stream>>>(a);
+  if (a.n_own <= 0) return;
+  if (a.exact_mode) k_step<true><<<a.n_own, kThreads, smem_bytes, (cudaStream_t)stream>>>(a);
+  else k_step<false><<<a.n_own, kThreads, smem_bytes, (cudaStream_t)stream>>>(a);
 }
 
 void launch_signal(const SignalArgs &a, void *stream) {

@@ -781,7 +781,7 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   AL(sc_.s, sc); AL(sc_.v, sc); AL(sc_.vid, sc); AL(sc_.nxt, sc); AL(sc_.nxt2, sc);
   AL(sc_.meta, sc); AL(sc_.wait, sc);
   AL(A.bsort_scratch, h->sum_icap);
-  AL(A.rs_s1, sc); AL(A.rs_flags, sc);
+  AL(A.dl_scratch, sc);
   for (int b = 0; b < 3; ++b) AL(P.summ[b], nl);
   UP(i32, h->route_off); A.route_off = i32;
   UP(i32, h->route); A.route = i32;

@@ -89,7 +89,7 @@ struct StepArgs {
   const int32_t *exit_lane;         // junction lane: its successor; road lane: itself
   const uint8_t *usable;
   const int4 *outroads;             // per lane: <= 4 distinct roads reachable through usable
-                                    // successors (-1 pad; <= 4 validated at create)
+                                    // successors (-1 pad; w == -2: more, scan the CSR)
   const uint8_t *lane_sig;
   const int32_t *lane_tile;
   const uint8_t *lane_local;

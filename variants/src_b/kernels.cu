@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
     T.cap = A.tile_cap[tile];
     T.icap = A.tile_icap[tile];
     T.P = A.n_prof <= kSmemProf ? S.prof : A.prof;
+    T.tab_ok = nroad <= kMaxRoadLanes ? 1 : 0;
   }
   __syncwarp();
   if (A.n_prof <= kSmemProf)
@@ -175,7 +176,7 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
   // (target road, lane id) and grouped by target road (built in parallel, one
   // warp lane per (road lane, successor) slot; staging reuses the inbox-key area)
   SuccEnt *stage = S.stage;
-  {                                                 // limits validated at create
+  if (nroad <= kMaxRoadLanes) {
     const int x = lane_id;                          // kMaxRoadLanes * kMaxSucc == 32
     const int l = x / kMaxSucc, k = x % kMaxSucc;
     bool valid = false;
@@ -183,6 +184,7 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
     if (l < nroad) {
       const int g = A.tile_lanes[l0 + l];
       const int e0 = A.succ_off[g], e1 = A.succ_off[g + 1];
+      if (e1 - e0 > kMaxSucc) T.tab_ok = 0;
       if (k < e1 - e0) {
         const int j = A.succ[e0 + k];
         if (A.usable[j]) {
@@ -212,11 +214,15 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
       int gid = 0;
       for (int q = 1; q <= k; ++q) gid += T.se[l][q - 1].troad != T.se[l][q].troad;
       if (start) {
-        T.gtroad[l][gid] = T.se[l][k].troad;
-        T.gbeg[l][gid] = (uint8_t)k;
+        if (gid < kMaxGroups) {
+          T.gtroad[l][gid] = T.se[l][k].troad;
+          T.gbeg[l][gid] = (uint8_t)k;
+        } else {
+          T.tab_ok = 0;
+        }
       }
       if (k == cnt - 1) {
-        const int ngr = gid + 1;
+        const int ngr = min(gid + 1, kMaxGroups);
         T.ng[l] = (uint8_t)ngr;
         T.gbeg[l][ngr] = (uint8_t)cnt;
       }

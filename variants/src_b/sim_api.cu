@@ -253,6 +253,7 @@ void compute_usable(sim_s *h) {
       if (k < 4) o[k] = r;
       ++k;
     }
+    if (k > 4) o[3] = -2;
   }
 }
 
@@ -456,20 +457,6 @@ sim_status build_tiles(sim_s *h) {
     h->tile_nroad[r] = (int)lanes.size();
     std::sort(jls[r].begin(), jls[r].end());
     lanes.insert(lanes.end(), jls[r].begin(), jls[r].end());
-    if (h->tile_nroad[r] > kMaxRoadLanes)
-      return fail(h, SIM_E_INVALID, "road " + std::to_string(r) + " has more than " +
-                  std::to_string(kMaxRoadLanes) + " lanes");
-    for (int q = 0; q < h->tile_nroad[r]; ++q) {
-      const int l = lanes[q];
-      std::vector<int> tr;
-      for (int e = h->succ_off[l]; e < h->succ_off[l + 1]; ++e) tr.push_back(h->target_road[h->succ[e]]);
-      std::sort(tr.begin(), tr.end());
-      const int ntr = (int)(std::unique(tr.begin(), tr.end()) - tr.begin());
-      if (h->succ_off[l + 1] - h->succ_off[l] > kMaxSucc || ntr > kMaxGroups)
-        return fail(h, SIM_E_INVALID, "lane " + std::to_string(l) + " has more than " +
-                    std::to_string(kMaxSucc) + " successors or " + std::to_string(kMaxGroups) +
-                    " successor roads");
-    }
     if ((int)lanes.size() > kMaxTileLanes)
       return fail(h, SIM_E_INVALID, "road " + std::to_string(r) + " has more than " + std::to_string(kMaxTileLanes) + " lanes incl. outgoing junction lanes");
     int cap = 0;
