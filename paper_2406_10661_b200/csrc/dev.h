@@ -44,6 +44,8 @@ struct Prof {                       // one vehicle profile
   double a_max_d, a_comf_d, T_d, s0_d, vmax_d, len_d, inv2sqrt_d, pad_d;
 };
 
+static_assert(sizeof(Prof) % 16 == 0, "Prof is copied as int4 words");
+
 struct InboxRec {                   // 32 B, one sector
   float s, v;
   int32_t vid, nxt, nxt2;

@@ -55,6 +55,32 @@ __device__ __forceinline__ void put_inbox(InboxRec *dst, const InboxRec &rec) {
   d[1] = s[1];
 }
 
+// Cold paths (inboxes larger than kSmemInbox, i.e. bulk lane changes after a
+// setter or a load): kept out of line so they do not occupy the I-cache.
+__device__ __noinline__ void rank_inbox_global(const InboxRec *inb, int n_in, int *bsort,
+                                               int lane_id) {
+  for (int j = lane_id; j < n_in; j += kThreads) {
+    const InboxRec r = inb[j];
+    const unsigned long long h = hikey(m_lane(r.meta), r.s);
+    int rank = 0;
+    for (int q = 0; q < n_in; ++q) {
+      const InboxRec o = inb[q];
+      rank += key_less(hikey(m_lane(o.meta), o.s), o.vid, h, r.vid);
+    }
+    bsort[rank] = j;
+  }
+}
+__device__ __noinline__ int lower_bound_inbox_global(const InboxRec *inb, const int *bsort,
+                                                     int n_in, unsigned long long h, int vid) {
+  int lo = 0, hi = n_in;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const InboxRec o = inb[bsort[mid]];
+    if (key_less(hikey(m_lane(o.meta), o.s), o.vid, h, vid)) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
 struct Acc8 {                        // per-thread counters of one tile
   long long travel = 0, waitfin = 0, delay = 0;
   int fin = 0, lc = 0, hand = 0, guard = 0, ovf = 0, ins = 0;
@@ -155,8 +181,11 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
     T.P = A.n_prof <= kSmemProf ? S.prof : A.prof;
   }
   __syncwarp();
-  if (A.n_prof <= kSmemProf)
-    for (int q = lane_id; q < A.n_prof; q += kThreads) S.prof[q] = A.prof[q];
+  if (A.n_prof <= kSmemProf) {                      // profiles as int4 words (Prof is 96 B)
+    const int nw = A.n_prof * (int)(sizeof(Prof) / 16);
+    for (int q = lane_id; q < nw; q += kThreads)
+      reinterpret_cast<int4 *>(S.prof)[q] = reinterpret_cast<const int4 *>(A.prof)[q];
+  }
   for (int l = lane_id; l < nl; l += kThreads) {
     const int g = A.tile_lanes[l0 + l];
     T.glob[l] = g;
@@ -270,25 +299,32 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
         S.sk_vid[rank] = vj;
       }
     } else {
-      for (int j = lane_id; j < n_in; j += kThreads) {
-        const InboxRec r = inb[j];
-        const unsigned long long h = hikey(m_lane(r.meta), r.s);
-        int rank = 0;
-        for (int q = 0; q < n_in; ++q) {
-          const InboxRec o = inb[q];
-          rank += key_less(hikey(m_lane(o.meta), o.s), o.vid, h, r.vid);
-        }
-        bsort[rank] = j;
-      }
+      rank_inbox_global(inb, n_in, bsort, lane_id);
     }
   }
   __syncwarp();
-  // stayers: position = own index + #inbox keys below (binary search in the sorted inbox)
-  for (int i = lane_id; i < n_st; i += kThreads) {
-    const int gi = base + i;
-    const float s = A.in.s[gi];
-    const uint32_t meta = A.in.meta[gi];
-    const int vid = A.in.vid[gi];
+  // stayers: position = own index + #inbox keys below (binary search in the sorted inbox).
+  // Two slab rows per iteration, loads issued before the stores (more bytes in flight).
+  for (int i0 = lane_id; i0 < n_st; i0 += 2 * kThreads) {
+    float sv[2], vv[2];
+    uint32_t mv[2];
+    int idv[2], n1v[2], n2v[2], wv[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = i0 + u * kThreads;
+      if (i < n_st) {
+        const int gi = base + i;
+        sv[u] = A.in.s[gi]; vv[u] = A.in.v[gi]; mv[u] = A.in.meta[gi]; idv[u] = A.in.vid[gi];
+        n1v[u] = A.in.nxt[gi]; n2v[u] = A.in.nxt2[gi]; wv[u] = A.in.wait[gi];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+    const int i = i0 + u * kThreads;
+    if (i >= n_st) break;
+    const float s = sv[u];
+    const uint32_t meta = mv[u];
+    const int vid = idv[u];
     int pos = i;
     if (n_in > 0) {
       const unsigned long long h = hikey(m_lane(meta), s);
@@ -299,21 +335,18 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
           if (key_less(S.sk_hi[mid], S.sk_vid[mid], h, vid)) lo = mid + 1; else hi = mid;
         }
       } else {
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          const InboxRec o = inb[bsort[mid]];
-          if (key_less(hikey(m_lane(o.meta), o.s), o.vid, h, vid)) lo = mid + 1; else hi = mid;
-        }
+        lo = lower_bound_inbox_global(inb, bsort, n_in, h, vid);
       }
       pos += lo;
     }
     C.s[pos] = s;
-    C.v[pos] = A.in.v[gi];
+    C.v[pos] = vv[u];
     C.vid[pos] = vid;
-    C.nxt[pos] = A.in.nxt[gi];
-    C.nxt2[pos] = A.in.nxt2[gi];
+    C.nxt[pos] = n1v[u];
+    C.nxt2[pos] = n2v[u];
     C.meta[pos] = meta;
-    C.wait[pos] = A.in.wait[gi];
+    C.wait[pos] = wv[u];
+    }
   }
   // inbox records: position = sorted rank + #stayers below (binary search in the slab)
   for (int r = lane_id; r < n_in; r += kThreads) {

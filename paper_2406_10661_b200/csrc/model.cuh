@@ -553,9 +553,10 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
   R pb = M::fp64 ? s1 : s;
   R pa = M::fp64 ? (R)0 : adv;
   int curg = T.glob[new_l], ri = me.cur, n = use.next1, hand = 0;
+  bool croad = T.isroad[new_l];                          // current lane: tile-local until a hand-off
+  R Lc = (R)T.len[new_l];
   bool fin = false;
   for (;;) {
-    const bool croad = __ldg(A.lane_road + curg) >= 0;
     const bool dest_road = croad && route_at(A, me.vid, me.cur, me.nxt, me.nxt2, ri + 1) < 0;
     if (dest_road) {
       const R es = (R)__ldg(A.end_s + me.vid);
@@ -565,7 +566,6 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
         g.hit = true, g.why |= (1u << 10);
       if (pa >= rem) { fin = true; break; }
     }
-    const R Lc = (R)__ldg(A.lane_len + curg);
     const R rem = M::sub(Lc, pb);
     if (GUARD && n >= 0 && !(adv_zero && hand == 0) &&
         fabsf((float)(pa - rem)) <= kEpsPos * (float)(fabs(pa) + fabs(rem) + (R)1e-3))
@@ -574,6 +574,8 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
       pb = M::sub(pb, Lc);
       curg = n;
       const bool nroad = __ldg(A.lane_road + curg) >= 0;
+      croad = nroad;
+      Lc = (R)__ldg(A.lane_len + curg);
       if (nroad) ri += 1;
       hand += 1;
       if (nroad) {
