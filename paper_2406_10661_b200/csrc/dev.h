@@ -25,6 +25,11 @@ constexpr int kNAcc = 12;            // per-tile int64 accumulators
 constexpr int kMaxRoadLanes = 4;     // road lanes per tile cached in the successor table
 constexpr int kMaxSucc = 8;          // successors per road lane cached in the table
 static_assert(kMaxRoadLanes * kMaxSucc == 32, "one warp builds the successor table");
+// tile descriptor (int32 words, 16-B padded): [nl, nroad, ne, 0], glob[nl], len[nl],
+// vmax[nl], flags[nl] (bit0 usable), then ne <= 32 successor entries of the
+// road lanes, 8 words each: j, target road, exit lane, flags (bit0 junction lane,
+// bit1 usable, lane_local << 8, k << 16), outroads(exit lane) x4
+constexpr int kDescMaxWords = 4 + 4 * kMaxTileLanes + 8 * kMaxRoadLanes * kMaxSucc;
 constexpr int kMaxGroups = 4;        // distinct target roads per road lane in the table
 constexpr int kSmemProf = 8;         // profiles staged in shared memory
 constexpr uint64_t kEmptyKey = ~0ull;
@@ -99,6 +104,7 @@ struct StepArgs {
   int32_t rank, n_own;
   const int32_t *tiles, *tile_owner;
   const int32_t *tile_lane_off, *tile_lanes, *tile_nroad;
+  const int32_t *desc, *desc_off;   // tile descriptors (words, per-tile offsets)
   const int32_t *tile_base, *tile_cap, *tile_ibase, *tile_icap;
   int32_t *cnt_in, *cnt_out;        // [n_tiles] stayer counts (read / write buffers)
   int32_t *icnt_in, *icnt_out;      // [n_tiles] inbox counts

@@ -145,6 +145,7 @@ struct StepShared {
       int sk_vid[kSmemInbox];
     };
     SuccEnt stage[32];                        // successor-table staging (before the merge)
+    int words[kDescMaxWords];                 // tile descriptor staging
   };
   Prof prof[kSmemProf];
 };
@@ -162,14 +163,53 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
   const int tile = A.tiles[blockIdx.x], lane_id = threadIdx.x;
 
   // ---- tile metadata -----------------------------------------------------
-  const int l0 = A.tile_lane_off[tile];
-  const int nl = A.tile_lane_off[tile + 1] - l0;
-  const int nroad = A.tile_nroad[tile];
+  // One coalesced read of the tile descriptor (host-built): lane
+  // ids / lengths / speed limits / usable flags and every road-lane successor
+  // with its target road, exit lane and the exit lane's reachable roads.
+  const int doff = A.desc_off[tile];
+  const int dsz = A.desc_off[tile + 1] - doff;
   const int n_st = A.cnt_in[tile];
   const int n_in = A.icnt_in[tile];
   const int n = n_st + n_in;
   const int base = A.tile_base[tile];
   const int ibase = A.tile_ibase[tile];
+  for (int q = lane_id; q < (dsz >> 2); q += kThreads)
+    reinterpret_cast<int4 *>(S.words)[q] = reinterpret_cast<const int4 *>(A.desc + doff)[q];
+  if (A.n_prof <= kSmemProf) {                      // profiles as int4 words (Prof is 96 B)
+    const int nw = A.n_prof * (int)(sizeof(Prof) / 16);
+    for (int q = lane_id; q < nw; q += kThreads)
+      reinterpret_cast<int4 *>(S.prof)[q] = reinterpret_cast<const int4 *>(A.prof)[q];
+  }
+  __syncwarp();
+  const int nl = S.words[0], nroad = S.words[1], ne = S.words[2];
+  // read this lane's lane record and successor entry into registers first (the
+  // staging area is reused for the successor sort below)
+  int lg = 0, lflags = 0;
+  float llen = 0.f, lvmax = 0.f;
+  if (lane_id < nl) {
+    lg = S.words[4 + lane_id];
+    llen = __int_as_float(S.words[4 + nl + lane_id]);
+    lvmax = __int_as_float(S.words[4 + 2 * nl + lane_id]);
+    lflags = S.words[4 + 3 * nl + lane_id];
+  }
+  SuccEnt s;
+  s.j = 0x7fffffff;
+  s.troad = 0x7fffffff;
+  int el = -1, ek = 0;
+  if (lane_id < ne) {
+    const int *w = S.words + 4 + 4 * nl + 8 * lane_id;
+    const int fl = w[3];
+    el = (fl >> 8) & 0xff;
+    ek = fl >> 16;
+    if (fl & 2) {                                   // usable successor
+      s.j = w[0];
+      s.troad = w[1];
+      s.b = w[2];
+      s.outr = make_int4(w[4], w[5], w[6], w[7]);
+      s.stop = ((fl & 1) && A.lane_sig[s.j] != SIG_GREEN) ? 1 : 0;
+    }
+  }
+  __syncwarp();
   if (lane_id == 0) {
     T.nl = nl;
     T.nroad = nroad;
@@ -180,19 +220,13 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
     T.icap = A.tile_icap[tile];
     T.P = A.n_prof <= kSmemProf ? S.prof : A.prof;
   }
-  __syncwarp();
-  if (A.n_prof <= kSmemProf) {                      // profiles as int4 words (Prof is 96 B)
-    const int nw = A.n_prof * (int)(sizeof(Prof) / 16);
-    for (int q = lane_id; q < nw; q += kThreads)
-      reinterpret_cast<int4 *>(S.prof)[q] = reinterpret_cast<const int4 *>(A.prof)[q];
-  }
-  for (int l = lane_id; l < nl; l += kThreads) {
-    const int g = A.tile_lanes[l0 + l];
-    T.glob[l] = g;
-    T.len[l] = A.lane_len[g];
-    T.vmax[l] = A.lane_vmax[g];
+  if (lane_id < nl) {
+    const int l = lane_id;
+    T.glob[l] = lg;
+    T.len[l] = llen;
+    T.vmax[l] = lvmax;
     T.isroad[l] = l < nroad;
-    T.usable[l] = A.usable[g];
+    T.usable[l] = lflags & 1;
     T.seg_start[l] = 0;
     T.seg_end[l] = 0;
     T.first_out[l] = 0x7fffffff;
@@ -201,39 +235,24 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
     T.right[l] = (l < nroad - 1) ? (int8_t)(l + 1) : (int8_t)-1;
   }
   // successor table of the tile's road lanes: usable successors sorted by
-  // (target road, lane id) and grouped by target road (built in parallel, one
-  // warp lane per (road lane, successor) slot; staging reuses the inbox-key area)
+  // (target road, lane id) and grouped by target road (one warp lane per slot)
   SuccEnt *stage = S.stage;
-  {                                                 // limits validated at create
-    const int x = lane_id;                          // kMaxRoadLanes * kMaxSucc == 32
-    const int l = x / kMaxSucc, k = x % kMaxSucc;
-    bool valid = false;
-    SuccEnt s;
-    if (l < nroad) {
-      const int g = A.tile_lanes[l0 + l];
-      const int e0 = A.succ_off[g], e1 = A.succ_off[g + 1];
-      if (k < e1 - e0) {
-        const int j = A.succ[e0 + k];
-        if (A.usable[j]) {
-          valid = true;
-          s.j = j;
-          s.troad = A.target_road[j];
-          s.b = A.exit_lane[j];
-          s.outr = A.outroads[s.b];
-          s.stop = (A.lane_road[j] < 0 && A.lane_sig[j] != SIG_GREEN) ? 1 : 0;
-        }
-      }
-    }
-    if (!valid) { s.j = 0x7fffffff; s.troad = 0x7fffffff; }
-    stage[x] = s;
-    __syncwarp();
+  stage[lane_id].j = 0x7fffffff;
+  stage[lane_id].troad = 0x7fffffff;
+  __syncwarp();
+  if (el >= 0) stage[el * kMaxSucc + ek] = s;
+  __syncwarp();
+  {
+    const int l = lane_id / kMaxSucc, k = lane_id % kMaxSucc;
+    const SuccEnt me = stage[lane_id];
+    const bool valid = me.j != 0x7fffffff;
     int rank = 0, cnt = 0;
     for (int q = 0; q < kMaxSucc; ++q) {
       const SuccEnt &o = stage[l * kMaxSucc + q];
       cnt += o.j != 0x7fffffff;
-      rank += (o.troad < s.troad) || (o.troad == s.troad && o.j < s.j);
+      rank += (o.troad < me.troad) || (o.troad == me.troad && o.j < me.j);
     }
-    if (valid) T.se[l][rank] = s;
+    if (valid) T.se[l][rank] = me;
     if (l < nroad && k == 0) T.sn[l] = (uint8_t)cnt;
     __syncwarp();
     if (l < nroad && k < cnt) {
@@ -245,9 +264,8 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
         T.gbeg[l][gid] = (uint8_t)k;
       }
       if (k == cnt - 1) {
-        const int ngr = gid + 1;
-        T.ng[l] = (uint8_t)ngr;
-        T.gbeg[l][ngr] = (uint8_t)cnt;
+        T.ng[l] = (uint8_t)(gid + 1);
+        T.gbeg[l][gid + 1] = (uint8_t)cnt;
       }
     }
     if (l < nroad && k == 0 && cnt == 0) T.ng[l] = 0;
