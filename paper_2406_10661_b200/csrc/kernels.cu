@@ -553,25 +553,63 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
 }
 
 // ---- a5: per-junction signal controller -------------
+// One warp per junction: lane 0 applies requests and advances the phase
+// machine, all lanes write the signals of the junction's lanes (coalesced).
 __global__ void k_signal(SignalArgs a) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (j >= a.n_junctions) return;
   const int K = a.ph_off[j + 1] - a.ph_off[j];
-  int pol = a.policy[j], ph = a.phase[j], el = a.elapsed[j], y = a.yellow_left[j],
-      q = a.pending[j];
-  const int req = a.request[j];
-  if (req >= 0) {                                   // requests apply before sig_t (L35)
-    a.request[j] = -1;
-    pol = POL_MANUAL;
-    if (y > 0) q = req;
-    else if (req != ph) {
-      if (a.yellow > 0) { y = a.yellow; q = req; }
-      else { ph = req; q = req; }
+  int pol = 0, ph = 0;
+  int y = 0;
+  if (lane == 0) {
+    pol = a.policy[j];
+    ph = a.phase[j];
+    int el = a.elapsed[j], q = a.pending[j];
+    y = a.yellow_left[j];
+    const int req = a.request[j];
+    if (req >= 0) {                                 // requests apply before sig_t (L35)
+      a.request[j] = -1;
+      pol = POL_MANUAL;
+      if (y > 0) q = req;
+      else if (req != ph) {
+        if (a.yellow > 0) { y = a.yellow; q = req; }
+        else { ph = req; q = req; }
+      }
     }
+    // advance t -> t+1 (O11) into the stored state; sig_t uses (pol, ph, y) above
+    int nph = ph, ny = y, nel = el, nq = q;
+    if (pol == POL_FIXED && K > 0) {
+      if (ny > 0) {
+        ny -= 1;
+        if (ny == 0) { nph = nq; nel = 0; }
+      } else {
+        nel += 1;
+        if (nel >= a.green_steps[a.ph_off[j] + nph]) {
+          const int nx = (nph + 1) % K;
+          if (a.yellow > 0) { ny = a.yellow; nq = nx; }
+          else { nph = nx; nq = nx; nel = 0; }
+        }
+      }
+    } else if (pol == POL_MANUAL) {
+      if (ny > 0) {
+        ny -= 1;
+        if (ny == 0) nph = nq;
+      }
+      nel += 1;
+    }
+    a.policy[j] = (uint8_t)pol;
+    a.phase[j] = nph;
+    a.elapsed[j] = nel;
+    a.yellow_left[j] = ny;
+    a.pending[j] = nq;
   }
+  pol = __shfl_sync(0xffffffffu, pol, 0);
+  ph = __shfl_sync(0xffffffffu, ph, 0);
+  y = __shfl_sync(0xffffffffu, y, 0);
   const int j0 = a.jl_off[j], nj = a.jl_off[j + 1] - j0;
   const uint8_t *grow = a.green + a.green_off[j] + (int64_t)ph * nj;
-  for (int k = 0; k < nj; ++k) {
+  for (int k = lane; k < nj; k += 32) {
     uint8_t sg;
     if (pol == POL_NONE || K == 0) sg = SIG_GREEN;
     else {
@@ -580,31 +618,6 @@ __global__ void k_signal(SignalArgs a) {
     }
     a.lane_sig[a.jl[j0 + k]] = sg;
   }
-  // advance t -> t+1 (O11)
-  if (pol == POL_FIXED && K > 0) {
-    if (y > 0) {
-      y -= 1;
-      if (y == 0) { ph = q; el = 0; }
-    } else {
-      el += 1;
-      if (el >= a.green_steps[a.ph_off[j] + ph]) {
-        const int nx = (ph + 1) % K;
-        if (a.yellow > 0) { y = a.yellow; q = nx; }
-        else { ph = nx; q = nx; el = 0; }
-      }
-    }
-  } else if (pol == POL_MANUAL) {
-    if (y > 0) {
-      y -= 1;
-      if (y == 0) ph = q;
-    }
-    el += 1;
-  }
-  a.policy[j] = (uint8_t)pol;
-  a.phase[j] = ph;
-  a.elapsed[j] = el;
-  a.yellow_left[j] = y;
-  a.pending[j] = q;
 }
 
 __global__ void k_apply_requests(int32_t *request, uint8_t *policy, const int32_t *junc,
@@ -743,7 +756,7 @@ void launch_step(const StepArgs &a, void *stream, int smem_bytes) {
 
 void launch_signal(const SignalArgs &a, void *stream) {
   if (a.n_junctions > 0)
-    k_signal<<<(a.n_junctions + 127) / 128, 128, 0, (cudaStream_t)stream>>>(a);
+    k_signal<<<(a.n_junctions + 3) / 4, 128, 0, (cudaStream_t)stream>>>(a);
 }
 
 void launch_apply_requests(int32_t *request, uint8_t *policy, const int32_t *junc,

@@ -19,12 +19,17 @@ namespace sim {
 
 constexpr int kMaxTileLanes = 32;    // lanes per tile (road lanes + outgoing junction lanes)
 constexpr int kThreads = 32;         // k_step block size: one warp per road tile
-constexpr int kSmemVeh = 160;        // snapshot slots held in shared memory (larger tiles use global scratch)
+constexpr int kSmemVeh = 128;        // snapshot slots held in shared memory (larger tiles use global scratch)
 constexpr int kSmemInbox = 48;       // inbox keys sorted in shared memory
 constexpr int kNAcc = 12;            // per-tile int64 accumulators
 constexpr int kMaxRoadLanes = 4;     // road lanes per tile cached in the successor table
 constexpr int kMaxSucc = 8;          // successors per road lane cached in the table
 static_assert(kMaxRoadLanes * kMaxSucc == 32, "one warp builds the successor table");
+// tile descriptor (int32 words, 16-B padded): [nl, nroad, ne, 0], glob[nl], len[nl],
+// vmax[nl], flags[nl] (bit0 usable), then ne <= 32 successor entries of the
+// road lanes, 8 words each: j, target road, exit lane, flags (bit0 junction lane,
+// bit1 usable, lane_local << 8, k << 16), outroads(exit lane) x4
+constexpr int kDescMaxWords = 4 + 4 * kMaxTileLanes + 8 * kMaxRoadLanes * kMaxSucc;
 constexpr int kMaxGroups = 4;        // distinct target roads per road lane in the table
 constexpr int kSmemProf = 8;         // profiles staged in shared memory
 constexpr uint64_t kEmptyKey = ~0ull;
@@ -43,6 +48,8 @@ struct Prof {                       // one vehicle profile
   float a_max, a_comf, T, s0, vmax, len, inv2sqrt_f, pad;
   double a_max_d, a_comf_d, T_d, s0_d, vmax_d, len_d, inv2sqrt_d, pad_d;
 };
+
+static_assert(sizeof(Prof) % 16 == 0, "Prof is copied as int4 words");
 
 struct InboxRec {                   // 32 B, one sector
   float s, v;
@@ -89,7 +96,7 @@ struct StepArgs {
   const int32_t *exit_lane;         // junction lane: its successor; road lane: itself
   const uint8_t *usable;
   const int4 *outroads;             // per lane: <= 4 distinct roads reachable through usable
-                                    // successors (-1 pad; w == -2: more, scan the CSR)
+                                    // successors (-1 pad; <= 4 validated at create)
   const uint8_t *lane_sig;
   const int32_t *lane_tile;
   const uint8_t *lane_local;
@@ -97,6 +104,7 @@ struct StepArgs {
   int32_t rank, n_own;
   const int32_t *tiles, *tile_owner;
   const int32_t *tile_lane_off, *tile_lanes, *tile_nroad;
+  const int32_t *desc, *desc_off;   // tile descriptors (words, per-tile offsets)
   const int32_t *tile_base, *tile_cap, *tile_ibase, *tile_icap;
   int32_t *cnt_in, *cnt_out;        // [n_tiles] stayer counts (read / write buffers)
   int32_t *icnt_in, *icnt_out;      // [n_tiles] inbox counts

@@ -55,6 +55,32 @@ __device__ __forceinline__ void put_inbox(InboxRec *dst, const InboxRec &rec) {
   d[1] = s[1];
 }
 
+// Cold paths (inboxes larger than kSmemInbox, i.e. bulk lane changes after a
+// setter or a load): kept out of line so they do not occupy the I-cache.
+__device__ __noinline__ void rank_inbox_global(const InboxRec *inb, int n_in, int *bsort,
+                                               int lane_id) {
+  for (int j = lane_id; j < n_in; j += kThreads) {
+    const InboxRec r = inb[j];
+    const unsigned long long h = hikey(m_lane(r.meta), r.s);
+    int rank = 0;
+    for (int q = 0; q < n_in; ++q) {
+      const InboxRec o = inb[q];
+      rank += key_less(hikey(m_lane(o.meta), o.s), o.vid, h, r.vid);
+    }
+    bsort[rank] = j;
+  }
+}
+__device__ __noinline__ int lower_bound_inbox_global(const InboxRec *inb, const int *bsort,
+                                                     int n_in, unsigned long long h, int vid) {
+  int lo = 0, hi = n_in;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const InboxRec o = inb[bsort[mid]];
+    if (key_less(hikey(m_lane(o.meta), o.s), o.vid, h, vid)) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
 struct Acc8 {                        // per-thread counters of one tile
   long long travel = 0, waitfin = 0, delay = 0;
   int fin = 0, lc = 0, hand = 0, guard = 0, ovf = 0, ins = 0;
@@ -119,6 +145,7 @@ struct StepShared {
       int sk_vid[kSmemInbox];
     };
     SuccEnt stage[32];                        // successor-table staging (before the merge)
+    int words[kDescMaxWords];                 // tile descriptor staging
   };
   Prof prof[kSmemProf];
 };
@@ -136,14 +163,53 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
   const int tile = A.tiles[blockIdx.x], lane_id = threadIdx.x;
 
   // ---- tile metadata -----------------------------------------------------
-  const int l0 = A.tile_lane_off[tile];
-  const int nl = A.tile_lane_off[tile + 1] - l0;
-  const int nroad = A.tile_nroad[tile];
+  // One coalesced read of the tile descriptor (host-built): lane
+  // ids / lengths / speed limits / usable flags and every road-lane successor
+  // with its target road, exit lane and the exit lane's reachable roads.
+  const int doff = A.desc_off[tile];
+  const int dsz = A.desc_off[tile + 1] - doff;
   const int n_st = A.cnt_in[tile];
   const int n_in = A.icnt_in[tile];
   const int n = n_st + n_in;
   const int base = A.tile_base[tile];
   const int ibase = A.tile_ibase[tile];
+  for (int q = lane_id; q < (dsz >> 2); q += kThreads)
+    reinterpret_cast<int4 *>(S.words)[q] = reinterpret_cast<const int4 *>(A.desc + doff)[q];
+  if (A.n_prof <= kSmemProf) {                      // profiles as int4 words (Prof is 96 B)
+    const int nw = A.n_prof * (int)(sizeof(Prof) / 16);
+    for (int q = lane_id; q < nw; q += kThreads)
+      reinterpret_cast<int4 *>(S.prof)[q] = reinterpret_cast<const int4 *>(A.prof)[q];
+  }
+  __syncwarp();
+  const int nl = S.words[0], nroad = S.words[1], ne = S.words[2];
+  // read this lane's lane record and successor entry into registers first (the
+  // staging area is reused for the successor sort below)
+  int lg = 0, lflags = 0;
+  float llen = 0.f, lvmax = 0.f;
+  if (lane_id < nl) {
+    lg = S.words[4 + lane_id];
+    llen = __int_as_float(S.words[4 + nl + lane_id]);
+    lvmax = __int_as_float(S.words[4 + 2 * nl + lane_id]);
+    lflags = S.words[4 + 3 * nl + lane_id];
+  }
+  SuccEnt s;
+  s.j = 0x7fffffff;
+  s.troad = 0x7fffffff;
+  int el = -1, ek = 0;
+  if (lane_id < ne) {
+    const int *w = S.words + 4 + 4 * nl + 8 * lane_id;
+    const int fl = w[3];
+    el = (fl >> 8) & 0xff;
+    ek = fl >> 16;
+    if (fl & 2) {                                   // usable successor
+      s.j = w[0];
+      s.troad = w[1];
+      s.b = w[2];
+      s.outr = make_int4(w[4], w[5], w[6], w[7]);
+      s.stop = ((fl & 1) && A.lane_sig[s.j] != SIG_GREEN) ? 1 : 0;
+    }
+  }
+  __syncwarp();
   if (lane_id == 0) {
     T.nl = nl;
     T.nroad = nroad;
@@ -153,18 +219,14 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
     T.cap = A.tile_cap[tile];
     T.icap = A.tile_icap[tile];
     T.P = A.n_prof <= kSmemProf ? S.prof : A.prof;
-    T.tab_ok = nroad <= kMaxRoadLanes ? 1 : 0;
   }
-  __syncwarp();
-  if (A.n_prof <= kSmemProf)
-    for (int q = lane_id; q < A.n_prof; q += kThreads) S.prof[q] = A.prof[q];
-  for (int l = lane_id; l < nl; l += kThreads) {
-    const int g = A.tile_lanes[l0 + l];
-    T.glob[l] = g;
-    T.len[l] = A.lane_len[g];
-    T.vmax[l] = A.lane_vmax[g];
+  if (lane_id < nl) {
+    const int l = lane_id;
+    T.glob[l] = lg;
+    T.len[l] = llen;
+    T.vmax[l] = lvmax;
     T.isroad[l] = l < nroad;
-    T.usable[l] = A.usable[g];
+    T.usable[l] = lflags & 1;
     T.seg_start[l] = 0;
     T.seg_end[l] = 0;
     T.first_out[l] = 0x7fffffff;
@@ -173,40 +235,24 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
     T.right[l] = (l < nroad - 1) ? (int8_t)(l + 1) : (int8_t)-1;
   }
   // successor table of the tile's road lanes: usable successors sorted by
-  // (target road, lane id) and grouped by target road (built in parallel, one
-  // warp lane per (road lane, successor) slot; staging reuses the inbox-key area)
+  // (target road, lane id) and grouped by target road (one warp lane per slot)
   SuccEnt *stage = S.stage;
-  if (nroad <= kMaxRoadLanes) {
-    const int x = lane_id;                          // kMaxRoadLanes * kMaxSucc == 32
-    const int l = x / kMaxSucc, k = x % kMaxSucc;
-    bool valid = false;
-    SuccEnt s;
-    if (l < nroad) {
-      const int g = A.tile_lanes[l0 + l];
-      const int e0 = A.succ_off[g], e1 = A.succ_off[g + 1];
-      if (e1 - e0 > kMaxSucc) T.tab_ok = 0;
-      if (k < e1 - e0) {
-        const int j = A.succ[e0 + k];
-        if (A.usable[j]) {
-          valid = true;
-          s.j = j;
-          s.troad = A.target_road[j];
-          s.b = A.exit_lane[j];
-          s.outr = A.outroads[s.b];
-          s.stop = (A.lane_road[j] < 0 && A.lane_sig[j] != SIG_GREEN) ? 1 : 0;
-        }
-      }
-    }
-    if (!valid) { s.j = 0x7fffffff; s.troad = 0x7fffffff; }
-    stage[x] = s;
-    __syncwarp();
+  stage[lane_id].j = 0x7fffffff;
+  stage[lane_id].troad = 0x7fffffff;
+  __syncwarp();
+  if (el >= 0) stage[el * kMaxSucc + ek] = s;
+  __syncwarp();
+  {
+    const int l = lane_id / kMaxSucc, k = lane_id % kMaxSucc;
+    const SuccEnt me = stage[lane_id];
+    const bool valid = me.j != 0x7fffffff;
     int rank = 0, cnt = 0;
     for (int q = 0; q < kMaxSucc; ++q) {
       const SuccEnt &o = stage[l * kMaxSucc + q];
       cnt += o.j != 0x7fffffff;
-      rank += (o.troad < s.troad) || (o.troad == s.troad && o.j < s.j);
+      rank += (o.troad < me.troad) || (o.troad == me.troad && o.j < me.j);
     }
-    if (valid) T.se[l][rank] = s;
+    if (valid) T.se[l][rank] = me;
     if (l < nroad && k == 0) T.sn[l] = (uint8_t)cnt;
     __syncwarp();
     if (l < nroad && k < cnt) {
@@ -214,17 +260,12 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
       int gid = 0;
       for (int q = 1; q <= k; ++q) gid += T.se[l][q - 1].troad != T.se[l][q].troad;
       if (start) {
-        if (gid < kMaxGroups) {
-          T.gtroad[l][gid] = T.se[l][k].troad;
-          T.gbeg[l][gid] = (uint8_t)k;
-        } else {
-          T.tab_ok = 0;
-        }
+        T.gtroad[l][gid] = T.se[l][k].troad;
+        T.gbeg[l][gid] = (uint8_t)k;
       }
       if (k == cnt - 1) {
-        const int ngr = min(gid + 1, kMaxGroups);
-        T.ng[l] = (uint8_t)ngr;
-        T.gbeg[l][ngr] = (uint8_t)cnt;
+        T.ng[l] = (uint8_t)(gid + 1);
+        T.gbeg[l][gid + 1] = (uint8_t)cnt;
       }
     }
     if (l < nroad && k == 0 && cnt == 0) T.ng[l] = 0;
@@ -276,25 +317,32 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
         S.sk_vid[rank] = vj;
       }
     } else {
-      for (int j = lane_id; j < n_in; j += kThreads) {
-        const InboxRec r = inb[j];
-        const unsigned long long h = hikey(m_lane(r.meta), r.s);
-        int rank = 0;
-        for (int q = 0; q < n_in; ++q) {
-          const InboxRec o = inb[q];
-          rank += key_less(hikey(m_lane(o.meta), o.s), o.vid, h, r.vid);
-        }
-        bsort[rank] = j;
-      }
+      rank_inbox_global(inb, n_in, bsort, lane_id);
     }
   }
   __syncwarp();
-  // stayers: position = own index + #inbox keys below (binary search in the sorted inbox)
-  for (int i = lane_id; i < n_st; i += kThreads) {
-    const int gi = base + i;
-    const float s = A.in.s[gi];
-    const uint32_t meta = A.in.meta[gi];
-    const int vid = A.in.vid[gi];
+  // stayers: position = own index + #inbox keys below (binary search in the sorted inbox).
+  // Two slab rows per iteration, loads issued before the stores (more bytes in flight).
+  for (int i0 = lane_id; i0 < n_st; i0 += 2 * kThreads) {
+    float sv[2], vv[2];
+    uint32_t mv[2];
+    int idv[2], n1v[2], n2v[2], wv[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = i0 + u * kThreads;
+      if (i < n_st) {
+        const int gi = base + i;
+        sv[u] = A.in.s[gi]; vv[u] = A.in.v[gi]; mv[u] = A.in.meta[gi]; idv[u] = A.in.vid[gi];
+        n1v[u] = A.in.nxt[gi]; n2v[u] = A.in.nxt2[gi]; wv[u] = A.in.wait[gi];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+    const int i = i0 + u * kThreads;
+    if (i >= n_st) break;
+    const float s = sv[u];
+    const uint32_t meta = mv[u];
+    const int vid = idv[u];
     int pos = i;
     if (n_in > 0) {
       const unsigned long long h = hikey(m_lane(meta), s);
@@ -305,21 +353,18 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
           if (key_less(S.sk_hi[mid], S.sk_vid[mid], h, vid)) lo = mid + 1; else hi = mid;
         }
       } else {
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          const InboxRec o = inb[bsort[mid]];
-          if (key_less(hikey(m_lane(o.meta), o.s), o.vid, h, vid)) lo = mid + 1; else hi = mid;
-        }
+        lo = lower_bound_inbox_global(inb, bsort, n_in, h, vid);
       }
       pos += lo;
     }
     C.s[pos] = s;
-    C.v[pos] = A.in.v[gi];
+    C.v[pos] = vv[u];
     C.vid[pos] = vid;
-    C.nxt[pos] = A.in.nxt[gi];
-    C.nxt2[pos] = A.in.nxt2[gi];
+    C.nxt[pos] = n1v[u];
+    C.nxt2[pos] = n2v[u];
     C.meta[pos] = meta;
-    C.wait[pos] = A.in.wait[gi];
+    C.wait[pos] = wv[u];
+    }
   }
   // inbox records: position = sorted rank + #stayers below (binary search in the slab)
   for (int r = lane_id; r < n_in; r += kThreads) {

@@ -98,6 +98,7 @@ struct Part {
   int32_t *pend_off_d = nullptr, *pend_vid_d = nullptr, *pend_head_d = nullptr;
   uint8_t *usable_d = nullptr;
   int32_t *outroads_d = nullptr;
+  int32_t *desc_d = nullptr;
   long long *red_d = nullptr;
   int32_t *lanestat_d = nullptr;
   std::vector<int> tiles;                       // own tiles
@@ -154,6 +155,7 @@ struct sim_s {
   int t = 0;
   std::vector<uint8_t> dir, usable;
   std::vector<int32_t> outroads;     // [4 * n_lanes]
+  std::vector<int32_t> desc, desc_off;   // tile descriptors (dev.h)
   int64_t fin0 = 0;                  // FINISHED vehicles in the last loaded state
   long long acc_fin0 = 0;            // finished counter at the last load
   // device
@@ -223,6 +225,38 @@ sim_status upload(sim_s *h, T **p, const std::vector<T> &v) {
 
 bool is_road(const sim_s *h, int l) { return h->road[l] >= 0; }
 
+// Tile descriptors (layout in dev.h): static graph data + the usable flags /
+// reachable roads that setters change; rebuilt by compute_usable.
+void build_desc(sim_s *h) {
+  if (h->tile_lane_off.empty()) return;
+  h->desc.clear();
+  h->desc_off.assign(h->nt + 1, 0);
+  for (int T = 0; T < h->nt; ++T) {
+    const int l0 = h->tile_lane_off[T], nl = h->tile_lane_off[T + 1] - l0, nroad = h->tile_nroad[T];
+    std::vector<int32_t> ent;
+    for (int l = 0; l < nroad; ++l) {
+      const int g = h->tile_lanes[l0 + l];
+      for (int e = h->succ_off[g], k = 0; e < h->succ_off[g + 1]; ++e, ++k) {
+        const int j = h->succ[e], b = h->exit_lane[j];
+        ent.push_back(j);
+        ent.push_back(h->target_road[j]);
+        ent.push_back(b);
+        ent.push_back((is_road(h, j) ? 0 : 1) | (h->usable[j] ? 2 : 0) | (l << 8) | (k << 16));
+        for (int q = 0; q < 4; ++q) ent.push_back(h->outroads[4 * (size_t)b + q]);
+      }
+    }
+    std::vector<int32_t> w{nl, nroad, (int)(ent.size() / 8), 0};
+    for (int l = 0; l < nl; ++l) w.push_back(h->tile_lanes[l0 + l]);
+    for (int l = 0; l < nl; ++l) { float x = h->L[h->tile_lanes[l0 + l]]; int32_t b; std::memcpy(&b, &x, 4); w.push_back(b); }
+    for (int l = 0; l < nl; ++l) { float x = h->vmax[h->tile_lanes[l0 + l]]; int32_t b; std::memcpy(&b, &x, 4); w.push_back(b); }
+    for (int l = 0; l < nl; ++l) w.push_back(h->usable[h->tile_lanes[l0 + l]] ? 1 : 0);
+    w.insert(w.end(), ent.begin(), ent.end());
+    while (w.size() % 4) w.push_back(0);
+    h->desc.insert(h->desc.end(), w.begin(), w.end());
+    h->desc_off[T + 1] = (int)h->desc.size();
+  }
+}
+
 // usable(ℓ) (ledger L29, L30)
 void compute_usable(sim_s *h) {
   h->usable.assign(h->nl, 1);
@@ -253,8 +287,8 @@ void compute_usable(sim_s *h) {
       if (k < 4) o[k] = r;
       ++k;
     }
-    if (k > 4) o[3] = -2;
   }
+  build_desc(h);
 }
 
 sim_status validate_and_copy(sim_s *h, const sim_graph *g, const sim_trips *tr,
@@ -457,6 +491,20 @@ sim_status build_tiles(sim_s *h) {
     h->tile_nroad[r] = (int)lanes.size();
     std::sort(jls[r].begin(), jls[r].end());
     lanes.insert(lanes.end(), jls[r].begin(), jls[r].end());
+    if (h->tile_nroad[r] > kMaxRoadLanes)
+      return fail(h, SIM_E_INVALID, "road " + std::to_string(r) + " has more than " +
+                  std::to_string(kMaxRoadLanes) + " lanes");
+    for (int q = 0; q < h->tile_nroad[r]; ++q) {
+      const int l = lanes[q];
+      std::vector<int> tr;
+      for (int e = h->succ_off[l]; e < h->succ_off[l + 1]; ++e) tr.push_back(h->target_road[h->succ[e]]);
+      std::sort(tr.begin(), tr.end());
+      const int ntr = (int)(std::unique(tr.begin(), tr.end()) - tr.begin());
+      if (h->succ_off[l + 1] - h->succ_off[l] > kMaxSucc || ntr > kMaxGroups)
+        return fail(h, SIM_E_INVALID, "lane " + std::to_string(l) + " has more than " +
+                    std::to_string(kMaxSucc) + " successors or " + std::to_string(kMaxGroups) +
+                    " successor roads");
+    }
     if ((int)lanes.size() > kMaxTileLanes)
       return fail(h, SIM_E_INVALID, "road " + std::to_string(r) + " has more than " + std::to_string(kMaxTileLanes) + " lanes incl. outgoing junction lanes");
     int cap = 0;
@@ -687,6 +735,7 @@ sim_status upload_state(sim_s *h, const HostState &S) {
     for (int T : P.tiles) pc[T] = cnt[T];
     CK(h, cudaMemcpyAsync(P.usable_d, h->usable.data(), h->nl, cudaMemcpyHostToDevice, st));
     CK(h, cudaMemcpyAsync(P.outroads_d, h->outroads.data(), h->outroads.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(P.desc_d, h->desc.data(), h->desc.size() * 4, cudaMemcpyHostToDevice, st));
     Slab &o = P.slab[par];
     CK(h, cudaMemcpyAsync(o.s, s.data(), s.size() * 4, cudaMemcpyHostToDevice, st));
     CK(h, cudaMemcpyAsync(o.v, v.data(), v.size() * 4, cudaMemcpyHostToDevice, st));
@@ -749,6 +798,8 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   UP(i32, h->exit_lane); A.exit_lane = i32;
   AL(P.usable_d, nl); A.usable = P.usable_d;
   AL(P.outroads_d, 4 * (size_t)nl); A.outroads = reinterpret_cast<const int4 *>(P.outroads_d);
+  AL(P.desc_d, h->desc.size()); A.desc = P.desc_d;
+  UP(i32, h->desc_off); A.desc_off = i32;
   uint8_t *sig; AL(sig, nl);
   CK(h, cudaMemset(sig, 0, nl));
   A.lane_sig = sig;
@@ -1083,6 +1134,7 @@ sim_status sim_create(const sim_graph *g, const sim_trips *tr, const sim_params 
     h->own_stream = true;
   }
   h->smem = step_smem_bytes();
+  compute_usable(h);                 // usable flags, reachable roads, tile descriptors
   Plan plan;
   if (h->world > 1) plan = make_plan(h);
   const int nparts = h->loopback ? h->world : 1;
@@ -1228,6 +1280,12 @@ sim_status sim_set_lane_direction_batch(sim_handle h, int32_t m, const int32_t *
     CK(h, cudaMemcpyAsync(P.usable_d, h->stage_dir_d + h->outroads.size() * 4, h->nl,
                           cudaMemcpyDeviceToDevice, h->stream));
   }
+  // tile descriptors carry usable flags and reachable roads: stream them too
+  st = push_staging(h, h->desc.data(), h->desc.size() * 4, h->parts[0].desc_d);
+  if (st) return st;
+  for (size_t i = 1; i < h->parts.size(); ++i)
+    CK(h, cudaMemcpyAsync(h->parts[i].desc_d, h->parts[0].desc_d, h->desc.size() * 4,
+                          cudaMemcpyDeviceToDevice, h->stream));
   return SIM_OK;
 }
 

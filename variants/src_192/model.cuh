@@ -82,7 +82,6 @@ struct SuccEnt { int j, troad, b, stop; int4 outr; };  // usable successor of a 
 struct TileSh {
   int nl, nroad, tile, base, ibase, cap, icap;
   const Prof *P;                     // profile table (shared-memory copy when small)
-  int tab_ok;                        // successor table valid for this tile
   uint8_t sn[kMaxRoadLanes];         // usable successors per road lane
   uint8_t ng[kMaxRoadLanes];         // groups (distinct target roads) per road lane
   uint8_t gbeg[kMaxRoadLanes][kMaxGroups + 1];
@@ -121,40 +120,33 @@ __device__ __forceinline__ bool in4(const int4 &o, int R) {
   return o.x == R || o.y == R || o.z == R || o.w == R;
 }
 
-// cand(b, R) != empty, global lane b
-__device__ __noinline__ bool has_outroad(const StepArgs &A, int b, int R) {
-  const int4 o = __ldg(A.outroads + b);
-  if (o.w != -2) return in4(o, R);
-  int e1 = __ldg(A.succ_off + b + 1);
-  for (int e = __ldg(A.succ_off + b); e < e1; ++e) {
-    int j = __ldg(A.succ + e);
-    if (A.usable[j] && __ldg(A.target_road + j) == R) return true;
-  }
-  return false;
+// cand(b, R) != empty, global lane b: the distinct roads
+// reachable through usable successors (<= 4 per lane, validated at create)
+__device__ __forceinline__ bool has_outroad(const StepArgs &A, int b, int R) {
+  return in4(__ldg(A.outroads + b), R);
 }
-__device__ __forceinline__ bool pref_ok(const StepArgs &A, const int4 &outr, int b, int R2) {
-  if (R2 < 0) return true;
-  return outr.w != -2 ? in4(outr, R2) : has_outroad(A, b, R2);
+__device__ __forceinline__ bool pref_ok(const int4 &outr, int R2) {
+  return R2 < 0 || in4(outr, R2);
 }
 
 // next lane from road lane m toward road R1 with preference toward R2 (ledger L24)
-__device__ __noinline__ int next_from_road(const StepArgs &A, int m, int R1, int R2) {
+__device__ __forceinline__ int next_from_road(const StepArgs &A, int m, int R1, int R2) {
   if (R1 < 0) return kLaneDest;
   int best_any = kLaneBlocked, best_pref = kLaneBlocked;
   int e1 = __ldg(A.succ_off + m + 1);
+#pragma unroll 1
   for (int e = __ldg(A.succ_off + m); e < e1; ++e) {
     int j = __ldg(A.succ + e);
     if (!A.usable[j] || __ldg(A.target_road + j) != R1) continue;
     if (best_any < 0 || j < best_any) best_any = j;
     const int b = __ldg(A.exit_lane + j);
-    if (pref_ok(A, __ldg(A.outroads + b), b, R2) && (best_pref < 0 || j < best_pref)) best_pref = j;
+    if (pref_ok(__ldg(A.outroads + b), R2) && (best_pref < 0 || j < best_pref)) best_pref = j;
   }
   return best_pref >= 0 ? best_pref : best_any;
 }
 // the same two predicates for a road lane of this tile, from the shared-memory
 // successor table (built per step; usable successors only)
 __device__ __forceinline__ bool has_outroad_t(const StepArgs &A, const TileSh &T, int a, int R) {
-  if (!T.tab_ok) return has_outroad(A, T.glob[a], R);
   for (int g = 0; g < T.ng[a]; ++g)
     if (T.gtroad[a][g] == R) return true;
   return false;
@@ -167,7 +159,6 @@ __device__ __forceinline__ Next next_stop_g(const StepArgs &A, int j) {
   return n;
 }
 __device__ __forceinline__ Next next1_t(const StepArgs &A, const TileSh &T, int l, int R1, int R2) {
-  if (!T.tab_ok) return next_stop_g(A, next_from_road(A, T.glob[l], R1, R2));
   if (R1 < 0) return Next{kLaneDest, false};
   for (int g = 0; g < T.ng[l]; ++g) {
     if (T.gtroad[l][g] != R1) continue;
@@ -176,7 +167,7 @@ __device__ __forceinline__ Next next1_t(const StepArgs &A, const TileSh &T, int 
     // whose exit lane continues toward R2 is the preferred one (ledger L24)
     for (int k = b; k < e; ++k) {
       const SuccEnt &x = T.se[l][k];
-      if (pref_ok(A, x.outr, x.b, R2)) return Next{x.j, x.stop != 0};
+      if (pref_ok(x.outr, R2)) return Next{x.j, x.stop != 0};
     }
     return Next{T.se[l][b].j, T.se[l][b].stop != 0};
   }
@@ -362,19 +353,16 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
   const R L = (R)T.len[l];
   const int lead = (i + 1 < T.seg_end[l]) ? i + 1 : -1;
   const int of = (i > T.seg_start[l]) ? i - 1 : -1;
-  LEv<R> cur = eval_lane<R, GUARD>(A, T, C, l, lead, s, v, p, me, g);
-  o.leader = cur.leader;
-  o.hops = cur.hops;
-  o.phantom = cur.phantom;
   o.of_vid = of >= 0 ? C.vid[of] : -1;
   o.side[0] = o.side[1] = o.side[2] = o.side[3] = -1;
-  LEv<R> use = cur;
-  int lc = 0, new_l = l;
   const R b_hard = (R)A.b_hard;
+  // ---- lane-change eligibility: needs no lane evaluation ----
+  const bool dest = me.nxt < 0;
+  bool inG = true, consider = false;
+  int mand = 0;
+  int sl0 = -1, sl1 = -1, f0 = -1, f1 = -1, b0 = -1, b1 = -1;
   if (T.isroad[l]) {                                     // no LC in junction lanes
-    const bool dest = me.nxt < 0;
-    const bool inG = dest || cur.next1 != kLaneBlocked;
-    int mand = 0;
+    inG = dest || has_outroad_t(A, T, l, me.nxt);        // l in G <=> next1 != BLOCKED
     if (!inG) {                                          // ledger L18, L37
       bool left_ok = false, right_ok = false;
       for (int a = 0; a < T.nroad; ++a) {
@@ -387,130 +375,144 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
     const R rem = M::sub(L, s);
     const R need = M::add(p.s0, M::mul(v, p.T));
     const bool l19 = rem < need;                         // ledger L19
-    if (GUARD && inG && v != (R)0 && fabsf((float)(rem - need)) <= kEpsPos * (float)(fabs(rem) + need)) g.hit = true, g.why |= (1u << 2);
-    int sl[2] = {T.left[l], T.right[l]};
-    int front[2] = {-1, -1}, back[2] = {-1, -1};
-#pragma unroll
-    for (int sd = 0; sd < 2; ++sd) {
-      if (sl[sd] < 0) continue;
-      int a = T.seg_start[sl[sd]], b = T.seg_end[sl[sd]];
-      int f = upper_bound_s(C, a, b, C.s[i]);
-      front[sd] = f < b ? f : -1;
-      back[sd] = f > a ? f - 1 : -1;
-      o.side[2 * sd] = front[sd] >= 0 ? C.vid[front[sd]] : -1;
-      o.side[2 * sd + 1] = back[sd] >= 0 ? C.vid[back[sd]] : -1;
+    if (GUARD && inG && v != (R)0 && fabsf((float)(rem - need)) <= kEpsPos * (float)(fabs(rem) + need))
+      g.hit = true, g.why |= (1u << 2);
+    sl0 = T.left[l];
+    sl1 = T.right[l];
+#pragma unroll 1
+    for (int sd = 0; sd < 2; ++sd) {                     // side pointers (ties -> back, L11)
+      const int ls = sd == 0 ? sl0 : sl1;
+      if (ls < 0) continue;
+      const int a = T.seg_start[ls], b = T.seg_end[ls];
+      const int f = upper_bound_s(C, a, b, C.s[i]);
+      const int fr = f < b ? f : -1, bk = f > a ? f - 1 : -1;
+      if (sd == 0) { f0 = fr; b0 = bk; } else { f1 = fr; b1 = bk; }
+      o.side[2 * sd] = fr >= 0 ? C.vid[fr] : -1;
+      o.side[2 * sd + 1] = bk >= 0 ? C.vid[bk] : -1;
     }
-    const bool consider = inG ? !l19 : (mand != 0);
-    if (consider) {
-      R a_of = (R)0, a_of_new = (R)0;                    // old follower (L10)
-      if (of >= 0) {
-        const PV<R> po = pvals(T.P[m_prof(C.meta[of])], (R)0);
-        const R so = (R)C.s[of], vo = (R)C.v[of];
-        const R v0o = (po.vmax < (R)T.vmax[l]) ? po.vmax : (R)T.vmax[l];
-        a_of = idm<R, GUARD>(vo, v0o, true, M::sub(M::sub(s, so), p.len), M::sub(vo, v), po,
-                             b_hard, fabs(s - so) + p.len, g);
-        if (lead >= 0) {
-          const R sl_ = (R)C.s[lead];
-          const R ll_ = (R)T.P[m_prof(C.meta[lead])].len;
-          a_of_new = idm<R, GUARD>(vo, v0o, true, M::sub(M::sub(sl_, so), ll_),
-                                   M::sub(vo, (R)C.v[lead]), po, b_hard, fabs(sl_ - so) + ll_, g);
-        } else {
-          a_of_new = idm<R, GUARD>(vo, v0o, false, (R)0, (R)0, po, b_hard, (R)0, g);
-        }
-      }
-      bool adm[2] = {false, false};
-      R u[2] = {(R)0, (R)0};
-      LEv<R> ev[2];
-#pragma unroll
-      for (int sd = 0; sd < 2; ++sd) {
-        const int ls = sl[sd];
-        const int sgn = sd == 0 ? -1 : 1;
-        if (ls < 0 || !T.usable[ls]) continue;
-        if (inG && !(dest || has_outroad_t(A, T, ls, me.nxt))) continue;
-        if (!inG && sgn != mand) continue;
-        ev[sd] = eval_lane<R, GUARD>(A, T, C, ls, front[sd], s, v, p, me, g);
-        R a_nf = (R)0, a_nf_new = (R)0;
-        bool ok = true;
-        if (back[sd] >= 0) {
-          const int bi = back[sd];
-          const PV<R> pb = pvals(T.P[m_prof(C.meta[bi])], (R)0);
-          const R sb = (R)C.s[bi], vb = (R)C.v[bi];
-          const R v0b = (pb.vmax < (R)T.vmax[ls]) ? pb.vmax : (R)T.vmax[ls];
-          if (front[sd] >= 0) {
-            const int fi = front[sd];
-            const R sf = (R)C.s[fi];
-            const R lf = (R)T.P[m_prof(C.meta[fi])].len;
-            a_nf = idm<R, GUARD>(vb, v0b, true, M::sub(M::sub(sf, sb), lf),
-                                 M::sub(vb, (R)C.v[fi]), pb, b_hard, fabs(sf - sb) + lf, g);
-          } else {
-            a_nf = idm<R, GUARD>(vb, v0b, false, (R)0, (R)0, pb, b_hard, (R)0, g);
-          }
-          const R gb = M::sub(M::sub(s, sb), p.len);
-          a_nf_new = idm<R, GUARD>(vb, v0b, true, gb, M::sub(vb, v), pb, b_hard, fabs(s - sb) + p.len, g);
-          if (GUARD && fabsf((float)(a_nf_new + (R)A.b_safe)) <= kEpsAcc) g.hit = true, g.why |= (1u << 3);
-          if (!(a_nf_new >= -(R)A.b_safe)) ok = false;  // L17 (1)
-          if (!(gb >= (R)0)) ok = false;                 // L17 (2)
-        } else {
-          const R mrg = M::sub(s, p.len);
-          if (GUARD && fabs((double)mrg - A.start_margin) <= (double)kEpsPos * ((double)s + A.start_margin))
-            g.hit = true, g.why |= (1u << 4);
-          if (!(mrg >= (R)A.start_margin)) ok = false;  // L17 (3) lane-start rule
-        }
-        if (front[sd] >= 0) {
-          const int fi = front[sd];
-          const R sf = (R)C.s[fi];
-          const R lf = (R)T.P[m_prof(C.meta[fi])].len;
-          const R gf = M::sub(M::sub(sf, s), lf);
-          if (GUARD && fabsf((float)gf) <= kEpsPos * (float)(fabs(sf - s) + lf)) g.hit = true, g.why |= (1u << 5);
-          if (!(gf >= (R)0)) ok = false;                 // L17 (2)
-        }
-        // MOBIL utility (tilde = after the change, ledger L13)
-        u[sd] = M::add(M::sub(ev[sd].a, cur.a),
-                       M::mul((R)A.polite, M::add(M::sub(a_nf_new, a_nf), M::sub(a_of_new, a_of))));
-        adm[sd] = ok;
-      }
-      int choice = -1;
-      if (inG) {
-        if (adm[0] || adm[1]) {
-          R u0 = adm[0] ? (((R)0 < u[0]) ? u[0] : (R)0) : (R)0;
-          R u1 = adm[1] ? (((R)0 < u[1]) ? u[1] : (R)0) : (R)0;
-          R uT = M::add(u0, u1);
-          double pl;                                     // P:188-194, ledger L14
-          if (uT >= (R)1) pl = 0.9;
-          else if (uT > (R)0) pl = (double)M::mul((R)(0.9 - 2e-8), uT);
-          else pl = 2e-8;
-          // U53 of Philox4x32-10(seed; vid, t) (ledger L16)
-          uint32_t c0 = (uint32_t)me.vid, c1 = (uint32_t)A.t, c2 = 0u, c3 = 0u;
-          uint32_t k0 = (uint32_t)(A.seed & 0xffffffffull), k1 = (uint32_t)(A.seed >> 32);
-#pragma unroll
-          for (int r = 0; r < 10; ++r) {
-            uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
-            uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
-            uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
-            c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
-            k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
-          }
-          const uint64_t mant = ((uint64_t)(c0 >> 5) << 26) + (uint64_t)(c1 >> 6);
-          const double r = (double)mant * (1.0 / 9007199254740992.0);
-          if (GUARD && fabs(r - pl) <= (double)kEpsP) g.hit = true, g.why |= (1u << 6);
-          if (r < pl) {                                  // P:196, ledger L15
-            if (adm[0] && adm[1]) {
-              if (GUARD && fabsf((float)(u[0] - u[1])) <= kEpsAcc) g.hit = true, g.why |= (1u << 7);
-              choice = (u[0] >= u[1]) ? 0 : 1;
-            } else {
-              choice = adm[0] ? 0 : 1;
-            }
-          }
-        }
+    consider = inG ? !l19 : (mand != 0);
+  }
+  bool want0 = false, want1 = false;
+  if (consider) {
+    want0 = sl0 >= 0 && T.usable[sl0] &&
+            (inG ? (dest || has_outroad_t(A, T, sl0, me.nxt)) : mand == -1);
+    want1 = sl1 >= 0 && T.usable[sl1] &&
+            (inG ? (dest || has_outroad_t(A, T, sl1, me.nxt)) : mand == 1);
+  }
+  // ---- O4-O6 on the current lane and on each candidate side lane (one
+  // evaluation site, so the lane evaluation is instantiated once) ----
+  LEv<R> cur, ev0, ev1;
+#pragma unroll 1
+  for (int k = 0; k < 3; ++k) {
+    if ((k == 1 && !want0) || (k == 2 && !want1)) continue;
+    const int ll = k == 0 ? l : (k == 1 ? sl0 : sl1);
+    const int li = k == 0 ? lead : (k == 1 ? f0 : f1);
+    const LEv<R> e = eval_lane<R, GUARD>(A, T, C, ll, li, s, v, p, me, g);
+    if (k == 0) cur = e;
+    else if (k == 1) ev0 = e;
+    else ev1 = e;
+  }
+  o.leader = cur.leader;
+  o.hops = cur.hops;
+  o.phantom = cur.phantom;
+  LEv<R> use = cur;
+  int lc = 0, new_l = l;
+  if (consider) {
+    R a_of = (R)0, a_of_new = (R)0;                      // old follower (L10)
+    if (of >= 0) {
+      const PV<R> po = pvals(T.P[m_prof(C.meta[of])], (R)0);
+      const R so = (R)C.s[of], vo = (R)C.v[of];
+      const R v0o = (po.vmax < (R)T.vmax[l]) ? po.vmax : (R)T.vmax[l];
+      a_of = idm<R, GUARD>(vo, v0o, true, M::sub(M::sub(s, so), p.len), M::sub(vo, v), po,
+                           b_hard, fabs(s - so) + p.len, g);
+      const int li = lead >= 0 ? lead : i;               // free road if the ego has no leader
+      const R sl_ = (R)C.s[li];
+      const R ll_ = (R)T.P[m_prof(C.meta[li])].len;
+      a_of_new = idm<R, GUARD>(vo, v0o, lead >= 0, M::sub(M::sub(sl_, so), ll_),
+                               M::sub(vo, (R)C.v[li]), po, b_hard, fabs(sl_ - so) + ll_, g);
+    }
+    bool adm0 = false, adm1 = false;
+    R u0 = (R)0, u1 = (R)0;
+#pragma unroll 1
+    for (int sd = 0; sd < 2; ++sd) {
+      if (!(sd == 0 ? want0 : want1)) continue;
+      const int ls = sd == 0 ? sl0 : sl1;
+      const int fi = sd == 0 ? f0 : f1, bi = sd == 0 ? b0 : b1;
+      const R ea = sd == 0 ? ev0.a : ev1.a;
+      R a_nf = (R)0, a_nf_new = (R)0;
+      bool ok = true;
+      if (bi >= 0) {
+        const PV<R> pb = pvals(T.P[m_prof(C.meta[bi])], (R)0);
+        const R sb = (R)C.s[bi], vb = (R)C.v[bi];
+        const R v0b = (pb.vmax < (R)T.vmax[ls]) ? pb.vmax : (R)T.vmax[ls];
+        const int fj = fi >= 0 ? fi : bi;                // free road if no front
+        const R sf = (R)C.s[fj];
+        const R lf = (R)T.P[m_prof(C.meta[fj])].len;
+        a_nf = idm<R, GUARD>(vb, v0b, fi >= 0, M::sub(M::sub(sf, sb), lf),
+                             M::sub(vb, (R)C.v[fj]), pb, b_hard, fabs(sf - sb) + lf, g);
+        const R gb = M::sub(M::sub(s, sb), p.len);
+        a_nf_new = idm<R, GUARD>(vb, v0b, true, gb, M::sub(vb, v), pb, b_hard, fabs(s - sb) + p.len, g);
+        if (GUARD && fabsf((float)(a_nf_new + (R)A.b_safe)) <= kEpsAcc) g.hit = true, g.why |= (1u << 3);
+        if (!(a_nf_new >= -(R)A.b_safe)) ok = false;    // L17 (1)
+        if (!(gb >= (R)0)) ok = false;                   // L17 (2)
       } else {
-        const int sd = mand < 0 ? 0 : 1;
-        if (adm[sd]) choice = sd;                        // ledger L18
+        const R mrg = M::sub(s, p.len);
+        if (GUARD && fabsf((float)mrg - (float)A.start_margin) <= kEpsPos * ((float)s + (float)A.start_margin))
+          g.hit = true, g.why |= (1u << 4);
+        if (!(mrg >= (R)A.start_margin)) ok = false;    // L17 (3) lane-start rule
       }
-      if (choice >= 0) {
-        use = choice == 0 ? ev[0] : ev[1];
-        lc = choice == 0 ? -1 : 1;
-        new_l = choice == 0 ? sl[0] : sl[1];
+      if (fi >= 0) {
+        const R sf = (R)C.s[fi];
+        const R lf = (R)T.P[m_prof(C.meta[fi])].len;
+        const R gf = M::sub(M::sub(sf, s), lf);
+        if (GUARD && fabsf((float)gf) <= kEpsPos * (float)(fabs(sf - s) + lf)) g.hit = true, g.why |= (1u << 5);
+        if (!(gf >= (R)0)) ok = false;                   // L17 (2)
       }
+      // MOBIL utility (tilde = after the change, ledger L13)
+      const R u = M::add(M::sub(ea, cur.a),
+                         M::mul((R)A.polite, M::add(M::sub(a_nf_new, a_nf), M::sub(a_of_new, a_of))));
+      if (sd == 0) { u0 = u; adm0 = ok; } else { u1 = u; adm1 = ok; }
+    }
+    int choice = -1;
+    if (inG) {
+      if (adm0 || adm1) {
+        const R p0 = adm0 ? (((R)0 < u0) ? u0 : (R)0) : (R)0;
+        const R p1 = adm1 ? (((R)0 < u1) ? u1 : (R)0) : (R)0;
+        const R uT = M::add(p0, p1);
+        double pl;                                       // P:188-194, ledger L14
+        if (uT >= (R)1) pl = 0.9;
+        else if (uT > (R)0) pl = (double)M::mul((R)(0.9 - 2e-8), uT);
+        else pl = 2e-8;
+        // U53 of Philox4x32-10(seed; vid, t) (ledger L16)
+        uint32_t c0 = (uint32_t)me.vid, c1 = (uint32_t)A.t, c2 = 0u, c3 = 0u;
+        uint32_t k0 = (uint32_t)(A.seed & 0xffffffffull), k1 = (uint32_t)(A.seed >> 32);
+#pragma unroll
+        for (int r = 0; r < 10; ++r) {
+          uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+          uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+          uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+          c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+          k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+        }
+        const uint64_t mant = ((uint64_t)(c0 >> 5) << 26) + (uint64_t)(c1 >> 6);
+        const double r = (double)mant * (1.0 / 9007199254740992.0);
+        if (GUARD && fabs(r - pl) <= (double)kEpsP) g.hit = true, g.why |= (1u << 6);
+        if (r < pl) {                                    // P:196, ledger L15
+          if (adm0 && adm1) {
+            if (GUARD && fabsf((float)(u0 - u1)) <= kEpsAcc) g.hit = true, g.why |= (1u << 7);
+            choice = (u0 >= u1) ? 0 : 1;
+          } else {
+            choice = adm0 ? 0 : 1;
+          }
+        }
+      }
+    } else {
+      if (mand < 0 ? adm0 : adm1) choice = mand < 0 ? 0 : 1;   // ledger L18
+    }
+    if (choice >= 0) {
+      use = choice == 0 ? ev0 : ev1;
+      lc = choice == 0 ? -1 : 1;
+      new_l = choice == 0 ? sl0 : sl1;
     }
   }
   // O8 integrate (ledger L1) + clamp (L22, L23).  The fp64 path follows the
@@ -551,9 +553,10 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
   R pb = M::fp64 ? s1 : s;
   R pa = M::fp64 ? (R)0 : adv;
   int curg = T.glob[new_l], ri = me.cur, n = use.next1, hand = 0;
+  bool croad = T.isroad[new_l];                          // current lane: tile-local until a hand-off
+  R Lc = (R)T.len[new_l];
   bool fin = false;
   for (;;) {
-    const bool croad = __ldg(A.lane_road + curg) >= 0;
     const bool dest_road = croad && route_at(A, me.vid, me.cur, me.nxt, me.nxt2, ri + 1) < 0;
     if (dest_road) {
       const R es = (R)__ldg(A.end_s + me.vid);
@@ -563,7 +566,6 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
         g.hit = true, g.why |= (1u << 10);
       if (pa >= rem) { fin = true; break; }
     }
-    const R Lc = (R)__ldg(A.lane_len + curg);
     const R rem = M::sub(Lc, pb);
     if (GUARD && n >= 0 && !(adv_zero && hand == 0) &&
         fabsf((float)(pa - rem)) <= kEpsPos * (float)(fabs(pa) + fabs(rem) + (R)1e-3))
@@ -572,6 +574,8 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
       pb = M::sub(pb, Lc);
       curg = n;
       const bool nroad = __ldg(A.lane_road + curg) >= 0;
+      croad = nroad;
+      Lc = (R)__ldg(A.lane_len + curg);
       if (nroad) ri += 1;
       hand += 1;
       if (nroad) {
