@@ -196,3 +196,59 @@ def test_boundary_status_codes(simlib):
     with pytest.raises(simlib.SimError) as e:
         simlib.Sim(bad, scen.trips, scen.profiles, scen.params)
     assert e.value.status == simlib.SIM_E_INVALID
+
+
+@pytest.mark.parametrize("warm", [0, 40])
+def test_full_size_c4_one_step_parity(simlib, oracle_lib, warm):
+    """BASELINE.json full size (C4: 2M vehicles, ~133k lanes) in the launch
+    configuration bench.py times (default fp32 + guard path): after `warm`
+    GPU steps, the GPU state is loaded into the oracle and both advance one
+    step; every vehicle's decisions and state are compared."""
+    scen = synth.city()                                   # C4 recipe, seed 4
+    g = simlib.Sim.from_scenario(scen, record_decisions=True)
+    if warm:
+        g.step(warm)
+    st = g.read_state()
+    st["s"] = st["s"].astype(np.float64)
+    st["v"] = st["v"].astype(np.float64)
+    o = oracle_lib.Oracle(scen)
+    o.load_state(st)
+    g.step(1)
+    o.step(1)
+    compare_decisions(g.read_decisions(), o.decisions(), st["status"], where=f"[C4 warm={warm}] ")
+    gs, os_ = g.read_state(lane_order=True), o.read_state()
+    compare_states(gs, os_, where=f"[C4 warm={warm}] ")
+    o_off, o_ord = o.lane_order()
+    compare_lane_orders(gs["lane_offsets"], gs["lane_order"], o_off, o_ord, gs)
+    m = g.read_metrics()
+    assert m["n_driving"] + m["n_finished"] + m["n_pending"] == scen.n_trips
+
+
+def test_full_size_c3_dynamic_tidal_parity(simlib, oracle_lib):
+    """BASELINE.json configs[2]: 20x20 grid, 3 lanes + tidal centre lane +
+    dynamic middle lane, 200k trips.  A rule controller flips the dynamic lanes
+    every 30 steps and the tidal lanes every 60; then one step
+    from the GPU state is compared with the oracle for every vehicle."""
+    scen = synth.grid(rows=20, cols=20, road_len=500.0, lanes=3, n_trips=200_000,
+                      depart_window=1200, seed=3, tidal=True, dynamic=True)
+    g = simlib.Sim.from_scenario(scen, record_decisions=True)
+    kinds = scen.graph["lane_kind"]
+    dyn = np.where(kinds == 1)[0]
+    tid = np.where((kinds == 2) & (scen.graph["tidal_partner"] > np.arange(scen.n_lanes)))[0]
+    for t in range(0, 120, 30):
+        m = g.read_metrics(lane_stats=True)
+        wait = m["lane_waiting_at_end"]
+        g.set_lane_direction_batch(dyn, (wait[dyn] > 2).astype(np.int32))
+        if t % 60 == 0:
+            g.set_lane_direction_batch(tid, ((t // 60) % 2) * np.ones(len(tid), np.int32))
+        g.step(30)
+    st = g.read_state()
+    st["s"] = st["s"].astype(np.float64)
+    st["v"] = st["v"].astype(np.float64)
+    o = oracle_lib.Oracle(scen)
+    o.load_state(st)
+    g.step(1)
+    o.step(1)
+    compare_decisions(g.read_decisions(), o.decisions(), st["status"], where="[C3] ")
+    compare_states(g.read_state(), o.read_state(), where="[C3] ")
+    assert (st["status"] == 1).sum() > 3_000
