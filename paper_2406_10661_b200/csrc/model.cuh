@@ -399,25 +399,12 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
     want1 = sl1 >= 0 && T.usable[sl1] &&
             (inG ? (dest || has_outroad_t(A, T, sl1, me.nxt)) : mand == 1);
   }
-  // ---- O4-O6 on the current lane and on each candidate side lane (one
-  // evaluation site, so the lane evaluation is instantiated once) ----
-  LEv<R> cur, ev0, ev1;
-#pragma unroll 1
-  for (int k = 0; k < 3; ++k) {
-    if ((k == 1 && !want0) || (k == 2 && !want1)) continue;
-    const int ll = k == 0 ? l : (k == 1 ? sl0 : sl1);
-    const int li = k == 0 ? lead : (k == 1 ? f0 : f1);
-    const LEv<R> e = eval_lane<R, GUARD>(A, T, C, ll, li, s, v, p, me, g);
-    if (k == 0) cur = e;
-    else if (k == 1) ev0 = e;
-    else ev1 = e;
-  }
-  o.leader = cur.leader;
-  o.hops = cur.hops;
-  o.phantom = cur.phantom;
-  LEv<R> use = cur;
-  int lc = 0, new_l = l;
-  if (consider) {
+  // ---- MOBIL terms that need no lane evaluation: the politeness terms and
+  // the safety / gap admissibility of each side (L10, L13, L17) ----
+  bool adm0 = false, adm1 = false;
+  R pol0 = (R)0, pol1 = (R)0;                            // (ã_nf - a_nf) + (ã_of - a_of)
+  double r = 1.0;                                        // U53 draw (L16), discretionary only
+  if (want0 || want1) {
     R a_of = (R)0, a_of_new = (R)0;                      // old follower (L10)
     if (of >= 0) {
       const PV<R> po = pvals(T.P[m_prof(C.meta[of])], (R)0);
@@ -431,14 +418,11 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
       a_of_new = idm<R, GUARD>(vo, v0o, lead >= 0, M::sub(M::sub(sl_, so), ll_),
                                M::sub(vo, (R)C.v[li]), po, b_hard, fabs(sl_ - so) + ll_, g);
     }
-    bool adm0 = false, adm1 = false;
-    R u0 = (R)0, u1 = (R)0;
 #pragma unroll 1
     for (int sd = 0; sd < 2; ++sd) {
       if (!(sd == 0 ? want0 : want1)) continue;
       const int ls = sd == 0 ? sl0 : sl1;
       const int fi = sd == 0 ? f0 : f1, bi = sd == 0 ? b0 : b1;
-      const R ea = sd == 0 ? ev0.a : ev1.a;
       R a_nf = (R)0, a_nf_new = (R)0;
       bool ok = true;
       if (bi >= 0) {
@@ -468,46 +452,93 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
         if (GUARD && fabsf((float)gf) <= kEpsPos * (float)(fabs(sf - s) + lf)) g.hit = true, g.why |= (1u << 5);
         if (!(gf >= (R)0)) ok = false;                   // L17 (2)
       }
-      // MOBIL utility (P:174-176; tilde = after the change, ledger L13)
-      const R u = M::add(M::sub(ea, cur.a),
-                         M::mul((R)A.polite, M::add(M::sub(a_nf_new, a_nf), M::sub(a_of_new, a_of))));
-      if (sd == 0) { u0 = u; adm0 = ok; } else { u1 = u; adm1 = ok; }
+      const R pol = M::add(M::sub(a_nf_new, a_nf), M::sub(a_of_new, a_of));
+      if (sd == 0) { pol0 = pol; adm0 = ok; } else { pol1 = pol; adm1 = ok; }
     }
+    if (inG && (adm0 || adm1)) {
+      // U53 of Philox4x32-10(seed; vid, t) (ledger L16)
+      uint32_t c0 = (uint32_t)me.vid, c1 = (uint32_t)A.t, c2 = 0u, c3 = 0u;
+      uint32_t k0 = (uint32_t)(A.seed & 0xffffffffull), k1 = (uint32_t)(A.seed >> 32);
+#pragma unroll
+      for (int rr = 0; rr < 10; ++rr) {
+        uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+        uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+        uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+        k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+      }
+      const uint64_t mant = ((uint64_t)(c0 >> 5) << 26) + (uint64_t)(c1 >> 6);
+      r = (double)mant * (1.0 / 9007199254740992.0);
+    }
+  }
+  // ---- O4-O6 on the current lane and on the admissible side lanes (one
+  // evaluation site, so the lane evaluation is instantiated once).  On the
+  // fp32 path a side is evaluated only if the draw can still fall below p_LC:
+  // with F = the free-road IDM bound of ã_ego on that lane, u <= (F - a_cur) +
+  // p * pol, and p_LC is monotone in u_T apart from its 2e-8 floor, so
+  // r >= p_LC(upper bound) + 1e-3 decides "stay" exactly ----
+  LEv<R> cur, ev0, ev1;
+  bool need0 = false, need1 = false;
+#pragma unroll 1
+  for (int k = 0; k < 3; ++k) {
+    if (k == 1) {
+      need0 = adm0 && (inG || mand < 0);
+      need1 = adm1 && (inG || mand > 0);
+      if (GUARD && inG && (need0 || need1)) {
+        R ub = (R)0;
+#pragma unroll 1
+        for (int sd = 0; sd < 2; ++sd) {
+          if (!(sd == 0 ? need0 : need1)) continue;
+          const int ls = sd == 0 ? sl0 : sl1;
+          const R v0s = (p.vmax < (R)T.vmax[ls]) ? p.vmax : (R)T.vmax[ls];
+          const R x = M::div(v, v0s);
+          const R x2 = M::mul(x, x);
+          R F = M::mul(p.a_max, M::sub((R)1, M::mul(x2, x2)));
+          F = (F < -b_hard) ? -b_hard : F;
+          const R U = M::add(M::sub(F, cur.a), M::mul((R)A.polite, sd == 0 ? pol0 : pol1));
+          ub = M::add(ub, ((R)0 < U) ? U : (R)0);
+        }
+        const double pmax = ub >= (R)1 ? 0.9 : fmax(2e-8, (double)(0.9 - 2e-8) * (double)ub);
+        if (r >= pmax + 1e-3) need0 = need1 = false;   // no change, for certain
+      }
+    }
+    if ((k == 1 && !need0) || (k == 2 && !need1)) continue;
+    const int ll = k == 0 ? l : (k == 1 ? sl0 : sl1);
+    const int li = k == 0 ? lead : (k == 1 ? f0 : f1);
+    const LEv<R> e = eval_lane<R, GUARD>(A, T, C, ll, li, s, v, p, me, g);
+    if (k == 0) cur = e;
+    else if (k == 1) ev0 = e;
+    else ev1 = e;
+  }
+  o.leader = cur.leader;
+  o.hops = cur.hops;
+  o.phantom = cur.phantom;
+  LEv<R> use = cur;
+  int lc = 0, new_l = l;
+  if (need0 || need1) {
     int choice = -1;
     if (inG) {
-      if (adm0 || adm1) {
-        const R p0 = adm0 ? (((R)0 < u0) ? u0 : (R)0) : (R)0;
-        const R p1 = adm1 ? (((R)0 < u1) ? u1 : (R)0) : (R)0;
-        const R uT = M::add(p0, p1);
-        double pl;                                       // P:188-194, ledger L14
-        if (uT >= (R)1) pl = 0.9;
-        else if (uT > (R)0) pl = (double)M::mul((R)(0.9 - 2e-8), uT);
-        else pl = 2e-8;
-        // U53 of Philox4x32-10(seed; vid, t) (ledger L16)
-        uint32_t c0 = (uint32_t)me.vid, c1 = (uint32_t)A.t, c2 = 0u, c3 = 0u;
-        uint32_t k0 = (uint32_t)(A.seed & 0xffffffffull), k1 = (uint32_t)(A.seed >> 32);
-#pragma unroll
-        for (int r = 0; r < 10; ++r) {
-          uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
-          uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
-          uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
-          c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
-          k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
-        }
-        const uint64_t mant = ((uint64_t)(c0 >> 5) << 26) + (uint64_t)(c1 >> 6);
-        const double r = (double)mant * (1.0 / 9007199254740992.0);
-        if (GUARD && fabs(r - pl) <= (double)kEpsP) g.hit = true, g.why |= (1u << 6);
-        if (r < pl) {                                    // P:196, ledger L15
-          if (adm0 && adm1) {
-            if (GUARD && fabsf((float)(u0 - u1)) <= kEpsAcc) g.hit = true, g.why |= (1u << 7);
-            choice = (u0 >= u1) ? 0 : 1;
-          } else {
-            choice = adm0 ? 0 : 1;
-          }
+      // MOBIL utility (P:174-176; tilde = after the change, ledger L13)
+      const R u0 = need0 ? M::add(M::sub(ev0.a, cur.a), M::mul((R)A.polite, pol0)) : (R)0;
+      const R u1 = need1 ? M::add(M::sub(ev1.a, cur.a), M::mul((R)A.polite, pol1)) : (R)0;
+      const R p0 = need0 ? (((R)0 < u0) ? u0 : (R)0) : (R)0;
+      const R p1 = need1 ? (((R)0 < u1) ? u1 : (R)0) : (R)0;
+      const R uT = M::add(p0, p1);
+      double pl;                                         // P:188-194, ledger L14
+      if (uT >= (R)1) pl = 0.9;
+      else if (uT > (R)0) pl = (double)M::mul((R)(0.9 - 2e-8), uT);
+      else pl = 2e-8;
+      if (GUARD && fabs(r - pl) <= (double)kEpsP) g.hit = true, g.why |= (1u << 6);
+      if (r < pl) {                                      // P:196, ledger L15
+        if (need0 && need1) {
+          if (GUARD && fabsf((float)(u0 - u1)) <= kEpsAcc) g.hit = true, g.why |= (1u << 7);
+          choice = (u0 >= u1) ? 0 : 1;
+        } else {
+          choice = need0 ? 0 : 1;
         }
       }
     } else {
-      if (mand < 0 ? adm0 : adm1) choice = mand < 0 ? 0 : 1;   // ledger L18
+      choice = mand < 0 ? 0 : 1;                         // ledger L18: admissible -> change
     }
     if (choice >= 0) {
       use = choice == 0 ? ev0 : ev1;

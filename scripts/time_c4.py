@@ -37,5 +37,6 @@ try:
         names = ["idm_gap", "lim_select", "l19", "b_safe", "lane_start", "front_gap", "r_vs_p",
                  "uL_vs_uR", "clamp_bind", "clamp_overlap", "arrival", "handoff", "wait"]
         print({names[i]: buf[i] for i in range(len(names))})
+        print("want", buf[20], "admissible", buf[21], "evaluated", buf[22], "vehicles", buf[23])
 except AttributeError:
     pass
