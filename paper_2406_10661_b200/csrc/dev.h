@@ -25,11 +25,14 @@ constexpr int kNAcc = 12;            // per-tile int64 accumulators
 constexpr int kMaxRoadLanes = 4;     // road lanes per tile cached in the successor table
 constexpr int kMaxSucc = 8;          // successors per road lane cached in the table
 static_assert(kMaxRoadLanes * kMaxSucc == 32, "one warp builds the successor table");
-// tile descriptor (int32 words, 16-B padded): [nl, nroad, ne, 0], glob[nl], len[nl],
-// vmax[nl], flags[nl] (bit0 usable), then ne <= 32 successor entries of the
-// road lanes, 8 words each: j, target road, exit lane, flags (bit0 junction lane,
-// bit1 usable, lane_local << 8, k << 16), outroads(exit lane) x4
-constexpr int kDescMaxWords = 4 + 4 * kMaxTileLanes + 8 * kMaxRoadLanes * kMaxSucc;
+// tile descriptor (int32 words, 16-B padded, host-built by build_desc and
+// rebuilt after setters): [nl, nroad, ne, 0], glob[nl], len[nl], vmax[nl],
+// flags[nl] (bit0 usable; road lanes: usable successors << 8, groups << 16),
+// per road lane 6 words (gbeg[0..3] bytes, gbeg[4], gtroad[0..3]), then the
+// ne <= 32 usable successors of the road lanes sorted by (lane, target road,
+// lane id), 8 words each: j, target road, exit lane, flags (bit0 junction lane,
+// lane_local << 8, rank k << 16), outroads(exit lane) x4
+constexpr int kDescMaxWords = 4 + 4 * kMaxTileLanes + 6 * kMaxRoadLanes + 8 * kMaxRoadLanes * kMaxSucc;
 constexpr int kMaxGroups = 4;        // distinct target roads per road lane in the table
 constexpr int kSmemProf = 8;         // profiles staged in shared memory
 constexpr uint64_t kEmptyKey = ~0ull;
@@ -102,7 +105,8 @@ struct StepArgs {
   const uint8_t *lane_local;
   // tiles (n_tiles global; this partition processes tiles[0 .. n_own))
   int32_t rank, n_own;
-  const int32_t *tiles, *tile_owner;
+  const int32_t *tiles, *tile_owner;  // tiles: own tiles, largest slot capacity first
+  int32_t *work;                    // [2] persistent-kernel work counter + finished warps (zero between launches)
   const int32_t *tile_lane_off, *tile_lanes, *tile_nroad;
   const int32_t *desc, *desc_off;   // tile descriptors (words, per-tile offsets)
   const int32_t *tile_base, *tile_cap, *tile_ibase, *tile_icap;

@@ -144,7 +144,6 @@ struct StepShared {
       unsigned long long sk_hi[kSmemInbox];   // inbox keys in sorted order
       int sk_vid[kSmemInbox];
     };
-    SuccEnt stage[32];                        // successor-table staging (before the merge)
     int words[kDescMaxWords];                 // tile descriptor staging
   };
   Prof prof[kSmemProf];
@@ -153,15 +152,12 @@ struct StepShared {
 #ifndef KSTEP_MINB
 #define KSTEP_MINB 24
 #endif
-// One WARP per road tile: no block barriers, warps progress independently
-// (DESIGN §3.3).  All intra-tile synchronisation is __syncwarp().
+// One road tile, processed by one warp (no block barriers: all intra-tile
+// synchronisation is __syncwarp()).
 template <bool EXACT>
-__global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
-  extern __shared__ __align__(16) unsigned char dyn[];
-  __shared__ StepShared S;
+__device__ __forceinline__ void step_tile(const StepArgs &A, StepShared &S, unsigned char *dyn,
+                                          const int tile, const int lane_id) {
   TileSh &T = S.T;
-  const int tile = A.tiles[blockIdx.x], lane_id = threadIdx.x;
-
   // ---- tile metadata -----------------------------------------------------
   // One coalesced read of the tile descriptor (host-built): lane
   // ids / lengths / speed limits / usable flags and every road-lane successor
@@ -175,41 +171,11 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
   const int ibase = A.tile_ibase[tile];
   for (int q = lane_id; q < (dsz >> 2); q += kThreads)
     reinterpret_cast<int4 *>(S.words)[q] = reinterpret_cast<const int4 *>(A.desc + doff)[q];
-  if (A.n_prof <= kSmemProf) {                      // profiles as int4 words (Prof is 96 B)
-    const int nw = A.n_prof * (int)(sizeof(Prof) / 16);
-    for (int q = lane_id; q < nw; q += kThreads)
-      reinterpret_cast<int4 *>(S.prof)[q] = reinterpret_cast<const int4 *>(A.prof)[q];
-  }
   __syncwarp();
   const int nl = S.words[0], nroad = S.words[1], ne = S.words[2];
-  // read this lane's lane record and successor entry into registers first (the
-  // staging area is reused for the successor sort below)
-  int lg = 0, lflags = 0;
-  float llen = 0.f, lvmax = 0.f;
-  if (lane_id < nl) {
-    lg = S.words[4 + lane_id];
-    llen = __int_as_float(S.words[4 + nl + lane_id]);
-    lvmax = __int_as_float(S.words[4 + 2 * nl + lane_id]);
-    lflags = S.words[4 + 3 * nl + lane_id];
-  }
-  SuccEnt s;
-  s.j = 0x7fffffff;
-  s.troad = 0x7fffffff;
-  int el = -1, ek = 0;
-  if (lane_id < ne) {
-    const int *w = S.words + 4 + 4 * nl + 8 * lane_id;
-    const int fl = w[3];
-    el = (fl >> 8) & 0xff;
-    ek = fl >> 16;
-    if (fl & 2) {                                   // usable successor
-      s.j = w[0];
-      s.troad = w[1];
-      s.b = w[2];
-      s.outr = make_int4(w[4], w[5], w[6], w[7]);
-      s.stop = ((fl & 1) && A.lane_sig[s.j] != SIG_GREEN) ? 1 : 0;
-    }
-  }
-  __syncwarp();
+  // lane records, the per-road-lane group tables and the (host-sorted) usable
+  // successors go straight into the tile's shared metadata; only the stop bit
+  // (signal of the junction lane at t) is computed here
   if (lane_id == 0) {
     T.nl = nl;
     T.nroad = nroad;
@@ -218,57 +184,45 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
     T.ibase = ibase;
     T.cap = A.tile_cap[tile];
     T.icap = A.tile_icap[tile];
-    T.P = A.n_prof <= kSmemProf ? S.prof : A.prof;
   }
   if (lane_id < nl) {
     const int l = lane_id;
-    T.glob[l] = lg;
-    T.len[l] = llen;
-    T.vmax[l] = lvmax;
+    const int fl = S.words[4 + 3 * nl + l];
+    T.glob[l] = S.words[4 + l];
+    T.len[l] = __int_as_float(S.words[4 + nl + l]);
+    T.vmax[l] = __int_as_float(S.words[4 + 2 * nl + l]);
     T.isroad[l] = l < nroad;
-    T.usable[l] = lflags & 1;
+    T.usable[l] = fl & 1;
     T.seg_start[l] = 0;
     T.seg_end[l] = 0;
     T.first_out[l] = 0x7fffffff;
     // road lanes are the first nroad local lanes, leftmost first (validated at create)
     T.left[l] = (l < nroad && l > 0) ? (int8_t)(l - 1) : (int8_t)-1;
     T.right[l] = (l < nroad - 1) ? (int8_t)(l + 1) : (int8_t)-1;
+    if (l < nroad) {
+      const int *gw = S.words + 4 + 4 * nl + 6 * l;
+      T.sn[l] = (uint8_t)((fl >> 8) & 0xff);
+      T.ng[l] = (uint8_t)((fl >> 16) & 0xff);
+      const unsigned g4 = (unsigned)gw[0];
+      T.gbeg[l][0] = (uint8_t)g4;
+      T.gbeg[l][1] = (uint8_t)(g4 >> 8);
+      T.gbeg[l][2] = (uint8_t)(g4 >> 16);
+      T.gbeg[l][3] = (uint8_t)(g4 >> 24);
+      T.gbeg[l][4] = (uint8_t)gw[1];
+#pragma unroll
+      for (int q = 0; q < kMaxGroups; ++q) T.gtroad[l][q] = gw[2 + q];
+    }
   }
-  // successor table of the tile's road lanes: usable successors sorted by
-  // (target road, lane id) and grouped by target road (one warp lane per slot)
-  SuccEnt *stage = S.stage;
-  stage[lane_id].j = 0x7fffffff;
-  stage[lane_id].troad = 0x7fffffff;
-  __syncwarp();
-  if (el >= 0) stage[el * kMaxSucc + ek] = s;
-  __syncwarp();
-  {
-    const int l = lane_id / kMaxSucc, k = lane_id % kMaxSucc;
-    const SuccEnt me = stage[lane_id];
-    const bool valid = me.j != 0x7fffffff;
-    int rank = 0, cnt = 0;
-    for (int q = 0; q < kMaxSucc; ++q) {
-      const SuccEnt &o = stage[l * kMaxSucc + q];
-      cnt += o.j != 0x7fffffff;
-      rank += (o.troad < me.troad) || (o.troad == me.troad && o.j < me.j);
-    }
-    if (valid) T.se[l][rank] = me;
-    if (l < nroad && k == 0) T.sn[l] = (uint8_t)cnt;
-    __syncwarp();
-    if (l < nroad && k < cnt) {
-      const bool start = k == 0 || T.se[l][k - 1].troad != T.se[l][k].troad;
-      int gid = 0;
-      for (int q = 1; q <= k; ++q) gid += T.se[l][q - 1].troad != T.se[l][q].troad;
-      if (start) {
-        T.gtroad[l][gid] = T.se[l][k].troad;
-        T.gbeg[l][gid] = (uint8_t)k;
-      }
-      if (k == cnt - 1) {
-        T.ng[l] = (uint8_t)(gid + 1);
-        T.gbeg[l][gid + 1] = (uint8_t)cnt;
-      }
-    }
-    if (l < nroad && k == 0 && cnt == 0) T.ng[l] = 0;
+  if (lane_id < ne) {
+    const int *w = S.words + 4 + 4 * nl + 6 * nroad + 8 * lane_id;
+    const int fl = w[3];
+    SuccEnt e;
+    e.j = w[0];
+    e.troad = w[1];
+    e.b = w[2];
+    e.outr = make_int4(w[4], w[5], w[6], w[7]);
+    e.stop = ((fl & 1) && A.lane_sig[e.j] != SIG_GREEN) ? 1 : 0;
+    T.se[(fl >> 8) & 0xff][fl >> 16] = e;
   }
   __syncwarp();
 
@@ -552,6 +506,38 @@ __global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
   }
 }
 
+// Persistent kernel: each warp takes road tiles from a work counter, largest
+// tiles first (A.tiles is sorted by slot capacity at create), so the grid is
+// sized to the resident capacity of the GPU and the tail is short.  The last
+// warp to finish resets the counters for the next launch.
+template <bool EXACT>
+__global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ StepShared S;
+  const int lane_id = threadIdx.x;
+  if (A.n_prof <= kSmemProf) {                      // profiles as int4 words (Prof is 96 B)
+    const int nw = A.n_prof * (int)(sizeof(Prof) / 16);
+    for (int q = lane_id; q < nw; q += kThreads)
+      reinterpret_cast<int4 *>(S.prof)[q] = reinterpret_cast<const int4 *>(A.prof)[q];
+  }
+  if (lane_id == 0) S.T.P = A.n_prof <= kSmemProf ? S.prof : A.prof;
+  for (;;) {
+    int idx = 0;
+    if (lane_id == 0) idx = atomicAdd(&A.work[0], 1);
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    if (idx >= A.n_own) break;
+    step_tile<EXACT>(A, S, dyn, A.tiles[idx], lane_id);
+    __syncwarp();
+  }
+  if (lane_id == 0) {
+    __threadfence();
+    if (atomicAdd(&A.work[1], 1) == (int)gridDim.x - 1) {
+      A.work[0] = 0;
+      A.work[1] = 0;
+    }
+  }
+}
+
 // ---- a5: per-junction signal controller -------------
 // One warp per junction: lane 0 applies requests and advances the phase
 // machine, all lanes write the signals of the junction's lanes (coalesced).
@@ -743,15 +729,23 @@ __global__ void k_halo_unpack(StepArgs A, const int32_t *lanes, const HaloRec *b
 int step_smem_bytes() { return kSmemVeh * 7 * 4; }
 
 void launch_step(const StepArgs &a, void *stream, int smem_bytes) {
-  static bool attr = false;
-  if (!attr) {
+  static int resident[2] = {0, 0};                  // resident warps per GPU, per instantiation
+  if (!resident[0]) {
     cudaFuncSetAttribute(k_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
-    attr = true;
+    int dev = 0, nsm = 0, b0 = 0, b1 = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b0, k_step<false>, kThreads, smem_bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_step<true>, kThreads, smem_bytes);
+    resident[0] = std::max(1, b0) * std::max(1, nsm);
+    resident[1] = std::max(1, b1) * std::max(1, nsm);
   }
   if (a.n_own <= 0) return;
-  if (a.exact_mode) k_step<true><<<a.n_own, kThreads, smem_bytes, (cudaStream_t)stream>>>(a);
-  else k_step<false><<<a.n_own, kThreads, smem_bytes, (cudaStream_t)stream>>>(a);
+  const int ex = a.exact_mode ? 1 : 0;
+  const int grid = std::min(a.n_own, resident[ex]);
+  if (ex) k_step<true><<<grid, kThreads, smem_bytes, (cudaStream_t)stream>>>(a);
+  else k_step<false><<<grid, kThreads, smem_bytes, (cudaStream_t)stream>>>(a);
 }
 
 void launch_signal(const SignalArgs &a, void *stream) {

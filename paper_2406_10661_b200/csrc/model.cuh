@@ -358,7 +358,7 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
   const R b_hard = (R)A.b_hard;
   // ---- lane-change eligibility: needs no lane evaluation ----
   const bool dest = me.nxt < 0;
-  bool inG = true, consider = false;
+  bool inG = true, consider = false, want0 = false, want1 = false;
   int mand = 0;
   int sl0 = -1, sl1 = -1, f0 = -1, f1 = -1, b0 = -1, b1 = -1;
   if (T.isroad[l]) {                                     // no LC in junction lanes
@@ -379,10 +379,17 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
       g.hit = true, g.why |= (1u << 2);
     sl0 = T.left[l];
     sl1 = T.right[l];
+    consider = inG ? !l19 : (mand != 0);
+    if (consider) {
+      want0 = sl0 >= 0 && T.usable[sl0] &&
+              (inG ? (dest || has_outroad_t(A, T, sl0, me.nxt)) : mand == -1);
+      want1 = sl1 >= 0 && T.usable[sl1] &&
+              (inG ? (dest || has_outroad_t(A, T, sl1, me.nxt)) : mand == 1);
+    }
 #pragma unroll 1
     for (int sd = 0; sd < 2; ++sd) {                     // side pointers (ties -> back, L11)
       const int ls = sd == 0 ? sl0 : sl1;
-      if (ls < 0) continue;
+      if (ls < 0 || !((sd == 0 ? want0 : want1) || A.record)) continue;
       const int a = T.seg_start[ls], b = T.seg_end[ls];
       const int f = upper_bound_s(C, a, b, C.s[i]);
       const int fr = f < b ? f : -1, bk = f > a ? f - 1 : -1;
@@ -390,61 +397,23 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
       o.side[2 * sd] = fr >= 0 ? C.vid[fr] : -1;
       o.side[2 * sd + 1] = bk >= 0 ? C.vid[bk] : -1;
     }
-    consider = inG ? !l19 : (mand != 0);
   }
-  bool want0 = false, want1 = false;
-  if (consider) {
-    want0 = sl0 >= 0 && T.usable[sl0] &&
-            (inG ? (dest || has_outroad_t(A, T, sl0, me.nxt)) : mand == -1);
-    want1 = sl1 >= 0 && T.usable[sl1] &&
-            (inG ? (dest || has_outroad_t(A, T, sl1, me.nxt)) : mand == 1);
-  }
-  // ---- MOBIL terms that need no lane evaluation: the politeness terms and
-  // the safety / gap admissibility of each side (L10, L13, L17) ----
+  // ---- MOBIL admissibility of each side, cheapest test first (gap signs,
+  // lane-start rule, then the b_safe IDM of the new follower); the politeness
+  // terms (L10, L13, L17) only for admissible sides.  A test that
+  // fails outside its guard band decides "inadmissible" exactly, so the later
+  // ones are skipped ----
   bool adm0 = false, adm1 = false;
   R pol0 = (R)0, pol1 = (R)0;                            // (ã_nf - a_nf) + (ã_of - a_of)
   double r = 1.0;                                        // U53 draw (L16), discretionary only
   if (want0 || want1) {
-    R a_of = (R)0, a_of_new = (R)0;                      // old follower (L10)
-    if (of >= 0) {
-      const PV<R> po = pvals(T.P[m_prof(C.meta[of])], (R)0);
-      const R so = (R)C.s[of], vo = (R)C.v[of];
-      const R v0o = (po.vmax < (R)T.vmax[l]) ? po.vmax : (R)T.vmax[l];
-      a_of = idm<R, GUARD>(vo, v0o, true, M::sub(M::sub(s, so), p.len), M::sub(vo, v), po,
-                           b_hard, fabs(s - so) + p.len, g);
-      const int li = lead >= 0 ? lead : i;               // free road if the ego has no leader
-      const R sl_ = (R)C.s[li];
-      const R ll_ = (R)T.P[m_prof(C.meta[li])].len;
-      a_of_new = idm<R, GUARD>(vo, v0o, lead >= 0, M::sub(M::sub(sl_, so), ll_),
-                               M::sub(vo, (R)C.v[li]), po, b_hard, fabs(sl_ - so) + ll_, g);
-    }
+    R anew0 = (R)0, anew1 = (R)0;                        // ã_nf per side
 #pragma unroll 1
     for (int sd = 0; sd < 2; ++sd) {
       if (!(sd == 0 ? want0 : want1)) continue;
       const int ls = sd == 0 ? sl0 : sl1;
       const int fi = sd == 0 ? f0 : f1, bi = sd == 0 ? b0 : b1;
-      R a_nf = (R)0, a_nf_new = (R)0;
       bool ok = true;
-      if (bi >= 0) {
-        const PV<R> pb = pvals(T.P[m_prof(C.meta[bi])], (R)0);
-        const R sb = (R)C.s[bi], vb = (R)C.v[bi];
-        const R v0b = (pb.vmax < (R)T.vmax[ls]) ? pb.vmax : (R)T.vmax[ls];
-        const int fj = fi >= 0 ? fi : bi;                // free road if no front
-        const R sf = (R)C.s[fj];
-        const R lf = (R)T.P[m_prof(C.meta[fj])].len;
-        a_nf = idm<R, GUARD>(vb, v0b, fi >= 0, M::sub(M::sub(sf, sb), lf),
-                             M::sub(vb, (R)C.v[fj]), pb, b_hard, fabs(sf - sb) + lf, g);
-        const R gb = M::sub(M::sub(s, sb), p.len);
-        a_nf_new = idm<R, GUARD>(vb, v0b, true, gb, M::sub(vb, v), pb, b_hard, fabs(s - sb) + p.len, g);
-        if (GUARD && fabsf((float)(a_nf_new + (R)A.b_safe)) <= kEpsAcc) g.hit = true, g.why |= (1u << 3);
-        if (!(a_nf_new >= -(R)A.b_safe)) ok = false;    // L17 (1)
-        if (!(gb >= (R)0)) ok = false;                   // L17 (2)
-      } else {
-        const R mrg = M::sub(s, p.len);
-        if (GUARD && fabsf((float)mrg - (float)A.start_margin) <= kEpsPos * ((float)s + (float)A.start_margin))
-          g.hit = true, g.why |= (1u << 4);
-        if (!(mrg >= (R)A.start_margin)) ok = false;    // L17 (3) lane-start rule
-      }
       if (fi >= 0) {
         const R sf = (R)C.s[fi];
         const R lf = (R)T.P[m_prof(C.meta[fi])].len;
@@ -452,23 +421,77 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
         if (GUARD && fabsf((float)gf) <= kEpsPos * (float)(fabs(sf - s) + lf)) g.hit = true, g.why |= (1u << 5);
         if (!(gf >= (R)0)) ok = false;                   // L17 (2)
       }
-      const R pol = M::add(M::sub(a_nf_new, a_nf), M::sub(a_of_new, a_of));
-      if (sd == 0) { pol0 = pol; adm0 = ok; } else { pol1 = pol; adm1 = ok; }
-    }
-    if (inG && (adm0 || adm1)) {
-      // U53 of Philox4x32-10(seed; vid, t) (ledger L16)
-      uint32_t c0 = (uint32_t)me.vid, c1 = (uint32_t)A.t, c2 = 0u, c3 = 0u;
-      uint32_t k0 = (uint32_t)(A.seed & 0xffffffffull), k1 = (uint32_t)(A.seed >> 32);
-#pragma unroll
-      for (int rr = 0; rr < 10; ++rr) {
-        uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
-        uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
-        uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
-        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
-        k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+      if (ok && bi >= 0) {
+        const R sb = (R)C.s[bi];
+        const R gb = M::sub(M::sub(s, sb), p.len);
+        const R gbs = fabs(s - sb) + p.len;
+        if (GUARD && fabsf((float)gb) <= kEpsPos * (float)gbs) g.hit = true, g.why |= (1u << 0);
+        if (!(gb >= (R)0)) ok = false;                   // L17 (2)
+        if (ok) {
+          const PV<R> pb = pvals(T.P[m_prof(C.meta[bi])], (R)0);
+          const R vb = (R)C.v[bi];
+          const R v0b = (pb.vmax < (R)T.vmax[ls]) ? pb.vmax : (R)T.vmax[ls];
+          const R an = idm<R, GUARD>(vb, v0b, true, gb, M::sub(vb, v), pb, b_hard, gbs, g);
+          if (GUARD && fabsf((float)(an + (R)A.b_safe)) <= kEpsAcc) g.hit = true, g.why |= (1u << 3);
+          if (!(an >= -(R)A.b_safe)) ok = false;         // L17 (1)
+          if (sd == 0) anew0 = an; else anew1 = an;
+        }
+      } else if (ok) {
+        const R mrg = M::sub(s, p.len);
+        if (GUARD && fabsf((float)mrg - (float)A.start_margin) <= kEpsPos * ((float)s + (float)A.start_margin))
+          g.hit = true, g.why |= (1u << 4);
+        if (!(mrg >= (R)A.start_margin)) ok = false;    // L17 (3) lane-start rule
       }
-      const uint64_t mant = ((uint64_t)(c0 >> 5) << 26) + (uint64_t)(c1 >> 6);
-      r = (double)mant * (1.0 / 9007199254740992.0);
+      if (sd == 0) adm0 = ok; else adm1 = ok;
+    }
+    if (inG && (adm0 || adm1)) {                         // discretionary: utilities + draw
+      R a_of = (R)0, a_of_new = (R)0;                    // old follower (L10)
+      if (of >= 0) {
+        const PV<R> po = pvals(T.P[m_prof(C.meta[of])], (R)0);
+        const R so = (R)C.s[of], vo = (R)C.v[of];
+        const R v0o = (po.vmax < (R)T.vmax[l]) ? po.vmax : (R)T.vmax[l];
+        a_of = idm<R, GUARD>(vo, v0o, true, M::sub(M::sub(s, so), p.len), M::sub(vo, v), po,
+                             b_hard, fabs(s - so) + p.len, g);
+        const int li = lead >= 0 ? lead : i;             // free road if the ego has no leader
+        const R sl_ = (R)C.s[li];
+        const R ll_ = (R)T.P[m_prof(C.meta[li])].len;
+        a_of_new = idm<R, GUARD>(vo, v0o, lead >= 0, M::sub(M::sub(sl_, so), ll_),
+                                 M::sub(vo, (R)C.v[li]), po, b_hard, fabs(sl_ - so) + ll_, g);
+      }
+#pragma unroll 1
+      for (int sd = 0; sd < 2; ++sd) {
+        if (!(sd == 0 ? adm0 : adm1)) continue;
+        const int ls = sd == 0 ? sl0 : sl1;
+        const int fi = sd == 0 ? f0 : f1, bi = sd == 0 ? b0 : b1;
+        R a_nf = (R)0;
+        if (bi >= 0) {                                   // new follower before the change
+          const PV<R> pb = pvals(T.P[m_prof(C.meta[bi])], (R)0);
+          const R sb = (R)C.s[bi], vb = (R)C.v[bi];
+          const R v0b = (pb.vmax < (R)T.vmax[ls]) ? pb.vmax : (R)T.vmax[ls];
+          const int fj = fi >= 0 ? fi : bi;              // free road if no front
+          const R sf = (R)C.s[fj];
+          const R lf = (R)T.P[m_prof(C.meta[fj])].len;
+          a_nf = idm<R, GUARD>(vb, v0b, fi >= 0, M::sub(M::sub(sf, sb), lf),
+                               M::sub(vb, (R)C.v[fj]), pb, b_hard, fabs(sf - sb) + lf, g);
+        }
+        const R pol = M::add(M::sub(sd == 0 ? anew0 : anew1, a_nf), M::sub(a_of_new, a_of));
+        if (sd == 0) pol0 = pol; else pol1 = pol;
+      }
+      {
+        // U53 of Philox4x32-10(seed; vid, t) (ledger L16)
+        uint32_t c0 = (uint32_t)me.vid, c1 = (uint32_t)A.t, c2 = 0u, c3 = 0u;
+        uint32_t k0 = (uint32_t)(A.seed & 0xffffffffull), k1 = (uint32_t)(A.seed >> 32);
+#pragma unroll
+        for (int rr = 0; rr < 10; ++rr) {
+          uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+          uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+          uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+          c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+          k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+        }
+        const uint64_t mant = ((uint64_t)(c0 >> 5) << 26) + (uint64_t)(c1 >> 6);
+        r = (double)mant * (1.0 / 9007199254740992.0);
+      }
     }
   }
   // ---- O4-O6 on the current lane and on the admissible side lanes (one

@@ -233,24 +233,55 @@ void build_desc(sim_s *h) {
   h->desc_off.assign(h->nt + 1, 0);
   for (int T = 0; T < h->nt; ++T) {
     const int l0 = h->tile_lane_off[T], nl = h->tile_lane_off[T + 1] - l0, nroad = h->tile_nroad[T];
-    std::vector<int32_t> ent;
+    // successor table of the road lanes (static between setters, so sorted and
+    // grouped here): usable successors sorted by (target road, lane id), grouped
+    // by target road; per road lane 6 words: gbeg[0..4] as bytes, gtroad[0..3]
+    std::vector<int32_t> ent, grp;
+    std::vector<int32_t> lane_sn(nroad, 0), lane_ng(nroad, 0);
+    int n_all = 0;                                  // all successors: fixes the descriptor size
     for (int l = 0; l < nroad; ++l) {
       const int g = h->tile_lanes[l0 + l];
-      for (int e = h->succ_off[g], k = 0; e < h->succ_off[g + 1]; ++e, ++k) {
-        const int j = h->succ[e], b = h->exit_lane[j];
+      n_all += h->succ_off[g + 1] - h->succ_off[g];
+      std::vector<int> js;
+      for (int e = h->succ_off[g]; e < h->succ_off[g + 1]; ++e)
+        if (h->usable[h->succ[e]]) js.push_back(h->succ[e]);
+      std::sort(js.begin(), js.end(), [&](int a, int b) {
+        return h->target_road[a] != h->target_road[b] ? h->target_road[a] < h->target_road[b] : a < b;
+      });
+      uint8_t gbeg[kMaxGroups + 1] = {0, 0, 0, 0, 0};
+      int32_t gtr[kMaxGroups] = {-1, -1, -1, -1};
+      int ng = 0;
+      for (int k = 0; k < (int)js.size(); ++k) {
+        const int j = js[k], b = h->exit_lane[j];
+        if (k == 0 || h->target_road[js[k - 1]] != h->target_road[j]) {
+          if (ng < kMaxGroups) { gbeg[ng] = (uint8_t)k; gtr[ng] = h->target_road[j]; }
+          ++ng;
+        }
         ent.push_back(j);
         ent.push_back(h->target_road[j]);
         ent.push_back(b);
-        ent.push_back((is_road(h, j) ? 0 : 1) | (h->usable[j] ? 2 : 0) | (l << 8) | (k << 16));
+        ent.push_back((is_road(h, j) ? 0 : 1) | (l << 8) | (k << 16));
         for (int q = 0; q < 4; ++q) ent.push_back(h->outroads[4 * (size_t)b + q]);
       }
+      if (ng <= kMaxGroups) gbeg[ng] = (uint8_t)js.size();
+      lane_sn[l] = (int)js.size();
+      lane_ng[l] = ng;
+      grp.push_back((int32_t)(gbeg[0] | (gbeg[1] << 8) | (gbeg[2] << 16) | ((uint32_t)gbeg[3] << 24)));
+      grp.push_back(gbeg[4]);
+      for (int q = 0; q < kMaxGroups; ++q) grp.push_back(gtr[q]);
     }
     std::vector<int32_t> w{nl, nroad, (int)(ent.size() / 8), 0};
     for (int l = 0; l < nl; ++l) w.push_back(h->tile_lanes[l0 + l]);
     for (int l = 0; l < nl; ++l) { float x = h->L[h->tile_lanes[l0 + l]]; int32_t b; std::memcpy(&b, &x, 4); w.push_back(b); }
     for (int l = 0; l < nl; ++l) { float x = h->vmax[h->tile_lanes[l0 + l]]; int32_t b; std::memcpy(&b, &x, 4); w.push_back(b); }
-    for (int l = 0; l < nl; ++l) w.push_back(h->usable[h->tile_lanes[l0 + l]] ? 1 : 0);
+    for (int l = 0; l < nl; ++l)
+      w.push_back((h->usable[h->tile_lanes[l0 + l]] ? 1 : 0) |
+                  (l < nroad ? (lane_sn[l] << 8) | (lane_ng[l] << 16) : 0));
+    w.insert(w.end(), grp.begin(), grp.end());
     w.insert(w.end(), ent.begin(), ent.end());
+    // pad to all successors so setters (which change the usable set) never
+    // change the descriptor's size or offsets
+    w.insert(w.end(), (size_t)(n_all - (int)(ent.size() / 8)) * 8, 0);
     while (w.size() % 4) w.push_back(0);
     h->desc.insert(h->desc.end(), w.begin(), w.end());
     h->desc_off[T + 1] = (int)h->desc.size();
@@ -813,7 +844,15 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   UP(i32, h->tile_ibase); A.tile_ibase = i32;
   UP(i32, h->tile_icap); A.tile_icap = i32;
   UP(i32, h->tile_owner); A.tile_owner = i32;
-  UP(i32, P.tiles); A.tiles = i32;
+  {
+    // largest tiles first: the persistent step kernel takes tiles in this order
+    std::vector<int> order(P.tiles);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int a, int b) { return h->tile_cap[a] > h->tile_cap[b]; });
+    UP(i32, order); A.tiles = i32;
+  }
+  AL(A.work, 2);
+  CK(h, cudaMemset(A.work, 0, 8));
   A.n_own = (int)P.tiles.size();
   A.rank = P.rank;
   for (int b = 0; b < 2; ++b) {
