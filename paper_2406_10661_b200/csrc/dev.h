@@ -19,7 +19,10 @@ namespace sim {
 
 constexpr int kMaxTileLanes = 32;    // lanes per tile (road lanes + outgoing junction lanes)
 constexpr int kThreads = 32;         // k_step block size: one warp per road tile
-constexpr int kSmemVeh = 160;        // snapshot slots held in shared memory (larger tiles use global scratch)
+#ifndef KSMEM_VEH
+#define KSMEM_VEH 256
+#endif
+constexpr int kSmemVeh = KSMEM_VEH;  // snapshot slots held in shared memory (larger tiles use global scratch)
 constexpr int kSmemInbox = 48;       // inbox keys sorted in shared memory
 constexpr int kNAcc = 12;            // per-tile int64 accumulators
 constexpr int kMaxRoadLanes = 4;     // road lanes per tile cached in the successor table
@@ -115,7 +118,7 @@ struct StepArgs {
   Slab in, out;                     // stayer slabs
   const InboxRec *inbox_in;
   InboxRec *inbox_out;
-  Slab scratch;                     // global fallback for large tiles ([base+ibase, +cap+icap))
+  uint32_t *scratch;                // per tile at 7 x (base + ibase): nxt, nxt2, wait of the snapshot, then (large tiles) s, v, vid, meta; stride cap + icap
   int32_t *bsort_scratch;           // [Σ icap] inbox sort order for large inboxes
   int32_t *dl_scratch;              // per-tile list of guard-deferred vehicles (scratch indexing)
   // migration to other partitions (world > 1): per-peer regions of MigRec

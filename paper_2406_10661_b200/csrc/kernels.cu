@@ -90,7 +90,7 @@ struct Acc8 {                        // per-thread counters of one tile
 // guard-deferred vehicle) or arrival (kind 3)
 __device__ __forceinline__ void emit_moved(const StepArgs &A, const View &C, int i, const Res &r,
                                            int kind, Acc8 &acc) {
-  const int vid = C.vid[i];
+  const int vid = C.vid(i);
   acc.lc += r.lc != 0;
   acc.hand += r.hand;
   if (kind == 3) {
@@ -102,14 +102,14 @@ __device__ __forceinline__ void emit_moved(const StepArgs &A, const View &C, int
     acc.waitfin += r.wait1;
     return;
   }
-  const uint32_t meta = C.meta[i];
+  const uint32_t meta = C.meta(i);
   const int cur = m_cursor(meta);
   InboxRec rec;
   rec.s = r.s1;
   rec.v = r.v1;
   rec.vid = vid;
-  rec.nxt = route_at(A, vid, cur, C.nxt[i], C.nxt2[i], r.cursor + 1);
-  rec.nxt2 = route_at(A, vid, cur, C.nxt[i], C.nxt2[i], r.cursor + 2);
+  rec.nxt = route_at(A, vid, cur, C.nxt(i), C.nxt2(i), r.cursor + 1);
+  rec.nxt2 = route_at(A, vid, cur, C.nxt(i), C.nxt2(i), r.cursor + 2);
   rec.meta = pack_meta(A.lane_local[r.lane_g], m_prof(meta), r.cursor);
   rec.wait = r.wait1;
   rec.pad = 0;
@@ -146,22 +146,33 @@ struct StepShared {
     };
     int words[kDescMaxWords];                 // tile descriptor staging
   };
-  Prof prof[kSmemProf];
 };
 
-#ifndef KSTEP_MINB
-#define KSTEP_MINB 24
+#ifndef KSTEP_WARPS
+#define KSTEP_WARPS 1
 #endif
-// One road tile, processed by one warp (no block barriers: all intra-tile
-// synchronisation is __syncwarp()).
+#ifndef KSTEP_MINB
+#define KSTEP_MINB (24 / KSTEP_WARPS)
+#endif
+constexpr int kStepWarps = KSTEP_WARPS;
+
+// What the phases of one tile hand to each other (registers of its warp).
+struct TileCtx {
+  int tile, n, base, ibase, nl, nroad;
+  View C;
+};
+
+// Phase 1 of a road tile (one warp; intra-tile synchronisation is __syncwarp()):
+// tile metadata and the merged snapshot (a1).
 template <bool EXACT>
-__device__ __forceinline__ void step_tile(const StepArgs &A, StepShared &S, unsigned char *dyn,
-                                          const int tile, const int lane_id) {
+__device__ __forceinline__ void tile_load(const StepArgs &A, StepShared &S, unsigned char *dyn,
+                                          TileCtx &x, const int lane_id) {
   TileSh &T = S.T;
   // ---- tile metadata -----------------------------------------------------
   // One coalesced read of the tile descriptor (host-built): lane
   // ids / lengths / speed limits / usable flags and every road-lane successor
   // with its target road, exit lane and the exit lane's reachable roads.
+  const int tile = x.tile;
   const int doff = A.desc_off[tile];
   const int dsz = A.desc_off[tile + 1] - doff;
   const int n_st = A.cnt_in[tile];
@@ -229,24 +240,14 @@ __device__ __forceinline__ void step_tile(const StepArgs &A, StepShared &S, unsi
   // snapshot view: shared memory, or this tile's global scratch if too large
   View C;
   const bool smem_ok = (n <= kSmemVeh) && (n_in <= kSmemInbox);
+  C.q = A.scratch + 7 * (size_t)(base + ibase);      // scratch region of the tile: 7 x (cap + icap) words
+  C.qt = T.cap + T.icap;
   if (smem_ok) {
-    float *f = reinterpret_cast<float *>(dyn);
-    C.s = f;
-    C.v = f + kSmemVeh;
-    C.vid = reinterpret_cast<int32_t *>(f + 2 * kSmemVeh);
-    C.nxt = C.vid + kSmemVeh;
-    C.nxt2 = C.vid + 2 * kSmemVeh;
-    C.meta = reinterpret_cast<uint32_t *>(C.vid + 3 * kSmemVeh);
-    C.wait = C.vid + 4 * kSmemVeh;
+    C.p = reinterpret_cast<uint32_t *>(dyn);
+    C.st = kSmemVeh;
   } else {
-    const int sb = base + ibase;               // scratch is indexed by base + ibase (size cap + icap)
-    C.s = A.scratch.s + sb;
-    C.v = A.scratch.v + sb;
-    C.vid = A.scratch.vid + sb;
-    C.nxt = A.scratch.nxt + sb;
-    C.nxt2 = A.scratch.nxt2 + sb;
-    C.meta = A.scratch.meta + sb;
-    C.wait = A.scratch.wait + sb;
+    C.p = C.q + 3 * C.qt;
+    C.st = C.qt;
   }
   int *bsort = (n_in <= kSmemInbox) ? S.bsort : (A.bsort_scratch + ibase);
   const InboxRec *inb = A.inbox_in + ibase;
@@ -311,13 +312,13 @@ __device__ __forceinline__ void step_tile(const StepArgs &A, StepShared &S, unsi
       }
       pos += lo;
     }
-    C.s[pos] = s;
-    C.v[pos] = vv[u];
-    C.vid[pos] = vid;
-    C.nxt[pos] = n1v[u];
-    C.nxt2[pos] = n2v[u];
-    C.meta[pos] = meta;
-    C.wait[pos] = wv[u];
+    C.s(pos) = s;
+    C.v(pos) = vv[u];
+    C.vid(pos) = vid;
+    C.nxt(pos) = n1v[u];
+    C.nxt2(pos) = n2v[u];
+    C.meta(pos) = meta;
+    C.wait(pos) = wv[u];
     }
   }
   // inbox records: position = sorted rank + #stayers below (binary search in the slab)
@@ -332,31 +333,41 @@ __device__ __forceinline__ void step_tile(const StepArgs &A, StepShared &S, unsi
       else hi = mid;
     }
     const int pos = r + lo;
-    C.s[pos] = rec.s;
-    C.v[pos] = rec.v;
-    C.vid[pos] = rec.vid;
-    C.nxt[pos] = rec.nxt;
-    C.nxt2[pos] = rec.nxt2;
-    C.meta[pos] = rec.meta;
-    C.wait[pos] = rec.wait;
+    C.s(pos) = rec.s;
+    C.v(pos) = rec.v;
+    C.vid(pos) = rec.vid;
+    C.nxt(pos) = rec.nxt;
+    C.nxt2(pos) = rec.nxt2;
+    C.meta(pos) = rec.meta;
+    C.wait(pos) = rec.wait;
   }
   __syncwarp();
   // lane segments of the snapshot
   for (int i = lane_id; i < n; i += kThreads) {
-    const int l = m_lane(C.meta[i]);
-    if (i == 0 || m_lane(C.meta[i - 1]) != l) T.seg_start[l] = i;
-    if (i == n - 1 || m_lane(C.meta[i + 1]) != l) T.seg_end[l] = i + 1;
+    const int l = m_lane(C.meta(i));
+    if (i == 0 || m_lane(C.meta(i - 1)) != l) T.seg_start[l] = i;
+    if (i == n - 1 || m_lane(C.meta(i + 1)) != l) T.seg_end[l] = i + 1;
   }
   __syncwarp();
+  x.n = n;
+  x.base = base;
+  x.ibase = ibase;
+  x.nl = nl;
+  x.nroad = nroad;
+  x.C = C;
+}
 
   // ---- 2-3. per-vehicle update (a2-a4) and outputs, 32 vehicles at a time ----
   // fp32 path: vehicles whose decision margins fall inside the guard band are
   // deferred and recomputed after the loop with the canonical fp64 sequence;
   // they leave through the inbox (as movers), so the in-order compaction of the
   // stayers never waits for them and the fp64 code stays out of the hot loop.
-  Acc8 acc;
-  int run = 0;                                      // stayers written so far
-  int ndef = 0;                                     // deferred vehicles (warp-uniform)
+template <bool EXACT>
+__device__ __forceinline__ void tile_update(const StepArgs &A, StepShared &S, const TileCtx &x,
+                                            Acc8 &acc, int &run, int &ndef, const int lane_id) {
+  TileSh &T = S.T;
+  const int n = x.n, base = x.base, ibase = x.ibase;
+  const View C = x.C;
   int *dlist = A.dl_scratch + base + ibase;
   for (int c0 = 0; c0 < n; c0 += kThreads) {
     const int i = c0 + lane_id;
@@ -382,8 +393,8 @@ __device__ __forceinline__ void step_tile(const StepArgs &A, StepShared &S, unsi
 #endif
       }
       if (!defer) {
-        if (A.record) record(A, C.vid[i], r, false);
-        const int l = m_lane(C.meta[i]);
+        if (A.record) record(A, C.vid(i), r, false);
+        const int l = m_lane(C.meta(i));
         if (r.fin) kind = 3;
         else if (r.lc == 0 && r.hand == 0 && r.lane_g == T.glob[l]) kind = 1;
         else kind = 2;
@@ -398,12 +409,12 @@ __device__ __forceinline__ void step_tile(const StepArgs &A, StepShared &S, unsi
     const unsigned ball = __ballot_sync(0xffffffffu, kind == 1);
     if (kind == 1) {
       const int pos = base + run + __popc(ball & ((1u << lane_id) - 1u));
-      const uint32_t meta = C.meta[i];
+      const uint32_t meta = C.meta(i);
       A.out.s[pos] = r.s1;
       A.out.v[pos] = r.v1;
-      A.out.vid[pos] = C.vid[i];
-      A.out.nxt[pos] = C.nxt[i];
-      A.out.nxt2[pos] = C.nxt2[i];
+      A.out.vid[pos] = C.vid(i);
+      A.out.nxt[pos] = C.nxt(i);
+      A.out.nxt2[pos] = C.nxt2(i);
       A.out.meta[pos] = meta;
       A.out.wait[pos] = r.wait1;
       atomicMin(&T.first_out[m_lane(meta)], pos);
@@ -412,6 +423,18 @@ __device__ __forceinline__ void step_tile(const StepArgs &A, StepShared &S, unsi
     }
     run += __popc(ball);
   }
+}
+
+// Phase 3: guard-deferred vehicles (fp64), lane summaries for t+1, departures
+// and counters (a4, a6).
+template <bool EXACT>
+__device__ __forceinline__ void tile_finish(const StepArgs &A, StepShared &S, const TileCtx &x,
+                                            Acc8 &acc, const int run, const int ndef,
+                                            const int lane_id) {
+  TileSh &T = S.T;
+  const int tile = x.tile, n = x.n, base = x.base, ibase = x.ibase, nl = x.nl, nroad = x.nroad;
+  const View C = x.C;
+  int *dlist = A.dl_scratch + base + ibase;
   if constexpr (!EXACT) {
     __syncwarp();
     for (int q = lane_id; q < ndef; q += kThreads) {
@@ -421,7 +444,7 @@ __device__ __forceinline__ void step_tile(const StepArgs &A, StepShared &S, unsi
       g.hit = false;
       g.why = 0;
       veh_update<double, false>(A, T, C, i, r, g);
-      if (A.record) record(A, C.vid[i], r, true);
+      if (A.record) record(A, C.vid(i), r, true);
       emit_moved(A, C, i, r, r.fin ? 3 : 2, acc);
       acc.guard += 1;
     }
@@ -452,14 +475,14 @@ __device__ __forceinline__ void step_tile(const StepArgs &A, StepShared &S, unsi
     const int fa = upper_bound_s(C, a0, b0, (float)ss);
     bool ok = true;
     if (fa < b0) {
-      const double sa = C.s[fa], la = T.P[m_prof(C.meta[fa])].len_d;
+      const double sa = C.s(fa), la = T.P[m_prof(C.meta(fa))].len_d;
       if (!(__dadd_rn(__dadd_rn(sa, -ss), -la) >= pk.s0_d)) ok = false;
     }
     if (fa > a0) {
       const int b = fa - 1;
-      const Prof &pb = T.P[m_prof(C.meta[b])];
-      const double need = __dadd_rn(__dadd_rn((double)C.v[b], __dmul_rn(0.5, pb.a_max_d)), pk.s0_d);
-      if (!(__dadd_rn(__dadd_rn(ss, -(double)C.s[b]), -pk.len_d) >= need)) ok = false;
+      const Prof &pb = T.P[m_prof(C.meta(b))];
+      const double need = __dadd_rn(__dadd_rn((double)C.v(b), __dmul_rn(0.5, pb.a_max_d)), pk.s0_d);
+      if (!(__dadd_rn(__dadd_rn(ss, -(double)C.s(b)), -pk.len_d) >= need)) ok = false;
     } else {
       if (!(__dadd_rn(ss, -pk.len_d) >= A.start_margin)) ok = false;
     }
@@ -486,50 +509,85 @@ __device__ __forceinline__ void step_tile(const StepArgs &A, StepShared &S, unsi
     acc.ins += 1;
     acc.delay += (long long)(A.t + 1 - A.depart[k]);
   }
-  // warp reduction of the counters (int64, exact, order independent)
-  long long vals[kNAcc] = {0, acc.fin, acc.travel, acc.waitfin, acc.delay, acc.lc, acc.hand,
-                           acc.ins, acc.guard, acc.ovf, 0, 0};
-  const unsigned any = __ballot_sync(0xffffffffu, (acc.fin | acc.lc | acc.hand | acc.ins |
-                                                   acc.guard | acc.ovf) != 0);
-  if (any) {
-#pragma unroll
-    for (int c = 1; c < kNAcc - 2; ++c)
-      for (int o = 16; o > 0; o >>= 1) vals[c] += __shfl_down_sync(0xffffffffu, vals[c], o);
+  // warp reduction of the counters (exact, order independent): 32-bit counts
+  // with redux.sync; the int64 sums only in warps that saw an arrival / insertion
+  const unsigned c_fin = __reduce_add_sync(0xffffffffu, (unsigned)acc.fin);
+  const unsigned c_ins = __reduce_add_sync(0xffffffffu, (unsigned)acc.ins);
+  const unsigned c_lc = __reduce_add_sync(0xffffffffu, (unsigned)acc.lc);
+  const unsigned c_hand = __reduce_add_sync(0xffffffffu, (unsigned)acc.hand);
+  const unsigned c_guard = __reduce_add_sync(0xffffffffu, (unsigned)acc.guard);
+  const unsigned c_ovf = __reduce_add_sync(0xffffffffu, (unsigned)acc.ovf);
+  long long s_travel = acc.travel, s_waitfin = acc.waitfin, s_delay = acc.delay;
+  if (c_fin | c_ins) {
+    for (int o = 16; o > 0; o >>= 1) {
+      s_travel += __shfl_down_sync(0xffffffffu, s_travel, o);
+      s_waitfin += __shfl_down_sync(0xffffffffu, s_waitfin, o);
+      s_delay += __shfl_down_sync(0xffffffffu, s_delay, o);
+    }
   }
   if (lane_id == 0) {
     long long *ta = A.tacc + (size_t)tile * kNAcc;
     ta[ACC_VEH_STEPS] += n;
-    if (any)
-      for (int c = 1; c < kNAcc - 2; ++c) ta[c] += vals[c];
+    if (c_fin) {
+      ta[ACC_FINISHED] += c_fin;
+      ta[ACC_SUM_TRAVEL] += s_travel;
+      ta[ACC_SUM_WAIT_FIN] += s_waitfin;
+    }
+    if (c_ins) {
+      ta[ACC_INSERTED] += c_ins;
+      ta[ACC_SUM_DELAY] += s_delay;
+    }
+    if (c_lc) ta[ACC_LANE_CHANGES] += c_lc;
+    if (c_hand) ta[ACC_HANDOFFS] += c_hand;
+    if (c_guard) ta[ACC_GUARD] += c_guard;
+    if (c_ovf) ta[ACC_OVERFLOW] += c_ovf;
     A.cnt_out[tile] = run;
     A.icnt_in[tile] = 0;
   }
 }
 
-// Persistent kernel: each warp takes road tiles from a work counter, largest
-// tiles first (A.tiles is sorted by slot capacity at create), so the grid is
-// sized to the resident capacity of the GPU and the tail is short.  The last
-// warp to finish resets the counters for the next launch.
+// Persistent kernel.  A block of kStepWarps warps takes kStepWarps consecutive
+// road tiles from a work counter (largest tiles first: A.tiles is sorted by slot
+// capacity at create), one tile per warp, and runs the three phases of its
+// tiles in step with block barriers in between, so all warps of an SM execute
+// the same code at a time (the whole kernel does not fit the instruction
+// cache) and issue their HBM loads together.  Consecutive tiles of the sorted
+// list have similar sizes, so little time is lost at the barriers.  The last
+// block to finish resets the counters for the next launch.
 template <bool EXACT>
-__global__ void __launch_bounds__(kThreads, KSTEP_MINB) k_step(StepArgs A) {
-  extern __shared__ __align__(16) unsigned char dyn[];
-  __shared__ StepShared S;
-  const int lane_id = threadIdx.x;
+__global__ void __launch_bounds__(kStepWarps * kThreads, KSTEP_MINB)
+    k_step(const __grid_constant__ StepArgs A) {
+  extern __shared__ __align__(16) unsigned char dyn_all[];
+  __shared__ StepShared SS[kStepWarps];
+  __shared__ Prof prof[kSmemProf];
+  __shared__ int s_base;
+  const int warp = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
+  StepShared &S = SS[warp];
+  unsigned char *dyn = dyn_all + (size_t)warp * (kSmemVeh * 4 * 4);
   if (A.n_prof <= kSmemProf) {                      // profiles as int4 words (Prof is 96 B)
     const int nw = A.n_prof * (int)(sizeof(Prof) / 16);
-    for (int q = lane_id; q < nw; q += kThreads)
-      reinterpret_cast<int4 *>(S.prof)[q] = reinterpret_cast<const int4 *>(A.prof)[q];
+    for (int q = threadIdx.x; q < nw; q += blockDim.x)
+      reinterpret_cast<int4 *>(prof)[q] = reinterpret_cast<const int4 *>(A.prof)[q];
   }
-  if (lane_id == 0) S.T.P = A.n_prof <= kSmemProf ? S.prof : A.prof;
+  if (lane_id == 0) S.T.P = A.n_prof <= kSmemProf ? prof : A.prof;
   for (;;) {
-    int idx = 0;
-    if (lane_id == 0) idx = atomicAdd(&A.work[0], 1);
-    idx = __shfl_sync(0xffffffffu, idx, 0);
-    if (idx >= A.n_own) break;
-    step_tile<EXACT>(A, S, dyn, A.tiles[idx], lane_id);
-    __syncwarp();
+    if (threadIdx.x == 0) s_base = atomicAdd(&A.work[0], kStepWarps);
+    __syncthreads();
+    const int b0 = s_base;
+    if (b0 >= A.n_own) break;
+    const int idx = b0 + warp;
+    const bool has = idx < A.n_own;
+    TileCtx x;
+    x.tile = has ? A.tiles[idx] : 0;
+    if (has) tile_load<EXACT>(A, S, dyn, x, lane_id);
+    __syncthreads();
+    Acc8 acc;
+    int run = 0, ndef = 0;
+    if (has) tile_update<EXACT>(A, S, x, acc, run, ndef, lane_id);
+    __syncthreads();
+    if (has) tile_finish<EXACT>(A, S, x, acc, run, ndef, lane_id);
   }
-  if (lane_id == 0) {
+  if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(&A.work[1], 1) == (int)gridDim.x - 1) {
       A.work[0] = 0;
@@ -726,26 +784,26 @@ __global__ void k_halo_unpack(StepArgs A, const int32_t *lanes, const HaloRec *b
 }
 
 // ---- launchers ---------------------------------------------------------------
-int step_smem_bytes() { return kSmemVeh * 7 * 4; }
+int step_smem_bytes() { return kStepWarps * kSmemVeh * 4 * 4; }
 
 void launch_step(const StepArgs &a, void *stream, int smem_bytes) {
-  static int resident[2] = {0, 0};                  // resident warps per GPU, per instantiation
+  static int resident[2] = {0, 0};                  // resident blocks per GPU, per instantiation
   if (!resident[0]) {
     cudaFuncSetAttribute(k_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     int dev = 0, nsm = 0, b0 = 0, b1 = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b0, k_step<false>, kThreads, smem_bytes);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_step<true>, kThreads, smem_bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b0, k_step<false>, kStepWarps * kThreads, smem_bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_step<true>, kStepWarps * kThreads, smem_bytes);
     resident[0] = std::max(1, b0) * std::max(1, nsm);
     resident[1] = std::max(1, b1) * std::max(1, nsm);
   }
   if (a.n_own <= 0) return;
   const int ex = a.exact_mode ? 1 : 0;
-  const int grid = std::min(a.n_own, resident[ex]);
-  if (ex) k_step<true><<<grid, kThreads, smem_bytes, (cudaStream_t)stream>>>(a);
-  else k_step<false><<<grid, kThreads, smem_bytes, (cudaStream_t)stream>>>(a);
+  const int grid = std::min((a.n_own + kStepWarps - 1) / kStepWarps, resident[ex]);
+  if (ex) k_step<true><<<grid, kStepWarps * kThreads, smem_bytes, (cudaStream_t)stream>>>(a);
+  else k_step<false><<<grid, kStepWarps * kThreads, smem_bytes, (cudaStream_t)stream>>>(a);
 }
 
 void launch_signal(const SignalArgs &a, void *stream) {

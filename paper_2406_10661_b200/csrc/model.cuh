@@ -95,12 +95,21 @@ struct TileSh {
   uint8_t isroad[kMaxTileLanes], usable[kMaxTileLanes];
 };
 
-// Snapshot of the tile at time t (shared memory or global scratch).
+// Snapshot of the tile at time t.  The fields other vehicles read (s, v, vid,
+// meta) are four word arrays of stride st from p (shared memory, or the
+// tile's global scratch when the tile is large); the fields only the vehicle
+// itself uses (nxt, nxt2, wait) are three word arrays of stride qt from q
+// (always global scratch), which keeps 16 B per vehicle in shared memory.
 struct View {
-  float *s, *v;
-  int32_t *vid, *nxt, *nxt2;
-  uint32_t *meta;
-  int32_t *wait;
+  uint32_t *p, *q;
+  int st, qt;
+  __device__ __forceinline__ float &s(int i) const { return reinterpret_cast<float *>(p)[i]; }
+  __device__ __forceinline__ float &v(int i) const { return reinterpret_cast<float *>(p)[st + i]; }
+  __device__ __forceinline__ int32_t &vid(int i) const { return reinterpret_cast<int32_t *>(p)[2 * st + i]; }
+  __device__ __forceinline__ uint32_t &meta(int i) const { return p[3 * st + i]; }
+  __device__ __forceinline__ int32_t &nxt(int i) const { return reinterpret_cast<int32_t *>(q)[i]; }
+  __device__ __forceinline__ int32_t &nxt2(int i) const { return reinterpret_cast<int32_t *>(q)[qt + i]; }
+  __device__ __forceinline__ int32_t &wait(int i) const { return reinterpret_cast<int32_t *>(q)[2 * qt + i]; }
 };
 
 __device__ __forceinline__ int m_lane(uint32_t m) { return (int)(m & 0xffu); }
@@ -200,10 +209,10 @@ __device__ __forceinline__ First first_of(const StepArgs &A, const TileSh &T, co
     int a = T.seg_start[ll];
     if (a < T.seg_end[ll]) {
       f.found = true;
-      f.s = C.s[a];
-      f.v = C.v[a];
-      f.vid = C.vid[a];
-      f.len = T.P[m_prof(C.meta[a])].len;
+      f.s = C.s(a);
+      f.v = C.v(a);
+      f.vid = C.vid(a);
+      f.len = T.P[m_prof(C.meta(a))].len;
     }
   } else {
     unsigned long long key = A.summ_cur[m];
@@ -251,13 +260,13 @@ __device__ LEv<R> eval_lane(const StepArgs &A, const TileSh &T, const View &C, i
   e.vlead = (R)0;
   R gscale = (R)0;
   if (lead_idx >= 0) {                                   // main pointer
-    R sf = (R)C.s[lead_idx];
-    R lf = (R)T.P[m_prof(C.meta[lead_idx])].len;
+    R sf = (R)C.s(lead_idx);
+    R lf = (R)T.P[m_prof(C.meta(lead_idx))].len;
     e.has_leader = true;
-    e.leader = C.vid[lead_idx];
+    e.leader = C.vid(lead_idx);
     e.hops = 0;
     e.gap = M::sub(M::sub(sf, s), lf);
-    e.vlead = (R)C.v[lead_idx];
+    e.vlead = (R)C.v(lead_idx);
     gscale = fabs(sf - s) + lf;
   } else {                                               // P:168-169 substitution
     R d = M::sub(L, s);
@@ -331,9 +340,103 @@ __device__ __forceinline__ int upper_bound_s(const View &C, int a, int b, float 
   // first index in [a, b) with C.s > s   (side pointers; ties -> back, L11)
   while (a < b) {
     int mid = (a + b) >> 1;
-    if (C.s[mid] > s) b = mid; else a = mid + 1;
+    if (C.s(mid) > s) b = mid; else a = mid + 1;
   }
   return a;
+}
+
+template <typename R> struct SideRes {
+  int choice;                        // -1 stay, 0 left, 1 right
+  R a, lim, limrel, vlim;
+  int next1;
+  bool has_lim, hit;
+  unsigned why;
+};
+
+// O7 decision for a vehicle with at least one admissible side:
+// evaluates O4-O6 on the side lanes still able to win and picks the side.  On
+// the fp32 path a side is evaluated only if the draw can still fall below
+// p_LC: with F = the free-road IDM bound of ã_ego on that lane, u <= (F - a_cur)
+// + p * pol, and p_LC is monotone in u_T apart from its 2e-8 floor, so r >=
+// p_LC(upper bound) + 1e-3 decides "stay" exactly.  Out of line:
+// it runs for ~1-2% of vehicles and keeps the hot loop small.
+template <typename R, bool GUARD>
+__device__ __noinline__ SideRes<R> lane_change(const StepArgs &A, const TileSh &T, const View &C,
+                                               bool adm0, bool adm1, bool inG, int mand, int sl0,
+                                               int sl1, int f0, int f1, R s, R v, const PV<R> p,
+                                               const Me me, R a_cur, R pol0, R pol1, double r) {
+  using M = Ar<R>;
+  Guard g;
+  g.hit = false;
+  g.why = 0;
+  SideRes<R> o;
+  o.choice = -1;
+  bool need0 = adm0 && (inG || mand < 0);
+  bool need1 = adm1 && (inG || mand > 0);
+  const R b_hard = (R)A.b_hard;
+  if (GUARD && inG && (need0 || need1)) {
+    R ub = (R)0;
+#pragma unroll 1
+    for (int sd = 0; sd < 2; ++sd) {
+      if (!(sd == 0 ? need0 : need1)) continue;
+      const int ls = sd == 0 ? sl0 : sl1;
+      const R v0s = (p.vmax < (R)T.vmax[ls]) ? p.vmax : (R)T.vmax[ls];
+      const R x = M::div(v, v0s);
+      const R x2 = M::mul(x, x);
+      R F = M::mul(p.a_max, M::sub((R)1, M::mul(x2, x2)));
+      F = (F < -b_hard) ? -b_hard : F;
+      const R U = M::add(M::sub(F, a_cur), M::mul((R)A.polite, sd == 0 ? pol0 : pol1));
+      ub = M::add(ub, ((R)0 < U) ? U : (R)0);
+    }
+    const double pmax = ub >= (R)1 ? 0.9 : fmax(2e-8, (double)(0.9 - 2e-8) * (double)ub);
+    if (r >= pmax + 1e-3) need0 = need1 = false;       // no change, for certain
+  }
+  if (!(need0 || need1)) { o.hit = g.hit; o.why = g.why; return o; }
+  // ã_ego on each side; keep the utility of both and the evaluation of the
+  // side that would be taken (argmax, tie -> left: P:196, ledger L15)
+  R u0 = (R)0, u1 = (R)0;
+  LEv<R> best;
+#pragma unroll 1
+  for (int sd = 0; sd < 2; ++sd) {
+    if (!(sd == 0 ? need0 : need1)) continue;
+    const LEv<R> e = eval_lane<R, GUARD>(A, T, C, sd == 0 ? sl0 : sl1, sd == 0 ? f0 : f1, s, v, p,
+                                         me, g);
+    // MOBIL utility (tilde = after the change, ledger L13)
+    const R u = M::add(M::sub(e.a, a_cur), M::mul((R)A.polite, sd == 0 ? pol0 : pol1));
+    if (sd == 0) u0 = u; else u1 = u;
+    if (sd == 0 || !need0 || u0 < u1) best = e;
+  }
+  int choice = -1;
+  if (inG) {
+    const R p0 = need0 ? (((R)0 < u0) ? u0 : (R)0) : (R)0;
+    const R p1 = need1 ? (((R)0 < u1) ? u1 : (R)0) : (R)0;
+    const R uT = M::add(p0, p1);
+    double pl;                                           // P:188-194, ledger L14
+    if (uT >= (R)1) pl = 0.9;
+    else if (uT > (R)0) pl = (double)M::mul((R)(0.9 - 2e-8), uT);
+    else pl = 2e-8;
+    if (GUARD && fabs(r - pl) <= (double)kEpsP) g.hit = true, g.why |= (1u << 6);
+    if (r < pl) {                                        // P:196, ledger L15
+      if (need0 && need1) {
+        if (GUARD && fabsf((float)(u0 - u1)) <= kEpsAcc) g.hit = true, g.why |= (1u << 7);
+        choice = (u0 >= u1) ? 0 : 1;
+      } else {
+        choice = need0 ? 0 : 1;
+      }
+    }
+  } else {
+    choice = mand < 0 ? 0 : 1;                           // ledger L18: admissible -> change
+  }
+  o.choice = choice;
+  o.a = best.a;
+  o.lim = best.lim;
+  o.limrel = best.limrel;
+  o.vlim = best.vlim;
+  o.next1 = best.next1;
+  o.has_lim = best.has_lim;
+  o.hit = g.hit;
+  o.why = g.why;
+  return o;
 }
 
 // One vehicle's update O4-O9 reading only state(t).
@@ -341,19 +444,19 @@ template <typename R, bool GUARD>
 __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, int i, Res &o,
                            Guard &g) {
   using M = Ar<R>;
-  const uint32_t meta = C.meta[i];
+  const uint32_t meta = C.meta(i);
   const int l = m_lane(meta), pr = m_prof(meta);
   Me me;
-  me.vid = C.vid[i];
+  me.vid = C.vid(i);
   me.cur = m_cursor(meta);
-  me.nxt = C.nxt[i];
-  me.nxt2 = C.nxt2[i];
+  me.nxt = C.nxt(i);
+  me.nxt2 = C.nxt2(i);
   const PV<R> p = pvals(T.P[pr], (R)0);
-  const R s = (R)C.s[i], v = (R)C.v[i];
+  const R s = (R)C.s(i), v = (R)C.v(i);
   const R L = (R)T.len[l];
   const int lead = (i + 1 < T.seg_end[l]) ? i + 1 : -1;
   const int of = (i > T.seg_start[l]) ? i - 1 : -1;
-  o.of_vid = of >= 0 ? C.vid[of] : -1;
+  o.of_vid = of >= 0 ? C.vid(of) : -1;
   o.side[0] = o.side[1] = o.side[2] = o.side[3] = -1;
   const R b_hard = (R)A.b_hard;
   // ---- lane-change eligibility: needs no lane evaluation ----
@@ -391,11 +494,11 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
       const int ls = sd == 0 ? sl0 : sl1;
       if (ls < 0 || !((sd == 0 ? want0 : want1) || A.record)) continue;
       const int a = T.seg_start[ls], b = T.seg_end[ls];
-      const int f = upper_bound_s(C, a, b, C.s[i]);
+      const int f = upper_bound_s(C, a, b, C.s(i));
       const int fr = f < b ? f : -1, bk = f > a ? f - 1 : -1;
-      if (sd == 0) { f0 = fr; b0 = bk; } else { f1 = fr; b1 = bk; }
-      o.side[2 * sd] = fr >= 0 ? C.vid[fr] : -1;
-      o.side[2 * sd + 1] = bk >= 0 ? C.vid[bk] : -1;
+      const int vf = fr >= 0 ? C.vid(fr) : -1, vb = bk >= 0 ? C.vid(bk) : -1;
+      if (sd == 0) { f0 = fr; b0 = bk; o.side[0] = vf; o.side[1] = vb; }
+      else { f1 = fr; b1 = bk; o.side[2] = vf; o.side[3] = vb; }
     }
   }
   // ---- MOBIL admissibility of each side, cheapest test first (gap signs,
@@ -415,21 +518,21 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
       const int fi = sd == 0 ? f0 : f1, bi = sd == 0 ? b0 : b1;
       bool ok = true;
       if (fi >= 0) {
-        const R sf = (R)C.s[fi];
-        const R lf = (R)T.P[m_prof(C.meta[fi])].len;
+        const R sf = (R)C.s(fi);
+        const R lf = (R)T.P[m_prof(C.meta(fi))].len;
         const R gf = M::sub(M::sub(sf, s), lf);
         if (GUARD && fabsf((float)gf) <= kEpsPos * (float)(fabs(sf - s) + lf)) g.hit = true, g.why |= (1u << 5);
         if (!(gf >= (R)0)) ok = false;                   // L17 (2)
       }
       if (ok && bi >= 0) {
-        const R sb = (R)C.s[bi];
+        const R sb = (R)C.s(bi);
         const R gb = M::sub(M::sub(s, sb), p.len);
         const R gbs = fabs(s - sb) + p.len;
         if (GUARD && fabsf((float)gb) <= kEpsPos * (float)gbs) g.hit = true, g.why |= (1u << 0);
         if (!(gb >= (R)0)) ok = false;                   // L17 (2)
         if (ok) {
-          const PV<R> pb = pvals(T.P[m_prof(C.meta[bi])], (R)0);
-          const R vb = (R)C.v[bi];
+          const PV<R> pb = pvals(T.P[m_prof(C.meta(bi))], (R)0);
+          const R vb = (R)C.v(bi);
           const R v0b = (pb.vmax < (R)T.vmax[ls]) ? pb.vmax : (R)T.vmax[ls];
           const R an = idm<R, GUARD>(vb, v0b, true, gb, M::sub(vb, v), pb, b_hard, gbs, g);
           if (GUARD && fabsf((float)(an + (R)A.b_safe)) <= kEpsAcc) g.hit = true, g.why |= (1u << 3);
@@ -447,16 +550,16 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
     if (inG && (adm0 || adm1)) {                         // discretionary: utilities + draw
       R a_of = (R)0, a_of_new = (R)0;                    // old follower (L10)
       if (of >= 0) {
-        const PV<R> po = pvals(T.P[m_prof(C.meta[of])], (R)0);
-        const R so = (R)C.s[of], vo = (R)C.v[of];
+        const PV<R> po = pvals(T.P[m_prof(C.meta(of))], (R)0);
+        const R so = (R)C.s(of), vo = (R)C.v(of);
         const R v0o = (po.vmax < (R)T.vmax[l]) ? po.vmax : (R)T.vmax[l];
         a_of = idm<R, GUARD>(vo, v0o, true, M::sub(M::sub(s, so), p.len), M::sub(vo, v), po,
                              b_hard, fabs(s - so) + p.len, g);
         const int li = lead >= 0 ? lead : i;             // free road if the ego has no leader
-        const R sl_ = (R)C.s[li];
-        const R ll_ = (R)T.P[m_prof(C.meta[li])].len;
+        const R sl_ = (R)C.s(li);
+        const R ll_ = (R)T.P[m_prof(C.meta(li))].len;
         a_of_new = idm<R, GUARD>(vo, v0o, lead >= 0, M::sub(M::sub(sl_, so), ll_),
-                                 M::sub(vo, (R)C.v[li]), po, b_hard, fabs(sl_ - so) + ll_, g);
+                                 M::sub(vo, (R)C.v(li)), po, b_hard, fabs(sl_ - so) + ll_, g);
       }
 #pragma unroll 1
       for (int sd = 0; sd < 2; ++sd) {
@@ -465,14 +568,14 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
         const int fi = sd == 0 ? f0 : f1, bi = sd == 0 ? b0 : b1;
         R a_nf = (R)0;
         if (bi >= 0) {                                   // new follower before the change
-          const PV<R> pb = pvals(T.P[m_prof(C.meta[bi])], (R)0);
-          const R sb = (R)C.s[bi], vb = (R)C.v[bi];
+          const PV<R> pb = pvals(T.P[m_prof(C.meta(bi))], (R)0);
+          const R sb = (R)C.s(bi), vb = (R)C.v(bi);
           const R v0b = (pb.vmax < (R)T.vmax[ls]) ? pb.vmax : (R)T.vmax[ls];
           const int fj = fi >= 0 ? fi : bi;              // free road if no front
-          const R sf = (R)C.s[fj];
-          const R lf = (R)T.P[m_prof(C.meta[fj])].len;
+          const R sf = (R)C.s(fj);
+          const R lf = (R)T.P[m_prof(C.meta(fj))].len;
           a_nf = idm<R, GUARD>(vb, v0b, fi >= 0, M::sub(M::sub(sf, sb), lf),
-                               M::sub(vb, (R)C.v[fj]), pb, b_hard, fabs(sf - sb) + lf, g);
+                               M::sub(vb, (R)C.v(fj)), pb, b_hard, fabs(sf - sb) + lf, g);
         }
         const R pol = M::add(M::sub(sd == 0 ? anew0 : anew1, a_nf), M::sub(a_of_new, a_of));
         if (sd == 0) pol0 = pol; else pol1 = pol;
@@ -494,79 +597,25 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
       }
     }
   }
-  // ---- O4-O6 on the current lane and on the admissible side lanes (one
-  // evaluation site, so the lane evaluation is instantiated once).  On the
-  // fp32 path a side is evaluated only if the draw can still fall below p_LC:
-  // with F = the free-road IDM bound of ã_ego on that lane, u <= (F - a_cur) +
-  // p * pol, and p_LC is monotone in u_T apart from its 2e-8 floor, so
-  // r >= p_LC(upper bound) + 1e-3 decides "stay" exactly ----
-  LEv<R> cur, ev0, ev1;
-  bool need0 = false, need1 = false;
-#pragma unroll 1
-  for (int k = 0; k < 3; ++k) {
-    if (k == 1) {
-      need0 = adm0 && (inG || mand < 0);
-      need1 = adm1 && (inG || mand > 0);
-      if (GUARD && inG && (need0 || need1)) {
-        R ub = (R)0;
-#pragma unroll 1
-        for (int sd = 0; sd < 2; ++sd) {
-          if (!(sd == 0 ? need0 : need1)) continue;
-          const int ls = sd == 0 ? sl0 : sl1;
-          const R v0s = (p.vmax < (R)T.vmax[ls]) ? p.vmax : (R)T.vmax[ls];
-          const R x = M::div(v, v0s);
-          const R x2 = M::mul(x, x);
-          R F = M::mul(p.a_max, M::sub((R)1, M::mul(x2, x2)));
-          F = (F < -b_hard) ? -b_hard : F;
-          const R U = M::add(M::sub(F, cur.a), M::mul((R)A.polite, sd == 0 ? pol0 : pol1));
-          ub = M::add(ub, ((R)0 < U) ? U : (R)0);
-        }
-        const double pmax = ub >= (R)1 ? 0.9 : fmax(2e-8, (double)(0.9 - 2e-8) * (double)ub);
-        if (r >= pmax + 1e-3) need0 = need1 = false;   // no change, for certain
-      }
-    }
-    if ((k == 1 && !need0) || (k == 2 && !need1)) continue;
-    const int ll = k == 0 ? l : (k == 1 ? sl0 : sl1);
-    const int li = k == 0 ? lead : (k == 1 ? f0 : f1);
-    const LEv<R> e = eval_lane<R, GUARD>(A, T, C, ll, li, s, v, p, me, g);
-    if (k == 0) cur = e;
-    else if (k == 1) ev0 = e;
-    else ev1 = e;
-  }
-  o.leader = cur.leader;
-  o.hops = cur.hops;
-  o.phantom = cur.phantom;
-  LEv<R> use = cur;
+  // ---- O4-O6 on the current lane ----
+  LEv<R> use = eval_lane<R, GUARD>(A, T, C, l, lead, s, v, p, me, g);
+  o.leader = use.leader;
+  o.hops = use.hops;
+  o.phantom = use.phantom;
   int lc = 0, new_l = l;
-  if (need0 || need1) {
-    int choice = -1;
-    if (inG) {
-      // MOBIL utility (tilde = after the change, ledger L13)
-      const R u0 = need0 ? M::add(M::sub(ev0.a, cur.a), M::mul((R)A.polite, pol0)) : (R)0;
-      const R u1 = need1 ? M::add(M::sub(ev1.a, cur.a), M::mul((R)A.polite, pol1)) : (R)0;
-      const R p0 = need0 ? (((R)0 < u0) ? u0 : (R)0) : (R)0;
-      const R p1 = need1 ? (((R)0 < u1) ? u1 : (R)0) : (R)0;
-      const R uT = M::add(p0, p1);
-      double pl;                                         // P:188-194, ledger L14
-      if (uT >= (R)1) pl = 0.9;
-      else if (uT > (R)0) pl = (double)M::mul((R)(0.9 - 2e-8), uT);
-      else pl = 2e-8;
-      if (GUARD && fabs(r - pl) <= (double)kEpsP) g.hit = true, g.why |= (1u << 6);
-      if (r < pl) {                                      // P:196, ledger L15
-        if (need0 && need1) {
-          if (GUARD && fabsf((float)(u0 - u1)) <= kEpsAcc) g.hit = true, g.why |= (1u << 7);
-          choice = (u0 >= u1) ? 0 : 1;
-        } else {
-          choice = need0 ? 0 : 1;
-        }
-      }
-    } else {
-      choice = mand < 0 ? 0 : 1;                         // ledger L18: admissible -> change
-    }
-    if (choice >= 0) {
-      use = choice == 0 ? ev0 : ev1;
-      lc = choice == 0 ? -1 : 1;
-      new_l = choice == 0 ? sl0 : sl1;
+  if (adm0 || adm1) {                                    // O7 decision (rare: out of line)
+    const SideRes<R> sr = lane_change<R, GUARD>(A, T, C, adm0, adm1, inG, mand, sl0, sl1, f0, f1,
+                                                s, v, p, me, use.a, pol0, pol1, r);
+    if (sr.hit) g.hit = true, g.why |= sr.why;
+    if (sr.choice >= 0) {
+      use.a = sr.a;
+      use.has_lim = sr.has_lim;
+      use.lim = sr.lim;
+      use.limrel = sr.limrel;
+      use.vlim = sr.vlim;
+      use.next1 = sr.next1;
+      lc = sr.choice == 0 ? -1 : 1;
+      new_l = sr.choice == 0 ? sl0 : sl1;
     }
   }
   // O8 integrate (ledger L1) + clamp (L22, L23).  The fp64 path follows the
@@ -646,7 +695,7 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
   s1 = M::fp64 ? pb : (hand == 0 ? s1 : M::add(pb, pa));
   const R vw = (R)A.v_wait;
   if (GUARD && fabsf((float)(v1 - vw)) <= kEpsV * (float)(fabs(v) + fabs(a) + (R)1)) g.hit = true, g.why |= (1u << 12);
-  o.wait1 = C.wait[i] + ((v1 < vw) ? 1 : 0);             // ledger L28
+  o.wait1 = C.wait(i) + ((v1 < vw) ? 1 : 0);             // ledger L28
   o.s1 = (float)s1;
   o.v1 = (float)v1;
   o.acc = (float)a;

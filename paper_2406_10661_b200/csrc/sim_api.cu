@@ -867,9 +867,7 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
     CK(h, cudaMemset(P.pubv[b], 0, nv * 4));
   }
   const int64_t sc = h->sum_cap + h->sum_icap;
-  Slab &sc_ = A.scratch;
-  AL(sc_.s, sc); AL(sc_.v, sc); AL(sc_.vid, sc); AL(sc_.nxt, sc); AL(sc_.nxt2, sc);
-  AL(sc_.meta, sc); AL(sc_.wait, sc);
+  AL(A.scratch, 7 * sc);
   AL(A.bsort_scratch, h->sum_icap);
   AL(A.dl_scratch, sc);
   for (int b = 0; b < 3; ++b) AL(P.summ[b], nl);
