@@ -664,10 +664,10 @@ __global__ void k_signal(SignalArgs a) {
   }
 }
 
-__global__ void k_apply_requests(int32_t *request, uint8_t *policy, const int32_t *junc,
-                                 const int32_t *phase, int m) {
-  if (blockIdx.x == 0 && threadIdx.x == 0)
-    for (int i = 0; i < m; ++i) request[junc[i]] = phase[i];   // in order
+__global__ void k_apply_requests(int32_t *request, const int32_t *junc, const int32_t *phase, int m) {
+  // entries are distinct junctions (the host keeps the last one per junction)
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) request[junc[i]] = phase[i];
 }
 
 __global__ void k_reduce_acc(const long long *tacc, int n_tiles, const int32_t *cnt,
@@ -703,10 +703,14 @@ __global__ void k_reduce_acc(const long long *tacc, int n_tiles, const int32_t *
 
 __global__ void k_lane_stats(StepArgs A, int32_t *cnt, int32_t *wt, float zone) {
   // lane queue length: per lane, vehicles and those with v < v_wait
-  // within the last `zone` metres, over stayers + inbox of each own tile
+  // within the last `zone` metres, over stayers + inbox of each own
+  // tile; a lane belongs to one tile, so its totals are written, not added
+  __shared__ int sc[kMaxTileLanes], sw[kMaxTileLanes];
   const int tile = A.tiles[blockIdx.x];
   const int ns = A.cnt_in[tile], ni = A.icnt_in[tile];
-  const int l0 = A.tile_lane_off[tile];
+  const int l0 = A.tile_lane_off[tile], nl = A.tile_lane_off[tile + 1] - l0;
+  if (threadIdx.x < kMaxTileLanes) sc[threadIdx.x] = sw[threadIdx.x] = 0;
+  __syncthreads();
   for (int i = threadIdx.x; i < ns + ni; i += blockDim.x) {
     float s, v;
     uint32_t meta;
@@ -717,9 +721,15 @@ __global__ void k_lane_stats(StepArgs A, int32_t *cnt, int32_t *wt, float zone) 
       const InboxRec r = A.inbox_in[A.tile_ibase[tile] + i - ns];
       s = r.s; v = r.v; meta = r.meta;
     }
-    const int g = A.tile_lanes[l0 + m_lane(meta)];
-    atomicAdd(&cnt[g], 1);
-    if (v < A.v_wait && (A.lane_len[g] - s) <= zone) atomicAdd(&wt[g], 1);
+    const int l = m_lane(meta);
+    atomicAdd(&sc[l], 1);
+    if (v < A.v_wait && (A.lane_len[A.tile_lanes[l0 + l]] - s) <= zone) atomicAdd(&sw[l], 1);
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+    const int g = A.tile_lanes[l0 + l];
+    cnt[g] = sc[l];
+    wt[g] = sw[l];
   }
 }
 
@@ -813,7 +823,8 @@ void launch_signal(const SignalArgs &a, void *stream) {
 
 void launch_apply_requests(int32_t *request, uint8_t *policy, const int32_t *junc,
                            const int32_t *phase, int m, void *stream) {
-  k_apply_requests<<<1, 1, 0, (cudaStream_t)stream>>>(request, policy, junc, phase, m);
+  (void)policy;
+  if (m > 0) k_apply_requests<<<(m + 255) / 256, 256, 0, (cudaStream_t)stream>>>(request, junc, phase, m);
 }
 
 void launch_reduce_acc(const long long *tacc, int n_tiles, const int32_t *cnt,

@@ -166,6 +166,10 @@ struct sim_s {
   uint8_t *stage_dir_d = nullptr;    // device staging for lane-direction setters
   void *pinned = nullptr;
   size_t pinned_cap = 0;
+  std::vector<int> req_mark;                    // set_signal_phase_batch: last entry per junction
+  int req_epoch = 0;
+  void *rd_pinned = nullptr;                    // read_metrics: counters + lane statistics
+  size_t rd_cap = 0;
   cudaEvent_t stage_ev = nullptr;
   int smem = 0;
   // device timing windows (sim_enable_timing / sim_read_timing)
@@ -1116,6 +1120,7 @@ static void destroy_impl(sim_s *h) {
   for (void *p : h->allocs) cudaFree(p);
   if (h->stage_d) cudaFree(h->stage_d);
   if (h->pinned) cudaFreeHost(h->pinned);
+  if (h->rd_pinned) cudaFreeHost(h->rd_pinned);
   if (h->stage_ev) cudaEventDestroy(h->stage_ev);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   if (h->comm) g_nccl.CommDestroy(h->comm);
@@ -1270,10 +1275,23 @@ sim_status sim_set_signal_phase_batch(sim_handle h, int32_t m, const int32_t *ju
     CK(h, cudaMalloc(&h->stage_d, 2 * (size_t)m * 4));
     h->stage_cap = 2 * m;
   }
+  // later entries for the same junction win: keep the last one per
+  // junction, so the device applies the batch in parallel
+  h->req_mark.resize(h->nj, -1);
   std::vector<int32_t> buf(2 * (size_t)m);
-  std::memcpy(buf.data(), junctions, m * 4);
-  std::memcpy(buf.data() + m, phases, m * 4);
-  st = push_staging(h, buf.data(), buf.size() * 4, h->stage_d);
+  int u = 0;
+  for (int i = m - 1; i >= 0; --i) {
+    const int j = junctions[i];
+    if (h->req_mark[j] == h->req_epoch) continue;
+    h->req_mark[j] = h->req_epoch;
+    buf[u] = j;
+    buf[m + u] = phases[i];
+    ++u;
+  }
+  if (++h->req_epoch == 0x7fffffff) { h->req_epoch = 0; std::fill(h->req_mark.begin(), h->req_mark.end(), -1); }
+  std::memmove(buf.data() + u, buf.data() + m, u * 4);
+  m = u;
+  st = push_staging(h, buf.data(), 2 * (size_t)m * 4, h->stage_d);
   if (st) return st;
   for (Part &P : h->parts) {           // replicated controllers: every partition applies it
     launch_apply_requests(P.SG.request, P.SG.policy, h->stage_d, h->stage_d + m, m, h->stream);
@@ -1482,9 +1500,55 @@ sim_status sim_read_metrics(sim_handle h, sim_metrics *m) {
   sim_status st = check(h);
   if (st) return st;
   if (!m) return fail(h, SIM_E_INVALID, "out is NULL");
-  std::vector<long long> c;
-  st = read_counters(h, c);
+  // everything is enqueued first and read back through one pinned buffer, so
+  // a read costs one synchronisation of the stream
+  const bool lanes = m->lane_count || m->lane_waiting_at_end;
+  const size_t ncnt = (size_t)(kNAcc + 3) * h->parts.size();
+  const size_t bytes = ncnt * 8 + (lanes ? 2 * (size_t)h->nl * 4 : 0);
+  if (h->rd_cap < bytes) {
+    CK(h, cudaStreamSynchronize(h->stream));
+    if (h->rd_pinned) cudaFreeHost(h->rd_pinned);
+    h->rd_pinned = nullptr;
+    CK(h, cudaHostAlloc(&h->rd_pinned, bytes, cudaHostAllocDefault));
+    h->rd_cap = bytes;
+  }
+  long long *hc = reinterpret_cast<long long *>(h->rd_pinned);
+  int32_t *hl = reinterpret_cast<int32_t *>(hc + ncnt);
+  for (Part &P : h->parts) {
+    StepArgs a = step_args(P, h->t);
+    launch_reduce_acc(P.A.tacc, h->nt, a.cnt_in, a.icnt_in, P.A.status, 0, P.red_d, h->stream);
+    h->n_launch += 1;
+  }
+  if (h->comm) {
+    Part &P = h->parts[0];
+    NK(h, g_nccl.AllReduce(P.red_d, P.red_d, kNAcc + 3, kNcclInt64, kNcclSum, h->comm, h->stream));
+  }
+  for (size_t q = 0; q < h->parts.size(); ++q)
+    CK(h, cudaMemcpyAsync(hc + q * (kNAcc + 3), h->parts[q].red_d, (kNAcc + 3) * 8,
+                          cudaMemcpyDeviceToHost, h->stream));
+  if (lanes) {
+    Part &P0 = h->parts[0];
+    int32_t *d = P0.lanestat_d;
+    // every lane belongs to one tile: the loopback partitions together write all
+    // of them; ranks of a real partition only their own, so zero first
+    if (h->comm) CK(h, cudaMemsetAsync(d, 0, 2 * (size_t)h->nl * 4, h->stream));
+    for (Part &P : h->parts) {
+      StepArgs a = step_args(P, h->t);
+      launch_lane_stats(a, d, d + h->nl, h->P.queue_zone_m, h->stream);
+      h->n_launch += 1;
+    }
+    if (h->comm) NK(h, g_nccl.AllReduce(d, d, 2 * (size_t)h->nl, 2 /*ncclInt32*/, kNcclSum, h->comm, h->stream));
+    CK(h, cudaMemcpyAsync(hl, d, 2 * (size_t)h->nl * 4, cudaMemcpyDeviceToHost, h->stream));
+  }
+  st = device_check(h);
   if (st) return st;
+  std::vector<long long> c(kNAcc + 3, 0);
+  for (size_t q = 0; q < h->parts.size(); ++q)
+    for (int k = 0; k < kNAcc + 3; ++k) c[k] += hc[q * (kNAcc + 3) + k];
+  if (c[ACC_OVERFLOW] > 0) {
+    h->sticky = SIM_E_CAPACITY;
+    return fail(h, SIM_E_CAPACITY, "a road-tile inbox or a migration buffer overflowed its capacity");
+  }
   m->t = h->t;
   m->n_driving = c[kNAcc];
   m->n_finished = h->fin0 + (c[ACC_FINISHED] - h->acc_fin0);
@@ -1498,23 +1562,8 @@ sim_status sim_read_metrics(sim_handle h, sim_metrics *m) {
   m->n_inserted = c[ACC_INSERTED];
   m->n_guard_hits = c[ACC_GUARD];
   m->att_finished = c[ACC_FINISHED] ? (double)c[ACC_SUM_TRAVEL] / (double)c[ACC_FINISHED] : 0.0;
-  if (m->lane_count || m->lane_waiting_at_end) {
-    Part &P0 = h->parts[0];
-    int32_t *d = P0.lanestat_d;
-    CK(h, cudaMemsetAsync(d, 0, 2 * (size_t)h->nl * 4, h->stream));
-    for (Part &P : h->parts) {          // every partition adds its own tiles' vehicles
-      StepArgs a = step_args(P, h->t);
-      launch_lane_stats(a, d, d + h->nl, h->P.queue_zone_m, h->stream);
-      h->n_launch += 1;
-    }
-    if (h->comm) NK(h, g_nccl.AllReduce(d, d, 2 * (size_t)h->nl, 2 /*ncclInt32*/, kNcclSum, h->comm, h->stream));
-    if (m->lane_count)
-      CK(h, cudaMemcpyAsync(m->lane_count, d, h->nl * 4, cudaMemcpyDeviceToHost, h->stream));
-    if (m->lane_waiting_at_end)
-      CK(h, cudaMemcpyAsync(m->lane_waiting_at_end, d + h->nl, h->nl * 4, cudaMemcpyDeviceToHost, h->stream));
-    st = device_check(h);
-    if (st) return st;
-  }
+  if (m->lane_count) std::memcpy(m->lane_count, hl, h->nl * 4);
+  if (m->lane_waiting_at_end) std::memcpy(m->lane_waiting_at_end, hl + h->nl, h->nl * 4);
   return SIM_OK;
 }
 
