@@ -118,7 +118,7 @@ struct StepArgs {
   Slab in, out;                     // stayer slabs
   const InboxRec *inbox_in;
   InboxRec *inbox_out;
-  uint32_t *scratch;                // per tile at 7 x (base + ibase): nxt, nxt2, wait of the snapshot, then (large tiles) s, v, vid, meta; stride cap + icap
+  uint32_t *scratch;                // snapshot of large tiles, at 5 x (base + ibase) words: s, v, vid, meta (stride cap + icap), then int16 src
   int32_t *bsort_scratch;           // [Σ icap] inbox sort order for large inboxes
   int32_t *dl_scratch;              // per-tile list of guard-deferred vehicles (scratch indexing)
   // migration to other partitions (world > 1): per-peer regions of MigRec

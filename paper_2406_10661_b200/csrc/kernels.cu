@@ -108,8 +108,8 @@ __device__ __forceinline__ void emit_moved(const StepArgs &A, const View &C, int
   rec.s = r.s1;
   rec.v = r.v1;
   rec.vid = vid;
-  rec.nxt = route_at(A, vid, cur, C.nxt(i), C.nxt2(i), r.cursor + 1);
-  rec.nxt2 = route_at(A, vid, cur, C.nxt(i), C.nxt2(i), r.cursor + 2);
+  rec.nxt = route_at(A, vid, cur, r.nxt, r.nxt2, r.cursor + 1);
+  rec.nxt2 = route_at(A, vid, cur, r.nxt, r.nxt2, r.cursor + 2);
   rec.meta = pack_meta(A.lane_local[r.lane_g], m_prof(meta), r.cursor);
   rec.wait = r.wait1;
   rec.pad = 0;
@@ -136,16 +136,11 @@ __device__ __forceinline__ void emit_moved(const StepArgs &A, const View &C, int
 
 struct StepShared {
   TileSh T;
-  union {
-    struct {
-      unsigned long long bk_hi[kSmemInbox];   // inbox keys (arrival order)
-      int bk_vid[kSmemInbox];
-      int bsort[kSmemInbox];
-      unsigned long long sk_hi[kSmemInbox];   // inbox keys in sorted order
-      int sk_vid[kSmemInbox];
-    };
-    int words[kDescMaxWords];                 // tile descriptor staging
-  };
+  unsigned long long bk_hi[kSmemInbox];       // inbox keys (arrival order)
+  int bk_vid[kSmemInbox];
+  int bsort[kSmemInbox];
+  unsigned long long sk_hi[kSmemInbox];       // inbox keys in sorted order
+  int sk_vid[kSmemInbox];
 };
 
 #ifndef KSTEP_WARPS
@@ -174,16 +169,13 @@ __device__ __forceinline__ void tile_load(const StepArgs &A, StepShared &S, unsi
   // with its target road, exit lane and the exit lane's reachable roads.
   const int tile = x.tile;
   const int doff = A.desc_off[tile];
-  const int dsz = A.desc_off[tile + 1] - doff;
   const int n_st = A.cnt_in[tile];
   const int n_in = A.icnt_in[tile];
   const int n = n_st + n_in;
   const int base = A.tile_base[tile];
   const int ibase = A.tile_ibase[tile];
-  for (int q = lane_id; q < (dsz >> 2); q += kThreads)
-    reinterpret_cast<int4 *>(S.words)[q] = reinterpret_cast<const int4 *>(A.desc + doff)[q];
-  __syncwarp();
-  const int nl = S.words[0], nroad = S.words[1], ne = S.words[2];
+  const int *W = A.desc + doff;                     // read straight from global (L2)
+  const int nl = W[0], nroad = W[1], ne = W[2];
   // lane records, the per-road-lane group tables and the (host-sorted) usable
   // successors go straight into the tile's shared metadata; only the stop bit
   // (signal of the junction lane at t) is computed here
@@ -198,10 +190,10 @@ __device__ __forceinline__ void tile_load(const StepArgs &A, StepShared &S, unsi
   }
   if (lane_id < nl) {
     const int l = lane_id;
-    const int fl = S.words[4 + 3 * nl + l];
-    T.glob[l] = S.words[4 + l];
-    T.len[l] = __int_as_float(S.words[4 + nl + l]);
-    T.vmax[l] = __int_as_float(S.words[4 + 2 * nl + l]);
+    const int fl = W[4 + 3 * nl + l];
+    T.glob[l] = W[4 + l];
+    T.len[l] = __int_as_float(W[4 + nl + l]);
+    T.vmax[l] = __int_as_float(W[4 + 2 * nl + l]);
     T.isroad[l] = l < nroad;
     T.usable[l] = fl & 1;
     T.seg_start[l] = 0;
@@ -211,7 +203,7 @@ __device__ __forceinline__ void tile_load(const StepArgs &A, StepShared &S, unsi
     T.left[l] = (l < nroad && l > 0) ? (int8_t)(l - 1) : (int8_t)-1;
     T.right[l] = (l < nroad - 1) ? (int8_t)(l + 1) : (int8_t)-1;
     if (l < nroad) {
-      const int *gw = S.words + 4 + 4 * nl + 6 * l;
+      const int *gw = W + 4 + 4 * nl + 6 * l;
       T.sn[l] = (uint8_t)((fl >> 8) & 0xff);
       T.ng[l] = (uint8_t)((fl >> 16) & 0xff);
       const unsigned g4 = (unsigned)gw[0];
@@ -225,7 +217,7 @@ __device__ __forceinline__ void tile_load(const StepArgs &A, StepShared &S, unsi
     }
   }
   if (lane_id < ne) {
-    const int *w = S.words + 4 + 4 * nl + 6 * nroad + 8 * lane_id;
+    const int *w = W + 4 + 4 * nl + 6 * nroad + 8 * lane_id;
     const int fl = w[3];
     SuccEnt e;
     e.j = w[0];
@@ -240,14 +232,14 @@ __device__ __forceinline__ void tile_load(const StepArgs &A, StepShared &S, unsi
   // snapshot view: shared memory, or this tile's global scratch if too large
   View C;
   const bool smem_ok = (n <= kSmemVeh) && (n_in <= kSmemInbox);
-  C.q = A.scratch + 7 * (size_t)(base + ibase);      // scratch region of the tile: 7 x (cap + icap) words
-  C.qt = T.cap + T.icap;
   if (smem_ok) {
     C.p = reinterpret_cast<uint32_t *>(dyn);
+    C.sp = reinterpret_cast<int16_t *>(dyn + kSmemVeh * 16);
     C.st = kSmemVeh;
-  } else {
-    C.p = C.q + 3 * C.qt;
-    C.st = C.qt;
+  } else {                                   // scratch region of the tile: 5 x (cap + icap) words
+    C.st = T.cap + T.icap;
+    C.p = A.scratch + 5 * (size_t)(base + ibase);
+    C.sp = reinterpret_cast<int16_t *>(C.p + 4 * C.st);
   }
   int *bsort = (n_in <= kSmemInbox) ? S.bsort : (A.bsort_scratch + ibase);
   const InboxRec *inb = A.inbox_in + ibase;
@@ -281,14 +273,13 @@ __device__ __forceinline__ void tile_load(const StepArgs &A, StepShared &S, unsi
   for (int i0 = lane_id; i0 < n_st; i0 += 2 * kThreads) {
     float sv[2], vv[2];
     uint32_t mv[2];
-    int idv[2], n1v[2], n2v[2], wv[2];
+    int idv[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int i = i0 + u * kThreads;
       if (i < n_st) {
         const int gi = base + i;
         sv[u] = A.in.s[gi]; vv[u] = A.in.v[gi]; mv[u] = A.in.meta[gi]; idv[u] = A.in.vid[gi];
-        n1v[u] = A.in.nxt[gi]; n2v[u] = A.in.nxt2[gi]; wv[u] = A.in.wait[gi];
       }
     }
 #pragma unroll
@@ -315,15 +306,14 @@ __device__ __forceinline__ void tile_load(const StepArgs &A, StepShared &S, unsi
     C.s(pos) = s;
     C.v(pos) = vv[u];
     C.vid(pos) = vid;
-    C.nxt(pos) = n1v[u];
-    C.nxt2(pos) = n2v[u];
     C.meta(pos) = meta;
-    C.wait(pos) = wv[u];
+    C.src(pos) = (int16_t)i;
     }
   }
   // inbox records: position = sorted rank + #stayers below (binary search in the slab)
   for (int r = lane_id; r < n_in; r += kThreads) {
-    const InboxRec rec = inb[bsort[r]];
+    const int j = bsort[r];
+    const InboxRec rec = inb[j];
     const unsigned long long h = hikey(m_lane(rec.meta), rec.s);
     int lo = 0, hi = n_st;
     while (lo < hi) {
@@ -336,10 +326,8 @@ __device__ __forceinline__ void tile_load(const StepArgs &A, StepShared &S, unsi
     C.s(pos) = rec.s;
     C.v(pos) = rec.v;
     C.vid(pos) = rec.vid;
-    C.nxt(pos) = rec.nxt;
-    C.nxt2(pos) = rec.nxt2;
     C.meta(pos) = rec.meta;
-    C.wait(pos) = rec.wait;
+    C.src(pos) = (int16_t)(-j - 1);
   }
   __syncwarp();
   // lane segments of the snapshot
@@ -413,8 +401,8 @@ __device__ __forceinline__ void tile_update(const StepArgs &A, StepShared &S, co
       A.out.s[pos] = r.s1;
       A.out.v[pos] = r.v1;
       A.out.vid[pos] = C.vid(i);
-      A.out.nxt[pos] = C.nxt(i);
-      A.out.nxt2[pos] = C.nxt2(i);
+      A.out.nxt[pos] = r.nxt;
+      A.out.nxt2[pos] = r.nxt2;
       A.out.meta[pos] = meta;
       A.out.wait[pos] = r.wait1;
       atomicMin(&T.first_out[m_lane(meta)], pos);
@@ -563,7 +551,7 @@ __global__ void __launch_bounds__(kStepWarps * kThreads, KSTEP_MINB)
   __shared__ int s_base;
   const int warp = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
   StepShared &S = SS[warp];
-  unsigned char *dyn = dyn_all + (size_t)warp * (kSmemVeh * 4 * 4);
+  unsigned char *dyn = dyn_all + (size_t)warp * (kSmemVeh * 18);
   if (A.n_prof <= kSmemProf) {                      // profiles as int4 words (Prof is 96 B)
     const int nw = A.n_prof * (int)(sizeof(Prof) / 16);
     for (int q = threadIdx.x; q < nw; q += blockDim.x)
@@ -794,7 +782,7 @@ __global__ void k_halo_unpack(StepArgs A, const int32_t *lanes, const HaloRec *b
 }
 
 // ---- launchers ---------------------------------------------------------------
-int step_smem_bytes() { return kStepWarps * kSmemVeh * 4 * 4; }
+int step_smem_bytes() { return kStepWarps * kSmemVeh * 18; }
 
 void launch_step(const StepArgs &a, void *stream, int smem_bytes) {
   static int resident[2] = {0, 0};                  // resident blocks per GPU, per instantiation

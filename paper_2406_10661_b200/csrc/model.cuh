@@ -89,27 +89,27 @@ struct TileSh {
   SuccEnt se[kMaxRoadLanes][kMaxSucc];   // sorted by (target road, lane id)
   int glob[kMaxTileLanes];
   float len[kMaxTileLanes], vmax[kMaxTileLanes];
-  int seg_start[kMaxTileLanes], seg_end[kMaxTileLanes];
+  int16_t seg_start[kMaxTileLanes], seg_end[kMaxTileLanes];   // lane segments of the snapshot
   int first_out[kMaxTileLanes];
   int8_t left[kMaxTileLanes], right[kMaxTileLanes];
   uint8_t isroad[kMaxTileLanes], usable[kMaxTileLanes];
 };
 
-// Snapshot of the tile at time t.  The fields other vehicles read (s, v, vid,
-// meta) are four word arrays of stride st from p (shared memory, or the
-// tile's global scratch when the tile is large); the fields only the vehicle
-// itself uses (nxt, nxt2, wait) are three word arrays of stride qt from q
-// (always global scratch), which keeps 16 B per vehicle in shared memory.
+// Snapshot of the tile at time t: the fields other vehicles read (s, v, vid,
+// meta) are four word arrays of stride st from p (shared memory, or the tile's
+// global scratch when the tile is large); src(i) says where slot i came from
+// (stayer index >= 0, or -(inbox record + 1)), so the fields only the vehicle
+// itself uses (nxt, nxt2, wait) are read once from the slab / inbox when the
+// vehicle is updated instead of being staged (16 + 2 B per vehicle on chip).
 struct View {
-  uint32_t *p, *q;
-  int st, qt;
+  uint32_t *p;
+  int16_t *sp;
+  int st;
   __device__ __forceinline__ float &s(int i) const { return reinterpret_cast<float *>(p)[i]; }
   __device__ __forceinline__ float &v(int i) const { return reinterpret_cast<float *>(p)[st + i]; }
   __device__ __forceinline__ int32_t &vid(int i) const { return reinterpret_cast<int32_t *>(p)[2 * st + i]; }
   __device__ __forceinline__ uint32_t &meta(int i) const { return p[3 * st + i]; }
-  __device__ __forceinline__ int32_t &nxt(int i) const { return reinterpret_cast<int32_t *>(q)[i]; }
-  __device__ __forceinline__ int32_t &nxt2(int i) const { return reinterpret_cast<int32_t *>(q)[qt + i]; }
-  __device__ __forceinline__ int32_t &wait(int i) const { return reinterpret_cast<int32_t *>(q)[2 * qt + i]; }
+  __device__ __forceinline__ int16_t &src(int i) const { return sp[i]; }
 };
 
 __device__ __forceinline__ int m_lane(uint32_t m) { return (int)(m & 0xffu); }
@@ -328,6 +328,7 @@ __device__ LEv<R> eval_lane(const StepArgs &A, const TileSh &T, const View &C, i
 
 struct Res {
   float s1, v1, acc;
+  int nxt, nxt2;                     // route[c+1], route[c+2] of the snapshot (cursor c)
   int lane_g, cursor;
   int lc, hand;
   bool fin;
@@ -449,8 +450,23 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
   Me me;
   me.vid = C.vid(i);
   me.cur = m_cursor(meta);
-  me.nxt = C.nxt(i);
-  me.nxt2 = C.nxt2(i);
+  int wait0;                                             // ego-only fields (slab or inbox)
+  {
+    const int si = C.src(i);
+    if (si >= 0) {
+      const int gi = T.base + si;
+      me.nxt = A.in.nxt[gi];
+      me.nxt2 = A.in.nxt2[gi];
+      wait0 = A.in.wait[gi];
+    } else {
+      const InboxRec *r = A.inbox_in + T.ibase + (-si - 1);
+      me.nxt = r->nxt;
+      me.nxt2 = r->nxt2;
+      wait0 = r->wait;
+    }
+  }
+  o.nxt = me.nxt;
+  o.nxt2 = me.nxt2;
   const PV<R> p = pvals(T.P[pr], (R)0);
   const R s = (R)C.s(i), v = (R)C.v(i);
   const R L = (R)T.len[l];
@@ -695,7 +711,7 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
   s1 = M::fp64 ? pb : (hand == 0 ? s1 : M::add(pb, pa));
   const R vw = (R)A.v_wait;
   if (GUARD && fabsf((float)(v1 - vw)) <= kEpsV * (float)(fabs(v) + fabs(a) + (R)1)) g.hit = true, g.why |= (1u << 12);
-  o.wait1 = C.wait(i) + ((v1 < vw) ? 1 : 0);             // ledger L28
+  o.wait1 = wait0 + ((v1 < vw) ? 1 : 0);                 // ledger L28
   o.s1 = (float)s1;
   o.v1 = (float)v1;
   o.acc = (float)a;

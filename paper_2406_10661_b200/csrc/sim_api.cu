@@ -551,6 +551,8 @@ sim_status build_tiles(sim_s *h) {
     }
     cap = cap + cap / 4 + 16;
     int icap = cap + feed[r] + h->tile_nroad[r] + 16;
+    if (cap > 32767 || icap > 32767)                // snapshot source indices are int16
+      return fail(h, SIM_E_INVALID, "road " + std::to_string(r) + " is too long (tile capacity > 32767 vehicles)");
     h->tile_lane_off[r + 1] = (int)h->tile_lanes.size();
     h->tile_base[r] = (int)base; h->tile_cap[r] = cap;
     h->tile_ibase[r] = (int)ibase; h->tile_icap[r] = icap;
@@ -871,7 +873,7 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
     CK(h, cudaMemset(P.pubv[b], 0, nv * 4));
   }
   const int64_t sc = h->sum_cap + h->sum_icap;
-  AL(A.scratch, 7 * sc);
+  AL(A.scratch, 5 * sc);
   AL(A.bsort_scratch, h->sum_icap);
   AL(A.dl_scratch, sc);
   for (int b = 0; b < 3; ++b) AL(P.summ[b], nl);
