@@ -72,7 +72,8 @@ typedef struct {
   const uint8_t *phase_green;        /* for junction j, phase k: row of n_slots(j) bytes,
                                         rows laid out junction by junction, phase by phase */
   const int32_t *phase_green_steps;  /* [n_phases] FIXED_TIME green duration (steps) */
-  const uint8_t *junc_policy;        /* [n_junctions] 0 NONE 1 FIXED_TIME 2 MANUAL */
+  const uint8_t *junc_policy;        /* [n_junctions] 0 NONE 1 FIXED_TIME 2 MANUAL
+                                        3 MAX_PRESSURE */
   const int32_t *junc_offset_steps;  /* [n_junctions] FIXED_TIME cycle offset */
 } sim_graph;
 
@@ -111,6 +112,12 @@ typedef struct {
   int32_t rank, world, loopback;
   const uint8_t *nccl_id;            /* 128 bytes, NCCL mode only */
   const int32_t *road_owner;
+  /* MAX_PRESSURE: a green phase is kept for at least
+   * this many steps, then the phase of maximum pressure (sum over its green
+   * movements of count(predecessor lane) - count(successor lane), DRIVING
+   * vehicles in state(t); ties -> lowest index) is chosen, with the yellow
+   * steps in between when it changes.  <= 0: 30. */
+  int32_t max_pressure_period;
 } sim_params;
 
 typedef struct {

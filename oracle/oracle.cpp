@@ -10,7 +10,8 @@
 //   * IDM, randomized MOBIL, signal response,
 //     App. A2.3;
 //   * the Step() sequence of App. A2.2;
-//   * signal policies, metrics.
+//   * signal policies incl. MAX_PRESSURE (
+//     Varaiya 2013, readings L38-L41), metrics.
 // Build: g++ -std=c++17 -O2 -ffp-contract=off -fno-fast-math -shared -fPIC.
 #include "oracle.h"
 
@@ -26,7 +27,7 @@ namespace {
 enum { PENDING = 0, DRIVING = 1, FINISHED = 2 };
 enum { TURN_STRAIGHT = 0, TURN_LEFT = 1, TURN_RIGHT = 2 };
 enum { KIND_NORMAL = 0, KIND_DYNAMIC = 1, KIND_TIDAL = 2 };
-enum { POL_NONE = 0, POL_FIXED = 1, POL_MANUAL = 2 };
+enum { POL_NONE = 0, POL_FIXED = 1, POL_MANUAL = 2, POL_MAXP = 3 };
 enum { SIG_GREEN = 0, SIG_YELLOW = 1, SIG_RED = 2 };
 const int LANE_DEST = -2, LANE_BLOCKED = -3;
 
@@ -78,6 +79,7 @@ struct Sim {
   std::vector<Profile> prof;
   double p_polite = 0.1, b_hard = 8, b_safe = 4, v_wait = 0.1, queue_zone = 100;
   int Y = 3, K = 2;
+  int mp_period = 30;                      // MAX_PRESSURE decision period (L41)
   bool store_fp32 = false, reverse_order = false;
   double start_margin = 0;
   // state
@@ -245,8 +247,42 @@ struct Sim {
       }
     }
   }
-  void advance_junction(Junction &j) const {
-    if (j.policy == POL_FIXED) {
+  // Max-pressure phase choice ("the junctions collect the pressures of
+  // entering and exiting lanes and update the signal phases using the maximum
+  // pressure algorithm"; Varaiya 2013): movement pressure of junction lane l =
+  // count(predecessor lane) - count(successor lane) with counts = DRIVING
+  // vehicles per lane in state(t) (L39); phase pressure = sum over its green
+  // movements (L40); the argmax phase, ties -> lowest index.
+  int max_pressure_phase(const Junction &j, const std::vector<std::vector<int>> &order) const {
+    int best = 0;
+    long long best_p = 0;
+    for (size_t k = 0; k < j.green.size(); ++k) {
+      long long pk = 0;
+      for (size_t q = 0; q < j.lanes.size(); ++q) {
+        if (!j.green[k][q]) continue;
+        const int l = j.lanes[q];
+        pk += (long long)order[pred[l][0]].size() - (long long)order[succ[l][0]].size();
+      }
+      if (k == 0 || pk > best_p) { best = (int)k; best_p = pk; }
+    }
+    return best;
+  }
+  // O11 for one junction; `order` = the lane order of state(t) (MAX_PRESSURE)
+  void advance_junction(Junction &j, const std::vector<std::vector<int>> *order = nullptr) const {
+    if (j.policy == POL_MAXP) {                  // L41
+      if (j.yellow > 0) {
+        j.yellow -= 1;
+        if (j.yellow == 0) { j.phase = j.pending; j.elapsed = 0; }
+      } else {
+        j.elapsed += 1;
+        if (j.elapsed >= mp_period) {
+          const int nxt = max_pressure_phase(j, *order);
+          if (nxt == j.phase) j.elapsed = 0;     // keep the green for another period
+          else if (Y > 0) { j.yellow = Y; j.pending = nxt; }
+          else { j.phase = nxt; j.pending = nxt; j.elapsed = 0; }
+        }
+      }
+    } else if (j.policy == POL_FIXED) {
       if (j.yellow > 0) {
         j.yellow -= 1;
         if (j.yellow == 0) { j.phase = j.pending; j.elapsed = 0; }
@@ -390,7 +426,7 @@ struct Sim {
     if (store_fp32)
       for (auto &me : V)
         if (me.status == DRIVING) { me.s = (double)(float)me.s; me.v = (double)(float)me.v; }
-    for (auto &j : J) advance_junction(j);                 // O11
+    for (auto &j : J) advance_junction(j, &order);         // O11 (counts of state(t))
     t += 1;
   }
 
@@ -645,6 +681,7 @@ void *or_create(const or_graph *g, const or_trips *tr, const or_params *pp,
   S->b_safe = (double)pp->b_safe; S->v_wait = (double)pp->v_wait;
   S->queue_zone = (double)pp->queue_zone_m;
   S->Y = pp->yellow_steps; S->K = pp->lookahead_lanes;
+  S->mp_period = pp->max_pressure_period > 0 ? pp->max_pressure_period : 30;
   S->store_fp32 = pp->store_fp32 != 0; S->reverse_order = pp->reverse_order != 0;
   // lane-start margin (L17): v_cap + 0.5 * a_cap, from the fp32 inputs
   double vcap = 0, acap = 0;

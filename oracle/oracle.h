@@ -31,7 +31,7 @@ typedef struct {
   const int32_t *junc_phase_offsets;
   const uint8_t *phase_green;
   const int32_t *phase_green_steps;
-  const uint8_t *junc_policy;
+  const uint8_t *junc_policy;   /* 0 NONE 1 FIXED_TIME 2 MANUAL 3 MAX_PRESSURE */
   const int32_t *junc_offset_steps;
 } or_graph;
 
@@ -53,6 +53,7 @@ typedef struct {
   int32_t yellow_steps, lookahead_lanes;
   int32_t store_fp32;           /* round s, v to fp32 after every step */
   int32_t reverse_order;        /* process vehicles in reverse vid order (P-PERM) */
+  int32_t max_pressure_period;  /* MAX_PRESSURE decision period in steps (<= 0: 30) */
 } or_params;
 
 typedef struct {

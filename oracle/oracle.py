@@ -87,7 +87,8 @@ class _Params(C.Structure):
                 ("politeness", C.c_float), ("b_hard", C.c_float), ("b_safe", C.c_float),
                 ("v_wait", C.c_float), ("queue_zone_m", C.c_float),
                 ("yellow_steps", C.c_int32), ("lookahead_lanes", C.c_int32),
-                ("store_fp32", C.c_int32), ("reverse_order", C.c_int32)]
+                ("store_fp32", C.c_int32), ("reverse_order", C.c_int32),
+                ("max_pressure_period", C.c_int32)]
 
 
 class _State(C.Structure):
@@ -148,7 +149,7 @@ class Oracle:
         Pm = _Params(p["seed"], prof.shape[0], _ptr(prof), p["politeness"], p["b_hard"],
                      p["b_safe"], p["v_wait"], p["queue_zone_m"], p["yellow_steps"],
                      p["lookahead_lanes"] if lookahead is None else lookahead,
-                     int(store_fp32), int(reverse_order))
+                     int(store_fp32), int(reverse_order), int(p.get("max_pressure_period", 30)))
         err = C.create_string_buffer(512)
         self.h = lib.or_create(C.byref(G), C.byref(T), C.byref(Pm), err, 512)
         if not self.h:

@@ -46,7 +46,7 @@ enum Acc {
 };
 enum { ST_PENDING = 0, ST_DRIVING = 1, ST_FINISHED = 2 };
 enum { SIG_GREEN = 0, SIG_YELLOW = 1, SIG_RED = 2 };
-enum { POL_NONE = 0, POL_FIXED = 1, POL_MANUAL = 2 };
+enum { POL_NONE = 0, POL_FIXED = 1, POL_MANUAL = 2, POL_MAXP = 3 };
 enum { KIND_NORMAL = 0, KIND_DYNAMIC = 1, KIND_TIDAL = 2 };
 constexpr int kLaneDest = -2, kLaneBlocked = -3;
 
@@ -143,6 +143,7 @@ struct StepArgs {
   int32_t *pend_head;
   const Prof *prof;
   long long *tacc;                  // [n_tiles][kNAcc]
+  int32_t *lane_cnt_next;           // [n_lanes] vehicles per lane at t+1 (MAX_PRESSURE; NULL if unused)
   // decision recording (vid-indexed), optional
   int32_t *r_leader, *r_of, *r_side;
   int8_t *r_hops, *r_phantom, *r_lc, *r_hand, *r_fin, *r_ins;
@@ -160,6 +161,11 @@ struct SignalArgs {
   const uint8_t *green;
   const int32_t *green_steps;
   uint8_t *lane_sig;
+  // MAX_PRESSURE: per junction-lane slot its predecessor
+  // and successor lane, lane vehicle counts of state(t), decision period
+  const int32_t *jl_pred, *jl_succ;
+  const int32_t *lane_cnt;
+  int32_t mp_period;
 };
 
 // kernel launchers (kernels.cu)

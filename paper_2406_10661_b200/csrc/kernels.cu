@@ -121,6 +121,7 @@ __device__ __forceinline__ void emit_moved(const StepArgs &A, const View &C, int
     else acc.ovf += 1;
     atomicMin(&A.summ_next[r.lane_g], vkey(r.s1, vid));
     A.pubv_next[vid] = r.v1;
+    if (A.lane_cnt_next) atomicAdd(&A.lane_cnt_next[r.lane_g], 1);
   } else {                                          // migrant to another partition
     const int slot = atomicAdd(&A.out_cnt[owner], 1);
     if (slot < A.out_cap[owner]) {
@@ -450,6 +451,12 @@ __device__ __forceinline__ void tile_finish(const StepArgs &A, StepShared &S, co
       A.pubv_next[vid] = A.out.v[pos];
     }
     A.summ_clear[g] = kEmptyKey;
+    if (A.lane_cnt_next && pos != 0x7fffffff) {     // stayers of lane l: [pos, next lane's first)
+      int end = base + run;
+      for (int q = l + 1; q < nl; ++q)
+        if (T.first_out[q] != 0x7fffffff) { end = T.first_out[q]; break; }
+      atomicAdd(&A.lane_cnt_next[g], end - pos);
+    }
   }
   for (int l = lane_id; l < nroad; l += kThreads) { // departures (K11; ledger L25)
     const int g = T.glob[l];
@@ -490,6 +497,7 @@ __device__ __forceinline__ void tile_finish(const StepArgs &A, StepShared &S, co
     else acc.ovf += 1;
     atomicMin(&A.summ_next[g], vkey(rec.s, k));
     A.pubv_next[k] = 0.f;
+    if (A.lane_cnt_next) atomicAdd(&A.lane_cnt_next[g], 1);
     A.pend_head[g] = h + 1;
     A.status[k] = ST_DRIVING;
     A.insert_time[k] = A.t + 1;
@@ -585,61 +593,71 @@ __global__ void __launch_bounds__(kStepWarps * kThreads, KSTEP_MINB)
 }
 
 // ---- a5: per-junction signal controller -------------
-// One warp per junction: lane 0 applies requests and advances the phase
-// machine, all lanes write the signals of the junction's lanes (coalesced).
+// One warp per junction.  Every lane runs the (tiny) phase machine on the same
+// inputs; the MAX_PRESSURE choice is a warp reduction of the
+// movement pressures count(pred) - count(succ) over the green slots of each
+// phase; lane 0 stores the state, all lanes write the junction's signals.
 __global__ void k_signal(SignalArgs a) {
   const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (j >= a.n_junctions) return;
   const int K = a.ph_off[j + 1] - a.ph_off[j];
-  int pol = 0, ph = 0;
-  int y = 0;
-  if (lane == 0) {
-    pol = a.policy[j];
-    ph = a.phase[j];
-    int el = a.elapsed[j], q = a.pending[j];
-    y = a.yellow_left[j];
-    const int req = a.request[j];
-    if (req >= 0) {                                 // requests apply before sig_t (L35)
-      a.request[j] = -1;
-      pol = POL_MANUAL;
-      if (y > 0) q = req;
-      else if (req != ph) {
-        if (a.yellow > 0) { y = a.yellow; q = req; }
-        else { ph = req; q = req; }
-      }
+  const int j0 = a.jl_off[j], nj = a.jl_off[j + 1] - j0;
+  int pol = a.policy[j], ph = a.phase[j];
+  int el = a.elapsed[j], q = a.pending[j], y = a.yellow_left[j];
+  const int req = a.request[j];
+  if (req >= 0) {                                   // requests apply before sig_t (L35)
+    pol = POL_MANUAL;
+    if (y > 0) q = req;
+    else if (req != ph) {
+      if (a.yellow > 0) { y = a.yellow; q = req; }
+      else { ph = req; q = req; }
     }
-    // advance t -> t+1 (O11) into the stored state; sig_t uses (pol, ph, y) above
-    int nph = ph, ny = y, nel = el, nq = q;
-    if (pol == POL_FIXED && K > 0) {
-      if (ny > 0) {
-        ny -= 1;
-        if (ny == 0) { nph = nq; nel = 0; }
-      } else {
-        nel += 1;
-        if (nel >= a.green_steps[a.ph_off[j] + nph]) {
-          const int nx = (nph + 1) % K;
-          if (a.yellow > 0) { ny = a.yellow; nq = nx; }
-          else { nph = nx; nq = nx; nel = 0; }
-        }
-      }
-    } else if (pol == POL_MANUAL) {
-      if (ny > 0) {
-        ny -= 1;
-        if (ny == 0) nph = nq;
-      }
+  }
+  // advance t -> t+1 (O11) into the stored state; sig_t uses (pol, ph, y) above
+  int nph = ph, ny = y, nel = el, nq = q;
+  if ((pol == POL_FIXED || pol == POL_MAXP) && K > 0) {
+    if (ny > 0) {
+      ny -= 1;
+      if (ny == 0) { nph = nq; nel = 0; }
+    } else {
       nel += 1;
+      if (pol == POL_FIXED && nel >= a.green_steps[a.ph_off[j] + nph]) {
+        const int nx = (nph + 1) % K;
+        if (a.yellow > 0) { ny = a.yellow; nq = nx; }
+        else { nph = nx; nq = nx; nel = 0; }
+      } else if (pol == POL_MAXP && nel >= a.mp_period) {
+        // movement pressures of this lane's slots, then per phase a warp sum
+        const uint8_t *gr = a.green + a.green_off[j];
+        int best = 0, best_p = 0;
+        for (int k = 0; k < K; ++k) {
+          int part = 0;
+          for (int sl = lane; sl < nj; sl += 32)
+            if (gr[(int64_t)k * nj + sl])
+              part += a.lane_cnt[a.jl_pred[j0 + sl]] - a.lane_cnt[a.jl_succ[j0 + sl]];
+          const int pk = __reduce_add_sync(0xffffffffu, part);
+          if (k == 0 || pk > best_p) { best = k; best_p = pk; }     // ties -> lowest index
+        }
+        if (best == nph) nel = 0;                   // keep the green for another period
+        else if (a.yellow > 0) { ny = a.yellow; nq = best; }
+        else { nph = best; nq = best; nel = 0; }
+      }
     }
+  } else if (pol == POL_MANUAL) {
+    if (ny > 0) {
+      ny -= 1;
+      if (ny == 0) nph = nq;
+    }
+    nel += 1;
+  }
+  if (lane == 0) {
+    if (req >= 0) a.request[j] = -1;
     a.policy[j] = (uint8_t)pol;
     a.phase[j] = nph;
     a.elapsed[j] = nel;
     a.yellow_left[j] = ny;
     a.pending[j] = nq;
   }
-  pol = __shfl_sync(0xffffffffu, pol, 0);
-  ph = __shfl_sync(0xffffffffu, ph, 0);
-  y = __shfl_sync(0xffffffffu, y, 0);
-  const int j0 = a.jl_off[j], nj = a.jl_off[j + 1] - j0;
   const uint8_t *grow = a.green + a.green_off[j] + (int64_t)ph * nj;
   for (int k = lane; k < nj; k += 32) {
     uint8_t sg;
@@ -755,6 +773,7 @@ __global__ void k_absorb(StepArgs A, const MigRec *in_buf, const int32_t *in_off
     if (slot < A.tile_icap[dt]) put_inbox(A.inbox_out + A.tile_ibase[dt] + slot, m.rec);
     atomicMin(&A.summ_next[lane_g], vkey(m.rec.s, vid));
     A.pubv_next[vid] = m.rec.v;
+    if (A.lane_cnt_next) atomicAdd(&A.lane_cnt_next[lane_g], 1);
     A.insert_time[vid] = m.insert_time;
     A.status[vid] = ST_DRIVING;
   }

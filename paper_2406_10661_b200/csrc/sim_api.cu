@@ -167,6 +167,9 @@ struct sim_s {
   void *pinned = nullptr;
   size_t pinned_cap = 0;
   std::vector<int> req_mark;                    // set_signal_phase_batch: last entry per junction
+  int32_t *lcnt[3] = {nullptr, nullptr, nullptr}; // MAX_PRESSURE lane counts for t, t+1, t+2 (mod 3)
+  bool any_maxp = false;                        // some junction runs MAX_PRESSURE
+  std::vector<int> jl_pred, jl_succ;            // per junction-lane slot: predecessor / successor lane
   int req_epoch = 0;
   void *rd_pinned = nullptr;                    // read_metrics: counters + lane statistics
   size_t rd_cap = 0;
@@ -426,13 +429,19 @@ sim_status validate_and_copy(sim_s *h, const sim_graph *g, const sim_trips *tr,
   h->pol0.assign(g->junc_policy, g->junc_policy + nj);
   h->offset0.assign(g->junc_offset_steps, g->junc_offset_steps + nj);
   h->green_off.assign(nj + 1, 0);
+  h->jl_pred.assign(h->jl.size(), 0);
+  h->jl_succ.assign(h->jl.size(), 0);
+  for (size_t e = 0; e < h->jl.size(); ++e) {       // junction lanes: one predecessor, one successor
+    const int l = h->jl[e];
+    if (l >= 0 && l < nl) { h->jl_pred[e] = std::max(h->pred[l], 0); h->jl_succ[e] = h->succ[h->succ_off[l]]; }
+  }
   for (int j = 0; j < nj; ++j) {
     int ns = h->jl_off[j + 1] - h->jl_off[j], np = h->ph_off[j + 1] - h->ph_off[j];
     if (ns < 0 || np < 0) return fail(h, SIM_E_INVALID, "bad junction CSR");
     for (int e = h->jl_off[j]; e < h->jl_off[j + 1]; ++e)
       if (h->jl[e] < 0 || h->jl[e] >= nl || h->junc[h->jl[e]] != j)
         return fail(h, SIM_E_INVALID, "junc_lanes inconsistent with lane_junction (junction " + std::to_string(j) + ")");
-    if (h->pol0[j] > 2) return fail(h, SIM_E_INVALID, "bad junc_policy");
+    if (h->pol0[j] > 3) return fail(h, SIM_E_INVALID, "bad junc_policy");
     for (int k = h->ph_off[j]; k < h->ph_off[j + 1]; ++k)
       if (h->pol0[j] == POL_FIXED && h->green_steps[k] < 1)
         return fail(h, SIM_E_INVALID, "FIXED_TIME green durations must be >= 1");
@@ -766,6 +775,17 @@ sim_status upload_state(sim_s *h, const HostState &S) {
   }
   std::vector<int> head(poff.begin(), poff.end() - 1);
   std::vector<int> req(h->nj, -1);
+  // MAX_PRESSURE lane counts of state(t) (L39)
+  h->any_maxp = false;
+  for (int j = 0; j < h->nj; ++j) h->any_maxp |= S.jpol[j] == POL_MAXP;
+  {
+    std::vector<int32_t> lc(h->nl, 0);
+    for (int k = 0; k < nv; ++k)
+      if (S.status[k] == ST_DRIVING) lc[S.lane[k]] += 1;
+    CK(h, cudaMemcpyAsync(h->lcnt[t % 3], lc.data(), h->nl * 4, cudaMemcpyHostToDevice, h->stream));
+    CK(h, cudaMemsetAsync(h->lcnt[(t + 1) % 3], 0, h->nl * 4, h->stream));
+    CK(h, cudaMemsetAsync(h->lcnt[(t + 2) % 3], 0, h->nl * 4, h->stream));
+  }
   for (Part &P : h->parts) {
     cudaStream_t st = h->stream;
     std::vector<int> pc(nt, 0);
@@ -944,6 +964,11 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   UP(u8, h->green); G.green = u8;
   UP(i32, h->green_steps); G.green_steps = i32;
   G.lane_sig = sig;
+  UP(i32, h->jl_pred); G.jl_pred = i32;
+  UP(i32, h->jl_succ); G.jl_succ = i32;
+  G.mp_period = h->P.max_pressure_period > 0 ? h->P.max_pressure_period : 30;
+  if (!h->lcnt[0])                                  // shared by loopback partitions
+    for (int b = 0; b < 3; ++b) { AL(h->lcnt[b], nl); CK(h, cudaMemset(h->lcnt[b], 0, nl * 4)); }
   // constants
   A.n_tiles = nt; A.n_lanes = nl; A.n_veh = nv;
   A.seed = h->P.seed;
@@ -975,6 +1000,7 @@ StepArgs step_args(const Part &P, int t) {
   a.summ_clear = P.summ[(t + 2) % 3];
   a.pubv_cur = P.pubv[par];
   a.pubv_next = P.pubv[par ^ 1];
+  a.lane_cnt_next = nullptr;
   return a;
 }
 
@@ -1043,10 +1069,20 @@ sim_status step_once(sim_s *h) {
     h->ev_used += 3;
     CK(h, cudaEventRecord(e[0], st));
   }
-  for (Part &P : h->parts) { launch_signal(P.SG, st); h->n_launch += h->nj > 0; }
+  // MAX_PRESSURE lane counts (L39): k_signal reads those of state(t), k_step
+  // (and k_absorb) accumulate those of state(t+1), the buffer of t+2 is cleared
+  int32_t *cnt_next = h->any_maxp ? h->lcnt[(t + 1) % 3] : nullptr;
+  if (h->any_maxp) CK(h, cudaMemsetAsync(h->lcnt[(t + 2) % 3], 0, h->nl * 4, st));
+  for (Part &P : h->parts) {
+    SignalArgs sg = P.SG;
+    sg.lane_cnt = h->lcnt[t % 3];
+    launch_signal(sg, st);
+    h->n_launch += h->nj > 0;
+  }
   if (h->timing) CK(h, cudaEventRecord(e[1], st));
   for (Part &P : h->parts) {
     StepArgs a = step_args(P, t);
+    a.lane_cnt_next = cnt_next;
     launch_step(a, st, h->smem);
     h->n_launch += a.n_own > 0;
   }
@@ -1075,9 +1111,13 @@ sim_status step_once(sim_s *h) {
     }
     for (Part &P : h->parts) {
       StepArgs a = step_args(P, t);
+      a.lane_cnt_next = cnt_next;
       launch_absorb(a, P.in_buf, P.in_off_d, P.in_cap_d, W, st);
       h->n_launch++;
     }
+    // every rank counted its own lanes (loopback partitions share one buffer)
+    if (cnt_next && !h->loopback)
+      NK(h, g_nccl.AllReduce(cnt_next, cnt_next, h->nl, 2 /*ncclInt32*/, kNcclSum, h->comm, st));
     // 2. halo: the first-vehicle summaries of the lanes each peer reads
     for (Part &P : h->parts) {
       StepArgs a = step_args(P, t);
@@ -1630,6 +1670,8 @@ sim_status sim_load_state(sim_handle h, const sim_state *in) {
     if (!(S.s[k] >= 0 && S.s[k] <= h->L[l]) || !(S.v[k] >= 0))
       return fail(h, SIM_E_RANGE, "s/v out of range for vehicle " + std::to_string(k));
   }
+  for (int j = 0; j < h->nj; ++j)
+    if (in->junc_policy[j] > POL_MAXP) return fail(h, SIM_E_RANGE, "junction policy out of range");
   S.jpol.assign(in->junc_policy, in->junc_policy + h->nj);
   S.jphase.assign(in->junc_phase, in->junc_phase + h->nj);
   S.jel.assign(in->junc_elapsed, in->junc_elapsed + h->nj);

@@ -51,7 +51,7 @@ class sim_params(C.Structure):
                 ("exact_mode", C.c_int32), ("record_decisions", C.c_int32),
                 ("device", C.c_int32), ("stream", P), ("rank", C.c_int32),
                 ("world", C.c_int32), ("loopback", C.c_int32), ("nccl_id", P),
-                ("road_owner", P)]
+                ("road_owner", P), ("max_pressure_period", C.c_int32)]
 
 
 class sim_sizes(C.Structure):
@@ -163,7 +163,8 @@ def _marshal(graph, trips, profiles, params, device=0, stream=None, exact_mode=F
                     int(device), C.c_void_p(stream) if stream else None, int(rank),
                     int(world), int(bool(loopback)),
                     _ptr(nid) if nid is not None else None,
-                    _ptr(own) if own is not None else None)
+                    _ptr(own) if own is not None else None,
+                    int(params.get("max_pressure_period", 30)))
     return G, T, Pm, keep
 
 

@@ -20,7 +20,7 @@ import numpy as np
 
 TURN_STRAIGHT, TURN_LEFT, TURN_RIGHT = 0, 1, 2
 KIND_NORMAL, KIND_DYNAMIC, KIND_TIDAL = 0, 1, 2
-POLICY_NONE, POLICY_FIXED, POLICY_MANUAL = 0, 1, 2
+POLICY_NONE, POLICY_FIXED, POLICY_MANUAL, POLICY_MAXP = 0, 1, 2, 3
 
 # heading index: 0 = +x (E), 1 = +y (N), 2 = -x (W), 3 = -y (S)
 _DXY = [(1, 0), (0, 1), (-1, 0), (0, -1)]
@@ -41,7 +41,7 @@ def city_profiles():
 def default_params(seed=1):
     return dict(seed=int(seed), dt=1.0, politeness=0.1, b_hard=8.0, b_safe=4.0,
                 v_wait=0.1, queue_zone_m=100.0, yellow_steps=3,
-                lookahead_lanes=2)
+                lookahead_lanes=2, max_pressure_period=30)
 
 
 @dataclass
@@ -720,3 +720,31 @@ def tiled_city(tiles_x=1, tiles_y=1, G=50, n_per_tile=1_000_000, seed=5, **kw):
         raise NotImplementedError("non-square tilings: use city(G=...)")
     s.name = f"tiled{tiles_x}x{tiles_y}_G{G}"
     return s
+
+
+def pressure_junction(counts, road_len=200.0, vmax=13.9, period=30, spacing=10.0):
+    """One MAX_PRESSURE junction with three single-lane approaches A, B, C and
+    exits D, E, F; movements A->D and B->E form phase 0, C->F phase 1 (the
+    two-phase example of S:336).  `counts` = vehicles initially on
+    (A, B, C, D, E, F), at rest, spaced `spacing` m from the far end; each
+    vehicle's route ends on its movement's exit road (or on its own exit road).
+    Returns (scenario, junction lanes (A->D, B->E, C->F))."""
+    b = NetBuilder()
+    j = b.add_junction(policy=POLICY_MAXP)
+    rid = [b.add_road(1, road_len, vmax, dst=j) for _ in range(3)] + \
+          [b.add_road(1, road_len, vmax, src=j) for _ in range(3)]
+    lane = [b.road_lanes[r][0] for r in rid]
+    jls = [b.connect(j, lane[i], lane[i + 3], TURN_STRAIGHT, 20.0, vmax) for i in range(3)]
+    b.set_phases(j, [{jls[0], jls[1]}, {jls[2]}], [period, period])
+    routes, sl, ss = [], [], []
+    for i, c in enumerate(counts):
+        for k in range(int(c)):
+            routes.append([rid[i], rid[i + 3]] if i < 3 else [rid[i]])
+            sl.append(lane[i])
+            ss.append(road_len - 1.0 - spacing * k)
+    n = len(routes)
+    trips = _trip_arrays(routes, sl, ss, np.zeros(n), [road_len] * n, np.zeros(n),
+                         np.ones(n), np.zeros(n))
+    params = default_params(1)
+    params["max_pressure_period"] = int(period)
+    return Scenario("pressure_junction", b.graph(), trips, default_profiles(), params), jls

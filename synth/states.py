@@ -10,7 +10,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .networks import KIND_DYNAMIC, KIND_TIDAL, POLICY_FIXED, POLICY_MANUAL, POLICY_NONE
+from .networks import KIND_DYNAMIC, KIND_TIDAL, POLICY_FIXED, POLICY_MANUAL, POLICY_MAXP, POLICY_NONE
 
 
 def random_state(scen, seed=0, t=None, frac_driving=0.6, frac_pending=0.25,
@@ -123,6 +123,15 @@ def random_state(scen, seed=0, t=None, frac_driving=0.6, frac_pending=0.25,
                 jy[j] = int(rng.integers(1, Y + 1))
                 jel[j] = g_p
             jpe[j] = (p + 1) % K if jy[j] > 0 else p
+        elif jpol[j] == POLICY_MAXP:
+            per = int(scen.params.get("max_pressure_period", 30))
+            jel[j] = per - 1 if rng.random() < 0.6 else int(rng.integers(per))
+            if rng.random() < 0.2 and Y > 0:
+                jy[j] = int(rng.integers(1, Y + 1))
+                jel[j] = per
+                jpe[j] = int(rng.integers(K))
+            else:
+                jpe[j] = p
         elif jpol[j] == POLICY_MANUAL:
             jel[j] = int(rng.integers(100))
             if rng.random() < 0.3 and Y > 0:

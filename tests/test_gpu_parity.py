@@ -39,6 +39,8 @@ SCENARIOS = {
     "grid1": lambda: synth.grid(rows=2, cols=3, road_len=150.0, lanes=1, n_trips=600, seed=23),
     "ring3": lambda: synth.ring(n_vehicles=120, n_lanes=3, length=800.0, seed=24),
     "city": lambda: synth.city(G=8, n_vehicles=6000, seed=25),
+    "grid2_maxpressure": lambda: synth.grid(rows=3, cols=3, road_len=200.0, lanes=2, n_trips=1500,
+                                            seed=26, policy=synth.POLICY_MAXP),
 }
 
 
@@ -61,7 +63,7 @@ def test_one_step_parity_random_states(simlib, oracle_lib, name, exact):
         compare_lane_orders(gs["lane_offsets"], gs["lane_order"], o_off, o_ord, gs)
 
 
-@pytest.mark.parametrize("name", ["grid2", "grid3_tidal_dyn", "city"])
+@pytest.mark.parametrize("name", ["grid2", "grid3_tidal_dyn", "city", "grid2_maxpressure"])
 def test_exact_mode_full_run_bit_identical(simlib, oracle_lib, name):
     """P-EXACT: GPU exact_mode (fp64 math, fp32 store) == oracle store_fp32."""
     scen = SCENARIOS[name]()

@@ -32,11 +32,16 @@ MKEYS = ("n_pending", "n_driving", "n_finished", "vehicle_steps", "sum_travel_st
 
 
 @pytest.mark.parametrize("world", [2, 3, 5])
-@pytest.mark.parametrize("name", ["grid", "city"])
+@pytest.mark.parametrize("name", ["grid", "city", "grid_maxpressure"])
 def test_partition_invariance(simlib, name, world):
-    scen = (synth.grid(rows=4, cols=4, road_len=250.0, lanes=2, n_trips=3000, seed=12,
-                       depart_window=400) if name == "grid"
-            else synth.city(G=12, n_vehicles=20000, seed=13))
+    """grid_maxpressure: the MAX_PRESSURE choice needs every lane's count, so
+    the partitions' counts must add up exactly (shared buffer / allreduce)."""
+    if name == "city":
+        scen = synth.city(G=12, n_vehicles=20000, seed=13)
+    else:
+        scen = synth.grid(rows=4, cols=4, road_len=250.0, lanes=2, n_trips=3000, seed=12,
+                          depart_window=400,
+                          policy=synth.POLICY_MAXP if name == "grid_maxpressure" else synth.POLICY_FIXED)
     s1, m1 = _run(simlib, scen, 150)
     sw, mw = _run(simlib, scen, 150, world=world, loopback=True)
     for k in KEYS:
