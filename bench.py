@@ -97,19 +97,25 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def make_workload(world=1):
+def make_workload(world=1, policy="fixed"):
     """C4 at N=1; weak scaling for N > 1: the same city recipe grown to N times
     the area (G = 72 * sqrt(N)) with 2M vehicles per GPU, spatially partitioned
-    over the N GPUs with boundary migration."""
+    over the N GPUs with boundary migration.
+    policy "maxpressure": every signalised junction runs MAX_PRESSURE (NEXT-1)."""
     import synth
     G = int(round(72 * np.sqrt(world)))
-    return synth.city(G=G, n_vehicles=2_000_000 * world, seed=4)
+    scen = synth.city(G=G, n_vehicles=2_000_000 * world, seed=4)
+    if policy == "maxpressure":
+        jp = scen.graph["junc_policy"]
+        scen.graph["junc_policy"] = np.where(jp == synth.POLICY_FIXED, synth.POLICY_MAXP, jp).astype(np.uint8)
+    return scen
 
 
-def workload_config(scen, extra=None):
+def workload_config(scen, extra=None, policy="fixed"):
     G = int(np.sqrt(len(scen.graph["junc_lane_offsets"]) - 1))
+    sig = "fixed-time signals" if policy == "fixed" else "max-pressure signals (period 30 s)"
     cfg = {"workload": f"C4 city-like synthetic network (SURVEY 8(d)): G={G} perturbed grid, "
-                       f"{scen.n_trips / 1e6:.0f}M vehicles on the network at t=0, fixed-time signals",
+                       f"{scen.n_trips / 1e6:.0f}M vehicles on the network at t=0, {sig}",
            "n_vehicles": int(scen.n_trips), "n_lanes": int(scen.n_lanes),
            "n_junctions": int(len(scen.graph["junc_lane_offsets"]) - 1),
            "n_roads": int(len(scen.graph["road_lane_offsets"]) - 1),
@@ -141,7 +147,7 @@ def cpu_baseline(scen, budget_s=20.0, max_steps=10):
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    scen = make_workload(1)
+    scen = make_workload(1, args.policy)
     import oracle
     oracle.build()
     o = oracle.Oracle(scen)
@@ -162,7 +168,7 @@ def run_reference(args, rank, world):
             "n_gpus": args.gpus, "steps": done, "warmup": args.warmup,
             "ms_per_step": 1e3 * dt / max(done, 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(scen),
+            "config": workload_config(scen, policy=args.policy),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -179,7 +185,7 @@ def run_gpu(args, rank, world, local_rank):
         p.build()
     if world > 1:
         torch.distributed.barrier()
-    scen = make_workload(world)
+    scen = make_workload(world, args.policy)
     stream = torch.cuda.Stream(dev)          # the simulation stream (events recorded on it)
     torch.cuda.set_stream(stream)
     if world > 1:
@@ -249,10 +255,12 @@ def run_gpu(args, rank, world, local_rank):
     torch.cuda.synchronize()
     me0 = sim.read_metrics()
     t0 = time.perf_counter()
+    host_ctl = args.policy == "fixed"                     # max pressure runs on the device
     for k in range(e2e_steps):
-        tau = (me0["t"] + k + offs) % 102                 # host fixed-time controller
-        ph = np.where(tau < 33, 0, np.where(tau < 51, 1, np.where(tau < 84, 2, 3))).astype(np.int32)
-        sim.set_signal_phase_batch(jids, ph)              # H2D: the step's control input
+        if host_ctl:
+            tau = (me0["t"] + k + offs) % 102             # host fixed-time controller
+            ph = np.where(tau < 33, 0, np.where(tau < 51, 1, np.where(tau < 84, 2, 3))).astype(np.int32)
+            sim.set_signal_phase_batch(jids, ph)          # H2D: the step's control input
         sim.step(1)
         obs = sim.read_metrics(lane_stats=True)           # D2H: counters + lane queues
     e2e_dt = time.perf_counter() - t0
@@ -269,7 +277,7 @@ def run_gpu(args, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": workload_config(scen, {
+        "config": workload_config(scen, policy=args.policy, extra={
             "parallelism": "single GPU" if world == 1 else
             f"spatial partition over {world} GPUs (recursive coordinate bisection of road tiles), "
             "boundary-vehicle migration + lane-summary halo per step via NCCL p2p",
@@ -280,7 +288,7 @@ def run_gpu(args, rank, world, local_rank):
                      "signal_kernel_ms_avg": ksig_ms / args.steps,
                      "alg_bytes_per_launch": per_launch_bytes},
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * nj,
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * nj if host_ctl else 0,
                 "d2h_bytes_per_step": lane_bytes + 8 * 15, "steps": e2e_steps},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
@@ -295,6 +303,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--policy", default="fixed", choices=["fixed", "maxpressure"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
