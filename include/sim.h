@@ -118,6 +118,18 @@ typedef struct {
    * vehicles in state(t); ties -> lowest index) is chosen, with the yellow
    * steps in between when it changes.  <= 0: 30. */
   int32_t max_pressure_period;
+  /* Batched environments (RL workloads P:146):
+   * independent networks stepped by one call are passed as one graph with
+   * disconnected components.  vehicle_seed [n_trips] / vehicle_rng_id
+   * [n_trips] (optional, NULL = params.seed / vid) set the Philox key and
+   * counter of each vehicle's draw (ledger L16), so every environment draws
+   * exactly as its standalone run; road_group [n_roads] (optional, values in
+   * [0, n_groups)) labels roads, and the vehicles whose start lane is on them,
+   * for sim_read_group_metrics. */
+  const uint64_t *vehicle_seed;
+  const int32_t *vehicle_rng_id;
+  const int32_t *road_group;
+  int32_t n_groups;
 } sim_params;
 
 typedef struct {
@@ -200,6 +212,11 @@ sim_status sim_query_sizes(sim_handle h, sim_sizes *out);
 sim_status sim_read_state(sim_handle h, sim_state *out);
 sim_status sim_read_decisions(sim_handle h, sim_decisions *out);
 sim_status sim_read_metrics(sim_handle h, sim_metrics *out);
+/* Per-group metrics (params.road_group): out[n_groups], counters of the tiles
+ * (roads) of each group and status counts of its vehicles; the lane buffers
+ * of out[] are ignored.  SIM_E_INVALID without road_group or on a different
+ * n_groups. */
+sim_status sim_read_group_metrics(sim_handle h, int32_t n_groups, sim_metrics *out);
 /* Replace the whole state (checkpoint / parity hook).  Pending queues are
  * rebuilt from status; all fields except lane_signal/lane_offsets/lane_order
  * are required. */

@@ -144,6 +144,8 @@ struct StepArgs {
   const Prof *prof;
   long long *tacc;                  // [n_tiles][kNAcc]
   int32_t *lane_cnt_next;           // [n_lanes] vehicles per lane at t+1 (MAX_PRESSURE; NULL if unused)
+  const uint64_t *veh_seed;         // [n_veh] Philox key per vehicle (batched environments) or NULL
+  const int32_t *rng_id;            // [n_veh] Philox counter id per vehicle or NULL (= vid)
   // decision recording (vid-indexed), optional
   int32_t *r_leader, *r_of, *r_side;
   int8_t *r_hops, *r_phantom, *r_lc, *r_hand, *r_fin, *r_ins;
@@ -181,6 +183,9 @@ void launch_reduce_acc(const long long *tacc, int n_tiles, const int32_t *cnt,
 void launch_lane_stats(const StepArgs &a, int32_t *lane_count, int32_t *lane_wait,
                        float queue_zone, void *stream);
 void launch_fill_u64(unsigned long long *p, unsigned long long v, int64_t n, void *stream);
+void launch_reduce_groups(const long long *tacc, const int32_t *tiles, int n_own,
+                          const int32_t *tile_group, const int32_t *cnt, const int32_t *icnt,
+                          int n_groups, long long *out, void *stream);
 void launch_mig_header(MigRec *out_buf, const int32_t *out_off, const int32_t *out_cap,
                        int32_t *out_cnt, int world, void *stream);
 void launch_absorb(const StepArgs &a, const MigRec *in_buf, const int32_t *in_off,

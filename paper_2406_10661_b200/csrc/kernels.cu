@@ -707,6 +707,24 @@ __global__ void k_reduce_acc(const long long *tacc, int n_tiles, const int32_t *
     atomicAdd(reinterpret_cast<unsigned long long *>(&out[threadIdx.x]), sh[threadIdx.x]);
 }
 
+// Per-group metrics (batched environments): the counters and driving counts
+// of the own tiles, per group.  out [n_groups][kNAcc + 1] (zeroed by the caller).
+__global__ void k_reduce_groups(const long long *tacc, const int32_t *tiles, int n_own,
+                                const int32_t *tile_group, const int32_t *cnt,
+                                const int32_t *icnt, long long *out) {
+  const int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_own; i += stride) {
+    const int t = tiles[i];
+    long long *o = out + (size_t)tile_group[t] * (kNAcc + 1);
+    for (int c = 0; c < kNAcc; ++c) {
+      const long long x = tacc[(size_t)t * kNAcc + c];
+      if (x) atomicAdd(reinterpret_cast<unsigned long long *>(o + c), (unsigned long long)x);
+    }
+    const int d = cnt[t] + icnt[t];
+    if (d) atomicAdd(reinterpret_cast<unsigned long long *>(o + kNAcc), (unsigned long long)d);
+  }
+}
+
 __global__ void k_lane_stats(StepArgs A, int32_t *cnt, int32_t *wt, float zone) {
   // lane queue length: per lane, vehicles and those with v < v_wait
   // within the last `zone` metres, over stayers + inbox of each own
@@ -845,6 +863,14 @@ void launch_lane_stats(const StepArgs &a, int32_t *lane_count, int32_t *lane_wai
                        void *stream) {
   if (a.n_own > 0)
     k_lane_stats<<<a.n_own, 128, 0, (cudaStream_t)stream>>>(a, lane_count, lane_wait, zone);
+}
+
+void launch_reduce_groups(const long long *tacc, const int32_t *tiles, int n_own,
+                          const int32_t *tile_group, const int32_t *cnt, const int32_t *icnt,
+                          int n_groups, long long *out, void *stream) {
+  cudaMemsetAsync(out, 0, (size_t)n_groups * (kNAcc + 1) * sizeof(long long), (cudaStream_t)stream);
+  if (n_own > 0)
+    k_reduce_groups<<<296, 256, 0, (cudaStream_t)stream>>>(tacc, tiles, n_own, tile_group, cnt, icnt, out);
 }
 
 void launch_fill_u64(unsigned long long *p, unsigned long long v, int64_t n, void *stream) {

@@ -598,8 +598,10 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
       }
       {
         // U53 of Philox4x32-10(seed; vid, t) (ledger L16)
-        uint32_t c0 = (uint32_t)me.vid, c1 = (uint32_t)A.t, c2 = 0u, c3 = 0u;
-        uint32_t k0 = (uint32_t)(A.seed & 0xffffffffull), k1 = (uint32_t)(A.seed >> 32);
+        const uint64_t sd = A.veh_seed ? A.veh_seed[me.vid] : A.seed;
+        uint32_t c0 = A.rng_id ? (uint32_t)A.rng_id[me.vid] : (uint32_t)me.vid;
+        uint32_t c1 = (uint32_t)A.t, c2 = 0u, c3 = 0u;
+        uint32_t k0 = (uint32_t)(sd & 0xffffffffull), k1 = (uint32_t)(sd >> 32);
 #pragma unroll
         for (int rr = 0; rr < 10; ++rr) {
           uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;

@@ -101,6 +101,8 @@ struct Part {
   int32_t *desc_d = nullptr;
   long long *red_d = nullptr;
   int32_t *lanestat_d = nullptr;
+  int32_t *tile_group_d = nullptr;              // batched environments: group of each tile
+  long long *grp_d = nullptr;                   // [n_groups][kNAcc + 1]
   std::vector<int> tiles;                       // own tiles
   // exchange plan (world > 1): migrant regions per peer (header record + cap)
   std::vector<int> out_off, out_cap, in_off, in_cap;
@@ -158,6 +160,11 @@ struct sim_s {
   std::vector<int32_t> desc, desc_off;   // tile descriptors (dev.h)
   int64_t fin0 = 0;                  // FINISHED vehicles in the last loaded state
   long long acc_fin0 = 0;            // finished counter at the last load
+  // batched environments (NEXT-3)
+  std::vector<uint64_t> vseed;
+  std::vector<int32_t> rngid, road_group, veh_group;
+  int n_groups = 0;
+  std::vector<long long> grp_nv, grp_fin0, grp_acc_fin0;
   // device
   std::vector<void *> allocs;
   int64_t bytes = 0;
@@ -487,6 +494,31 @@ sim_status validate_and_copy(sim_s *h, const sim_graph *g, const sim_trips *tr,
   }
   h->P = *p;
   h->Y = p->yellow_steps;
+  // batched environments (NEXT-3): per-vehicle Philox key / counter id, road groups
+  if (p->vehicle_seed) h->vseed.assign(p->vehicle_seed, p->vehicle_seed + nv);
+  if (p->vehicle_rng_id) {
+    h->rngid.assign(p->vehicle_rng_id, p->vehicle_rng_id + nv);
+    for (int k = 0; k < nv; ++k)
+      if (h->rngid[k] < 0) return fail(h, SIM_E_INVALID, "vehicle_rng_id must be >= 0");
+  }
+  h->n_groups = 0;
+  if (p->road_group) {
+    if (p->n_groups < 1) return fail(h, SIM_E_INVALID, "n_groups must be >= 1 with road_group");
+    h->n_groups = p->n_groups;
+    h->road_group.assign(p->road_group, p->road_group + h->nr);
+    for (int r = 0; r < h->nr; ++r)
+      if (h->road_group[r] < 0 || h->road_group[r] >= p->n_groups)
+        return fail(h, SIM_E_INVALID, "road_group out of [0, n_groups)");
+    h->veh_group.assign(nv, 0);
+    h->grp_nv.assign(h->n_groups, 0);
+    for (int k = 0; k < nv; ++k) {
+      h->veh_group[k] = h->road_group[h->road[h->start_lane[k]]];
+      h->grp_nv[h->veh_group[k]] += 1;
+    }
+  }
+  h->P.vehicle_seed = nullptr;                       // not retained (ABI: inputs are copied)
+  h->P.vehicle_rng_id = nullptr;
+  h->P.road_group = nullptr;
   h->profs.resize(p->n_profiles);
   float acap = 0;
   for (int i = 0; i < p->n_profiles; ++i) {
@@ -829,10 +861,16 @@ sim_status upload_state(sim_s *h, const HostState &S) {
   CK(h, cudaStreamSynchronize(h->stream));   // host vectors die at return
   // counters keep accumulating across loads: remember the finished baseline
   h->acc_fin0 = 0;
+  h->grp_fin0.assign(h->n_groups, 0);
+  h->grp_acc_fin0.assign(h->n_groups, 0);
+  for (int k = 0; k < nv && h->n_groups; ++k) h->grp_fin0[h->veh_group[k]] += S.status[k] == ST_FINISHED;
   for (Part &P : h->parts) {
     std::vector<long long> ta((size_t)nt * kNAcc);
     CK(h, cudaMemcpy(ta.data(), P.A.tacc, ta.size() * 8, cudaMemcpyDeviceToHost));
-    for (int T = 0; T < nt; ++T) h->acc_fin0 += ta[(size_t)T * kNAcc + ACC_FINISHED];
+    for (int T : P.tiles) {
+      h->acc_fin0 += ta[(size_t)T * kNAcc + ACC_FINISHED];
+      if (h->n_groups) h->grp_acc_fin0[h->road_group[T]] += ta[(size_t)T * kNAcc + ACC_FINISHED];
+    }
   }
   return SIM_OK;
 }
@@ -907,6 +945,14 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   AL(P.pend_off_d, nl + 1); AL(P.pend_vid_d, nv); AL(P.pend_head_d, nl);
   A.pend_off = P.pend_off_d; A.pend_vid = P.pend_vid_d; A.pend_head = P.pend_head_d;
   Prof *pr; UP(pr, h->profs); A.prof = pr;
+  A.veh_seed = nullptr;
+  A.rng_id = nullptr;
+  if (!h->vseed.empty()) { uint64_t *u64; UP(u64, h->vseed); A.veh_seed = u64; }
+  if (!h->rngid.empty()) { UP(i32, h->rngid); A.rng_id = i32; }
+  if (h->n_groups) {
+    UP(P.tile_group_d, h->road_group);               // tile = road
+    AL(P.grp_d, (size_t)h->n_groups * (kNAcc + 1));
+  }
   AL(A.tacc, (size_t)nt * kNAcc);
   CK(h, cudaMemset(A.tacc, 0, (size_t)nt * kNAcc * 8));
   AL(P.red_d, kNAcc + 3);
@@ -1606,6 +1652,51 @@ sim_status sim_read_metrics(sim_handle h, sim_metrics *m) {
   m->att_finished = c[ACC_FINISHED] ? (double)c[ACC_SUM_TRAVEL] / (double)c[ACC_FINISHED] : 0.0;
   if (m->lane_count) std::memcpy(m->lane_count, hl, h->nl * 4);
   if (m->lane_waiting_at_end) std::memcpy(m->lane_waiting_at_end, hl + h->nl, h->nl * 4);
+  return SIM_OK;
+}
+
+sim_status sim_read_group_metrics(sim_handle h, int32_t n_groups, sim_metrics *out) {
+  sim_status st = check(h);
+  if (st) return st;
+  if (!out) return fail(h, SIM_E_INVALID, "out is NULL");
+  if (!h->n_groups || n_groups != h->n_groups)
+    return fail(h, SIM_E_INVALID, "the handle has no road_group or a different n_groups");
+  const size_t w = (size_t)h->n_groups * (kNAcc + 1);
+  std::vector<long long> c(w, 0), tmp(w);
+  for (Part &P : h->parts) {
+    StepArgs a = step_args(P, h->t);
+    launch_reduce_groups(P.A.tacc, P.A.tiles, P.A.n_own, P.tile_group_d, a.cnt_in, a.icnt_in,
+                         h->n_groups, P.grp_d, h->stream);
+    h->n_launch += 1;
+  }
+  if (h->comm) {
+    Part &P = h->parts[0];
+    NK(h, g_nccl.AllReduce(P.grp_d, P.grp_d, w, kNcclInt64, kNcclSum, h->comm, h->stream));
+  }
+  for (size_t q = 0; q < h->parts.size(); ++q) {
+    CK(h, cudaMemcpyAsync(tmp.data(), h->parts[q].grp_d, w * 8, cudaMemcpyDeviceToHost, h->stream));
+    st = device_check(h);
+    if (st) return st;
+    for (size_t i = 0; i < w; ++i) c[i] += tmp[i];
+    if (h->comm) break;                               // allreduced: one copy holds the total
+  }
+  for (int g = 0; g < h->n_groups; ++g) {
+    const long long *x = c.data() + (size_t)g * (kNAcc + 1);
+    sim_metrics &m = out[g];
+    m.t = h->t;
+    m.n_driving = x[kNAcc];
+    m.n_finished = h->grp_fin0[g] + (x[ACC_FINISHED] - h->grp_acc_fin0[g]);
+    m.n_pending = h->grp_nv[g] - m.n_driving - m.n_finished;
+    m.vehicle_steps = x[ACC_VEH_STEPS];
+    m.sum_travel_steps = x[ACC_SUM_TRAVEL];
+    m.sum_wait_steps_finished = x[ACC_SUM_WAIT_FIN];
+    m.sum_depart_delay = x[ACC_SUM_DELAY];
+    m.n_lane_changes = x[ACC_LANE_CHANGES];
+    m.n_handoffs = x[ACC_HANDOFFS];
+    m.n_inserted = x[ACC_INSERTED];
+    m.n_guard_hits = x[ACC_GUARD];
+    m.att_finished = x[ACC_FINISHED] ? (double)x[ACC_SUM_TRAVEL] / (double)x[ACC_FINISHED] : 0.0;
+  }
   return SIM_OK;
 }
 

@@ -51,7 +51,9 @@ class sim_params(C.Structure):
                 ("exact_mode", C.c_int32), ("record_decisions", C.c_int32),
                 ("device", C.c_int32), ("stream", P), ("rank", C.c_int32),
                 ("world", C.c_int32), ("loopback", C.c_int32), ("nccl_id", P),
-                ("road_owner", P), ("max_pressure_period", C.c_int32)]
+                ("road_owner", P), ("max_pressure_period", C.c_int32),
+                ("vehicle_seed", P), ("vehicle_rng_id", P), ("road_group", P),
+                ("n_groups", C.c_int32)]
 
 
 class sim_sizes(C.Structure):
@@ -83,7 +85,7 @@ class sim_metrics(C.Structure):
 ABI_FUNCTIONS = ["sim_create", "sim_get_nccl_unique_id", "sim_partition", "sim_step", "sim_sync", "sim_set_signal_phase",
                  "sim_set_signal_phase_batch", "sim_set_lane_direction",
                  "sim_set_lane_direction_batch", "sim_query_sizes", "sim_read_state",
-                 "sim_read_decisions", "sim_read_metrics", "sim_load_state",
+                 "sim_read_decisions", "sim_read_metrics", "sim_read_group_metrics", "sim_load_state",
                  "sim_enable_timing", "sim_read_timing", "sim_destroy", "sim_last_error"]
 
 _lib = None
@@ -106,7 +108,8 @@ def load_library(path=LIB):
         "sim_set_signal_phase": [h, i32, i32], "sim_set_signal_phase_batch": [h, i32, P, P],
         "sim_set_lane_direction": [h, i32, i32], "sim_set_lane_direction_batch": [h, i32, P, P],
         "sim_query_sizes": [h, P], "sim_read_state": [h, P], "sim_read_decisions": [h, P],
-        "sim_read_metrics": [h, P], "sim_load_state": [h, P], "sim_destroy": [h],
+        "sim_read_metrics": [h, P], "sim_read_group_metrics": [h, i32, P],
+        "sim_load_state": [h, P], "sim_destroy": [h],
         "sim_enable_timing": [h, i32], "sim_read_timing": [h, P, P, P],
     }
     for name, args in sig.items():
@@ -164,8 +167,26 @@ def _marshal(graph, trips, profiles, params, device=0, stream=None, exact_mode=F
                     int(world), int(bool(loopback)),
                     _ptr(nid) if nid is not None else None,
                     _ptr(own) if own is not None else None,
-                    int(params.get("max_pressure_period", 30)))
+                    int(params.get("max_pressure_period", 30)),
+                    *_batch_arrays(params, keep))
     return G, T, Pm, keep
+
+
+def _batch_arrays(params, keep):
+    """Optional batched-environment inputs (sim_params.vehicle_seed,
+    vehicle_rng_id, road_group, n_groups)."""
+    out = []
+    for name, dt in (("vehicle_seed", np.uint64), ("vehicle_rng_id", np.int32),
+                     ("road_group", np.int32)):
+        a = params.get(name)
+        if a is None:
+            out.append(None)
+        else:
+            a = np.ascontiguousarray(a, dt)
+            keep.append(a)
+            out.append(_ptr(a))
+    out.append(int(params.get("n_groups", 0)))
+    return out
 
 
 def get_nccl_unique_id():
@@ -305,6 +326,12 @@ class Sim:
         if bufs is not None:
             out["lane_count"], out["lane_waiting_at_end"] = bufs
         return out
+
+    def read_group_metrics(self, n_groups):
+        """Per-group metrics (batched environments, sim_read_group_metrics)."""
+        arr = (sim_metrics * int(n_groups))()
+        self._chk(self.lib.sim_read_group_metrics(self.h, int(n_groups), arr))
+        return [{n: getattr(m, n) for n, _ in sim_metrics._fields_[:-2]} for m in arr]
 
     def enable_timing(self, on=True):
         self._chk(self.lib.sim_enable_timing(self.h, int(on)))

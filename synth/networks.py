@@ -748,3 +748,63 @@ def pressure_junction(counts, road_len=200.0, vmax=13.9, period=30, spacing=10.0
     params = default_params(1)
     params["max_pressure_period"] = int(period)
     return Scenario("pressure_junction", b.graph(), trips, default_profiles(), params), jls
+
+
+def batch(scens):
+    """NEXT-3 batched environments: the disjoint union of independent
+    scenarios as one input (ids offset per environment), plus the per-vehicle
+    Philox seed / counter id and per-road group that make each environment
+    behave exactly like its standalone run (sim_params.vehicle_seed,
+    vehicle_rng_id, road_group).  Input construction only (no model logic).
+    The profile table and model parameters of scens[0] apply to all."""
+    g0 = scens[0].graph
+    out_g = {k: [] for k in g0}
+    trips = {k: [] for k in scens[0].trips}
+    lo = ro = jo = po = 0
+    vseed, rid, rgroup = [], [], []
+    for e, sc in enumerate(scens):
+        g, tr = sc.graph, sc.trips
+        nl, nr = len(g["lane_length"]), len(g["road_lane_offsets"]) - 1
+        nj = len(g["junc_lane_offsets"]) - 1
+        sh = lambda a, o: np.where(np.asarray(a) >= 0, np.asarray(a) + o, np.asarray(a))
+        for k in ("lane_length", "lane_max_speed", "lane_turn", "lane_kind", "lane_dir0",
+                  "phase_green", "phase_green_steps", "junc_policy", "junc_offset_steps"):
+            out_g[k].append(np.asarray(g[k]))
+        out_g["lane_road"].append(sh(g["lane_road"], ro))
+        out_g["lane_junction"].append(sh(g["lane_junction"], jo))
+        out_g["lane_left"].append(sh(g["lane_left"], lo))
+        out_g["lane_right"].append(sh(g["lane_right"], lo))
+        out_g["tidal_partner"].append(sh(g["tidal_partner"], lo))
+        out_g["succ_lanes"].append(np.asarray(g["succ_lanes"]) + lo)
+        out_g["road_lanes"].append(np.asarray(g["road_lanes"]) + lo)
+        out_g["junc_lanes"].append(np.asarray(g["junc_lanes"]) + lo)
+        for k, base in (("succ_offsets", sum(len(x) for x in out_g["succ_lanes"][:-1])),
+                        ("road_lane_offsets", sum(len(x) for x in out_g["road_lanes"][:-1])),
+                        ("junc_lane_offsets", sum(len(x) for x in out_g["junc_lanes"][:-1])),
+                        ("junc_phase_offsets", po)):
+            a = np.asarray(g[k])
+            out_g[k].append((a if e == 0 else a[1:]) + base)
+        n = len(tr["depart_step"])
+        for k in trips:
+            if k != "route_offsets":
+                trips[k].append(np.asarray(tr[k]))
+        trips["route_roads"][-1] = trips["route_roads"][-1] + ro
+        trips["start_lane"][-1] = trips["start_lane"][-1] + lo
+        ro_base = sum(len(x) for x in trips["route_roads"][:-1])
+        a = np.asarray(tr["route_offsets"])
+        trips["route_offsets"].append((a if e == 0 else a[1:]) + ro_base)
+        vseed += [int(sc.params["seed"])] * n
+        rid += list(range(n))
+        rgroup += [e] * nr
+        lo += nl; ro += nr; jo += nj; po += int(np.asarray(g["junc_phase_offsets"])[-1])
+    G = {k: np.concatenate(v).astype(np.asarray(g0[k]).dtype) for k, v in out_g.items()}
+    T = {k: np.concatenate(v).astype(np.asarray(scens[0].trips[k]).dtype) for k, v in trips.items()}
+    params = dict(scens[0].params)
+    params["vehicle_seed"] = np.asarray(vseed, np.uint64)
+    params["vehicle_rng_id"] = np.asarray(rid, np.int32)
+    params["road_group"] = np.asarray(rgroup, np.int32)
+    params["n_groups"] = len(scens)
+    return Scenario(f"batch{len(scens)}", G, T, scens[0].profiles, params,
+                    meta=dict(env_lanes=[len(s.graph["lane_length"]) for s in scens],
+                              env_trips=[s.n_trips for s in scens],
+                              env_junctions=[len(s.graph["junc_lane_offsets"]) - 1 for s in scens]))
