@@ -176,6 +176,8 @@ typedef struct {
   double att_finished;               /* sum_travel_steps / n_finished */
   int32_t *lane_count;               /* optional caller buffer [n_lanes] or NULL */
   int32_t *lane_waiting_at_end;      /* optional [n_lanes]: v < v_wait within queue_zone_m */
+  float *road_avg_speed;             /* optional [n_roads]: mean speed of the vehicles on the road's
+                                        lanes, the road's max lane speed if none */
 } sim_metrics;
 
 /* Create a simulation.  Validates the graph and trips
@@ -207,6 +209,26 @@ sim_status sim_set_signal_phase_batch(sim_handle h, int32_t m, const int32_t *ju
 sim_status sim_set_lane_direction(sim_handle h, int32_t lane, int32_t dir);
 sim_status sim_set_lane_direction_batch(sim_handle h, int32_t m, const int32_t *lanes,
                                         const int32_t *dirs);
+/* Signal policy (set_tl_policy): 0 NONE 1 FIXED_TIME 2 MANUAL
+ * 3 MAX_PRESSURE, applied at the next step before its signals and before
+ * phase requests; FIXED_TIME / MAX_PRESSURE restart the current phase's green
+ * timer, a running yellow completes.  SIM_E_RANGE for a bad
+ * id or policy; a junction without phases stays NONE. */
+sim_status sim_set_signal_policy(sim_handle h, int32_t junction, int32_t policy);
+sim_status sim_set_signal_policy_batch(sim_handle h, int32_t m, const int32_t *junctions,
+                                       const int32_t *policies);
+/* Lane max speed (set_lane_max_speed): m/s > 0, from the next step
+ * (v0 = min(lane, vehicle), L6).  The lane-start margin keeps its create-time
+ * value (L17). */
+sim_status sim_set_lane_max_speed(sim_handle h, int32_t lane, float max_speed);
+sim_status sim_set_lane_max_speed_batch(sim_handle h, int32_t m, const int32_t *lanes,
+                                        const float *max_speeds);
+/* Lane restriction (set_lane_restriction): flag 1 = no entry; the lane
+ * is not usable (no lane change into it, no junction lane leads into it,
+ * DESIGN §1.3); vehicles already on it continue.  flag 0 lifts it. */
+sim_status sim_set_lane_restriction(sim_handle h, int32_t lane, int32_t flag);
+sim_status sim_set_lane_restriction_batch(sim_handle h, int32_t m, const int32_t *lanes,
+                                          const int32_t *flags);
 sim_status sim_query_sizes(sim_handle h, sim_sizes *out);
 /* Synchronising reads into caller-owned host buffers. */
 sim_status sim_read_state(sim_handle h, sim_state *out);

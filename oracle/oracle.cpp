@@ -48,6 +48,7 @@ struct Vehicle {
 struct Junction {
   int policy = POL_NONE, phase = 0, elapsed = 0, yellow = 0, pending = 0;
   int request = -1;
+  int pol_request = -1;                   // set_tl_policy, applied at the next step (L42)
   std::vector<int> lanes;                 // junction lanes (slot order)
   std::vector<std::vector<uint8_t>> green; // [phase][slot]
   std::vector<int> green_steps;
@@ -80,6 +81,7 @@ struct Sim {
   double p_polite = 0.1, b_hard = 8, b_safe = 4, v_wait = 0.1, queue_zone = 100;
   int Y = 3, K = 2;
   int mp_period = 30;                      // MAX_PRESSURE decision period (L41)
+  std::vector<uint8_t> restricted;         // set_lane_restriction flags (L44)
   bool store_fp32 = false, reverse_order = false;
   double start_margin = 0;
   // state
@@ -103,6 +105,7 @@ struct Sim {
 
   // §1.3 usable(ℓ) (ledger L29, L30)
   bool usable(int l) const {
+    if (restricted[l]) return false;                        // set_lane_restriction (L44)
     if (is_road(l)) return !(kind[l] == KIND_TIDAL && dir[l] != 0);
     int a = pred[l][0], b = succ[l][0];
     if (!usable(b)) return false;
@@ -223,6 +226,17 @@ struct Sim {
 
   // ---- signals (a5) ----
   void apply_requests() {
+    // set_tl_policy (L42): the new policy from this step on; a
+    // FIXED_TIME / MAX_PRESSURE junction restarts the current phase's green
+    // timer (a running yellow completes); then phase requests (MANUAL)
+    for (auto &j : J) {
+      if (j.pol_request < 0) continue;
+      const int np = j.pol_request;
+      j.pol_request = -1;
+      if (j.green.empty() || np == j.policy) continue;
+      j.policy = np;
+      if (np == POL_FIXED || np == POL_MAXP) j.elapsed = 0;
+    }
     for (auto &j : J) {
       if (j.request < 0) continue;
       int r = j.request;
@@ -628,6 +642,7 @@ void *or_create(const or_graph *g, const or_trips *tr, const or_params *pp,
   S->L.resize(nl); S->vmax.resize(nl); S->road.resize(nl); S->junc.resize(nl);
   S->left.resize(nl); S->right.resize(nl); S->turn.resize(nl); S->kind.resize(nl);
   S->partner.resize(nl); S->succ.assign(nl, {}); S->pred.assign(nl, {});
+  S->restricted.assign(nl, 0);
   S->dir.resize(nl); S->sig.assign(nl, SIG_GREEN); S->lane_pos.assign(nl, 0);
   S->lane_junc_slot.assign(nl, -1);
   for (int l = 0; l < nl; ++l) {
@@ -820,6 +835,50 @@ int32_t or_set_signal_phase(void *h, int32_t j, int32_t phase) {
   if (phase < 0 || phase >= (int)S->J[j].green.size()) return 2;
   S->J[j].request = phase;
   return 0;
+}
+
+int32_t or_set_signal_policy(void *h, int32_t j, int32_t policy) {
+  Sim *S = (Sim *)h;
+  if (j < 0 || j >= S->nj || policy < POL_NONE || policy > POL_MAXP) return 2;
+  S->J[j].pol_request = policy;
+  return 0;
+}
+
+int32_t or_set_lane_max_speed(void *h, int32_t l, float v) {
+  // set_lane_max_speed: v0 = min(lane, vehicle) from the next step (L6)
+  Sim *S = (Sim *)h;
+  if (l < 0 || l >= S->nl) return 2;
+  if (!(v > 0.0f) || !std::isfinite(v)) return 1;
+  S->vmax[l] = (double)v;
+  return 0;
+}
+
+int32_t or_set_lane_restriction(void *h, int32_t l, int32_t flag) {
+  // set_lane_restriction (L44): a restricted lane is not usable
+  Sim *S = (Sim *)h;
+  if (l < 0 || l >= S->nl || flag < 0 || flag > 1) return 2;
+  S->restricted[l] = (uint8_t)flag;
+  return 0;
+}
+
+void or_road_avg_speed(void *h, double *out) {
+  // road travelling speed: mean speed of the vehicles on the
+  // road's lanes; no vehicle -> free-flow speed = max lane speed of the road (L45)
+  Sim *S = (Sim *)h;
+  const int nr = (int)S->road_lanes.size();
+  std::vector<double> sum(nr, 0.0);
+  std::vector<long> cnt(nr, 0);
+  for (auto &v : S->V) {
+    if (v.status != DRIVING || !S->is_road(v.lane)) continue;
+    sum[S->road[v.lane]] += v.v;
+    cnt[S->road[v.lane]] += 1;
+  }
+  for (int r = 0; r < nr; ++r) {
+    if (cnt[r]) { out[r] = sum[r] / (double)cnt[r]; continue; }
+    double vm = 0.0;
+    for (int l : S->road_lanes[r]) vm = std::max(vm, S->vmax[l]);
+    out[r] = vm;
+  }
 }
 
 int32_t or_set_lane_direction(void *h, int32_t l, int32_t d) {

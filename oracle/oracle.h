@@ -105,6 +105,11 @@ void or_read_metrics(void *h, or_metrics *out);
 void or_lane_stats(void *h, int32_t *lane_count, int32_t *lane_waiting);
 int32_t or_set_signal_phase(void *h, int32_t junction, int32_t phase);
 int32_t or_set_lane_direction(void *h, int32_t lane, int32_t dir);
+int32_t or_set_signal_policy(void *h, int32_t junction, int32_t policy);
+int32_t or_set_lane_max_speed(void *h, int32_t lane, float v);
+int32_t or_set_lane_restriction(void *h, int32_t lane, int32_t flag);
+/* [n_roads] mean speed of the vehicles on each road (free-flow if empty) */
+void or_road_avg_speed(void *h, double *out);
 /* Philox4x32-10 block function, exposed for the known-answer test (P-RNG) */
 void or_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 double or_u53(uint64_t seed, int32_t vid, int32_t t);

@@ -53,6 +53,10 @@ def _load():
         _lib.or_lane_stats.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         _lib.or_set_signal_phase.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
         _lib.or_set_lane_direction.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
+        _lib.or_set_signal_policy.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
+        _lib.or_set_lane_max_speed.argtypes = [C.c_void_p, C.c_int32, C.c_float]
+        _lib.or_set_lane_restriction.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
+        _lib.or_road_avg_speed.argtypes = [C.c_void_p, C.c_void_p]
         _lib.or_philox4x32_10.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         _lib.or_u53.restype = C.c_double
         _lib.or_u53.argtypes = [C.c_uint64, C.c_int32, C.c_int32]
@@ -138,6 +142,7 @@ class Oracle:
         tr = {k: np.ascontiguousarray(scen.trips[k], dtype=dt) for k, dt in _TRIP_DT.items()}
         self._keep += [g, tr]
         self.n_lanes = int(g["lane_length"].shape[0])
+        self.n_roads = int(g["road_lane_offsets"].shape[0] - 1)
         self.n_junctions = int(g["junc_lane_offsets"].shape[0] - 1)
         self.n = int(tr["depart_step"].shape[0])
         G = _Graph(self.n_lanes, int(g["road_lane_offsets"].shape[0] - 1), self.n_junctions,
@@ -225,6 +230,20 @@ class Oracle:
 
     def set_lane_direction(self, lane, d):
         return self.lib.or_set_lane_direction(self.h, int(lane), int(d))
+
+    def set_signal_policy(self, j, policy):
+        return self.lib.or_set_signal_policy(self.h, int(j), int(policy))
+
+    def set_lane_max_speed(self, lane, v):
+        return self.lib.or_set_lane_max_speed(self.h, int(lane), float(v))
+
+    def set_lane_restriction(self, lane, flag):
+        return self.lib.or_set_lane_restriction(self.h, int(lane), int(flag))
+
+    def road_avg_speed(self):
+        out = np.zeros(self.n_roads, np.float64)
+        self.lib.or_road_avg_speed(self.h, _ptr(out))
+        return out
 
 
 def philox4x32_10(ctr, key):

@@ -157,6 +157,7 @@ struct SignalArgs {
   int32_t n_junctions, yellow;
   uint8_t *policy;
   int32_t *phase, *elapsed, *yellow_left, *pending, *request;
+  int32_t *pol_request;             // set_tl_policy requests (-1 none), applied before `request`
   const int32_t *jl_off, *jl;       // junction -> lanes (slots)
   const int32_t *ph_off;            // junction -> phases
   const int64_t *green_off;         // junction -> first byte of its phase rows
@@ -181,7 +182,7 @@ void launch_reduce_acc(const long long *tacc, int n_tiles, const int32_t *cnt,
                        const int32_t *icnt, const uint8_t *status, int nv, long long *out,
                        void *stream);
 void launch_lane_stats(const StepArgs &a, int32_t *lane_count, int32_t *lane_wait,
-                       float queue_zone, void *stream);
+                       float *road_speed, float queue_zone, void *stream);
 void launch_fill_u64(unsigned long long *p, unsigned long long v, int64_t n, void *stream);
 void launch_reduce_groups(const long long *tacc, const int32_t *tiles, int n_own,
                           const int32_t *tile_group, const int32_t *cnt, const int32_t *icnt,

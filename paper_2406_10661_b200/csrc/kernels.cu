@@ -605,6 +605,11 @@ __global__ void k_signal(SignalArgs a) {
   const int j0 = a.jl_off[j], nj = a.jl_off[j + 1] - j0;
   int pol = a.policy[j], ph = a.phase[j];
   int el = a.elapsed[j], q = a.pending[j], y = a.yellow_left[j];
+  const int preq = a.pol_request[j];
+  if (preq >= 0 && K > 0 && preq != pol) {         // set_tl_policy first (L42)
+    pol = preq;
+    if (pol == POL_FIXED || pol == POL_MAXP) el = 0;
+  }
   const int req = a.request[j];
   if (req >= 0) {                                   // requests apply before sig_t (L35)
     pol = POL_MANUAL;
@@ -652,6 +657,7 @@ __global__ void k_signal(SignalArgs a) {
   }
   if (lane == 0) {
     if (req >= 0) a.request[j] = -1;
+    if (preq >= 0) a.pol_request[j] = -1;
     a.policy[j] = (uint8_t)pol;
     a.phase[j] = nph;
     a.elapsed[j] = nel;
@@ -725,15 +731,17 @@ __global__ void k_reduce_groups(const long long *tacc, const int32_t *tiles, int
   }
 }
 
-__global__ void k_lane_stats(StepArgs A, int32_t *cnt, int32_t *wt, float zone) {
+__global__ void k_lane_stats(StepArgs A, int32_t *cnt, int32_t *wt, float *road_speed, float zone) {
   // lane queue length: per lane, vehicles and those with v < v_wait
   // within the last `zone` metres, over stayers + inbox of each own
-  // tile; a lane belongs to one tile, so its totals are written, not added
+  // tile; a lane belongs to one tile, so its totals are written, not added.
+  // Road travelling speed: the tile's road lanes are its road.
   __shared__ int sc[kMaxTileLanes], sw[kMaxTileLanes];
+  __shared__ double sv[kMaxTileLanes];
   const int tile = A.tiles[blockIdx.x];
   const int ns = A.cnt_in[tile], ni = A.icnt_in[tile];
   const int l0 = A.tile_lane_off[tile], nl = A.tile_lane_off[tile + 1] - l0;
-  if (threadIdx.x < kMaxTileLanes) sc[threadIdx.x] = sw[threadIdx.x] = 0;
+  if (threadIdx.x < kMaxTileLanes) { sc[threadIdx.x] = sw[threadIdx.x] = 0; sv[threadIdx.x] = 0.0; }
   __syncthreads();
   for (int i = threadIdx.x; i < ns + ni; i += blockDim.x) {
     float s, v;
@@ -747,6 +755,7 @@ __global__ void k_lane_stats(StepArgs A, int32_t *cnt, int32_t *wt, float zone) 
     }
     const int l = m_lane(meta);
     atomicAdd(&sc[l], 1);
+    if (road_speed) atomicAdd(&sv[l], (double)v);
     if (v < A.v_wait && (A.lane_len[A.tile_lanes[l0 + l]] - s) <= zone) atomicAdd(&sw[l], 1);
   }
   __syncthreads();
@@ -754,6 +763,18 @@ __global__ void k_lane_stats(StepArgs A, int32_t *cnt, int32_t *wt, float zone) 
     const int g = A.tile_lanes[l0 + l];
     cnt[g] = sc[l];
     wt[g] = sw[l];
+  }
+  if (road_speed && threadIdx.x == 0) {            // lanes [0, nroad) are the road's
+    const int nroad = A.tile_nroad[tile];
+    double sum = 0.0;
+    int c = 0;
+    float vfree = 0.f;
+    for (int l = 0; l < nroad; ++l) {
+      sum += sv[l];
+      c += sc[l];
+      vfree = fmaxf(vfree, A.lane_vmax[A.tile_lanes[l0 + l]]);
+    }
+    road_speed[tile] = c ? (float)(sum / c) : vfree;
   }
 }
 
@@ -859,10 +880,10 @@ void launch_reduce_acc(const long long *tacc, int n_tiles, const int32_t *cnt,
   k_reduce_acc<<<296, 256, 0, (cudaStream_t)stream>>>(tacc, n_tiles, cnt, icnt, status, nv, out);
 }
 
-void launch_lane_stats(const StepArgs &a, int32_t *lane_count, int32_t *lane_wait, float zone,
-                       void *stream) {
+void launch_lane_stats(const StepArgs &a, int32_t *lane_count, int32_t *lane_wait,
+                       float *road_speed, float zone, void *stream) {
   if (a.n_own > 0)
-    k_lane_stats<<<a.n_own, 128, 0, (cudaStream_t)stream>>>(a, lane_count, lane_wait, zone);
+    k_lane_stats<<<a.n_own, 128, 0, (cudaStream_t)stream>>>(a, lane_count, lane_wait, road_speed, zone);
 }
 
 void launch_reduce_groups(const long long *tacc, const int32_t *tiles, int n_own,

@@ -102,6 +102,7 @@ struct Part {
   long long *red_d = nullptr;
   int32_t *lanestat_d = nullptr;
   int32_t *tile_group_d = nullptr;              // batched environments: group of each tile
+  float *lane_vmax_d = nullptr;                 // writable alias of A.lane_vmax (set_lane_max_speed)
   long long *grp_d = nullptr;                   // [n_groups][kNAcc + 1]
   std::vector<int> tiles;                       // own tiles
   // exchange plan (world > 1): migrant regions per peer (header record + cap)
@@ -174,6 +175,7 @@ struct sim_s {
   void *pinned = nullptr;
   size_t pinned_cap = 0;
   std::vector<int> req_mark;                    // set_signal_phase_batch: last entry per junction
+  std::vector<uint8_t> restricted;              // set_lane_restriction flags (L44)
   int32_t *lcnt[3] = {nullptr, nullptr, nullptr}; // MAX_PRESSURE lane counts for t, t+1, t+2 (mod 3)
   bool any_maxp = false;                        // some junction runs MAX_PRESSURE
   std::vector<int> jl_pred, jl_succ;            // per junction-lane slot: predecessor / successor lane
@@ -305,8 +307,9 @@ void build_desc(sim_s *h) {
 // usable(ℓ) (ledger L29, L30)
 void compute_usable(sim_s *h) {
   h->usable.assign(h->nl, 1);
+  if (h->restricted.size() != (size_t)h->nl) h->restricted.assign(h->nl, 0);
   for (int l = 0; l < h->nl; ++l)
-    if (is_road(h, l)) h->usable[l] = !(h->kind[l] == KIND_TIDAL && h->dir[l] != 0);
+    if (is_road(h, l)) h->usable[l] = !h->restricted[l] && !(h->kind[l] == KIND_TIDAL && h->dir[l] != 0);
   for (int l = 0; l < h->nl; ++l) {
     if (is_road(h, l)) continue;
     int a = h->pred[l], b = h->succ[h->succ_off[l]];
@@ -315,7 +318,7 @@ void compute_usable(sim_s *h) {
       if (h->turn[l] == 1) u = h->dir[a] == 1;
       else if (h->turn[l] == 0) u = h->dir[a] == 0;
     }
-    h->usable[l] = u;
+    h->usable[l] = u && !h->restricted[l];
   }
   // outroads: distinct roads reachable through usable successors (<= 4, else -2 marker)
   h->outroads.assign(4 * (size_t)h->nl, -1);
@@ -855,6 +858,7 @@ sim_status upload_state(sim_s *h, const HostState &S) {
       CK(h, cudaMemcpyAsync(P.SG.yellow_left, S.jy.data(), h->nj * 4, cudaMemcpyHostToDevice, st));
       CK(h, cudaMemcpyAsync(P.SG.pending, S.jpend.data(), h->nj * 4, cudaMemcpyHostToDevice, st));
       CK(h, cudaMemcpyAsync(P.SG.request, req.data(), h->nj * 4, cudaMemcpyHostToDevice, st));
+      CK(h, cudaMemcpyAsync(P.SG.pol_request, req.data(), h->nj * 4, cudaMemcpyHostToDevice, st));
     }
     if (P.out_cnt) CK(h, cudaMemsetAsync(P.out_cnt, 0, h->world * 4, st));
   }
@@ -883,7 +887,7 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   const int nl = h->nl, nv = h->nv, nt = h->nt;
   float *f; int32_t *i32;
   UP(f, h->L); A.lane_len = f;
-  UP(f, h->vmax); A.lane_vmax = f;
+  UP(f, h->vmax); A.lane_vmax = f; P.lane_vmax_d = f;
   UP(i32, h->road); A.lane_road = i32;
   UP(i32, h->left); A.lane_left = i32;
   UP(i32, h->right); A.lane_right = i32;
@@ -956,7 +960,7 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   AL(A.tacc, (size_t)nt * kNAcc);
   CK(h, cudaMemset(A.tacc, 0, (size_t)nt * kNAcc * 8));
   AL(P.red_d, kNAcc + 3);
-  AL(P.lanestat_d, 2 * (size_t)nl);
+  AL(P.lanestat_d, 2 * (size_t)nl + h->nr);           // lane counts, waiting, road speeds
   if (h->P.record_decisions) {
     AL(A.r_leader, nv); AL(A.r_of, nv); AL(A.r_side, 4 * (size_t)nv);
     AL(A.r_hops, nv); AL(A.r_phantom, nv); AL(A.r_lc, nv); AL(A.r_hand, nv);
@@ -1002,7 +1006,7 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   SignalArgs &G = P.SG;
   G.n_junctions = h->nj; G.yellow = h->Y;
   AL(G.policy, h->nj); AL(G.phase, h->nj); AL(G.elapsed, h->nj); AL(G.yellow_left, h->nj);
-  AL(G.pending, h->nj); AL(G.request, h->nj);
+  AL(G.pending, h->nj); AL(G.request, h->nj); AL(G.pol_request, h->nj);
   UP(i32, h->jl_off); G.jl_off = i32;
   UP(i32, h->jl); G.jl = i32;
   UP(i32, h->ph_off); G.ph_off = i32;
@@ -1196,6 +1200,49 @@ sim_status step_once(sim_s *h) {
     }
   }
   h->t += 1;
+  return SIM_OK;
+}
+
+// After a change of lane directions / restrictions / speeds: recompute the
+// usable flags, reachable roads and tile descriptors and stream them.
+sim_status push_lane_tables(sim_s *h) {
+  sim_status st;
+  compute_usable(h);
+  // one staging buffer: the outroads table followed by the usable bytes
+  std::vector<uint8_t> buf((size_t)h->nl + h->outroads.size() * 4);
+  std::memcpy(buf.data(), h->outroads.data(), h->outroads.size() * 4);
+  std::memcpy(buf.data() + h->outroads.size() * 4, h->usable.data(), h->nl);
+  st = push_staging(h, buf.data(), buf.size(), h->stage_dir_d);
+  if (st) return st;
+  for (Part &P : h->parts) {
+    CK(h, cudaMemcpyAsync(P.outroads_d, h->stage_dir_d, h->outroads.size() * 4,
+                          cudaMemcpyDeviceToDevice, h->stream));
+    CK(h, cudaMemcpyAsync(P.usable_d, h->stage_dir_d + h->outroads.size() * 4, h->nl,
+                          cudaMemcpyDeviceToDevice, h->stream));
+  }
+  // tile descriptors carry usable flags and reachable roads: stream them too
+  st = push_staging(h, h->desc.data(), h->desc.size() * 4, h->parts[0].desc_d);
+  if (st) return st;
+  for (size_t i = 1; i < h->parts.size(); ++i)
+    CK(h, cudaMemcpyAsync(h->parts[i].desc_d, h->parts[0].desc_d, h->desc.size() * 4,
+                          cudaMemcpyDeviceToDevice, h->stream));
+  return SIM_OK;
+}
+
+// MAX_PRESSURE switched on by a setter: the lane counts of state(t) are
+// rebuilt from the slabs + inboxes (k_lane_stats) and the other buffers cleared.
+sim_status rebuild_counts(sim_s *h) {
+  const int t = h->t;
+  CK(h, cudaMemsetAsync(h->lcnt[t % 3], 0, h->nl * 4, h->stream));
+  CK(h, cudaMemsetAsync(h->lcnt[(t + 1) % 3], 0, h->nl * 4, h->stream));
+  CK(h, cudaMemsetAsync(h->lcnt[(t + 2) % 3], 0, h->nl * 4, h->stream));
+  int32_t *wscratch = h->parts[0].lanestat_d + h->nl;
+  for (Part &P : h->parts) {
+    StepArgs a = step_args(P, t);
+    launch_lane_stats(a, h->lcnt[t % 3], wscratch, nullptr, h->P.queue_zone_m, h->stream);
+    h->n_launch += 1;
+  }
+  if (h->comm) NK(h, g_nccl.AllReduce(h->lcnt[t % 3], h->lcnt[t % 3], h->nl, 2 /*ncclInt32*/, kNcclSum, h->comm, h->stream));
   return SIM_OK;
 }
 
@@ -1410,30 +1457,100 @@ sim_status sim_set_lane_direction_batch(sim_handle h, int32_t m, const int32_t *
     if (h->kind[l] == KIND_TIDAL && h->partner[l] >= 0) h->dir[h->partner[l]] = (uint8_t)(1 - dirs[i]);
   }
   if (m == 0) return SIM_OK;
-  compute_usable(h);
-  // one staging buffer: the outroads table followed by the usable bytes
-  std::vector<uint8_t> buf((size_t)h->nl + h->outroads.size() * 4);
-  std::memcpy(buf.data(), h->outroads.data(), h->outroads.size() * 4);
-  std::memcpy(buf.data() + h->outroads.size() * 4, h->usable.data(), h->nl);
-  st = push_staging(h, buf.data(), buf.size(), h->stage_dir_d);
-  if (st) return st;
-  for (Part &P : h->parts) {
-    CK(h, cudaMemcpyAsync(P.outroads_d, h->stage_dir_d, h->outroads.size() * 4,
-                          cudaMemcpyDeviceToDevice, h->stream));
-    CK(h, cudaMemcpyAsync(P.usable_d, h->stage_dir_d + h->outroads.size() * 4, h->nl,
-                          cudaMemcpyDeviceToDevice, h->stream));
-  }
-  // tile descriptors carry usable flags and reachable roads: stream them too
-  st = push_staging(h, h->desc.data(), h->desc.size() * 4, h->parts[0].desc_d);
-  if (st) return st;
-  for (size_t i = 1; i < h->parts.size(); ++i)
-    CK(h, cudaMemcpyAsync(h->parts[i].desc_d, h->parts[0].desc_d, h->desc.size() * 4,
-                          cudaMemcpyDeviceToDevice, h->stream));
-  return SIM_OK;
+  return push_lane_tables(h);
 }
 
 sim_status sim_set_lane_direction(sim_handle h, int32_t lane, int32_t dir) {
   return sim_set_lane_direction_batch(h, 1, &lane, &dir);
+}
+
+sim_status sim_set_signal_policy_batch(sim_handle h, int32_t m, const int32_t *junctions,
+                                       const int32_t *policies) {
+  sim_status st = check(h);
+  if (st) return st;
+  if (m < 0 || (m > 0 && (!junctions || !policies))) return fail(h, SIM_E_INVALID, "bad batch");
+  for (int i = 0; i < m; ++i) {
+    if (junctions[i] < 0 || junctions[i] >= h->nj) return fail(h, SIM_E_RANGE, "junction out of range");
+    if (policies[i] < POL_NONE || policies[i] > POL_MAXP) return fail(h, SIM_E_RANGE, "policy out of range");
+  }
+  if (m == 0) return SIM_OK;
+  bool maxp = false;
+  for (int i = 0; i < m; ++i) maxp |= policies[i] == POL_MAXP;
+  if (maxp && !h->any_maxp) {                        // counts of state(t) needed from the next step
+    h->any_maxp = true;
+    st = rebuild_counts(h);
+    if (st) return st;
+  }
+  h->req_mark.resize(h->nj, -1);
+  std::vector<int32_t> buf(2 * (size_t)m);
+  int u = 0;
+  for (int i = m - 1; i >= 0; --i) {                 // the last entry per junction wins
+    const int j = junctions[i];
+    if (h->req_mark[j] == h->req_epoch) continue;
+    h->req_mark[j] = h->req_epoch;
+    buf[u] = j;
+    buf[m + u] = policies[i];
+    ++u;
+  }
+  if (++h->req_epoch == 0x7fffffff) { h->req_epoch = 0; std::fill(h->req_mark.begin(), h->req_mark.end(), -1); }
+  std::memmove(buf.data() + u, buf.data() + m, u * 4);
+  if (h->stage_cap < 2 * u) {
+    if (h->stage_d) { CK(h, cudaStreamSynchronize(h->stream)); cudaFree(h->stage_d); }
+    CK(h, cudaMalloc(&h->stage_d, 2 * (size_t)u * 4));
+    h->stage_cap = 2 * u;
+  }
+  st = push_staging(h, buf.data(), 2 * (size_t)u * 4, h->stage_d);
+  if (st) return st;
+  for (Part &P : h->parts) {
+    launch_apply_requests(P.SG.pol_request, P.SG.policy, h->stage_d, h->stage_d + u, u, h->stream);
+    h->n_launch++;
+  }
+  return SIM_OK;
+}
+
+sim_status sim_set_signal_policy(sim_handle h, int32_t j, int32_t policy) {
+  return sim_set_signal_policy_batch(h, 1, &j, &policy);
+}
+
+sim_status sim_set_lane_max_speed_batch(sim_handle h, int32_t m, const int32_t *lanes,
+                                        const float *speeds) {
+  sim_status st = check(h);
+  if (st) return st;
+  if (m < 0 || (m > 0 && (!lanes || !speeds))) return fail(h, SIM_E_INVALID, "bad batch");
+  for (int i = 0; i < m; ++i) {
+    if (lanes[i] < 0 || lanes[i] >= h->nl) return fail(h, SIM_E_RANGE, "lane out of range");
+    if (!(speeds[i] > 0.0f) || !std::isfinite(speeds[i])) return fail(h, SIM_E_RANGE, "max speed must be > 0");
+  }
+  if (m == 0) return SIM_OK;
+  for (int i = 0; i < m; ++i) h->vmax[lanes[i]] = speeds[i];
+  st = push_staging(h, h->vmax.data(), h->vmax.size() * 4, h->parts[0].lane_vmax_d);
+  if (st) return st;
+  for (size_t i = 1; i < h->parts.size(); ++i)
+    CK(h, cudaMemcpyAsync(h->parts[i].lane_vmax_d, h->parts[0].lane_vmax_d, h->vmax.size() * 4,
+                          cudaMemcpyDeviceToDevice, h->stream));
+  return push_lane_tables(h);                        // descriptors carry the lane speeds
+}
+
+sim_status sim_set_lane_max_speed(sim_handle h, int32_t lane, float v) {
+  return sim_set_lane_max_speed_batch(h, 1, &lane, &v);
+}
+
+sim_status sim_set_lane_restriction_batch(sim_handle h, int32_t m, const int32_t *lanes,
+                                          const int32_t *flags) {
+  sim_status st = check(h);
+  if (st) return st;
+  if (m < 0 || (m > 0 && (!lanes || !flags))) return fail(h, SIM_E_INVALID, "bad batch");
+  for (int i = 0; i < m; ++i)
+    if (lanes[i] < 0 || lanes[i] >= h->nl || flags[i] < 0 || flags[i] > 1)
+      return fail(h, SIM_E_RANGE, "lane or flag out of range");
+  if (m == 0) return SIM_OK;
+  if (h->restricted.size() != (size_t)h->nl) h->restricted.assign(h->nl, 0);
+  for (int i = 0; i < m; ++i) h->restricted[lanes[i]] = (uint8_t)flags[i];
+  return push_lane_tables(h);
+}
+
+sim_status sim_set_lane_restriction(sim_handle h, int32_t lane, int32_t flag) {
+  return sim_set_lane_restriction_batch(h, 1, &lane, &flag);
 }
 
 sim_status sim_query_sizes(sim_handle h, sim_sizes *out) {
@@ -1590,9 +1707,9 @@ sim_status sim_read_metrics(sim_handle h, sim_metrics *m) {
   if (!m) return fail(h, SIM_E_INVALID, "out is NULL");
   // everything is enqueued first and read back through one pinned buffer, so
   // a read costs one synchronisation of the stream
-  const bool lanes = m->lane_count || m->lane_waiting_at_end;
+  const bool lanes = m->lane_count || m->lane_waiting_at_end || m->road_avg_speed;
   const size_t ncnt = (size_t)(kNAcc + 3) * h->parts.size();
-  const size_t bytes = ncnt * 8 + (lanes ? 2 * (size_t)h->nl * 4 : 0);
+  const size_t bytes = ncnt * 8 + (lanes ? (2 * (size_t)h->nl + h->nr) * 4 : 0);
   if (h->rd_cap < bytes) {
     CK(h, cudaStreamSynchronize(h->stream));
     if (h->rd_pinned) cudaFreeHost(h->rd_pinned);
@@ -1619,14 +1736,18 @@ sim_status sim_read_metrics(sim_handle h, sim_metrics *m) {
     int32_t *d = P0.lanestat_d;
     // every lane belongs to one tile: the loopback partitions together write all
     // of them; ranks of a real partition only their own, so zero first
-    if (h->comm) CK(h, cudaMemsetAsync(d, 0, 2 * (size_t)h->nl * 4, h->stream));
+    float *rs = m->road_avg_speed ? reinterpret_cast<float *>(d + 2 * (size_t)h->nl) : nullptr;
+    if (h->comm) CK(h, cudaMemsetAsync(d, 0, (2 * (size_t)h->nl + h->nr) * 4, h->stream));
     for (Part &P : h->parts) {
       StepArgs a = step_args(P, h->t);
-      launch_lane_stats(a, d, d + h->nl, h->P.queue_zone_m, h->stream);
+      launch_lane_stats(a, d, d + h->nl, rs, h->P.queue_zone_m, h->stream);
       h->n_launch += 1;
     }
-    if (h->comm) NK(h, g_nccl.AllReduce(d, d, 2 * (size_t)h->nl, 2 /*ncclInt32*/, kNcclSum, h->comm, h->stream));
-    CK(h, cudaMemcpyAsync(hl, d, 2 * (size_t)h->nl * 4, cudaMemcpyDeviceToHost, h->stream));
+    if (h->comm) {
+      NK(h, g_nccl.AllReduce(d, d, 2 * (size_t)h->nl, 2 /*ncclInt32*/, kNcclSum, h->comm, h->stream));
+      if (rs) NK(h, g_nccl.AllReduce(rs, rs, h->nr, 7 /*ncclFloat32*/, kNcclSum, h->comm, h->stream));
+    }
+    CK(h, cudaMemcpyAsync(hl, d, (2 * (size_t)h->nl + h->nr) * 4, cudaMemcpyDeviceToHost, h->stream));
   }
   st = device_check(h);
   if (st) return st;
@@ -1652,6 +1773,7 @@ sim_status sim_read_metrics(sim_handle h, sim_metrics *m) {
   m->att_finished = c[ACC_FINISHED] ? (double)c[ACC_SUM_TRAVEL] / (double)c[ACC_FINISHED] : 0.0;
   if (m->lane_count) std::memcpy(m->lane_count, hl, h->nl * 4);
   if (m->lane_waiting_at_end) std::memcpy(m->lane_waiting_at_end, hl + h->nl, h->nl * 4);
+  if (m->road_avg_speed) std::memcpy(m->road_avg_speed, hl + 2 * (size_t)h->nl, h->nr * 4);
   return SIM_OK;
 }
 

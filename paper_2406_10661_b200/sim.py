@@ -79,13 +79,13 @@ class sim_metrics(C.Structure):
         "n_pending", "n_driving", "n_finished", "vehicle_steps", "sum_travel_steps",
         "sum_wait_steps_finished", "sum_depart_delay", "n_lane_changes", "n_handoffs",
         "n_inserted", "n_guard_hits")] + [("att_finished", C.c_double), ("lane_count", P),
-                                          ("lane_waiting_at_end", P)]
+                                          ("lane_waiting_at_end", P), ("road_avg_speed", P)]
 
 
 ABI_FUNCTIONS = ["sim_create", "sim_get_nccl_unique_id", "sim_partition", "sim_step", "sim_sync", "sim_set_signal_phase",
                  "sim_set_signal_phase_batch", "sim_set_lane_direction",
                  "sim_set_lane_direction_batch", "sim_query_sizes", "sim_read_state",
-                 "sim_read_decisions", "sim_read_metrics", "sim_read_group_metrics", "sim_load_state",
+                 "sim_read_decisions", "sim_read_metrics", "sim_read_group_metrics", "sim_set_signal_policy", "sim_set_signal_policy_batch", "sim_set_lane_max_speed", "sim_set_lane_max_speed_batch", "sim_set_lane_restriction", "sim_set_lane_restriction_batch", "sim_load_state",
                  "sim_enable_timing", "sim_read_timing", "sim_destroy", "sim_last_error"]
 
 _lib = None
@@ -109,6 +109,9 @@ def load_library(path=LIB):
         "sim_set_lane_direction": [h, i32, i32], "sim_set_lane_direction_batch": [h, i32, P, P],
         "sim_query_sizes": [h, P], "sim_read_state": [h, P], "sim_read_decisions": [h, P],
         "sim_read_metrics": [h, P], "sim_read_group_metrics": [h, i32, P],
+        "sim_set_signal_policy": [h, i32, i32], "sim_set_signal_policy_batch": [h, i32, P, P],
+        "sim_set_lane_max_speed": [h, i32, C.c_float], "sim_set_lane_max_speed_batch": [h, i32, P, P],
+        "sim_set_lane_restriction": [h, i32, i32], "sim_set_lane_restriction_batch": [h, i32, P, P],
         "sim_load_state": [h, P], "sim_destroy": [h],
         "sim_enable_timing": [h, i32], "sim_read_timing": [h, P, P, P],
     }
@@ -227,6 +230,7 @@ class Sim:
         G, T, Pm, keep = _marshal(graph, trips, profiles, params, device, stream, exact_mode,
                                   record_decisions, world, rank, loopback, nccl_id, road_owner)
         self.n_lanes, self.n_junctions, self.n = G.n_lanes, G.n_junctions, T.n_trips
+        self.n_roads = G.n_roads
         self.world, self.rank = max(1, int(world)), int(rank)
         hh = C.c_void_p()
         st = lib.sim_create(C.byref(G), C.byref(T), C.byref(Pm), C.byref(hh))
@@ -314,24 +318,54 @@ class Sim:
         b["side_vid"] = b["side_vid"].reshape(n, 4)
         return b
 
-    def read_metrics(self, lane_stats=False):
+    def read_metrics(self, lane_stats=False, road_speed=False):
         m = sim_metrics()
         bufs = None
         if lane_stats:
             bufs = (np.zeros(self.n_lanes, np.int32), np.zeros(self.n_lanes, np.int32))
             m.lane_count = _ptr(bufs[0])
             m.lane_waiting_at_end = _ptr(bufs[1])
+        rs = None
+        if road_speed:
+            rs = np.zeros(self.n_roads, np.float32)
+            m.road_avg_speed = _ptr(rs)
         self._chk(self.lib.sim_read_metrics(self.h, C.byref(m)))
-        out = {n: getattr(m, n) for n, _ in sim_metrics._fields_[:-2]}
+        out = {n: getattr(m, n) for n, _ in sim_metrics._fields_[:-3]}
         if bufs is not None:
             out["lane_count"], out["lane_waiting_at_end"] = bufs
+        if rs is not None:
+            out["road_avg_speed"] = rs
         return out
+
+    def set_signal_policy(self, junction, policy):
+        self._chk(self.lib.sim_set_signal_policy(self.h, int(junction), int(policy)))
+
+    def set_signal_policy_batch(self, junctions, policies):
+        j = np.ascontiguousarray(junctions, np.int32)
+        p = np.ascontiguousarray(policies, np.int32)
+        self._chk(self.lib.sim_set_signal_policy_batch(self.h, len(j), _ptr(j), _ptr(p)))
+
+    def set_lane_max_speed(self, lane, v):
+        self._chk(self.lib.sim_set_lane_max_speed(self.h, int(lane), float(v)))
+
+    def set_lane_max_speed_batch(self, lanes, speeds):
+        l = np.ascontiguousarray(lanes, np.int32)
+        v = np.ascontiguousarray(speeds, np.float32)
+        self._chk(self.lib.sim_set_lane_max_speed_batch(self.h, len(l), _ptr(l), _ptr(v)))
+
+    def set_lane_restriction(self, lane, flag):
+        self._chk(self.lib.sim_set_lane_restriction(self.h, int(lane), int(flag)))
+
+    def set_lane_restriction_batch(self, lanes, flags):
+        l = np.ascontiguousarray(lanes, np.int32)
+        f = np.ascontiguousarray(flags, np.int32)
+        self._chk(self.lib.sim_set_lane_restriction_batch(self.h, len(l), _ptr(l), _ptr(f)))
 
     def read_group_metrics(self, n_groups):
         """Per-group metrics (batched environments, sim_read_group_metrics)."""
         arr = (sim_metrics * int(n_groups))()
         self._chk(self.lib.sim_read_group_metrics(self.h, int(n_groups), arr))
-        return [{n: getattr(m, n) for n, _ in sim_metrics._fields_[:-2]} for m in arr]
+        return [{n: getattr(m, n) for n, _ in sim_metrics._fields_[:-3]} for m in arr]
 
     def enable_timing(self, on=True):
         self._chk(self.lib.sim_enable_timing(self.h, int(on)))

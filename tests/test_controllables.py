@@ -1,0 +1,186 @@
+"""Remaining controllable objects and metrics (Table 1
+P:1074-1082, §3.2): set_tl_policy, set_lane_max_speed,
+set_lane_restriction, road travelling speed.  Readings L42-L45.
+
+Oracle pins (CPU):
+  * NONE policy -> every junction lane GREEN;
+  * a lane speed change moves the free-road equilibrium speed to the new
+    v0 = min(lane, vehicle) (IDM closed form: a = 0 iff v = v0);
+  * restricting the only exit lane makes approaching vehicles queue at the
+    road end; lifting it releases them;
+  * switching FIXED_TIME -> MAX_PRESSURE restarts the green timer (L42);
+  * road average speed = brute-force mean of the vehicle speeds on the road's
+    lanes, the road's max lane speed when it is empty (L45).
+GPU: the same setter sequences bit-identical to the oracle in exact mode, and
+road speeds within the fp tolerance.
+"""
+import numpy as np
+import pytest
+
+import synth
+
+SIG_GREEN = 0
+POL_NONE, POL_FIXED, POL_MANUAL, POL_MAXP = 0, 1, 2, 3
+
+
+def test_none_policy_all_green(oracle_lib):
+    sc = synth.grid(rows=2, cols=2, road_len=200.0, lanes=2, n_trips=100, seed=5)
+    o = oracle_lib.Oracle(sc)
+    for j in range(o.n_junctions):
+        assert o.set_signal_policy(j, POL_NONE) == 0
+    o.step(1)
+    st = o.read_state()
+    jl = sc.graph["junc_lanes"]
+    assert np.all(st["lane_signal"][jl] == SIG_GREEN)
+    assert np.all(st["junc_policy"] == POL_NONE)
+
+
+def _one_lane(length=2000.0, vmax=13.9, n=1):
+    b = synth.NetBuilder()
+    r = b.add_road(1, length, vmax)
+    lane = b.road_lanes[r][0]
+    trips = dict(depart_step=np.zeros(n, np.int32), on_network_at_t0=np.ones(n, np.uint8),
+                 route_offsets=np.arange(n + 1, dtype=np.int32), route_roads=np.full(n, r, np.int32),
+                 start_lane=np.full(n, lane, np.int32),
+                 start_s=np.array([10.0 + 20 * k for k in range(n)], np.float32),
+                 start_v=np.zeros(n, np.float32), end_s=np.full(n, length, np.float32),
+                 profile=np.zeros(n, np.uint8))
+    return synth.Scenario("lane", b.graph(), trips, synth.default_profiles(),
+                          synth.default_params(1)), lane
+
+
+def test_lane_max_speed_sets_free_flow(oracle_lib):
+    sc, lane = _one_lane()
+    o = oracle_lib.Oracle(sc)
+    o.step(60)
+    assert abs(o.read_state()["v"][0] - 13.9) < 1e-3          # v0 = min(13.9, 16.667)
+    assert o.set_lane_max_speed(lane, 8.0) == 0
+    o.step(1)
+    a = o.decisions()["accel"][0]
+    x = o.read_state()["v"][0]
+    assert a < -1.0                                            # IDM free term 2(1-(13.9/8)^4) < 0
+    o.step(80)
+    assert abs(o.read_state()["v"][0] - 8.0) < 1e-3
+    assert o.set_lane_max_speed(lane, 0.0) != 0                # rejected
+
+
+def test_restriction_queues_and_releases(oracle_lib):
+    sc, jls = synth.pressure_junction([4, 0, 0, 0, 0, 0], period=30)
+    g = sc.graph
+    o = oracle_lib.Oracle(sc)
+    for j in range(o.n_junctions):
+        o.set_signal_policy(j, POL_NONE)                       # no signal: only the restriction stops them
+    exit_lane = int(g["succ_lanes"][g["succ_offsets"][jls[0]]])
+    o.set_lane_restriction(exit_lane, 1)
+    o.step(120)
+    st = o.read_state()
+    a_lane = int(g["road_lanes"][0])
+    assert np.all(st["lane"] == a_lane) and np.all(st["status"] == 1)
+    assert np.all(st["s"] <= g["lane_length"][a_lane] + 1e-9)
+    assert np.all(st["v"] < 0.1)                               # queued at the road end
+    o.set_lane_restriction(exit_lane, 0)
+    o.step(120)
+    assert np.all(o.read_state()["status"] == 2)               # released, all arrived
+
+
+def test_policy_switch_restarts_timer(oracle_lib):
+    sc = synth.grid(rows=2, cols=2, road_len=200.0, lanes=2, n_trips=200, seed=6)
+    o = oracle_lib.Oracle(sc)
+    o.step(17)
+    o.set_signal_policy(0, POL_MAXP)
+    o.step(1)
+    st = o.read_state()
+    assert st["junc_policy"][0] == POL_MAXP
+    # timer restarted at the switch, then advanced once by this step
+    assert st["junc_elapsed"][0] == 1 or st["junc_yellow_left"][0] > 0
+
+
+def test_road_avg_speed_brute_force(oracle_lib):
+    sc = synth.grid(rows=3, cols=3, road_len=200.0, lanes=2, n_trips=900, seed=7)
+    g = sc.graph
+    o = oracle_lib.Oracle(sc)
+    o.step(200)
+    st = o.read_state()
+    got = o.road_avg_speed()
+    nr = len(g["road_lane_offsets"]) - 1
+    for r in range(nr):
+        lanes = g["road_lanes"][g["road_lane_offsets"][r]:g["road_lane_offsets"][r + 1]]
+        on = (st["status"] == 1) & np.isin(st["lane"], lanes)
+        exp = st["v"][on].mean() if on.any() else g["lane_max_speed"][lanes].max()
+        assert abs(got[r] - exp) <= 1e-12 * max(1.0, abs(exp)), r
+
+
+def _setter_script(sc, rng, n_rounds):
+    """Random sequence of (kind, args) setter calls between 25-step chunks."""
+    g = sc.graph
+    nj = len(g["junc_lane_offsets"]) - 1
+    road_lanes = np.where(g["lane_road"] >= 0)[0]
+    out = []
+    for _ in range(n_rounds):
+        calls = []
+        for j in rng.choice(nj, 2, replace=False):
+            calls.append(("policy", int(j), int(rng.choice([POL_NONE, POL_FIXED, POL_MANUAL, POL_MAXP]))))
+        for l in rng.choice(road_lanes, 3, replace=False):
+            calls.append(("speed", int(l), float(rng.choice([6.0, 10.0, 16.667]))))
+        for l in rng.choice(len(g["lane_length"]), 2, replace=False):
+            calls.append(("restrict", int(l), int(rng.integers(2))))
+        out.append(calls)
+    return out
+
+
+def _apply(sim, calls):
+    for kind, a, b in calls:
+        if kind == "policy":
+            sim.set_signal_policy(a, b)
+        elif kind == "speed":
+            sim.set_lane_max_speed(a, b)
+        else:
+            sim.set_lane_restriction(a, b)
+
+
+@pytest.mark.gpu
+def test_setters_exact_mode_bit_identical(oracle_lib):
+    import paper_2406_10661_b200 as p
+    p.build()
+    sc = synth.grid(rows=3, cols=3, road_len=200.0, lanes=2, n_trips=1500, seed=81)
+    g = p.Sim.from_scenario(sc, exact_mode=True)
+    o = oracle_lib.Oracle(sc, store_fp32=True)
+    for rnd, calls in enumerate(_setter_script(sc, np.random.default_rng(3), 8)):
+        _apply(g, calls)
+        _apply(o, calls)
+        g.step(25)
+        o.step(25)
+        gs, os_ = g.read_state(), o.read_state()
+        for k in ("status", "lane", "cursor", "wait_steps", "junc_policy", "junc_phase",
+                  "junc_elapsed", "junc_yellow_left", "lane_signal"):
+            assert np.array_equal(gs[k], os_[k]), (rnd, k)
+        d = os_["status"] == 1
+        assert np.array_equal(gs["s"][d].astype(np.float64), os_["s"][d]), rnd
+        rs = g.read_metrics(road_speed=True)["road_avg_speed"]
+        ro = o.road_avg_speed()
+        assert np.all(np.abs(rs - ro) <= 1e-5 * np.maximum(1.0, np.abs(ro))), rnd
+
+
+@pytest.mark.gpu
+def test_setter_pins_gpu():
+    import paper_2406_10661_b200 as p
+    p.build()
+    sc, lane = _one_lane()
+    g = p.Sim.from_scenario(sc)
+    g.step(60)
+    g.set_lane_max_speed(lane, 8.0)
+    g.step(81)
+    assert abs(g.read_state()["v"][0] - 8.0) < 1e-3
+    sc, jls = synth.pressure_junction([4, 0, 0, 0, 0, 0], period=30)
+    gr = sc.graph
+    g = p.Sim.from_scenario(sc)
+    g.set_signal_policy(0, POL_NONE)
+    ex = int(gr["succ_lanes"][gr["succ_offsets"][jls[0]]])
+    g.set_lane_restriction(ex, 1)
+    g.step(120)
+    st = g.read_state()
+    assert np.all(st["status"] == 1) and np.all(st["v"] < 0.1)
+    assert np.all(st["lane_signal"][gr["junc_lanes"]] == SIG_GREEN)
+    g.set_lane_restriction(ex, 0)
+    g.step(120)
+    assert np.all(g.read_state()["status"] == 2)
