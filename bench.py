@@ -97,14 +97,14 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def make_workload(world=1, policy="fixed"):
+def make_workload(world=1, policy="fixed", scale=1.0):
     """C4 at N=1; weak scaling for N > 1: the same city recipe grown to N times
     the area (G = 72 * sqrt(N)) with 2M vehicles per GPU, spatially partitioned
     over the N GPUs with boundary migration.
     policy "maxpressure": every signalised junction runs MAX_PRESSURE (NEXT-1)."""
     import synth
-    G = int(round(72 * np.sqrt(world)))
-    scen = synth.city(G=G, n_vehicles=2_000_000 * world, seed=4)
+    G = int(round(72 * np.sqrt(world * scale)))
+    scen = synth.city(G=G, n_vehicles=int(round(2_000_000 * world * scale)), seed=4)
     if policy == "maxpressure":
         jp = scen.graph["junc_policy"]
         scen.graph["junc_policy"] = np.where(jp == synth.POLICY_FIXED, synth.POLICY_MAXP, jp).astype(np.uint8)
@@ -185,7 +185,7 @@ def run_gpu(args, rank, world, local_rank):
         p.build()
     if world > 1:
         torch.distributed.barrier()
-    scen = make_workload(world, args.policy)
+    scen = make_workload(world, args.policy, args.scale)
     stream = torch.cuda.Stream(dev)          # the simulation stream (events recorded on it)
     torch.cuda.set_stream(stream)
     if world > 1:
@@ -304,6 +304,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--policy", default="fixed", choices=["fixed", "maxpressure"])
+    ap.add_argument("--scale", type=float, default=1.0,
+                    help="per-GPU size relative to C4 (4 = the 8M-vehicle single-GPU instance of SURVEY 8(d))")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -147,6 +147,8 @@ typedef struct {
   float *s, *v;
   uint8_t *junc_policy;
   int32_t *junc_phase, *junc_elapsed, *junc_yellow_left, *junc_pending;
+  int32_t *junc_remaining;           /* MANUAL set_tl_duration green steps left, -1 none
+                                        (optional on load: NULL = -1) */
   uint8_t *lane_dir;
   uint8_t *lane_signal;              /* read only: signals seen in the last step */
   int32_t *lane_offsets;             /* read only, optional: [n_lanes+1] per-lane order CSR */
@@ -217,6 +219,13 @@ sim_status sim_set_lane_direction_batch(sim_handle h, int32_t m, const int32_t *
 sim_status sim_set_signal_policy(sim_handle h, int32_t junction, int32_t policy);
 sim_status sim_set_signal_policy_batch(sim_handle h, int32_t m, const int32_t *junctions,
                                        const int32_t *policies);
+/* Phase duration (set_tl_duration): the junction switches to MANUAL
+ * and its current green (the requested phase's, after a yellow) is held for
+ * `steps` >= 1 steps from the next step, then it moves to the next phase
+ * (with the yellow) and holds it until the next request. */
+sim_status sim_set_signal_duration(sim_handle h, int32_t junction, int32_t steps);
+sim_status sim_set_signal_duration_batch(sim_handle h, int32_t m, const int32_t *junctions,
+                                         const int32_t *steps);
 /* Lane max speed (set_lane_max_speed): m/s > 0, from the next step
  * (v0 = min(lane, vehicle), L6).  The lane-start margin keeps its create-time
  * value (L17). */

@@ -49,6 +49,8 @@ struct Junction {
   int policy = POL_NONE, phase = 0, elapsed = 0, yellow = 0, pending = 0;
   int request = -1;
   int pol_request = -1;                   // set_tl_policy, applied at the next step (L42)
+  int remaining = -1;                     // MANUAL: green steps left in the current phase (L43)
+  int dur_request = -1;                   // set_tl_duration, applied at the next step (L43)
   std::vector<int> lanes;                 // junction lanes (slot order)
   std::vector<std::vector<uint8_t>> green; // [phase][slot]
   std::vector<int> green_steps;
@@ -238,16 +240,24 @@ struct Sim {
       if (np == POL_FIXED || np == POL_MAXP) j.elapsed = 0;
     }
     for (auto &j : J) {
-      if (j.request < 0) continue;
-      int r = j.request;
-      j.request = -1;
-      j.policy = POL_MANUAL;
-      if (j.yellow > 0) {
-        j.pending = r;
-      } else if (r != j.phase) {
-        if (Y > 0) { j.yellow = Y; j.pending = r; }
-        else { j.phase = r; j.pending = r; }
+      if (j.request >= 0) {
+        int r = j.request;
+        j.request = -1;
+        j.policy = POL_MANUAL;
+        j.remaining = -1;
+        if (j.yellow > 0) {
+          j.pending = r;
+        } else if (r != j.phase) {
+          if (Y > 0) { j.yellow = Y; j.pending = r; }
+          else { j.phase = r; j.pending = r; }
+        }
       }
+      // set_tl_duration (L43): MANUAL, the (next) green is held for d steps
+      if (j.dur_request >= 1 && !j.green.empty()) {
+        j.policy = POL_MANUAL;
+        j.remaining = j.dur_request;
+      }
+      j.dur_request = -1;
     }
   }
   void compute_signals() {
@@ -312,6 +322,14 @@ struct Sim {
       if (j.yellow > 0) {
         j.yellow -= 1;
         if (j.yellow == 0) j.phase = j.pending;
+      } else if (j.remaining > 0) {              // L43: hold d green steps, then the next phase
+        j.remaining -= 1;
+        if (j.remaining == 0) {
+          const int nxt = (j.phase + 1) % (int)j.green.size();
+          if (Y > 0) { j.yellow = Y; j.pending = nxt; }
+          else { j.phase = nxt; j.pending = nxt; }
+          j.remaining = -1;
+        }
       }
       j.elapsed += 1;
     }
@@ -758,6 +776,7 @@ void or_read_state(void *h, or_state *o) {
     o->junc_policy[j] = (uint8_t)J.policy; o->junc_phase[j] = J.phase;
     o->junc_elapsed[j] = J.elapsed; o->junc_yellow_left[j] = J.yellow;
     o->junc_pending[j] = J.pending;
+    o->junc_remaining[j] = J.remaining;
   }
   for (int l = 0; l < S->nl; ++l) { o->lane_dir[l] = (uint8_t)S->dir[l]; o->lane_signal[l] = S->sig[l]; }
 }
@@ -776,6 +795,7 @@ void or_load_state(void *h, const or_state *in) {
     J.policy = in->junc_policy[j]; J.phase = in->junc_phase[j];
     J.elapsed = in->junc_elapsed[j]; J.yellow = in->junc_yellow_left[j];
     J.pending = in->junc_pending[j]; J.request = -1;
+    J.remaining = in->junc_remaining[j]; J.pol_request = -1; J.dur_request = -1;
   }
   for (int l = 0; l < S->nl; ++l) S->dir[l] = in->lane_dir[l];
   S->rebuild_pending();
@@ -841,6 +861,13 @@ int32_t or_set_signal_policy(void *h, int32_t j, int32_t policy) {
   Sim *S = (Sim *)h;
   if (j < 0 || j >= S->nj || policy < POL_NONE || policy > POL_MAXP) return 2;
   S->J[j].pol_request = policy;
+  return 0;
+}
+
+int32_t or_set_signal_duration(void *h, int32_t j, int32_t steps) {
+  Sim *S = (Sim *)h;
+  if (j < 0 || j >= S->nj || steps < 1) return 2;
+  S->J[j].dur_request = steps;
   return 0;
 }
 

@@ -65,6 +65,7 @@ typedef struct {
   /* junction-indexed */
   uint8_t *junc_policy;
   int32_t *junc_phase, *junc_elapsed, *junc_yellow_left, *junc_pending;
+  int32_t *junc_remaining;      /* MANUAL set_tl_duration steps left, -1 none */
   /* lane-indexed */
   uint8_t *lane_dir;
   uint8_t *lane_signal;         /* signals seen by vehicles in the last step */
@@ -106,6 +107,7 @@ void or_lane_stats(void *h, int32_t *lane_count, int32_t *lane_waiting);
 int32_t or_set_signal_phase(void *h, int32_t junction, int32_t phase);
 int32_t or_set_lane_direction(void *h, int32_t lane, int32_t dir);
 int32_t or_set_signal_policy(void *h, int32_t junction, int32_t policy);
+int32_t or_set_signal_duration(void *h, int32_t junction, int32_t steps);
 int32_t or_set_lane_max_speed(void *h, int32_t lane, float v);
 int32_t or_set_lane_restriction(void *h, int32_t lane, int32_t flag);
 /* [n_roads] mean speed of the vehicles on each road (free-flow if empty) */

@@ -54,6 +54,7 @@ def _load():
         _lib.or_set_signal_phase.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
         _lib.or_set_lane_direction.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
         _lib.or_set_signal_policy.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
+        _lib.or_set_signal_duration.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
         _lib.or_set_lane_max_speed.argtypes = [C.c_void_p, C.c_int32, C.c_float]
         _lib.or_set_lane_restriction.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
         _lib.or_road_avg_speed.argtypes = [C.c_void_p, C.c_void_p]
@@ -99,7 +100,7 @@ class _State(C.Structure):
     _fields_ = [("t", C.c_int32)] + [(n, P) for n in (
         "status", "lane", "cursor", "wait_steps", "insert_time", "arrive_time", "s", "v",
         "junc_policy", "junc_phase", "junc_elapsed", "junc_yellow_left", "junc_pending",
-        "lane_dir", "lane_signal")]
+        "junc_remaining", "lane_dir", "lane_signal")]
 
 
 class _Dec(C.Structure):
@@ -177,7 +178,8 @@ class Oracle:
                     s=np.zeros(n, np.float64), v=np.zeros(n, np.float64),
                     junc_policy=np.zeros(nj, np.uint8), junc_phase=np.zeros(nj, np.int32),
                     junc_elapsed=np.zeros(nj, np.int32), junc_yellow_left=np.zeros(nj, np.int32),
-                    junc_pending=np.zeros(nj, np.int32), lane_dir=np.zeros(nl, np.uint8),
+                    junc_pending=np.zeros(nj, np.int32), junc_remaining=np.zeros(nj, np.int32),
+                    lane_dir=np.zeros(nl, np.uint8),
                     lane_signal=np.zeros(nl, np.uint8))
 
     def read_state(self):
@@ -190,6 +192,9 @@ class Oracle:
     def load_state(self, state):
         b = self._state_buffers()
         for k in b:
+            if k == "junc_remaining" and k not in state:
+                b[k][:] = -1                                   # no set_tl_duration timer
+                continue
             b[k][:] = np.asarray(state[k]).astype(b[k].dtype)
         st = _State(int(state["t"]), *[_ptr(b[n]) for n, _ in _State._fields_[1:]])
         self.lib.or_load_state(self.h, C.byref(st))
@@ -233,6 +238,9 @@ class Oracle:
 
     def set_signal_policy(self, j, policy):
         return self.lib.or_set_signal_policy(self.h, int(j), int(policy))
+
+    def set_signal_duration(self, j, steps):
+        return self.lib.or_set_signal_duration(self.h, int(j), int(steps))
 
     def set_lane_max_speed(self, lane, v):
         return self.lib.or_set_lane_max_speed(self.h, int(lane), float(v))

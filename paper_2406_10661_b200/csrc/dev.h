@@ -158,6 +158,8 @@ struct SignalArgs {
   uint8_t *policy;
   int32_t *phase, *elapsed, *yellow_left, *pending, *request;
   int32_t *pol_request;             // set_tl_policy requests (-1 none), applied before `request`
+  int32_t *remaining;               // MANUAL set_tl_duration green steps left (-1 none, L43)
+  int32_t *dur_request;             // set_tl_duration requests (-1 none), applied after `request`
   const int32_t *jl_off, *jl;       // junction -> lanes (slots)
   const int32_t *ph_off;            // junction -> phases
   const int64_t *green_off;         // junction -> first byte of its phase rows

@@ -611,13 +611,20 @@ __global__ void k_signal(SignalArgs a) {
     if (pol == POL_FIXED || pol == POL_MAXP) el = 0;
   }
   const int req = a.request[j];
+  int rem = a.remaining[j];
   if (req >= 0) {                                   // requests apply before sig_t (L35)
     pol = POL_MANUAL;
+    rem = -1;
     if (y > 0) q = req;
     else if (req != ph) {
       if (a.yellow > 0) { y = a.yellow; q = req; }
       else { ph = req; q = req; }
     }
+  }
+  const int dreq = a.dur_request[j];
+  if (dreq >= 1 && K > 0) {                         // set_tl_duration (L43)
+    pol = POL_MANUAL;
+    rem = dreq;
   }
   // advance t -> t+1 (O11) into the stored state; sig_t uses (pol, ph, y) above
   int nph = ph, ny = y, nel = el, nq = q;
@@ -652,12 +659,22 @@ __global__ void k_signal(SignalArgs a) {
     if (ny > 0) {
       ny -= 1;
       if (ny == 0) nph = nq;
+    } else if (rem > 0) {                           // hold d green steps, then the next phase
+      rem -= 1;
+      if (rem == 0) {
+        const int nx = (nph + 1) % K;
+        if (a.yellow > 0) { ny = a.yellow; nq = nx; }
+        else { nph = nx; nq = nx; }
+        rem = -1;
+      }
     }
     nel += 1;
   }
   if (lane == 0) {
     if (req >= 0) a.request[j] = -1;
     if (preq >= 0) a.pol_request[j] = -1;
+    if (dreq >= 0) a.dur_request[j] = -1;
+    a.remaining[j] = rem;
     a.policy[j] = (uint8_t)pol;
     a.phase[j] = nph;
     a.elapsed[j] = nel;

@@ -47,7 +47,7 @@ struct HostState {                  // vid / junction / lane indexed state
   std::vector<int> lane, cursor, wait, insert_time, arrive_time;
   std::vector<float> s, v;
   std::vector<uint8_t> jpol;
-  std::vector<int> jphase, jel, jy, jpend;
+  std::vector<int> jphase, jel, jy, jpend, jrem;
   std::vector<uint8_t> dir;
 };
 
@@ -610,7 +610,7 @@ sim_status build_tiles(sim_s *h) {
 // initial signal state: FIXED_TIME advanced `offset` steps
 void init_junctions(sim_s *h, HostState &S) {
   S.jpol.assign(h->nj, 0); S.jphase.assign(h->nj, 0); S.jel.assign(h->nj, 0);
-  S.jy.assign(h->nj, 0); S.jpend.assign(h->nj, 0);
+  S.jy.assign(h->nj, 0); S.jpend.assign(h->nj, 0); S.jrem.assign(h->nj, -1);
   for (int j = 0; j < h->nj; ++j) {
     int K = h->ph_off[j + 1] - h->ph_off[j];
     int pol = K == 0 ? POL_NONE : h->pol0[j];
@@ -857,6 +857,8 @@ sim_status upload_state(sim_s *h, const HostState &S) {
       CK(h, cudaMemcpyAsync(P.SG.elapsed, S.jel.data(), h->nj * 4, cudaMemcpyHostToDevice, st));
       CK(h, cudaMemcpyAsync(P.SG.yellow_left, S.jy.data(), h->nj * 4, cudaMemcpyHostToDevice, st));
       CK(h, cudaMemcpyAsync(P.SG.pending, S.jpend.data(), h->nj * 4, cudaMemcpyHostToDevice, st));
+      CK(h, cudaMemcpyAsync(P.SG.remaining, S.jrem.data(), h->nj * 4, cudaMemcpyHostToDevice, st));
+      CK(h, cudaMemcpyAsync(P.SG.dur_request, req.data(), h->nj * 4, cudaMemcpyHostToDevice, st));
       CK(h, cudaMemcpyAsync(P.SG.request, req.data(), h->nj * 4, cudaMemcpyHostToDevice, st));
       CK(h, cudaMemcpyAsync(P.SG.pol_request, req.data(), h->nj * 4, cudaMemcpyHostToDevice, st));
     }
@@ -1007,6 +1009,7 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   G.n_junctions = h->nj; G.yellow = h->Y;
   AL(G.policy, h->nj); AL(G.phase, h->nj); AL(G.elapsed, h->nj); AL(G.yellow_left, h->nj);
   AL(G.pending, h->nj); AL(G.request, h->nj); AL(G.pol_request, h->nj);
+  AL(G.remaining, h->nj); AL(G.dur_request, h->nj);
   UP(i32, h->jl_off); G.jl_off = i32;
   UP(i32, h->jl); G.jl = i32;
   UP(i32, h->ph_off); G.ph_off = i32;
@@ -1246,6 +1249,40 @@ sim_status rebuild_counts(sim_s *h) {
   return SIM_OK;
 }
 
+// Per-junction requests (later entries for the same junction win):
+// kind 0 phase (request), 1 policy (pol_request), 2 duration (dur_request);
+// deduplicated on the host and applied by one thread per junction.
+sim_status push_junction_requests(sim_s *h, int m, const int32_t *junctions, const int32_t *vals,
+                                  int kind) {
+  sim_status st;
+  h->req_mark.resize(h->nj, -1);
+  std::vector<int32_t> buf(2 * (size_t)m);
+  int u = 0;
+  for (int i = m - 1; i >= 0; --i) {
+    const int j = junctions[i];
+    if (h->req_mark[j] == h->req_epoch) continue;
+    h->req_mark[j] = h->req_epoch;
+    buf[u] = j;
+    buf[m + u] = vals[i];
+    ++u;
+  }
+  if (++h->req_epoch == 0x7fffffff) { h->req_epoch = 0; std::fill(h->req_mark.begin(), h->req_mark.end(), -1); }
+  std::memmove(buf.data() + u, buf.data() + m, u * 4);
+  if (h->stage_cap < 2 * u) {
+    if (h->stage_d) { CK(h, cudaStreamSynchronize(h->stream)); cudaFree(h->stage_d); }
+    CK(h, cudaMalloc(&h->stage_d, 2 * (size_t)u * 4));
+    h->stage_cap = 2 * u;
+  }
+  st = push_staging(h, buf.data(), 2 * (size_t)u * 4, h->stage_d);
+  if (st) return st;
+  for (Part &P : h->parts) {
+    int32_t *dst = kind == 0 ? P.SG.request : (kind == 1 ? P.SG.pol_request : P.SG.dur_request);
+    launch_apply_requests(dst, P.SG.policy, h->stage_d, h->stage_d + u, u, h->stream);
+    h->n_launch++;
+  }
+  return SIM_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1405,34 +1442,7 @@ sim_status sim_set_signal_phase_batch(sim_handle h, int32_t m, const int32_t *ju
     if (phases[i] < 0 || phases[i] >= K) return fail(h, SIM_E_RANGE, "phase out of range");
   }
   if (m == 0) return SIM_OK;
-  if (h->stage_cap < 2 * m) {
-    if (h->stage_d) { CK(h, cudaStreamSynchronize(h->stream)); cudaFree(h->stage_d); }
-    CK(h, cudaMalloc(&h->stage_d, 2 * (size_t)m * 4));
-    h->stage_cap = 2 * m;
-  }
-  // later entries for the same junction win: keep the last one per
-  // junction, so the device applies the batch in parallel
-  h->req_mark.resize(h->nj, -1);
-  std::vector<int32_t> buf(2 * (size_t)m);
-  int u = 0;
-  for (int i = m - 1; i >= 0; --i) {
-    const int j = junctions[i];
-    if (h->req_mark[j] == h->req_epoch) continue;
-    h->req_mark[j] = h->req_epoch;
-    buf[u] = j;
-    buf[m + u] = phases[i];
-    ++u;
-  }
-  if (++h->req_epoch == 0x7fffffff) { h->req_epoch = 0; std::fill(h->req_mark.begin(), h->req_mark.end(), -1); }
-  std::memmove(buf.data() + u, buf.data() + m, u * 4);
-  m = u;
-  st = push_staging(h, buf.data(), 2 * (size_t)m * 4, h->stage_d);
-  if (st) return st;
-  for (Part &P : h->parts) {           // replicated controllers: every partition applies it
-    launch_apply_requests(P.SG.request, P.SG.policy, h->stage_d, h->stage_d + m, m, h->stream);
-    h->n_launch++;
-  }
-  return SIM_OK;
+  return push_junction_requests(h, m, junctions, phases, 0);   // replicated controllers
 }
 
 sim_status sim_set_signal_phase(sim_handle h, int32_t j, int32_t p) {
@@ -1481,31 +1491,24 @@ sim_status sim_set_signal_policy_batch(sim_handle h, int32_t m, const int32_t *j
     st = rebuild_counts(h);
     if (st) return st;
   }
-  h->req_mark.resize(h->nj, -1);
-  std::vector<int32_t> buf(2 * (size_t)m);
-  int u = 0;
-  for (int i = m - 1; i >= 0; --i) {                 // the last entry per junction wins
-    const int j = junctions[i];
-    if (h->req_mark[j] == h->req_epoch) continue;
-    h->req_mark[j] = h->req_epoch;
-    buf[u] = j;
-    buf[m + u] = policies[i];
-    ++u;
-  }
-  if (++h->req_epoch == 0x7fffffff) { h->req_epoch = 0; std::fill(h->req_mark.begin(), h->req_mark.end(), -1); }
-  std::memmove(buf.data() + u, buf.data() + m, u * 4);
-  if (h->stage_cap < 2 * u) {
-    if (h->stage_d) { CK(h, cudaStreamSynchronize(h->stream)); cudaFree(h->stage_d); }
-    CK(h, cudaMalloc(&h->stage_d, 2 * (size_t)u * 4));
-    h->stage_cap = 2 * u;
-  }
-  st = push_staging(h, buf.data(), 2 * (size_t)u * 4, h->stage_d);
+  return push_junction_requests(h, m, junctions, policies, 1);
+}
+
+sim_status sim_set_signal_duration_batch(sim_handle h, int32_t m, const int32_t *junctions,
+                                         const int32_t *steps) {
+  sim_status st = check(h);
   if (st) return st;
-  for (Part &P : h->parts) {
-    launch_apply_requests(P.SG.pol_request, P.SG.policy, h->stage_d, h->stage_d + u, u, h->stream);
-    h->n_launch++;
+  if (m < 0 || (m > 0 && (!junctions || !steps))) return fail(h, SIM_E_INVALID, "bad batch");
+  for (int i = 0; i < m; ++i) {
+    if (junctions[i] < 0 || junctions[i] >= h->nj) return fail(h, SIM_E_RANGE, "junction out of range");
+    if (steps[i] < 1) return fail(h, SIM_E_RANGE, "duration must be >= 1 step");
   }
-  return SIM_OK;
+  if (m == 0) return SIM_OK;
+  return push_junction_requests(h, m, junctions, steps, 2);
+}
+
+sim_status sim_set_signal_duration(sim_handle h, int32_t j, int32_t steps) {
+  return sim_set_signal_duration_batch(h, 1, &j, &steps);
 }
 
 sim_status sim_set_signal_policy(sim_handle h, int32_t j, int32_t policy) {
@@ -1630,6 +1633,7 @@ sim_status sim_read_state(sim_handle h, sim_state *o) {
     if (o->junc_elapsed) CK(h, cudaMemcpy(o->junc_elapsed, P0.SG.elapsed, h->nj * 4, cudaMemcpyDeviceToHost));
     if (o->junc_yellow_left) CK(h, cudaMemcpy(o->junc_yellow_left, P0.SG.yellow_left, h->nj * 4, cudaMemcpyDeviceToHost));
     if (o->junc_pending) CK(h, cudaMemcpy(o->junc_pending, P0.SG.pending, h->nj * 4, cudaMemcpyDeviceToHost));
+    if (o->junc_remaining) CK(h, cudaMemcpy(o->junc_remaining, P0.SG.remaining, h->nj * 4, cudaMemcpyDeviceToHost));
   }
   if (o->lane_dir) std::memcpy(o->lane_dir, h->dir.data(), h->nl);
   if (o->lane_signal) CK(h, cudaMemcpy(o->lane_signal, P0.A.lane_sig, h->nl, cudaMemcpyDeviceToHost));
@@ -1890,6 +1894,8 @@ sim_status sim_load_state(sim_handle h, const sim_state *in) {
   S.jel.assign(in->junc_elapsed, in->junc_elapsed + h->nj);
   S.jy.assign(in->junc_yellow_left, in->junc_yellow_left + h->nj);
   S.jpend.assign(in->junc_pending, in->junc_pending + h->nj);
+  if (in->junc_remaining) S.jrem.assign(in->junc_remaining, in->junc_remaining + h->nj);
+  else S.jrem.assign(h->nj, -1);
   S.dir.assign(in->lane_dir, in->lane_dir + h->nl);
   return upload_state(h, S);
 }

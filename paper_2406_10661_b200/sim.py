@@ -65,6 +65,7 @@ class sim_state(C.Structure):
     _fields_ = [("t", C.c_int32)] + [(n, P) for n in (
         "status", "lane", "cursor", "wait_steps", "insert_time", "arrive_time", "s", "v",
         "junc_policy", "junc_phase", "junc_elapsed", "junc_yellow_left", "junc_pending",
+        "junc_remaining",
         "lane_dir", "lane_signal", "lane_offsets", "lane_order")]
 
 
@@ -85,7 +86,7 @@ class sim_metrics(C.Structure):
 ABI_FUNCTIONS = ["sim_create", "sim_get_nccl_unique_id", "sim_partition", "sim_step", "sim_sync", "sim_set_signal_phase",
                  "sim_set_signal_phase_batch", "sim_set_lane_direction",
                  "sim_set_lane_direction_batch", "sim_query_sizes", "sim_read_state",
-                 "sim_read_decisions", "sim_read_metrics", "sim_read_group_metrics", "sim_set_signal_policy", "sim_set_signal_policy_batch", "sim_set_lane_max_speed", "sim_set_lane_max_speed_batch", "sim_set_lane_restriction", "sim_set_lane_restriction_batch", "sim_load_state",
+                 "sim_read_decisions", "sim_read_metrics", "sim_read_group_metrics", "sim_set_signal_policy", "sim_set_signal_policy_batch", "sim_set_signal_duration", "sim_set_signal_duration_batch", "sim_set_lane_max_speed", "sim_set_lane_max_speed_batch", "sim_set_lane_restriction", "sim_set_lane_restriction_batch", "sim_load_state",
                  "sim_enable_timing", "sim_read_timing", "sim_destroy", "sim_last_error"]
 
 _lib = None
@@ -110,6 +111,7 @@ def load_library(path=LIB):
         "sim_query_sizes": [h, P], "sim_read_state": [h, P], "sim_read_decisions": [h, P],
         "sim_read_metrics": [h, P], "sim_read_group_metrics": [h, i32, P],
         "sim_set_signal_policy": [h, i32, i32], "sim_set_signal_policy_batch": [h, i32, P, P],
+        "sim_set_signal_duration": [h, i32, i32], "sim_set_signal_duration_batch": [h, i32, P, P],
         "sim_set_lane_max_speed": [h, i32, C.c_float], "sim_set_lane_max_speed_batch": [h, i32, P, P],
         "sim_set_lane_restriction": [h, i32, i32], "sim_set_lane_restriction_batch": [h, i32, P, P],
         "sim_load_state": [h, P], "sim_destroy": [h],
@@ -282,8 +284,8 @@ class Sim:
                  s=np.zeros(n, np.float32), v=np.zeros(n, np.float32),
                  junc_policy=np.zeros(nj, np.uint8), junc_phase=np.zeros(nj, np.int32),
                  junc_elapsed=np.zeros(nj, np.int32), junc_yellow_left=np.zeros(nj, np.int32),
-                 junc_pending=np.zeros(nj, np.int32), lane_dir=np.zeros(nl, np.uint8),
-                 lane_signal=np.zeros(nl, np.uint8))
+                 junc_pending=np.zeros(nj, np.int32), junc_remaining=np.zeros(nj, np.int32),
+                 lane_dir=np.zeros(nl, np.uint8), lane_signal=np.zeros(nl, np.uint8))
         if lane_order:
             b["lane_offsets"] = np.zeros(nl + 1, np.int32)
             b["lane_order"] = np.zeros(max(n, 1), np.int32)
@@ -301,6 +303,8 @@ class Sim:
                     junc_policy=np.uint8, junc_phase=np.int32, junc_elapsed=np.int32,
                     junc_yellow_left=np.int32, junc_pending=np.int32, lane_dir=np.uint8)
         b = {k: np.ascontiguousarray(state[k], dtype=dt) for k, dt in conv.items()}
+        if "junc_remaining" in state:                      # optional (NULL = no timers)
+            b["junc_remaining"] = np.ascontiguousarray(state["junc_remaining"], dtype=np.int32)
         st = sim_state(int(state["t"]), *[_ptr(b[nm]) if nm in b else None
                                           for nm, _ in sim_state._fields_[1:]])
         self._chk(self.lib.sim_load_state(self.h, C.byref(st)))
@@ -344,6 +348,14 @@ class Sim:
         j = np.ascontiguousarray(junctions, np.int32)
         p = np.ascontiguousarray(policies, np.int32)
         self._chk(self.lib.sim_set_signal_policy_batch(self.h, len(j), _ptr(j), _ptr(p)))
+
+    def set_signal_duration(self, junction, steps):
+        self._chk(self.lib.sim_set_signal_duration(self.h, int(junction), int(steps)))
+
+    def set_signal_duration_batch(self, junctions, steps):
+        j = np.ascontiguousarray(junctions, np.int32)
+        d = np.ascontiguousarray(steps, np.int32)
+        self._chk(self.lib.sim_set_signal_duration_batch(self.h, len(j), _ptr(j), _ptr(d)))
 
     def set_lane_max_speed(self, lane, v):
         self._chk(self.lib.sim_set_lane_max_speed(self.h, int(lane), float(v)))

@@ -107,6 +107,7 @@ def random_state(scen, seed=0, t=None, frac_driving=0.6, frac_pending=0.25,
     jel = np.zeros(nj, np.int32)
     jy = np.zeros(nj, np.int32)
     jpe = np.zeros(nj, np.int32)
+    jrem = np.full(nj, -1, np.int32)
     for j in range(nj):
         K = int(nph[j])
         if K == 0:
@@ -134,6 +135,8 @@ def random_state(scen, seed=0, t=None, frac_driving=0.6, frac_pending=0.25,
                 jpe[j] = p
         elif jpol[j] == POLICY_MANUAL:
             jel[j] = int(rng.integers(100))
+            if rng.random() < 0.4:                     # a set_tl_duration timer running
+                jrem[j] = int(rng.integers(1, 4))
             if rng.random() < 0.3 and Y > 0:
                 jy[j] = int(rng.integers(1, Y + 1))
                 jpe[j] = int(rng.integers(K))
@@ -151,5 +154,6 @@ def random_state(scen, seed=0, t=None, frac_driving=0.6, frac_pending=0.25,
     return dict(t=int(t), status=status, lane=lane, cursor=cursor, wait_steps=wait,
                 insert_time=insert_time, arrive_time=arrive_time, s=s, v=v,
                 junc_policy=jpol.astype(np.uint8), junc_phase=jph, junc_elapsed=jel,
-                junc_yellow_left=jy, junc_pending=jpe, lane_dir=ldir.astype(np.uint8),
+                junc_yellow_left=jy, junc_pending=jpe, junc_remaining=jrem,
+                lane_dir=ldir.astype(np.uint8),
                 lane_signal=np.zeros(nl, np.uint8))

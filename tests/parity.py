@@ -9,7 +9,8 @@ import numpy as np
 REL = 1e-5
 
 INT_STATE = ("status", "lane", "cursor", "wait_steps", "insert_time", "arrive_time")
-JUNC = ("junc_policy", "junc_phase", "junc_elapsed", "junc_yellow_left", "junc_pending")
+JUNC = ("junc_policy", "junc_phase", "junc_elapsed", "junc_yellow_left", "junc_pending",
+        "junc_remaining")
 
 
 def close(a, b, rel=REL):

@@ -1,6 +1,7 @@
 """Remaining controllable objects and metrics (Table 1
 P:1074-1082, §3.2): set_tl_policy, set_lane_max_speed,
-set_lane_restriction, road travelling speed.  Readings L42-L45.
+set_lane_restriction, set_tl_duration, road travelling speed.
+Readings L42-L45.
 
 Oracle pins (CPU):
   * NONE policy -> every junction lane GREEN;
@@ -9,6 +10,8 @@ Oracle pins (CPU):
   * restricting the only exit lane makes approaching vehicles queue at the
     road end; lifting it releases them (S:344);
   * switching FIXED_TIME -> MAX_PRESSURE restarts the green timer (L42);
+  * set_tl_duration holds the current green d steps, then yellow, then the
+    next phase (L43), signal by signal;
   * road average speed = brute-force mean of the vehicle speeds on the road's
     lanes, the road's max lane speed when it is empty (L45).
 GPU: the same setter sequences bit-identical to the oracle in exact mode, and
@@ -33,6 +36,11 @@ def test_none_policy_all_green(oracle_lib):
     jl = sc.graph["junc_lanes"]
     assert np.all(st["lane_signal"][jl] == SIG_GREEN)
     assert np.all(st["junc_policy"] == POL_NONE)
+
+
+def synth_oracle():
+    import oracle
+    return oracle.Oracle(synth.grid(rows=2, cols=2, road_len=200.0, lanes=2, n_trips=50, seed=8))
 
 
 def _one_lane(length=2000.0, vmax=13.9, n=1):
@@ -95,6 +103,42 @@ def test_policy_switch_restarts_timer(oracle_lib):
     assert st["junc_elapsed"][0] == 1 or st["junc_yellow_left"][0] > 0
 
 
+def _duration_timeline(sim, sc, t0, d, n_steps):
+    """Per step: (phase of the green / yellow seen by vehicles) for junction 0."""
+    g = sc.graph
+    lanes = g["junc_lanes"][g["junc_lane_offsets"][0]:g["junc_lane_offsets"][1]]
+    sim.step(t0)
+    st = sim.read_state()
+    p0, y0 = int(st["junc_phase"][0]), int(st["junc_yellow_left"][0])
+    sim.set_signal_duration(0, d)
+    out = []
+    for _ in range(n_steps):
+        sim.step(1)
+        st = sim.read_state()
+        out.append(tuple(int(x) for x in st["lane_signal"][lanes]))
+    return p0, y0, out, st
+
+
+def test_signal_duration_holds_then_advances(oracle_lib):
+    """set_tl_duration: the current green is held d steps, then
+    the yellow (Y = 3) and the next phase."""
+    sc = synth.grid(rows=2, cols=2, road_len=200.0, lanes=2, n_trips=50, seed=8)
+    o = oracle_lib.Oracle(sc)
+    p0, y0, tl, st = _duration_timeline(o, sc, 40, 5, 10)
+    g = sc.graph
+    K = g["junc_phase_offsets"][1] - g["junc_phase_offsets"][0]
+    ns = g["junc_lane_offsets"][1] - g["junc_lane_offsets"][0]
+    green = g["phase_green"][:K * ns].reshape(K, ns)
+    assert y0 == 0                                             # called during a green
+    exp_p = tuple(0 if green[p0][k] else 2 for k in range(ns))
+    exp_y = tuple(1 if green[p0][k] else 2 for k in range(ns))
+    exp_n = tuple(0 if green[(p0 + 1) % K][k] else 2 for k in range(ns))
+    assert tl[:5] == [exp_p] * 5, tl
+    assert tl[5:8] == [exp_y] * 3, tl
+    assert tl[8:] == [exp_n] * 2, tl
+    assert st["junc_policy"][0] == POL_MANUAL and st["junc_remaining"][0] == -1
+
+
 def test_road_avg_speed_brute_force(oracle_lib):
     sc = synth.grid(rows=3, cols=3, road_len=200.0, lanes=2, n_trips=900, seed=7)
     g = sc.graph
@@ -124,6 +168,7 @@ def _setter_script(sc, rng, n_rounds):
             calls.append(("speed", int(l), float(rng.choice([6.0, 10.0, 16.667]))))
         for l in rng.choice(len(g["lane_length"]), 2, replace=False):
             calls.append(("restrict", int(l), int(rng.integers(2))))
+        calls.append(("duration", int(rng.integers(nj)), int(rng.integers(1, 12))))
         out.append(calls)
     return out
 
@@ -134,6 +179,8 @@ def _apply(sim, calls):
             sim.set_signal_policy(a, b)
         elif kind == "speed":
             sim.set_lane_max_speed(a, b)
+        elif kind == "duration":
+            sim.set_signal_duration(a, b)
         else:
             sim.set_lane_restriction(a, b)
 
@@ -152,7 +199,7 @@ def test_setters_exact_mode_bit_identical(oracle_lib):
         o.step(25)
         gs, os_ = g.read_state(), o.read_state()
         for k in ("status", "lane", "cursor", "wait_steps", "junc_policy", "junc_phase",
-                  "junc_elapsed", "junc_yellow_left", "lane_signal"):
+                  "junc_elapsed", "junc_yellow_left", "junc_remaining", "lane_signal"):
             assert np.array_equal(gs[k], os_[k]), (rnd, k)
         d = os_["status"] == 1
         assert np.array_equal(gs["s"][d].astype(np.float64), os_["s"][d]), rnd
@@ -165,6 +212,10 @@ def test_setters_exact_mode_bit_identical(oracle_lib):
 def test_setter_pins_gpu():
     import paper_2406_10661_b200 as p
     p.build()
+    sc = synth.grid(rows=2, cols=2, road_len=200.0, lanes=2, n_trips=50, seed=8)
+    o_tl = _duration_timeline(synth_oracle(), sc, 40, 5, 10)
+    g_tl = _duration_timeline(p.Sim.from_scenario(sc), sc, 40, 5, 10)
+    assert o_tl[2] == g_tl[2]
     sc, lane = _one_lane()
     g = p.Sim.from_scenario(sc)
     g.step(60)
