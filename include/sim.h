@@ -238,6 +238,18 @@ sim_status sim_set_lane_max_speed_batch(sim_handle h, int32_t m, const int32_t *
 sim_status sim_set_lane_restriction(sim_handle h, int32_t lane, int32_t flag);
 sim_status sim_set_lane_restriction_batch(sim_handle h, int32_t m, const int32_t *lanes,
                                           const int32_t *flags);
+/* Vehicle route (set_vehicle_route): the vehicle's remaining trip
+ * becomes roads[0..n) ending at end_s on roads[n-1] (consecutive roads
+ * connected).  roads[0] must be the vehicle's current road (a DRIVING vehicle
+ * inside a junction also keeps its committed next road as roads[1]; a PENDING
+ * vehicle keeps its first road and start lane); the route cursor restarts at
+ * 0.  Synchronising (it reads the vehicles' positions); SIM_E_INVALID and no
+ * change on any violation (DESIGN L46). */
+sim_status sim_set_vehicle_route(sim_handle h, int32_t vid, int32_t n, const int32_t *roads,
+                                 float end_s);
+sim_status sim_set_vehicle_route_batch(sim_handle h, int32_t m, const int32_t *vids,
+                                       const int32_t *route_offsets, const int32_t *roads,
+                                       const float *end_s);
 sim_status sim_query_sizes(sim_handle h, sim_sizes *out);
 /* Synchronising reads into caller-owned host buffers. */
 sim_status sim_read_state(sim_handle h, sim_state *out);

@@ -864,6 +864,39 @@ int32_t or_set_signal_policy(void *h, int32_t j, int32_t policy) {
   return 0;
 }
 
+int32_t or_set_vehicle_route(void *h, int32_t k, int32_t n, const int32_t *roads, float end_s) {
+  // set_vehicle_route (L46): the remaining trip becomes roads[0..n),
+  // starting with the current road (inside a junction also the committed next
+  // road); the route cursor restarts at 0
+  Sim *S = (Sim *)h;
+  if (k < 0 || k >= (int)S->V.size() || n < 1) return 2;
+  const int nr = (int)S->road_lanes.size();
+  for (int e = 0; e < n; ++e) {
+    if (roads[e] < 0 || roads[e] >= nr) return 2;
+    if (e + 1 < n) {                                   // connected: some lane of roads[e] leads to roads[e+1]
+      bool ok = false;
+      for (int l : S->road_lanes[roads[e]])
+        for (int j : S->succ[l]) ok |= S->target_road(j) == roads[e + 1];
+      if (!ok) return 1;
+    }
+  }
+  const int dl = S->road_lanes[roads[n - 1]][0];
+  if (!((double)end_s >= 0.0 && (double)end_s <= S->L[dl])) return 1;
+  Vehicle &v = S->V[k];
+  if (v.status == FINISHED) return 1;
+  if (v.status == DRIVING) {
+    if (roads[0] != v.route[v.cursor]) return 1;
+    if (!S->is_road(v.lane) && (n < 2 || (int)v.route.size() <= v.cursor + 1 || roads[1] != v.route[v.cursor + 1]))
+      return 1;
+  } else if (roads[0] != v.route[0]) {
+    return 1;
+  }
+  v.route.assign(roads, roads + n);
+  v.cursor = 0;
+  v.end_s = (double)end_s;
+  return 0;
+}
+
 int32_t or_set_signal_duration(void *h, int32_t j, int32_t steps) {
   Sim *S = (Sim *)h;
   if (j < 0 || j >= S->nj || steps < 1) return 2;

@@ -108,6 +108,7 @@ int32_t or_set_signal_phase(void *h, int32_t junction, int32_t phase);
 int32_t or_set_lane_direction(void *h, int32_t lane, int32_t dir);
 int32_t or_set_signal_policy(void *h, int32_t junction, int32_t policy);
 int32_t or_set_signal_duration(void *h, int32_t junction, int32_t steps);
+int32_t or_set_vehicle_route(void *h, int32_t vid, int32_t n, const int32_t *roads, float end_s);
 int32_t or_set_lane_max_speed(void *h, int32_t lane, float v);
 int32_t or_set_lane_restriction(void *h, int32_t lane, int32_t flag);
 /* [n_roads] mean speed of the vehicles on each road (free-flow if empty) */

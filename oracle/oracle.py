@@ -55,6 +55,7 @@ def _load():
         _lib.or_set_lane_direction.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
         _lib.or_set_signal_policy.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
         _lib.or_set_signal_duration.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
+        _lib.or_set_vehicle_route.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_float]
         _lib.or_set_lane_max_speed.argtypes = [C.c_void_p, C.c_int32, C.c_float]
         _lib.or_set_lane_restriction.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
         _lib.or_road_avg_speed.argtypes = [C.c_void_p, C.c_void_p]
@@ -241,6 +242,10 @@ class Oracle:
 
     def set_signal_duration(self, j, steps):
         return self.lib.or_set_signal_duration(self.h, int(j), int(steps))
+
+    def set_vehicle_route(self, vid, roads, end_s):
+        r = np.ascontiguousarray(roads, np.int32)
+        return self.lib.or_set_vehicle_route(self.h, int(vid), len(r), _ptr(r), float(end_s))
 
     def set_lane_max_speed(self, lane, v):
         return self.lib.or_set_lane_max_speed(self.h, int(lane), float(v))

@@ -131,7 +131,7 @@ struct StepArgs {
   const float *pubv_cur;            // [n_veh] speed of summary vehicles at t
   float *pubv_next;
   // cold per-vehicle data
-  const int32_t *route_off, *route;
+  const int32_t *route_start, *route_len, *route;   // per vehicle: its roads route[start .. start+len)
   const float *end_s;
   const uint8_t *veh_prof;
   int32_t *insert_time, *arrive_time, *wait_fin;
@@ -186,6 +186,12 @@ void launch_reduce_acc(const long long *tacc, int n_tiles, const int32_t *cnt,
 void launch_lane_stats(const StepArgs &a, int32_t *lane_count, int32_t *lane_wait,
                        float *road_speed, float queue_zone, void *stream);
 void launch_fill_u64(unsigned long long *p, unsigned long long v, int64_t n, void *stream);
+void launch_patch_routes(const StepArgs &a, const int32_t *patch, void *stream);
+void launch_locate(const StepArgs &a, const int32_t *want, int32_t *out, void *stream);
+void launch_scatter_i32(int32_t *dst, const int32_t *idx, const int32_t *val, int32_t cval, int m,
+                        void *stream);
+void launch_scatter_f32(float *dst, const int32_t *idx, const float *val, int m, void *stream);
+void launch_gather_u8(const uint8_t *src, const int32_t *idx, uint8_t *out, int m, void *stream);
 void launch_reduce_groups(const long long *tacc, const int32_t *tiles, int n_own,
                           const int32_t *tile_group, const int32_t *cnt, const int32_t *icnt,
                           int n_groups, long long *out, void *stream);

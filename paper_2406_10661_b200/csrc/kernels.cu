@@ -486,7 +486,7 @@ __device__ __forceinline__ void tile_finish(const StepArgs &A, StepShared &S, co
     rec.s = (float)ss;
     rec.v = 0.f;
     rec.vid = k;
-    const int off = A.route_off[k], rl = A.route_off[k + 1] - off;
+    const int off = A.route_start[k], rl = A.route_len[k];
     rec.nxt = rl > 1 ? A.route[off + 1] : -1;
     rec.nxt2 = rl > 2 ? A.route[off + 2] : -1;
     rec.meta = pack_meta(l, A.veh_prof[k], 0);
@@ -909,6 +909,89 @@ void launch_reduce_groups(const long long *tacc, const int32_t *tiles, int n_own
   cudaMemsetAsync(out, 0, (size_t)n_groups * (kNAcc + 1) * sizeof(long long), (cudaStream_t)stream);
   if (n_own > 0)
     k_reduce_groups<<<296, 256, 0, (cudaStream_t)stream>>>(tacc, tiles, n_own, tile_group, cnt, icnt, out);
+}
+
+// set_vehicle_route: every DRIVING vehicle with patch[vid] >= 0
+// restarts at cursor patch[vid] (0) of its new route; its cached next roads
+// are refreshed in the slab or inbox record that holds it.
+__global__ void k_patch_routes(StepArgs A, const int32_t *patch) {
+  const int tile = A.tiles[blockIdx.x];
+  const int ns = A.cnt_in[tile], ni = A.icnt_in[tile];
+  for (int i = threadIdx.x; i < ns + ni; i += blockDim.x) {
+    int vid;
+    uint32_t *meta;
+    int32_t *nxt, *nxt2;
+    InboxRec *r = nullptr;
+    if (i < ns) {
+      const int gi = A.tile_base[tile] + i;
+      vid = A.in.vid[gi]; meta = A.in.meta + gi; nxt = A.in.nxt + gi; nxt2 = A.in.nxt2 + gi;
+    } else {
+      r = const_cast<InboxRec *>(A.inbox_in) + A.tile_ibase[tile] + i - ns;
+      vid = r->vid; meta = &r->meta; nxt = &r->nxt; nxt2 = &r->nxt2;
+    }
+    const int c = patch[vid];
+    if (c < 0) continue;
+    const int off = A.route_start[vid], len = A.route_len[vid];
+    *meta = (*meta & 0xffffu) | ((uint32_t)c << 16);
+    *nxt = c + 1 < len ? A.route[off + c + 1] : -1;
+    *nxt2 = c + 2 < len ? A.route[off + c + 2] : -1;
+  }
+}
+
+// set_vehicle_route support: where is each vehicle of a batch (want[vid] =
+// batch index b)?  out[2b] = cursor, out[2b+1] = global lane (DRIVING only).
+__global__ void k_locate(StepArgs A, const int32_t *want, int32_t *out) {
+  const int tile = A.tiles[blockIdx.x];
+  const int ns = A.cnt_in[tile], ni = A.icnt_in[tile];
+  const int l0 = A.tile_lane_off[tile];
+  for (int i = threadIdx.x; i < ns + ni; i += blockDim.x) {
+    int vid;
+    uint32_t meta;
+    if (i < ns) {
+      const int gi = A.tile_base[tile] + i;
+      vid = A.in.vid[gi]; meta = A.in.meta[gi];
+    } else {
+      const InboxRec &r = A.inbox_in[A.tile_ibase[tile] + i - ns];
+      vid = r.vid; meta = r.meta;
+    }
+    const int b = want[vid];
+    if (b < 0) continue;
+    out[2 * b] = m_cursor(meta);
+    out[2 * b + 1] = A.tile_lanes[l0 + m_lane(meta)];
+  }
+}
+
+__global__ void k_scatter_i32(int32_t *dst, const int32_t *idx, const int32_t *val, int32_t cval,
+                              int m) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) dst[idx[i]] = val ? val[i] : cval;
+}
+__global__ void k_scatter_f32(float *dst, const int32_t *idx, const float *val, int m) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) dst[idx[i]] = val[i];
+}
+
+__global__ void k_gather_u8(const uint8_t *src, const int32_t *idx, uint8_t *out, int m) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) out[i] = src[idx[i]];
+}
+void launch_gather_u8(const uint8_t *src, const int32_t *idx, uint8_t *out, int m, void *stream) {
+  if (m > 0) k_gather_u8<<<(m + 255) / 256, 256, 0, (cudaStream_t)stream>>>(src, idx, out, m);
+}
+
+void launch_locate(const StepArgs &a, const int32_t *want, int32_t *out, void *stream) {
+  if (a.n_own > 0) k_locate<<<a.n_own, 128, 0, (cudaStream_t)stream>>>(a, want, out);
+}
+void launch_scatter_i32(int32_t *dst, const int32_t *idx, const int32_t *val, int32_t cval, int m,
+                        void *stream) {
+  if (m > 0) k_scatter_i32<<<(m + 255) / 256, 256, 0, (cudaStream_t)stream>>>(dst, idx, val, cval, m);
+}
+void launch_scatter_f32(float *dst, const int32_t *idx, const float *val, int m, void *stream) {
+  if (m > 0) k_scatter_f32<<<(m + 255) / 256, 256, 0, (cudaStream_t)stream>>>(dst, idx, val, m);
+}
+
+void launch_patch_routes(const StepArgs &a, const int32_t *patch, void *stream) {
+  if (a.n_own > 0) k_patch_routes<<<a.n_own, 128, 0, (cudaStream_t)stream>>>(a, patch);
 }
 
 void launch_fill_u64(unsigned long long *p, unsigned long long v, int64_t n, void *stream) {

@@ -120,8 +120,8 @@ __device__ __forceinline__ int route_at(const StepArgs &A, int vid, int c, int n
                                         int idx) {
   if (idx == c + 1) return nxt;
   if (idx == c + 2) return nxt2;
-  int off = __ldg(A.route_off + vid);
-  int len = __ldg(A.route_off + vid + 1) - off;
+  int off = __ldg(A.route_start + vid);
+  int len = __ldg(A.route_len + vid);
   return (idx >= 0 && idx < len) ? __ldg(A.route + off + idx) : -1;
 }
 

@@ -103,6 +103,9 @@ struct Part {
   int32_t *lanestat_d = nullptr;
   int32_t *tile_group_d = nullptr;              // batched environments: group of each tile
   float *lane_vmax_d = nullptr;                 // writable alias of A.lane_vmax (set_lane_max_speed)
+  int32_t *route_start_d = nullptr, *route_len_d = nullptr, *route_d = nullptr;   // writable aliases
+  float *end_s_d = nullptr;
+  int32_t *patch_d = nullptr;                   // [n_veh] set_vehicle_route: new cursor or -1
   long long *grp_d = nullptr;                   // [n_groups][kNAcc + 1]
   std::vector<int> tiles;                       // own tiles
   // exchange plan (world > 1): migrant regions per peer (header record + cap)
@@ -141,6 +144,9 @@ struct sim_s {
   int64_t sum_cap = 0, sum_icap = 0;
   // trips
   std::vector<int> route_off, route, depart, start_lane;
+  std::vector<int> rstart, rlen;                // per vehicle: route[rstart .. rstart + rlen) (set_vehicle_route appends)
+  std::vector<std::vector<int>> radj;           // road -> roads reachable through one lane connection
+  int64_t route_cap = 0;                        // device route buffer capacity (entries)
   std::vector<float> start_s, start_v, end_s;
   std::vector<uint8_t> vprof, on0;
   // params
@@ -495,6 +501,10 @@ sim_status validate_and_copy(sim_s *h, const sim_graph *g, const sim_trips *tr,
     if (h->vprof[k] >= p->n_profiles) return fail(h, SIM_E_INVALID, "profile index out of range" + id);
     if (h->depart[k] < 0) return fail(h, SIM_E_INVALID, "depart_step must be >= 0" + id);
   }
+  h->radj = radj;
+  h->rstart.assign(nv, 0);
+  h->rlen.assign(nv, 0);
+  for (int k = 0; k < nv; ++k) { h->rstart[k] = h->route_off[k]; h->rlen[k] = h->route_off[k + 1] - h->route_off[k]; }
   h->P = *p;
   h->Y = p->yellow_steps;
   // batched environments (NEXT-3): per-vehicle Philox key / counter id, road groups
@@ -632,7 +642,7 @@ void init_junctions(sim_s *h, HostState &S) {
 
 
 int route_at(const sim_s *h, int vid, int idx) {
-  int a = h->route_off[vid], n = h->route_off[vid + 1] - a;
+  int a = h->rstart[vid], n = h->rlen[vid];
   return (idx >= 0 && idx < n) ? h->route[a + idx] : -1;
 }
 
@@ -941,9 +951,14 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   AL(A.bsort_scratch, h->sum_icap);
   AL(A.dl_scratch, sc);
   for (int b = 0; b < 3; ++b) AL(P.summ[b], nl);
-  UP(i32, h->route_off); A.route_off = i32;
-  UP(i32, h->route); A.route = i32;
-  UP(f, h->end_s); A.end_s = f;
+  UP(P.route_start_d, h->rstart); A.route_start = P.route_start_d;
+  UP(P.route_len_d, h->rlen); A.route_len = P.route_len_d;
+  if (!h->route_cap) h->route_cap = (int64_t)h->route.size() + (int64_t)h->route.size() / 4 + 4096;
+  AL(P.route_d, h->route_cap); A.route = P.route_d;
+  CK(h, cudaMemcpy(P.route_d, h->route.data(), h->route.size() * 4, cudaMemcpyHostToDevice));
+  UP(f, h->end_s); A.end_s = f; P.end_s_d = f;
+  AL(P.patch_d, nv);
+  CK(h, cudaMemset(P.patch_d, 0xff, (size_t)nv * 4));
   UP(u8, h->vprof); A.veh_prof = u8;
   AL(A.insert_time, nv); AL(A.arrive_time, nv); AL(A.wait_fin, nv); AL(A.status, nv);
   UP(i32, h->depart); A.depart = i32;
@@ -1556,6 +1571,148 @@ sim_status sim_set_lane_restriction(sim_handle h, int32_t lane, int32_t flag) {
   return sim_set_lane_restriction_batch(h, 1, &lane, &flag);
 }
 
+sim_status sim_set_vehicle_route_batch(sim_handle h, int32_t m, const int32_t *vids,
+                                       const int32_t *route_offsets, const int32_t *roads,
+                                       const float *end_s) {
+  sim_status st = check(h);
+  if (st) return st;
+  if (m < 0 || (m > 0 && (!vids || !route_offsets || !roads || !end_s)))
+    return fail(h, SIM_E_INVALID, "bad batch");
+  if (m == 0) return SIM_OK;
+  if (route_offsets[0] != 0) return fail(h, SIM_E_INVALID, "route_offsets[0] != 0");
+  std::vector<int> last(m, 1);                       // later entries for a vehicle win
+  {
+    std::vector<int> seen;
+    for (int i = m - 1; i >= 0; --i) {
+      if (vids[i] < 0 || vids[i] >= h->nv) return fail(h, SIM_E_RANGE, "vehicle out of range");
+      if (std::find(seen.begin(), seen.end(), vids[i]) != seen.end()) last[i] = 0;
+      else seen.push_back(vids[i]);
+    }
+  }
+  for (int i = 0; i < m; ++i) {
+    const int a = route_offsets[i], b = route_offsets[i + 1];
+    if (b <= a || b - a > 65000) return fail(h, SIM_E_INVALID, "route length must be in [1, 65000]");
+    for (int e = a; e < b; ++e) {
+      if (roads[e] < 0 || roads[e] >= h->nr) return fail(h, SIM_E_RANGE, "route road out of range");
+      if (e + 1 < b && !std::binary_search(h->radj[roads[e]].begin(), h->radj[roads[e]].end(), roads[e + 1]))
+        return fail(h, SIM_E_INVALID, "consecutive route roads are not connected");
+    }
+    const int dl = h->road_lanes[h->road_off[roads[b - 1]]];
+    if (!(end_s[i] >= 0 && end_s[i] <= h->L[dl])) return fail(h, SIM_E_INVALID, "end_s outside [0, L]");
+  }
+  std::vector<int32_t> sel;                          // batch entries kept
+  for (int i = 0; i < m; ++i) if (last[i]) sel.push_back(i);
+  const int u = (int)sel.size();
+  st = device_check(h);
+  if (st) return st;
+  // where is each vehicle (cursor, lane) and what is its status
+  std::vector<int32_t> hv(u), hb(u);
+  for (int q = 0; q < u; ++q) { hv[q] = vids[sel[q]]; hb[q] = q; }
+  int32_t *d = nullptr;
+  uint8_t *dst8 = nullptr;
+  CK(h, cudaMalloc(&d, (4 * (size_t)u + 8) * 4));
+  CK(h, cudaMalloc(&dst8, (size_t)u * h->parts.size() + 8));
+  int32_t *d_vid = d, *d_idx = d + u, *d_out = d + 2 * u;
+  CK(h, cudaMemcpy(d_vid, hv.data(), u * 4, cudaMemcpyHostToDevice));
+  CK(h, cudaMemcpy(d_idx, hb.data(), u * 4, cudaMemcpyHostToDevice));
+  CK(h, cudaMemset(d_out, 0xff, 2 * (size_t)u * 4));
+  for (size_t pi = 0; pi < h->parts.size(); ++pi) {
+    Part &P = h->parts[pi];
+    StepArgs a = step_args(P, h->t);
+    launch_scatter_i32(P.patch_d, d_vid, d_idx, 0, u, h->stream);
+    launch_locate(a, P.patch_d, d_out, h->stream);
+    launch_scatter_i32(P.patch_d, d_vid, nullptr, -1, u, h->stream);
+    launch_gather_u8(P.A.status, d_vid, dst8 + pi * u, u, h->stream);
+  }
+  std::vector<int32_t> loc(2 * (size_t)u);
+  std::vector<uint8_t> stt((size_t)u * h->parts.size());
+  CK(h, cudaMemcpyAsync(loc.data(), d_out, 2 * (size_t)u * 4, cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaMemcpyAsync(stt.data(), dst8, stt.size(), cudaMemcpyDeviceToHost, h->stream));
+  st = device_check(h);
+  cudaFree(d_vid);
+  cudaFree(dst8);
+  if (st) return st;
+  // validation against the current position (L46); nothing changes on failure
+  std::vector<int32_t> drv;                          // DRIVING vehicles of the batch
+  for (int q = 0; q < u; ++q) {
+    const int i = sel[q], k = vids[i];
+    const int *r = roads + route_offsets[i];
+    const int n = route_offsets[i + 1] - route_offsets[i];
+    const int c = loc[2 * q], lane = loc[2 * q + 1];
+    bool fin = false;
+    for (size_t pi = 0; pi < h->parts.size(); ++pi) fin |= stt[pi * u + q] == ST_FINISHED;
+    const std::string id = " (vehicle " + std::to_string(k) + ")";
+    if (c >= 0) {                                    // DRIVING
+      if (r[0] != route_at(h, k, c)) return fail(h, SIM_E_INVALID, "new route must start with the vehicle's current road" + id);
+      if (!is_road(h, lane) && (n < 2 || r[1] != route_at(h, k, c + 1)))
+        return fail(h, SIM_E_INVALID, "inside a junction the route must continue with the committed road" + id);
+      drv.push_back(k);
+    } else if (fin) {
+      return fail(h, SIM_E_INVALID, "vehicle already finished" + id);
+    } else {                                         // PENDING: start lane stays
+      if (r[0] != route_at(h, k, 0)) return fail(h, SIM_E_INVALID, "new route must start with the trip's first road" + id);
+    }
+  }
+  // apply: append the routes, point the vehicles at them
+  const size_t old_n = h->route.size();
+  std::vector<int32_t> ns(u), nl(u);
+  std::vector<float> ne(u);
+  for (int q = 0; q < u; ++q) {
+    const int i = sel[q], k = vids[i];
+    const int n = route_offsets[i + 1] - route_offsets[i];
+    ns[q] = (int32_t)h->route.size();
+    nl[q] = n;
+    ne[q] = end_s[i];
+    h->route.insert(h->route.end(), roads + route_offsets[i], roads + route_offsets[i + 1]);
+    h->rstart[k] = ns[q];
+    h->rlen[k] = n;
+    h->end_s[k] = end_s[i];
+  }
+  if ((int64_t)h->route.size() > 2000000000LL) return fail(h, SIM_E_INVALID, "route storage exceeds 32-bit offsets");
+  const bool grow = (int64_t)h->route.size() > h->route_cap;
+  if (grow) h->route_cap = (int64_t)h->route.size() * 2;
+  for (Part &P : h->parts) {
+    if (grow) {                                      // the old buffer is released at destroy
+      st = dalloc(h, &P.route_d, (size_t)h->route_cap);
+      if (st) return st;
+      P.A.route = P.route_d;
+      CK(h, cudaMemcpy(P.route_d, h->route.data(), h->route.size() * 4, cudaMemcpyHostToDevice));
+    } else {
+      CK(h, cudaMemcpy(P.route_d + old_n, h->route.data() + old_n, (h->route.size() - old_n) * 4,
+                       cudaMemcpyHostToDevice));
+    }
+  }
+  int32_t *e = nullptr;
+  CK(h, cudaMalloc(&e, (4 * (size_t)u + drv.size() + 8) * 4));
+  CK(h, cudaMemcpy(e, hv.data(), u * 4, cudaMemcpyHostToDevice));
+  CK(h, cudaMemcpy(e + u, ns.data(), u * 4, cudaMemcpyHostToDevice));
+  CK(h, cudaMemcpy(e + 2 * u, nl.data(), u * 4, cudaMemcpyHostToDevice));
+  CK(h, cudaMemcpy(e + 3 * u, ne.data(), u * 4, cudaMemcpyHostToDevice));
+  if (!drv.empty()) CK(h, cudaMemcpy(e + 4 * u, drv.data(), drv.size() * 4, cudaMemcpyHostToDevice));
+  for (Part &P : h->parts) {
+    launch_scatter_i32(P.route_start_d, e, e + u, 0, u, h->stream);
+    launch_scatter_i32(P.route_len_d, e, e + 2 * u, 0, u, h->stream);
+    launch_scatter_f32(P.end_s_d, e, reinterpret_cast<const float *>(e + 3 * u), u, h->stream);
+    if (!drv.empty()) {                              // restart at cursor 0 of the new route
+      StepArgs a = step_args(P, h->t);
+      a.route = P.route_d;
+      launch_scatter_i32(P.patch_d, e + 4 * u, nullptr, 0, (int)drv.size(), h->stream);
+      launch_patch_routes(a, P.patch_d, h->stream);
+      launch_scatter_i32(P.patch_d, e + 4 * u, nullptr, -1, (int)drv.size(), h->stream);
+    }
+    h->n_launch += 6;
+  }
+  st = device_check(h);
+  cudaFree(e);
+  return st;
+}
+
+sim_status sim_set_vehicle_route(sim_handle h, int32_t vid, int32_t n, const int32_t *roads,
+                                 float end_s) {
+  const int32_t off[2] = {0, n};
+  return sim_set_vehicle_route_batch(h, 1, &vid, off, roads, &end_s);
+}
+
 sim_status sim_query_sizes(sim_handle h, sim_sizes *out) {
   if (!h || !is_live(h)) return SIM_E_STATE;
   if (!out) return SIM_E_INVALID;
@@ -1883,7 +2040,7 @@ sim_status sim_load_state(sim_handle h, const sim_state *in) {
     int l = S.lane[k];
     if (l < 0 || l >= h->nl) return fail(h, SIM_E_RANGE, "lane out of range");
     int c = S.cursor[k];
-    if (c < 0 || c >= h->route_off[k + 1] - h->route_off[k]) return fail(h, SIM_E_RANGE, "cursor out of range");
+    if (c < 0 || c >= h->rlen[k]) return fail(h, SIM_E_RANGE, "cursor out of range");
     if (!(S.s[k] >= 0 && S.s[k] <= h->L[l]) || !(S.v[k] >= 0))
       return fail(h, SIM_E_RANGE, "s/v out of range for vehicle " + std::to_string(k));
   }

@@ -86,7 +86,7 @@ class sim_metrics(C.Structure):
 ABI_FUNCTIONS = ["sim_create", "sim_get_nccl_unique_id", "sim_partition", "sim_step", "sim_sync", "sim_set_signal_phase",
                  "sim_set_signal_phase_batch", "sim_set_lane_direction",
                  "sim_set_lane_direction_batch", "sim_query_sizes", "sim_read_state",
-                 "sim_read_decisions", "sim_read_metrics", "sim_read_group_metrics", "sim_set_signal_policy", "sim_set_signal_policy_batch", "sim_set_signal_duration", "sim_set_signal_duration_batch", "sim_set_lane_max_speed", "sim_set_lane_max_speed_batch", "sim_set_lane_restriction", "sim_set_lane_restriction_batch", "sim_load_state",
+                 "sim_read_decisions", "sim_read_metrics", "sim_read_group_metrics", "sim_set_signal_policy", "sim_set_signal_policy_batch", "sim_set_signal_duration", "sim_set_signal_duration_batch", "sim_set_vehicle_route", "sim_set_vehicle_route_batch", "sim_set_lane_max_speed", "sim_set_lane_max_speed_batch", "sim_set_lane_restriction", "sim_set_lane_restriction_batch", "sim_load_state",
                  "sim_enable_timing", "sim_read_timing", "sim_destroy", "sim_last_error"]
 
 _lib = None
@@ -112,6 +112,8 @@ def load_library(path=LIB):
         "sim_read_metrics": [h, P], "sim_read_group_metrics": [h, i32, P],
         "sim_set_signal_policy": [h, i32, i32], "sim_set_signal_policy_batch": [h, i32, P, P],
         "sim_set_signal_duration": [h, i32, i32], "sim_set_signal_duration_batch": [h, i32, P, P],
+        "sim_set_vehicle_route": [h, i32, i32, P, C.c_float],
+        "sim_set_vehicle_route_batch": [h, i32, P, P, P, P],
         "sim_set_lane_max_speed": [h, i32, C.c_float], "sim_set_lane_max_speed_batch": [h, i32, P, P],
         "sim_set_lane_restriction": [h, i32, i32], "sim_set_lane_restriction_batch": [h, i32, P, P],
         "sim_load_state": [h, P], "sim_destroy": [h],
@@ -356,6 +358,20 @@ class Sim:
         j = np.ascontiguousarray(junctions, np.int32)
         d = np.ascontiguousarray(steps, np.int32)
         self._chk(self.lib.sim_set_signal_duration_batch(self.h, len(j), _ptr(j), _ptr(d)))
+
+    def set_vehicle_route(self, vid, roads, end_s):
+        r = np.ascontiguousarray(roads, np.int32)
+        self._chk(self.lib.sim_set_vehicle_route(self.h, int(vid), len(r), _ptr(r), float(end_s)))
+
+    def set_vehicle_route_batch(self, vids, routes, end_s):
+        """routes: list of road sequences, one per vid."""
+        v = np.ascontiguousarray(vids, np.int32)
+        off = np.zeros(len(routes) + 1, np.int32)
+        off[1:] = np.cumsum([len(r) for r in routes])
+        rr = np.ascontiguousarray(np.concatenate([np.asarray(r, np.int32) for r in routes])
+                                  if routes else np.zeros(0, np.int32), np.int32)
+        e = np.ascontiguousarray(end_s, np.float32)
+        self._chk(self.lib.sim_set_vehicle_route_batch(self.h, len(v), _ptr(v), _ptr(off), _ptr(rr), _ptr(e)))
 
     def set_lane_max_speed(self, lane, v):
         self._chk(self.lib.sim_set_lane_max_speed(self.h, int(lane), float(v)))

@@ -235,3 +235,102 @@ def test_setter_pins_gpu():
     g.set_lane_restriction(ex, 0)
     g.step(120)
     assert np.all(g.read_state()["status"] == 2)
+
+
+def _road_adj(g):
+    adj = {}
+    lr = g["lane_road"]
+    for l in np.where(lr >= 0)[0]:
+        for e in range(g["succ_offsets"][l], g["succ_offsets"][l + 1]):
+            j = g["succ_lanes"][e]
+            t = lr[j] if lr[j] >= 0 else lr[g["succ_lanes"][g["succ_offsets"][j]]]
+            adj.setdefault(int(lr[l]), set()).add(int(t))
+    return {k: sorted(v) for k, v in adj.items()}
+
+
+def _walk(adj, start, n, rng, second=None):
+    r = [start] + ([second] if second is not None else [])
+    while len(r) < n and adj.get(r[-1]):
+        r.append(int(rng.choice(adj[r[-1]])))
+    return r
+
+
+def _reroutes(sc, st, rng, k_driving=20, k_pending=10):
+    """Valid new routes for random DRIVING / PENDING vehicles of state st."""
+    g, tr = sc.graph, sc.trips
+    adj = _road_adj(g)
+    lr = g["lane_road"]
+    out = []
+    cur_road = lambda k: int(tr["route_roads"][tr["route_offsets"][k]])
+    drv = np.where(st["status"] == 1)[0]
+    pen = np.where(st["status"] == 0)[0]
+    for k in rng.choice(drv, min(k_driving, len(drv)), replace=False):
+        lane = int(st["lane"][k])
+        if lr[lane] < 0:
+            continue                                   # junction lanes: covered by the GPU test's rule
+        r = _walk(adj, int(lr[lane]), 4, rng)
+        out.append((int(k), r, float(g["lane_length"][g["road_lanes"][g["road_lane_offsets"][r[-1]]]])))
+    for k in rng.choice(pen, min(k_pending, len(pen)), replace=False):
+        r = _walk(adj, cur_road(int(k)), 5, rng)
+        out.append((int(k), r, 10.0))
+    return out
+
+
+def test_vehicle_route_pins(oracle_lib):
+    """set_vehicle_route: after the change the vehicle travels the
+    new route's roads in order and arrives at its end; invalid
+    requests change nothing."""
+    sc = synth.grid(rows=3, cols=3, road_len=200.0, lanes=2, n_trips=600, seed=9)
+    g = sc.graph
+    o = oracle_lib.Oracle(sc)
+    o.step(150)
+    st = o.read_state()
+    rng = np.random.default_rng(4)
+    lr = g["lane_road"]
+    adj = _road_adj(g)
+    k = next(int(k) for k in np.where(st["status"] == 1)[0] if lr[st["lane"][k]] >= 0)
+    r = _walk(adj, int(lr[st["lane"][k]]), 4, rng)
+    end = float(g["lane_length"][g["road_lanes"][g["road_lane_offsets"][r[-1]]]])
+    bad = [x for x in range(len(g["road_lane_offsets"]) - 1) if x != r[0]][0]
+    assert o.set_vehicle_route(k, [bad] + r[1:], end) != 0       # must start on the current road
+    assert o.set_vehicle_route(k, r, end) == 0
+    seen = []
+    for _ in range(1500):
+        o.step(1)
+        s2 = o.read_state()
+        if s2["status"][k] == 2:
+            break
+        rd = int(lr[s2["lane"][k]])
+        if rd >= 0 and (not seen or seen[-1] != rd):
+            seen.append(rd)
+    assert s2["status"][k] == 2
+    assert seen == r[:len(seen)] and seen[-1] == r[-1], (seen, r)
+    assert o.set_vehicle_route(k, r, end) != 0                    # finished
+
+
+@pytest.mark.gpu
+def test_vehicle_route_exact_mode_bit_identical(oracle_lib):
+    import paper_2406_10661_b200 as p
+    p.build()
+    sc = synth.grid(rows=3, cols=3, road_len=200.0, lanes=2, n_trips=1500, seed=82)
+    gsim = p.Sim.from_scenario(sc, exact_mode=True)
+    o = oracle_lib.Oracle(sc, store_fp32=True)
+    rng = np.random.default_rng(5)
+    for rnd in range(6):
+        gsim.step(40)
+        o.step(40)
+        req = _reroutes(sc, o.read_state(), rng)
+        for k, r, e in req:
+            assert o.set_vehicle_route(k, r, e) == 0
+        gsim.set_vehicle_route_batch([k for k, _, _ in req], [r for _, r, _ in req],
+                                     [e for _, _, e in req])
+        gs, os_ = gsim.read_state(), o.read_state()
+        for key in ("status", "lane", "cursor"):
+            assert np.array_equal(gs[key], os_[key]), (rnd, key)
+    gsim.step(300)
+    o.step(300)
+    gs, os_ = gsim.read_state(), o.read_state()
+    for key in ("status", "lane", "cursor", "wait_steps", "arrive_time"):
+        assert np.array_equal(gs[key], os_[key]), key
+    d = os_["status"] == 1
+    assert np.array_equal(gs["s"][d].astype(np.float64), os_["s"][d])
