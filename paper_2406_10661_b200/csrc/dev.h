@@ -20,7 +20,7 @@ namespace sim {
 constexpr int kMaxTileLanes = 32;    // lanes per tile (road lanes + outgoing junction lanes)
 constexpr int kThreads = 32;         // k_step block size: one warp per road tile
 #ifndef KSMEM_VEH
-#define KSMEM_VEH 256
+#define KSMEM_VEH 112
 #endif
 constexpr int kSmemVeh = KSMEM_VEH;  // snapshot slots held in shared memory (larger tiles use global scratch)
 constexpr int kSmemInbox = 48;       // inbox keys sorted in shared memory

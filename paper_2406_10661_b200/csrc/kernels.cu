@@ -148,7 +148,7 @@ struct StepShared {
 #define KSTEP_WARPS 1
 #endif
 #ifndef KSTEP_MINB
-#define KSTEP_MINB (24 / KSTEP_WARPS)
+#define KSTEP_MINB (32 / KSTEP_WARPS)
 #endif
 constexpr int kStepWarps = KSTEP_WARPS;
 
