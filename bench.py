@@ -176,9 +176,28 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def _same_device():
+    # BENCH_SAME_DEVICE=1: every rank on cuda:0 with a gloo process group, to
+    # exercise the multi-process path on a one-GPU box (numbers not meaningful)
+    return os.environ.get("BENCH_SAME_DEVICE") == "1"
+
+
+def _device_of(local_rank):
+    return 0 if _same_device() else local_rank
+
+
+def _max_over_ranks(x, dev):
+    import torch
+    t = torch.tensor([float(x)], dtype=torch.float64,
+                     device="cpu" if _same_device() else dev)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_gpu(args, rank, world, local_rank):
     import torch
     import paper_2406_10661_b200 as p
+    local_rank = _device_of(local_rank)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if rank == 0:
@@ -188,7 +207,16 @@ def run_gpu(args, rank, world, local_rank):
     scen = make_workload(world, args.policy, args.scale)
     stream = torch.cuda.Stream(dev)          # the simulation stream (events recorded on it)
     torch.cuda.set_stream(stream)
-    if world > 1:
+    if world > 1 and args.transport == "direct":
+        # NEXT-2: k_step stores boundary movers straight into the
+        # owner GPU's inbox over NVLink peer memory (CUDA IPC), one device
+        # barrier per step; the handles are all-gathered once here
+        import synth
+        sim = p.Sim.from_scenario(scen, device=local_rank, stream=stream.cuda_stream, world=world,
+                                  rank=rank, direct=True,
+                                  road_owner=synth.rcb_partition(scen, world))
+        sim.connect_process_group()
+    elif world > 1:
         import synth
         nid = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
@@ -226,11 +254,7 @@ def run_gpu(args, rank, world, local_rank):
     tot_vsteps = m1["vehicle_steps"] - m0["vehicle_steps"]
     movers = (m1["n_lane_changes"] - m0["n_lane_changes"]) + (m1["n_handoffs"] - m0["n_handoffs"]) \
         + (m1["n_finished"] - m0["n_finished"])
-    t_max = step_ms
-    if world > 1:
-        t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        t_max = float(t.item())
+    t_max = _max_over_ranks(step_ms, dev) if world > 1 else step_ms
     value = tot_vsteps / (t_max / 1e3)
     # roofline of the dominant kernel (k_step), per GPU
     peak, peak_kind = peaks()
@@ -267,9 +291,7 @@ def run_gpu(args, rank, world, local_rank):
     e2e_v = obs["vehicle_steps"] - me0["vehicle_steps"]       # global
     e2e_val = e2e_v / e2e_dt
     if world > 1:
-        t = torch.tensor([e2e_dt], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_val = e2e_v / float(t.item())
+        e2e_val = e2e_v / _max_over_ranks(e2e_dt, dev)
     if rank != 0:
         return
     cpu = cpu_baseline(scen) if world == 1 and not args.no_cpu else None
@@ -279,8 +301,11 @@ def run_gpu(args, rank, world, local_rank):
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": workload_config(scen, policy=args.policy, extra={
             "parallelism": "single GPU" if world == 1 else
-            f"spatial partition over {world} GPUs (recursive coordinate bisection of road tiles), "
-            "boundary-vehicle migration + lane-summary halo per step via NCCL p2p",
+            f"spatial partition over {world} GPUs (recursive coordinate bisection of road tiles), " +
+            ("boundary movers stored by k_step into the owner GPU's inbox over NVLink peer memory "
+             "(CUDA IPC), one device barrier per step" if args.transport == "direct" else
+             "boundary-vehicle migration + lane-summary halo per step via NCCL p2p") +
+            (" [all ranks on one GPU: path check, not a scaling number]" if _same_device() else ""),
             "fp64_guard_hits_per_step": (m1["n_guard_hits"] - m0["n_guard_hits"]) / args.steps}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
@@ -304,6 +329,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--policy", default="fixed", choices=["fixed", "maxpressure"])
+    ap.add_argument("--transport", default="direct", choices=["direct", "nccl"],
+                    help="N > 1: direct peer-memory stores from k_step (NEXT-2) or NCCL p2p exchange")
     ap.add_argument("--scale", type=float, default=1.0,
                     help="per-GPU size relative to C4 (4 = the 8M-vehicle single-GPU instance of SURVEY 8(d))")
     args = ap.parse_args()
@@ -316,8 +343,8 @@ def main():
         return
     if world > 1:
         import torch
-        torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl")
+        torch.cuda.set_device(_device_of(local_rank))
+        torch.distributed.init_process_group("gloo" if _same_device() else "nccl")
     run_gpu(args, rank, world, local_rank)
     if world > 1:
         import torch

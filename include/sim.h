@@ -108,8 +108,18 @@ typedef struct {
    * invariance) or one process per GPU with the same nccl_id (from
    * sim_get_nccl_unique_id on one rank) and rank in [0, world).  road_owner
    * (optional, [n_roads]) fixes the partition of each road (with its outgoing
-   * junction lanes); NULL = the library's breadth-first partitioner. */
-  int32_t rank, world, loopback;
+   * junction lanes); NULL = the library's breadth-first partitioner.
+   * direct = 1: the step kernel stores each
+   * mover crossing the cut straight into the owning partition's inbox and
+   * folds it into that partition's lane summary, and reads other partitions'
+   * summaries in place — no migration / halo exchange step.  With loopback = 1
+   * the partitions share this process; with loopback = 0 it is one process per
+   * GPU (rank in [0, world), world <= 32, nccl_id unused) whose buffers are
+   * mapped by CUDA IPC (NVLink peer memory): every rank calls sim_ipc_export,
+   * the blobs are all-gathered in rank order (e.g. with torch.distributed) and
+   * passed to sim_ipc_connect before the first step or read; each step then
+   * ends with a device barrier over the ranks. */
+  int32_t rank, world, loopback, direct;
   const uint8_t *nccl_id;            /* 128 bytes, NCCL mode only */
   const int32_t *road_owner;
   /* MAX_PRESSURE: a green phase is kept for at least
@@ -187,6 +197,17 @@ typedef struct {
  * device memory on params->device and uploads the t = 0 state. */
 sim_status sim_create(const sim_graph *g, const sim_trips *trips,
                       const sim_params *params, sim_handle *out);
+/* Direct transport across processes (params.direct = 1, loopback = 0).
+ * sim_ipc_export writes this rank's CUDA IPC handles (*n_bytes bytes; out =
+ * NULL only reports the size) into out[cap].  sim_ipc_connect takes the blobs
+ * of all ranks concatenated in rank order (world x n_bytes; this rank's entry
+ * is ignored) and maps the peers' buffers; SIM_E_CUDA if a mapping fails.
+ * Until it succeeds sim_step and the reads fail with SIM_E_STATE.  A device
+ * barrier that waits > 60 s for a peer makes the handle sticky (SIM_E_STATE
+ * at the next synchronising call) instead of hanging. */
+sim_status sim_ipc_export(sim_handle h, uint8_t *out, int32_t cap, int32_t *n_bytes);
+sim_status sim_ipc_connect(sim_handle h, const uint8_t *blobs, int32_t n_bytes);
+
 /* NCCL unique id for a partitioned run (call on one rank, broadcast the 128
  * bytes to all ranks, e.g. with torch.distributed). */
 sim_status sim_get_nccl_unique_id(uint8_t out[128]);

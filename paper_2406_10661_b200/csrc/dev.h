@@ -75,6 +75,24 @@ struct HaloRec {                    // 16 B: first-vehicle summary of one lane f
   int32_t pad;
 };
 
+// Direct peer-memory transport: the device
+// buffers of partition q that other partitions write into (movers entering
+// q's tiles, first-vehicle summaries and lane counts of q's lanes) or read
+// (q's summaries / counts at t), indexed by the step parity like Part's own.
+// In one process (loopback) these are the partitions' own pointers; across
+// processes they are CUDA IPC mappings (NVLink peer memory on a multi-GPU box).
+struct PeerView {
+  InboxRec *inbox[2];
+  int32_t *icnt[2];
+  unsigned long long *summ[3];
+  float *pubv[2];
+  int32_t *lcnt[3];
+  int32_t *insert_time;
+  uint8_t *status;
+  unsigned int *bar;                // barrier arrival counter of partition q
+  void *xbuf[3];                    // read-side reduction buffers: counters, lane statistics, group metrics
+};
+
 struct Slab {                       // SoA hot record, 28 B / vehicle
   float *s, *v;
   int32_t *vid, *nxt, *nxt2;        // route[c+1], route[c+2] (-1 past the end)
@@ -147,6 +165,7 @@ struct StepArgs {
   const uint64_t *veh_seed;         // [n_veh] Philox key per vehicle (batched environments) or NULL
   const int32_t *rng_id;            // [n_veh] Philox counter id per vehicle or NULL (= vid)
   // decision recording (vid-indexed), optional
+  const PeerView *peers;            // [world] direct transport (NEXT-2), else NULL
   int32_t *r_leader, *r_of, *r_side;
   int8_t *r_hops, *r_phantom, *r_lc, *r_hand, *r_fin, *r_ins;
   float *r_acc;
@@ -170,6 +189,10 @@ struct SignalArgs {
   // and successor lane, lane vehicle counts of state(t), decision period
   const int32_t *jl_pred, *jl_succ;
   const int32_t *lane_cnt;
+  // direct transport: the count of lane x lives with its owner partition
+  const PeerView *peers;            // NULL: lane_cnt holds every lane
+  const int32_t *lane_tile, *tile_owner;
+  int32_t cnt_buf;                  // index of the lcnt buffer of state(t)
   int32_t mp_period;
 };
 
@@ -199,6 +222,10 @@ void launch_mig_header(MigRec *out_buf, const int32_t *out_off, const int32_t *o
                        int32_t *out_cnt, int world, void *stream);
 void launch_absorb(const StepArgs &a, const MigRec *in_buf, const int32_t *in_off,
                    const int32_t *in_cap, int world, void *stream);
+void launch_barrier(const PeerView *peers, int world, int rank, unsigned target, int32_t *err,
+                    void *stream);
+void launch_peer_sum(const PeerView *peers, int world, int kind, int dtype, int64_t off, int64_t n,
+                     void *out, void *stream);
 void launch_halo_pack(const StepArgs &a, const int32_t *lanes, HaloRec *buf, int64_t n, void *stream);
 void launch_halo_unpack(const StepArgs &a, const int32_t *lanes, const HaloRec *buf, int64_t n,
                         void *stream);

@@ -122,6 +122,20 @@ __device__ __forceinline__ void emit_moved(const StepArgs &A, const View &C, int
     atomicMin(&A.summ_next[r.lane_g], vkey(r.s1, vid));
     A.pubv_next[vid] = r.v1;
     if (A.lane_cnt_next) atomicAdd(&A.lane_cnt_next[r.lane_g], 1);
+  } else if (A.peers) {                             // direct transport (NEXT-2):
+    // the mover is stored straight into the owner's inbox for t+1 and folded
+    // into the owner's summary / lane count with the same integer atomics a
+    // local mover uses, so no exchange or absorb step follows
+    const PeerView &Q = A.peers[owner];
+    const int nb = (A.t + 1) & 1, ns = (A.t + 1) % 3;
+    const int slot = atomicAdd(&Q.icnt[nb][dt], 1);
+    if (slot < A.tile_icap[dt]) put_inbox(Q.inbox[nb] + A.tile_ibase[dt] + slot, rec);
+    else acc.ovf += 1;
+    atomicMin(&Q.summ[ns][r.lane_g], vkey(r.s1, vid));
+    Q.pubv[nb][vid] = r.v1;
+    if (A.lane_cnt_next) atomicAdd(&Q.lcnt[ns][r.lane_g], 1);
+    Q.insert_time[vid] = A.insert_time[vid];
+    Q.status[vid] = ST_DRIVING;
   } else {                                          // migrant to another partition
     const int slot = atomicAdd(&A.out_cnt[owner], 1);
     if (slot < A.out_cap[owner]) {
@@ -597,6 +611,11 @@ __global__ void __launch_bounds__(kStepWarps * kThreads, KSTEP_MINB)
 // inputs; the MAX_PRESSURE choice is a warp reduction of the
 // movement pressures count(pred) - count(succ) over the green slots of each
 // phase; lane 0 stores the state, all lanes write the junction's signals.
+__device__ __forceinline__ int sig_count(const SignalArgs &a, int lane) {
+  if (!a.peers) return a.lane_cnt[lane];
+  return a.peers[a.tile_owner[a.lane_tile[lane]]].lcnt[a.cnt_buf][lane];   // owner's count (NEXT-2)
+}
+
 __global__ void k_signal(SignalArgs a) {
   const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -646,7 +665,7 @@ __global__ void k_signal(SignalArgs a) {
           int part = 0;
           for (int sl = lane; sl < nj; sl += 32)
             if (gr[(int64_t)k * nj + sl])
-              part += a.lane_cnt[a.jl_pred[j0 + sl]] - a.lane_cnt[a.jl_succ[j0 + sl]];
+              part += sig_count(a, a.jl_pred[j0 + sl]) - sig_count(a, a.jl_succ[j0 + sl]);
           const int pk = __reduce_add_sync(0xffffffffu, part);
           if (k == 0 || pk > best_p) { best = k; best_p = pk; }     // ties -> lowest index
         }
@@ -854,6 +873,67 @@ __global__ void k_halo_unpack(StepArgs A, const int32_t *lanes, const HaloRec *b
     A.summ_next[lanes[i]] = r.key;
     if (r.key != kEmptyKey) A.pubv_next[(int)(unsigned)(r.key & 0xffffffffu)] = r.v;
   }
+}
+
+// ---- direct transport (NEXT-2) ------------------------------------
+// Barrier over the partitions of a multi-process run: one arrival per peer
+// (system-scope release after everything this stream did before), then wait
+// until all `world` arrivals of this round have reached our counter.  A wait
+// that exceeds 60 s (a peer died) sets *err and returns instead of hanging.
+__global__ void k_barrier(const PeerView *peers, int world, int rank, unsigned target, int32_t *err) {
+  const int q = threadIdx.x;
+  if (q < world) {
+    __threadfence_system();
+    atomicAdd_system(peers[q].bar, 1u);
+  }
+  if (q == 0) {
+    const unsigned *mine = peers[rank].bar;
+    unsigned long long t0, now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      unsigned v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
+      if ((int)(v - target) >= 0) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now - t0 > 60000000000ull) { atomicExch(err, 1); break; }
+      __nanosleep(200);
+    }
+    __threadfence_system();
+  }
+}
+
+// out[i] = sum over partitions q of xbuf[kind] of q at element off + i
+// (dtype 0 int64, 1 int32, 2 float32; integer sums are exact, float sums of
+// one non-zero contribution and zeros are exact as well).
+__global__ void k_peer_sum(const PeerView *peers, int world, int kind, int dtype, int64_t off,
+                           int64_t n, void *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (dtype == 0) {
+      long long x = 0;
+      for (int q = 0; q < world; ++q) x += reinterpret_cast<const long long *>(peers[q].xbuf[kind])[off + i];
+      reinterpret_cast<long long *>(out)[i] = x;
+    } else if (dtype == 1) {
+      int x = 0;
+      for (int q = 0; q < world; ++q) x += reinterpret_cast<const int *>(peers[q].xbuf[kind])[off + i];
+      reinterpret_cast<int *>(out)[i] = x;
+    } else {
+      float x = 0.f;
+      for (int q = 0; q < world; ++q) x += reinterpret_cast<const float *>(peers[q].xbuf[kind])[off + i];
+      reinterpret_cast<float *>(out)[i] = x;
+    }
+  }
+}
+
+void launch_barrier(const PeerView *peers, int world, int rank, unsigned target, int32_t *err,
+                    void *stream) {
+  k_barrier<<<1, 32, 0, (cudaStream_t)stream>>>(peers, world, rank, target, err);
+}
+void launch_peer_sum(const PeerView *peers, int world, int kind, int dtype, int64_t off, int64_t n,
+                     void *out, void *stream) {
+  if (n > 0)
+    k_peer_sum<<<(int)std::min<int64_t>((n + 255) / 256, 1184), 256, 0, (cudaStream_t)stream>>>(
+        peers, world, kind, dtype, off, n, out);
 }
 
 // ---- launchers ---------------------------------------------------------------

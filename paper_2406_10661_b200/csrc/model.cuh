@@ -204,7 +204,8 @@ __device__ __forceinline__ First first_of(const StepArgs &A, const TileSh &T, co
                                           int m) {
   First f;
   f.found = false;
-  if (__ldg(A.lane_tile + m) == T.tile) {
+  const int mt = __ldg(A.lane_tile + m);
+  if (mt == T.tile) {
     int ll = A.lane_local[m];
     int a = T.seg_start[ll];
     if (a < T.seg_end[ll]) {
@@ -215,12 +216,21 @@ __device__ __forceinline__ First first_of(const StepArgs &A, const TileSh &T, co
       f.len = T.P[m_prof(C.meta(a))].len;
     }
   } else {
-    unsigned long long key = A.summ_cur[m];
+    // direct transport (NEXT-2): a lane of another partition is read from its
+    // owner's summary of t, written there during step t-1 (no halo copy)
+    const unsigned long long *sc = A.summ_cur;
+    const float *pv = A.pubv_cur;
+    if (A.peers) {
+      const PeerView &Q = A.peers[__ldg(A.tile_owner + mt)];
+      sc = Q.summ[A.t % 3];
+      pv = Q.pubv[A.t & 1];
+    }
+    unsigned long long key = sc[m];
     if (key != kEmptyKey) {
       f.found = true;
       f.s = __uint_as_float((unsigned)(key >> 32));
       f.vid = (int)(unsigned)(key & 0xffffffffu);
-      f.v = A.pubv_cur[f.vid];
+      f.v = pv[f.vid];
       f.len = T.P[A.veh_prof[f.vid]].len;
     }
   }

@@ -119,6 +119,11 @@ struct Part {
   int32_t *hs_lanes = nullptr, *hr_lanes = nullptr;
   HaloRec *hs_buf = nullptr, *hr_buf = nullptr;
   int64_t hs_n = 0, hr_n = 0;
+  // direct transport (NEXT-2): this partition's exported buffers and the
+  // device table of every partition's buffers
+  PeerView view{};
+  unsigned int *bar_d = nullptr;
+  PeerView *peers_d = nullptr;
 };
 
 struct sim_s {
@@ -157,6 +162,13 @@ struct sim_s {
   // partitioning
   int world = 1, rank = 0;                      // rank: this process (NCCL mode)
   bool loopback = false;
+  bool direct = false;                          // NEXT-2: k_step writes into the owner's buffers
+  bool ipc = false;                             // direct across processes (CUDA IPC mappings)
+  bool connected = false;                       // ipc: sim_ipc_connect done
+  unsigned bar_epoch = 0;                       // ipc: barriers passed
+  int32_t *bar_err_d = nullptr;                 // ipc: set by a barrier that timed out
+  void *ipc_tmp = nullptr;                      // ipc: reduction result buffer
+  std::vector<void *> ipc_opened;               // ipc: peer mappings to close
   std::vector<int> tile_owner;
   NcclComm comm = nullptr;
   std::vector<Part> parts;
@@ -1019,6 +1031,10 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
     UP(P.hs_lanes, hs); UP(P.hr_lanes, hr);
     AL(P.hs_buf, P.hs_n); AL(P.hr_buf, P.hr_n);
   }
+  if (h->direct) {
+    AL(P.bar_d, 1);
+    CK(h, cudaMemset(P.bar_d, 0, 4));
+  }
   // signals (replicated: every partition runs every junction's controller)
   SignalArgs &G = P.SG;
   G.n_junctions = h->nj; G.yellow = h->Y;
@@ -1046,6 +1062,19 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   A.exact_mode = h->P.exact_mode;
   A.record = h->P.record_decisions;
   A.n_prof = (int)h->profs.size();
+  A.peers = nullptr;
+  G.peers = nullptr;
+  G.lane_tile = A.lane_tile;
+  G.tile_owner = A.tile_owner;
+  PeerView &V = P.view;
+  for (int b = 0; b < 2; ++b) { V.inbox[b] = P.inbox[b]; V.icnt[b] = P.icnt[b]; V.pubv[b] = P.pubv[b]; }
+  for (int b = 0; b < 3; ++b) { V.summ[b] = P.summ[b]; V.lcnt[b] = h->lcnt[b]; }
+  V.insert_time = A.insert_time;
+  V.status = A.status;
+  V.bar = P.bar_d;
+  V.xbuf[0] = P.red_d;
+  V.xbuf[1] = P.lanestat_d;
+  V.xbuf[2] = P.grp_d;
   return SIM_OK;
 #undef AL
 #undef UP
@@ -1084,6 +1113,94 @@ sim_status device_check(sim_s *h) {
     h->sticky = SIM_E_CUDA;
     return fail(h, SIM_E_CUDA, std::string("CUDA (deferred): ") + cudaGetErrorString(e));
   }
+  if (h->bar_err_d) {
+    int32_t be = 0;
+    if (cudaMemcpy(&be, h->bar_err_d, 4, cudaMemcpyDeviceToHost) == cudaSuccess && be) {
+      h->sticky = SIM_E_STATE;
+      return fail(h, SIM_E_STATE, "direct transport: a peer barrier timed out (a peer stopped stepping)");
+    }
+  }
+  return SIM_OK;
+}
+
+// Direct transport (NEXT-2): the table of every partition's buffers.  In one
+// process it is complete at create; across processes this rank's own entry is
+// filled now and the peers' by sim_ipc_connect.
+sim_status upload_peers(sim_s *h, const std::vector<PeerView> &views) {
+  for (Part &P : h->parts) {
+    if (!P.peers_d) {
+      sim_status st = dalloc(h, &P.peers_d, (size_t)h->world);
+      if (st) return st;
+    }
+    CK(h, cudaMemcpy(P.peers_d, views.data(), views.size() * sizeof(PeerView), cudaMemcpyHostToDevice));
+    P.A.peers = P.peers_d;
+    P.SG.peers = P.peers_d;
+  }
+  return SIM_OK;
+}
+
+sim_status setup_direct(sim_s *h) {
+  if (!h->ipc) {
+    std::vector<PeerView> v;
+    for (Part &P : h->parts) v.push_back(P.view);
+    return upload_peers(h, v);
+  }
+  sim_status st = dalloc(h, &h->bar_err_d, 1);
+  if (st) return st;
+  CK(h, cudaMemset(h->bar_err_d, 0, 4));
+  const size_t tmp = std::max<size_t>({(size_t)(kNAcc + 3) * 8, (2 * (size_t)h->nl + h->nr) * 4,
+                                       (size_t)h->n_groups * (kNAcc + 1) * 8});
+  char *t = nullptr;
+  st = dalloc(h, &t, tmp);
+  h->ipc_tmp = t;
+  return st;
+}
+
+// The exported buffers of a PeerView, in a fixed order (sim_ipc_export).
+constexpr int kIpcBufs = 18;
+void **view_slot(PeerView &V, int k) {
+  static_assert(kIpcBufs == 2 + 2 + 3 + 2 + 3 + 3 + 3, "PeerView layout");
+  if (k < 2) return reinterpret_cast<void **>(&V.inbox[k]);
+  if (k < 4) return reinterpret_cast<void **>(&V.icnt[k - 2]);
+  if (k < 7) return reinterpret_cast<void **>(&V.summ[k - 4]);
+  if (k < 9) return reinterpret_cast<void **>(&V.pubv[k - 7]);
+  if (k < 12) return reinterpret_cast<void **>(&V.lcnt[k - 9]);
+  if (k == 12) return reinterpret_cast<void **>(&V.insert_time);
+  if (k == 13) return reinterpret_cast<void **>(&V.status);
+  if (k == 14) return reinterpret_cast<void **>(&V.bar);
+  return &V.xbuf[k - 15];
+}
+
+// Direct transport across processes (NEXT-2): a device barrier over all
+// partitions, stream-ordered.
+sim_status barrier(sim_s *h) {
+  if (!h->ipc) return SIM_OK;
+  if (!h->connected) return fail(h, SIM_E_STATE, "direct transport: sim_ipc_connect has not been called");
+  h->bar_epoch += 1;
+  launch_barrier(h->parts[0].peers_d, h->world, h->rank, h->bar_epoch * (unsigned)h->world,
+                 h->bar_err_d, h->stream);
+  h->n_launch++;
+  return SIM_OK;
+}
+
+// Sum over ranks of a read-side buffer (xbuf[kind] + off, n elements of
+// dtype 0 int64 / 1 int32 / 2 float32): ncclAllReduce, or with the direct
+// transport a peer-memory sum between two barriers.
+sim_status allreduce_sum(sim_s *h, int kind, int dtype, int64_t off, int64_t n) {
+  Part &P = h->parts[0];
+  char *buf = reinterpret_cast<char *>(P.view.xbuf[kind]) + off * (dtype == 0 ? 8 : 4);
+  if (h->comm) {
+    const int nd = dtype == 0 ? kNcclInt64 : (dtype == 1 ? 2 /*ncclInt32*/ : 7 /*ncclFloat32*/);
+    NK(h, g_nccl.AllReduce(buf, buf, n, nd, kNcclSum, h->comm, h->stream));
+  } else if (h->ipc) {
+    sim_status st = barrier(h);                     // every rank's contribution is written
+    if (st) return st;
+    launch_peer_sum(P.peers_d, h->world, kind, dtype, off, n, h->ipc_tmp, h->stream);
+    h->n_launch++;
+    st = barrier(h);                                // every rank has read ours
+    if (st) return st;
+    CK(h, cudaMemcpyAsync(buf, h->ipc_tmp, n * (dtype == 0 ? 8 : 4), cudaMemcpyDeviceToDevice, h->stream));
+  }
   return SIM_OK;
 }
 
@@ -1096,9 +1213,9 @@ sim_status read_counters(sim_s *h, std::vector<long long> &out) {
     launch_reduce_acc(P.A.tacc, h->nt, a.cnt_in, a.icnt_in, P.A.status, 0, P.red_d, h->stream);
     h->n_launch += 1;
   }
-  if (h->comm) {
-    Part &P = h->parts[0];
-    NK(h, g_nccl.AllReduce(P.red_d, P.red_d, kNAcc + 3, kNcclInt64, kNcclSum, h->comm, h->stream));
+  if (h->comm || h->ipc) {
+    sim_status st = allreduce_sum(h, 0, 0, 0, kNAcc + 3);
+    if (st) return st;
   }
   std::vector<long long> tmp(kNAcc + 3);
   for (Part &P : h->parts) {
@@ -1144,6 +1261,7 @@ sim_status step_once(sim_s *h) {
   for (Part &P : h->parts) {
     SignalArgs sg = P.SG;
     sg.lane_cnt = h->lcnt[t % 3];
+    sg.cnt_buf = t % 3;
     launch_signal(sg, st);
     h->n_launch += h->nj > 0;
   }
@@ -1155,7 +1273,11 @@ sim_status step_once(sim_s *h) {
     h->n_launch += a.n_own > 0;
   }
   if (h->timing) CK(h, cudaEventRecord(e[2], st));
-  if (W > 1) {
+  if (h->ipc) {                                     // direct transport: movers and summaries are
+    sim_status bs = barrier(h);                     // already in the owners' buffers (NEXT-2)
+    if (bs) return bs;
+  }
+  if (W > 1 && !h->direct) {
     // 1. migration: headers carry the counts, whole regions are exchanged
     for (Part &P : h->parts) { launch_mig_header(P.out_buf, P.A.out_off, P.A.out_cap, P.out_cnt, W, st); h->n_launch++; }
     if (h->loopback) {
@@ -1260,6 +1382,7 @@ sim_status rebuild_counts(sim_s *h) {
     launch_lane_stats(a, h->lcnt[t % 3], wscratch, nullptr, h->P.queue_zone_m, h->stream);
     h->n_launch += 1;
   }
+  // (direct transport: each count stays with the lane's owner, k_signal reads it there)
   if (h->comm) NK(h, g_nccl.AllReduce(h->lcnt[t % 3], h->lcnt[t % 3], h->nl, 2 /*ncclInt32*/, kNcclSum, h->comm, h->stream));
   return SIM_OK;
 }
@@ -1311,8 +1434,62 @@ static void destroy_impl(sim_s *h) {
   if (h->stage_ev) cudaEventDestroy(h->stage_ev);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   if (h->comm) g_nccl.CommDestroy(h->comm);
+  for (void *q : h->ipc_opened) cudaIpcCloseMemHandle(q);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
+}
+
+sim_status sim_ipc_export(sim_handle h, uint8_t *out, int32_t cap, int32_t *n_bytes) {
+  sim_status st = check(h);
+  if (st) return st;
+  if (!h->ipc) return fail(h, SIM_E_INVALID, "sim_ipc_export needs world > 1, direct = 1, loopback = 0");
+  const int32_t need = kIpcBufs * (int32_t)(sizeof(cudaIpcMemHandle_t) + 1);
+  if (n_bytes) *n_bytes = need;
+  if (!out) return SIM_OK;                          // size query
+  if (cap < need) return fail(h, SIM_E_INVALID, "export buffer too small");
+  std::memset(out, 0, need);
+  PeerView &V = h->parts[0].view;
+  for (int k = 0; k < kIpcBufs; ++k) {
+    void *ptr = *view_slot(V, k);
+    if (!ptr) continue;                             // absent buffer (e.g. no groups): flag 0
+    cudaIpcMemHandle_t mh;
+    CK(h, cudaIpcGetMemHandle(&mh, ptr));
+    std::memcpy(out + k * sizeof(cudaIpcMemHandle_t), &mh, sizeof(mh));
+    out[kIpcBufs * sizeof(cudaIpcMemHandle_t) + k] = 1;
+  }
+  return SIM_OK;
+}
+
+sim_status sim_ipc_connect(sim_handle h, const uint8_t *blobs, int32_t n_bytes) {
+  sim_status st = check(h);
+  if (st) return st;
+  if (!h->ipc) return fail(h, SIM_E_INVALID, "sim_ipc_connect needs world > 1, direct = 1, loopback = 0");
+  if (h->connected) return fail(h, SIM_E_STATE, "already connected");
+  const int32_t need = kIpcBufs * (int32_t)(sizeof(cudaIpcMemHandle_t) + 1);
+  if (!blobs || n_bytes != need) return fail(h, SIM_E_INVALID, "blobs must be world x sim_ipc_export bytes");
+  std::vector<PeerView> views(h->world);
+  for (int q = 0; q < h->world; ++q) {
+    if (q == h->rank) { views[q] = h->parts[0].view; continue; }
+    const uint8_t *b = blobs + (size_t)q * need;
+    PeerView V{};
+    for (int k = 0; k < kIpcBufs; ++k) {
+      if (!b[kIpcBufs * sizeof(cudaIpcMemHandle_t) + k]) continue;
+      cudaIpcMemHandle_t mh;
+      std::memcpy(&mh, b + k * sizeof(cudaIpcMemHandle_t), sizeof(mh));
+      void *ptr = nullptr;
+      cudaError_t e = cudaIpcOpenMemHandle(&ptr, mh, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess)
+        return fail(h, SIM_E_CUDA, std::string("cudaIpcOpenMemHandle (peer ") + std::to_string(q) +
+                                       "): " + cudaGetErrorString(e));
+      h->ipc_opened.push_back(ptr);
+      *view_slot(V, k) = ptr;
+    }
+    views[q] = V;
+  }
+  st = upload_peers(h, views);
+  if (st) return st;
+  h->connected = true;
+  return SIM_OK;
 }
 
 sim_status sim_get_nccl_unique_id(uint8_t out[128]) {
@@ -1336,8 +1513,13 @@ sim_status sim_create(const sim_graph *g, const sim_trips *tr, const sim_params 
     h->world = std::max(1, p->world);
     h->rank = p->rank;
     h->loopback = h->world > 1 && p->loopback;
-    if (h->world > 1 && !h->loopback && (!p->nccl_id || p->rank < 0 || p->rank >= h->world))
-      st = fail(h, SIM_E_INVALID, "world > 1 needs loopback = 1 or (nccl_id, 0 <= rank < world)");
+    h->direct = h->world > 1 && p->direct;
+    h->ipc = h->direct && !h->loopback;
+    if (h->world > 1 && !h->loopback && !h->direct &&
+        (!p->nccl_id || p->rank < 0 || p->rank >= h->world))
+      st = fail(h, SIM_E_INVALID, "world > 1 needs loopback = 1, direct = 1 or (nccl_id, 0 <= rank < world)");
+    if (h->ipc && (p->rank < 0 || p->rank >= h->world || h->world > 32))
+      st = fail(h, SIM_E_INVALID, "direct transport across processes needs 0 <= rank < world <= 32");
     if (h->world > 1 && h->nt < h->world) st = fail(h, SIM_E_INVALID, "fewer road tiles than partitions");
   }
   if (!st) {
@@ -1365,16 +1547,17 @@ sim_status sim_create(const sim_graph *g, const sim_trips *tr, const sim_params 
   h->smem = step_smem_bytes();
   compute_usable(h);                 // usable flags, reachable roads, tile descriptors
   Plan plan;
-  if (h->world > 1) plan = make_plan(h);
+  if (h->world > 1 && !h->direct) plan = make_plan(h);
   const int nparts = h->loopback ? h->world : 1;
   h->parts.resize(nparts);
   for (int i = 0; i < nparts && !st; ++i) {
     Part &P = h->parts[i];
     P.rank = h->loopback ? i : (h->world > 1 ? h->rank : 0);
     for (int T = 0; T < h->nt; ++T) if (h->tile_owner[T] == P.rank) P.tiles.push_back(T);
-    st = alloc_part(h, P, h->world > 1 ? &plan : nullptr);
+    st = alloc_part(h, P, (h->world > 1 && !h->direct) ? &plan : nullptr);
   }
-  if (!st && h->world > 1 && !h->loopback) {
+  if (!st && h->direct) st = setup_direct(h);
+  if (!st && h->world > 1 && !h->loopback && !h->direct) {
     std::string err;
     if (!g_nccl.load(err)) st = fail(h, SIM_E_NCCL, err);
     else {
@@ -1427,6 +1610,10 @@ sim_status sim_step(sim_handle h, int32_t n) {
   sim_status st = check(h);
   if (st) return st;
   if (n < 0) return fail(h, SIM_E_RANGE, "n must be >= 0");
+  if (n > 0 && h->ipc) {                            // host-side changes of every rank precede
+    st = barrier(h);                                // the first peer write of this call
+    if (st) return st;
+  }
   for (int i = 0; i < n; ++i) {
     st = step_once(h);
     if (st) return st;
@@ -1885,9 +2072,9 @@ sim_status sim_read_metrics(sim_handle h, sim_metrics *m) {
     launch_reduce_acc(P.A.tacc, h->nt, a.cnt_in, a.icnt_in, P.A.status, 0, P.red_d, h->stream);
     h->n_launch += 1;
   }
-  if (h->comm) {
-    Part &P = h->parts[0];
-    NK(h, g_nccl.AllReduce(P.red_d, P.red_d, kNAcc + 3, kNcclInt64, kNcclSum, h->comm, h->stream));
+  if (h->comm || h->ipc) {
+    sim_status st = allreduce_sum(h, 0, 0, 0, kNAcc + 3);
+    if (st) return st;
   }
   for (size_t q = 0; q < h->parts.size(); ++q)
     CK(h, cudaMemcpyAsync(hc + q * (kNAcc + 3), h->parts[q].red_d, (kNAcc + 3) * 8,
@@ -1898,15 +2085,16 @@ sim_status sim_read_metrics(sim_handle h, sim_metrics *m) {
     // every lane belongs to one tile: the loopback partitions together write all
     // of them; ranks of a real partition only their own, so zero first
     float *rs = m->road_avg_speed ? reinterpret_cast<float *>(d + 2 * (size_t)h->nl) : nullptr;
-    if (h->comm) CK(h, cudaMemsetAsync(d, 0, (2 * (size_t)h->nl + h->nr) * 4, h->stream));
+    if (h->comm || h->ipc) CK(h, cudaMemsetAsync(d, 0, (2 * (size_t)h->nl + h->nr) * 4, h->stream));
     for (Part &P : h->parts) {
       StepArgs a = step_args(P, h->t);
       launch_lane_stats(a, d, d + h->nl, rs, h->P.queue_zone_m, h->stream);
       h->n_launch += 1;
     }
-    if (h->comm) {
-      NK(h, g_nccl.AllReduce(d, d, 2 * (size_t)h->nl, 2 /*ncclInt32*/, kNcclSum, h->comm, h->stream));
-      if (rs) NK(h, g_nccl.AllReduce(rs, rs, h->nr, 7 /*ncclFloat32*/, kNcclSum, h->comm, h->stream));
+    if (h->comm || h->ipc) {
+      st = allreduce_sum(h, 1, 1, 0, 2 * (int64_t)h->nl);
+      if (!st && rs) st = allreduce_sum(h, 1, 2, 2 * (int64_t)h->nl, h->nr);
+      if (st) return st;
     }
     CK(h, cudaMemcpyAsync(hl, d, (2 * (size_t)h->nl + h->nr) * 4, cudaMemcpyDeviceToHost, h->stream));
   }
@@ -1952,16 +2140,16 @@ sim_status sim_read_group_metrics(sim_handle h, int32_t n_groups, sim_metrics *o
                          h->n_groups, P.grp_d, h->stream);
     h->n_launch += 1;
   }
-  if (h->comm) {
-    Part &P = h->parts[0];
-    NK(h, g_nccl.AllReduce(P.grp_d, P.grp_d, w, kNcclInt64, kNcclSum, h->comm, h->stream));
+  if (h->comm || h->ipc) {
+    st = allreduce_sum(h, 2, 0, 0, (int64_t)w);
+    if (st) return st;
   }
   for (size_t q = 0; q < h->parts.size(); ++q) {
     CK(h, cudaMemcpyAsync(tmp.data(), h->parts[q].grp_d, w * 8, cudaMemcpyDeviceToHost, h->stream));
     st = device_check(h);
     if (st) return st;
     for (size_t i = 0; i < w; ++i) c[i] += tmp[i];
-    if (h->comm) break;                               // allreduced: one copy holds the total
+    if (h->comm || h->ipc) break;                     // allreduced: one copy holds the total
   }
   for (int g = 0; g < h->n_groups; ++g) {
     const long long *x = c.data() + (size_t)g * (kNAcc + 1);

@@ -50,7 +50,7 @@ class sim_params(C.Structure):
                 ("yellow_steps", C.c_int32), ("lookahead_lanes", C.c_int32),
                 ("exact_mode", C.c_int32), ("record_decisions", C.c_int32),
                 ("device", C.c_int32), ("stream", P), ("rank", C.c_int32),
-                ("world", C.c_int32), ("loopback", C.c_int32), ("nccl_id", P),
+                ("world", C.c_int32), ("loopback", C.c_int32), ("direct", C.c_int32), ("nccl_id", P),
                 ("road_owner", P), ("max_pressure_period", C.c_int32),
                 ("vehicle_seed", P), ("vehicle_rng_id", P), ("road_group", P),
                 ("n_groups", C.c_int32)]
@@ -83,7 +83,7 @@ class sim_metrics(C.Structure):
                                           ("lane_waiting_at_end", P), ("road_avg_speed", P)]
 
 
-ABI_FUNCTIONS = ["sim_create", "sim_get_nccl_unique_id", "sim_partition", "sim_step", "sim_sync", "sim_set_signal_phase",
+ABI_FUNCTIONS = ["sim_create", "sim_get_nccl_unique_id", "sim_ipc_export", "sim_ipc_connect", "sim_partition", "sim_step", "sim_sync", "sim_set_signal_phase",
                  "sim_set_signal_phase_batch", "sim_set_lane_direction",
                  "sim_set_lane_direction_batch", "sim_query_sizes", "sim_read_state",
                  "sim_read_decisions", "sim_read_metrics", "sim_read_group_metrics", "sim_set_signal_policy", "sim_set_signal_policy_batch", "sim_set_signal_duration", "sim_set_signal_duration_batch", "sim_set_vehicle_route", "sim_set_vehicle_route_batch", "sim_set_lane_max_speed", "sim_set_lane_max_speed_batch", "sim_set_lane_restriction", "sim_set_lane_restriction_batch", "sim_load_state",
@@ -105,6 +105,7 @@ def load_library(path=LIB):
     sig = {
         "sim_create": [P, P, P, C.POINTER(C.c_void_p)],
         "sim_get_nccl_unique_id": [P], "sim_partition": [P, P, P, P, P],
+        "sim_ipc_export": [h, P, i32, P], "sim_ipc_connect": [h, P, i32],
         "sim_step": [h, i32], "sim_sync": [h],
         "sim_set_signal_phase": [h, i32, i32], "sim_set_signal_phase_batch": [h, i32, P, P],
         "sim_set_lane_direction": [h, i32, i32], "sim_set_lane_direction_batch": [h, i32, P, P],
@@ -147,7 +148,7 @@ _TRIP_DT = dict(depart_step=np.int32, on_network_at_t0=np.uint8, route_offsets=n
 
 def _marshal(graph, trips, profiles, params, device=0, stream=None, exact_mode=False,
              record_decisions=False, world=1, rank=0, loopback=False, nccl_id=None,
-             road_owner=None):
+             road_owner=None, direct=False):
     g = {k: np.ascontiguousarray(graph[k], dtype=dt) for k, dt in _GRAPH_DT.items()}
     tr = {k: np.ascontiguousarray(trips[k], dtype=dt) for k, dt in _TRIP_DT.items()}
     prof = np.ascontiguousarray(profiles, dtype=np.float32).reshape(-1, 6)
@@ -171,7 +172,7 @@ def _marshal(graph, trips, profiles, params, device=0, stream=None, exact_mode=F
                     params["v_wait"], params["queue_zone_m"], params["yellow_steps"],
                     params["lookahead_lanes"], int(exact_mode), int(record_decisions),
                     int(device), C.c_void_p(stream) if stream else None, int(rank),
-                    int(world), int(bool(loopback)),
+                    int(world), int(bool(loopback)), int(bool(direct)),
                     _ptr(nid) if nid is not None else None,
                     _ptr(own) if own is not None else None,
                     int(params.get("max_pressure_period", 30)),
@@ -228,11 +229,12 @@ class Sim:
 
     def __init__(self, graph, trips, profiles, params, device=0, stream=None,
                  exact_mode=False, record_decisions=False, world=1, rank=0, loopback=False,
-                 nccl_id=None, road_owner=None):
+                 nccl_id=None, road_owner=None, direct=False):
         lib = load_library()
         self.lib = lib
         G, T, Pm, keep = _marshal(graph, trips, profiles, params, device, stream, exact_mode,
-                                  record_decisions, world, rank, loopback, nccl_id, road_owner)
+                                  record_decisions, world, rank, loopback, nccl_id, road_owner,
+                                  direct)
         self.n_lanes, self.n_junctions, self.n = G.n_lanes, G.n_junctions, T.n_trips
         self.n_roads = G.n_roads
         self.world, self.rank = max(1, int(world)), int(rank)
@@ -250,6 +252,27 @@ class Sim:
     def _chk(self, st):
         if st != SIM_OK:
             raise SimError(st, (self.lib.sim_last_error(self.h) or b"").decode())
+
+    def ipc_export(self):
+        """This rank's CUDA IPC handles (direct transport across processes)."""
+        n = C.c_int32(0)
+        self._chk(self.lib.sim_ipc_export(self.h, None, 0, C.byref(n)))
+        buf = np.zeros(n.value, np.uint8)
+        self._chk(self.lib.sim_ipc_export(self.h, _ptr(buf), n.value, C.byref(n)))
+        return bytes(buf)
+
+    def ipc_connect(self, blobs):
+        """Map the peers' buffers; blobs = every rank's ipc_export() in rank order."""
+        n = len(blobs[0])
+        a = np.frombuffer(b"".join(blobs), np.uint8).copy()
+        self._chk(self.lib.sim_ipc_connect(self.h, _ptr(a), n))
+
+    def connect_process_group(self, group=None):
+        """All-gather the IPC handles over torch.distributed and connect."""
+        import torch.distributed as dist
+        blobs = [None] * self.world
+        dist.all_gather_object(blobs, self.ipc_export(), group=group)
+        self.ipc_connect(blobs)
 
     def step(self, n=1):
         self._chk(self.lib.sim_step(self.h, int(n)))

@@ -1,0 +1,43 @@
+"""Per-step cost of the partition exchange on one GPU: C4 as one
+partition, and as 8 partitions in one process with the copy transport
+(migration regions + k_absorb + halo pack / copy / unpack) and with the direct
+transport (NEXT-2: k_step stores movers and summaries into the owner's
+buffers; nothing after the step).  The 8-partition runs do the same
+vehicle-steps as the single partition, so the difference is the exchange."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import synth
+import paper_2406_10661_b200 as p
+
+cache = "/tmp/c4.npz"
+scen = synth.load_scenario(cache) if os.path.exists(cache) else synth.city()
+if not os.path.exists(cache):
+    synth.save_scenario(scen, cache)
+W = int(sys.argv[1]) if len(sys.argv) > 1 else 8
+own = synth.rcb_partition(scen, W)
+out = {"workload": "C4", "partitions": W}
+for name, kw in (("single", {}), ("copy", dict(world=W, loopback=True, road_owner=own)),
+                 ("direct", dict(world=W, loopback=True, direct=True, road_owner=own))):
+    st = torch.cuda.Stream()
+    sim = p.Sim.from_scenario(scen, stream=st.cuda_stream, **kw)
+    sim.step(10)
+    sim.sync()
+    m0 = sim.read_metrics()
+    n = 40
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(st):
+        e0.record(st)
+        sim.step(n)
+        e1.record(st)
+    torch.cuda.synchronize()
+    m1 = sim.read_metrics()
+    ms = e0.elapsed_time(e1) / n
+    out[name] = {"ms_per_step": ms, "vehicle_steps_per_s": (m1["vehicle_steps"] - m0["vehicle_steps"]) / (ms * n / 1e3)}
+    del sim
+    torch.cuda.synchronize()
+print(json.dumps(out))

@@ -2,7 +2,9 @@
 migration of boundary vehicles, halo of lane summaries) run with
 the loopback transport gives bit-identical state and metrics for any number
 of partitions — decisions depend only on the snapshot and (seed, vid, t), and
-every reduction is integer."""
+every reduction is integer.  direct=True is the NEXT-2
+transport: the step kernel writes movers and summaries straight
+into the owning partition's buffers, with no exchange step."""
 import numpy as np
 import pytest
 
@@ -31,9 +33,10 @@ MKEYS = ("n_pending", "n_driving", "n_finished", "vehicle_steps", "sum_travel_st
          "n_inserted", "n_guard_hits")
 
 
+@pytest.mark.parametrize("direct", [False, True])
 @pytest.mark.parametrize("world", [2, 3, 5])
 @pytest.mark.parametrize("name", ["grid", "city", "grid_maxpressure"])
-def test_partition_invariance(simlib, name, world):
+def test_partition_invariance(simlib, name, world, direct):
     """grid_maxpressure: the MAX_PRESSURE choice needs every lane's count, so
     the partitions' counts must add up exactly (shared buffer / allreduce)."""
     if name == "city":
@@ -43,7 +46,7 @@ def test_partition_invariance(simlib, name, world):
                           depart_window=400,
                           policy=synth.POLICY_MAXP if name == "grid_maxpressure" else synth.POLICY_FIXED)
     s1, m1 = _run(simlib, scen, 150)
-    sw, mw = _run(simlib, scen, 150, world=world, loopback=True)
+    sw, mw = _run(simlib, scen, 150, world=world, loopback=True, direct=direct)
     for k in KEYS:
         assert np.array_equal(s1[k], sw[k]), (k, world)
     for k in MKEYS:
@@ -53,11 +56,12 @@ def test_partition_invariance(simlib, name, world):
     assert m1["n_handoffs"] > 0
 
 
-def test_partitioned_exact_mode_matches_oracle(simlib, oracle_lib):
+@pytest.mark.parametrize("direct", [False, True])
+def test_partitioned_exact_mode_matches_oracle(simlib, oracle_lib, direct):
     """The partitioned path is still the model: exact mode with 3 partitions
     equals the oracle (store_fp32) bit for bit."""
     scen = synth.grid(rows=3, cols=3, road_len=200.0, lanes=2, n_trips=1500, seed=21)
-    g = simlib.Sim.from_scenario(scen, exact_mode=True, world=3, loopback=True)
+    g = simlib.Sim.from_scenario(scen, exact_mode=True, world=3, loopback=True, direct=direct)
     o = oracle_lib.Oracle(scen, store_fp32=True)
     g.step(200)
     o.step(200)
@@ -68,11 +72,13 @@ def test_partitioned_exact_mode_matches_oracle(simlib, oracle_lib):
     assert np.array_equal(gs["s"][d].astype(np.float64), os_["s"][d])
 
 
-def test_partitioned_decisions_and_setters(simlib):
+@pytest.mark.parametrize("direct", [False, True])
+def test_partitioned_decisions_and_setters(simlib, direct):
     scen = synth.grid(rows=3, cols=3, road_len=250.0, lanes=3, n_trips=1500, seed=31,
                       tidal=True, dynamic=True, depart_window=300)
     a = simlib.Sim.from_scenario(scen, record_decisions=True)
-    b = simlib.Sim.from_scenario(scen, record_decisions=True, world=4, loopback=True)
+    b = simlib.Sim.from_scenario(scen, record_decisions=True, world=4, loopback=True,
+                                 direct=direct)
     rng = np.random.default_rng(1)
     dyn = np.where(scen.graph["lane_kind"] == 1)[0]
     for t in range(6):
