@@ -86,6 +86,27 @@ struct Acc8 {                        // per-thread counters of one tile
   int fin = 0, lc = 0, hand = 0, guard = 0, ovf = 0, ins = 0;
 };
 
+// Direct transport (NEXT-2): a mover entering another partition's
+// tile is stored straight into the owner's inbox for t+1 and folded into the
+// owner's summary / lane count with the same integer atomics a local mover
+// uses, so no exchange or absorb step follows.  Returns 1 on inbox overflow.
+__device__ __noinline__ int emit_peer(const StepArgs &A, const InboxRec &rec, int owner, int dt,
+                                      int lane_g) {
+  const PeerView &Q = A.peers[owner];
+  const int nb = (A.t + 1) & 1, ns = (A.t + 1) % 3;
+  const int vid = rec.vid;
+  const int slot = atomicAdd(&Q.icnt[nb][dt], 1);
+  int ovf = 0;
+  if (slot < A.tile_icap[dt]) put_inbox(Q.inbox[nb] + A.tile_ibase[dt] + slot, rec);
+  else ovf = 1;
+  atomicMin(&Q.summ[ns][lane_g], vkey(rec.s, vid));
+  Q.pubv[nb][vid] = rec.v;
+  if (A.lane_cnt_next) atomicAdd(&Q.lcnt[ns][lane_g], 1);
+  Q.insert_time[vid] = A.insert_time[vid];
+  Q.status[vid] = ST_DRIVING;
+  return ovf;
+}
+
 // a vehicle that leaves its slot: lane change / hand-off (kind 2, also every
 // guard-deferred vehicle) or arrival (kind 3)
 __device__ __forceinline__ void emit_moved(const StepArgs &A, const View &C, int i, const Res &r,
@@ -122,20 +143,8 @@ __device__ __forceinline__ void emit_moved(const StepArgs &A, const View &C, int
     atomicMin(&A.summ_next[r.lane_g], vkey(r.s1, vid));
     A.pubv_next[vid] = r.v1;
     if (A.lane_cnt_next) atomicAdd(&A.lane_cnt_next[r.lane_g], 1);
-  } else if (A.peers) {                             // direct transport (NEXT-2):
-    // the mover is stored straight into the owner's inbox for t+1 and folded
-    // into the owner's summary / lane count with the same integer atomics a
-    // local mover uses, so no exchange or absorb step follows
-    const PeerView &Q = A.peers[owner];
-    const int nb = (A.t + 1) & 1, ns = (A.t + 1) % 3;
-    const int slot = atomicAdd(&Q.icnt[nb][dt], 1);
-    if (slot < A.tile_icap[dt]) put_inbox(Q.inbox[nb] + A.tile_ibase[dt] + slot, rec);
-    else acc.ovf += 1;
-    atomicMin(&Q.summ[ns][r.lane_g], vkey(r.s1, vid));
-    Q.pubv[nb][vid] = r.v1;
-    if (A.lane_cnt_next) atomicAdd(&Q.lcnt[ns][r.lane_g], 1);
-    Q.insert_time[vid] = A.insert_time[vid];
-    Q.status[vid] = ST_DRIVING;
+  } else if (A.peers) {                             // direct transport (NEXT-2)
+    acc.ovf += emit_peer(A, rec, owner, dt, r.lane_g);
   } else {                                          // migrant to another partition
     const int slot = atomicAdd(&A.out_cnt[owner], 1);
     if (slot < A.out_cap[owner]) {
@@ -241,6 +250,44 @@ __device__ __forceinline__ void tile_load(const StepArgs &A, StepShared &S, unsi
     e.outr = make_int4(w[4], w[5], w[6], w[7]);
     e.stop = ((fl & 1) && A.lane_sig[e.j] != SIG_GREEN) ? 1 : 0;
     T.se[(fl >> 8) & 0xff][fl >> 16] = e;
+  }
+  reinterpret_cast<int16_t *>(&T.gidx[0][0])[lane_id] = (int16_t)-1;    // 64 bytes
+  __syncwarp();
+  {
+    // distinct target roads of the road lanes (entry e = lane a, group g),
+    // numbered in order of first appearance; per road a lane bitmask
+    static_assert(kMaxRoadLanes * kMaxGroups <= 32, "one entry per thread");
+    const int a = lane_id / kMaxGroups, g = lane_id % kMaxGroups;
+    const bool valid = a < nroad && g < T.ng[a];
+    const int R = valid ? T.gtroad[a][g] : -1;
+    const unsigned vb = __ballot_sync(0xffffffffu, valid);
+    bool first = valid;
+    int myk = -1;
+    unsigned fb = 0;
+#pragma unroll 1
+    for (int q = 0; q < kMaxRoadLanes * kMaxGroups; ++q) {
+      const int Rq = __shfl_sync(0xffffffffu, R, q);
+      if (valid && ((vb >> q) & 1u) && Rq == R && q < lane_id) first = false;
+    }
+    fb = __ballot_sync(0xffffffffu, first);
+#pragma unroll 1
+    for (int q = 0; q < kMaxRoadLanes * kMaxGroups; ++q) {
+      const int Rq = __shfl_sync(0xffffffffu, R, q);
+      if (valid && ((fb >> q) & 1u) && Rq == R) myk = __popc(fb & ((1u << q) - 1u));
+    }
+    if (first) T.troad[myk] = R;
+    if (valid) T.gidx[a][myk] = (int8_t)g;
+    const int ntr = __popc(fb);
+    for (int k = 0; k < ntr; ++k) {
+      const unsigned m = __ballot_sync(0xffffffffu, valid && myk == k);
+      unsigned lanes = 0;
+#pragma unroll
+      for (int aa = 0; aa < kMaxRoadLanes; ++aa)
+        if ((m >> (aa * kMaxGroups)) & ((1u << kMaxGroups) - 1u)) lanes |= 1u << aa;
+      if (lane_id == 0) T.reach[k] = (uint8_t)lanes;
+    }
+    const unsigned um = __ballot_sync(0xffffffffu, lane_id < nroad && T.usable[lane_id]);
+    if (lane_id == 0) { T.ntr = ntr; T.umask = um; }
   }
   __syncwarp();
 

@@ -93,6 +93,16 @@ struct TileSh {
   int first_out[kMaxTileLanes];
   int8_t left[kMaxTileLanes], right[kMaxTileLanes];
   uint8_t isroad[kMaxTileLanes], usable[kMaxTileLanes];
+  // the distinct roads the tile's road lanes lead to (<= 4 lanes x 4 groups):
+  // reach[k] = road lanes with a usable successor toward troad[k],
+  // gidx[a][k] = that group of lane a (-1 none); umask = usable road lanes.
+  // A vehicle finds k for its next road once; every "lane a leads to my next
+  // road" test is then one bit
+  int ntr;
+  uint32_t umask;
+  int troad[kMaxRoadLanes * kMaxGroups];
+  uint8_t reach[kMaxRoadLanes * kMaxGroups];
+  int8_t gidx[kMaxRoadLanes][kMaxRoadLanes * kMaxGroups];
 };
 
 // Snapshot of the tile at time t: the fields other vehicles read (s, v, vid,
@@ -182,6 +192,23 @@ __device__ __forceinline__ Next next1_t(const StepArgs &A, const TileSh &T, int 
   }
   return Next{kLaneBlocked, false};
 }
+// next1_t for the vehicle's own next road, known as troad[k] (k < 0: no road
+// lane of the tile leads there)
+__device__ __forceinline__ Next next1_k(const TileSh &T, int l, int k, int R2) {
+  const int g = k >= 0 ? T.gidx[l][k] : -1;
+  if (g < 0) return Next{kLaneBlocked, false};
+  const int b = T.gbeg[l][g], e = T.gbeg[l][g + 1];
+  for (int q = b; q < e; ++q) {
+    const SuccEnt &x = T.se[l][q];
+    if (pref_ok(x.outr, R2)) return Next{x.j, x.stop != 0};
+  }
+  return Next{T.se[l][b].j, T.se[l][b].stop != 0};
+}
+__device__ __forceinline__ int troad_index(const TileSh &T, int R) {
+  for (int k = 0; k < T.ntr; ++k)
+    if (T.troad[k] == R) return k;
+  return -1;
+}
 __device__ __forceinline__ int next_from_road_t(const StepArgs &A, const TileSh &T, int l, int R1,
                                                 int R2) {
   return next1_t(A, T, l, R1, R2).j;
@@ -197,6 +224,15 @@ __device__ __forceinline__ int next_from_road_any(const StepArgs &A, const TileS
 }
 
 struct First { bool found; float s, v, len; int vid; };
+
+// direct transport: lane m of tile mt from its owner partition's buffers of t
+// (out of line: keeps the single-partition lookahead path unchanged)
+__device__ __noinline__ unsigned long long peer_summary(const StepArgs &A, int mt, int m,
+                                                        const float *&pv) {
+  const PeerView &Q = A.peers[__ldg(A.tile_owner + mt)];
+  pv = Q.pubv[A.t & 1];
+  return Q.summ[A.t % 3][m];
+}
 
 // first vehicle of lane m at time t: from the tile snapshot if m is ours, else
 // from the lane summary built race-free during step t-1
@@ -218,14 +254,10 @@ __device__ __forceinline__ First first_of(const StepArgs &A, const TileSh &T, co
   } else {
     // direct transport (NEXT-2): a lane of another partition is read from its
     // owner's summary of t, written there during step t-1 (no halo copy)
-    const unsigned long long *sc = A.summ_cur;
+    unsigned long long key;
     const float *pv = A.pubv_cur;
-    if (A.peers) {
-      const PeerView &Q = A.peers[__ldg(A.tile_owner + mt)];
-      sc = Q.summ[A.t % 3];
-      pv = Q.pubv[A.t & 1];
-    }
-    unsigned long long key = sc[m];
+    if (!A.peers) key = A.summ_cur[m];
+    else key = peer_summary(A, mt, m, pv);
     if (key != kEmptyKey) {
       f.found = true;
       f.s = __uint_as_float((unsigned)(key >> 32));
@@ -246,6 +278,7 @@ template <typename R> struct LEv {
 
 struct Me {                          // the ego vehicle's identity / route cache
   int vid, cur, nxt, nxt2;
+  int k;                             // index of nxt in the tile's target roads (TileSh::troad)
 };
 
 // O4-O6 for the ego placed on tile-local lane l (App. A2.3)
@@ -257,7 +290,7 @@ __device__ LEv<R> eval_lane(const StepArgs &A, const TileSh &T, const View &C, i
   const int lg = T.glob[l];
   const bool road = T.isroad[l];
   Next nx;
-  if (road) nx = me.nxt < 0 ? Next{kLaneDest, false} : next1_t(A, T, l, me.nxt, me.nxt2);
+  if (road) nx = me.nxt < 0 ? Next{kLaneDest, false} : next1_k(T, l, me.k, me.nxt2);
   else nx = Next{__ldg(A.exit_lane + lg), false};
   e.next1 = nx.j;
   const R vmax_l = (R)T.vmax[l];
@@ -490,16 +523,18 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
   bool inG = true, consider = false, want0 = false, want1 = false;
   int mand = 0;
   int sl0 = -1, sl1 = -1, f0 = -1, f1 = -1, b0 = -1, b1 = -1;
+  me.k = -1;
   if (T.isroad[l]) {                                     // no LC in junction lanes
-    inG = dest || has_outroad_t(A, T, l, me.nxt);        // l in G <=> next1 != BLOCKED
+    // road lanes of the tile leading to the next road: one bit each
+    uint32_t G = T.umask;                                // destination road: every usable lane
+    if (!dest) {
+      me.k = troad_index(T, me.nxt);
+      G = me.k >= 0 ? T.reach[me.k] : 0u;
+    }
+    inG = dest || ((G >> l) & 1u);                       // l in G <=> next1 != BLOCKED
     if (!inG) {                                          // ledger L18, L37
-      bool left_ok = false, right_ok = false;
-      for (int a = 0; a < T.nroad; ++a) {
-        if (!T.usable[a] || !has_outroad_t(A, T, a, me.nxt)) continue;
-        if (a < l) left_ok = true;
-        if (a > l) right_ok = true;
-      }
-      mand = left_ok ? -1 : (right_ok ? 1 : 0);
+      const uint32_t M = G & T.umask;
+      mand = (M & ((1u << l) - 1u)) ? -1 : ((M >> (l + 1)) ? 1 : 0);
     }
     const R rem = M::sub(L, s);
     const R need = M::add(p.s0, M::mul(v, p.T));
@@ -510,10 +545,11 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
     sl1 = T.right[l];
     consider = inG ? !l19 : (mand != 0);
     if (consider) {
-      want0 = sl0 >= 0 && T.usable[sl0] &&
-              (inG ? (dest || has_outroad_t(A, T, sl0, me.nxt)) : mand == -1);
-      want1 = sl1 >= 0 && T.usable[sl1] &&
-              (inG ? (dest || has_outroad_t(A, T, sl1, me.nxt)) : mand == 1);
+      // discretionary: usable side lanes that also lead to the next road;
+      // mandatory (L18): the usable side lane toward G
+      const uint32_t W = T.umask & (inG ? G : ~0u);
+      want0 = sl0 >= 0 && ((W >> sl0) & 1u) && (inG || mand == -1);
+      want1 = sl1 >= 0 && ((W >> sl1) & 1u) && (inG || mand == 1);
     }
 #pragma unroll 1
     for (int sd = 0; sd < 2; ++sd) {                     // side pointers (ties -> back, L11)
