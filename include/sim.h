@@ -208,6 +208,19 @@ sim_status sim_create(const sim_graph *g, const sim_trips *trips,
 sim_status sim_ipc_export(sim_handle h, uint8_t *out, int32_t cap, int32_t *n_bytes);
 sim_status sim_ipc_connect(sim_handle h, const uint8_t *blobs, int32_t n_bytes);
 
+/* Dynamic repartitioning (direct = 1 only,
+ * SPMD: every rank calls it at the same step with the same argument).
+ * road_owner [n_roads] is the new owner of each road tile; NULL = the library
+ * rebalances: its breadth-first partition weighted by the vehicles currently
+ * on each road tile (+1), summed over the partitions.  At the step boundary
+ * each tile that changes owner is handed over on the device (stayers, inbox,
+ * lane summaries and counts, pending-queue heads, its vehicles' insert time
+ * and status) — results stay bit-identical to an unpartitioned run (P-PART).
+ * *moved_tiles (may be NULL) = tiles that changed owner.  Synchronises the
+ * stream.  SIM_E_INVALID without the direct transport, SIM_E_RANGE for an
+ * owner outside [0, world). */
+sim_status sim_repartition(sim_handle h, const int32_t *road_owner, int32_t *moved_tiles);
+
 /* NCCL unique id for a partitioned run (call on one rank, broadcast the 128
  * bytes to all ranks, e.g. with torch.distributed). */
 sim_status sim_get_nccl_unique_id(uint8_t out[128]);

@@ -57,7 +57,7 @@ struct Prof {                       // one vehicle profile
 
 static_assert(sizeof(Prof) % 16 == 0, "Prof is copied as int4 words");
 
-struct InboxRec {                   // 32 B, one sector
+struct __align__(16) InboxRec {      // 32 B, one sector (16-B aligned: moved as two int4)
   float s, v;
   int32_t vid, nxt, nxt2;
   uint32_t meta;                    // lane_local:8 | profile:8 | cursor:16
@@ -75,13 +75,20 @@ struct HaloRec {                    // 16 B: first-vehicle summary of one lane f
   int32_t pad;
 };
 
+struct Slab {                       // SoA hot record, 28 B / vehicle
+  float *s, *v;
+  int32_t *vid, *nxt, *nxt2;        // route[c+1], route[c+2] (-1 past the end)
+  uint32_t *meta;
+  int32_t *wait;
+};
+
 // Direct peer-memory transport: the device
 // buffers of partition q that other partitions write into (movers entering
 // q's tiles, first-vehicle summaries and lane counts of q's lanes) or read
 // (q's summaries / counts at t), indexed by the step parity like Part's own.
 // In one process (loopback) these are the partitions' own pointers; across
 // processes they are CUDA IPC mappings (NVLink peer memory on a multi-GPU box).
-struct PeerView {
+struct PeerView {                   // pointers only (exported as an array of handles)
   InboxRec *inbox[2];
   int32_t *icnt[2];
   unsigned long long *summ[3];
@@ -90,15 +97,12 @@ struct PeerView {
   int32_t *insert_time;
   uint8_t *status;
   unsigned int *bar;                // barrier arrival counter of partition q
+  Slab slab[2];                     // stayers, cnt and pending-queue heads: moved when a
+  int32_t *cnt[2];                  // tile changes owner (sim_repartition)
+  int32_t *pend_head;
   void *xbuf[3];                    // read-side reduction buffers: counters, lane statistics, group metrics
 };
 
-struct Slab {                       // SoA hot record, 28 B / vehicle
-  float *s, *v;
-  int32_t *vid, *nxt, *nxt2;        // route[c+1], route[c+2] (-1 past the end)
-  uint32_t *meta;
-  int32_t *wait;
-};
 
 __host__ __device__ inline uint32_t pack_meta(int lane_local, int prof, int cursor) {
   return (uint32_t)lane_local | ((uint32_t)prof << 8) | ((uint32_t)cursor << 16);
@@ -226,6 +230,8 @@ void launch_barrier(const PeerView *peers, int world, int rank, unsigned target,
                     void *stream);
 void launch_peer_sum(const PeerView *peers, int world, int kind, int dtype, int64_t off, int64_t n,
                      void *out, void *stream);
+void launch_rehome(const StepArgs &a, const int32_t *new_owner, void *stream);
+void launch_tile_counts(const StepArgs &a, int32_t *out, void *stream);
 void launch_halo_pack(const StepArgs &a, const int32_t *lanes, HaloRec *buf, int64_t n, void *stream);
 void launch_halo_unpack(const StepArgs &a, const int32_t *lanes, const HaloRec *buf, int64_t n,
                         void *stream);

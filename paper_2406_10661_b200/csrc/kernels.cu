@@ -972,6 +972,72 @@ __global__ void k_peer_sum(const PeerView *peers, int world, int kind, int dtype
   }
 }
 
+// Repartition (NEXT-2): every own tile whose new owner is
+// another partition is handed over at a step boundary — its stayer rows and
+// inbox records of t, its lanes' summaries / summary speeds / lane counts of
+// t and pending-queue heads, and its vehicles' insert time and status are
+// stored into the new owner's buffers at the same (global) positions; the old
+// owner's counts for the tile become 0.  One block per own tile.
+__global__ void k_rehome(StepArgs A, const int32_t *new_owner) {
+  const int T = A.tiles[blockIdx.x];
+  const int q = new_owner[T];
+  if (q == A.rank) return;
+  const PeerView &Q = A.peers[q];
+  const PeerView &P = A.peers[A.rank];
+  const int par = A.t & 1, s3 = A.t % 3;
+  const int n = A.cnt_in[T], m = A.icnt_in[T];
+  const int base = A.tile_base[T], ibase = A.tile_ibase[T];
+  const Slab &D = Q.slab[par];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int g = base + i, vid = A.in.vid[g];
+    D.s[g] = A.in.s[g]; D.v[g] = A.in.v[g]; D.vid[g] = vid; D.nxt[g] = A.in.nxt[g];
+    D.nxt2[g] = A.in.nxt2[g]; D.meta[g] = A.in.meta[g]; D.wait[g] = A.in.wait[g];
+    Q.insert_time[vid] = A.insert_time[vid];
+    Q.status[vid] = ST_DRIVING;
+  }
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const InboxRec r = A.inbox_in[ibase + i];
+    put_inbox(Q.inbox[par] + ibase + i, r);
+    Q.insert_time[r.vid] = A.insert_time[r.vid];
+    Q.status[r.vid] = ST_DRIVING;
+  }
+  const int l0 = A.tile_lane_off[T], nl = A.tile_lane_off[T + 1] - l0;
+  for (int k = threadIdx.x; k < nl; k += blockDim.x) {
+    const int g = A.tile_lanes[l0 + k];
+    const unsigned long long key = A.summ_cur[g];
+    Q.summ[s3][g] = key;
+    Q.summ[(s3 + 1) % 3][g] = kEmptyKey;
+    if (key != kEmptyKey) {
+      const int vid = (int)(unsigned)(key & 0xffffffffu);
+      Q.pubv[par][vid] = A.pubv_cur[vid];
+    }
+    if (Q.lcnt[s3] != P.lcnt[s3]) Q.lcnt[s3][g] = P.lcnt[s3][g];
+    Q.pend_head[g] = A.pend_head[g];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Q.cnt[par][T] = n;
+    Q.icnt[par][T] = m;
+    A.cnt_in[T] = 0;
+    A.icnt_in[T] = 0;
+  }
+}
+
+// vehicles (stayers + inbox) of every own tile -> out[tile] (others untouched)
+__global__ void k_tile_counts(StepArgs A, int32_t *out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n_own; i += gridDim.x * blockDim.x) {
+    const int T = A.tiles[i];
+    out[T] = A.cnt_in[T] + A.icnt_in[T];
+  }
+}
+
+void launch_rehome(const StepArgs &a, const int32_t *new_owner, void *stream) {
+  if (a.n_own > 0) k_rehome<<<a.n_own, 128, 0, (cudaStream_t)stream>>>(a, new_owner);
+}
+void launch_tile_counts(const StepArgs &a, int32_t *out, void *stream) {
+  if (a.n_own > 0) k_tile_counts<<<(a.n_own + 255) / 256, 256, 0, (cudaStream_t)stream>>>(a, out);
+}
+
 void launch_barrier(const PeerView *peers, int world, int rank, unsigned target, int32_t *err,
                     void *stream) {
   k_barrier<<<1, 32, 0, (cudaStream_t)stream>>>(peers, world, rank, target, err);

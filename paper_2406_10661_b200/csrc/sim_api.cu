@@ -663,7 +663,8 @@ int route_at(const sim_s *h, int vid, int idx) {
 // road adjacency (deterministic, from road 0, ties by id), cut into `world`
 // contiguous chunks of equal slot capacity.  Callers with coordinates can pass
 // their own road_owner (bench.py uses recursive coordinate bisection).
-std::vector<int> default_partition(const sim_s *h, int world) {
+std::vector<int> default_partition(const sim_s *h, int world,
+                                   const std::vector<int64_t> *weight = nullptr) {
   std::vector<std::vector<int>> adj(h->nr);
   for (int l = 0; l < h->nl; ++l) {
     if (!is_road(h, l)) continue;
@@ -685,13 +686,15 @@ std::vector<int> default_partition(const sim_s *h, int world) {
       for (int x : adj[r]) if (!seen[x]) { seen[x] = 1; q.push_back(x); }
     }
   }
+  // weight of a road tile: its slot capacity, or (repartition) the given load
+  auto wt = [&](int r) { return weight ? (*weight)[r] : (int64_t)h->tile_cap[r]; };
   int64_t tot = 0;
-  for (int r = 0; r < h->nr; ++r) tot += h->tile_cap[r];
+  for (int r = 0; r < h->nr; ++r) tot += wt(r);
   std::vector<int> owner(h->nr, 0);
   int64_t acc = 0;
   for (int r : order) {
     owner[r] = (int)std::min<int64_t>(world - 1, (acc * world) / std::max<int64_t>(tot, 1));
-    acc += h->tile_cap[r];
+    acc += wt(r);
   }
   return owner;
 }
@@ -1072,6 +1075,8 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   V.insert_time = A.insert_time;
   V.status = A.status;
   V.bar = P.bar_d;
+  for (int b = 0; b < 2; ++b) { V.slab[b] = P.slab[b]; V.cnt[b] = P.cnt[b]; }
+  V.pend_head = P.pend_head_d;
   V.xbuf[0] = P.red_d;
   V.xbuf[1] = P.lanestat_d;
   V.xbuf[2] = P.grp_d;
@@ -1157,19 +1162,9 @@ sim_status setup_direct(sim_s *h) {
 }
 
 // The exported buffers of a PeerView, in a fixed order (sim_ipc_export).
-constexpr int kIpcBufs = 18;
-void **view_slot(PeerView &V, int k) {
-  static_assert(kIpcBufs == 2 + 2 + 3 + 2 + 3 + 3 + 3, "PeerView layout");
-  if (k < 2) return reinterpret_cast<void **>(&V.inbox[k]);
-  if (k < 4) return reinterpret_cast<void **>(&V.icnt[k - 2]);
-  if (k < 7) return reinterpret_cast<void **>(&V.summ[k - 4]);
-  if (k < 9) return reinterpret_cast<void **>(&V.pubv[k - 7]);
-  if (k < 12) return reinterpret_cast<void **>(&V.lcnt[k - 9]);
-  if (k == 12) return reinterpret_cast<void **>(&V.insert_time);
-  if (k == 13) return reinterpret_cast<void **>(&V.status);
-  if (k == 14) return reinterpret_cast<void **>(&V.bar);
-  return &V.xbuf[k - 15];
-}
+constexpr int kIpcBufs = (int)(sizeof(PeerView) / sizeof(void *));
+static_assert(sizeof(PeerView) == kIpcBufs * sizeof(void *), "PeerView holds pointers only");
+void **view_slot(PeerView &V, int k) { return reinterpret_cast<void **>(&V) + k; }
 
 // Direct transport across processes (NEXT-2): a device barrier over all
 // partitions, stream-ordered.
@@ -1490,6 +1485,79 @@ sim_status sim_ipc_connect(sim_handle h, const uint8_t *blobs, int32_t n_bytes) 
   if (st) return st;
   h->connected = true;
   return SIM_OK;
+}
+
+sim_status sim_repartition(sim_handle h, const int32_t *road_owner, int32_t *moved_tiles) {
+  sim_status st = check(h);
+  if (st) return st;
+  if (!h->direct) return fail(h, SIM_E_INVALID, "sim_repartition needs world > 1 and direct = 1");
+  if (h->ipc && !h->connected) return fail(h, SIM_E_STATE, "direct transport: sim_ipc_connect has not been called");
+  const int W = h->world, nt = h->nt, t = h->t;
+  std::vector<int> own;
+  if (road_owner) {
+    own.assign(road_owner, road_owner + nt);
+    for (int x : own)
+      if (x < 0 || x >= W) return fail(h, SIM_E_RANGE, "road_owner out of [0, world)");
+  } else {
+    // balance the current load: vehicles per road tile (+1 so empty roads
+    // still spread), summed over the partitions
+    Part &P0 = h->parts[0];
+    int32_t *d = P0.lanestat_d;
+    std::vector<int64_t> w(nt, 1);
+    std::vector<int32_t> c(nt);
+    for (Part &P : h->parts) {
+      int32_t *dst = h->loopback ? P.lanestat_d : d;
+      CK(h, cudaMemsetAsync(dst, 0, nt * 4, h->stream));
+      launch_tile_counts(step_args(P, t), dst, h->stream);
+      h->n_launch++;
+    }
+    if (h->ipc) {
+      st = allreduce_sum(h, 1, 1, 0, nt);
+      if (st) return st;
+    }
+    for (Part &P : h->parts) {
+      CK(h, cudaMemcpyAsync(c.data(), h->loopback ? P.lanestat_d : d, nt * 4, cudaMemcpyDeviceToHost, h->stream));
+      st = device_check(h);
+      if (st) return st;
+      for (int T = 0; T < nt; ++T) w[T] += c[T];
+      if (!h->loopback) break;
+    }
+    own = default_partition(h, W, &w);
+  }
+  int moved = 0;
+  for (int T = 0; T < nt; ++T) moved += own[T] != h->tile_owner[T];
+  if (moved_tiles) *moved_tiles = moved;
+  if (!moved) return SIM_OK;
+  st = barrier(h);                                  // every rank is at the same step boundary
+  if (st) return st;
+  int32_t *own_d = nullptr;
+  st = dalloc(h, &own_d, (size_t)nt);
+  if (st) return st;
+  CK(h, cudaMemcpyAsync(own_d, own.data(), nt * 4, cudaMemcpyHostToDevice, h->stream));
+  for (Part &P : h->parts) {
+    launch_rehome(step_args(P, t), own_d, h->stream);
+    h->n_launch++;
+  }
+  st = barrier(h);                                  // the hand-over has landed everywhere
+  if (st) return st;
+  h->tile_owner = own;
+  for (Part &P : h->parts) {
+    P.tiles.clear();
+    for (int T = 0; T < nt; ++T) if (own[T] == P.rank) P.tiles.push_back(T);
+    std::vector<int> order(P.tiles);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int a, int b) { return h->tile_cap[a] > h->tile_cap[b]; });
+    int32_t *tl = nullptr;
+    st = dalloc(h, &tl, order.size());
+    if (st) return st;
+    if (!order.empty())
+      CK(h, cudaMemcpyAsync(tl, order.data(), order.size() * 4, cudaMemcpyHostToDevice, h->stream));
+    CK(h, cudaMemcpyAsync(const_cast<int32_t *>(P.A.tile_owner), own_d, nt * 4,
+                          cudaMemcpyDeviceToDevice, h->stream));
+    P.A.tiles = tl;
+    P.A.n_own = (int)order.size();
+  }
+  return device_check(h);                           // host vectors above stay valid until done
 }
 
 sim_status sim_get_nccl_unique_id(uint8_t out[128]) {

@@ -83,7 +83,8 @@ class sim_metrics(C.Structure):
                                           ("lane_waiting_at_end", P), ("road_avg_speed", P)]
 
 
-ABI_FUNCTIONS = ["sim_create", "sim_get_nccl_unique_id", "sim_ipc_export", "sim_ipc_connect", "sim_partition", "sim_step", "sim_sync", "sim_set_signal_phase",
+ABI_FUNCTIONS = ["sim_create", "sim_get_nccl_unique_id", "sim_ipc_export", "sim_ipc_connect",
+                 "sim_repartition", "sim_partition", "sim_step", "sim_sync", "sim_set_signal_phase",
                  "sim_set_signal_phase_batch", "sim_set_lane_direction",
                  "sim_set_lane_direction_batch", "sim_query_sizes", "sim_read_state",
                  "sim_read_decisions", "sim_read_metrics", "sim_read_group_metrics", "sim_set_signal_policy", "sim_set_signal_policy_batch", "sim_set_signal_duration", "sim_set_signal_duration_batch", "sim_set_vehicle_route", "sim_set_vehicle_route_batch", "sim_set_lane_max_speed", "sim_set_lane_max_speed_batch", "sim_set_lane_restriction", "sim_set_lane_restriction_batch", "sim_load_state",
@@ -106,6 +107,7 @@ def load_library(path=LIB):
         "sim_create": [P, P, P, C.POINTER(C.c_void_p)],
         "sim_get_nccl_unique_id": [P], "sim_partition": [P, P, P, P, P],
         "sim_ipc_export": [h, P, i32, P], "sim_ipc_connect": [h, P, i32],
+        "sim_repartition": [h, P, P],
         "sim_step": [h, i32], "sim_sync": [h],
         "sim_set_signal_phase": [h, i32, i32], "sim_set_signal_phase_batch": [h, i32, P, P],
         "sim_set_lane_direction": [h, i32, i32], "sim_set_lane_direction_batch": [h, i32, P, P],
@@ -273,6 +275,16 @@ class Sim:
         blobs = [None] * self.world
         dist.all_gather_object(blobs, self.ipc_export(), group=group)
         self.ipc_connect(blobs)
+
+    def repartition(self, road_owner=None):
+        """Hand road tiles to new owners at this step boundary (direct
+        transport); road_owner None = rebalance by the current vehicle counts.
+        Returns the number of tiles that moved."""
+        moved = C.c_int32(0)
+        own = None if road_owner is None else np.ascontiguousarray(road_owner, np.int32)
+        self._chk(self.lib.sim_repartition(self.h, None if own is None else _ptr(own),
+                                           C.byref(moved)))
+        return moved.value
 
     def step(self, n=1):
         self._chk(self.lib.sim_step(self.h, int(n)))

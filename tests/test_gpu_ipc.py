@@ -35,10 +35,12 @@ def _worker(rank, world, port, name, out_dir):
     g = p.Sim.from_scenario(scen, world=world, rank=rank, direct=True, device=0)
     g.connect_process_group()
     g.step(STEPS // 2)
+    moved = g.repartition()                          # NEXT-2 rebalance by current load
     g.step(STEPS - STEPS // 2)
     st = g.read_state()
     m = g.read_metrics(lane_stats=True)
-    np.savez(os.path.join(out_dir, f"r{rank}.npz"), **{k: np.asarray(v) for k, v in st.items()},
+    np.savez(os.path.join(out_dir, f"r{rank}.npz"), moved=moved,
+             **{k: np.asarray(v) for k, v in st.items()},
              **{"m_" + k: np.asarray(v) for k, v in m.items() if v is not None})
     dist.barrier()
     dist.destroy_process_group()
@@ -63,6 +65,7 @@ def test_multi_process_direct_transport(name, world):
     ref.step(STEPS)
     s1 = ref.read_state()
     m1 = ref.read_metrics(lane_stats=True)
+    assert len({int(r["moved"]) for r in rs}) == 1 and int(rs[0]["moved"]) > 0
     # union of the partitions: each DRIVING vehicle is reported by its owner only
     drv = np.stack([r["status"] == 1 for r in rs])
     assert (drv.sum(0) <= 1).all()

@@ -96,3 +96,43 @@ def test_partitioned_decisions_and_setters(simlib, direct):
         sa, sb = a.read_state(), b.read_state()
         for k in ("status", "lane", "s", "v", "junc_phase", "lane_signal"):
             assert np.array_equal(sa[k], sb[k]), (t, k)
+
+
+@pytest.mark.parametrize("name", ["city", "grid_maxpressure"])
+def test_repartition_invariance(simlib, name):
+    """NEXT-2 dynamic repartitioning: tiles handed to new owners
+    at step boundaries (an explicit scattered partition, then the library's
+    load rebalance) leave every result bit-identical to one partition."""
+    if name == "city":
+        scen = synth.city(G=12, n_vehicles=20000, seed=13)
+    else:
+        scen = synth.grid(rows=4, cols=4, road_len=250.0, lanes=2, n_trips=3000, seed=12,
+                          depart_window=400, policy=synth.POLICY_MAXP)
+    world = 3
+    a = simlib.Sim.from_scenario(scen)
+    b = simlib.Sim.from_scenario(scen, world=world, loopback=True, direct=True)
+    nr = len(scen.graph["road_lane_offsets"]) - 1
+    for sim in (a, b):
+        sim.step(60)
+    assert b.repartition((np.arange(nr) * 7) % world) > 0
+    for sim in (a, b):
+        sim.step(60)
+    b.repartition()
+    assert b.repartition() == 0                    # balanced already: nothing moves
+    for sim in (a, b):
+        sim.step(40)
+    s1, m1 = a.read_state(lane_order=True), a.read_metrics(lane_stats=True)
+    sw, mw = b.read_state(lane_order=True), b.read_metrics(lane_stats=True)
+    for k in KEYS:
+        assert np.array_equal(s1[k], sw[k]), k
+    for k in MKEYS:
+        assert m1[k] == mw[k], (k, m1[k], mw[k])
+    assert np.array_equal(m1["lane_count"], mw["lane_count"])
+
+
+def test_repartition_needs_direct_transport(simlib):
+    scen = synth.grid(rows=2, cols=2, road_len=200.0, lanes=1, n_trips=50, seed=3)
+    g = simlib.Sim.from_scenario(scen, world=2, loopback=True)
+    with pytest.raises(simlib.SimError) as e:
+        g.repartition()
+    assert e.value.status == 1                     # SIM_E_INVALID
