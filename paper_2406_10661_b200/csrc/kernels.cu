@@ -821,10 +821,15 @@ __global__ void k_lane_stats(StepArgs A, int32_t *cnt, int32_t *wt, float *road_
   // Road travelling speed: the tile's road lanes are its road.
   __shared__ int sc[kMaxTileLanes], sw[kMaxTileLanes];
   __shared__ double sv[kMaxTileLanes];
+  __shared__ float slen[kMaxTileLanes];              // lane lengths (read once per lane)
   const int tile = A.tiles[blockIdx.x];
   const int ns = A.cnt_in[tile], ni = A.icnt_in[tile];
   const int l0 = A.tile_lane_off[tile], nl = A.tile_lane_off[tile + 1] - l0;
-  if (threadIdx.x < kMaxTileLanes) { sc[threadIdx.x] = sw[threadIdx.x] = 0; sv[threadIdx.x] = 0.0; }
+  if (threadIdx.x < kMaxTileLanes) {
+    sc[threadIdx.x] = sw[threadIdx.x] = 0;
+    sv[threadIdx.x] = 0.0;
+    if (threadIdx.x < nl) slen[threadIdx.x] = A.lane_len[A.tile_lanes[l0 + threadIdx.x]];
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < ns + ni; i += blockDim.x) {
     float s, v;
@@ -839,7 +844,7 @@ __global__ void k_lane_stats(StepArgs A, int32_t *cnt, int32_t *wt, float *road_
     const int l = m_lane(meta);
     atomicAdd(&sc[l], 1);
     if (road_speed) atomicAdd(&sv[l], (double)v);
-    if (v < A.v_wait && (A.lane_len[A.tile_lanes[l0 + l]] - s) <= zone) atomicAdd(&sw[l], 1);
+    if (v < A.v_wait && (slen[l] - s) <= zone) atomicAdd(&sw[l], 1);
   }
   __syncthreads();
   for (int l = threadIdx.x; l < nl; l += blockDim.x) {
