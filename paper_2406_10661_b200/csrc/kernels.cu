@@ -35,11 +35,6 @@ __device__ __forceinline__ bool key_less(unsigned long long h1, int v1, unsigned
 // fp64 canonical path (exact_mode and guard fallback) kept out of line so the
 // hot fp32 path is register-allocated on its own
 __device__ __forceinline__ void record(const StepArgs &A, int vid, const Res &r, bool guard) {
-  A.r_leader[vid] = r.leader;
-  A.r_hops[vid] = (int8_t)r.hops;
-  A.r_phantom[vid] = (int8_t)r.phantom;
-  A.r_of[vid] = r.of_vid;
-  for (int q = 0; q < 4; ++q) A.r_side[4 * vid + q] = r.side[q];
   A.r_lc[vid] = (int8_t)r.lc;
   A.r_hand[vid] = (int8_t)(r.hand > 127 ? 127 : r.hand);
   A.r_acc[vid] = r.acc;
@@ -82,7 +77,7 @@ __device__ __noinline__ int lower_bound_inbox_global(const InboxRec *inb, const 
 }
 
 struct Acc8 {                        // per-thread counters of one tile
-  long long travel = 0, waitfin = 0, delay = 0;
+  long long delay = 0;               // (travel / wait sums of arrivals go straight to tacc)
   int fin = 0, lc = 0, hand = 0, guard = 0, ovf = 0, ins = 0;
 };
 
@@ -110,7 +105,7 @@ __device__ __noinline__ int emit_peer(const StepArgs &A, const InboxRec &rec, in
 // a vehicle that leaves its slot: lane change / hand-off (kind 2, also every
 // guard-deferred vehicle) or arrival (kind 3)
 __device__ __forceinline__ void emit_moved(const StepArgs &A, const View &C, int i, const Res &r,
-                                           int kind, Acc8 &acc) {
+                                           int kind, Acc8 &acc, int tile) {
   const int vid = C.vid(i);
   acc.lc += r.lc != 0;
   acc.hand += r.hand;
@@ -119,8 +114,12 @@ __device__ __forceinline__ void emit_moved(const StepArgs &A, const View &C, int
     A.arrive_time[vid] = A.t + 1;
     A.wait_fin[vid] = r.wait1;
     acc.fin += 1;
-    acc.travel += (long long)(A.t + 1 - A.insert_time[vid]);
-    acc.waitfin += r.wait1;
+    // int64 sums straight into the tile's accumulators (arrivals are rare; no
+    // 64-bit register state through the update loop)
+    long long *ta = A.tacc + (size_t)tile * kNAcc;
+    atomicAdd(reinterpret_cast<unsigned long long *>(ta + ACC_SUM_TRAVEL),
+              (unsigned long long)(long long)(A.t + 1 - A.insert_time[vid]));
+    atomicAdd(reinterpret_cast<unsigned long long *>(ta + ACC_SUM_WAIT_FIN), (unsigned long long)(long long)r.wait1);
     return;
   }
   const uint32_t meta = C.meta(i);
@@ -469,7 +468,7 @@ __device__ __forceinline__ void tile_update(const StepArgs &A, StepShared &S, co
       A.out.wait[pos] = r.wait1;
       atomicMin(&T.first_out[m_lane(meta)], pos);
     } else if (kind >= 2) {
-      emit_moved(A, C, i, r, kind, acc);
+      emit_moved(A, C, i, r, kind, acc, x.tile);
     }
     run += __popc(ball);
   }
@@ -495,7 +494,7 @@ __device__ __forceinline__ void tile_finish(const StepArgs &A, StepShared &S, co
       g.why = 0;
       veh_update<double, false>(A, T, C, i, r, g);
       if (A.record) record(A, C.vid(i), r, true);
-      emit_moved(A, C, i, r, r.fin ? 3 : 2, acc);
+      emit_moved(A, C, i, r, r.fin ? 3 : 2, acc, tile);
       acc.guard += 1;
     }
   }
@@ -574,22 +573,14 @@ __device__ __forceinline__ void tile_finish(const StepArgs &A, StepShared &S, co
   const unsigned c_hand = __reduce_add_sync(0xffffffffu, (unsigned)acc.hand);
   const unsigned c_guard = __reduce_add_sync(0xffffffffu, (unsigned)acc.guard);
   const unsigned c_ovf = __reduce_add_sync(0xffffffffu, (unsigned)acc.ovf);
-  long long s_travel = acc.travel, s_waitfin = acc.waitfin, s_delay = acc.delay;
-  if (c_fin | c_ins) {
-    for (int o = 16; o > 0; o >>= 1) {
-      s_travel += __shfl_down_sync(0xffffffffu, s_travel, o);
-      s_waitfin += __shfl_down_sync(0xffffffffu, s_waitfin, o);
-      s_delay += __shfl_down_sync(0xffffffffu, s_delay, o);
-    }
+  long long s_delay = acc.delay;
+  if (c_ins) {
+    for (int o = 16; o > 0; o >>= 1) s_delay += __shfl_down_sync(0xffffffffu, s_delay, o);
   }
   if (lane_id == 0) {
     long long *ta = A.tacc + (size_t)tile * kNAcc;
     ta[ACC_VEH_STEPS] += n;
-    if (c_fin) {
-      ta[ACC_FINISHED] += c_fin;
-      ta[ACC_SUM_TRAVEL] += s_travel;
-      ta[ACC_SUM_WAIT_FIN] += s_waitfin;
-    }
+    if (c_fin) ta[ACC_FINISHED] += c_fin;
     if (c_ins) {
       ta[ACC_INSERTED] += c_ins;
       ta[ACC_SUM_DELAY] += s_delay;

@@ -376,8 +376,6 @@ struct Res {
   int lc, hand;
   bool fin;
   int wait1;
-  // recorded decisions
-  int leader, hops, phantom, of_vid, side[4];
 };
 
 __device__ __forceinline__ int upper_bound_s(const View &C, int a, int b, float s) {
@@ -515,8 +513,12 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
   const R L = (R)T.len[l];
   const int lead = (i + 1 < T.seg_end[l]) ? i + 1 : -1;
   const int of = (i > T.seg_start[l]) ? i - 1 : -1;
-  o.of_vid = of >= 0 ? C.vid(of) : -1;
-  o.side[0] = o.side[1] = o.side[2] = o.side[3] = -1;
+  // recorded decisions (test mode) go straight to their arrays, so none of
+  // them stays live in registers through the update
+  if (A.record) {
+    A.r_of[me.vid] = of >= 0 ? C.vid(of) : -1;
+    for (int q = 0; q < 4; ++q) A.r_side[4 * me.vid + q] = -1;
+  }
   const R b_hard = (R)A.b_hard;
   // ---- lane-change eligibility: needs no lane evaluation ----
   const bool dest = me.nxt < 0;
@@ -558,9 +560,11 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
       const int a = T.seg_start[ls], b = T.seg_end[ls];
       const int f = upper_bound_s(C, a, b, C.s(i));
       const int fr = f < b ? f : -1, bk = f > a ? f - 1 : -1;
-      const int vf = fr >= 0 ? C.vid(fr) : -1, vb = bk >= 0 ? C.vid(bk) : -1;
-      if (sd == 0) { f0 = fr; b0 = bk; o.side[0] = vf; o.side[1] = vb; }
-      else { f1 = fr; b1 = bk; o.side[2] = vf; o.side[3] = vb; }
+      if (sd == 0) { f0 = fr; b0 = bk; } else { f1 = fr; b1 = bk; }
+      if (A.record) {
+        A.r_side[4 * me.vid + 2 * sd] = fr >= 0 ? C.vid(fr) : -1;
+        A.r_side[4 * me.vid + 2 * sd + 1] = bk >= 0 ? C.vid(bk) : -1;
+      }
     }
   }
   // ---- MOBIL admissibility of each side, cheapest test first (gap signs,
@@ -663,9 +667,11 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
   }
   // ---- O4-O6 on the current lane ----
   LEv<R> use = eval_lane<R, GUARD>(A, T, C, l, lead, s, v, p, me, g);
-  o.leader = use.leader;
-  o.hops = use.hops;
-  o.phantom = use.phantom;
+  if (A.record) {
+    A.r_leader[me.vid] = use.leader;
+    A.r_hops[me.vid] = (int8_t)use.hops;
+    A.r_phantom[me.vid] = (int8_t)use.phantom;
+  }
   int lc = 0, new_l = l;
   if (adm0 || adm1) {                                    // O7 decision (rare: out of line)
     const SideRes<R> sr = lane_change<R, GUARD>(A, T, C, adm0, adm1, inG, mand, sl0, sl1, f0, f1,
