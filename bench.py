@@ -262,12 +262,13 @@ def run_gpu(args, rank, world, local_rank):
                                          scen.n_lanes / world)
     kstep_avg_s = kstep_ms / 1e3 / args.steps
     achieved = per_launch_bytes / kstep_avg_s / 1e9
-    traffic = None
+    traffic = issue = None
     try:
         with open(NCU_TRAFFIC) as f:
             tr = json.load(f)
         if tr.get("workload") == "C4" and tr.get("n_vehicles") == scen.n_trips:
             traffic = tr.get("dram_bytes_per_launch")
+            issue = tr.get("issue_frac")
     except Exception:
         pass
     # e2e: RL-style loop through the public API with host buffers
@@ -311,7 +312,10 @@ def run_gpu(args, rank, world, local_rank):
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "kernel": "k_step", "kernel_ms_avg": kstep_ms / args.steps,
                      "signal_kernel_ms_avg": ksig_ms / args.steps,
-                     "alg_bytes_per_launch": per_launch_bytes},
+                     "alg_bytes_per_launch": per_launch_bytes,
+                     # k_step is latency / issue bound: warp instructions
+                     # issued / (148 SMs x 4 schedulers x 1965 MHz), from the ncu capture
+                     "issue_frac_ncu": issue},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * nj if host_ctl else 0,
                 "d2h_bytes_per_step": lane_bytes + 8 * 15, "steps": e2e_steps},

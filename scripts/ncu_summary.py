@@ -34,6 +34,15 @@ if traffic_json:
         v = float(v.replace(",", ""))
         return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
     t = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
+    inst = num("smsp__inst_executed.sum")
+    dv, du = d["gpu__time_duration.sum"]
+    dur_s = float(dv.replace(",", "")) * {"ns": 1e-9, "nsecond": 1e-9, "us": 1e-6, "usecond": 1e-6,
+                                          "ms": 1e-3, "msecond": 1e-3}.get(du, 1e-6)
+    # issue ceiling: 148 SMs x 4 schedulers x 1 warp instruction per cycle at 1965 MHz
+    issue_peak = 148 * 4 * 1965e6
     json.dump({"workload": "C4", "n_vehicles": 2000000, "kernel": "k_step",
-               "dram_bytes_per_launch": t, "report": rep}, open(traffic_json, "w"), indent=1)
+               "dram_bytes_per_launch": t, "warp_inst_per_launch": inst,
+               "issue_frac": inst / dur_s / issue_peak,
+               "issue_active_pct": float(d["smsp__issue_active.avg.pct_of_peak_sustained_active"][0]),
+               "report": rep}, open(traffic_json, "w"), indent=1)
 print(open(out_txt).read())
