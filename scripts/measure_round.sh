@@ -1,6 +1,26 @@
 #!/bin/bash
 # All measurement artefacts of a round, on one B200 (run under gpurun):
+#   an ncu --set full capture of one k_step launch (summarised into profiles/
+#   first, so the bench lines carry this build's DRAM traffic / issue fraction),
 #   bench lines (C4 2M, 8M, max pressure, oracle reference arm, batched),
-#   ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv \
+#   the one-GPU transport comparison, the floor / L2 / issue-peak numbers, and
+#   the cold launch list of bench.py.  Outputs land in gpurun_out/; copy the
+#   bench lines into profiles/.
+set -x
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+ncu --set full --clock-control none --import-source on -k regex:k_step -s 20 -c 1 \
+    -o gpurun_out/prof_kstep -f python scripts/time_c4.py > gpurun_out/ncu_full.log 2>&1
+ncu -i gpurun_out/prof_kstep.ncu-rep --page source --csv > gpurun_out/kstep_source.csv 2>/dev/null
+ncu -i gpurun_out/prof_kstep.ncu-rep --page raw --csv > gpurun_out/kstep_raw.csv 2>/dev/null
+python scripts/ncu_summary.py gpurun_out/prof_kstep.ncu-rep profiles/r01_kstep_ncu_full.txt \
+    profiles/ncu_kstep_traffic.json > /dev/null
+python bench.py > gpurun_out/bench.log 2>&1
+python bench.py --scale 4 --steps 50 --no-cpu > gpurun_out/bench_8m.log 2>&1
+python bench.py --policy maxpressure --no-cpu > gpurun_out/bench_mp.log 2>&1
+python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1
+python scripts/bench_batched.py > gpurun_out/bench_batched.log 2>&1
+python scripts/bench_transport.py 8 > gpurun_out/transport.log 2>&1
+python scripts/floor_and_peaks.py > gpurun_out/floor.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv \
     --log-file gpurun_out/launches.csv python bench.py --steps 20 --warmup 3 --no-cpu > gpurun_out/bench_ncu.log 2>&1
-tail -n 2 gpurun_out/bench*.log
+tail -n 2 gpurun_out/bench*.log gpurun_out/floor.log
