@@ -14,10 +14,7 @@ import torch
 import synth
 import paper_2406_10661_b200 as p
 
-cache = "/tmp/c4.npz"
-scen = synth.load_scenario(cache) if os.path.exists(cache) else synth.city()
-if not os.path.exists(cache):
-    synth.save_scenario(scen, cache)
+scen = synth.city()                       # (not the npz cache: the partitioner needs the geometry)
 W = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 own = synth.rcb_partition(scen, W)
 out = {"workload": "C4", "partitions": W}

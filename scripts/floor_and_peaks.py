@@ -2,7 +2,7 @@
   * fixed-cost floor of a step: sim_step(1) on C1 (1 km ring, 20 vehicles),
     device time per step with CUDA events — launches + the persistent step
     kernel's minimum, no bandwidth;
-  * L2-resident copy bandwidth (8 MiB -> 8 MiB, repeated) next to the HBM copy
+  * L2-resident copy bandwidth (24 MiB -> 24 MiB, repeated) next to the HBM copy
     peak of MEASURED_PEAKS.json, to place the 2M-vehicle working set;
   * the issue ceiling used for the k_step issue fraction: 148 SMs x 4 warp
     schedulers x 1 warp-instruction / cycle at the max SM clock.
@@ -30,7 +30,7 @@ sim.step(n)
 e1.record(st)
 torch.cuda.synchronize()
 out["c1_step_floor_us"] = e0.elapsed_time(e1) / n * 1e3
-a = torch.empty(8 << 20, dtype=torch.uint8, device="cuda")
+a = torch.empty(24 << 20, dtype=torch.uint8, device="cuda")
 b = torch.empty_like(a)
 for _ in range(10):
     b.copy_(a)
