@@ -207,15 +207,31 @@ def run_gpu(args, rank, world, local_rank):
     scen = make_workload(world, args.policy, args.scale)
     stream = torch.cuda.Stream(dev)          # the simulation stream (events recorded on it)
     torch.cuda.set_stream(stream)
+    sim = None
     if world > 1 and args.transport == "direct":
         # NEXT-2: k_step stores boundary movers straight into the
         # owner GPU's inbox over NVLink peer memory (CUDA IPC), one device
-        # barrier per step; the handles are all-gathered once here
+        # barrier per step; the handles are all-gathered once here.  If any
+        # rank cannot map its peers, every rank falls back to NCCL p2p.
         import synth
-        sim = p.Sim.from_scenario(scen, device=local_rank, stream=stream.cuda_stream, world=world,
-                                  rank=rank, direct=True,
-                                  road_owner=synth.rcb_partition(scen, world))
-        sim.connect_process_group()
+        from paper_2406_10661_b200.sim import connect_process_group
+        ok = 1
+        try:
+            try:
+                sim = p.Sim.from_scenario(scen, device=local_rank, stream=stream.cuda_stream,
+                                          world=world, rank=rank, direct=True,
+                                          road_owner=synth.rcb_partition(scen, world))
+            finally:
+                connect_process_group(sim, world)
+        except p.SimError as e:
+            print(f"rank {rank}: direct transport unavailable ({e}); falling back to NCCL",
+                  file=sys.stderr, flush=True)
+            ok = 0
+        if _max_over_ranks(1 - ok, dev) > 0:
+            sim = None
+            args.transport = "nccl"
+    if sim is not None:
+        pass
     elif world > 1:
         import synth
         nid = torch.zeros(128, dtype=torch.uint8, device=dev)

@@ -199,6 +199,22 @@ def _batch_arrays(params, keep):
     return out
 
 
+def connect_process_group(sim, world, group=None):
+    """Collective IPC connect for the direct transport; `sim` may be None on a
+    rank whose sim_create failed (it still takes part, and all ranks raise)."""
+    import torch.distributed as dist
+    mine = None
+    try:
+        mine = sim.ipc_export() if sim is not None else None
+    except SimError:
+        pass
+    blobs = [None] * world
+    dist.all_gather_object(blobs, mine, group=group)
+    if any(b is None for b in blobs):
+        raise SimError(6, "direct transport: a rank could not create or export its buffers")
+    sim.ipc_connect(blobs)
+
+
 def get_nccl_unique_id():
     """128-byte NCCL unique id for a partitioned multi-process run."""
     lib = load_library()
@@ -270,11 +286,10 @@ class Sim:
         self._chk(self.lib.sim_ipc_connect(self.h, _ptr(a), n))
 
     def connect_process_group(self, group=None):
-        """All-gather the IPC handles over torch.distributed and connect."""
-        import torch.distributed as dist
-        blobs = [None] * self.world
-        dist.all_gather_object(blobs, self.ipc_export(), group=group)
-        self.ipc_connect(blobs)
+        """All-gather the IPC handles over torch.distributed and connect.
+        Collective: every rank takes part even if its export fails, and then
+        every rank raises."""
+        connect_process_group(self, self.world, group)
 
     def repartition(self, road_owner=None):
         """Hand road tiles to new owners at this step boundary (direct
