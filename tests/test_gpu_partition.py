@@ -136,3 +136,25 @@ def test_repartition_needs_direct_transport(simlib):
     with pytest.raises(simlib.SimError) as e:
         g.repartition()
     assert e.value.status == 1                     # SIM_E_INVALID
+
+
+def test_full_size_c4_direct_partitions(simlib):
+    """BASELINE.json configs[3] at full size (C4, 2M vehicles): 8 partitions
+    (the recursive coordinate bisection bench.py uses) with the direct
+    transport, a load rebalance half way, against one partition — bit for bit."""
+    scen = synth.city()
+    a = simlib.Sim.from_scenario(scen)
+    b = simlib.Sim.from_scenario(scen, world=8, loopback=True, direct=True,
+                                 road_owner=synth.rcb_partition(scen, 8))
+    for sim in (a, b):
+        sim.step(20)
+    assert b.repartition() > 0
+    for sim in (a, b):
+        sim.step(10)
+    s1, sw = a.read_state(), b.read_state()
+    for k in ("status", "lane", "cursor", "wait_steps", "insert_time", "arrive_time", "s", "v"):
+        assert np.array_equal(s1[k], sw[k]), k
+    m1, mw = a.read_metrics(), b.read_metrics()
+    for k in MKEYS:
+        assert m1[k] == mw[k], (k, m1[k], mw[k])
+    assert m1["n_handoffs"] > 50_000
