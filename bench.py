@@ -293,17 +293,25 @@ def run_gpu(args, rank, world, local_rank):
     offs = scen.graph["junc_offset_steps"].astype(np.int64)
     e2e_steps = max(10, min(args.steps, 50))
     lane_bytes = 8 * scen.n_lanes
+    host_ctl = args.policy == "fixed"                     # max pressure runs on the device
+    # host fixed-time controller (C = 102 s: NS 30+3, NS-left 15+3, EW 30+3,
+    # EW-left 15+3, per-junction offsets): the plan is periodic, so the phase
+    # vector of every cycle second is tabulated once
+    tau_phase = np.where(np.arange(102) < 33, 0, np.where(np.arange(102) < 51, 1,
+                         np.where(np.arange(102) < 84, 2, 3))).astype(np.int32)
+    plan = np.ascontiguousarray(tau_phase[(np.arange(102)[:, None] + offs[None, :]) % 102])
+    # observation buffers: page-locked, reused every step (filled by DMA)
+    obs_buf = {k: torch.empty(scen.n_lanes, dtype=torch.int32, pin_memory=True).numpy()
+               for k in ("lane_count", "lane_waiting_at_end")}
     torch.cuda.synchronize()
     me0 = sim.read_metrics()
-    t0 = time.perf_counter()
-    host_ctl = args.policy == "fixed"                     # max pressure runs on the device
+    t0 = time.perf_counter()                              # one-time setup above is outside
     for k in range(e2e_steps):
         if host_ctl:
-            tau = (me0["t"] + k + offs) % 102             # host fixed-time controller
-            ph = np.where(tau < 33, 0, np.where(tau < 51, 1, np.where(tau < 84, 2, 3))).astype(np.int32)
+            ph = plan[(me0["t"] + k) % 102]               # host fixed-time controller
             sim.set_signal_phase_batch(jids, ph)          # H2D: the step's control input
         sim.step(1)
-        obs = sim.read_metrics(lane_stats=True)           # D2H: counters + lane queues
+        obs = sim.read_metrics(lane_stats=True, out=obs_buf)  # D2H: counters + lane queues
     e2e_dt = time.perf_counter() - t0
     e2e_v = obs["vehicle_steps"] - me0["vehicle_steps"]       # global
     e2e_val = e2e_v / e2e_dt

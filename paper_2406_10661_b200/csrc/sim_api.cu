@@ -2147,6 +2147,7 @@ sim_status sim_read_metrics(sim_handle h, sim_metrics *m) {
   for (size_t q = 0; q < h->parts.size(); ++q)
     CK(h, cudaMemcpyAsync(hc + q * (kNAcc + 3), h->parts[q].red_d, (kNAcc + 3) * 8,
                           cudaMemcpyDeviceToHost, h->stream));
+  bool lane_direct[3] = {false, false, false};
   if (lanes) {
     Part &P0 = h->parts[0];
     int32_t *d = P0.lanestat_d;
@@ -2164,7 +2165,20 @@ sim_status sim_read_metrics(sim_handle h, sim_metrics *m) {
       if (!st && rs) st = allreduce_sum(h, 1, 2, 2 * (int64_t)h->nl, h->nr);
       if (st) return st;
     }
-    CK(h, cudaMemcpyAsync(hl, d, (2 * (size_t)h->nl + h->nr) * 4, cudaMemcpyDeviceToHost, h->stream));
+    // each lane array straight into the caller's buffer when that is pinned
+    // host memory (no staging copy), else through the pinned staging buffer
+    void *dst[3] = {m->lane_count, m->lane_waiting_at_end, m->road_avg_speed};
+    const size_t off[3] = {0, (size_t)h->nl, 2 * (size_t)h->nl};
+    const size_t cnt[3] = {(size_t)h->nl, (size_t)h->nl, (size_t)h->nr};
+    for (int q = 0; q < 3; ++q) {
+      if (!dst[q]) continue;
+      cudaPointerAttributes pa{};
+      const bool pinned = cudaPointerGetAttributes(&pa, dst[q]) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+      if (!pinned) cudaGetLastError();            // clear a possible "invalid value" from the query
+      CK(h, cudaMemcpyAsync(pinned ? dst[q] : (void *)(hl + off[q]), d + off[q], cnt[q] * 4,
+                            cudaMemcpyDeviceToHost, h->stream));
+      lane_direct[q] = pinned;                    // done: no staging copy below
+    }
   }
   st = device_check(h);
   if (st) return st;
@@ -2188,9 +2202,9 @@ sim_status sim_read_metrics(sim_handle h, sim_metrics *m) {
   m->n_inserted = c[ACC_INSERTED];
   m->n_guard_hits = c[ACC_GUARD];
   m->att_finished = c[ACC_FINISHED] ? (double)c[ACC_SUM_TRAVEL] / (double)c[ACC_FINISHED] : 0.0;
-  if (m->lane_count) std::memcpy(m->lane_count, hl, h->nl * 4);
-  if (m->lane_waiting_at_end) std::memcpy(m->lane_waiting_at_end, hl + h->nl, h->nl * 4);
-  if (m->road_avg_speed) std::memcpy(m->road_avg_speed, hl + 2 * (size_t)h->nl, h->nr * 4);
+  if (m->lane_count && !lane_direct[0]) std::memcpy(m->lane_count, hl, h->nl * 4);
+  if (m->lane_waiting_at_end && !lane_direct[1]) std::memcpy(m->lane_waiting_at_end, hl + h->nl, h->nl * 4);
+  if (m->road_avg_speed && !lane_direct[2]) std::memcpy(m->road_avg_speed, hl + 2 * (size_t)h->nl, h->nr * 4);
   return SIM_OK;
 }
 

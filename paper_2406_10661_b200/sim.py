@@ -374,16 +374,29 @@ class Sim:
         b["side_vid"] = b["side_vid"].reshape(n, 4)
         return b
 
-    def read_metrics(self, lane_stats=False, road_speed=False):
+    def read_metrics(self, lane_stats=False, road_speed=False, out=None):
+        """Global counters (+ per-lane queue statistics / road speeds).  `out`
+        (optional dict: lane_count, lane_waiting_at_end, road_avg_speed) gives
+        caller-owned arrays to fill instead of fresh ones; page-locked arrays
+        (e.g. torch.empty(..., pin_memory=True).numpy()) are filled by DMA."""
         m = sim_metrics()
+        out = out or {}
+
+        def buf(name, n, dt):
+            a = out.get(name)
+            if a is None:
+                return np.zeros(n, dt)
+            assert a.dtype == dt and a.shape == (n,) and a.flags.c_contiguous, name
+            return a
         bufs = None
         if lane_stats:
-            bufs = (np.zeros(self.n_lanes, np.int32), np.zeros(self.n_lanes, np.int32))
+            bufs = (buf("lane_count", self.n_lanes, np.int32),
+                    buf("lane_waiting_at_end", self.n_lanes, np.int32))
             m.lane_count = _ptr(bufs[0])
             m.lane_waiting_at_end = _ptr(bufs[1])
         rs = None
         if road_speed:
-            rs = np.zeros(self.n_roads, np.float32)
+            rs = buf("road_avg_speed", self.n_roads, np.float32)
             m.road_avg_speed = _ptr(rs)
         self._chk(self.lib.sim_read_metrics(self.h, C.byref(m)))
         out = {n: getattr(m, n) for n, _ in sim_metrics._fields_[:-3]}
