@@ -805,31 +805,38 @@ __global__ void k_reduce_groups(const long long *tacc, const int32_t *tiles, int
   }
 }
 
-__global__ void k_lane_stats(StepArgs A, int32_t *cnt, int32_t *wt, float *road_speed, float zone) {
+__global__ void __launch_bounds__(128) k_lane_stats(StepArgs A, int32_t *cnt, int32_t *wt,
+                                                   float *road_speed, float zone) {
   // lane queue length: per lane, vehicles and those with v < v_wait
   // within the last `zone` metres, over stayers + inbox of each own
   // tile; a lane belongs to one tile, so its totals are written, not added.
   // Road travelling speed: the tile's road lanes are its road.
-  __shared__ int sc[kMaxTileLanes], sw[kMaxTileLanes];
-  __shared__ double sv[kMaxTileLanes];
-  __shared__ float slen[kMaxTileLanes];              // lane lengths (read once per lane)
-  const int tile = A.tiles[blockIdx.x];
+  // One warp per tile (tiles hold ~100 vehicles), four tiles per block.
+  __shared__ int sc_[4][kMaxTileLanes], sw_[4][kMaxTileLanes];
+  __shared__ double sv_[4][kMaxTileLanes];
+  __shared__ float slen_[4][kMaxTileLanes];          // lane lengths (read once per lane)
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int idx = blockIdx.x * 4 + w;
+  if (idx >= A.n_own) return;
+  int *sc = sc_[w], *sw = sw_[w];
+  double *sv = sv_[w];
+  float *slen = slen_[w];
+  const int tile = A.tiles[idx];
   const int ns = A.cnt_in[tile], ni = A.icnt_in[tile];
   const int l0 = A.tile_lane_off[tile], nl = A.tile_lane_off[tile + 1] - l0;
-  if (threadIdx.x < kMaxTileLanes) {
-    sc[threadIdx.x] = sw[threadIdx.x] = 0;
-    sv[threadIdx.x] = 0.0;
-    if (threadIdx.x < nl) slen[threadIdx.x] = A.lane_len[A.tile_lanes[l0 + threadIdx.x]];
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < ns + ni; i += blockDim.x) {
+  sc[lane] = sw[lane] = 0;
+  sv[lane] = 0.0;
+  if (lane < nl) slen[lane] = A.lane_len[A.tile_lanes[l0 + lane]];
+  __syncwarp();
+  const int base = A.tile_base[tile], ibase = A.tile_ibase[tile];
+  for (int i = lane; i < ns + ni; i += 32) {
     float s, v;
     uint32_t meta;
     if (i < ns) {
-      const int gi = A.tile_base[tile] + i;
+      const int gi = base + i;
       s = A.in.s[gi]; v = A.in.v[gi]; meta = A.in.meta[gi];
     } else {
-      const InboxRec r = A.inbox_in[A.tile_ibase[tile] + i - ns];
+      const InboxRec r = A.inbox_in[ibase + i - ns];
       s = r.s; v = r.v; meta = r.meta;
     }
     const int l = m_lane(meta);
@@ -837,13 +844,13 @@ __global__ void k_lane_stats(StepArgs A, int32_t *cnt, int32_t *wt, float *road_
     if (road_speed) atomicAdd(&sv[l], (double)v);
     if (v < A.v_wait && (slen[l] - s) <= zone) atomicAdd(&sw[l], 1);
   }
-  __syncthreads();
-  for (int l = threadIdx.x; l < nl; l += blockDim.x) {
-    const int g = A.tile_lanes[l0 + l];
-    cnt[g] = sc[l];
-    wt[g] = sw[l];
+  __syncwarp();
+  if (lane < nl) {
+    const int g = A.tile_lanes[l0 + lane];
+    cnt[g] = sc[lane];
+    wt[g] = sw[lane];
   }
-  if (road_speed && threadIdx.x == 0) {            // lanes [0, nroad) are the road's
+  if (road_speed && lane == 0) {                    // lanes [0, nroad) are the road's
     const int nroad = A.tile_nroad[tile];
     double sum = 0.0;
     int c = 0;
@@ -1089,7 +1096,7 @@ void launch_reduce_acc(const long long *tacc, int n_tiles, const int32_t *cnt,
 void launch_lane_stats(const StepArgs &a, int32_t *lane_count, int32_t *lane_wait,
                        float *road_speed, float zone, void *stream) {
   if (a.n_own > 0)
-    k_lane_stats<<<a.n_own, 128, 0, (cudaStream_t)stream>>>(a, lane_count, lane_wait, road_speed, zone);
+    k_lane_stats<<<(a.n_own + 3) / 4, 128, 0, (cudaStream_t)stream>>>(a, lane_count, lane_wait, road_speed, zone);
 }
 
 void launch_reduce_groups(const long long *tacc, const int32_t *tiles, int n_own,
