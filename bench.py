@@ -115,7 +115,7 @@ def workload_config(scen, extra=None, policy="fixed"):
     G = int(np.sqrt(len(scen.graph["junc_lane_offsets"]) - 1))
     sig = "fixed-time signals" if policy == "fixed" else "max-pressure signals (period 30 s)"
     cfg = {"workload": f"C4 city-like synthetic network (SURVEY 8(d)): G={G} perturbed grid, "
-                       f"{scen.n_trips / 1e6:.0f}M vehicles on the network at t=0, {sig}",
+                       f"{scen.n_trips / 1e6:.3g}M vehicles on the network at t=0, {sig}",
            "n_vehicles": int(scen.n_trips), "n_lanes": int(scen.n_lanes),
            "n_junctions": int(len(scen.graph["junc_lane_offsets"]) - 1),
            "n_roads": int(len(scen.graph["road_lane_offsets"]) - 1),
@@ -147,7 +147,7 @@ def cpu_baseline(scen, budget_s=20.0, max_steps=10):
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    scen = make_workload(1, args.policy)
+    scen = make_workload(1, args.policy, args.scale)
     import oracle
     oracle.build()
     o = oracle.Oracle(scen)
