@@ -21,7 +21,8 @@
  *     (SIM_E_STATE afterwards);
  *   - setters take effect at the next step boundary (stream-ordered);
  *     _batch variants equal the single calls applied in order;
- *   - one controlling host thread per handle.
+ *   - one controlling host thread per handle; every call makes the handle's
+ *     device (params.device) current on the calling thread.
  */
 #ifndef SIM_H
 #define SIM_H

@@ -1109,6 +1109,9 @@ StepArgs step_args(const Part &P, int t) {
 sim_status check(sim_s *h) {
   if (!h || !is_live(h)) return fail(nullptr, SIM_E_STATE, "null or destroyed handle");
   if (h->sticky) return fail(h, SIM_E_STATE, "handle is in a sticky error state: " + h->err);
+  // every call works on the handle's device (allocations, launches, IPC
+  // mappings), whatever device the calling thread had current
+  if (cudaSetDevice(h->device) != cudaSuccess) return fail(h, SIM_E_CUDA, "cudaSetDevice failed");
   return SIM_OK;
 }
 
