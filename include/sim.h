@@ -204,8 +204,9 @@ sim_status sim_create(const sim_graph *g, const sim_trips *trips,
  * of all ranks concatenated in rank order (world x n_bytes; this rank's entry
  * is ignored) and maps the peers' buffers; SIM_E_CUDA if a mapping fails.
  * Until it succeeds sim_step and the reads fail with SIM_E_STATE.  A device
- * barrier that waits > 60 s for a peer makes the handle sticky (SIM_E_STATE
- * at the next synchronising call) instead of hanging. */
+ * barrier that waits longer than 60 s (environment SIM_BARRIER_TIMEOUT_MS at
+ * create) for a peer makes the handle sticky (SIM_E_STATE at the next
+ * synchronising call) instead of hanging. */
 sim_status sim_ipc_export(sim_handle h, uint8_t *out, int32_t cap, int32_t *n_bytes);
 sim_status sim_ipc_connect(sim_handle h, const uint8_t *blobs, int32_t n_bytes);
 

@@ -227,7 +227,7 @@ void launch_mig_header(MigRec *out_buf, const int32_t *out_off, const int32_t *o
 void launch_absorb(const StepArgs &a, const MigRec *in_buf, const int32_t *in_off,
                    const int32_t *in_cap, int world, void *stream);
 void launch_barrier(const PeerView *peers, int world, int rank, unsigned target, int32_t *err,
-                    void *stream);
+                    unsigned long long timeout_ns, void *stream);
 void launch_peer_sum(const PeerView *peers, int world, int kind, int dtype, int64_t off, int64_t n,
                      void *out, void *stream);
 void launch_rehome(const StepArgs &a, const int32_t *new_owner, void *stream);

@@ -929,8 +929,9 @@ __global__ void k_halo_unpack(StepArgs A, const int32_t *lanes, const HaloRec *b
 // Barrier over the partitions of a multi-process run: one arrival per peer
 // (system-scope release after everything this stream did before), then wait
 // until all `world` arrivals of this round have reached our counter.  A wait
-// that exceeds 60 s (a peer died) sets *err and returns instead of hanging.
-__global__ void k_barrier(const PeerView *peers, int world, int rank, unsigned target, int32_t *err) {
+// longer than timeout_ns (a peer died) sets *err and returns instead of hanging.
+__global__ void k_barrier(const PeerView *peers, int world, int rank, unsigned target, int32_t *err,
+                          unsigned long long timeout_ns) {
   const int q = threadIdx.x;
   if (q < world) {
     __threadfence_system();
@@ -945,7 +946,7 @@ __global__ void k_barrier(const PeerView *peers, int world, int rank, unsigned t
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
       if ((int)(v - target) >= 0) break;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-      if (now - t0 > 60000000000ull) { atomicExch(err, 1); break; }
+      if (now - t0 > timeout_ns) { atomicExch(err, 1); break; }
       __nanosleep(200);
     }
     __threadfence_system();
@@ -1042,8 +1043,8 @@ void launch_tile_counts(const StepArgs &a, int32_t *out, void *stream) {
 }
 
 void launch_barrier(const PeerView *peers, int world, int rank, unsigned target, int32_t *err,
-                    void *stream) {
-  k_barrier<<<1, 32, 0, (cudaStream_t)stream>>>(peers, world, rank, target, err);
+                    unsigned long long timeout_ns, void *stream) {
+  k_barrier<<<1, 32, 0, (cudaStream_t)stream>>>(peers, world, rank, target, err, timeout_ns);
 }
 void launch_peer_sum(const PeerView *peers, int world, int kind, int dtype, int64_t off, int64_t n,
                      void *out, void *stream) {

@@ -18,6 +18,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -166,6 +167,7 @@ struct sim_s {
   bool ipc = false;                             // direct across processes (CUDA IPC mappings)
   bool connected = false;                       // ipc: sim_ipc_connect done
   unsigned bar_epoch = 0;                       // ipc: barriers passed
+  unsigned long long bar_timeout_ns = 60000000000ull;  // ipc: SIM_BARRIER_TIMEOUT_MS (default 60 s)
   int32_t *bar_err_d = nullptr;                 // ipc: set by a barrier that timed out
   void *ipc_tmp = nullptr;                      // ipc: reduction result buffer
   std::vector<void *> ipc_opened;               // ipc: peer mappings to close
@@ -1153,6 +1155,10 @@ sim_status setup_direct(sim_s *h) {
     for (Part &P : h->parts) v.push_back(P.view);
     return upload_peers(h, v);
   }
+  if (const char *e = std::getenv("SIM_BARRIER_TIMEOUT_MS")) {
+    const long long ms = std::atoll(e);
+    if (ms > 0) h->bar_timeout_ns = (unsigned long long)ms * 1000000ull;
+  }
   sim_status st = dalloc(h, &h->bar_err_d, 1);
   if (st) return st;
   CK(h, cudaMemset(h->bar_err_d, 0, 4));
@@ -1176,7 +1182,7 @@ sim_status barrier(sim_s *h) {
   if (!h->connected) return fail(h, SIM_E_STATE, "direct transport: sim_ipc_connect has not been called");
   h->bar_epoch += 1;
   launch_barrier(h->parts[0].peers_d, h->world, h->rank, h->bar_epoch * (unsigned)h->world,
-                 h->bar_err_d, h->stream);
+                 h->bar_err_d, h->bar_timeout_ns, h->stream);
   h->n_launch++;
   return SIM_OK;
 }

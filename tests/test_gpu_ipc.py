@@ -88,3 +88,46 @@ def test_multi_process_direct_transport(name, world):
         for r in rs:
             assert np.array_equal(r[k], s1[k]), k
     assert m1["n_handoffs"] > 0
+
+
+def _stall_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["SIM_BARRIER_TIMEOUT_MS"] = "2000"
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2406_10661_b200 as p
+    scen = synth.grid(rows=3, cols=3, road_len=200.0, lanes=2, n_trips=500, seed=5)
+    g = p.Sim.from_scenario(scen, world=world, rank=rank, direct=True, device=0)
+    g.connect_process_group()
+    result = "none"
+    if rank == 0:                                    # rank 1 never steps
+        g.step(1)
+        try:
+            g.sync()
+            result = "no error"
+        except p.SimError as e:
+            result = f"{e.status}:{e}"
+        try:
+            g.step(1)                                # the handle stays sticky
+            result += "|stepped"
+        except p.SimError as e:
+            result += f"|{e.status}"
+        with open(os.path.join(out_dir, "r0.txt"), "w") as f:
+            f.write(result)
+    dist.barrier()                                   # rank 1 keeps its buffers mapped until here
+    dist.destroy_process_group()
+
+
+def test_peer_that_stops_stepping_does_not_hang():
+    """A rank whose peer never reaches the barrier gets a sticky SIM_E_STATE
+    after the barrier timeout instead of a hung GPU."""
+    import torch.multiprocessing as mp
+    import paper_2406_10661_b200 as p
+    p.build()
+    with tempfile.TemporaryDirectory() as d:
+        mp.start_processes(_stall_worker, args=(2, _free_port(), d), nprocs=2, join=True,
+                           start_method="spawn")
+        res = open(os.path.join(d, "r0.txt")).read()
+    assert res.startswith("6:") and "barrier timed out" in res, res
+    assert res.endswith("|6"), res
