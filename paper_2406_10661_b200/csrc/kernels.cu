@@ -76,6 +76,11 @@ __device__ __noinline__ int lower_bound_inbox_global(const InboxRec *inb, const 
   return lo;
 }
 
+// fire-and-forget 64-bit add (RED: no load round trip at the end of a tile)
+__device__ __forceinline__ void red_add(long long *p, long long v) {
+  atomicAdd(reinterpret_cast<unsigned long long *>(p), (unsigned long long)v);
+}
+
 struct Acc8 {                        // per-thread counters of one tile
   long long delay = 0;               // (travel / wait sums of arrivals go straight to tacc)
   int fin = 0, lc = 0, hand = 0, guard = 0, ovf = 0, ins = 0;
@@ -579,16 +584,16 @@ __device__ __forceinline__ void tile_finish(const StepArgs &A, StepShared &S, co
   }
   if (lane_id == 0) {
     long long *ta = A.tacc + (size_t)tile * kNAcc;
-    ta[ACC_VEH_STEPS] += n;
-    if (c_fin) ta[ACC_FINISHED] += c_fin;
+    red_add(ta + ACC_VEH_STEPS, n);
+    if (c_fin) red_add(ta + ACC_FINISHED, c_fin);
     if (c_ins) {
-      ta[ACC_INSERTED] += c_ins;
-      ta[ACC_SUM_DELAY] += s_delay;
+      red_add(ta + ACC_INSERTED, c_ins);
+      red_add(ta + ACC_SUM_DELAY, s_delay);
     }
-    if (c_lc) ta[ACC_LANE_CHANGES] += c_lc;
-    if (c_hand) ta[ACC_HANDOFFS] += c_hand;
-    if (c_guard) ta[ACC_GUARD] += c_guard;
-    if (c_ovf) ta[ACC_OVERFLOW] += c_ovf;
+    if (c_lc) red_add(ta + ACC_LANE_CHANGES, c_lc);
+    if (c_hand) red_add(ta + ACC_HANDOFFS, c_hand);
+    if (c_guard) red_add(ta + ACC_GUARD, c_guard);
+    if (c_ovf) red_add(ta + ACC_OVERFLOW, c_ovf);
     A.cnt_out[tile] = run;
     A.icnt_in[tile] = 0;
   }
