@@ -196,14 +196,28 @@ __device__ __forceinline__ void tile_load(const StepArgs &A, StepShared &S, unsi
   // ids / lengths / speed limits / usable flags and every road-lane successor
   // with its target road, exit lane and the exit lane's reachable roads.
   const int tile = x.tile;
-  const int doff = A.desc_off[tile];
+  const int doff = A.desc_off[tile], dend = A.desc_off[tile + 1];
   const int n_st = A.cnt_in[tile];
   const int n_in = A.icnt_in[tile];
   const int n = n_st + n_in;
   const int base = A.tile_base[tile];
   const int ibase = A.tile_ibase[tile];
+  // lane counts from the static tile tables (same load wave as the offsets),
+  // so every descriptor word below is addressed without waiting for it
+  const int nl = A.tile_lane_off[tile + 1] - A.tile_lane_off[tile], nroad = A.tile_nroad[tile];
   const int *W = A.desc + doff;                     // read straight from global (L2)
-  const int nl = W[0], nroad = W[1], ne = W[2];
+  int ew[8];                                        // successor entry of this lane (if any)
+  {
+    const int eo = 4 + 4 * nl + 6 * nroad + 8 * lane_id;
+    if (doff + eo + 8 <= dend) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) ew[q] = W[eo + q];
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) ew[q] = 0;
+    }
+  }
+  const int ne = W[2];
   // lane records, the per-road-lane group tables and the (host-sorted) usable
   // successors go straight into the tile's shared metadata; only the stop bit
   // (signal of the junction lane at t) is computed here
@@ -245,13 +259,12 @@ __device__ __forceinline__ void tile_load(const StepArgs &A, StepShared &S, unsi
     }
   }
   if (lane_id < ne) {
-    const int *w = W + 4 + 4 * nl + 6 * nroad + 8 * lane_id;
-    const int fl = w[3];
+    const int fl = ew[3];
     SuccEnt e;
-    e.j = w[0];
-    e.troad = w[1];
-    e.b = w[2];
-    e.outr = make_int4(w[4], w[5], w[6], w[7]);
+    e.j = ew[0];
+    e.troad = ew[1];
+    e.b = ew[2];
+    e.outr = make_int4(ew[4], ew[5], ew[6], ew[7]);
     e.stop = ((fl & 1) && A.lane_sig[e.j] != SIG_GREEN) ? 1 : 0;
     T.se[(fl >> 8) & 0xff][fl >> 16] = e;
   }
