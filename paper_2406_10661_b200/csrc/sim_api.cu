@@ -1397,6 +1397,37 @@ sim_status rebuild_counts(sim_s *h) {
 sim_status push_junction_requests(sim_s *h, int m, const int32_t *junctions, const int32_t *vals,
                                   int kind) {
   sim_status st;
+  // fast path: strictly increasing junction ids (every junction once, e.g. a
+  // whole-network controller) need no de-duplication and go straight to the
+  // pinned staging buffer
+  bool uniq = true;
+  for (int i = 1; i < m && uniq; ++i) uniq = junctions[i - 1] < junctions[i];
+  if (uniq) {
+    if (h->stage_cap < 2 * m) {
+      if (h->stage_d) { CK(h, cudaStreamSynchronize(h->stream)); cudaFree(h->stage_d); }
+      CK(h, cudaMalloc(&h->stage_d, 2 * (size_t)m * 4));
+      h->stage_cap = 2 * m;
+    }
+    const size_t bytes = 2 * (size_t)m * 4;
+    if (h->pinned_cap < bytes) {
+      if (h->pinned) { CK(h, cudaEventSynchronize(h->stage_ev)); cudaFreeHost(h->pinned); }
+      h->pinned = nullptr;
+      CK(h, cudaHostAlloc(&h->pinned, bytes, cudaHostAllocDefault));
+      h->pinned_cap = bytes;
+    } else {
+      CK(h, cudaEventSynchronize(h->stage_ev));
+    }
+    std::memcpy(h->pinned, junctions, (size_t)m * 4);
+    std::memcpy(reinterpret_cast<int32_t *>(h->pinned) + m, vals, (size_t)m * 4);
+    CK(h, cudaMemcpyAsync(h->stage_d, h->pinned, bytes, cudaMemcpyHostToDevice, h->stream));
+    CK(h, cudaEventRecord(h->stage_ev, h->stream));
+    for (Part &P : h->parts) {
+      int32_t *dst = kind == 0 ? P.SG.request : (kind == 1 ? P.SG.pol_request : P.SG.dur_request);
+      launch_apply_requests(dst, P.SG.policy, h->stage_d, h->stage_d + m, m, h->stream);
+      h->n_launch++;
+    }
+    return SIM_OK;
+  }
   h->req_mark.resize(h->nj, -1);
   std::vector<int32_t> buf(2 * (size_t)m);
   int u = 0;

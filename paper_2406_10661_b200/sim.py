@@ -133,7 +133,7 @@ def load_library(path=LIB):
 
 
 def _ptr(a):
-    return a.ctypes.data_as(C.c_void_p)
+    return C.c_void_p(a.ctypes.data)        # (data_as is ~2x slower on the per-step path)
 
 
 _GRAPH_DT = dict(lane_length=np.float32, lane_max_speed=np.float32, lane_road=np.int32,
