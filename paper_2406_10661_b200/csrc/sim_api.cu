@@ -125,6 +125,7 @@ struct Part {
   PeerView view{};
   unsigned int *bar_d = nullptr;
   PeerView *peers_d = nullptr;
+  int32_t *tiles_cap_d = nullptr;               // sim_repartition: own-tile list (capacity n_tiles)
 };
 
 struct sim_s {
@@ -171,6 +172,7 @@ struct sim_s {
   int32_t *bar_err_d = nullptr;                 // ipc: set by a barrier that timed out
   void *ipc_tmp = nullptr;                      // ipc: reduction result buffer
   std::vector<void *> ipc_opened;               // ipc: peer mappings to close
+  int32_t *repart_own_d = nullptr;              // sim_repartition: new owners (device)
   std::vector<int> tile_owner;
   NcclComm comm = nullptr;
   std::vector<Part> parts;
@@ -1570,9 +1572,11 @@ sim_status sim_repartition(sim_handle h, const int32_t *road_owner, int32_t *mov
   if (!moved) return SIM_OK;
   st = barrier(h);                                  // every rank is at the same step boundary
   if (st) return st;
-  int32_t *own_d = nullptr;
-  st = dalloc(h, &own_d, (size_t)nt);
-  if (st) return st;
+  if (!h->repart_own_d) {                           // allocated once, reused by later calls
+    st = dalloc(h, &h->repart_own_d, (size_t)nt);
+    if (st) return st;
+  }
+  int32_t *own_d = h->repart_own_d;
   CK(h, cudaMemcpyAsync(own_d, own.data(), nt * 4, cudaMemcpyHostToDevice, h->stream));
   for (Part &P : h->parts) {
     launch_rehome(step_args(P, t), own_d, h->stream);
@@ -1587,9 +1591,11 @@ sim_status sim_repartition(sim_handle h, const int32_t *road_owner, int32_t *mov
     std::vector<int> order(P.tiles);
     std::stable_sort(order.begin(), order.end(),
                      [&](int a, int b) { return h->tile_cap[a] > h->tile_cap[b]; });
-    int32_t *tl = nullptr;
-    st = dalloc(h, &tl, order.size());
-    if (st) return st;
+    if (!P.tiles_cap_d) {                           // own-tile list with room for every tile
+      st = dalloc(h, &P.tiles_cap_d, (size_t)nt);
+      if (st) return st;
+    }
+    int32_t *tl = P.tiles_cap_d;
     if (!order.empty())
       CK(h, cudaMemcpyAsync(tl, order.data(), order.size() * 4, cudaMemcpyHostToDevice, h->stream));
     CK(h, cudaMemcpyAsync(const_cast<int32_t *>(P.A.tile_owner), own_d, nt * 4,
