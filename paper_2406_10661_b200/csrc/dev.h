@@ -100,7 +100,8 @@ struct PeerView {                   // pointers only (exported as an array of ha
   Slab slab[2];                     // stayers, cnt and pending-queue heads: moved when a
   int32_t *cnt[2];                  // tile changes owner (sim_repartition)
   int32_t *pend_head;
-  void *xbuf[3];                    // read-side reduction buffers: counters, lane statistics, group metrics
+  void *xbuf[4];                    // reduction buffers: counters, lane statistics, group metrics,
+                                    // host-call exchange (set_vehicle_route: where each vehicle is)
 };
 
 

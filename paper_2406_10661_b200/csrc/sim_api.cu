@@ -126,6 +126,7 @@ struct Part {
   unsigned int *bar_d = nullptr;
   PeerView *peers_d = nullptr;
   int32_t *tiles_cap_d = nullptr;               // sim_repartition: own-tile list (capacity n_tiles)
+  int32_t *xch_d = nullptr;                     // multi-process: host-call exchange, 3 x n_veh
 };
 
 struct sim_s {
@@ -997,6 +998,7 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   CK(h, cudaMemset(A.tacc, 0, (size_t)nt * kNAcc * 8));
   AL(P.red_d, kNAcc + 3);
   AL(P.lanestat_d, 2 * (size_t)nl + h->nr);           // lane counts, waiting, road speeds
+  if (h->world > 1 && !h->loopback) AL(P.xch_d, 3 * (size_t)nv + 8);   // one process per rank
   if (h->P.record_decisions) {
     AL(A.r_leader, nv); AL(A.r_of, nv); AL(A.r_side, 4 * (size_t)nv);
     AL(A.r_hops, nv); AL(A.r_phantom, nv); AL(A.r_lc, nv); AL(A.r_hand, nv);
@@ -1084,6 +1086,7 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   V.xbuf[0] = P.red_d;
   V.xbuf[1] = P.lanestat_d;
   V.xbuf[2] = P.grp_d;
+  V.xbuf[3] = P.xch_d;
   return SIM_OK;
 #undef AL
 #undef UP
@@ -1933,6 +1936,28 @@ sim_status sim_set_vehicle_route_batch(sim_handle h, int32_t m, const int32_t *v
   cudaFree(d_vid);
   cudaFree(dst8);
   if (st) return st;
+  if (h->comm || h->ipc) {
+    // one process per rank: a vehicle is located by the rank that owns its
+    // tile and may have finished on any rank — sum (position + 1, finished)
+    // over the ranks so that every rank validates and applies identically
+    std::vector<int32_t> x(3 * (size_t)u, 0);
+    for (int q = 0; q < u; ++q) {
+      if (loc[2 * q] >= 0) { x[2 * q] = loc[2 * q] + 1; x[2 * q + 1] = loc[2 * q + 1] + 1; }
+      x[2 * (size_t)u + q] = stt[q] == ST_FINISHED;
+    }
+    Part &P0 = h->parts[0];
+    CK(h, cudaMemcpyAsync(P0.xch_d, x.data(), x.size() * 4, cudaMemcpyHostToDevice, h->stream));
+    st = allreduce_sum(h, 3, 1, 0, 3 * (int64_t)u);
+    if (st) return st;
+    CK(h, cudaMemcpyAsync(x.data(), P0.xch_d, x.size() * 4, cudaMemcpyDeviceToHost, h->stream));
+    st = device_check(h);
+    if (st) return st;
+    for (int q = 0; q < u; ++q) {
+      loc[2 * q] = x[2 * q] - 1;
+      loc[2 * q + 1] = x[2 * q + 1] - 1;
+      stt[q] = x[2 * (size_t)u + q] ? ST_FINISHED : ST_PENDING;
+    }
+  }
   // validation against the current position (L46); nothing changes on failure
   std::vector<int32_t> drv;                          // DRIVING vehicles of the batch
   for (int q = 0; q < u; ++q) {

@@ -131,3 +131,58 @@ def test_peer_that_stops_stepping_does_not_hang():
         res = open(os.path.join(d, "r0.txt")).read()
     assert res.startswith("6:") and "barrier timed out" in res, res
     assert res.endswith("|6"), res
+
+
+def _route_worker(rank, world, port, out_dir):
+    import json as _json
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2406_10661_b200 as p
+    scen = _scen("grid_maxpressure")
+    req = _json.load(open(os.path.join(out_dir, "req.json")))
+    g = p.Sim.from_scenario(scen, world=world, rank=rank, direct=True, device=0)
+    g.connect_process_group()
+    g.step(40)
+    g.set_vehicle_route_batch(req["vids"], req["routes"], req["end_s"])   # SPMD, same batch
+    g.step(40)
+    st = g.read_state()
+    np.savez(os.path.join(out_dir, f"r{rank}.npz"), **{k: np.asarray(v) for k, v in st.items()})
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_multi_process_set_vehicle_route():
+    """NEXT-4's set_vehicle_route across processes: a vehicle is located by
+    the rank that owns it (sum of the ranks' answers), so every rank validates
+    and applies the batch identically; the result equals one partition."""
+    import json as _json
+    import torch.multiprocessing as mp
+    import paper_2406_10661_b200 as p
+    from test_controllables import _reroutes
+    p.build()
+    scen = _scen("grid_maxpressure")
+    ref = p.Sim.from_scenario(scen)
+    ref.step(40)
+    req = _reroutes(scen, ref.read_state(), np.random.default_rng(3))
+    assert any(True for _ in req)
+    vids, routes, ends = [k for k, _, _ in req], [r for _, r, _ in req], [e for _, _, e in req]
+    ref.set_vehicle_route_batch(vids, routes, ends)
+    ref.step(40)
+    s1 = ref.read_state()
+    world = 2
+    with tempfile.TemporaryDirectory() as d:
+        _json.dump({"vids": vids, "routes": [list(map(int, r)) for r in routes], "end_s": ends},
+                   open(os.path.join(d, "req.json"), "w"))
+        mp.start_processes(_route_worker, args=(world, _free_port(), d), nprocs=world,
+                           join=True, start_method="spawn")
+        rs = [dict(np.load(os.path.join(d, f"r{r}.npz"))) for r in range(world)]
+    drv = np.stack([r["status"] == 1 for r in rs])
+    assert np.array_equal(drv.any(0), s1["status"] == 1)
+    for k in ("lane", "cursor", "s", "v"):
+        u = np.zeros_like(s1[k])
+        for q, r in enumerate(rs):
+            u[drv[q]] = r[k][drv[q]]
+        m = s1["status"] == 1
+        assert np.array_equal(u[m], s1[k][m]), k
