@@ -287,8 +287,16 @@ sim_status sim_set_vehicle_route_batch(sim_handle h, int32_t m, const int32_t *v
                                        const int32_t *route_offsets, const int32_t *roads,
                                        const float *end_s);
 sim_status sim_query_sizes(sim_handle h, sim_sizes *out);
-/* Synchronising reads into caller-owned host buffers. */
+/* Synchronising reads into caller-owned host buffers.  With partitions,
+ * sim_read_state reports the vehicles of the partitions in this handle (one
+ * process per rank: its own; the others read as PENDING unless they finished
+ * here); sim_read_state_global (collective: every rank calls it) reports every
+ * partition's vehicles — with the direct transport across processes it reads
+ * the peers' buffers through their IPC mappings; otherwise it equals
+ * sim_read_state.  Vehicles are vid-indexed, so the result equals a
+ * single-partition run's. */
 sim_status sim_read_state(sim_handle h, sim_state *out);
+sim_status sim_read_state_global(sim_handle h, sim_state *out);
 sim_status sim_read_decisions(sim_handle h, sim_decisions *out);
 sim_status sim_read_metrics(sim_handle h, sim_metrics *out);
 /* Per-group metrics (params.road_group): out[n_groups], counters of the tiles

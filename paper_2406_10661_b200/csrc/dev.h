@@ -100,6 +100,7 @@ struct PeerView {                   // pointers only (exported as an array of ha
   Slab slab[2];                     // stayers, cnt and pending-queue heads: moved when a
   int32_t *cnt[2];                  // tile changes owner (sim_repartition)
   int32_t *pend_head;
+  int32_t *arrive_time, *wait_fin;  // read by sim_read_state_global
   void *xbuf[4];                    // reduction buffers: counters, lane statistics, group metrics,
                                     // host-call exchange (set_vehicle_route: where each vehicle is)
 };

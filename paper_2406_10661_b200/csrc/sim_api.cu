@@ -174,6 +174,7 @@ struct sim_s {
   void *ipc_tmp = nullptr;                      // ipc: reduction result buffer
   std::vector<void *> ipc_opened;               // ipc: peer mappings to close
   int32_t *repart_own_d = nullptr;              // sim_repartition: new owners (device)
+  std::vector<PeerView> peer_views;             // ipc: every rank's buffers (host copy of the table)
   std::vector<int> tile_owner;
   NcclComm comm = nullptr;
   std::vector<Part> parts;
@@ -1083,6 +1084,8 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   V.bar = P.bar_d;
   for (int b = 0; b < 2; ++b) { V.slab[b] = P.slab[b]; V.cnt[b] = P.cnt[b]; }
   V.pend_head = P.pend_head_d;
+  V.arrive_time = A.arrive_time;
+  V.wait_fin = A.wait_fin;
   V.xbuf[0] = P.red_d;
   V.xbuf[1] = P.lanestat_d;
   V.xbuf[2] = P.grp_d;
@@ -1528,6 +1531,7 @@ sim_status sim_ipc_connect(sim_handle h, const uint8_t *blobs, int32_t n_bytes) 
   }
   st = upload_peers(h, views);
   if (st) return st;
+  h->peer_views = views;
   h->connected = true;
   return SIM_OK;
 }
@@ -2050,23 +2054,39 @@ sim_status sim_query_sizes(sim_handle h, sim_sizes *out) {
 // Vehicles on the tiles of the handle's partition(s) are read from the slabs /
 // inboxes; cold fields are merged over partitions (a vehicle's FINISHED record
 // lives on the partition where it arrived).
-sim_status sim_read_state(sim_handle h, sim_state *o) {
+// sim_read_state / sim_read_state_global: the vehicles of every partition
+// this process can see — its own (loopback: all of them), or with `global`
+// and the direct transport across processes every rank's, read through the
+// peer mappings after the collective counter reduction.
+static sim_status read_state_impl(sim_s *h, sim_state *o, bool global) {
   sim_status st = check(h);
   if (st) return st;
   if (!o) return fail(h, SIM_E_INVALID, "out is NULL");
   std::vector<long long> cs;
-  st = read_counters(h, cs);
+  st = read_counters(h, cs);                        // (collective across ranks: also the barrier)
   if (st) return st;
   const int par = h->t & 1, nv = h->nv, nt = h->nt;
   std::vector<int> lane(nv, -1), cur(nv, 0), wait(nv, 0), ins(nv, -1), arr(nv, -1);
   std::vector<float> vs(nv, 0.f), vv(nv, 0.f);
   std::vector<uint8_t> status(nv, ST_PENDING);
   std::vector<char> driving(nv, 0);
-  for (Part &P : h->parts) {
+  struct Src { PeerView V; std::vector<int> tiles; };
+  std::vector<Src> src;
+  if (global && h->ipc) {
+    for (int q = 0; q < h->world; ++q) {
+      Src x;
+      x.V = h->peer_views[q];
+      for (int T = 0; T < nt; ++T) if (h->tile_owner[T] == q) x.tiles.push_back(T);
+      src.push_back(std::move(x));
+    }
+  } else {
+    for (Part &P : h->parts) src.push_back(Src{P.view, P.tiles});
+  }
+  for (Src &P : src) {
     std::vector<int> cnt(nt), icnt(nt);
-    CK(h, cudaMemcpy(cnt.data(), P.cnt[par], nt * 4, cudaMemcpyDeviceToHost));
-    CK(h, cudaMemcpy(icnt.data(), P.icnt[par], nt * 4, cudaMemcpyDeviceToHost));
-    const Slab &sl = P.slab[par];
+    CK(h, cudaMemcpy(cnt.data(), P.V.cnt[par], nt * 4, cudaMemcpyDeviceToHost));
+    CK(h, cudaMemcpy(icnt.data(), P.V.icnt[par], nt * 4, cudaMemcpyDeviceToHost));
+    const Slab &sl = P.V.slab[par];
     std::vector<float> s(h->sum_cap), v(h->sum_cap);
     std::vector<int> vid(h->sum_cap), wt(h->sum_cap);
     std::vector<uint32_t> meta(h->sum_cap);
@@ -2076,13 +2096,13 @@ sim_status sim_read_state(sim_handle h, sim_state *o) {
     CK(h, cudaMemcpy(wt.data(), sl.wait, wt.size() * 4, cudaMemcpyDeviceToHost));
     CK(h, cudaMemcpy(meta.data(), sl.meta, meta.size() * 4, cudaMemcpyDeviceToHost));
     std::vector<InboxRec> ib(h->sum_icap);
-    CK(h, cudaMemcpy(ib.data(), P.inbox[par], ib.size() * sizeof(InboxRec), cudaMemcpyDeviceToHost));
+    CK(h, cudaMemcpy(ib.data(), P.V.inbox[par], ib.size() * sizeof(InboxRec), cudaMemcpyDeviceToHost));
     std::vector<uint8_t> pst(nv);
     std::vector<int> pins(nv), parr(nv), pwf(nv);
-    CK(h, cudaMemcpy(pst.data(), P.A.status, nv, cudaMemcpyDeviceToHost));
-    CK(h, cudaMemcpy(pins.data(), P.A.insert_time, nv * 4, cudaMemcpyDeviceToHost));
-    CK(h, cudaMemcpy(parr.data(), P.A.arrive_time, nv * 4, cudaMemcpyDeviceToHost));
-    CK(h, cudaMemcpy(pwf.data(), P.A.wait_fin, nv * 4, cudaMemcpyDeviceToHost));
+    CK(h, cudaMemcpy(pst.data(), P.V.status, nv, cudaMemcpyDeviceToHost));
+    CK(h, cudaMemcpy(pins.data(), P.V.insert_time, nv * 4, cudaMemcpyDeviceToHost));
+    CK(h, cudaMemcpy(parr.data(), P.V.arrive_time, nv * 4, cudaMemcpyDeviceToHost));
+    CK(h, cudaMemcpy(pwf.data(), P.V.wait_fin, nv * 4, cudaMemcpyDeviceToHost));
     for (int k = 0; k < nv; ++k) {
       ins[k] = std::max(ins[k], pins[k]);
       if (pst[k] == ST_FINISHED) { status[k] = ST_FINISHED; arr[k] = parr[k]; wait[k] = pwf[k]; }
@@ -2135,6 +2155,9 @@ sim_status sim_read_state(sim_handle h, sim_state *o) {
   }
   return SIM_OK;
 }
+
+sim_status sim_read_state(sim_handle h, sim_state *o) { return read_state_impl(h, o, false); }
+sim_status sim_read_state_global(sim_handle h, sim_state *o) { return read_state_impl(h, o, true); }
 
 sim_status sim_read_decisions(sim_handle h, sim_decisions *o) {
   sim_status st = check(h);

@@ -84,7 +84,7 @@ class sim_metrics(C.Structure):
 
 
 ABI_FUNCTIONS = ["sim_create", "sim_get_nccl_unique_id", "sim_ipc_export", "sim_ipc_connect",
-                 "sim_repartition", "sim_partition", "sim_step", "sim_sync", "sim_set_signal_phase",
+                 "sim_repartition", "sim_read_state_global", "sim_partition", "sim_step", "sim_sync", "sim_set_signal_phase",
                  "sim_set_signal_phase_batch", "sim_set_lane_direction",
                  "sim_set_lane_direction_batch", "sim_query_sizes", "sim_read_state",
                  "sim_read_decisions", "sim_read_metrics", "sim_read_group_metrics", "sim_set_signal_policy", "sim_set_signal_policy_batch", "sim_set_signal_duration", "sim_set_signal_duration_batch", "sim_set_vehicle_route", "sim_set_vehicle_route_batch", "sim_set_lane_max_speed", "sim_set_lane_max_speed_batch", "sim_set_lane_restriction", "sim_set_lane_restriction_batch", "sim_load_state",
@@ -107,7 +107,7 @@ def load_library(path=LIB):
         "sim_create": [P, P, P, C.POINTER(C.c_void_p)],
         "sim_get_nccl_unique_id": [P], "sim_partition": [P, P, P, P, P],
         "sim_ipc_export": [h, P, i32, P], "sim_ipc_connect": [h, P, i32],
-        "sim_repartition": [h, P, P],
+        "sim_repartition": [h, P, P], "sim_read_state_global": [h, P],
         "sim_step": [h, i32], "sim_sync": [h],
         "sim_set_signal_phase": [h, i32, i32], "sim_set_signal_phase_batch": [h, i32, P, P],
         "sim_set_lane_direction": [h, i32, i32], "sim_set_lane_direction_batch": [h, i32, P, P],
@@ -328,7 +328,9 @@ class Sim:
         self._chk(self.lib.sim_query_sizes(self.h, C.byref(s)))
         return {n: getattr(s, n) for n, _ in sim_sizes._fields_}
 
-    def read_state(self, lane_order=False):
+    def read_state(self, lane_order=False, global_view=False):
+        """vid-indexed state; global_view (collective) = every partition's
+        vehicles, also across processes (sim_read_state_global)."""
         n, nj, nl = self.n, self.n_junctions, self.n_lanes
         b = dict(status=np.zeros(n, np.uint8), lane=np.zeros(n, np.int32),
                  cursor=np.zeros(n, np.int32), wait_steps=np.zeros(n, np.int32),
@@ -342,7 +344,8 @@ class Sim:
             b["lane_offsets"] = np.zeros(nl + 1, np.int32)
             b["lane_order"] = np.zeros(max(n, 1), np.int32)
         st = sim_state(0, *[_ptr(b[nm]) if nm in b else None for nm, _ in sim_state._fields_[1:]])
-        self._chk(self.lib.sim_read_state(self.h, C.byref(st)))
+        fn = self.lib.sim_read_state_global if global_view else self.lib.sim_read_state
+        self._chk(fn(self.h, C.byref(st)))
         b["t"] = st.t
         if lane_order:
             b["lane_order"] = b["lane_order"][:b["lane_offsets"][-1]]

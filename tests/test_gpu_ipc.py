@@ -38,7 +38,9 @@ def _worker(rank, world, port, name, out_dir):
     moved = g.repartition()                          # NEXT-2 rebalance by current load
     g.step(STEPS - STEPS // 2)
     st = g.read_state()
+    sg = g.read_state(global_view=True)                   # every rank's vehicles via peer memory
     m = g.read_metrics(lane_stats=True)
+    np.savez(os.path.join(out_dir, f"g{rank}.npz"), **{k: np.asarray(v) for k, v in sg.items()})
     np.savez(os.path.join(out_dir, f"r{rank}.npz"), moved=moved,
              **{k: np.asarray(v) for k, v in st.items()},
              **{"m_" + k: np.asarray(v) for k, v in m.items() if v is not None})
@@ -61,6 +63,7 @@ def test_multi_process_direct_transport(name, world):
         mp.start_processes(_worker, args=(world, _free_port(), name, d), nprocs=world,
                            join=True, start_method="spawn")
         rs = [dict(np.load(os.path.join(d, f"r{r}.npz"))) for r in range(world)]
+        gs = [dict(np.load(os.path.join(d, f"g{r}.npz"))) for r in range(world)]
     ref = p.Sim.from_scenario(_scen(name))
     ref.step(STEPS)
     s1 = ref.read_state()
@@ -88,6 +91,9 @@ def test_multi_process_direct_transport(name, world):
         for r in rs:
             assert np.array_equal(r[k], s1[k]), k
     assert m1["n_handoffs"] > 0
+    for gq in gs:                                    # the global view on every rank = one partition
+        for k in ("status", "lane", "cursor", "wait_steps", "insert_time", "arrive_time", "s", "v"):
+            assert np.array_equal(gq[k], s1[k]), k
 
 
 def _stall_worker(rank, world, port, out_dir):
