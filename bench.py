@@ -204,7 +204,9 @@ def run_gpu(args, rank, world, local_rank):
         p.build()
     if world > 1:
         torch.distributed.barrier()
-    scen = make_workload(world, args.policy, args.scale)
+    # weak (default): C4 per GPU, the city grown N x; strong (BASELINE configs[3],
+    # "1 GPU vs 8 GPUs partitioned"): the one C4 instance split over the N GPUs
+    scen = make_workload(1 if args.scaling == "strong" else world, args.policy, args.scale)
     stream = torch.cuda.Stream(dev)          # the simulation stream (events recorded on it)
     torch.cuda.set_stream(stream)
     sim = None
@@ -323,7 +325,7 @@ def run_gpu(args, rank, world, local_rank):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": workload_config(scen, policy=args.policy, extra={
             "parallelism": "single GPU" if world == 1 else
             f"spatial partition over {world} GPUs (recursive coordinate bisection of road tiles), " +
@@ -359,6 +361,8 @@ def main():
     ap.add_argument("--policy", default="fixed", choices=["fixed", "maxpressure"])
     ap.add_argument("--transport", default="direct", choices=["direct", "nccl"],
                     help="N > 1: direct peer-memory stores from k_step (NEXT-2) or NCCL p2p exchange")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: C4 per GPU (weak) or one C4 split over the N GPUs (strong)")
     ap.add_argument("--scale", type=float, default=1.0,
                     help="per-GPU size relative to C4 (4 = the 8M-vehicle single-GPU instance of SURVEY 8(d))")
     args = ap.parse_args()
