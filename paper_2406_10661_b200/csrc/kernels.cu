@@ -492,6 +492,23 @@ __device__ __forceinline__ void tile_update(const StepArgs &A, StepShared &S, co
   }
 }
 
+// The guard fallback of one deferred vehicle (fp64 canonical sequence, DESIGN
+// §3.3), out of line: a real call keeps the fp64 code and its registers out
+// of k_step<false>'s hot loop (C4: 277 -> 274 us).  Removing the fp64 path
+// from k_step entirely measured 262 us, but a separate k_defer kernel that
+// rebuilds the deferred tiles cost more (~28 us of single-warp latency).
+__device__ __noinline__ void defer_recompute(const StepArgs &A, const TileSh &T, const View &C,
+                                             int i, Acc8 &acc, int tile) {
+  Res r;
+  Guard g;
+  g.hit = false;
+  g.why = 0;
+  veh_update<double, false>(A, T, C, i, r, g);
+  if (A.record) record(A, C.vid(i), r, true);
+  emit_moved(A, C, i, r, r.fin ? 3 : 2, acc, tile);
+  acc.guard += 1;
+}
+
 // Phase 3: guard-deferred vehicles (fp64), lane summaries for t+1, departures
 // and counters (a4, a6).
 template <bool EXACT>
@@ -504,17 +521,7 @@ __device__ __forceinline__ void tile_finish(const StepArgs &A, StepShared &S, co
   int *dlist = A.dl_scratch + base + ibase;
   if constexpr (!EXACT) {
     __syncwarp();
-    for (int q = lane_id; q < ndef; q += kThreads) {
-      const int i = dlist[q];
-      Res r;
-      Guard g;
-      g.hit = false;
-      g.why = 0;
-      veh_update<double, false>(A, T, C, i, r, g);
-      if (A.record) record(A, C.vid(i), r, true);
-      emit_moved(A, C, i, r, r.fin ? 3 : 2, acc, tile);
-      acc.guard += 1;
-    }
+    for (int q = lane_id; q < ndef; q += kThreads) defer_recompute(A, T, C, dlist[q], acc, tile);
   }
   __syncwarp();
 
