@@ -281,14 +281,15 @@ def run_gpu(args, rank, world, local_rank):
     kstep_avg_s = kstep_ms / 1e3 / args.steps
     achieved = per_launch_bytes / kstep_avg_s / 1e9
     traffic = issue = None
-    try:
-        with open(NCU_TRAFFIC) as f:
-            tr = json.load(f)
-        if tr.get("workload") == "C4" and tr.get("n_vehicles") == scen.n_trips:
-            traffic = tr.get("dram_bytes_per_launch")
-            issue = tr.get("issue_frac")
-    except Exception:
-        pass
+    for path in (NCU_TRAFFIC, NCU_TRAFFIC.replace(".json", "_8m.json")):
+        try:                                              # the capture of this instance, if any
+            with open(path) as f:
+                tr = json.load(f)
+            if tr.get("workload") == "C4" and tr.get("n_vehicles") == scen.n_trips:
+                traffic = tr.get("dram_bytes_per_launch")
+                issue = tr.get("issue_frac")
+        except Exception:
+            pass
     # e2e: RL-style loop through the public API with host buffers
     nj = len(scen.graph["junc_lane_offsets"]) - 1
     jids = np.arange(nj, dtype=np.int32)

@@ -14,6 +14,10 @@ ncu -i gpurun_out/prof_kstep.ncu-rep --page source --csv > gpurun_out/kstep_sour
 ncu -i gpurun_out/prof_kstep.ncu-rep --page raw --csv > gpurun_out/kstep_raw.csv 2>/dev/null
 python scripts/ncu_summary.py gpurun_out/prof_kstep.ncu-rep profiles/r01_kstep_ncu_full.txt \
     profiles/ncu_kstep_traffic.json > /dev/null
+SCALE=4 ncu --set full --clock-control none -k regex:k_step -s 20 -c 1 \
+    -o gpurun_out/prof_kstep_8m -f python scripts/time_c4.py > gpurun_out/ncu_full_8m.log 2>&1
+python scripts/ncu_summary.py gpurun_out/prof_kstep_8m.ncu-rep profiles/r01_kstep_ncu_full_8m.txt \
+    profiles/ncu_kstep_traffic_8m.json 8000000 > /dev/null
 python bench.py > gpurun_out/bench.log 2>&1
 python bench.py --scale 4 --steps 50 --no-cpu > gpurun_out/bench_8m.log 2>&1
 python bench.py --policy maxpressure --no-cpu > gpurun_out/bench_mp.log 2>&1

@@ -40,7 +40,8 @@ if traffic_json:
                                           "ms": 1e-3, "msecond": 1e-3}.get(du, 1e-6)
     # issue ceiling: 148 SMs x 4 schedulers x 1 warp instruction per cycle at 1965 MHz
     issue_peak = 148 * 4 * 1965e6
-    json.dump({"workload": "C4", "n_vehicles": 2000000, "kernel": "k_step",
+    nveh = int(sys.argv[4]) if len(sys.argv) > 4 else 2000000
+    json.dump({"workload": "C4", "n_vehicles": nveh, "kernel": "k_step",
                "dram_bytes_per_launch": t, "warp_inst_per_launch": inst,
                "issue_frac": inst / dur_s / issue_peak,
                "issue_active_pct": float(d["smsp__issue_active.avg.pct_of_peak_sustained_active"][0]),

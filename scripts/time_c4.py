@@ -5,11 +5,14 @@ import numpy as np, torch
 import synth
 import paper_2406_10661_b200.sim as S
 lib = sys.argv[1] if len(sys.argv) > 1 else S.LIB
-cache = "/tmp/c4.npz"
+# SCALE=4: the 8M-vehicle instance of bench.py --scale 4 (G = 144)
+scale = float(os.environ.get("SCALE", "1"))
+cache = "/tmp/c4.npz" if scale == 1 else f"/tmp/c4_x{scale:g}.npz"
 if os.path.exists(cache):
     scen = synth.load_scenario(cache)
 else:
-    scen = synth.city(); synth.save_scenario(scen, cache)
+    scen = synth.city(G=int(round(72 * np.sqrt(scale))), n_vehicles=int(round(2_000_000 * scale)))
+    synth.save_scenario(scen, cache)
 S.load_library(lib)
 st = torch.cuda.Stream()
 sim = S.Sim.from_scenario(scen, stream=st.cuda_stream)
