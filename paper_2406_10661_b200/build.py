@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsim_b200.so")
-SOURCES = ["kernels.cu", "sim_api.cu"]
+SOURCES = ["kstep.cu", "kernels.cu", "sim_api.cu"]
 HEADERS = ["dev.h", "model.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

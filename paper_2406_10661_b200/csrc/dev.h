@@ -31,11 +31,11 @@ static_assert(kMaxRoadLanes * kMaxSucc == 32, "one warp builds the successor tab
 // tile descriptor (int32 words, 16-B padded, host-built by build_desc and
 // rebuilt after setters): [nl, nroad, ne, 0], glob[nl], len[nl], vmax[nl],
 // flags[nl] (bit0 usable; road lanes: usable successors << 8, groups << 16),
-// per road lane 6 words (gbeg[0..3] bytes, gbeg[4], gtroad[0..3]), then the
+// xl[nl] (junction lanes: exit lane, road lanes -1), per road lane 6 words (gbeg[0..3] bytes, gbeg[4], gtroad[0..3]), then the
 // ne <= 32 usable successors of the road lanes sorted by (lane, target road,
 // lane id), 8 words each: j, target road, exit lane, flags (bit0 junction lane,
 // lane_local << 8, rank k << 16), outroads(exit lane) x4
-constexpr int kDescMaxWords = 4 + 4 * kMaxTileLanes + 6 * kMaxRoadLanes + 8 * kMaxRoadLanes * kMaxSucc;
+constexpr int kDescMaxWords = 4 + 5 * kMaxTileLanes + 6 * kMaxRoadLanes + 8 * kMaxRoadLanes * kMaxSucc;
 constexpr int kMaxGroups = 4;        // distinct target roads per road lane in the table
 constexpr int kSmemProf = 8;         // profiles staged in shared memory
 constexpr uint64_t kEmptyKey = ~0ull;
@@ -62,6 +62,26 @@ struct __align__(16) InboxRec {      // 32 B, one sector (16-B aligned: moved as
   int32_t vid, nxt, nxt2;
   uint32_t meta;                    // lane_local:8 | profile:8 | cursor:16
   int32_t wait, pad;
+};
+
+// Gathered by the producer warp of k_step for every junction lane of a tile
+// (DESIGN §3.2): the first vehicle of the junction lane's exit lane at t (the
+// lookahead target of P:168-169 one lane beyond the tile) and the signal of
+// the junction lane at t.
+struct ExtFirst {
+  float s, v, len, Lb;              // position / speed / vehicle length; Lb = length of the exit lane
+  int32_t vid;                      // -1: the exit lane is empty
+  int32_t sig;                      // signal of the junction lane at t
+  int32_t b, pad;                   // the exit lane
+};
+
+// Head of a road lane's pending-departure queue at t (K11), gathered
+// by the producer warp: k = vid (-1: none due), its depart step, start
+// position and profile, h = queue position.
+struct PendHead {
+  int32_t k, depart, prof, h;
+  float start_s;
+  int32_t pad[3];
 };
 
 struct MigRec {                     // 48 B: a vehicle migrating to another partition
@@ -206,9 +226,8 @@ struct SignalArgs {
 void launch_signal(const SignalArgs &a, void *stream);
 void launch_step(const StepArgs &a, void *stream, int smem_bytes);
 int step_smem_bytes();
-void launch_set_i32(int32_t *dst, const int32_t *idx, const int32_t *val, int m, void *stream);
-void launch_apply_requests(int32_t *request, uint8_t *policy, const int32_t *junc,
-                           const int32_t *phase, int m, void *stream);
+void launch_apply_requests(int32_t *request, const int32_t *junc, const int32_t *phase, int m,
+                           void *stream);
 void launch_reduce_acc(const long long *tacc, int n_tiles, const int32_t *cnt,
                        const int32_t *icnt, const uint8_t *status, int nv, long long *out,
                        void *stream);

@@ -1,16 +1,5 @@
-// kernels.cu — the fused step kernel (a0-a4, a6) and the signal kernel (a5).
-//
-// k_step: one CTA per road tile.  Per step and tile:
-//   1. merge the in-order stayers (slab) with the sorted inbox into the tile
-//      snapshot in shared memory (a1; the paper's index update K3, P:130,
-//      without a global sort: stayers cannot overtake, movers are few);
-//   2. every thread updates one vehicle (a2 lookup, a3 IDM + MOBIL + signal,
-//      a4 integrate / hand-off / arrival) reading only the snapshot;
-//   3. stayers are compacted in order into the output slab (coalesced),
-//      movers are appended to the destination tile's inbox, arrivals retired;
-//   4. per-lane first-vehicle summaries for step t+1 are built with 64-bit
-//      integer atomicMin (order independent), departures are inserted (K11,
-//      P:142), and per-tile int64 counters accumulate (a6).
+// kernels.cu — the signal kernel (a5) and the read-side / exchange kernels.
+// The fused step kernel k_step (a0-a4, a6) is in kstep.cu.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -23,25 +12,6 @@ namespace sim {
 __device__ __forceinline__ unsigned long long vkey(float s, int vid) {
   return ((unsigned long long)__float_as_uint(s) << 32) | (unsigned)vid;
 }
-// composite order key (lane_local, s, vid)
-__device__ __forceinline__ unsigned long long hikey(int lane, float s) {
-  return ((unsigned long long)(unsigned)lane << 32) | __float_as_uint(s);
-}
-__device__ __forceinline__ bool key_less(unsigned long long h1, int v1, unsigned long long h2,
-                                         int v2) {
-  return h1 < h2 || (h1 == h2 && v1 < v2);
-}
-
-// fp64 canonical path (exact_mode and guard fallback) kept out of line so the
-// hot fp32 path is register-allocated on its own
-__device__ __forceinline__ void record(const StepArgs &A, int vid, const Res &r, bool guard) {
-  A.r_lc[vid] = (int8_t)r.lc;
-  A.r_hand[vid] = (int8_t)(r.hand > 127 ? 127 : r.hand);
-  A.r_acc[vid] = r.acc;
-  A.r_fin[vid] = (int8_t)r.fin;
-  A.r_guard[vid] = (uint8_t)(guard ? 1 : 0);
-  A.r_mark[vid] = 1;
-}
 
 __device__ __forceinline__ void put_inbox(InboxRec *dst, const InboxRec &rec) {
   int4 *d = reinterpret_cast<int4 *>(dst);
@@ -50,624 +20,6 @@ __device__ __forceinline__ void put_inbox(InboxRec *dst, const InboxRec &rec) {
   d[1] = s[1];
 }
 
-// Cold paths (inboxes larger than kSmemInbox, i.e. bulk lane changes after a
-// setter or a load): kept out of line so they do not occupy the I-cache.
-__device__ __noinline__ void rank_inbox_global(const InboxRec *inb, int n_in, int *bsort,
-                                               int lane_id) {
-  for (int j = lane_id; j < n_in; j += kThreads) {
-    const InboxRec r = inb[j];
-    const unsigned long long h = hikey(m_lane(r.meta), r.s);
-    int rank = 0;
-    for (int q = 0; q < n_in; ++q) {
-      const InboxRec o = inb[q];
-      rank += key_less(hikey(m_lane(o.meta), o.s), o.vid, h, r.vid);
-    }
-    bsort[rank] = j;
-  }
-}
-__device__ __noinline__ int lower_bound_inbox_global(const InboxRec *inb, const int *bsort,
-                                                     int n_in, unsigned long long h, int vid) {
-  int lo = 0, hi = n_in;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    const InboxRec o = inb[bsort[mid]];
-    if (key_less(hikey(m_lane(o.meta), o.s), o.vid, h, vid)) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
-
-// fire-and-forget 64-bit add (RED: no load round trip at the end of a tile)
-__device__ __forceinline__ void red_add(long long *p, long long v) {
-  atomicAdd(reinterpret_cast<unsigned long long *>(p), (unsigned long long)v);
-}
-
-struct Acc8 {                        // per-thread counters of one tile
-  long long delay = 0;               // (travel / wait sums of arrivals go straight to tacc)
-  int fin = 0, lc = 0, hand = 0, guard = 0, ovf = 0, ins = 0;
-};
-
-// Direct transport (NEXT-2): a mover entering another partition's
-// tile is stored straight into the owner's inbox for t+1 and folded into the
-// owner's summary / lane count with the same integer atomics a local mover
-// uses, so no exchange or absorb step follows.  Returns 1 on inbox overflow.
-__device__ __noinline__ int emit_peer(const StepArgs &A, const InboxRec &rec, int owner, int dt,
-                                      int lane_g) {
-  const PeerView &Q = A.peers[owner];
-  const int nb = (A.t + 1) & 1, ns = (A.t + 1) % 3;
-  const int vid = rec.vid;
-  const int slot = atomicAdd(&Q.icnt[nb][dt], 1);
-  int ovf = 0;
-  if (slot < A.tile_icap[dt]) put_inbox(Q.inbox[nb] + A.tile_ibase[dt] + slot, rec);
-  else ovf = 1;
-  atomicMin(&Q.summ[ns][lane_g], vkey(rec.s, vid));
-  Q.pubv[nb][vid] = rec.v;
-  if (A.lane_cnt_next) atomicAdd(&Q.lcnt[ns][lane_g], 1);
-  Q.insert_time[vid] = A.insert_time[vid];
-  Q.status[vid] = ST_DRIVING;
-  return ovf;
-}
-
-// a vehicle that leaves its slot: lane change / hand-off (kind 2, also every
-// guard-deferred vehicle) or arrival (kind 3)
-__device__ __forceinline__ void emit_moved(const StepArgs &A, const View &C, int i, const Res &r,
-                                           int kind, Acc8 &acc, int tile) {
-  const int vid = C.vid(i);
-  acc.lc += r.lc != 0;
-  acc.hand += r.hand;
-  if (kind == 3) {
-    A.status[vid] = ST_FINISHED;
-    A.arrive_time[vid] = A.t + 1;
-    A.wait_fin[vid] = r.wait1;
-    acc.fin += 1;
-    // int64 sums straight into the tile's accumulators (arrivals are rare; no
-    // 64-bit register state through the update loop)
-    long long *ta = A.tacc + (size_t)tile * kNAcc;
-    atomicAdd(reinterpret_cast<unsigned long long *>(ta + ACC_SUM_TRAVEL),
-              (unsigned long long)(long long)(A.t + 1 - A.insert_time[vid]));
-    atomicAdd(reinterpret_cast<unsigned long long *>(ta + ACC_SUM_WAIT_FIN), (unsigned long long)(long long)r.wait1);
-    return;
-  }
-  const uint32_t meta = C.meta(i);
-  const int cur = m_cursor(meta);
-  InboxRec rec;
-  rec.s = r.s1;
-  rec.v = r.v1;
-  rec.vid = vid;
-  rec.nxt = route_at(A, vid, cur, r.nxt, r.nxt2, r.cursor + 1);
-  rec.nxt2 = route_at(A, vid, cur, r.nxt, r.nxt2, r.cursor + 2);
-  rec.meta = pack_meta(A.lane_local[r.lane_g], m_prof(meta), r.cursor);
-  rec.wait = r.wait1;
-  rec.pad = 0;
-  const int dt = A.lane_tile[r.lane_g];
-  const int owner = A.tile_owner[dt];
-  if (owner == A.rank) {
-    const int slot = atomicAdd(&A.icnt_out[dt], 1);
-    if (slot < A.tile_icap[dt]) put_inbox(A.inbox_out + A.tile_ibase[dt] + slot, rec);
-    else acc.ovf += 1;
-    atomicMin(&A.summ_next[r.lane_g], vkey(r.s1, vid));
-    A.pubv_next[vid] = r.v1;
-    if (A.lane_cnt_next) atomicAdd(&A.lane_cnt_next[r.lane_g], 1);
-  } else if (A.peers) {                             // direct transport (NEXT-2)
-    acc.ovf += emit_peer(A, rec, owner, dt, r.lane_g);
-  } else {                                          // migrant to another partition
-    const int slot = atomicAdd(&A.out_cnt[owner], 1);
-    if (slot < A.out_cap[owner]) {
-      MigRec *m = A.out_buf + A.out_off[owner] + 1 + slot;
-      put_inbox(&m->rec, rec);
-      m->tile = dt;
-      m->insert_time = A.insert_time[vid];
-    } else {
-      acc.ovf += 1;
-    }
-  }
-}
-
-struct StepShared {
-  TileSh T;
-  unsigned long long bk_hi[kSmemInbox];       // inbox keys (arrival order)
-  int bk_vid[kSmemInbox];
-  int bsort[kSmemInbox];
-  unsigned long long sk_hi[kSmemInbox];       // inbox keys in sorted order
-  int sk_vid[kSmemInbox];
-};
-
-#ifndef KSTEP_WARPS
-#define KSTEP_WARPS 1
-#endif
-#ifndef KSTEP_MINB
-#define KSTEP_MINB (32 / KSTEP_WARPS)
-#endif
-constexpr int kStepWarps = KSTEP_WARPS;
-
-// What the phases of one tile hand to each other (registers of its warp).
-struct TileCtx {
-  int tile, n, base, ibase, nl, nroad;
-  View C;
-};
-
-// Phase 1 of a road tile (one warp; intra-tile synchronisation is __syncwarp()):
-// tile metadata and the merged snapshot (a1).
-template <bool EXACT>
-__device__ __forceinline__ void tile_load(const StepArgs &A, StepShared &S, unsigned char *dyn,
-                                          TileCtx &x, const int lane_id) {
-  TileSh &T = S.T;
-  // ---- tile metadata -----------------------------------------------------
-  // One coalesced read of the tile descriptor (host-built): lane
-  // ids / lengths / speed limits / usable flags and every road-lane successor
-  // with its target road, exit lane and the exit lane's reachable roads.
-  const int tile = x.tile;
-  const int doff = A.desc_off[tile], dend = A.desc_off[tile + 1];
-  const int n_st = A.cnt_in[tile];
-  const int n_in = A.icnt_in[tile];
-  const int n = n_st + n_in;
-  const int base = A.tile_base[tile];
-  const int ibase = A.tile_ibase[tile];
-  // lane counts from the static tile tables (same load wave as the offsets),
-  // so every descriptor word below is addressed without waiting for it
-  const int nl = A.tile_lane_off[tile + 1] - A.tile_lane_off[tile], nroad = A.tile_nroad[tile];
-  const int *W = A.desc + doff;                     // read straight from global (L2)
-  int ew[8];                                        // successor entry of this lane (if any)
-  {
-    const int eo = 4 + 4 * nl + 6 * nroad + 8 * lane_id;
-    if (doff + eo + 8 <= dend) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) ew[q] = W[eo + q];
-    } else {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) ew[q] = 0;
-    }
-  }
-  const int ne = W[2];
-  // lane records, the per-road-lane group tables and the (host-sorted) usable
-  // successors go straight into the tile's shared metadata; only the stop bit
-  // (signal of the junction lane at t) is computed here
-  if (lane_id == 0) {
-    T.nl = nl;
-    T.nroad = nroad;
-    T.tile = tile;
-    T.base = base;
-    T.ibase = ibase;
-    T.cap = A.tile_cap[tile];
-    T.icap = A.tile_icap[tile];
-  }
-  if (lane_id < nl) {
-    const int l = lane_id;
-    const int fl = W[4 + 3 * nl + l];
-    T.glob[l] = W[4 + l];
-    T.len[l] = __int_as_float(W[4 + nl + l]);
-    T.vmax[l] = __int_as_float(W[4 + 2 * nl + l]);
-    T.isroad[l] = l < nroad;
-    T.usable[l] = fl & 1;
-    T.seg_start[l] = 0;
-    T.seg_end[l] = 0;
-    T.first_out[l] = 0x7fffffff;
-    // road lanes are the first nroad local lanes, leftmost first (validated at create)
-    T.left[l] = (l < nroad && l > 0) ? (int8_t)(l - 1) : (int8_t)-1;
-    T.right[l] = (l < nroad - 1) ? (int8_t)(l + 1) : (int8_t)-1;
-    if (l < nroad) {
-      const int *gw = W + 4 + 4 * nl + 6 * l;
-      T.sn[l] = (uint8_t)((fl >> 8) & 0xff);
-      T.ng[l] = (uint8_t)((fl >> 16) & 0xff);
-      const unsigned g4 = (unsigned)gw[0];
-      T.gbeg[l][0] = (uint8_t)g4;
-      T.gbeg[l][1] = (uint8_t)(g4 >> 8);
-      T.gbeg[l][2] = (uint8_t)(g4 >> 16);
-      T.gbeg[l][3] = (uint8_t)(g4 >> 24);
-      T.gbeg[l][4] = (uint8_t)gw[1];
-#pragma unroll
-      for (int q = 0; q < kMaxGroups; ++q) T.gtroad[l][q] = gw[2 + q];
-    }
-  }
-  if (lane_id < ne) {
-    const int fl = ew[3];
-    SuccEnt e;
-    e.j = ew[0];
-    e.troad = ew[1];
-    e.b = ew[2];
-    e.outr = make_int4(ew[4], ew[5], ew[6], ew[7]);
-    e.stop = ((fl & 1) && A.lane_sig[e.j] != SIG_GREEN) ? 1 : 0;
-    T.se[(fl >> 8) & 0xff][fl >> 16] = e;
-  }
-  reinterpret_cast<int16_t *>(&T.gidx[0][0])[lane_id] = (int16_t)-1;    // 64 bytes
-  __syncwarp();
-  {
-    // distinct target roads of the road lanes (entry e = lane a, group g),
-    // numbered in order of first appearance; per road a lane bitmask
-    static_assert(kMaxRoadLanes * kMaxGroups <= 32, "one entry per thread");
-    const int a = lane_id / kMaxGroups, g = lane_id % kMaxGroups;
-    const bool valid = a < nroad && g < T.ng[a];
-    const int R = valid ? T.gtroad[a][g] : -1;
-    const unsigned vb = __ballot_sync(0xffffffffu, valid);
-    bool first = valid;
-    int myk = -1;
-    unsigned fb = 0;
-#pragma unroll 1
-    for (int q = 0; q < kMaxRoadLanes * kMaxGroups; ++q) {
-      const int Rq = __shfl_sync(0xffffffffu, R, q);
-      if (valid && ((vb >> q) & 1u) && Rq == R && q < lane_id) first = false;
-    }
-    fb = __ballot_sync(0xffffffffu, first);
-#pragma unroll 1
-    for (int q = 0; q < kMaxRoadLanes * kMaxGroups; ++q) {
-      const int Rq = __shfl_sync(0xffffffffu, R, q);
-      if (valid && ((fb >> q) & 1u) && Rq == R) myk = __popc(fb & ((1u << q) - 1u));
-    }
-    if (first) T.troad[myk] = R;
-    if (valid) T.gidx[a][myk] = (int8_t)g;
-    const int ntr = __popc(fb);
-    for (int k = 0; k < ntr; ++k) {
-      const unsigned m = __ballot_sync(0xffffffffu, valid && myk == k);
-      unsigned lanes = 0;
-#pragma unroll
-      for (int aa = 0; aa < kMaxRoadLanes; ++aa)
-        if ((m >> (aa * kMaxGroups)) & ((1u << kMaxGroups) - 1u)) lanes |= 1u << aa;
-      if (lane_id == 0) T.reach[k] = (uint8_t)lanes;
-    }
-    const unsigned um = __ballot_sync(0xffffffffu, lane_id < nroad && T.usable[lane_id]);
-    if (lane_id == 0) { T.ntr = ntr; T.umask = um; }
-  }
-  __syncwarp();
-
-  // snapshot view: shared memory, or this tile's global scratch if too large
-  View C;
-  const bool smem_ok = (n <= kSmemVeh) && (n_in <= kSmemInbox);
-  if (smem_ok) {
-    C.p = reinterpret_cast<uint32_t *>(dyn);
-    C.sp = reinterpret_cast<int16_t *>(dyn + kSmemVeh * 16);
-    C.st = kSmemVeh;
-  } else {                                   // scratch region of the tile: 5 x (cap + icap) words
-    C.st = T.cap + T.icap;
-    C.p = A.scratch + 5 * (size_t)(base + ibase);
-    C.sp = reinterpret_cast<int16_t *>(C.p + 4 * C.st);
-  }
-  int *bsort = (n_in <= kSmemInbox) ? S.bsort : (A.bsort_scratch + ibase);
-  const InboxRec *inb = A.inbox_in + ibase;
-  const bool small_in = n_in <= kSmemInbox;
-
-  // ---- 1. merge stayers + sorted inbox (a1) ---------------------------------
-  if (n_in > 0) {
-    if (small_in) {
-      for (int j = lane_id; j < n_in; j += kThreads) {
-        const InboxRec r = inb[j];
-        S.bk_hi[j] = hikey(m_lane(r.meta), r.s);
-        S.bk_vid[j] = r.vid;
-      }
-      __syncwarp();
-      for (int j = lane_id; j < n_in; j += kThreads) {
-        const unsigned long long h = S.bk_hi[j];
-        const int vj = S.bk_vid[j];
-        int rank = 0;
-        for (int q = 0; q < n_in; ++q) rank += key_less(S.bk_hi[q], S.bk_vid[q], h, vj);
-        bsort[rank] = j;
-        S.sk_hi[rank] = h;
-        S.sk_vid[rank] = vj;
-      }
-    } else {
-      rank_inbox_global(inb, n_in, bsort, lane_id);
-    }
-  }
-  __syncwarp();
-  // stayers: position = own index + #inbox keys below (binary search in the sorted inbox).
-  // Two slab rows per iteration, loads issued before the stores (more bytes in flight).
-  for (int i0 = lane_id; i0 < n_st; i0 += 2 * kThreads) {
-    float sv[2], vv[2];
-    uint32_t mv[2];
-    int idv[2];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int i = i0 + u * kThreads;
-      if (i < n_st) {
-        const int gi = base + i;
-        sv[u] = A.in.s[gi]; vv[u] = A.in.v[gi]; mv[u] = A.in.meta[gi]; idv[u] = A.in.vid[gi];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-    const int i = i0 + u * kThreads;
-    if (i >= n_st) break;
-    const float s = sv[u];
-    const uint32_t meta = mv[u];
-    const int vid = idv[u];
-    int pos = i;
-    if (n_in > 0) {
-      const unsigned long long h = hikey(m_lane(meta), s);
-      int lo = 0, hi = n_in;
-      if (small_in) {
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (key_less(S.sk_hi[mid], S.sk_vid[mid], h, vid)) lo = mid + 1; else hi = mid;
-        }
-      } else {
-        lo = lower_bound_inbox_global(inb, bsort, n_in, h, vid);
-      }
-      pos += lo;
-    }
-    C.s(pos) = s;
-    C.v(pos) = vv[u];
-    C.vid(pos) = vid;
-    C.meta(pos) = meta;
-    C.src(pos) = (int16_t)i;
-    }
-  }
-  // inbox records: position = sorted rank + #stayers below (binary search in the slab)
-  for (int r = lane_id; r < n_in; r += kThreads) {
-    const int j = bsort[r];
-    const InboxRec rec = inb[j];
-    const unsigned long long h = hikey(m_lane(rec.meta), rec.s);
-    int lo = 0, hi = n_st;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      const int gi = base + mid;
-      if (key_less(hikey(m_lane(A.in.meta[gi]), A.in.s[gi]), A.in.vid[gi], h, rec.vid)) lo = mid + 1;
-      else hi = mid;
-    }
-    const int pos = r + lo;
-    C.s(pos) = rec.s;
-    C.v(pos) = rec.v;
-    C.vid(pos) = rec.vid;
-    C.meta(pos) = rec.meta;
-    C.src(pos) = (int16_t)(-j - 1);
-  }
-  __syncwarp();
-  // lane segments of the snapshot
-  for (int i = lane_id; i < n; i += kThreads) {
-    const int l = m_lane(C.meta(i));
-    if (i == 0 || m_lane(C.meta(i - 1)) != l) T.seg_start[l] = i;
-    if (i == n - 1 || m_lane(C.meta(i + 1)) != l) T.seg_end[l] = i + 1;
-  }
-  __syncwarp();
-  x.n = n;
-  x.base = base;
-  x.ibase = ibase;
-  x.nl = nl;
-  x.nroad = nroad;
-  x.C = C;
-}
-
-  // ---- 2-3. per-vehicle update (a2-a4) and outputs, 32 vehicles at a time ----
-  // fp32 path: vehicles whose decision margins fall inside the guard band are
-  // deferred and recomputed after the loop with the canonical fp64 sequence;
-  // they leave through the inbox (as movers), so the in-order compaction of the
-  // stayers never waits for them and the fp64 code stays out of the hot loop.
-template <bool EXACT>
-__device__ __forceinline__ void tile_update(const StepArgs &A, StepShared &S, const TileCtx &x,
-                                            Acc8 &acc, int &run, int &ndef, const int lane_id) {
-  TileSh &T = S.T;
-  const int n = x.n, base = x.base, ibase = x.ibase;
-  const View C = x.C;
-  int *dlist = A.dl_scratch + base + ibase;
-  for (int c0 = 0; c0 < n; c0 += kThreads) {
-    const int i = c0 + lane_id;
-    Res r;
-    int kind = 0;                                   // 0 none, 1 stayer, 2 mover, 3 finished
-    bool defer = false;
-    if (i < n) {
-      if constexpr (EXACT) {
-        Guard g;
-        g.hit = false;
-        g.why = 0;
-        veh_update<double, false>(A, T, C, i, r, g);
-      } else {
-        Guard g;
-        g.hit = false;
-        g.why = 0;
-        veh_update<float, true>(A, T, C, i, r, g);
-        defer = g.hit;
-#ifdef GUARD_STATS
-        if (g.hit)
-          for (int b = 0; b < 32; ++b)
-            if (g.why & (1u << b)) atomicAdd(&g_guard_stats[b], 1ull);
-#endif
-      }
-      if (!defer) {
-        if (A.record) record(A, C.vid(i), r, false);
-        const int l = m_lane(C.meta(i));
-        if (r.fin) kind = 3;
-        else if (r.lc == 0 && r.hand == 0 && r.lane_g == T.glob[l]) kind = 1;
-        else kind = 2;
-      }
-    }
-    if constexpr (!EXACT) {
-      const unsigned dball = __ballot_sync(0xffffffffu, defer);
-      if (defer) dlist[ndef + __popc(dball & ((1u << lane_id) - 1u))] = i;
-      ndef += __popc(dball);
-    }
-    // order-preserving compaction of stayers (warp ballot)
-    const unsigned ball = __ballot_sync(0xffffffffu, kind == 1);
-    if (kind == 1) {
-      const int pos = base + run + __popc(ball & ((1u << lane_id) - 1u));
-      const uint32_t meta = C.meta(i);
-      A.out.s[pos] = r.s1;
-      A.out.v[pos] = r.v1;
-      A.out.vid[pos] = C.vid(i);
-      A.out.nxt[pos] = r.nxt;
-      A.out.nxt2[pos] = r.nxt2;
-      A.out.meta[pos] = meta;
-      A.out.wait[pos] = r.wait1;
-      atomicMin(&T.first_out[m_lane(meta)], pos);
-    } else if (kind >= 2) {
-      emit_moved(A, C, i, r, kind, acc, x.tile);
-    }
-    run += __popc(ball);
-  }
-}
-
-// The guard fallback of one deferred vehicle (fp64 canonical sequence, DESIGN
-// §3.3), out of line: a real call keeps the fp64 code and its registers out
-// of k_step<false>'s hot loop (C4: 277 -> 274 us).  Removing the fp64 path
-// from k_step entirely measured 262 us, but a separate k_defer kernel that
-// rebuilds the deferred tiles cost more (~28 us of single-warp latency).
-__device__ __noinline__ void defer_recompute(const StepArgs &A, const TileSh &T, const View &C,
-                                             int i, Acc8 &acc, int tile) {
-  Res r;
-  Guard g;
-  g.hit = false;
-  g.why = 0;
-  veh_update<double, false>(A, T, C, i, r, g);
-  if (A.record) record(A, C.vid(i), r, true);
-  emit_moved(A, C, i, r, r.fin ? 3 : 2, acc, tile);
-  acc.guard += 1;
-}
-
-// Phase 3: guard-deferred vehicles (fp64), lane summaries for t+1, departures
-// and counters (a4, a6).
-template <bool EXACT>
-__device__ __forceinline__ void tile_finish(const StepArgs &A, StepShared &S, const TileCtx &x,
-                                            Acc8 &acc, const int run, const int ndef,
-                                            const int lane_id) {
-  TileSh &T = S.T;
-  const int tile = x.tile, n = x.n, base = x.base, ibase = x.ibase, nl = x.nl, nroad = x.nroad;
-  const View C = x.C;
-  int *dlist = A.dl_scratch + base + ibase;
-  if constexpr (!EXACT) {
-    __syncwarp();
-    for (int q = lane_id; q < ndef; q += kThreads) defer_recompute(A, T, C, dlist[q], acc, tile);
-  }
-  __syncwarp();
-
-  // ---- 4. summaries, insertions, counters ------------------------------------
-  for (int l = lane_id; l < nl; l += kThreads) {
-    const int g = T.glob[l];
-    const int pos = T.first_out[l];
-    if (pos != 0x7fffffff) {
-      const float s1 = A.out.s[pos];
-      const int vid = A.out.vid[pos];
-      atomicMin(&A.summ_next[g], vkey(s1, vid));
-      A.pubv_next[vid] = A.out.v[pos];
-    }
-    A.summ_clear[g] = kEmptyKey;
-    if (A.lane_cnt_next && pos != 0x7fffffff) {     // stayers of lane l: [pos, next lane's first)
-      int end = base + run;
-      for (int q = l + 1; q < nl; ++q)
-        if (T.first_out[q] != 0x7fffffff) { end = T.first_out[q]; break; }
-      atomicAdd(&A.lane_cnt_next[g], end - pos);
-    }
-  }
-  for (int l = lane_id; l < nroad; l += kThreads) { // departures (K11; ledger L25)
-    const int g = T.glob[l];
-    const int h = A.pend_head[g];
-    if (h >= A.pend_off[g + 1]) continue;
-    const int k = A.pend_vid[h];
-    if (A.depart[k] > A.t || !T.usable[l]) continue;
-    const double ss = (double)A.start_s[k];
-    const Prof &pk = T.P[A.veh_prof[k]];
-    const int a0 = T.seg_start[l], b0 = T.seg_end[l];
-    const int fa = upper_bound_s(C, a0, b0, (float)ss);
-    bool ok = true;
-    if (fa < b0) {
-      const double sa = C.s(fa), la = T.P[m_prof(C.meta(fa))].len_d;
-      if (!(__dadd_rn(__dadd_rn(sa, -ss), -la) >= pk.s0_d)) ok = false;
-    }
-    if (fa > a0) {
-      const int b = fa - 1;
-      const Prof &pb = T.P[m_prof(C.meta(b))];
-      const double need = __dadd_rn(__dadd_rn((double)C.v(b), __dmul_rn(0.5, pb.a_max_d)), pk.s0_d);
-      if (!(__dadd_rn(__dadd_rn(ss, -(double)C.s(b)), -pk.len_d) >= need)) ok = false;
-    } else {
-      if (!(__dadd_rn(ss, -pk.len_d) >= A.start_margin)) ok = false;
-    }
-    if (!ok) continue;
-    InboxRec rec;
-    rec.s = (float)ss;
-    rec.v = 0.f;
-    rec.vid = k;
-    const int off = A.route_start[k], rl = A.route_len[k];
-    rec.nxt = rl > 1 ? A.route[off + 1] : -1;
-    rec.nxt2 = rl > 2 ? A.route[off + 2] : -1;
-    rec.meta = pack_meta(l, A.veh_prof[k], 0);
-    rec.wait = 0;
-    rec.pad = 0;
-    const int slot = atomicAdd(&A.icnt_out[tile], 1);
-    if (slot < T.icap) put_inbox(A.inbox_out + ibase + slot, rec);
-    else acc.ovf += 1;
-    atomicMin(&A.summ_next[g], vkey(rec.s, k));
-    A.pubv_next[k] = 0.f;
-    if (A.lane_cnt_next) atomicAdd(&A.lane_cnt_next[g], 1);
-    A.pend_head[g] = h + 1;
-    A.status[k] = ST_DRIVING;
-    A.insert_time[k] = A.t + 1;
-    if (A.record) A.r_ins[k] = 1;
-    acc.ins += 1;
-    acc.delay += (long long)(A.t + 1 - A.depart[k]);
-  }
-  // warp reduction of the counters (exact, order independent): 32-bit counts
-  // with redux.sync; the int64 sums only in warps that saw an arrival / insertion
-  const unsigned c_fin = __reduce_add_sync(0xffffffffu, (unsigned)acc.fin);
-  const unsigned c_ins = __reduce_add_sync(0xffffffffu, (unsigned)acc.ins);
-  const unsigned c_lc = __reduce_add_sync(0xffffffffu, (unsigned)acc.lc);
-  const unsigned c_hand = __reduce_add_sync(0xffffffffu, (unsigned)acc.hand);
-  const unsigned c_guard = __reduce_add_sync(0xffffffffu, (unsigned)acc.guard);
-  const unsigned c_ovf = __reduce_add_sync(0xffffffffu, (unsigned)acc.ovf);
-  long long s_delay = acc.delay;
-  if (c_ins) {
-    for (int o = 16; o > 0; o >>= 1) s_delay += __shfl_down_sync(0xffffffffu, s_delay, o);
-  }
-  if (lane_id == 0) {
-    long long *ta = A.tacc + (size_t)tile * kNAcc;
-    red_add(ta + ACC_VEH_STEPS, n);
-    if (c_fin) red_add(ta + ACC_FINISHED, c_fin);
-    if (c_ins) {
-      red_add(ta + ACC_INSERTED, c_ins);
-      red_add(ta + ACC_SUM_DELAY, s_delay);
-    }
-    if (c_lc) red_add(ta + ACC_LANE_CHANGES, c_lc);
-    if (c_hand) red_add(ta + ACC_HANDOFFS, c_hand);
-    if (c_guard) red_add(ta + ACC_GUARD, c_guard);
-    if (c_ovf) red_add(ta + ACC_OVERFLOW, c_ovf);
-    A.cnt_out[tile] = run;
-    A.icnt_in[tile] = 0;
-  }
-}
-
-// Persistent kernel.  A block of kStepWarps warps takes kStepWarps consecutive
-// road tiles from a work counter (largest tiles first: A.tiles is sorted by slot
-// capacity at create), one tile per warp, and runs the three phases of its
-// tiles in step with block barriers in between, so all warps of an SM execute
-// the same code at a time (the whole kernel does not fit the instruction
-// cache) and issue their HBM loads together.  Consecutive tiles of the sorted
-// list have similar sizes, so little time is lost at the barriers.  The last
-// block to finish resets the counters for the next launch.
-template <bool EXACT>
-__global__ void __launch_bounds__(kStepWarps * kThreads, KSTEP_MINB)
-    k_step(const __grid_constant__ StepArgs A) {
-  extern __shared__ __align__(16) unsigned char dyn_all[];
-  __shared__ StepShared SS[kStepWarps];
-  __shared__ Prof prof[kSmemProf];
-  __shared__ int s_base;
-  const int warp = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
-  StepShared &S = SS[warp];
-  unsigned char *dyn = dyn_all + (size_t)warp * (kSmemVeh * 18);
-  if (A.n_prof <= kSmemProf) {                      // profiles as int4 words (Prof is 96 B)
-    const int nw = A.n_prof * (int)(sizeof(Prof) / 16);
-    for (int q = threadIdx.x; q < nw; q += blockDim.x)
-      reinterpret_cast<int4 *>(prof)[q] = reinterpret_cast<const int4 *>(A.prof)[q];
-  }
-  if (lane_id == 0) S.T.P = A.n_prof <= kSmemProf ? prof : A.prof;
-  for (;;) {
-    if (threadIdx.x == 0) s_base = atomicAdd(&A.work[0], kStepWarps);
-    __syncthreads();
-    const int b0 = s_base;
-    if (b0 >= A.n_own) break;
-    const int idx = b0 + warp;
-    const bool has = idx < A.n_own;
-    TileCtx x;
-    x.tile = has ? A.tiles[idx] : 0;
-    if (has) tile_load<EXACT>(A, S, dyn, x, lane_id);
-    __syncthreads();
-    Acc8 acc;
-    int run = 0, ndef = 0;
-    if (has) tile_update<EXACT>(A, S, x, acc, run, ndef, lane_id);
-    __syncthreads();
-    if (has) tile_finish<EXACT>(A, S, x, acc, run, ndef, lane_id);
-  }
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(&A.work[1], 1) == (int)gridDim.x - 1) {
-      A.work[0] = 0;
-      A.work[1] = 0;
-    }
-  }
-}
 
 // ---- a5: per-junction signal controller -------------
 // One warp per junction.  Every lane runs the (tiny) phase machine on the same
@@ -1079,36 +431,13 @@ void launch_peer_sum(const PeerView *peers, int world, int kind, int dtype, int6
 }
 
 // ---- launchers ---------------------------------------------------------------
-int step_smem_bytes() { return kStepWarps * kSmemVeh * 18; }
-
-void launch_step(const StepArgs &a, void *stream, int smem_bytes) {
-  static int resident[2] = {0, 0};                  // resident blocks per GPU, per instantiation
-  if (!resident[0]) {
-    cudaFuncSetAttribute(k_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
-    cudaFuncSetAttribute(k_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
-    int dev = 0, nsm = 0, b0 = 0, b1 = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b0, k_step<false>, kStepWarps * kThreads, smem_bytes);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_step<true>, kStepWarps * kThreads, smem_bytes);
-    resident[0] = std::max(1, b0) * std::max(1, nsm);
-    resident[1] = std::max(1, b1) * std::max(1, nsm);
-  }
-  if (a.n_own <= 0) return;
-  const int ex = a.exact_mode ? 1 : 0;
-  const int grid = std::min((a.n_own + kStepWarps - 1) / kStepWarps, resident[ex]);
-  if (ex) k_step<true><<<grid, kStepWarps * kThreads, smem_bytes, (cudaStream_t)stream>>>(a);
-  else k_step<false><<<grid, kStepWarps * kThreads, smem_bytes, (cudaStream_t)stream>>>(a);
-}
-
 void launch_signal(const SignalArgs &a, void *stream) {
   if (a.n_junctions > 0)
     k_signal<<<(a.n_junctions + 3) / 4, 128, 0, (cudaStream_t)stream>>>(a);
 }
 
-void launch_apply_requests(int32_t *request, uint8_t *policy, const int32_t *junc,
-                           const int32_t *phase, int m, void *stream) {
-  (void)policy;
+void launch_apply_requests(int32_t *request, const int32_t *junc, const int32_t *phase, int m,
+                           void *stream) {
   if (m > 0) k_apply_requests<<<(m + 255) / 256, 256, 0, (cudaStream_t)stream>>>(request, junc, phase, m);
 }
 
@@ -1220,8 +549,6 @@ void launch_fill_u64(unsigned long long *p, unsigned long long v, int64_t n, voi
   if (n > 0) k_fill_u64<<<256, 256, 0, (cudaStream_t)stream>>>(p, v, n);
 }
 
-void launch_set_i32(int32_t *, const int32_t *, const int32_t *, int, void *) {}
-
 void launch_mig_header(MigRec *out_buf, const int32_t *out_off, const int32_t *out_cap,
                        int32_t *out_cnt, int world, void *stream) {
   k_mig_header<<<1, 32, 0, (cudaStream_t)stream>>>(out_buf, out_off, out_cap, out_cnt, world);
@@ -1240,16 +567,3 @@ void launch_halo_unpack(const StepArgs &a, const int32_t *lanes, const HaloRec *
 
 }  // namespace sim
 
-extern "C" int sim_debug_guard_stats(unsigned long long *out) {
-#ifdef GUARD_STATS
-  cudaDeviceSynchronize();
-  return cudaMemcpyFromSymbol(out, sim::g_guard_stats, 32 * 8) == cudaSuccess ? 32 : -1;
-#else
-  (void)out;
-  return 0;
-#endif
-}
-
-namespace sim {
-
-}  // namespace sim

@@ -75,13 +75,19 @@ __device__ __forceinline__ R idm(R v, R v0, bool lead, R gap, R dv, const PV<R> 
   return (a < -b_hard) ? -b_hard : a;
 }
 
-struct SuccEnt { int j, troad, b, stop; int4 outr; };  // usable successor of a tile road lane
-                                                          // (b: exit lane; stop: junction lane not GREEN)
+// usable successor of a tile road lane: j, its target road, exit lane b, the
+// exit lane's reachable roads; fl: bit0 stop (junction lane not GREEN at t),
+// bits 8-15 tile-local index of j when j is a junction lane of this tile
+// (0xff: a direct road -> road link)
+struct SuccEnt { int j, troad, b, fl; int4 outr; };
 
 // Tile-local lane metadata staged in shared memory.
 struct TileSh {
   int nl, nroad, tile, base, ibase, cap, icap;
+  int snap0, n;                      // snapshot range [snap0, snap0 + n) of the tile's vehicles
   const Prof *P;                     // profile table (shared-memory copy when small)
+  const ExtFirst *ext;               // [nl - nroad]: first vehicle of each junction lane's exit lane
+  const PendHead *pend;              // [nroad]: heads of the pending-departure queues
   uint8_t sn[kMaxRoadLanes];         // usable successors per road lane
   uint8_t ng[kMaxRoadLanes];         // groups (distinct target roads) per road lane
   uint8_t gbeg[kMaxRoadLanes][kMaxGroups + 1];
@@ -90,7 +96,7 @@ struct TileSh {
   int glob[kMaxTileLanes];
   float len[kMaxTileLanes], vmax[kMaxTileLanes];
   int16_t seg_start[kMaxTileLanes], seg_end[kMaxTileLanes];   // lane segments of the snapshot
-  int first_out[kMaxTileLanes];
+  int first_out[kMaxTileLanes];      // (output rank << 15) | snapshot index of the lane's first stayer
   int8_t left[kMaxTileLanes], right[kMaxTileLanes];
   uint8_t isroad[kMaxTileLanes], usable[kMaxTileLanes];
   // the distinct roads the tile's road lanes lead to (<= 4 lanes x 4 groups):
@@ -103,23 +109,26 @@ struct TileSh {
   int troad[kMaxRoadLanes * kMaxGroups];
   uint8_t reach[kMaxRoadLanes * kMaxGroups];
   int8_t gidx[kMaxRoadLanes][kMaxRoadLanes * kMaxGroups];
+  // per-tile outputs of the step
+  int run;                           // stayers written (compaction, in snapshot order)
+  int c_fin, c_lc, c_hand, c_guard, c_ovf, c_ins;
+  unsigned long long c_delay;
 };
 
-// Snapshot of the tile at time t: the fields other vehicles read (s, v, vid,
-// meta) are four word arrays of stride st from p (shared memory, or the tile's
-// global scratch when the tile is large); src(i) says where slot i came from
-// (stayer index >= 0, or -(inbox record + 1)), so the fields only the vehicle
-// itself uses (nxt, nxt2, wait) are read once from the slab / inbox when the
-// vehicle is updated instead of being staged (16 + 2 B per vehicle on chip).
+// Snapshot of a batch of tiles at time t (shared memory; the tile's global
+// scratch for a tile larger than a batch): seven word arrays of stride st —
+// the fields other vehicles read (s, v, vid, meta) and the fields only the
+// vehicle itself uses (nxt, nxt2, wait), all merged once per step (a1).
 struct View {
   uint32_t *p;
-  int16_t *sp;
   int st;
   __device__ __forceinline__ float &s(int i) const { return reinterpret_cast<float *>(p)[i]; }
   __device__ __forceinline__ float &v(int i) const { return reinterpret_cast<float *>(p)[st + i]; }
   __device__ __forceinline__ int32_t &vid(int i) const { return reinterpret_cast<int32_t *>(p)[2 * st + i]; }
   __device__ __forceinline__ uint32_t &meta(int i) const { return p[3 * st + i]; }
-  __device__ __forceinline__ int16_t &src(int i) const { return sp[i]; }
+  __device__ __forceinline__ int32_t &nxt(int i) const { return reinterpret_cast<int32_t *>(p)[4 * st + i]; }
+  __device__ __forceinline__ int32_t &nxt2(int i) const { return reinterpret_cast<int32_t *>(p)[5 * st + i]; }
+  __device__ __forceinline__ int32_t &wait(int i) const { return reinterpret_cast<int32_t *>(p)[6 * st + i]; }
 };
 
 __device__ __forceinline__ int m_lane(uint32_t m) { return (int)(m & 0xffu); }
@@ -170,15 +179,17 @@ __device__ __forceinline__ bool has_outroad_t(const StepArgs &A, const TileSh &T
     if (T.gtroad[a][g] == R) return true;
   return false;
 }
-struct Next { int j; bool stop; };  // next lane and "stop line applies" (junction lane not GREEN)
-__device__ __forceinline__ Next next_stop_g(const StepArgs &A, int j) {
-  Next n;
-  n.j = j;
-  n.stop = j >= 0 && __ldg(A.lane_road + j) < 0 && A.lane_sig[j] != SIG_GREEN;
-  return n;
+// next lane, "stop line applies" (junction lane not GREEN) and how to find
+// the lane's first vehicle without a global lookup: hint >= 0 is the
+// tile-local index of a junction lane of this tile (snapshot segment), -1
+// none (generic lookup)
+struct Next { int j; bool stop; int hint; };
+__device__ __forceinline__ Next ent_next(const SuccEnt &x) {
+  const int jl = (x.fl >> 8) & 0xff;
+  return Next{x.j, (x.fl & 1) != 0, jl == 0xff ? -1 : jl};
 }
 __device__ __forceinline__ Next next1_t(const StepArgs &A, const TileSh &T, int l, int R1, int R2) {
-  if (R1 < 0) return Next{kLaneDest, false};
+  if (R1 < 0) return Next{kLaneDest, false, -1};
   for (int g = 0; g < T.ng[l]; ++g) {
     if (T.gtroad[l][g] != R1) continue;
     const int b = T.gbeg[l][g], e = T.gbeg[l][g + 1];
@@ -186,23 +197,23 @@ __device__ __forceinline__ Next next1_t(const StepArgs &A, const TileSh &T, int 
     // whose exit lane continues toward R2 is the preferred one (ledger L24)
     for (int k = b; k < e; ++k) {
       const SuccEnt &x = T.se[l][k];
-      if (pref_ok(x.outr, R2)) return Next{x.j, x.stop != 0};
+      if (pref_ok(x.outr, R2)) return ent_next(x);
     }
-    return Next{T.se[l][b].j, T.se[l][b].stop != 0};
+    return ent_next(T.se[l][b]);
   }
-  return Next{kLaneBlocked, false};
+  return Next{kLaneBlocked, false, -1};
 }
 // next1_t for the vehicle's own next road, known as troad[k] (k < 0: no road
 // lane of the tile leads there)
 __device__ __forceinline__ Next next1_k(const TileSh &T, int l, int k, int R2) {
   const int g = k >= 0 ? T.gidx[l][k] : -1;
-  if (g < 0) return Next{kLaneBlocked, false};
+  if (g < 0) return Next{kLaneBlocked, false, -1};
   const int b = T.gbeg[l][g], e = T.gbeg[l][g + 1];
   for (int q = b; q < e; ++q) {
     const SuccEnt &x = T.se[l][q];
-    if (pref_ok(x.outr, R2)) return Next{x.j, x.stop != 0};
+    if (pref_ok(x.outr, R2)) return ent_next(x);
   }
-  return Next{T.se[l][b].j, T.se[l][b].stop != 0};
+  return ent_next(T.se[l][b]);
 }
 __device__ __forceinline__ int troad_index(const TileSh &T, int R) {
   for (int k = 0; k < T.ntr; ++k)
@@ -227,7 +238,7 @@ struct First { bool found; float s, v, len; int vid; };
 
 // direct transport: lane m of tile mt from its owner partition's buffers of t
 // (out of line: keeps the single-partition lookahead path unchanged)
-__device__ __noinline__ unsigned long long peer_summary(const StepArgs &A, int mt, int m,
+static __device__ __noinline__ unsigned long long peer_summary(const StepArgs &A, int mt, int m,
                                                         const float *&pv) {
   const PeerView &Q = A.peers[__ldg(A.tile_owner + mt)];
   pv = Q.pubv[A.t & 1];
@@ -236,8 +247,7 @@ __device__ __noinline__ unsigned long long peer_summary(const StepArgs &A, int m
 
 // first vehicle of lane m at time t: from the tile snapshot if m is ours, else
 // from the lane summary built race-free during step t-1
-__device__ __forceinline__ First first_of(const StepArgs &A, const TileSh &T, const View &C,
-                                          int m) {
+static __device__ __noinline__ First first_of(const StepArgs &A, const TileSh &T, const View &C, int m) {
   First f;
   f.found = false;
   const int mt = __ldg(A.lane_tile + m);
@@ -268,6 +278,31 @@ __device__ __forceinline__ First first_of(const StepArgs &A, const TileSh &T, co
   }
   return f;
 }
+// first vehicle of the tile's own junction lane jl (snapshot segment)
+__device__ __forceinline__ First first_local(const TileSh &T, const View &C, int jl) {
+  First f;
+  const int a = T.seg_start[jl];
+  f.found = a < T.seg_end[jl];
+  if (f.found) {
+    f.s = C.s(a);
+    f.v = C.v(a);
+    f.vid = C.vid(a);
+    f.len = T.P[m_prof(C.meta(a))].len;
+  }
+  return f;
+}
+__device__ __forceinline__ int xl_of(const TileSh &T, int jl) { return T.ext[jl - T.nroad].b; }
+// first vehicle of the exit lane of the tile's junction lane jl (gathered)
+__device__ __forceinline__ First first_ext(const TileSh &T, int jl) {
+  const ExtFirst &x = T.ext[jl - T.nroad];
+  First f;
+  f.found = x.vid >= 0;
+  f.s = x.s;
+  f.v = x.v;
+  f.vid = x.vid;
+  f.len = x.len;
+  return f;
+}
 
 template <typename R> struct LEv {
   R a, gap, vlead, lim, vlim;
@@ -281,17 +316,27 @@ struct Me {                          // the ego vehicle's identity / route cache
   int k;                             // index of nxt in the tile's target roads (TileSh::troad)
 };
 
-// O4-O6 for the ego placed on tile-local lane l (App. A2.3)
+// O4-O6 for the ego placed on tile-local lane l (App. A2.3).
+// The lookahead walks the next lanes along the route; the first
+// two of them are resolved on chip in the common case — a junction lane of
+// this tile (its snapshot segment) and that junction lane's exit lane (the
+// first vehicle gathered by the producer warp) — and through the lane
+// summaries otherwise (first_of).  The values read are the same either way.
 template <typename R, bool GUARD>
-__device__ LEv<R> eval_lane(const StepArgs &A, const TileSh &T, const View &C, int l,
-                            int lead_idx, R s, R v, const PV<R> &p, const Me &me, Guard &g) {
+__device__ __forceinline__ LEv<R> eval_lane(const StepArgs &A, const TileSh &T, const View &C, int l,
+                                            int lead_idx, R s, R v, const PV<R> &p, const Me &me,
+                                            Guard &g) {
   using M = Ar<R>;
   LEv<R> e;
-  const int lg = T.glob[l];
   const bool road = T.isroad[l];
   Next nx;
-  if (road) nx = me.nxt < 0 ? Next{kLaneDest, false} : next1_k(T, l, me.k, me.nxt2);
-  else nx = Next{__ldg(A.exit_lane + lg), false};
+  int ext = -1;                                          // junction lane whose exit lane is next
+  if (road) {
+    nx = me.nxt < 0 ? Next{kLaneDest, false, -1} : next1_k(T, l, me.k, me.nxt2);
+  } else {                                               // junction lane: its exit lane
+    nx = Next{xl_of(T, l), false, -1};
+    ext = l;
+  }
   e.next1 = nx.j;
   const R vmax_l = (R)T.vmax[l];
   const R v0 = (p.vmax < vmax_l) ? p.vmax : vmax_l;
@@ -314,11 +359,27 @@ __device__ LEv<R> eval_lane(const StepArgs &A, const TileSh &T, const View &C, i
   } else {                                               // P:168-169 substitution
     R d = M::sub(L, s);
     int m = e.next1, rel = 0;
+    int own = road ? nx.hint : -1;                       // m is the tile's junction lane `own`
+#pragma unroll 1
     for (int h = 1; h <= A.lookahead; ++h) {
       if (m < 0) break;
-      const bool mroad = __ldg(A.lane_road + m) >= 0;
+      First f;
+      bool mroad;
+      R Lm;
+      if (own >= 0) {
+        mroad = false;
+        f = first_local(T, C, own);
+        Lm = (R)T.len[own];
+      } else if (ext >= 0) {
+        mroad = true;                                    // exit lanes are road lanes
+        f = first_ext(T, ext);
+        Lm = (R)T.ext[ext - T.nroad].Lb;
+      } else {
+        mroad = __ldg(A.lane_road + m) >= 0;
+        f = first_of(A, T, C, m);
+        Lm = (R)__ldg(A.lane_len + m);
+      }
       if (mroad) rel += 1;
-      First f = first_of(A, T, C, m);
       if (f.found) {
         e.has_leader = true;
         e.leader = f.vid;
@@ -328,10 +389,14 @@ __device__ LEv<R> eval_lane(const StepArgs &A, const TileSh &T, const View &C, i
         gscale = d + (R)f.s + (R)f.len;
         break;
       }
-      d = M::add(d, (R)__ldg(A.lane_len + m));
+      d = M::add(d, Lm);
       if (!mroad) {
-        m = __ldg(A.exit_lane + m);
+        if (own >= 0) { ext = own; m = xl_of(T, own); }
+        else m = __ldg(A.exit_lane + m);
+        own = -1;
       } else {
+        ext = -1;
+        own = -1;
         int R1 = route_at(A, me.vid, me.cur, me.nxt, me.nxt2, me.cur + rel + 1);
         int R2 = route_at(A, me.vid, me.cur, me.nxt, me.nxt2, me.cur + rel + 2);
         m = next_from_road_any(A, T, m, R1, R2);
@@ -352,6 +417,7 @@ __device__ LEv<R> eval_lane(const StepArgs &A, const TileSh &T, const View &C, i
   e.has_lim = false;
   e.lim = (R)0;
   e.vlim = (R)0;
+  e.limrel = (R)0;
   if (GUARD && e.phantom && e.has_leader &&
       fabsf((float)(L - lim_lead)) <= kEpsPos * (float)(L + fabs(lim_lead)))
     g.hit = true, g.why |= (1u << 1);
@@ -481,50 +547,26 @@ __device__ __noinline__ SideRes<R> lane_change(const StepArgs &A, const TileSh &
   return o;
 }
 
-// One vehicle's update O4-O9 reading only state(t).
+// ---- one vehicle's update O4-O9, reading only state(t) ----
+// Three pieces, so that the fp32 step kernel can run them as separate dense
+// passes and the fp64 canonical path runs them back to back
+// (veh_update): lc_elig + eval_lane (current lane), lc_decide (MOBIL, only
+// for vehicles that may change lane), integrate (O8-O9).
+
+struct Elig {                        // lane-change eligibility (L18, L19, L37)
+  int sl0, sl1, mand;
+  bool inG, want0, want1;
+};
+
 template <typename R, bool GUARD>
-__device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, int i, Res &o,
-                           Guard &g) {
+__device__ __forceinline__ Elig lc_elig(const StepArgs &A, const TileSh &T, int l, R s, R v,
+                                        const PV<R> &p, Me &me, Guard &g) {
   using M = Ar<R>;
-  const uint32_t meta = C.meta(i);
-  const int l = m_lane(meta), pr = m_prof(meta);
-  Me me;
-  me.vid = C.vid(i);
-  me.cur = m_cursor(meta);
-  int wait0;                                             // ego-only fields (slab or inbox)
-  {
-    const int si = C.src(i);
-    if (si >= 0) {
-      const int gi = T.base + si;
-      me.nxt = A.in.nxt[gi];
-      me.nxt2 = A.in.nxt2[gi];
-      wait0 = A.in.wait[gi];
-    } else {
-      const InboxRec *r = A.inbox_in + T.ibase + (-si - 1);
-      me.nxt = r->nxt;
-      me.nxt2 = r->nxt2;
-      wait0 = r->wait;
-    }
-  }
-  o.nxt = me.nxt;
-  o.nxt2 = me.nxt2;
-  const PV<R> p = pvals(T.P[pr], (R)0);
-  const R s = (R)C.s(i), v = (R)C.v(i);
+  Elig E;
   const R L = (R)T.len[l];
-  const int lead = (i + 1 < T.seg_end[l]) ? i + 1 : -1;
-  const int of = (i > T.seg_start[l]) ? i - 1 : -1;
-  // recorded decisions (test mode) go straight to their arrays, so none of
-  // them stays live in registers through the update
-  if (A.record) {
-    A.r_of[me.vid] = of >= 0 ? C.vid(of) : -1;
-    for (int q = 0; q < 4; ++q) A.r_side[4 * me.vid + q] = -1;
-  }
-  const R b_hard = (R)A.b_hard;
-  // ---- lane-change eligibility: needs no lane evaluation ----
-  const bool dest = me.nxt < 0;
   bool inG = true, consider = false, want0 = false, want1 = false;
-  int mand = 0;
-  int sl0 = -1, sl1 = -1, f0 = -1, f1 = -1, b0 = -1, b1 = -1;
+  int mand = 0, sl0 = -1, sl1 = -1;
+  const bool dest = me.nxt < 0;
   me.k = -1;
   if (T.isroad[l]) {                                     // no LC in junction lanes
     // road lanes of the tile leading to the next road: one bit each
@@ -553,18 +595,40 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
       want0 = sl0 >= 0 && ((W >> sl0) & 1u) && (inG || mand == -1);
       want1 = sl1 >= 0 && ((W >> sl1) & 1u) && (inG || mand == 1);
     }
+  }
+  E.sl0 = sl0;
+  E.sl1 = sl1;
+  E.mand = mand;
+  E.inG = inG;
+  E.want0 = want0;
+  E.want1 = want1;
+  return E;
+}
+
+// O7 for one vehicle: side pointers, admissibility,
+// politeness, the draw and the decision (lane_change).  choice -1: stay.
+template <typename R, bool GUARD>
+__device__ __forceinline__ SideRes<R> lc_decide(const StepArgs &A, const TileSh &T, const View &C,
+                                                int i, int l, R s, R v, const PV<R> &p, const Me &me,
+                                                const Elig &E, R a_cur, Guard &g) {
+  using M = Ar<R>;
+  const R b_hard = (R)A.b_hard;
+  const int sl0 = E.sl0, sl1 = E.sl1, mand = E.mand;
+  const bool inG = E.inG, want0 = E.want0, want1 = E.want1;
+  const int lead = (i + 1 < T.seg_end[l]) ? i + 1 : -1;
+  const int of = (i > T.seg_start[l]) ? i - 1 : -1;
+  int f0 = -1, f1 = -1, b0 = -1, b1 = -1;
 #pragma unroll 1
-    for (int sd = 0; sd < 2; ++sd) {                     // side pointers (ties -> back, L11)
-      const int ls = sd == 0 ? sl0 : sl1;
-      if (ls < 0 || !((sd == 0 ? want0 : want1) || A.record)) continue;
-      const int a = T.seg_start[ls], b = T.seg_end[ls];
-      const int f = upper_bound_s(C, a, b, C.s(i));
-      const int fr = f < b ? f : -1, bk = f > a ? f - 1 : -1;
-      if (sd == 0) { f0 = fr; b0 = bk; } else { f1 = fr; b1 = bk; }
-      if (A.record) {
-        A.r_side[4 * me.vid + 2 * sd] = fr >= 0 ? C.vid(fr) : -1;
-        A.r_side[4 * me.vid + 2 * sd + 1] = bk >= 0 ? C.vid(bk) : -1;
-      }
+  for (int sd = 0; sd < 2; ++sd) {                       // side pointers (ties -> back, L11)
+    const int ls = sd == 0 ? sl0 : sl1;
+    if (ls < 0 || !((sd == 0 ? want0 : want1) || A.record)) continue;
+    const int a = T.seg_start[ls], b = T.seg_end[ls];
+    const int f = upper_bound_s(C, a, b, C.s(i));
+    const int fr = f < b ? f : -1, bk = f > a ? f - 1 : -1;
+    if (sd == 0) { f0 = fr; b0 = bk; } else { f1 = fr; b1 = bk; }
+    if (A.record) {
+      A.r_side[4 * me.vid + 2 * sd] = fr >= 0 ? C.vid(fr) : -1;
+      A.r_side[4 * me.vid + 2 * sd + 1] = bk >= 0 ? C.vid(bk) : -1;
     }
   }
   // ---- MOBIL admissibility of each side, cheapest test first (gap signs,
@@ -665,29 +729,26 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
       }
     }
   }
-  // ---- O4-O6 on the current lane ----
-  LEv<R> use = eval_lane<R, GUARD>(A, T, C, l, lead, s, v, p, me, g);
-  if (A.record) {
-    A.r_leader[me.vid] = use.leader;
-    A.r_hops[me.vid] = (int8_t)use.hops;
-    A.r_phantom[me.vid] = (int8_t)use.phantom;
-  }
-  int lc = 0, new_l = l;
-  if (adm0 || adm1) {                                    // O7 decision (rare: out of line)
-    const SideRes<R> sr = lane_change<R, GUARD>(A, T, C, adm0, adm1, inG, mand, sl0, sl1, f0, f1,
-                                                s, v, p, me, use.a, pol0, pol1, r);
-    if (sr.hit) g.hit = true, g.why |= sr.why;
-    if (sr.choice >= 0) {
-      use.a = sr.a;
-      use.has_lim = sr.has_lim;
-      use.lim = sr.lim;
-      use.limrel = sr.limrel;
-      use.vlim = sr.vlim;
-      use.next1 = sr.next1;
-      lc = sr.choice == 0 ? -1 : 1;
-      new_l = sr.choice == 0 ? sl0 : sl1;
-    }
-  }
+  SideRes<R> sr;
+  sr.choice = -1;
+  sr.hit = false;
+  sr.why = 0;
+  if (adm0 || adm1)                                      // O7 decision
+    sr = lane_change<R, GUARD>(A, T, C, adm0, adm1, inG, mand, sl0, sl1, f0, f1, s, v, p, me,
+                               a_cur, pol0, pol1, r);
+  if (sr.hit) g.hit = true, g.why |= sr.why;
+  return sr;
+}
+
+// O8-O9 for one vehicle given its acceleration and clamp (after O7): the
+// ballistic update, the clamp, hand-off and arrival, the wait counter.
+template <typename R, bool GUARD>
+__device__ __forceinline__ void integrate(const StepArgs &A, const TileSh &T, R s, R v,
+                                          const Me &me, const LEv<R> &use, int lc, int new_l,
+                                          int wait0, Res &o, Guard &g) {
+  using M = Ar<R>;
+  o.nxt = me.nxt;
+  o.nxt2 = me.nxt2;
   // O8 integrate (ledger L1) + clamp (L22, L23).  The fp64 path follows the
   // canonical sequence (position s1); the fp32 path carries the position as
   // base + advance so that stop-line / hand-off decisions and the residual
@@ -774,6 +835,56 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
   o.lc = lc;
   o.hand = hand;
   o.fin = fin;
+}
+
+template <typename R, bool GUARD>
+__device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, int i, Res &o,
+                           Guard &g) {
+  const uint32_t meta = C.meta(i);
+  const int l = m_lane(meta), pr = m_prof(meta);
+  Me me;
+  me.vid = C.vid(i);
+  me.cur = m_cursor(meta);
+  me.nxt = C.nxt(i);                                     // ego-only fields
+  me.nxt2 = C.nxt2(i);
+  const int wait0 = C.wait(i);
+  const PV<R> p = pvals(T.P[pr], (R)0);
+  const R s = (R)C.s(i), v = (R)C.v(i);
+  const int lead = (i + 1 < T.seg_end[l]) ? i + 1 : -1;
+  // recorded decisions (test mode) go straight to their arrays
+  if (A.record) {
+    const int of = (i > T.seg_start[l]) ? i - 1 : -1;
+    A.r_of[me.vid] = of >= 0 ? C.vid(of) : -1;
+    for (int q = 0; q < 4; ++q) A.r_side[4 * me.vid + q] = -1;
+  }
+  Elig E;
+  E.sl0 = E.sl1 = -1;
+  E.mand = 0;
+  E.inG = true;
+  E.want0 = E.want1 = false;
+  me.k = -1;
+  if (T.isroad[l]) E = lc_elig<R, GUARD>(A, T, l, s, v, p, me, g);   // no LC in junction lanes
+  LEv<R> use = eval_lane<R, GUARD>(A, T, C, l, lead, s, v, p, me, g);   // O4-O6
+  if (A.record) {
+    A.r_leader[me.vid] = use.leader;
+    A.r_hops[me.vid] = (int8_t)use.hops;
+    A.r_phantom[me.vid] = (int8_t)use.phantom;
+  }
+  int lc = 0, new_l = l;
+  if (E.want0 || E.want1 || (A.record && T.isroad[l])) {
+    const SideRes<R> sr = lc_decide<R, GUARD>(A, T, C, i, l, s, v, p, me, E, use.a, g);
+    if (sr.choice >= 0) {
+      use.a = sr.a;
+      use.has_lim = sr.has_lim;
+      use.lim = sr.lim;
+      use.limrel = sr.limrel;
+      use.vlim = sr.vlim;
+      use.next1 = sr.next1;
+      lc = sr.choice == 0 ? -1 : 1;
+      new_l = sr.choice == 0 ? E.sl0 : E.sl1;
+    }
+  }
+  integrate<R, GUARD>(A, T, s, v, me, use, lc, new_l, wait0, o, g);
 }
 
 }  // namespace sim

@@ -300,7 +300,10 @@ void build_desc(sim_s *h) {
         ent.push_back(j);
         ent.push_back(h->target_road[j]);
         ent.push_back(b);
-        ent.push_back((is_road(h, j) ? 0 : 1) | (l << 8) | (k << 16));
+        // bits 24-31: tile-local index of j when j is a junction lane (it then
+        // belongs to this tile), 0xff for a direct road -> road link
+        const uint32_t jl = is_road(h, j) ? 0xffu : (uint32_t)h->lane_local[j];
+        ent.push_back((int32_t)((is_road(h, j) ? 0u : 1u) | ((uint32_t)l << 8) | ((uint32_t)k << 16) | (jl << 24)));
         for (int q = 0; q < 4; ++q) ent.push_back(h->outroads[4 * (size_t)b + q]);
       }
       if (ng <= kMaxGroups) gbeg[ng] = (uint8_t)js.size();
@@ -317,6 +320,9 @@ void build_desc(sim_s *h) {
     for (int l = 0; l < nl; ++l)
       w.push_back((h->usable[h->tile_lanes[l0 + l]] ? 1 : 0) |
                   (l < nroad ? (lane_sn[l] << 8) | (lane_ng[l] << 16) : 0));
+    // junction lanes: their exit lane (the producer warp of k_step gathers its
+    // first vehicle at t); road lanes: -1
+    for (int l = 0; l < nl; ++l) w.push_back(l < nroad ? -1 : h->exit_lane[h->tile_lanes[l0 + l]]);
     w.insert(w.end(), grp.begin(), grp.end());
     w.insert(w.end(), ent.begin(), ent.end());
     // pad to all successors so setters (which change the usable set) never
@@ -621,7 +627,7 @@ sim_status build_tiles(sim_s *h) {
       h->tile_lanes.push_back(lanes[k]);
       cap += lane_cap(lanes[k]);
     }
-    cap = cap + cap / 4 + 16;
+    cap = (cap + cap / 4 + 16 + 3) & ~3;            // multiple of 4: 16-B aligned bulk copies
     int icap = cap + feed[r] + h->tile_nroad[r] + 16;
     if (cap > 32767 || icap > 32767)                // snapshot source indices are int16
       return fail(h, SIM_E_INVALID, "road " + std::to_string(r) + " is too long (tile capacity > 32767 vehicles)");
@@ -968,7 +974,7 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
     CK(h, cudaMemset(P.pubv[b], 0, nv * 4));
   }
   const int64_t sc = h->sum_cap + h->sum_icap;
-  AL(A.scratch, 5 * sc);
+  AL(A.scratch, 7 * sc);
   AL(A.bsort_scratch, h->sum_icap);
   AL(A.dl_scratch, sc);
   for (int b = 0; b < 3; ++b) AL(P.summ[b], nl);
@@ -1431,7 +1437,7 @@ sim_status push_junction_requests(sim_s *h, int m, const int32_t *junctions, con
     CK(h, cudaEventRecord(h->stage_ev, h->stream));
     for (Part &P : h->parts) {
       int32_t *dst = kind == 0 ? P.SG.request : (kind == 1 ? P.SG.pol_request : P.SG.dur_request);
-      launch_apply_requests(dst, P.SG.policy, h->stage_d, h->stage_d + m, m, h->stream);
+      launch_apply_requests(dst, h->stage_d, h->stage_d + m, m, h->stream);
       h->n_launch++;
     }
     return SIM_OK;
@@ -1458,7 +1464,7 @@ sim_status push_junction_requests(sim_s *h, int m, const int32_t *junctions, con
   if (st) return st;
   for (Part &P : h->parts) {
     int32_t *dst = kind == 0 ? P.SG.request : (kind == 1 ? P.SG.pol_request : P.SG.dur_request);
-    launch_apply_requests(dst, P.SG.policy, h->stage_d, h->stage_d + u, u, h->stream);
+    launch_apply_requests(dst, h->stage_d, h->stage_d + u, u, h->stream);
     h->n_launch++;
   }
   return SIM_OK;
