@@ -14,6 +14,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.cpp")
 _LIB = os.path.join(_HERE, "liboracle.so")
+# scripts/oracle_mutations.py points this at a deliberately broken build
+_LIB_OVERRIDE = os.environ.get("ORACLE_LIB_OVERRIDE")
 
 
 def lib_path():
@@ -38,8 +40,11 @@ _lib = None
 def _load():
     global _lib
     if _lib is None:
-        build()
-        _lib = C.CDLL(_LIB)
+        if _LIB_OVERRIDE:
+            _lib = C.CDLL(_LIB_OVERRIDE)
+        else:
+            build()
+            _lib = C.CDLL(_LIB)
         _lib.or_create.restype = C.c_void_p
         _lib.or_create.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_char_p, C.c_int32]
         for f in ("or_destroy",):
