@@ -29,14 +29,20 @@ constexpr int kMaxRoadLanes = 4;     // road lanes per tile cached in the succes
 constexpr int kMaxSucc = 8;          // successors per road lane cached in the table
 static_assert(kMaxRoadLanes * kMaxSucc == 32, "one warp builds the successor table");
 // tile descriptor (int32 words, 16-B padded, host-built by build_desc and
-// rebuilt after setters): [nl, nroad, ne, 0], glob[nl], len[nl], vmax[nl],
+// rebuilt after setters): [nl, nroad, ne, n_all], glob[nl], len[nl], vmax[nl],
 // flags[nl] (bit0 usable; road lanes: usable successors << 8, groups << 16),
 // xl[nl] (junction lanes: exit lane, road lanes -1), per road lane 6 words (gbeg[0..3] bytes, gbeg[4], gtroad[0..3]), then the
 // ne <= 32 usable successors of the road lanes sorted by (lane, target road,
 // lane id), 8 words each: j, target road, exit lane, flags (bit0 junction lane,
-// lane_local << 8, rank k << 16), outroads(exit lane) x4
-constexpr int kDescMaxWords = 4 + 5 * kMaxTileLanes + 6 * kMaxRoadLanes + 8 * kMaxRoadLanes * kMaxSucc;
+// lane_local << 8, rank k << 16), outroads(exit lane) x4, padded to n_all
+// entries; then the target-road section (kDescTroadWords)
 constexpr int kMaxGroups = 4;        // distinct target roads per road lane in the table
+// target-road section at the end of a descriptor: ntr, umask, troad[16],
+// reach[16] (bytes), gidx[4][16] (bytes)
+constexpr int kDescTroadWords = 2 + kMaxRoadLanes * kMaxGroups + (kMaxRoadLanes * kMaxGroups) / 4 +
+                                (kMaxRoadLanes * kMaxRoadLanes * kMaxGroups) / 4;
+constexpr int kDescMaxWords = 4 + 5 * kMaxTileLanes + 6 * kMaxRoadLanes + 8 * kMaxRoadLanes * kMaxSucc +
+                              kDescTroadWords + 3;
 constexpr int kSmemProf = 8;         // profiles staged in shared memory
 constexpr uint64_t kEmptyKey = ~0ull;
 
@@ -165,6 +171,16 @@ struct StepArgs {
   uint32_t *scratch;                // snapshot of large tiles, at 5 x (base + ibase) words: s, v, vid, meta (stride cap + icap), then int16 src
   int32_t *bsort_scratch;           // [Σ icap] inbox sort order for large inboxes
   int32_t *dl_scratch;              // per-tile list of guard-deferred vehicles (scratch indexing)
+  // per tile, static (host-built): {base, ibase, cap, icap}, {desc_off, desc words,
+  // lanes, road lanes}, {ext offset, pend offset, 0, 0} (records of ext_buf / pend_buf)
+  const int4 *tinfo;
+  // k_prep output for k_step: per junction lane of a tile the
+  // signal and the exit lane's first vehicle at t, per road lane the head of
+  // its pending-departure queue at t; contiguous per tile
+  ExtFirst *ext_buf;
+  PendHead *pend_buf;
+  uint32_t *pscratch;               // pass state of tiles in global mode: 10 words per slot at
+                                    // 10 x (base + ibase + 4 x tile)
   // migration to other partitions (world > 1): per-peer regions of MigRec
   MigRec *out_buf;
   const int32_t *out_off, *out_cap;
@@ -225,6 +241,7 @@ struct SignalArgs {
 // kernel launchers (kernels.cu)
 void launch_signal(const SignalArgs &a, void *stream);
 void launch_step(const StepArgs &a, void *stream, int smem_bytes);
+void launch_prep(const StepArgs &a, void *stream);
 int step_smem_bytes();
 void launch_apply_requests(int32_t *request, const int32_t *junc, const int32_t *phase, int m,
                            void *stream);

@@ -1,35 +1,35 @@
 // kstep.cu — the fused step kernel k_step (rows a0-a4, a6).
 //
-// A warp-specialised persistent kernel.  Each CTA has one PRODUCER warp and
-// kCW CONSUMER warps and works through BATCHES of road tiles (a tile = one
-// road's lanes + the junction lanes leaving it, dev.h):
+// A warp-specialised persistent kernel, one CTA per SM.  One PRODUCER warp
+// feeds kCW autonomous CONSUMER warps through a ring of tile slots in shared
+// memory (a tile = one road's lanes + the junction lanes leaving it, dev.h):
 //
-//   producer  claims tiles from a global work counter (largest first), packs
-//             consecutive ones into a batch of at most kBatch vehicles, and
-//             streams the batch's stayer slab segments, inbox records and
-//             tile descriptors into a shared-memory stage with 1-D bulk copies
-//             (cp.async.bulk + mbarrier complete_tx).  It also gathers what
-//             the batch needs from other tiles — the first vehicle of every
-//             junction lane's exit lane at t (the P:168-169 lookahead target),
-//             the junction lanes' signals, the heads of the pending-departure
-//             queues — so the consumers' critical path has no global loads in
-//             the common case.  kStages stages form a ring (full / empty
-//             mbarriers), so batch b+1 streams in while batch b is computed.
-//   consumers run the batch in dense phases separated by a named barrier:
-//             tile metadata; merge of in-order stayers + sorted inbox into
-//             the snapshot (a1); pass 1 = eligibility +
-//             leader / lookahead + IDM on the current lane for every vehicle
-//             (a2, a3); pass 2 = MOBIL for the compacted list of vehicles that
-//             may change lane; pass 3 = integrate / hand-off /
-//             arrival (a4) with movers emitted to their destination inbox;
-//             the fp64 canonical recomputation of vehicles whose fp32 margins
-//             fell inside the guard band; then per tile the
+//   producer  claims tiles from a global work counter (largest first), gives
+//             each a variable-size slot in a byte ring (ring entries with full /
+//             empty mbarriers, freed in order) and streams the tile's stayer
+//             slab segment, inbox records and descriptor into it with 1-D bulk
+//             copies (cp.async.bulk + mbarrier complete_tx), together with
+//             what k_prep staged for it from other tiles — the first vehicle
+//             of every junction lane's exit lane at t (the P:168-169 lookahead
+//             target), the junction lanes' signals, the heads of the
+//             pending-departure queues — so the consumers' common path has no
+//             global loads.
+//   consumers each take the next slot in order and run the whole tile alone,
+//             with no block-wide barrier: tile metadata; merge of in-order
+//             stayers + sorted inbox into the snapshot (a1);
+//             pass 1 = eligibility + leader / lookahead + IDM on the current
+//             lane for every vehicle (a2, a3); pass 2 = MOBIL for the compacted
+//             list of vehicles that may change lane; pass 3 =
+//             integrate / hand-off / arrival (a4) with movers emitted to their
+//             destination inbox; the fp64 canonical recomputation of vehicles
+//             whose fp32 margins fell inside the guard band; the
 //             in-order compaction of stayers, lane summaries for t+1,
-//             departures (K11) and counters (a6).
+//             departures (K11) and counters (a6).  The snapshot and the
+//             per-vehicle pass state live in the tile's own slot.
 //
 // Every decision reads only state(t) (the snapshot) and all
 // cross-tile outputs are integer atomics into the t+1 buffers, so the result
-// does not depend on which CTA takes which tile or in what order.
+// does not depend on which CTA or warp takes which tile or in what order.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -40,74 +40,87 @@
 namespace sim {
 
 #ifndef KS_CONS_WARPS
-#define KS_CONS_WARPS 8
+#define KS_CONS_WARPS 12
 #endif
-#ifndef KS_BATCH
-#define KS_BATCH 352
+#ifndef KS_RING_KB
+#define KS_RING_KB 190
 #endif
-#ifndef KS_MAXT
-#define KS_MAXT 10
-#endif
-#ifndef KS_STAGES
-#define KS_STAGES 2
+#ifndef KS_MINB
+#define KS_MINB 1
 #endif
 constexpr int kCW = KS_CONS_WARPS;            // consumer warps
-constexpr int kCT = kCW * 32;                 // consumer threads
-constexpr int kStepThreads = kCT + 32;        // + the producer warp (the last warp)
-constexpr int kBatch = KS_BATCH;              // vehicle slots of a batch
-constexpr int kMaxT = KS_MAXT;                // tiles per batch
-constexpr int kStages = KS_STAGES;
-constexpr int kInPool = 160;                  // inbox records per batch
-constexpr int kDescPool = 1280;               // descriptor words per batch
-constexpr int kXPool = 80;                    // junction lanes per batch (gathered exit-lane firsts)
-constexpr int kPPool = 40;                    // road lanes per batch (pending-queue heads)
-constexpr int kSlabWords = 7 * kBatch + 7 * 3 * kMaxT;   // stayer fields, each padded to 4 elements
+constexpr int kStepThreads = (kCW + 1) * 32;  // + the producer warp (the last warp)
+constexpr int kRing = KS_RING_KB * 1024;      // slot ring bytes
+constexpr int kNH = 32;                       // ring entries (slot headers)
 constexpr int kGroup = 16;                    // tiles claimed from the work counter at a time
-constexpr int kCBar = 1;                      // named barrier of the consumer warps
-static_assert(kBatch % 32 == 0 && kBatch < 32768, "batch slots");
+static_assert(kCW <= kNH, "ring entries");
 static_assert(kGroup * 2 <= 32, "the producer warp holds two groups");
 
-struct BatchHdr {
-  int nt, gmode, done, nveh, nst, nin;
-  int tile[kMaxT], n_st[kMaxT], n_in[kMaxT], base[kMaxT], ibase[kMaxT], cap[kMaxT], icap[kMaxT];
-  int nl[kMaxT], nroad[kMaxT], doff[kMaxT], dw[kMaxT];
-  int slab[kMaxT], r4[kMaxT];       // stage word offset of the tile's 7 stayer arrays, their stride
-  int in0[kMaxT];                   // flat inbox offset (stage record offset)
-  int st0[kMaxT];                   // flat stayer offset
-  int desc[kMaxT];                  // stage word offset of the descriptor
-  int xo[kMaxT], po[kMaxT];         // gather offsets (junction lanes, road lanes)
-  int snap0[kMaxT];                 // flat snapshot offset
+// Byte layout of one tile slot (all offsets 16-B aligned).  A tile too large
+// for the ring (> kRing / 2) runs in global mode: its slot holds only the
+// descriptor and the gathered ext / pend records, the snapshot and pass state
+// live in the global scratch arrays.
+struct SlotLayout {
+  uint32_t slab, inbox, desc, ext, pend, snap, st, sortk, size;
+  int r4, n4;
 };
+__device__ __forceinline__ SlotLayout slot_layout(int n_st, int n_in, int dw, int nj, int nroad) {
+  SlotLayout L;
+  L.r4 = (n_st + 3) & ~3;
+  L.n4 = (n_st + n_in + 3) & ~3;
+  uint32_t o = 0;
+  L.slab = o;  o += 28u * (uint32_t)L.r4;              // 7 stayer arrays (s v vid nxt nxt2 meta wait)
+  L.inbox = o; o += 32u * (uint32_t)n_in;
+  L.desc = o;  o += 4u * (uint32_t)dw;                 // dw is a multiple of 4
+  L.ext = o;   o += 32u * (uint32_t)nj;
+  L.pend = o;  o += 32u * (uint32_t)nroad;
+  L.snap = o;  o += 28u * (uint32_t)L.n4;              // merged snapshot (View, stride n4)
+  L.st = o;    o += 40u * (uint32_t)L.n4;              // pass state (PState)
+  L.sortk = o; o += 16u * (uint32_t)n_in;              // sorted inbox keys
+  L.size = o;
+  return L;
+}
 
-struct __align__(16) Stage {
+struct __align__(16) Hdr {          // one ring entry
   unsigned long long full, empty;   // mbarriers
-  BatchHdr H;
-  __align__(16) uint32_t slab[kSlabWords];
-  InboxRec inbox[kInPool];
-  __align__(16) int32_t desc[kDescPool];
-  ExtFirst ext[kXPool];
-  PendHead pend[kPPool];
+  int tile, n_st, n_in, base, ibase, cap, icap, nl, nroad, dw;
+  int gm, done;                     // global mode / end-of-work sentinel
+  uint32_t off;                     // slot byte offset in the ring
+  int pad;
 };
 
-struct __align__(16) Cons {
-  uint32_t snap[7 * kBatch];        // snapshot of the batch (View)
-  float rs1[kBatch], rv1[kBatch];   // stayer results
-  float pa[kBatch], plim[kBatch], plimrel[kBatch], pvlim[kBatch];   // pass state
-  int pnext1[kBatch];
-  uint32_t pfl[kBatch];
-  uint8_t tix[kBatch], kind[kBatch];
-  uint16_t cand[kBatch], defl[kBatch];
-  unsigned long long skh[kInPool];  // inbox keys per tile, sorted
-  int skv[kInPool], bs[kInPool];
-  int ncand, ndef;
-  TileSh T[kMaxT];
+// per-vehicle pass state of one tile (slot in shared memory, or the global
+// pass scratch for a tile in global mode), indexed by snapshot position
+struct PState {
+  float *pa, *plim, *plimrel, *pvlim, *rs1, *rv1;
+  int *pnext1;
+  uint32_t *pfl;
+  uint8_t *kind;
+  uint16_t *cand, *defl;
+};
+__device__ __forceinline__ PState pstate_at(unsigned char *p, int n4) {
+  PState S;
+  float *f = reinterpret_cast<float *>(p);
+  S.pa = f; S.plim = f + n4; S.plimrel = f + 2 * n4; S.pvlim = f + 3 * n4;
+  S.rs1 = f + 4 * n4; S.rv1 = f + 5 * n4;
+  S.pnext1 = reinterpret_cast<int *>(f + 6 * n4);
+  S.pfl = reinterpret_cast<uint32_t *>(f + 7 * n4);
+  S.kind = reinterpret_cast<uint8_t *>(f + 8 * n4);
+  S.cand = reinterpret_cast<uint16_t *>(S.kind + n4);
+  S.defl = S.cand + n4;
+  return S;
+}
+
+struct __align__(128) StepSmem {
+  Hdr H[kNH];
+  int next_seq;
+  int pad[3];
   Prof prof[kSmemProf];
+  TileSh T[kCW];
+  __align__(128) unsigned char ring[kRing];
 };
 
-struct StepSmem {
-  Stage S[kStages];
-  Cons C;
-};
+static_assert(sizeof(StepSmem) <= 227 * 1024, "one CTA per SM: at most 227 KB of shared memory");
 
 // pass-state flag bits
 enum : uint32_t {
@@ -151,9 +164,44 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ void cbar() {
-  asm volatile("bar.sync %0, %1;" ::"r"(kCBar), "r"(kCT) : "memory");
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// producer-side wait on an `empty` barrier: back off instead of spinning so
+// the waiting producer does not take issue slots from the consumers
+__device__ __forceinline__ void mbar_wait_sleep(unsigned long long *b, unsigned parity) {
+  unsigned ok = 0;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(64);
+  }
+}
+
+// ---- phase profiling (dev builds with -DKS_PROF; sim_debug_kstep_prof) ----------
+#ifdef KS_PROF
+__device__ unsigned long long g_ks_prof[32];
+#define KP_DECL long long kp_last = clock64();
+#define KP(idx, on)                                                    \
+  do {                                                                 \
+    if (on) {                                                          \
+      const long long kp_now = clock64();                              \
+      atomicAdd(&g_ks_prof[idx], (unsigned long long)(kp_now - kp_last)); \
+      kp_last = kp_now;                                                \
+    }                                                                  \
+  } while (0)
+#define KPN(idx, on, n) do { if (on) atomicAdd(&g_ks_prof[idx], (unsigned long long)(n)); } while (0)
+#else
+#define KP_DECL
+#define KP(idx, on) do {} while (0)
+#define KPN(idx, on, n) do {} while (0)
+#endif
 
 // ---- small helpers -----------------------------------------------------------
 __device__ __forceinline__ unsigned long long vkey(float s, int vid) {
@@ -284,219 +332,256 @@ __device__ __noinline__ void emit_moved(const StepArgs &A, const View &C, int i,
   }
 }
 
-// ---- producer warp --------------------------------------------------------------
-struct TInfo { int tile, n_st, n_in, base, ibase, cap, icap, doff, dw, nl, nroad; };
+// ---- k_prep: what k_step reads from other tiles, staged per tile -----------------------
+// One warp per own tile, one lane per tile lane (<= 32).  Junction lane: its
+// signal at t and the first vehicle of its exit lane at t (the P:168-169
+// lookahead target one lane beyond the tile: summary key, speed, length);
+// road lane: the head of its pending-departure queue at t (K11).
+// Written contiguously per tile into ext_buf / pend_buf, from where k_step's
+// producer warp bulk-copies them with the tile.  Runs after k_signal (the
+// signals of t) and reads only state(t).
+__global__ void __launch_bounds__(128) k_prep(const __grid_constant__ StepArgs A) {
+  const int w = blockIdx.x * 4 + (threadIdx.x >> 5), l = threadIdx.x & 31;
+  if (w >= A.n_own) return;
+  const int T = A.tiles[w];
+  const int4 t1 = A.tinfo[3 * T + 1], t2 = A.tinfo[3 * T + 2];
+  const int nl = t1.z, nroad = t1.w;
+  if (l >= nl) return;
+  const int g = A.tile_lanes[A.tile_lane_off[T] + l];
+  if (l >= nroad) {                                 // junction lane
+    const int b = A.exit_lane[g];
+    ExtFirst e;
+    e.sig = A.lane_sig[g];
+    e.b = b;
+    e.Lb = A.lane_len[b];
+    e.pad = 0;
+    unsigned long long key;
+    const float *pv = A.pubv_cur;
+    if (!A.peers) {
+      key = A.summ_cur[b];
+    } else {
+      const int bt = A.lane_tile[b];
+      if (A.tile_owner[bt] == A.rank) key = A.summ_cur[b];
+      else key = peer_summary(A, bt, b, pv);
+    }
+    e.vid = -1;
+    e.s = e.v = e.len = 0.f;
+    if (key != kEmptyKey) {
+      e.vid = (int)(unsigned)(key & 0xffffffffu);
+      e.s = __uint_as_float((unsigned)(key >> 32));
+      e.v = pv[e.vid];
+      e.len = A.prof[A.veh_prof[e.vid]].len;
+    }
+    A.ext_buf[t2.x + l - nroad] = e;
+  } else {                                          // road lane
+    PendHead ph;
+    ph.k = -1;
+    ph.depart = ph.prof = 0;
+    ph.start_s = 0.f;
+    ph.pad[0] = ph.pad[1] = ph.pad[2] = 0;
+    const int h = A.pend_head[g];
+    ph.h = h;
+    if (h < A.pend_off[g + 1]) {
+      const int vk = A.pend_vid[h];
+      const int dep = A.depart[vk];
+      if (dep <= A.t) {
+        ph.k = vk;
+        ph.depart = dep;
+        ph.start_s = A.start_s[vk];
+        ph.prof = A.veh_prof[vk];
+      }
+    }
+    A.pend_buf[t2.y + l] = ph;
+  }
+}
 
-__device__ __forceinline__ TInfo load_tinfo(const StepArgs &A, int idx) {
+void launch_prep(const StepArgs &a, void *stream) {
+  if (a.n_own <= 0) return;
+  k_prep<<<(a.n_own + 3) / 4, 128, 0, (cudaStream_t)stream>>>(a);
+}
+
+// ---- producer warp --------------------------------------------------------------------
+// The tiles this CTA will take, claimed kGroup at a time from the work counter
+// and prefetched: `cur` is being published, `nxt` has its fields in flight,
+// `ids` holds the tile ids of the group after (lane q < kGroup: tile q).
+struct TInfo { int tile, n_st, n_in; int4 t0, t1, t2; };
+__device__ __forceinline__ int claim_ids(const StepArgs &A, int lane) {
+  int c = 0;
+  if (lane == 0) c = atomicAdd(&A.work[0], kGroup);
+  c = __shfl_sync(0xffffffffu, c, 0) + (lane & (kGroup - 1));
+  return (lane < kGroup && c < A.n_own) ? A.tiles[c] : -1;
+}
+__device__ __forceinline__ TInfo load_fields(const StepArgs &A, int t) {
   TInfo x;
-  x.tile = -1;
-  x.n_st = x.n_in = x.base = x.ibase = x.cap = x.icap = x.doff = x.dw = x.nl = x.nroad = 0;
-  if (idx < A.n_own) {
-    const int t = A.tiles[idx];
-    x.tile = t;
+  x.tile = t;
+  x.n_st = x.n_in = 0;
+  x.t0 = x.t1 = x.t2 = make_int4(0, 0, 0, 0);
+  if (t >= 0) {
     x.n_st = A.cnt_in[t];
     x.n_in = A.icnt_in[t];
-    x.base = A.tile_base[t];
-    x.ibase = A.tile_ibase[t];
-    x.cap = A.tile_cap[t];
-    x.icap = A.tile_icap[t];
-    x.doff = A.desc_off[t];
-    x.dw = A.desc_off[t + 1] - x.doff;
-    x.nl = A.tile_lane_off[t + 1] - A.tile_lane_off[t];
-    x.nroad = A.tile_nroad[t];
+    x.t0 = A.tinfo[3 * t];
+    x.t1 = A.tinfo[3 * t + 1];
+    x.t2 = A.tinfo[3 * t + 2];
   }
   return x;
+}
+__device__ __forceinline__ int4 shfl4(const int4 &v, int src) {
+  return make_int4(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
+                   __shfl_sync(0xffffffffu, v.z, src), __shfl_sync(0xffffffffu, v.w, src));
 }
 __device__ __forceinline__ TInfo shfl_tinfo(const TInfo &x, int src) {
   TInfo y;
   y.tile = __shfl_sync(0xffffffffu, x.tile, src);
   y.n_st = __shfl_sync(0xffffffffu, x.n_st, src);
   y.n_in = __shfl_sync(0xffffffffu, x.n_in, src);
-  y.base = __shfl_sync(0xffffffffu, x.base, src);
-  y.ibase = __shfl_sync(0xffffffffu, x.ibase, src);
-  y.cap = __shfl_sync(0xffffffffu, x.cap, src);
-  y.icap = __shfl_sync(0xffffffffu, x.icap, src);
-  y.doff = __shfl_sync(0xffffffffu, x.doff, src);
-  y.dw = __shfl_sync(0xffffffffu, x.dw, src);
-  y.nl = __shfl_sync(0xffffffffu, x.nl, src);
-  y.nroad = __shfl_sync(0xffffffffu, x.nroad, src);
+  y.t0 = shfl4(x.t0, src);
+  y.t1 = shfl4(x.t1, src);
+  y.t2 = shfl4(x.t2, src);
   return y;
 }
 
-__device__ __noinline__ void producer(const StepArgs &A, StepSmem &M, const Prof *P, int lane) {
-  int stage = 0;
-  unsigned phase = 0;
-  // lanes 0..15 hold the current group of claimed tiles, lanes 16..31 the next
-  int gb = 0;
-  if (lane == 0) gb = atomicAdd(&A.work[0], kGroup);
-  gb = __shfl_sync(0xffffffffu, gb, 0);
-  int nb = 0;
-  if (lane == 0) nb = atomicAdd(&A.work[0], kGroup);
-  nb = __shfl_sync(0xffffffffu, nb, 0);
-  TInfo mine = load_tinfo(A, (lane < kGroup ? gb : nb) + (lane & (kGroup - 1)));
-  int gpos = 0;
+__device__ __noinline__ void producer(const StepArgs &A, StepSmem &M, int lane) {
+  TInfo cur = load_fields(A, claim_ids(A, lane));
+  int ids = claim_ids(A, lane);
+  TInfo nxt = load_fields(A, ids);
+  ids = claim_ids(A, lane);
+  int pos = 0;
   bool exhausted = false;
+  int n_sent = 0;                                   // end-of-work sentinels published
+  unsigned long long head = 0, tail = 0;            // ring bytes allocated / freed (monotonic)
+  unsigned long long ent_end = 0;                   // lane e: end (head) of entry e's slot
+  bool fenced = true;                               // no bytes freed since the last proxy fence
+  int seq = 0, tail_seq = 0;
+  KP_DECL
   for (;;) {
-    Stage &S = M.S[stage];
-    BatchHdr &H = S.H;
-    mbar_wait(&S.empty, phase ^ 1u);                 // the consumers released the stage
-    int nt = 0, nveh = 0, nin = 0, nst = 0, nd = 0, nx = 0, np = 0, sw = 0, gm = 0;
-    unsigned tx = 0;
-    while (!exhausted) {
-      if (gpos == kGroup) {                          // next group: shift and claim another
-        TInfo up = shfl_tinfo(mine, (lane + kGroup) & 31);
-        int c = 0;
-        if (lane == 0) c = atomicAdd(&A.work[0], kGroup);
-        c = __shfl_sync(0xffffffffu, c, 0);
-        TInfo fresh = load_tinfo(A, c + (lane & (kGroup - 1)));
-        mine = lane < kGroup ? up : fresh;
-        gpos = 0;
+    TInfo x;
+    x.tile = -1;
+    if (!exhausted) {
+      if (pos == kGroup) {                           // next group
+        cur = nxt;
+        nxt = load_fields(A, ids);
+        ids = claim_ids(A, lane);
+        pos = 0;
       }
-      const TInfo x = shfl_tinfo(mine, gpos);
-      if (x.tile < 0) { exhausted = true; break; }
-      const int n = x.n_st + x.n_in, r4 = (x.n_st + 3) & ~3, nj = x.nl - x.nroad;
-      const bool big = n > kBatch || x.n_in > kInPool || x.dw > kDescPool || nj > kXPool ||
-                       x.nroad > kPPool || 7 * r4 > kSlabWords;
-      if (big && nt > 0) break;                      // a large tile goes alone (global mode)
-      if (!big && (nt == kMaxT || nveh + n > kBatch || nin + x.n_in > kInPool || nd + x.dw > kDescPool ||
-                   nx + nj > kXPool || np + x.nroad > kPPool || sw + 7 * r4 > kSlabWords))
-        break;
-      if (lane == 0) {
-        H.tile[nt] = x.tile; H.n_st[nt] = x.n_st; H.n_in[nt] = x.n_in; H.base[nt] = x.base;
-        H.ibase[nt] = x.ibase; H.cap[nt] = x.cap; H.icap[nt] = x.icap; H.nl[nt] = x.nl;
-        H.nroad[nt] = x.nroad; H.doff[nt] = x.doff; H.dw[nt] = x.dw;
-        H.slab[nt] = sw; H.r4[nt] = r4; H.in0[nt] = nin; H.st0[nt] = nst; H.desc[nt] = nd;
-        H.xo[nt] = nx; H.po[nt] = np; H.snap0[nt] = nveh;
-      }
-      if (!big) {
-        tx += (x.n_st > 0 ? 7u * 4u * (unsigned)r4 : 0u) + 32u * (unsigned)x.n_in + 4u * (unsigned)x.dw;
-        sw += 7 * r4;
-        nin += x.n_in;
-        nd += x.dw;
-      }
-      nt += 1;
-      nveh += n;
-      nst += x.n_st;
-      nx += nj;
-      np += x.nroad;
-      gpos += 1;
-      if (big) { gm = 1; break; }
+      x = shfl_tinfo(cur, pos);
+      if (x.tile < 0) exhausted = true;
     }
+    const bool sentinel = exhausted;
+    if (sentinel && n_sent == kCW) break;
+    const int base = x.t0.x, ibase = x.t0.y, cap = x.t0.z, icap = x.t0.w;
+    const int doff = x.t1.x, dw = x.t1.y, nl = x.t1.z, nroad = x.t1.w, nj = nl - nroad;
+    SlotLayout L = slot_layout(x.n_st, x.n_in, dw, nj, nroad);
+    bool gm = false;
+    if (sentinel) {
+      L.size = 0;
+    } else if (L.size > (uint32_t)(kRing / 2)) {     // too large for the ring: global mode
+      gm = true;
+      L = slot_layout(0, 0, dw, nj, nroad);
+    }
+    const unsigned long long size = L.size;
+    // an entry and contiguous bytes; the oldest slots are freed in order
+    KP(1, lane == 0);
+    for (;;) {
+      const unsigned long long p = head % kRing;
+      const unsigned long long waste = (p + size > (unsigned long long)kRing) ? kRing - p : 0;
+      if (seq - tail_seq < kNH && head + waste + size - tail <= (unsigned long long)kRing) break;
+      const int e = tail_seq % kNH;
+      mbar_wait_sleep(&M.H[e].empty, (unsigned)(tail_seq / kNH) & 1u);
+      tail = __shfl_sync(0xffffffffu, ent_end, e);
+      tail_seq += 1;
+      fenced = false;
+    }
+    KP(0, lane == 0);
+    {
+      const unsigned long long p = head % kRing;
+      if (p + size > (unsigned long long)kRing) head += kRing - p;
+    }
+    const uint32_t off = (uint32_t)(head % kRing);
+    head += size;
+    const int e = seq % kNH;
+    if (lane == e) ent_end = head;
+    Hdr &H = M.H[e];
     if (lane == 0) {
-      H.nt = nt; H.gmode = gm; H.done = nt == 0; H.nveh = nveh; H.nst = nst; H.nin = nin;
-      mbar_arrive_tx(&S.full, gm ? 0u : tx);
+      H.tile = x.tile; H.n_st = x.n_st; H.n_in = x.n_in; H.base = base; H.ibase = ibase;
+      H.cap = cap; H.icap = icap; H.nl = nl; H.nroad = nroad; H.dw = dw;
+      H.gm = gm ? 1 : 0;
+      H.done = sentinel ? 1 : 0;
+      H.off = off;
+      unsigned tx = 0;
+      if (!sentinel) {
+        tx = 4u * (unsigned)dw + 32u * (unsigned)(nj + nroad);
+        if (!gm) tx += (x.n_st > 0 ? 28u * (unsigned)L.r4 : 0u) + 32u * (unsigned)x.n_in;
+        if (!fenced) fence_proxy_async();            // generic writes of the freed slots' last use
+      }
+      mbar_arrive_tx(&H.full, tx);                   // the single arrival; copies complete the phase
     }
+    if (!sentinel) fenced = true;
     __syncwarp();
-    if (nt == 0) {                                   // no more work: tell the consumers
-      if (lane == 0) mbar_arrive(&S.full);
-      break;
-    }
-    if (!gm && lane < nt) {                          // bulk copies of tile `lane`
-      const int k = lane;
-      const int ns = H.n_st[k], ni = H.n_in[k], b0 = H.base[k], r4 = H.r4[k];
-      if (ns > 0) {
-        uint32_t *d = S.slab + H.slab[k];
-        const unsigned by = 4u * (unsigned)r4;
-        bulk_g2s(d + 0 * r4, A.in.s + b0, by, &S.full);
-        bulk_g2s(d + 1 * r4, A.in.v + b0, by, &S.full);
-        bulk_g2s(d + 2 * r4, A.in.vid + b0, by, &S.full);
-        bulk_g2s(d + 3 * r4, A.in.nxt + b0, by, &S.full);
-        bulk_g2s(d + 4 * r4, A.in.nxt2 + b0, by, &S.full);
-        bulk_g2s(d + 5 * r4, A.in.meta + b0, by, &S.full);
-        bulk_g2s(d + 6 * r4, A.in.wait + b0, by, &S.full);
+    if (!sentinel) {                                 // bulk copies, one per lane
+      unsigned char *slot = M.ring + off;
+      const int r4 = L.r4;
+      if (!gm && x.n_st > 0 && lane < 7) {
+        const void *src = lane == 0 ? (const void *)(A.in.s + base)
+                        : lane == 1 ? (const void *)(A.in.v + base)
+                        : lane == 2 ? (const void *)(A.in.vid + base)
+                        : lane == 3 ? (const void *)(A.in.nxt + base)
+                        : lane == 4 ? (const void *)(A.in.nxt2 + base)
+                        : lane == 5 ? (const void *)(A.in.meta + base)
+                                    : (const void *)(A.in.wait + base);
+        bulk_g2s(slot + L.slab + 4u * (uint32_t)(lane * r4), src, 4u * (unsigned)r4, &H.full);
       }
-      if (ni > 0) bulk_g2s(S.inbox + H.in0[k], A.inbox_in + H.ibase[k], 32u * (unsigned)ni, &S.full);
-      bulk_g2s(S.desc + H.desc[k], A.desc + H.doff[k], 4u * (unsigned)H.dw[k], &S.full);
+      if (!gm && x.n_in > 0 && lane == 7)
+        bulk_g2s(slot + L.inbox, A.inbox_in + ibase, 32u * (unsigned)x.n_in, &H.full);
+      if (lane == 8) bulk_g2s(slot + L.desc, A.desc + doff, 4u * (unsigned)dw, &H.full);
+      if (lane == 9 && nj > 0) bulk_g2s(slot + L.ext, A.ext_buf + x.t2.x, 32u * (unsigned)nj, &H.full);
+      if (lane == 10 && nroad > 0) bulk_g2s(slot + L.pend, A.pend_buf + x.t2.y, 32u * (unsigned)nroad, &H.full);
+      pos += 1;
+    } else {
+      n_sent += 1;
     }
-    // gathers (global loads, off the consumers' critical path): per junction
-    // lane its signal at t and the first vehicle of its exit lane at t
-    for (int q = lane; q < nx; q += 32) {
-      int k = 0;
-      while (k + 1 < nt && H.xo[k + 1] <= q) ++k;
-      const int nl = H.nl[k], l = H.nroad[k] + (q - H.xo[k]);
-      const int *W = A.desc + H.doff[k];
-      const int g = W[4 + l], b = W[4 + 4 * nl + l];
-      ExtFirst e;
-      e.sig = A.lane_sig[g];
-      e.b = b;
-      e.Lb = A.lane_len[b];
-      e.pad = 0;
-      unsigned long long key;
-      const float *pv = A.pubv_cur;
-      if (!A.peers) {
-        key = A.summ_cur[b];
-      } else {
-        const int bt = A.lane_tile[b];
-        const int ow = A.tile_owner[bt];
-        if (ow == A.rank) key = A.summ_cur[b];
-        else key = peer_summary(A, bt, b, pv);
-      }
-      e.vid = -1;
-      e.s = e.v = e.len = 0.f;
-      if (key != kEmptyKey) {
-        e.vid = (int)(unsigned)(key & 0xffffffffu);
-        e.s = __uint_as_float((unsigned)(key >> 32));
-        e.v = pv[e.vid];
-        e.len = P[A.veh_prof[e.vid]].len;
-      }
-      S.ext[q] = e;
-    }
-    // heads of the pending-departure queues of the road lanes (K11)
-    for (int q = lane; q < np; q += 32) {
-      int k = 0;
-      while (k + 1 < nt && H.po[k + 1] <= q) ++k;
-      const int l = q - H.po[k];
-      const int g = A.desc[H.doff[k] + 4 + l];
-      PendHead ph;
-      ph.k = -1;
-      ph.depart = ph.prof = 0;
-      ph.start_s = 0.f;
-      ph.pad[0] = ph.pad[1] = ph.pad[2] = 0;
-      const int h = A.pend_head[g];
-      ph.h = h;
-      if (h < A.pend_off[g + 1]) {
-        const int vk = A.pend_vid[h];
-        const int dep = A.depart[vk];
-        if (dep <= A.t) {
-          ph.k = vk;
-          ph.depart = dep;
-          ph.start_s = A.start_s[vk];
-          ph.prof = A.veh_prof[vk];
-        }
-      }
-      S.pend[q] = ph;
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&S.full);
-    stage += 1;
-    if (stage == kStages) { stage = 0; phase ^= 1u; }
+    seq += 1;
+    KP(2, lane == 0);
   }
 }
 
-// ---- consumer phases ------------------------------------------------------------
-// Tile metadata from its descriptor into shared memory (one warp).
-__device__ __forceinline__ void tile_setup(const StepArgs &A, const BatchHdr &H, int k,
-                                           const int *W, const ExtFirst *ext, const PendHead *pend,
-                                           const Prof *P, TileSh &T, int lane_id) {
-  const int nl = H.nl[k], nroad = H.nroad[k];
-  const int ne = W[2];
+// ---- consumer: one tile, one warp ----------------------------------------------------
+// Tile metadata from its descriptor into the warp's TileSh.
+__device__ __forceinline__ void tile_setup(const Hdr &H, const int *W, const ExtFirst *ext,
+                                           const PendHead *pend, const Prof *P, TileSh &T,
+                                           int lane_id) {
+  const int nl = H.nl, nroad = H.nroad;
+  const int ne = W[2], n_all = W[3];
   const int eo = 4 + 5 * nl + 6 * nroad;
+  const int to = eo + 8 * n_all;                     // target-road section
   if (lane_id == 0) {
     T.nl = nl;
     T.nroad = nroad;
-    T.tile = H.tile[k];
-    T.base = H.base[k];
-    T.ibase = H.ibase[k];
-    T.cap = H.cap[k];
-    T.icap = H.icap[k];
-    T.snap0 = H.snap0[k];
-    T.n = H.n_st[k] + H.n_in[k];
+    T.tile = H.tile;
+    T.base = H.base;
+    T.ibase = H.ibase;
+    T.cap = H.cap;
+    T.icap = H.icap;
+    T.snap0 = 0;
+    T.n = H.n_st + H.n_in;
     T.P = P;
     T.ext = ext;
     T.pend = pend;
     T.run = 0;
     T.c_fin = T.c_lc = T.c_hand = T.c_guard = T.c_ovf = T.c_ins = 0;
     T.c_delay = 0ull;
+    T.ntr = W[to];
+    T.umask = (uint32_t)W[to + 1];
+  }
+  if (lane_id < kMaxRoadLanes * kMaxGroups) {
+    T.troad[lane_id] = W[to + 2 + lane_id];
+    T.reach[lane_id] = reinterpret_cast<const uint8_t *>(W + to + 2 + kMaxRoadLanes * kMaxGroups)[lane_id];
+  }
+  {
+    const int8_t *gx = reinterpret_cast<const int8_t *>(W + to + 2 + kMaxRoadLanes * kMaxGroups +
+                                                        (kMaxRoadLanes * kMaxGroups) / 4);
+    static_assert(kMaxRoadLanes * kMaxRoadLanes * kMaxGroups == 64, "two gidx bytes per lane");
+    (&T.gidx[0][0])[lane_id] = gx[lane_id];
+    (&T.gidx[0][0])[32 + lane_id] = gx[32 + lane_id];
   }
   if (lane_id < nl) {
     const int l = lane_id;
@@ -539,86 +624,31 @@ __device__ __forceinline__ void tile_setup(const StepArgs &A, const BatchHdr &H,
     e.fl = (stop ? 1 : 0) | ((int)(jl & 0xff) << 8);
     T.se[(fl >> 8) & 0xff][(fl >> 16) & 0xff] = e;
   }
-  reinterpret_cast<int16_t *>(&T.gidx[0][0])[lane_id] = (int16_t)-1;    // 64 bytes
   __syncwarp();
-  {
-    // distinct target roads of the road lanes (entry e = lane a, group g),
-    // numbered in order of first appearance; per road a lane bitmask
-    static_assert(kMaxRoadLanes * kMaxGroups <= 32, "one entry per thread");
-    const int a = lane_id / kMaxGroups, g = lane_id % kMaxGroups;
-    const bool valid = a < nroad && g < T.ng[a];
-    const int R = valid ? T.gtroad[a][g] : -1;
-    const unsigned vb = __ballot_sync(0xffffffffu, valid);
-    bool first = valid;
-    int myk = -1;
-#pragma unroll 1
-    for (int q = 0; q < kMaxRoadLanes * kMaxGroups; ++q) {
-      const int Rq = __shfl_sync(0xffffffffu, R, q);
-      if (valid && ((vb >> q) & 1u) && Rq == R && q < lane_id) first = false;
-    }
-    const unsigned fb = __ballot_sync(0xffffffffu, first);
-#pragma unroll 1
-    for (int q = 0; q < kMaxRoadLanes * kMaxGroups; ++q) {
-      const int Rq = __shfl_sync(0xffffffffu, R, q);
-      if (valid && ((fb >> q) & 1u) && Rq == R) myk = __popc(fb & ((1u << q) - 1u));
-    }
-    if (first) T.troad[myk] = R;
-    if (valid) T.gidx[a][myk] = (int8_t)g;
-    const int ntr = __popc(fb);
-    for (int kk = 0; kk < ntr; ++kk) {
-      const unsigned m = __ballot_sync(0xffffffffu, valid && myk == kk);
-      unsigned lanes = 0;
-#pragma unroll
-      for (int aa = 0; aa < kMaxRoadLanes; ++aa)
-        if ((m >> (aa * kMaxGroups)) & ((1u << kMaxGroups) - 1u)) lanes |= 1u << aa;
-      if (lane_id == 0) T.reach[kk] = (uint8_t)lanes;
-    }
-    const unsigned um = __ballot_sync(0xffffffffu, lane_id < nroad && T.usable[lane_id]);
-    if (lane_id == 0) { T.ntr = ntr; T.umask = um; }
-  }
-}
-
-// tile of a flat index given per-tile starts (nt <= kMaxT, ascending)
-__device__ __forceinline__ int find_tile(const int *start, int nt, int f) {
-  int k = 0;
-  while (k + 1 < nt && start[k + 1] <= f) ++k;
-  return k;
-}
-
-// warp-aggregated append to a shared list
-__device__ __forceinline__ void push_list(bool pred, uint16_t *list, int *count, int val) {
-  const unsigned m = __ballot_sync(0xffffffffu, pred);
-  if (!m) return;
-  const int lane = threadIdx.x & 31;
-  int base = 0;
-  const int leader = __ffs(m) - 1;
-  if (lane == leader) base = atomicAdd(count, __popc(m));
-  base = __shfl_sync(0xffffffffu, base, leader);
-  if (pred) list[base + __popc(m & ((1u << lane) - 1u))] = (uint16_t)val;
 }
 
 // the vehicle at snapshot slot i has been updated (fp32 path or fp64
-// canonical path): stayer results stay in shared memory for the in-order
+// canonical path): stayer results stay in the pass state for the in-order
 // compaction, movers and arrivals leave now
-__device__ __forceinline__ void settle(const StepArgs &A, Cons &K, const View &C, int i, int li,
+__device__ __forceinline__ void settle(const StepArgs &A, const PState &K, const View &C, int i,
                                        const Res &r, TileSh &T) {
   const int l = m_lane(C.meta(i));
   if (r.fin) {
     emit_moved(A, C, i, r, 3, T);
-    K.kind[li] = 3;
+    K.kind[i] = 3;
   } else if (r.lc == 0 && r.hand == 0 && r.lane_g == T.glob[l]) {
-    K.rs1[li] = r.s1;
-    K.rv1[li] = r.v1;
+    K.rs1[i] = r.s1;
+    K.rv1[i] = r.v1;
     C.wait(i) = r.wait1;
-    K.kind[li] = 1;
+    K.kind[i] = 1;
   } else {
     emit_moved(A, C, i, r, 2, T);
-    K.kind[li] = 2;
+    K.kind[i] = 2;
   }
 }
 
 // pass 1: lane-change eligibility and O4-O6 on the current lane (fp32)
-__device__ __forceinline__ void pass1(const StepArgs &A, Cons &K, const View &C, int i, int li,
+__device__ __forceinline__ void pass1(const StepArgs &A, const PState &K, const View &C, int i,
                                       const TileSh &T) {
   const uint32_t meta = C.meta(i);
   const int l = m_lane(meta);
@@ -651,22 +681,22 @@ __device__ __forceinline__ void pass1(const StepArgs &A, Cons &K, const View &C,
     A.r_hops[me.vid] = (int8_t)use.hops;
     A.r_phantom[me.vid] = (int8_t)use.phantom;
   }
-  K.pa[li] = use.a;
-  K.plim[li] = use.lim;
-  K.plimrel[li] = use.limrel;
-  K.pvlim[li] = use.vlim;
-  K.pnext1[li] = use.next1;
-  K.pfl[li] = (use.has_lim ? F_LIM : 0u) | (g.hit ? F_HIT : 0u) | (E.inG ? F_ING : 0u) |
-              (E.want0 ? F_W0 : 0u) | (E.want1 ? F_W1 : 0u) | ((uint32_t)(E.mand + 1) << F_MAND_SH) |
-              ((uint32_t)(me.k + 1) << F_K_SH) | ((uint32_t)l << F_NL_SH) | (1u << F_LC_SH);
+  K.pa[i] = use.a;
+  K.plim[i] = use.lim;
+  K.plimrel[i] = use.limrel;
+  K.pvlim[i] = use.vlim;
+  K.pnext1[i] = use.next1;
+  K.pfl[i] = (use.has_lim ? F_LIM : 0u) | (g.hit ? F_HIT : 0u) | (E.inG ? F_ING : 0u) |
+             (E.want0 ? F_W0 : 0u) | (E.want1 ? F_W1 : 0u) | ((uint32_t)(E.mand + 1) << F_MAND_SH) |
+             ((uint32_t)(me.k + 1) << F_K_SH) | ((uint32_t)l << F_NL_SH) | (1u << F_LC_SH);
 }
 
 // pass 2: O7 (MOBIL) for a vehicle that may change lane (fp32)
-__device__ __forceinline__ void pass2(const StepArgs &A, Cons &K, const View &C, int i, int li,
+__device__ __forceinline__ void pass2(const StepArgs &A, const PState &K, const View &C, int i,
                                       const TileSh &T) {
   const uint32_t meta = C.meta(i);
   const int l = m_lane(meta);
-  const uint32_t fl = K.pfl[li];
+  const uint32_t fl = K.pfl[i];
   Me me;
   me.vid = C.vid(i);
   me.cur = m_cursor(meta);
@@ -685,26 +715,26 @@ __device__ __forceinline__ void pass2(const StepArgs &A, Cons &K, const View &C,
   Guard g;
   g.hit = false;
   g.why = 0;
-  const SideRes<float> sr = lc_decide<float, true>(A, T, C, i, l, s, v, p, me, E, K.pa[li], g);
+  const SideRes<float> sr = lc_decide<float, true>(A, T, C, i, l, s, v, p, me, E, K.pa[i], g);
   if (g.hit) {
-    K.pfl[li] = fl | F_HIT;
+    K.pfl[i] = fl | F_HIT;
   } else if (sr.choice >= 0) {
-    K.pa[li] = sr.a;
-    K.plim[li] = sr.lim;
-    K.plimrel[li] = sr.limrel;
-    K.pvlim[li] = sr.vlim;
-    K.pnext1[li] = sr.next1;
+    K.pa[i] = sr.a;
+    K.plim[i] = sr.lim;
+    K.plimrel[i] = sr.limrel;
+    K.pvlim[i] = sr.vlim;
+    K.pnext1[i] = sr.next1;
     const int nl = sr.choice == 0 ? E.sl0 : E.sl1;
     const int lc = sr.choice == 0 ? -1 : 1;
-    K.pfl[li] = (fl & ~(F_LIM | (0xffu << F_NL_SH) | (3u << F_LC_SH))) | (sr.has_lim ? F_LIM : 0u) |
-                ((uint32_t)nl << F_NL_SH) | ((uint32_t)(lc + 1) << F_LC_SH);
+    K.pfl[i] = (fl & ~(F_LIM | (0xffu << F_NL_SH) | (3u << F_LC_SH))) | (sr.has_lim ? F_LIM : 0u) |
+               ((uint32_t)nl << F_NL_SH) | ((uint32_t)(lc + 1) << F_LC_SH);
   }
 }
 
 // pass 3: O8-O9 (fp32).  Returns false if the vehicle must be recomputed.
-__device__ __forceinline__ bool pass3(const StepArgs &A, Cons &K, const View &C, int i, int li,
+__device__ __forceinline__ bool pass3(const StepArgs &A, const PState &K, const View &C, int i,
                                       TileSh &T) {
-  const uint32_t fl = K.pfl[li];
+  const uint32_t fl = K.pfl[i];
   if (fl & F_HIT) return false;
   const uint32_t meta = C.meta(i);
   Me me;
@@ -714,11 +744,11 @@ __device__ __forceinline__ bool pass3(const StepArgs &A, Cons &K, const View &C,
   me.nxt2 = C.nxt2(i);
   me.k = -1;
   LEv<float> use;
-  use.a = K.pa[li];
-  use.lim = K.plim[li];
-  use.limrel = K.plimrel[li];
-  use.vlim = K.pvlim[li];
-  use.next1 = K.pnext1[li];
+  use.a = K.pa[i];
+  use.lim = K.plim[i];
+  use.limrel = K.plimrel[i];
+  use.vlim = K.pvlim[i];
+  use.next1 = K.pnext1[i];
   use.has_lim = (fl & F_LIM) != 0;
   const int new_l = (int)((fl >> F_NL_SH) & 0xffu);
   const int lc = (int)((fl >> F_LC_SH) & 3u) - 1;
@@ -729,12 +759,12 @@ __device__ __forceinline__ bool pass3(const StepArgs &A, Cons &K, const View &C,
   integrate<float, true>(A, T, C.s(i), C.v(i), me, use, lc, new_l, C.wait(i), r, g);
   if (g.hit) return false;
   if (A.record) record(A, me.vid, r, false);
-  settle(A, K, C, i, li, r, T);
+  settle(A, K, C, i, r, T);
   return true;
 }
 
 // the fp64 canonical recomputation of one vehicle
-__device__ __noinline__ void pass_fp64(const StepArgs &A, Cons &K, const View &C, int i, int li,
+__device__ __noinline__ void pass_fp64(const StepArgs &A, const PState &K, const View &C, int i,
                                        TileSh &T) {
   Res r;
   Guard g;
@@ -742,32 +772,78 @@ __device__ __noinline__ void pass_fp64(const StepArgs &A, Cons &K, const View &C
   g.why = 0;
   veh_update<double, false>(A, T, C, i, r, g);
   if (A.record) record(A, C.vid(i), r, true);
-  settle(A, K, C, i, li, r, T);
+  settle(A, K, C, i, r, T);
 }
 
-// In-order compaction of the stayers of snapshot range [a, b) of tile T (one
-// warp): each goes to the tile's slab at base + run (coalesced), the first
-// stayer of each lane is remembered for the t+1 summary.
-__device__ __forceinline__ void compact(const StepArgs &A, Cons &K, const View &C, TileSh &T, int a,
-                                        int b, int c0, int lane_id) {
-  int run = T.run;
-  for (int i0 = a; i0 < b; i0 += 32) {
+// warp-aggregated append to a per-tile list
+__device__ __forceinline__ int push_list(bool pred, uint16_t *list, int count, int val, int lane) {
+  const unsigned m = __ballot_sync(0xffffffffu, pred);
+  if (pred) list[count + __popc(m & ((1u << lane) - 1u))] = (uint16_t)val;
+  return count + __popc(m);
+}
+
+// passes 1-3 and the fp64 recomputation over the tile's n snapshot slots
+template <bool EXACT>
+__device__ __forceinline__ void run_passes(const StepArgs &A, const PState &K, const View &C,
+                                           TileSh &T, int n, int lane) {
+  int nd = 0;
+  if constexpr (!EXACT) {
+    int nc = 0;
+    for (int q0 = 0; q0 < n; q0 += 32) {             // pass 1 (every vehicle)
+      const int q = q0 + lane;
+      bool cand = false;
+      if (q < n) {
+        pass1(A, K, C, q, T);
+        const uint32_t fl = K.pfl[q];
+        cand = !(fl & F_HIT) && ((fl & (F_W0 | F_W1)) || (A.record && T.isroad[m_lane(C.meta(q))]));
+      }
+      nc = push_list(cand, K.cand, nc, q, lane);
+    }
+    __syncwarp();
+    for (int q = lane; q < nc; q += 32) pass2(A, K, C, K.cand[q], T);   // pass 2 (compacted)
+    __syncwarp();
+    for (int q0 = 0; q0 < n; q0 += 32) {             // pass 3 (every vehicle)
+      const int q = q0 + lane;
+      bool def = false;
+      if (q < n) def = !pass3(A, K, C, q, T);
+      nd = push_list(def, K.defl, nd, q, lane);
+    }
+    __syncwarp();
+  } else {
+    for (int q = lane; q < n; q += 32) K.defl[q] = (uint16_t)q;
+    nd = n;
+    __syncwarp();
+  }
+  for (int q = lane; q < nd; q += 32) {              // fp64 canonical path
+    pass_fp64(A, K, C, K.defl[q], T);
+    if (!EXACT) atomicAdd(&T.c_guard, 1);
+  }
+  __syncwarp();
+}
+
+// In-order compaction of the tile's stayers: each goes to the tile's slab at
+// base + run (coalesced), the first stayer of each lane is remembered for the
+// t+1 summary.
+__device__ __forceinline__ void compact(const StepArgs &A, const PState &K, const View &C, TileSh &T,
+                                        int n, int lane_id) {
+  int run = 0;
+  for (int i0 = 0; i0 < n; i0 += 32) {
     const int i = i0 + lane_id;
-    const bool st = i < b && K.kind[i - c0] == 1;
+    const bool st = i < n && K.kind[i] == 1;
     const unsigned ball = __ballot_sync(0xffffffffu, st);
     if (st) {
       const int rank = run + __popc(ball & ((1u << lane_id) - 1u));
       if (rank < T.cap) {
         const int pos = T.base + rank;
         const uint32_t meta = C.meta(i);
-        A.out.s[pos] = K.rs1[i - c0];
-        A.out.v[pos] = K.rv1[i - c0];
+        A.out.s[pos] = K.rs1[i];
+        A.out.v[pos] = K.rv1[i];
         A.out.vid[pos] = C.vid(i);
         A.out.nxt[pos] = C.nxt(i);
         A.out.nxt2[pos] = C.nxt2(i);
         A.out.meta[pos] = meta;
         A.out.wait[pos] = C.wait(i);
-        atomicMin(&T.first_out[m_lane(meta)], (rank << 15) | (i - T.snap0));
+        atomicMin(&T.first_out[m_lane(meta)], (rank << 15) | i);
       } else {
         atomicAdd(&T.c_ovf, 1);                     // slab capacity exceeded: sticky SIM_E_CAPACITY
       }
@@ -780,22 +856,19 @@ __device__ __forceinline__ void compact(const StepArgs &A, Cons &K, const View &
 }
 
 // Lane summaries for t+1, departures (K11; L25) and counters (a6) of
-// one tile (one warp), after all its vehicles are settled.
-__device__ __forceinline__ void tile_finish(const StepArgs &A, Cons &K, const View &C, TileSh &T,
-                                            bool gmode, int lane_id) {
+// the tile, after all its vehicles are settled.
+__device__ __forceinline__ void tile_finish(const StepArgs &A, const PState &K, const View &C,
+                                            TileSh &T, int lane_id) {
   const int nl = T.nl, nroad = T.nroad, tile = T.tile;
   const int run = T.run < T.cap ? T.run : T.cap;
   for (int l = lane_id; l < nl; l += 32) {
     const int g = T.glob[l];
     const int fo = T.first_out[l];
     if (fo != 0x7fffffff) {
-      const int rank = fo >> 15, idx = T.snap0 + (fo & 0x7fff);
+      const int rank = fo >> 15, idx = fo & 0x7fff;
       const int vid = C.vid(idx);
-      float s1, v1;
-      if (!gmode) { s1 = K.rs1[idx]; v1 = K.rv1[idx]; }
-      else { s1 = A.out.s[T.base + rank]; v1 = A.out.v[T.base + rank]; }
-      atomicMin(&A.summ_next[g], vkey(s1, vid));
-      A.pubv_next[vid] = v1;
+      atomicMin(&A.summ_next[g], vkey(K.rs1[idx], vid));
+      A.pubv_next[vid] = K.rv1[idx];
       if (A.lane_cnt_next) {                          // stayers of lane l: [rank, next lane's first)
         int end = run;
         for (int q = l + 1; q < nl; ++q)
@@ -867,232 +940,177 @@ __device__ __forceinline__ void tile_finish(const StepArgs &A, Cons &K, const Vi
     A.cnt_out[tile] = run;
     A.icnt_in[tile] = 0;
   }
+  __syncwarp();
 }
 
-// passes 1-3 and the fp64 recomputation over snapshot slots [c0, c1)
-template <bool EXACT>
-__device__ __forceinline__ void run_passes(const StepArgs &A, Cons &K, const View &C, int c0, int c1,
-                                           bool gm, int tid) {
-  const int n = c1 - c0;
-  if (tid == 0) { K.ncand = 0; K.ndef = 0; }
-  cbar();
-  if constexpr (!EXACT) {
-    for (int q0 = 0; q0 < n; q0 += kCT) {            // pass 1 (every vehicle)
-      const int q = q0 + tid;
-      bool cand = false;
-      if (q < n) {
-        const int i = c0 + q;
-        const TileSh &T = K.T[gm ? 0 : K.tix[q]];
-        pass1(A, K, C, i, q, T);
-        const uint32_t fl = K.pfl[q];
-        const int l = m_lane(C.meta(i));
-        cand = !(fl & F_HIT) && ((fl & (F_W0 | F_W1)) || (A.record && T.isroad[l]));
-      }
-      push_list(cand, K.cand, &K.ncand, q);
-    }
-    cbar();
-    const int nc = K.ncand;
-    for (int q = tid; q < nc; q += kCT) {            // pass 2 (compacted MOBIL candidates)
-      const int li = K.cand[q];
-      pass2(A, K, C, c0 + li, li, K.T[gm ? 0 : K.tix[li]]);
-    }
-    cbar();
-    for (int q0 = 0; q0 < n; q0 += kCT) {            // pass 3 (every vehicle)
-      const int q = q0 + tid;
-      bool def = false;
-      if (q < n) def = !pass3(A, K, C, c0 + q, q, K.T[gm ? 0 : K.tix[q]]);
-      push_list(def, K.defl, &K.ndef, q);
-    }
-    cbar();
+// one tile, start to finish, by one consumer warp
+// GM: the tile is in global mode.  A separate instantiation, so that in the
+// common one every snapshot / pass-state access is provably to shared memory
+// (LDS/STS instead of generic loads).
+template <bool EXACT, bool GM>
+__device__ __forceinline__ void run_tile(const StepArgs &A, StepSmem &M, const Hdr &H, TileSh &T,
+                                         const Prof *P, int lane) {
+  constexpr bool gm = GM;
+  const int ns = H.n_st, ni = H.n_in, n = ns + ni;
+  const int nj = H.nl - H.nroad;
+  const SlotLayout L = gm ? slot_layout(0, 0, H.dw, nj, H.nroad) : slot_layout(ns, ni, H.dw, nj, H.nroad);
+  unsigned char *slot = M.ring + H.off;
+  tile_setup(H, reinterpret_cast<const int *>(slot + L.desc), reinterpret_cast<const ExtFirst *>(slot + L.ext),
+             reinterpret_cast<const PendHead *>(slot + L.pend), P, T, lane);
+  View C;
+  PState K;
+  if (!gm) {
+    C.p = reinterpret_cast<uint32_t *>(slot + L.snap);
+    C.st = L.n4;
+    K = pstate_at(slot + L.st, L.n4);
   } else {
-    for (int q = tid; q < n; q += kCT) K.defl[q] = (uint16_t)q;
-    if (tid == 0) K.ndef = n;
-    cbar();
+    const size_t o = (size_t)H.base + (size_t)H.ibase;
+    C.st = H.cap + H.icap;
+    C.p = A.scratch + 7 * o;
+    const size_t o2 = o + 4 * (size_t)H.tile;       // 4 slots of slack per tile: 16-B strides
+    K = pstate_at(reinterpret_cast<unsigned char *>(A.pscratch + 10 * o2), (C.st + 3) & ~3);
   }
-  const int nd = K.ndef;
-  for (int q = tid; q < nd; q += kCT) {              // fp64 canonical path
-    const int li = K.defl[q];
-    TileSh &T = K.T[gm ? 0 : K.tix[li]];
-    pass_fp64(A, K, C, c0 + li, li, T);
-    if (!EXACT) atomicAdd(&T.c_guard, 1);
+  // ---- merge stayers + sorted inbox into the snapshot (a1) --------------------------
+  if (!gm) {
+    const uint32_t *sl = reinterpret_cast<const uint32_t *>(slot + L.slab);
+    const InboxRec *inb = reinterpret_cast<const InboxRec *>(slot + L.inbox);
+    unsigned long long *skh = reinterpret_cast<unsigned long long *>(slot + L.sortk);
+    int *skv = reinterpret_cast<int *>(skh + ni);
+    int *bs = skv + ni;
+    const int r4 = L.r4;
+    for (int r = lane; r < ni; r += 32) {            // inbox keys ranked
+      const InboxRec &x = inb[r];
+      const unsigned long long h = hikey(m_lane(x.meta), x.s);
+      int rank = 0;
+      for (int q = 0; q < ni; ++q) {
+        const InboxRec &o = inb[q];
+        rank += key_less(hikey(m_lane(o.meta), o.s), o.vid, h, x.vid);
+      }
+      skh[rank] = h;
+      skv[rank] = x.vid;
+      bs[rank] = r;
+    }
+    __syncwarp();
+    for (int i = lane; i < ns; i += 32) {            // stayers: own index + inbox keys below
+      const float s = __uint_as_float(sl[i]);
+      const uint32_t meta = sl[5 * r4 + i];
+      const int vid = (int)sl[2 * r4 + i];
+      int lo = 0, hi = ni;
+      if (ni > 0) {
+        const unsigned long long h = hikey(m_lane(meta), s);
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (key_less(skh[mid], skv[mid], h, vid)) lo = mid + 1; else hi = mid;
+        }
+      }
+      const int pos = i + lo;
+      C.s(pos) = s;
+      C.v(pos) = __uint_as_float(sl[r4 + i]);
+      C.vid(pos) = vid;
+      C.meta(pos) = meta;
+      C.nxt(pos) = (int)sl[3 * r4 + i];
+      C.nxt2(pos) = (int)sl[4 * r4 + i];
+      C.wait(pos) = (int)sl[6 * r4 + i];
+    }
+    for (int r = lane; r < ni; r += 32) {            // inbox records: rank + stayers below
+      const InboxRec &x = inb[bs[r]];
+      const unsigned long long h = skh[r];
+      int lo = 0, hi = ns;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (key_less(hikey(m_lane(sl[5 * r4 + mid]), __uint_as_float(sl[mid])), (int)sl[2 * r4 + mid], h, x.vid))
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      const int pos = r + lo;
+      C.s(pos) = x.s;
+      C.v(pos) = x.v;
+      C.vid(pos) = x.vid;
+      C.meta(pos) = x.meta;
+      C.nxt(pos) = x.nxt;
+      C.nxt2(pos) = x.nxt2;
+      C.wait(pos) = x.wait;
+    }
+  } else {
+    const int base = H.base, ib = H.ibase;
+    const InboxRec *inb = A.inbox_in + ib;
+    const int *bsort = A.bsort_scratch + ib;
+    if (ni > 0) rank_inbox_global(inb, ni, A.bsort_scratch + ib, lane, 32);
+    __syncwarp();
+    for (int i = lane; i < ns; i += 32) {
+      const int gi = base + i;
+      const float s = A.in.s[gi];
+      const uint32_t meta = A.in.meta[gi];
+      const int vid = A.in.vid[gi];
+      const int lo = ni > 0 ? lower_bound_inbox_global(inb, bsort, ni, hikey(m_lane(meta), s), vid) : 0;
+      const int pos = i + lo;
+      C.s(pos) = s;
+      C.v(pos) = A.in.v[gi];
+      C.vid(pos) = vid;
+      C.meta(pos) = meta;
+      C.nxt(pos) = A.in.nxt[gi];
+      C.nxt2(pos) = A.in.nxt2[gi];
+      C.wait(pos) = A.in.wait[gi];
+    }
+    for (int r = lane; r < ni; r += 32) {
+      const InboxRec x = inb[bsort[r]];
+      const unsigned long long h = hikey(m_lane(x.meta), x.s);
+      int lo = 0, hi = ns;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const int gi = base + mid;
+        if (key_less(hikey(m_lane(A.in.meta[gi]), A.in.s[gi]), A.in.vid[gi], h, x.vid)) lo = mid + 1;
+        else hi = mid;
+      }
+      const int pos = r + lo;
+      C.s(pos) = x.s;
+      C.v(pos) = x.v;
+      C.vid(pos) = x.vid;
+      C.meta(pos) = x.meta;
+      C.nxt(pos) = x.nxt;
+      C.nxt2(pos) = x.nxt2;
+      C.wait(pos) = x.wait;
+    }
   }
-  cbar();
+  __syncwarp();
+  // ---- lane segments of the snapshot -------------------------------------------------
+  for (int i = lane; i < n; i += 32) {
+    const int l = m_lane(C.meta(i));
+    if (i == 0 || m_lane(C.meta(i - 1)) != l) T.seg_start[l] = (int16_t)i;
+    if (i == n - 1 || m_lane(C.meta(i + 1)) != l) T.seg_end[l] = (int16_t)(i + 1);
+  }
+  __syncwarp();
+  run_passes<EXACT>(A, K, C, T, n, lane);
+  compact(A, K, C, T, n, lane);
+  tile_finish(A, K, C, T, lane);
 }
 
 template <bool EXACT>
-__device__ __forceinline__ void consumer(const StepArgs &A, StepSmem &M, const Prof *P, int tid) {
-  Cons &K = M.C;
-  const int warp = tid >> 5, lane_id = tid & 31;
-  int stage = 0;
-  unsigned phase = 0;
+__device__ __forceinline__ void consumer(const StepArgs &A, StepSmem &M, const Prof *P, int warp,
+                                         int lane) {
+  TileSh &T = M.T[warp];
+  KP_DECL
   for (;;) {
-    Stage &S = M.S[stage];
-    mbar_wait(&S.full, phase);
-    const BatchHdr &H = S.H;
+    int seq = 0;
+    if (lane == 0) seq = atomicAdd(&M.next_seq, 1);
+    seq = __shfl_sync(0xffffffffu, seq, 0);
+    Hdr &H = M.H[seq % kNH];
+    KP(9, lane == 0);
+    mbar_wait(&H.full, (unsigned)(seq / kNH) & 1u);
+    KP(8, lane == 0);
     if (H.done) break;
-    const int nt = H.nt;
-    const bool gm = H.gmode != 0;
-    View C;
-    if (!gm) {
-      C.p = K.snap;
-      C.st = kBatch;
-    } else {
-      C.st = H.cap[0] + H.icap[0];
-      C.p = A.scratch + 7 * (size_t)(H.base[0] + H.ibase[0]);
-    }
-    // ---- A: tile metadata (warp per tile) + inbox ranks (flat) -----------------
-    for (int k = warp; k < nt; k += kCW) {
-      const int *W = gm ? A.desc + H.doff[k] : S.desc + H.desc[k];
-      tile_setup(A, H, k, W, S.ext + H.xo[k], S.pend + H.po[k], P, K.T[k], lane_id);
-    }
-    if (!gm) {
-      for (int r = tid; r < H.nin; r += kCT) {
-        const int k = find_tile(H.in0, nt, r);
-        const int a = H.in0[k], ni = H.n_in[k];
-        const InboxRec &x = S.inbox[r];
-        const unsigned long long h = hikey(m_lane(x.meta), x.s);
-        int rank = 0;
-        for (int q = 0; q < ni; ++q) {
-          const InboxRec &o = S.inbox[a + q];
-          rank += key_less(hikey(m_lane(o.meta), o.s), o.vid, h, x.vid);
-        }
-        K.skh[a + rank] = h;
-        K.skv[a + rank] = x.vid;
-        K.bs[a + rank] = r - a;
-      }
-    } else if (H.n_in[0] > 0) {
-      rank_inbox_global(A.inbox_in + H.ibase[0], H.n_in[0], A.bsort_scratch + H.ibase[0], tid, kCT);
-    }
-    cbar();
-    // ---- B: merge stayers + sorted inbox into the snapshot (a1) ----------------
-    if (!gm) {
-      for (int f = tid; f < H.nst; f += kCT) {        // stayers
-        const int k = find_tile(H.st0, nt, f);
-        const int i = f - H.st0[k], r4 = H.r4[k];
-        const uint32_t *sl = S.slab + H.slab[k];
-        const float s = __uint_as_float(sl[i]);
-        const uint32_t meta = sl[5 * r4 + i];
-        const int vid = (int)sl[2 * r4 + i];
-        const int a = H.in0[k], ni = H.n_in[k];
-        int lo = 0, hi = ni;
-        if (ni > 0) {
-          const unsigned long long h = hikey(m_lane(meta), s);
-          while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (key_less(K.skh[a + mid], K.skv[a + mid], h, vid)) lo = mid + 1; else hi = mid;
-          }
-        }
-        const int pos = H.snap0[k] + i + lo;
-        C.s(pos) = s;
-        C.v(pos) = __uint_as_float(sl[r4 + i]);
-        C.vid(pos) = vid;
-        C.meta(pos) = meta;
-        C.nxt(pos) = (int)sl[3 * r4 + i];
-        C.nxt2(pos) = (int)sl[4 * r4 + i];
-        C.wait(pos) = (int)sl[6 * r4 + i];
-        K.tix[pos] = (uint8_t)k;
-      }
-      for (int r = tid; r < H.nin; r += kCT) {        // inbox records
-        const int k = find_tile(H.in0, nt, r);
-        const int a = H.in0[k], rank = r - a, ns = H.n_st[k], r4 = H.r4[k];
-        const InboxRec &x = S.inbox[a + K.bs[r]];
-        const unsigned long long h = hikey(m_lane(x.meta), x.s);
-        const uint32_t *sl = S.slab + H.slab[k];
-        int lo = 0, hi = ns;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (key_less(hikey(m_lane(sl[5 * r4 + mid]), __uint_as_float(sl[mid])), (int)sl[2 * r4 + mid], h,
-                       x.vid))
-            lo = mid + 1;
-          else
-            hi = mid;
-        }
-        const int pos = H.snap0[k] + rank + lo;
-        C.s(pos) = x.s;
-        C.v(pos) = x.v;
-        C.vid(pos) = x.vid;
-        C.meta(pos) = x.meta;
-        C.nxt(pos) = x.nxt;
-        C.nxt2(pos) = x.nxt2;
-        C.wait(pos) = x.wait;
-        K.tix[pos] = (uint8_t)k;
-      }
-    } else {
-      const int ns = H.n_st[0], ni = H.n_in[0], base = H.base[0], ib = H.ibase[0];
-      const InboxRec *inb = A.inbox_in + ib;
-      const int *bsort = A.bsort_scratch + ib;
-      for (int i = tid; i < ns; i += kCT) {
-        const int gi = base + i;
-        const float s = A.in.s[gi];
-        const uint32_t meta = A.in.meta[gi];
-        const int vid = A.in.vid[gi];
-        const int lo = ni > 0 ? lower_bound_inbox_global(inb, bsort, ni, hikey(m_lane(meta), s), vid) : 0;
-        const int pos = i + lo;
-        C.s(pos) = s;
-        C.v(pos) = A.in.v[gi];
-        C.vid(pos) = vid;
-        C.meta(pos) = meta;
-        C.nxt(pos) = A.in.nxt[gi];
-        C.nxt2(pos) = A.in.nxt2[gi];
-        C.wait(pos) = A.in.wait[gi];
-      }
-      for (int r = tid; r < ni; r += kCT) {
-        const InboxRec x = inb[bsort[r]];
-        const unsigned long long h = hikey(m_lane(x.meta), x.s);
-        int lo = 0, hi = ns;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          const int gi = base + mid;
-          if (key_less(hikey(m_lane(A.in.meta[gi]), A.in.s[gi]), A.in.vid[gi], h, x.vid)) lo = mid + 1;
-          else hi = mid;
-        }
-        const int pos = r + lo;
-        C.s(pos) = x.s;
-        C.v(pos) = x.v;
-        C.vid(pos) = x.vid;
-        C.meta(pos) = x.meta;
-        C.nxt(pos) = x.nxt;
-        C.nxt2(pos) = x.nxt2;
-        C.wait(pos) = x.wait;
-      }
-    }
-    cbar();
-    // ---- C: lane segments of the snapshot ---------------------------------------
-    const int nveh = H.nveh;
-    for (int i = tid; i < nveh; i += kCT) {
-      const int k = gm ? 0 : K.tix[i];
-      TileSh &T = K.T[k];
-      const int l = m_lane(C.meta(i));
-      if (i == T.snap0 || m_lane(C.meta(i - 1)) != l) T.seg_start[l] = (int16_t)i;
-      if (i == T.snap0 + T.n - 1 || m_lane(C.meta(i + 1)) != l) T.seg_end[l] = (int16_t)(i + 1);
-    }
-    cbar();
-    // ---- D-G: the vehicle passes; H: compaction and per-tile finish -------------
-    if (!gm) {
-      run_passes<EXACT>(A, K, C, 0, nveh, false, tid);
-      for (int k = warp; k < nt; k += kCW) {
-        TileSh &T = K.T[k];
-        compact(A, K, C, T, T.snap0, T.snap0 + T.n, 0, lane_id);
-        tile_finish(A, K, C, T, false, lane_id);
-      }
-    } else {
-      for (int c0 = 0; c0 < nveh; c0 += kBatch) {
-        const int c1 = min(nveh, c0 + kBatch);
-        run_passes<EXACT>(A, K, C, c0, c1, true, tid);
-        if (warp == 0) compact(A, K, C, K.T[0], c0, c1, c0, lane_id);
-        cbar();
-      }
-      if (warp == 0) tile_finish(A, K, C, K.T[0], true, lane_id);
-    }
-    cbar();
-    if (tid == 0) mbar_arrive(&S.empty);             // the stage can be refilled
-    stage += 1;
-    if (stage == kStages) { stage = 0; phase ^= 1u; }
+    if (H.gm) run_tile<EXACT, true>(A, M, H, T, P, lane);
+    else run_tile<EXACT, false>(A, M, H, T, P, lane);
+    KP(10, lane == 0);
+    KPN(20, lane == 0, 1);
+    KPN(21, lane == 0, H.gm);
+    if (lane == 0) mbar_arrive(&H.empty);           // the slot can be reused
   }
 }
 
 template <bool EXACT>
-__global__ void __launch_bounds__(kStepThreads, 2) k_step(const __grid_constant__ StepArgs A) {
+__global__ void __launch_bounds__(kStepThreads, KS_MINB) k_step(const __grid_constant__ StepArgs A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   StepSmem &M = *reinterpret_cast<StepSmem *>(smem_raw);
   const int tid = threadIdx.x;
@@ -1100,19 +1118,20 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(const __grid_constant_
   if (A.n_prof <= kSmemProf) {                      // profiles as int4 words (Prof is 96 B)
     const int nw = A.n_prof * (int)(sizeof(Prof) / 16);
     for (int q = tid; q < nw; q += blockDim.x)
-      reinterpret_cast<int4 *>(M.C.prof)[q] = reinterpret_cast<const int4 *>(A.prof)[q];
-    P = M.C.prof;
+      reinterpret_cast<int4 *>(M.prof)[q] = reinterpret_cast<const int4 *>(A.prof)[q];
+    P = M.prof;
   }
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&M.S[s].full, 2);
-      mbar_init(&M.S[s].empty, 1);
+    for (int e = 0; e < kNH; ++e) {
+      mbar_init(&M.H[e].full, 1);
+      mbar_init(&M.H[e].empty, 1);
     }
+    M.next_seq = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (tid >= kCT) producer(A, M, P, tid & 31);
-  else consumer<EXACT>(A, M, P, tid);
+  if (tid >= kCW * 32) producer(A, M, tid & 31);
+  else consumer<EXACT>(A, M, P, tid >> 5, tid & 31);
   __syncthreads();
   if (tid == 0) {
     __threadfence();
@@ -1124,6 +1143,24 @@ __global__ void __launch_bounds__(kStepThreads, 2) k_step(const __grid_constant_
 }
 
 int step_smem_bytes() { return (int)sizeof(StepSmem); }
+
+}  // namespace sim
+
+// dev builds (-DKS_PROF): per-phase clock totals of k_step since the last call
+extern "C" int sim_debug_kstep_prof(unsigned long long *out) {
+#ifdef KS_PROF
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, sim::g_ks_prof, sizeof(sim::g_ks_prof));
+  static const unsigned long long z[32] = {0};
+  cudaMemcpyToSymbol(sim::g_ks_prof, z, sizeof(z));
+  return 32;
+#else
+  (void)out;
+  return 0;
+#endif
+}
+
+namespace sim {
 
 void launch_step(const StepArgs &a, void *stream, int smem_bytes) {
   static int resident[2] = {0, 0};                  // resident blocks per GPU, per instantiation
@@ -1140,8 +1177,8 @@ void launch_step(const StepArgs &a, void *stream, int smem_bytes) {
   }
   if (a.n_own <= 0) return;
   const int ex = a.exact_mode ? 1 : 0;
-  // enough CTAs for the work (a CTA takes kGroup tiles at a time), at most
-  // the resident capacity (persistent)
+  // enough CTAs for the work (a producer claims kGroup tiles at a time), at
+  // most the resident capacity (persistent)
   const int grid = std::min((a.n_own + kGroup - 1) / kGroup, resident[ex]);
   if (ex) k_step<true><<<grid, kStepThreads, smem_bytes, (cudaStream_t)stream>>>(a);
   else k_step<false><<<grid, kStepThreads, smem_bytes, (cudaStream_t)stream>>>(a);

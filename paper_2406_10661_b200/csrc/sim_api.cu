@@ -313,7 +313,7 @@ void build_desc(sim_s *h) {
       grp.push_back(gbeg[4]);
       for (int q = 0; q < kMaxGroups; ++q) grp.push_back(gtr[q]);
     }
-    std::vector<int32_t> w{nl, nroad, (int)(ent.size() / 8), 0};
+    std::vector<int32_t> w{nl, nroad, (int)(ent.size() / 8), n_all};
     for (int l = 0; l < nl; ++l) w.push_back(h->tile_lanes[l0 + l]);
     for (int l = 0; l < nl; ++l) { float x = h->L[h->tile_lanes[l0 + l]]; int32_t b; std::memcpy(&b, &x, 4); w.push_back(b); }
     for (int l = 0; l < nl; ++l) { float x = h->vmax[h->tile_lanes[l0 + l]]; int32_t b; std::memcpy(&b, &x, 4); w.push_back(b); }
@@ -328,6 +328,37 @@ void build_desc(sim_s *h) {
     // pad to all successors so setters (which change the usable set) never
     // change the descriptor's size or offsets
     w.insert(w.end(), (size_t)(n_all - (int)(ent.size() / 8)) * 8, 0);
+    // target-road section (kDescTroadWords): the distinct roads the
+    // road lanes lead to, numbered in order of first appearance over (lane,
+    // group); reach[k] = road lanes with a group toward troad[k]; gidx[a][k] =
+    // that group of lane a (-1 none); umask = usable road lanes
+    {
+      int32_t tw[kDescTroadWords] = {0};
+      int ntr = 0;
+      int troad[kMaxRoadLanes * kMaxGroups];
+      uint8_t reach[kMaxRoadLanes * kMaxGroups] = {0};
+      int8_t gidx[kMaxRoadLanes][kMaxRoadLanes * kMaxGroups];
+      std::memset(gidx, 0xff, sizeof(gidx));
+      uint32_t umask = 0;
+      for (int a = 0; a < nroad; ++a) {
+        if (h->usable[h->tile_lanes[l0 + a]]) umask |= 1u << a;
+        const int32_t *gr = &grp[6 * (size_t)a];
+        for (int g = 0; g < lane_ng[a] && g < kMaxGroups; ++g) {
+          const int R = gr[2 + g];
+          int k = 0;
+          while (k < ntr && troad[k] != R) ++k;
+          if (k == ntr) troad[ntr++] = R;
+          reach[k] |= (uint8_t)(1u << a);
+          gidx[a][k] = (int8_t)g;
+        }
+      }
+      tw[0] = ntr;
+      tw[1] = (int32_t)umask;
+      for (int k = 0; k < kMaxRoadLanes * kMaxGroups; ++k) tw[2 + k] = k < ntr ? troad[k] : -1;
+      std::memcpy(&tw[2 + kMaxRoadLanes * kMaxGroups], reach, sizeof(reach));
+      std::memcpy(&tw[2 + kMaxRoadLanes * kMaxGroups + sizeof(reach) / 4], gidx, sizeof(gidx));
+      w.insert(w.end(), tw, tw + kDescTroadWords);
+    }
     while (w.size() % 4) w.push_back(0);
     h->desc.insert(h->desc.end(), w.begin(), w.end());
     h->desc_off[T + 1] = (int)h->desc.size();
@@ -977,6 +1008,24 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   AL(A.scratch, 7 * sc);
   AL(A.bsort_scratch, h->sum_icap);
   AL(A.dl_scratch, sc);
+  AL(A.pscratch, 10 * (sc + 4 * (int64_t)nt));
+  {
+    // static per-tile record of k_step's producer warp + the k_prep staging
+    // buffers (offsets over all tiles, so repartitioning needs no change)
+    std::vector<int4> ti(3 * (size_t)nt);
+    int64_t xo = 0, po = 0;
+    for (int T = 0; T < nt; ++T) {
+      const int nlT = h->tile_lane_off[T + 1] - h->tile_lane_off[T], nr = h->tile_nroad[T];
+      ti[3 * T + 0] = make_int4(h->tile_base[T], h->tile_ibase[T], h->tile_cap[T], h->tile_icap[T]);
+      ti[3 * T + 1] = make_int4(h->desc_off[T], h->desc_off[T + 1] - h->desc_off[T], nlT, nr);
+      ti[3 * T + 2] = make_int4((int)xo, (int)po, 0, 0);
+      xo += nlT - nr;
+      po += nr;
+    }
+    int4 *i4; UP(i4, ti); A.tinfo = i4;
+    AL(A.ext_buf, std::max<int64_t>(xo, 1));
+    AL(A.pend_buf, std::max<int64_t>(po, 1));
+  }
   for (int b = 0; b < 3; ++b) AL(P.summ[b], nl);
   UP(P.route_start_d, h->rstart); A.route_start = P.route_start_d;
   UP(P.route_len_d, h->rlen); A.route_len = P.route_len_d;
@@ -1287,8 +1336,9 @@ sim_status step_once(sim_s *h) {
   for (Part &P : h->parts) {
     StepArgs a = step_args(P, t);
     a.lane_cnt_next = cnt_next;
+    launch_prep(a, st);
     launch_step(a, st, h->smem);
-    h->n_launch += a.n_own > 0;
+    h->n_launch += 2 * (a.n_own > 0);
   }
   if (h->timing) CK(h, cudaEventRecord(e[2], st));
   if (h->ipc) {                                     // direct transport: movers and summaries are

@@ -33,6 +33,26 @@ print(f"{os.path.basename(lib)}: k_step {ks/n*1e3:.1f} us  k_signal {sg/n*1e3:.1
       f"veh-steps/s(kstep) {vs/(ks/1e3):.3e}  guard/step {(m1['n_guard_hits']-m0['n_guard_hits'])/n:.0f}", flush=True)
 import ctypes
 L = S.load_library(lib)
+pb = (ctypes.c_ulonglong * 32)()
+try:
+    if L.sim_debug_kstep_prof(pb) > 0:
+        # counters since the library was loaded: take a fresh window
+        L.sim_debug_kstep_prof(pb)
+        with torch.cuda.stream(st):
+            for k in range(10):
+                flush.fill_(k & 255)
+                sim.step(1)
+        torch.cuda.synchronize()
+        L.sim_debug_kstep_prof(pb)
+        names = {0: "P wait_empty", 1: "P build", 2: "P issue", 3: "P gather",
+                 8: "C wait_full", 9: "C claim", 10: "C tile"}
+        tot_p = sum(pb[i] for i in range(0, 5)); tot_c = sum(pb[i] for i in range(8, 19))
+        for i, nm in names.items():
+            tot = tot_p if i < 8 else tot_c
+            print(f"  {nm:18s} {pb[i]/max(tot,1)*100:5.1f}%  ({pb[i]/1e6:.1f} Mcyc)")
+        print(f"  tiles {pb[20]/10:.0f}/step  gmode {pb[21]/10:.0f}")
+except AttributeError:
+    pass
 buf = (ctypes.c_ulonglong * 32)()
 try:
     n = L.sim_debug_guard_stats(buf)
