@@ -63,7 +63,7 @@ struct Prof {                       // one vehicle profile
 
 static_assert(sizeof(Prof) % 16 == 0, "Prof is copied as int4 words");
 
-struct __align__(16) InboxRec {      // 32 B, one sector (16-B aligned: moved as two int4)
+struct __align__(16) InboxRec {      // 32 B vehicle record (stayer or inbox), one sector
   float s, v;
   int32_t vid, nxt, nxt2;
   uint32_t meta;                    // lane_local:8 | profile:8 | cursor:16
@@ -101,12 +101,6 @@ struct HaloRec {                    // 16 B: first-vehicle summary of one lane f
   int32_t pad;
 };
 
-struct Slab {                       // SoA hot record, 28 B / vehicle
-  float *s, *v;
-  int32_t *vid, *nxt, *nxt2;        // route[c+1], route[c+2] (-1 past the end)
-  uint32_t *meta;
-  int32_t *wait;
-};
 
 // Direct peer-memory transport: the device
 // buffers of partition q that other partitions write into (movers entering
@@ -115,7 +109,7 @@ struct Slab {                       // SoA hot record, 28 B / vehicle
 // In one process (loopback) these are the partitions' own pointers; across
 // processes they are CUDA IPC mappings (NVLink peer memory on a multi-GPU box).
 struct PeerView {                   // pointers only (exported as an array of handles)
-  InboxRec *inbox[2];
+  InboxRec *inbox[2];               // vehicle records (stayers + inboxes, by step parity)
   int32_t *icnt[2];
   unsigned long long *summ[3];
   float *pubv[2];
@@ -123,8 +117,8 @@ struct PeerView {                   // pointers only (exported as an array of ha
   int32_t *insert_time;
   uint8_t *status;
   unsigned int *bar;                // barrier arrival counter of partition q
-  Slab slab[2];                     // stayers, cnt and pending-queue heads: moved when a
-  int32_t *cnt[2];                  // tile changes owner (sim_repartition)
+  int32_t *cnt[2];                  // stayer counts and pending-queue heads: moved when a
+                                    // tile changes owner (sim_repartition)
   int32_t *pend_head;
   int32_t *arrive_time, *wait_fin;  // read by sim_read_state_global
   void *xbuf[4];                    // reduction buffers: counters, lane statistics, group metrics,
@@ -161,26 +155,26 @@ struct StepArgs {
   const int32_t *tiles, *tile_owner;  // tiles: own tiles, largest slot capacity first
   int32_t *work;                    // [2] persistent-kernel work counter + finished warps (zero between launches)
   const int32_t *tile_lane_off, *tile_lanes, *tile_nroad;
-  const int32_t *desc, *desc_off;   // tile descriptors (words, per-tile offsets)
+  int32_t *desc;                    // tile blocks: descriptor words, then the k_prep staging
+  const int32_t *desc_off;          // (ExtFirst per junction lane, PendHead per road lane)
   const int32_t *tile_base, *tile_cap, *tile_ibase, *tile_icap;
   int32_t *cnt_in, *cnt_out;        // [n_tiles] stayer counts (read / write buffers)
   int32_t *icnt_in, *icnt_out;      // [n_tiles] inbox counts
-  Slab in, out;                     // stayer slabs
-  const InboxRec *inbox_in;
-  InboxRec *inbox_out;
-  uint32_t *scratch;                // snapshot of large tiles, at 5 x (base + ibase) words: s, v, vid, meta (stride cap + icap), then int16 src
-  int32_t *bsort_scratch;           // [Σ icap] inbox sort order for large inboxes
-  int32_t *dl_scratch;              // per-tile list of guard-deferred vehicles (scratch indexing)
-  // per tile, static (host-built): {base, ibase, cap, icap}, {desc_off, desc words,
-  // lanes, road lanes}, {ext offset, pend offset, 0, 0} (records of ext_buf / pend_buf)
+  // vehicle records of t (in) and t+1 (out), 32 B each: tile T
+  // owns [tile_base, tile_base + cap + icap); its stayers are right-aligned in
+  // [tile_base + cap - cnt, tile_base + cap), sorted by (lane_local, s, vid),
+  // its inbox follows at tile_ibase = tile_base + cap, so one contiguous copy
+  // fetches both
+  const InboxRec *vin;
+  InboxRec *vout;
+  uint32_t *scratch;                // snapshot of tiles in global mode, at 7 x tile_base words (stride cap + icap)
+  int32_t *bsort_scratch;           // [slots] inbox sort order of tiles in global mode (at tile_ibase)
+  // per tile, static (host-built): {base, ibase, cap, icap}, {block offset,
+  // block words, lanes, road lanes}, {descriptor words (= where the k_prep
+  // staging starts), 0, 0, 0}
   const int4 *tinfo;
-  // k_prep output for k_step: per junction lane of a tile the
-  // signal and the exit lane's first vehicle at t, per road lane the head of
-  // its pending-departure queue at t; contiguous per tile
-  ExtFirst *ext_buf;
-  PendHead *pend_buf;
   uint32_t *pscratch;               // pass state of tiles in global mode: 10 words per slot at
-                                    // 10 x (base + ibase + 4 x tile)
+                                    // 10 x (tile_base + 4 x tile)
   // migration to other partitions (world > 1): per-peer regions of MigRec
   MigRec *out_buf;
   const int32_t *out_off, *out_cap;
@@ -213,6 +207,11 @@ struct StepArgs {
   float *r_acc;
   uint8_t *r_guard, *r_mark;        // r_mark: processed by this partition in the last step
 };
+
+// the vehicles of tile T at t, stayers (sorted) then inbox records, contiguous
+__host__ __device__ inline const InboxRec *tile_recs(const StepArgs &A, int T, int n_st) {
+  return A.vin + A.tile_base[T] + A.tile_cap[T] - n_st;
+}
 
 struct SignalArgs {
   int32_t n_junctions, yellow;

@@ -205,17 +205,11 @@ __global__ void __launch_bounds__(128) k_lane_stats(StepArgs A, int32_t *cnt, in
   sv[lane] = 0.0;
   if (lane < nl) slen[lane] = A.lane_len[A.tile_lanes[l0 + lane]];
   __syncwarp();
-  const int base = A.tile_base[tile], ibase = A.tile_ibase[tile];
+  const InboxRec *rec = tile_recs(A, tile, ns);    // stayers then inbox, contiguous
   for (int i = lane; i < ns + ni; i += 32) {
-    float s, v;
-    uint32_t meta;
-    if (i < ns) {
-      const int gi = base + i;
-      s = A.in.s[gi]; v = A.in.v[gi]; meta = A.in.meta[gi];
-    } else {
-      const InboxRec r = A.inbox_in[ibase + i - ns];
-      s = r.s; v = r.v; meta = r.meta;
-    }
+    const InboxRec r = rec[i];
+    const float s = r.s, v = r.v;
+    const uint32_t meta = r.meta;
     const int l = m_lane(meta);
     atomicAdd(&sc[l], 1);
     if (road_speed) atomicAdd(&sv[l], (double)v);
@@ -272,7 +266,7 @@ __global__ void k_absorb(StepArgs A, const MigRec *in_buf, const int32_t *in_off
     const int dt = m.tile, vid = m.rec.vid;
     const int lane_g = A.tile_lanes[A.tile_lane_off[dt] + m_lane(m.rec.meta)];
     const int slot = atomicAdd(&A.icnt_out[dt], 1);
-    if (slot < A.tile_icap[dt]) put_inbox(A.inbox_out + A.tile_ibase[dt] + slot, m.rec);
+    if (slot < A.tile_icap[dt]) put_inbox(A.vout + A.tile_ibase[dt] + slot, m.rec);
     atomicMin(&A.summ_next[lane_g], vkey(m.rec.s, vid));
     A.pubv_next[vid] = m.rec.v;
     if (A.lane_cnt_next) atomicAdd(&A.lane_cnt_next[lane_g], 1);
@@ -367,18 +361,12 @@ __global__ void k_rehome(StepArgs A, const int32_t *new_owner) {
   const PeerView &P = A.peers[A.rank];
   const int par = A.t & 1, s3 = A.t % 3;
   const int n = A.cnt_in[T], m = A.icnt_in[T];
-  const int base = A.tile_base[T], ibase = A.tile_ibase[T];
-  const Slab &D = Q.slab[par];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int g = base + i, vid = A.in.vid[g];
-    D.s[g] = A.in.s[g]; D.v[g] = A.in.v[g]; D.vid[g] = vid; D.nxt[g] = A.in.nxt[g];
-    D.nxt2[g] = A.in.nxt2[g]; D.meta[g] = A.in.meta[g]; D.wait[g] = A.in.wait[g];
-    Q.insert_time[vid] = A.insert_time[vid];
-    Q.status[vid] = ST_DRIVING;
-  }
-  for (int i = threadIdx.x; i < m; i += blockDim.x) {
-    const InboxRec r = A.inbox_in[ibase + i];
-    put_inbox(Q.inbox[par] + ibase + i, r);
+  const int base = A.tile_base[T];
+  // stayers and inbox records: one contiguous range at the same positions
+  const int r0 = base + A.tile_cap[T] - n;
+  for (int i = threadIdx.x; i < n + m; i += blockDim.x) {
+    const InboxRec r = A.vin[r0 + i];
+    put_inbox(Q.inbox[par] + r0 + i, r);
     Q.insert_time[r.vid] = A.insert_time[r.vid];
     Q.status[r.vid] = ST_DRIVING;
   }
@@ -468,18 +456,12 @@ void launch_reduce_groups(const long long *tacc, const int32_t *tiles, int n_own
 __global__ void k_patch_routes(StepArgs A, const int32_t *patch) {
   const int tile = A.tiles[blockIdx.x];
   const int ns = A.cnt_in[tile], ni = A.icnt_in[tile];
+  InboxRec *rec = const_cast<InboxRec *>(tile_recs(A, tile, ns));
   for (int i = threadIdx.x; i < ns + ni; i += blockDim.x) {
-    int vid;
-    uint32_t *meta;
-    int32_t *nxt, *nxt2;
-    InboxRec *r = nullptr;
-    if (i < ns) {
-      const int gi = A.tile_base[tile] + i;
-      vid = A.in.vid[gi]; meta = A.in.meta + gi; nxt = A.in.nxt + gi; nxt2 = A.in.nxt2 + gi;
-    } else {
-      r = const_cast<InboxRec *>(A.inbox_in) + A.tile_ibase[tile] + i - ns;
-      vid = r->vid; meta = &r->meta; nxt = &r->nxt; nxt2 = &r->nxt2;
-    }
+    InboxRec *r = rec + i;
+    const int vid = r->vid;
+    uint32_t *meta = &r->meta;
+    int32_t *nxt = &r->nxt, *nxt2 = &r->nxt2;
     const int c = patch[vid];
     if (c < 0) continue;
     const int off = A.route_start[vid], len = A.route_len[vid];
@@ -495,16 +477,10 @@ __global__ void k_locate(StepArgs A, const int32_t *want, int32_t *out) {
   const int tile = A.tiles[blockIdx.x];
   const int ns = A.cnt_in[tile], ni = A.icnt_in[tile];
   const int l0 = A.tile_lane_off[tile];
+  const InboxRec *rec = tile_recs(A, tile, ns);
   for (int i = threadIdx.x; i < ns + ni; i += blockDim.x) {
-    int vid;
-    uint32_t meta;
-    if (i < ns) {
-      const int gi = A.tile_base[tile] + i;
-      vid = A.in.vid[gi]; meta = A.in.meta[gi];
-    } else {
-      const InboxRec &r = A.inbox_in[A.tile_ibase[tile] + i - ns];
-      vid = r.vid; meta = r.meta;
-    }
+    const int vid = rec[i].vid;
+    const uint32_t meta = rec[i].meta;
     const int b = want[vid];
     if (b < 0) continue;
     out[2 * b] = m_cursor(meta);

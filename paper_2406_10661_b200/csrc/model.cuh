@@ -38,7 +38,7 @@ constexpr float kEpsAcc = 2e-4f;    // m/s^2, accelerations / utilities
 constexpr float kEpsP = 2e-4f;      // draw vs p_LC
 constexpr float kEpsV = 2e-5f;      // relative, speed vs v_wait
 
-struct Guard { bool hit; unsigned why; };   // why: guard reason bits (stats builds)
+struct Guard { bool hit; };
 
 template <typename R> struct PV { R a_max, a_comf, T, s0, vmax, len, inv2; };
 __device__ __forceinline__ PV<double> pvals(const Prof &p, double) {
@@ -49,8 +49,13 @@ __device__ __forceinline__ PV<float> pvals(const Prof &p, float) {
 }
 
 // IDM (delta = 4) in canonical order; ledger L7 (no leader), L8.
+#ifdef KS_IDM_NOINLINE
+#define IDM_INLINE __noinline__
+#else
+#define IDM_INLINE __forceinline__
+#endif
 template <typename R, bool GUARD>
-__device__ __forceinline__ R idm(R v, R v0, bool lead, R gap, R dv, const PV<R> &p, R b_hard,
+__device__ IDM_INLINE R idm(R v, R v0, bool lead, R gap, R dv, const PV<R> &p, R b_hard,
                                  R gap_scale, Guard &g) {
   using M = Ar<R>;
   R x = M::div(v, v0);
@@ -61,7 +66,7 @@ __device__ __forceinline__ R idm(R v, R v0, bool lead, R gap, R dv, const PV<R> 
   if (!lead) {
     a = M::mul(p.a_max, fr);
   } else {
-    if (GUARD && gap_scale > (R)0 && fabsf((float)gap) <= kEpsPos * (float)gap_scale) g.hit = true, g.why |= (1u << 0);
+    if (GUARD && gap_scale > (R)0 && fabsf((float)gap) <= kEpsPos * (float)gap_scale) g.hit = true;
     if (gap <= (R)0) {
       a = -b_hard;
     } else {
@@ -135,13 +140,18 @@ __device__ __forceinline__ int m_lane(uint32_t m) { return (int)(m & 0xffu); }
 __device__ __forceinline__ int m_prof(uint32_t m) { return (int)((m >> 8) & 0xffu); }
 __device__ __forceinline__ int m_cursor(uint32_t m) { return (int)(m >> 16); }
 
+// route[idx] beyond the cached next two roads (rare: lookahead / hand-offs
+// past the next road), out of line to keep the hot passes small
+static __device__ __noinline__ int route_far(const StepArgs &A, int vid, int idx) {
+  int off = __ldg(A.route_start + vid);
+  int len = __ldg(A.route_len + vid);
+  return (idx >= 0 && idx < len) ? __ldg(A.route + off + idx) : -1;
+}
 __device__ __forceinline__ int route_at(const StepArgs &A, int vid, int c, int nxt, int nxt2,
                                         int idx) {
   if (idx == c + 1) return nxt;
   if (idx == c + 2) return nxt2;
-  int off = __ldg(A.route_start + vid);
-  int len = __ldg(A.route_len + vid);
-  return (idx >= 0 && idx < len) ? __ldg(A.route + off + idx) : -1;
+  return route_far(A, vid, idx);
 }
 
 __device__ __forceinline__ bool in4(const int4 &o, int R) {
@@ -224,8 +234,8 @@ __device__ __forceinline__ int next_from_road_t(const StepArgs &A, const TileSh 
                                                 int R2) {
   return next1_t(A, T, l, R1, R2).j;
 }
-// any road lane (global id g)
-__device__ __forceinline__ int next_from_road_any(const StepArgs &A, const TileSh &T, int g,
+// any road lane (global id g); out of line (hand-offs and deep lookahead only)
+static __device__ __noinline__ int next_from_road_any(const StepArgs &A, const TileSh &T, int g,
                                                   int R1, int R2) {
   if (__ldg(A.lane_tile + g) == T.tile) {
     const int l = A.lane_local[g];
@@ -420,7 +430,7 @@ __device__ __forceinline__ LEv<R> eval_lane(const StepArgs &A, const TileSh &T, 
   e.limrel = (R)0;
   if (GUARD && e.phantom && e.has_leader &&
       fabsf((float)(L - lim_lead)) <= kEpsPos * (float)(L + fabs(lim_lead)))
-    g.hit = true, g.why |= (1u << 1);
+    g.hit = true;
   if (e.phantom && (!e.has_leader || L <= lim_lead)) {
     e.has_lim = true;
     e.lim = L;
@@ -458,7 +468,6 @@ template <typename R> struct SideRes {
   R a, lim, limrel, vlim;
   int next1;
   bool has_lim, hit;
-  unsigned why;
 };
 
 // O7 decision for a vehicle with at least one admissible side:
@@ -476,7 +485,6 @@ __device__ __noinline__ SideRes<R> lane_change(const StepArgs &A, const TileSh &
   using M = Ar<R>;
   Guard g;
   g.hit = false;
-  g.why = 0;
   SideRes<R> o;
   o.choice = -1;
   bool need0 = adm0 && (inG || mand < 0);
@@ -499,7 +507,7 @@ __device__ __noinline__ SideRes<R> lane_change(const StepArgs &A, const TileSh &
     const double pmax = ub >= (R)1 ? 0.9 : fmax(2e-8, (double)(0.9 - 2e-8) * (double)ub);
     if (r >= pmax + 1e-3) need0 = need1 = false;       // no change, for certain
   }
-  if (!(need0 || need1)) { o.hit = g.hit; o.why = g.why; return o; }
+  if (!(need0 || need1)) { o.hit = g.hit; return o; }
   // ã_ego on each side; keep the utility of both and the evaluation of the
   // side that would be taken (argmax, tie -> left: P:196, ledger L15)
   R u0 = (R)0, u1 = (R)0;
@@ -523,10 +531,10 @@ __device__ __noinline__ SideRes<R> lane_change(const StepArgs &A, const TileSh &
     if (uT >= (R)1) pl = 0.9;
     else if (uT > (R)0) pl = (double)M::mul((R)(0.9 - 2e-8), uT);
     else pl = 2e-8;
-    if (GUARD && fabs(r - pl) <= (double)kEpsP) g.hit = true, g.why |= (1u << 6);
+    if (GUARD && fabs(r - pl) <= (double)kEpsP) g.hit = true;
     if (r < pl) {                                        // P:196, ledger L15
       if (need0 && need1) {
-        if (GUARD && fabsf((float)(u0 - u1)) <= kEpsAcc) g.hit = true, g.why |= (1u << 7);
+        if (GUARD && fabsf((float)(u0 - u1)) <= kEpsAcc) g.hit = true;
         choice = (u0 >= u1) ? 0 : 1;
       } else {
         choice = need0 ? 0 : 1;
@@ -543,7 +551,6 @@ __device__ __noinline__ SideRes<R> lane_change(const StepArgs &A, const TileSh &
   o.next1 = best.next1;
   o.has_lim = best.has_lim;
   o.hit = g.hit;
-  o.why = g.why;
   return o;
 }
 
@@ -584,7 +591,7 @@ __device__ __forceinline__ Elig lc_elig(const StepArgs &A, const TileSh &T, int 
     const R need = M::add(p.s0, M::mul(v, p.T));
     const bool l19 = rem < need;                         // ledger L19
     if (GUARD && inG && v != (R)0 && fabsf((float)(rem - need)) <= kEpsPos * (float)(fabs(rem) + need))
-      g.hit = true, g.why |= (1u << 2);
+      g.hit = true;
     sl0 = T.left[l];
     sl1 = T.right[l];
     consider = inG ? !l19 : (mand != 0);
@@ -651,28 +658,28 @@ __device__ __forceinline__ SideRes<R> lc_decide(const StepArgs &A, const TileSh 
         const R sf = (R)C.s(fi);
         const R lf = (R)T.P[m_prof(C.meta(fi))].len;
         const R gf = M::sub(M::sub(sf, s), lf);
-        if (GUARD && fabsf((float)gf) <= kEpsPos * (float)(fabs(sf - s) + lf)) g.hit = true, g.why |= (1u << 5);
+        if (GUARD && fabsf((float)gf) <= kEpsPos * (float)(fabs(sf - s) + lf)) g.hit = true;
         if (!(gf >= (R)0)) ok = false;                   // L17 (2)
       }
       if (ok && bi >= 0) {
         const R sb = (R)C.s(bi);
         const R gb = M::sub(M::sub(s, sb), p.len);
         const R gbs = fabs(s - sb) + p.len;
-        if (GUARD && fabsf((float)gb) <= kEpsPos * (float)gbs) g.hit = true, g.why |= (1u << 0);
+        if (GUARD && fabsf((float)gb) <= kEpsPos * (float)gbs) g.hit = true;
         if (!(gb >= (R)0)) ok = false;                   // L17 (2)
         if (ok) {
           const PV<R> pb = pvals(T.P[m_prof(C.meta(bi))], (R)0);
           const R vb = (R)C.v(bi);
           const R v0b = (pb.vmax < (R)T.vmax[ls]) ? pb.vmax : (R)T.vmax[ls];
           const R an = idm<R, GUARD>(vb, v0b, true, gb, M::sub(vb, v), pb, b_hard, gbs, g);
-          if (GUARD && fabsf((float)(an + (R)A.b_safe)) <= kEpsAcc) g.hit = true, g.why |= (1u << 3);
+          if (GUARD && fabsf((float)(an + (R)A.b_safe)) <= kEpsAcc) g.hit = true;
           if (!(an >= -(R)A.b_safe)) ok = false;         // L17 (1)
           if (sd == 0) anew0 = an; else anew1 = an;
         }
       } else if (ok) {
         const R mrg = M::sub(s, p.len);
         if (GUARD && fabsf((float)mrg - (float)A.start_margin) <= kEpsPos * ((float)s + (float)A.start_margin))
-          g.hit = true, g.why |= (1u << 4);
+          g.hit = true;
         if (!(mrg >= (R)A.start_margin)) ok = false;    // L17 (3) lane-start rule
       }
       if (sd == 0) adm0 = ok; else adm1 = ok;
@@ -732,11 +739,10 @@ __device__ __forceinline__ SideRes<R> lc_decide(const StepArgs &A, const TileSh 
   SideRes<R> sr;
   sr.choice = -1;
   sr.hit = false;
-  sr.why = 0;
   if (adm0 || adm1)                                      // O7 decision
     sr = lane_change<R, GUARD>(A, T, C, adm0, adm1, inG, mand, sl0, sl1, f0, f1, s, v, p, me,
                                a_cur, pol0, pol1, r);
-  if (sr.hit) g.hit = true, g.why |= sr.why;
+  if (sr.hit) g.hit = true;
   return sr;
 }
 
@@ -774,11 +780,11 @@ __device__ __forceinline__ void integrate(const StepArgs &A, const TileSh &T, R 
     } else {
       bind = adv > use.limrel;
       if (GUARD && !adv_zero && fabsf((float)(adv - use.limrel)) <= kEpsPos * (float)(fabs(adv) + fabs(use.limrel) + (R)1e-3))
-        g.hit = true, g.why |= (1u << 8);
+        g.hit = true;
     }
     if (bind) {
       if (GUARD && fabsf((float)use.limrel) <= kEpsPos * (float)(fabs(s) + fabs(use.lim)))
-        g.hit = true, g.why |= (1u << 9);
+        g.hit = true;
       if (M::fp64 ? (use.lim < s) : (use.limrel < (R)0)) { s1 = s; adv = (R)0; v1 = (R)0; }
       else { s1 = use.lim; adv = use.limrel; v1 = (use.vlim < v1) ? use.vlim : v1; }
     }
@@ -797,13 +803,13 @@ __device__ __forceinline__ void integrate(const StepArgs &A, const TileSh &T, R 
       const R rem = M::sub(es, pb);
       if (GUARD && !(adv_zero && hand == 0) &&
           fabsf((float)(pa - rem)) <= kEpsPos * (float)(fabs(pa) + fabs(rem) + (R)1e-3))
-        g.hit = true, g.why |= (1u << 10);
+        g.hit = true;
       if (pa >= rem) { fin = true; break; }
     }
     const R rem = M::sub(Lc, pb);
     if (GUARD && n >= 0 && !(adv_zero && hand == 0) &&
         fabsf((float)(pa - rem)) <= kEpsPos * (float)(fabs(pa) + fabs(rem) + (R)1e-3))
-      g.hit = true, g.why |= (1u << 11);
+      g.hit = true;
     if (pa > rem && n >= 0) {
       pb = M::sub(pb, Lc);
       curg = n;
@@ -825,7 +831,7 @@ __device__ __forceinline__ void integrate(const StepArgs &A, const TileSh &T, R 
   }
   s1 = M::fp64 ? pb : (hand == 0 ? s1 : M::add(pb, pa));
   const R vw = (R)A.v_wait;
-  if (GUARD && fabsf((float)(v1 - vw)) <= kEpsV * (float)(fabs(v) + fabs(a) + (R)1)) g.hit = true, g.why |= (1u << 12);
+  if (GUARD && fabsf((float)(v1 - vw)) <= kEpsV * (float)(fabs(v) + fabs(a) + (R)1)) g.hit = true;
   o.wait1 = wait0 + ((v1 < vw) ? 1 : 0);                 // ledger L28
   o.s1 = (float)s1;
   o.v1 = (float)v1;

@@ -91,7 +91,6 @@ struct Part {
   int rank = 0;
   StepArgs A{};
   SignalArgs SG{};
-  Slab slab[2]{};
   InboxRec *inbox[2]{};
   int32_t *cnt[2]{}, *icnt[2]{};
   unsigned long long *summ[3]{};
@@ -149,7 +148,7 @@ struct sim_s {
   std::vector<int> tile_lane_off, tile_lanes, tile_nroad, tile_base, tile_cap, tile_ibase, tile_icap;
   std::vector<int> lane_tile;
   std::vector<uint8_t> lane_local;
-  int64_t sum_cap = 0, sum_icap = 0;
+  int64_t n_slots = 0;                          // vehicle record slots (all tiles' regions)
   // trips
   std::vector<int> route_off, route, depart, start_lane;
   std::vector<int> rstart, rlen;                // per vehicle: route[rstart .. rstart + rlen) (set_vehicle_route appends)
@@ -182,7 +181,8 @@ struct sim_s {
   int t = 0;
   std::vector<uint8_t> dir, usable;
   std::vector<int32_t> outroads;     // [4 * n_lanes]
-  std::vector<int32_t> desc, desc_off;   // tile descriptors (dev.h)
+  std::vector<int32_t> desc, desc_off;   // tile blocks: descriptor (dev.h) + k_prep staging
+  std::vector<int32_t> desc_words;       // per tile: words of the descriptor part
   int64_t fin0 = 0;                  // FINISHED vehicles in the last loaded state
   long long acc_fin0 = 0;            // finished counter at the last load
   // batched environments (NEXT-3)
@@ -271,6 +271,7 @@ void build_desc(sim_s *h) {
   if (h->tile_lane_off.empty()) return;
   h->desc.clear();
   h->desc_off.assign(h->nt + 1, 0);
+  h->desc_words.assign(h->nt, 0);
   for (int T = 0; T < h->nt; ++T) {
     const int l0 = h->tile_lane_off[T], nl = h->tile_lane_off[T + 1] - l0, nroad = h->tile_nroad[T];
     // successor table of the road lanes (static between setters, so sorted and
@@ -360,6 +361,11 @@ void build_desc(sim_s *h) {
       w.insert(w.end(), tw, tw + kDescTroadWords);
     }
     while (w.size() % 4) w.push_back(0);
+    // then room for what k_prep stages per step: an ExtFirst per
+    // junction lane and a PendHead per road lane (8 words each), so that the
+    // tile's whole block is one bulk copy
+    h->desc_words[T] = (int)w.size();
+    w.insert(w.end(), (size_t)8 * nl, 0);
     h->desc.insert(h->desc.end(), w.begin(), w.end());
     h->desc_off[T + 1] = (int)h->desc.size();
   }
@@ -663,12 +669,14 @@ sim_status build_tiles(sim_s *h) {
     if (cap > 32767 || icap > 32767)                // snapshot source indices are int16
       return fail(h, SIM_E_INVALID, "road " + std::to_string(r) + " is too long (tile capacity > 32767 vehicles)");
     h->tile_lane_off[r + 1] = (int)h->tile_lanes.size();
+    // one record region per tile: stayers right-aligned in the
+    // first cap slots, the inbox in the next icap
     h->tile_base[r] = (int)base; h->tile_cap[r] = cap;
-    h->tile_ibase[r] = (int)ibase; h->tile_icap[r] = icap;
-    base += cap; ibase += icap;
-    if (base + ibase > 2000000000LL) return fail(h, SIM_E_INVALID, "network too large for 32-bit slot indices");
+    h->tile_ibase[r] = (int)(base + cap); h->tile_icap[r] = icap;
+    base += cap + icap;
+    if (base > 2000000000LL) return fail(h, SIM_E_INVALID, "network too large for 32-bit slot indices");
   }
-  h->sum_cap = base; h->sum_icap = ibase;
+  h->n_slots = base;
   return SIM_OK;
 }
 
@@ -826,9 +834,8 @@ sim_status upload_state(sim_s *h, const HostState &S) {
       if (l < 0 || l >= h->nl) return fail(h, SIM_E_RANGE, "lane out of range for driving vehicle " + std::to_string(k));
       per_tile[h->lane_tile[l]].push_back(k);
     }
-  std::vector<float> s(h->sum_cap, 0.f), v(h->sum_cap, 0.f);
-  std::vector<int> vid(h->sum_cap, 0), nx(h->sum_cap, 0), nx2(h->sum_cap, 0), wt(h->sum_cap, 0);
-  std::vector<uint32_t> meta(h->sum_cap, 0);
+  std::vector<InboxRec> rec(h->n_slots);
+  std::memset(rec.data(), 0, rec.size() * sizeof(InboxRec));
   std::vector<int> cnt(nt, 0);
   std::vector<unsigned long long> summ(h->nl, kEmptyKey);
   std::vector<float> pubv(nv, 0.f);
@@ -842,16 +849,19 @@ sim_status upload_state(sim_s *h, const HostState &S) {
     });
     if ((int)ks.size() > h->tile_cap[T])
       return fail(h, SIM_E_CAPACITY, "state exceeds the slot capacity of road tile " + std::to_string(T));
+    const int p0 = h->tile_base[T] + h->tile_cap[T] - (int)ks.size();   // right-aligned stayers
     for (size_t i = 0; i < ks.size(); ++i) {
-      int k = ks[i], p = h->tile_base[T] + (int)i;
-      s[p] = S.s[k] == 0.0f ? 0.0f : S.s[k];
-      v[p] = S.v[k];
-      vid[p] = k;
-      nx[p] = route_at(h, k, S.cursor[k] + 1);
-      nx2[p] = route_at(h, k, S.cursor[k] + 2);
-      meta[p] = pack_meta(h->lane_local[S.lane[k]], h->vprof[k], S.cursor[k]);
-      wt[p] = S.wait[k];
-      unsigned long long key = ((unsigned long long)*(const uint32_t *)&s[p] << 32) | (unsigned)k;
+      int k = ks[i];
+      InboxRec &r = rec[(size_t)p0 + i];
+      r.s = S.s[k] == 0.0f ? 0.0f : S.s[k];
+      r.v = S.v[k];
+      r.vid = k;
+      r.nxt = route_at(h, k, S.cursor[k] + 1);
+      r.nxt2 = route_at(h, k, S.cursor[k] + 2);
+      r.meta = pack_meta(h->lane_local[S.lane[k]], h->vprof[k], S.cursor[k]);
+      r.wait = S.wait[k];
+      r.pad = 0;
+      unsigned long long key = ((unsigned long long)*(const uint32_t *)&r.s << 32) | (unsigned)k;
       int l = S.lane[k];
       if (key < summ[l]) summ[l] = key;
       pubv[k] = S.v[k];
@@ -896,14 +906,7 @@ sim_status upload_state(sim_s *h, const HostState &S) {
     CK(h, cudaMemcpyAsync(P.usable_d, h->usable.data(), h->nl, cudaMemcpyHostToDevice, st));
     CK(h, cudaMemcpyAsync(P.outroads_d, h->outroads.data(), h->outroads.size() * 4, cudaMemcpyHostToDevice, st));
     CK(h, cudaMemcpyAsync(P.desc_d, h->desc.data(), h->desc.size() * 4, cudaMemcpyHostToDevice, st));
-    Slab &o = P.slab[par];
-    CK(h, cudaMemcpyAsync(o.s, s.data(), s.size() * 4, cudaMemcpyHostToDevice, st));
-    CK(h, cudaMemcpyAsync(o.v, v.data(), v.size() * 4, cudaMemcpyHostToDevice, st));
-    CK(h, cudaMemcpyAsync(o.vid, vid.data(), vid.size() * 4, cudaMemcpyHostToDevice, st));
-    CK(h, cudaMemcpyAsync(o.nxt, nx.data(), nx.size() * 4, cudaMemcpyHostToDevice, st));
-    CK(h, cudaMemcpyAsync(o.nxt2, nx2.data(), nx2.size() * 4, cudaMemcpyHostToDevice, st));
-    CK(h, cudaMemcpyAsync(o.meta, meta.data(), meta.size() * 4, cudaMemcpyHostToDevice, st));
-    CK(h, cudaMemcpyAsync(o.wait, wt.data(), wt.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(P.inbox[par], rec.data(), rec.size() * sizeof(InboxRec), cudaMemcpyHostToDevice, st));
     CK(h, cudaMemcpyAsync(P.cnt[par], pc.data(), nt * 4, cudaMemcpyHostToDevice, st));
     CK(h, cudaMemsetAsync(P.icnt[0], 0, nt * 4, st));
     CK(h, cudaMemsetAsync(P.icnt[1], 0, nt * 4, st));
@@ -994,37 +997,27 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   A.n_own = (int)P.tiles.size();
   A.rank = P.rank;
   for (int b = 0; b < 2; ++b) {
-    Slab &s = P.slab[b];
-    AL(s.s, h->sum_cap); AL(s.v, h->sum_cap); AL(s.vid, h->sum_cap); AL(s.nxt, h->sum_cap);
-    AL(s.nxt2, h->sum_cap); AL(s.meta, h->sum_cap); AL(s.wait, h->sum_cap);
-    AL(P.inbox[b], h->sum_icap);
+    AL(P.inbox[b], h->n_slots);                   // vehicle records: stayers + inboxes
     AL(P.cnt[b], nt); AL(P.icnt[b], nt);
     AL(P.pubv[b], nv);
     CK(h, cudaMemset(P.cnt[b], 0, nt * 4));
     CK(h, cudaMemset(P.icnt[b], 0, nt * 4));
     CK(h, cudaMemset(P.pubv[b], 0, nv * 4));
   }
-  const int64_t sc = h->sum_cap + h->sum_icap;
+  const int64_t sc = h->n_slots;
   AL(A.scratch, 7 * sc);
-  AL(A.bsort_scratch, h->sum_icap);
-  AL(A.dl_scratch, sc);
+  AL(A.bsort_scratch, sc);
   AL(A.pscratch, 10 * (sc + 4 * (int64_t)nt));
   {
-    // static per-tile record of k_step's producer warp + the k_prep staging
-    // buffers (offsets over all tiles, so repartitioning needs no change)
+    // static per-tile record read by k_step's producer warp and k_prep
     std::vector<int4> ti(3 * (size_t)nt);
-    int64_t xo = 0, po = 0;
     for (int T = 0; T < nt; ++T) {
       const int nlT = h->tile_lane_off[T + 1] - h->tile_lane_off[T], nr = h->tile_nroad[T];
       ti[3 * T + 0] = make_int4(h->tile_base[T], h->tile_ibase[T], h->tile_cap[T], h->tile_icap[T]);
       ti[3 * T + 1] = make_int4(h->desc_off[T], h->desc_off[T + 1] - h->desc_off[T], nlT, nr);
-      ti[3 * T + 2] = make_int4((int)xo, (int)po, 0, 0);
-      xo += nlT - nr;
-      po += nr;
+      ti[3 * T + 2] = make_int4(h->desc_words[T], 0, 0, 0);
     }
     int4 *i4; UP(i4, ti); A.tinfo = i4;
-    AL(A.ext_buf, std::max<int64_t>(xo, 1));
-    AL(A.pend_buf, std::max<int64_t>(po, 1));
   }
   for (int b = 0; b < 3; ++b) AL(P.summ[b], nl);
   UP(P.route_start_d, h->rstart); A.route_start = P.route_start_d;
@@ -1137,7 +1130,7 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   V.insert_time = A.insert_time;
   V.status = A.status;
   V.bar = P.bar_d;
-  for (int b = 0; b < 2; ++b) { V.slab[b] = P.slab[b]; V.cnt[b] = P.cnt[b]; }
+  for (int b = 0; b < 2; ++b) V.cnt[b] = P.cnt[b];
   V.pend_head = P.pend_head_d;
   V.arrive_time = A.arrive_time;
   V.wait_fin = A.wait_fin;
@@ -1154,14 +1147,12 @@ StepArgs step_args(const Part &P, int t) {
   StepArgs a = P.A;
   const int par = t & 1;
   a.t = t;
-  a.in = P.slab[par];
-  a.out = P.slab[par ^ 1];
   a.cnt_in = P.cnt[par];
   a.cnt_out = P.cnt[par ^ 1];
   a.icnt_in = P.icnt[par];
   a.icnt_out = P.icnt[par ^ 1];
-  a.inbox_in = P.inbox[par];
-  a.inbox_out = P.inbox[par ^ 1];
+  a.vin = P.inbox[par];
+  a.vout = P.inbox[par ^ 1];
   a.summ_cur = P.summ[t % 3];
   a.summ_next = P.summ[(t + 1) % 3];
   a.summ_clear = P.summ[(t + 2) % 3];
@@ -2142,16 +2133,7 @@ static sim_status read_state_impl(sim_s *h, sim_state *o, bool global) {
     std::vector<int> cnt(nt), icnt(nt);
     CK(h, cudaMemcpy(cnt.data(), P.V.cnt[par], nt * 4, cudaMemcpyDeviceToHost));
     CK(h, cudaMemcpy(icnt.data(), P.V.icnt[par], nt * 4, cudaMemcpyDeviceToHost));
-    const Slab &sl = P.V.slab[par];
-    std::vector<float> s(h->sum_cap), v(h->sum_cap);
-    std::vector<int> vid(h->sum_cap), wt(h->sum_cap);
-    std::vector<uint32_t> meta(h->sum_cap);
-    CK(h, cudaMemcpy(s.data(), sl.s, s.size() * 4, cudaMemcpyDeviceToHost));
-    CK(h, cudaMemcpy(v.data(), sl.v, v.size() * 4, cudaMemcpyDeviceToHost));
-    CK(h, cudaMemcpy(vid.data(), sl.vid, vid.size() * 4, cudaMemcpyDeviceToHost));
-    CK(h, cudaMemcpy(wt.data(), sl.wait, wt.size() * 4, cudaMemcpyDeviceToHost));
-    CK(h, cudaMemcpy(meta.data(), sl.meta, meta.size() * 4, cudaMemcpyDeviceToHost));
-    std::vector<InboxRec> ib(h->sum_icap);
+    std::vector<InboxRec> ib(h->n_slots);
     CK(h, cudaMemcpy(ib.data(), P.V.inbox[par], ib.size() * sizeof(InboxRec), cudaMemcpyDeviceToHost));
     std::vector<uint8_t> pst(nv);
     std::vector<int> pins(nv), parr(nv), pwf(nv);
@@ -2168,7 +2150,10 @@ static sim_status read_state_impl(sim_s *h, sim_state *o, bool global) {
       vs[k] = ss; vv[k] = v_; cur[k] = (int)(m >> 16); wait[k] = w; driving[k] = 1;
     };
     for (int T : P.tiles) {
-      for (int i = 0; i < cnt[T]; ++i) { int p = h->tile_base[T] + i; put(T, vid[p], s[p], v[p], meta[p], wt[p]); }
+      for (int i = 0; i < cnt[T]; ++i) {
+        const InboxRec &r = ib[h->tile_base[T] + h->tile_cap[T] - cnt[T] + i];
+        put(T, r.vid, r.s, r.v, r.meta, r.wait);
+      }
       for (int i = 0; i < icnt[T]; ++i) { const InboxRec &r = ib[h->tile_ibase[T] + i]; put(T, r.vid, r.s, r.v, r.meta, r.wait); }
     }
   }

@@ -1,7 +1,7 @@
 set -x
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
-timeout 300 python scripts/time_c4.py > gpurun_out/sweep6.log 2>&1
-for v in prof cw8 cw10; do timeout 300 python scripts/time_c4.py variants/$v.so; done >> gpurun_out/sweep6.log 2>&1
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "one_step or exact_mode" > gpurun_out/parity6.log 2>&1
-tail -3 gpurun_out/parity6.log
-cat gpurun_out/sweep6.log
+timeout 120 python scripts/time_c4.py > gpurun_out/sweep18.log 2>&1
+for v in free prof cw10 cw14; do timeout 120 python scripts/time_c4.py variants/$v.so; done >> gpurun_out/sweep18.log 2>&1
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/gputests18.log 2>&1
+tail -3 gpurun_out/gputests18.log
+cat gpurun_out/sweep18.log

@@ -45,7 +45,7 @@ try:
         torch.cuda.synchronize()
         L.sim_debug_kstep_prof(pb)
         names = {0: "P wait_empty", 1: "P build", 2: "P issue", 3: "P gather",
-                 8: "C wait_full", 9: "C claim", 10: "C tile"}
+                 8: "C wait_full", 9: "C claim", 10: "C tile", 11: "C round barrier"}
         tot_p = sum(pb[i] for i in range(0, 5)); tot_c = sum(pb[i] for i in range(8, 19))
         for i, nm in names.items():
             tot = tot_p if i < 8 else tot_c
