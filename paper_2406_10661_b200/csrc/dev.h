@@ -67,8 +67,9 @@ struct __align__(16) InboxRec {      // 32 B vehicle record (stayer or inbox), o
   float s, v;
   int32_t vid, nxt, nxt2;
   uint32_t meta;                    // lane_local:8 | profile:8 | cursor:16
-  int32_t wait, pad;
-};
+  int32_t wait;
+  float end_s;                      // end position on the destination road (trip input, carried
+};                                  // so the step needs no per-vehicle global read)
 
 // Gathered by the producer warp of k_step for every junction lane of a tile
 // (DESIGN §3.2): the first vehicle of the junction lane's exit lane at t (the
@@ -78,8 +79,13 @@ struct ExtFirst {
   float s, v, len, Lb;              // position / speed / vehicle length; Lb = length of the exit lane
   int32_t vid;                      // -1: the exit lane is empty
   int32_t sig;                      // signal of the junction lane at t
-  int32_t b, pad;                   // the exit lane
+  int32_t b;                        // the exit lane
+  // where a vehicle handed off into b goes (its tile's inbox): tile, b's
+  // tile-local index, the tile's inbox start and capacity, the owner partition
+  int32_t dtile, dlocal, dibase, dicap, downer;
 };
+static_assert(sizeof(ExtFirst) == 48, "ExtFirst: 12 words (16-B multiple for bulk copies)");
+constexpr int kExtWords = (int)(sizeof(ExtFirst) / 4);
 
 // Head of a road lane's pending-departure queue at t (K11), gathered
 // by the producer warp: k = vid (-1: none due), its depart step, start
@@ -167,7 +173,7 @@ struct StepArgs {
   // fetches both
   const InboxRec *vin;
   InboxRec *vout;
-  uint32_t *scratch;                // snapshot of tiles in global mode, at 7 x tile_base words (stride cap + icap)
+  uint32_t *scratch;                // snapshot of tiles in global mode, at 8 x tile_base words (stride cap + icap)
   int32_t *bsort_scratch;           // [slots] inbox sort order of tiles in global mode (at tile_ibase)
   // per tile, static (host-built): {base, ibase, cap, icap}, {block offset,
   // block words, lanes, road lanes}, {descriptor words (= where the k_prep

@@ -468,6 +468,7 @@ __global__ void k_patch_routes(StepArgs A, const int32_t *patch) {
     *meta = (*meta & 0xffffu) | ((uint32_t)c << 16);
     *nxt = c + 1 < len ? A.route[off + c + 1] : -1;
     *nxt2 = c + 2 < len ? A.route[off + c + 2] : -1;
+    r->end_s = A.end_s[vid];                        // the new destination's end position
   }
 }
 

@@ -73,7 +73,7 @@ __device__ __forceinline__ SlotLayout slot_layout(int n_st, int n_in, int dw) {
   uint32_t o = 0;
   L.veh = o;   o += 32u * (uint32_t)L.n4;              // InboxRec records, then the PState
   L.desc = o;  o += 4u * (uint32_t)dw;                 // dw is a multiple of 4
-  L.snap = o;  o += 28u * (uint32_t)L.n4;              // merged snapshot (View, stride n4)
+  L.snap = o;  o += 32u * (uint32_t)L.n4;              // merged snapshot (View, stride n4)
   L.sortk = o; o += 16u * (uint32_t)n_in;              // sorted inbox keys
   L.size = o;
   return L;
@@ -88,14 +88,14 @@ struct __align__(16) Hdr {          // one ring entry
 
 // per-vehicle pass state of one tile (slot in shared memory, or the global
 // pass scratch for a tile in global mode), indexed by snapshot position;
-// 29 B per vehicle (fits the 32 B of the vehicle record it replaces).  The
+// 30 B per vehicle (fits the 32 B of the vehicle record it replaces).  The
 // stayer results rs1 / rv1 share pa / plim: both are written by the thread
 // that has just read a / lim of the same vehicle (pass 3, fp64 path).
 struct PState {
   float *pa, *plim, *plimrel, *pvlim, *rs1, *rv1;
   int *pnext1;
   uint32_t *pfl;
-  uint8_t *kind;
+  uint8_t *kind, *pnl;                // pnl: next1 as a local junction lane (0xff none)
   uint16_t *cand, *defl;
 };
 __device__ __forceinline__ PState pstate_at(unsigned char *p, int n4) {
@@ -108,6 +108,7 @@ __device__ __forceinline__ PState pstate_at(unsigned char *p, int n4) {
   S.kind = reinterpret_cast<uint8_t *>(f + 6 * n4);
   S.cand = reinterpret_cast<uint16_t *>(S.kind + n4);
   S.defl = S.cand + n4;
+  S.pnl = reinterpret_cast<uint8_t *>(S.defl + n4);
   return S;
 }
 
@@ -192,6 +193,7 @@ __device__ __forceinline__ void mbar_wait_sleep(unsigned long long *b, unsigned 
 // ---- phase profiling (dev builds with -DKS_PROF; sim_debug_kstep_prof) ----------
 #ifdef KS_PROF
 __device__ unsigned long long g_ks_prof[32];
+__device__ unsigned int g_tile_cyc[65536][4];       // per tile: cycles, vehicles, candidates, round slowest
 #define KP_DECL long long kp_last = clock64();
 #define KP(idx, on)                                                    \
   do {                                                                 \
@@ -310,14 +312,24 @@ __device__ __noinline__ void emit_moved(const StepArgs &A, const View &C, int i,
   rec.vid = vid;
   rec.nxt = route_at(A, vid, cur, r.nxt, r.nxt2, r.cursor + 1);
   rec.nxt2 = route_at(A, vid, cur, r.nxt, r.nxt2, r.cursor + 2);
-  rec.meta = pack_meta(A.lane_local[r.lane_g], m_prof(meta), r.cursor);
+  // the destination tile: this one (lane change, hand-off into its junction
+  // lane), the exit lane's tile staged by k_prep, or the global tables
+  int dt, dl, dib, dic, owner;
+  if (r.cl >= 0) {
+    dt = T.tile; dl = r.cl; dib = T.ibase; dic = T.icap; owner = A.rank;
+  } else if (r.cx >= 0) {
+    const ExtFirst &x = T.ext[r.cx - T.nroad];
+    dt = x.dtile; dl = x.dlocal; dib = x.dibase; dic = x.dicap; owner = x.downer;
+  } else {
+    dt = A.lane_tile[r.lane_g]; dl = A.lane_local[r.lane_g];
+    dib = A.tile_ibase[dt]; dic = A.tile_icap[dt]; owner = A.tile_owner[dt];
+  }
+  rec.meta = pack_meta(dl, m_prof(meta), r.cursor);
   rec.wait = r.wait1;
-  rec.pad = 0;
-  const int dt = A.lane_tile[r.lane_g];
-  const int owner = A.tile_owner[dt];
+  rec.end_s = C.ends(i);
   if (owner == A.rank) {
     const int slot = atomicAdd(&A.icnt_out[dt], 1);
-    if (slot < A.tile_icap[dt]) put_inbox(A.vout + A.tile_ibase[dt] + slot, rec);
+    if (slot < dic) put_inbox(A.vout + dib + slot, rec);
     else atomicAdd(&T.c_ovf, 1);
     atomicMin(&A.summ_next[r.lane_g], vkey(r.s1, vid));
     A.pubv_next[vid] = r.v1;
@@ -360,7 +372,12 @@ __global__ void __launch_bounds__(128) k_prep(const __grid_constant__ StepArgs A
     e.sig = A.lane_sig[g];
     e.b = b;
     e.Lb = A.lane_len[b];
-    e.pad = 0;
+    const int dt = A.lane_tile[b];
+    e.dtile = dt;
+    e.dlocal = A.lane_local[b];
+    e.dibase = A.tile_ibase[dt];
+    e.dicap = A.tile_icap[dt];
+    e.downer = A.tile_owner[dt];
     unsigned long long key;
     const float *pv = A.pubv_cur;
     if (!A.peers) {
@@ -397,7 +414,7 @@ __global__ void __launch_bounds__(128) k_prep(const __grid_constant__ StepArgs A
         ph.prof = A.veh_prof[vk];
       }
     }
-    reinterpret_cast<PendHead *>(stage + 8 * (nl - nroad))[l] = ph;
+    reinterpret_cast<PendHead *>(stage + kExtWords * (nl - nroad))[l] = ph;
   }
 }
 
@@ -650,6 +667,7 @@ __device__ __forceinline__ void pass1(const StepArgs &A, const PState &K, const 
   me.cur = m_cursor(meta);
   me.nxt = C.nxt(i);
   me.nxt2 = C.nxt2(i);
+  me.ends = C.ends(i);
   const PV<float> p = pvals(T.P[m_prof(meta)], 0.f);
   const float s = C.s(i), v = C.v(i);
   const int lead = (i + 1 < T.seg_end[l]) ? i + 1 : -1;
@@ -678,6 +696,7 @@ __device__ __forceinline__ void pass1(const StepArgs &A, const PState &K, const 
   K.plimrel[i] = use.limrel;
   K.pvlim[i] = use.vlim;
   K.pnext1[i] = use.next1;
+  K.pnl[i] = (uint8_t)(use.nl1 < 0 ? 0xff : use.nl1);
   K.pfl[i] = (use.has_lim ? F_LIM : 0u) | (g.hit ? F_HIT : 0u) | (E.inG ? F_ING : 0u) |
              (E.want0 ? F_W0 : 0u) | (E.want1 ? F_W1 : 0u) | ((uint32_t)(E.mand + 1) << F_MAND_SH) |
              ((uint32_t)(me.k + 1) << F_K_SH) | ((uint32_t)l << F_NL_SH) | (1u << F_LC_SH);
@@ -694,6 +713,7 @@ __device__ __forceinline__ void pass2(const StepArgs &A, const PState &K, const 
   me.cur = m_cursor(meta);
   me.nxt = C.nxt(i);
   me.nxt2 = C.nxt2(i);
+  me.ends = C.ends(i);
   me.k = (int)((fl >> F_K_SH) & 31u) - 1;
   const PV<float> p = pvals(T.P[m_prof(meta)], 0.f);
   const float s = C.s(i), v = C.v(i);
@@ -715,6 +735,7 @@ __device__ __forceinline__ void pass2(const StepArgs &A, const PState &K, const 
     K.plimrel[i] = sr.limrel;
     K.pvlim[i] = sr.vlim;
     K.pnext1[i] = sr.next1;
+    K.pnl[i] = (uint8_t)(sr.nl1 < 0 ? 0xff : sr.nl1);
     const int nl = sr.choice == 0 ? E.sl0 : E.sl1;
     const int lc = sr.choice == 0 ? -1 : 1;
     K.pfl[i] = (fl & ~(F_LIM | (0xffu << F_NL_SH) | (3u << F_LC_SH))) | (sr.has_lim ? F_LIM : 0u) |
@@ -733,6 +754,7 @@ __device__ __forceinline__ bool pass3(const StepArgs &A, const PState &K, const 
   me.cur = m_cursor(meta);
   me.nxt = C.nxt(i);
   me.nxt2 = C.nxt2(i);
+  me.ends = C.ends(i);
   me.k = -1;
   LEv<float> use;
   use.a = K.pa[i];
@@ -740,6 +762,7 @@ __device__ __forceinline__ bool pass3(const StepArgs &A, const PState &K, const 
   use.limrel = K.plimrel[i];
   use.vlim = K.pvlim[i];
   use.next1 = K.pnext1[i];
+  use.nl1 = K.pnl[i] == 0xff ? -1 : (int)K.pnl[i];
   use.has_lim = (fl & F_LIM) != 0;
   const int new_l = (int)((fl >> F_NL_SH) & 0xffu);
   const int lc = (int)((fl >> F_LC_SH) & 3u) - 1;
@@ -844,7 +867,7 @@ __device__ __forceinline__ void compact(const StepArgs &A, const PState &K, cons
         r.nxt2 = C.nxt2(i);
         r.meta = meta;
         r.wait = C.wait(i);
-        r.pad = 0;
+        r.end_s = C.ends(i);
         put_inbox(dst + rank, r);
         atomicMin(&T.first_out[m_lane(meta)], (rank << 15) | i);
       }
@@ -891,7 +914,7 @@ __device__ __noinline__ void depart(const StepArgs &A, const View &C, TileSh &T,
   rec.nxt2 = rl > 2 ? A.route[off + 2] : -1;
   rec.meta = pack_meta(l, ph.prof, 0);
   rec.wait = 0;
-  rec.pad = 0;
+  rec.end_s = A.end_s[k];
   const int slot = atomicAdd(&A.icnt_out[tile], 1);
   if (slot < T.icap) put_inbox(A.vout + T.ibase + slot, rec);
   else atomicAdd(&T.c_ovf, 1);
@@ -961,7 +984,7 @@ __device__ __forceinline__ void run_tile(const StepArgs &A, StepSmem &M, const H
   unsigned char *slot = M.ring + H.off;
   const int *W = reinterpret_cast<const int *>(slot + L.desc);
   tile_setup(H, W, reinterpret_cast<const ExtFirst *>(W + H.dwd),
-             reinterpret_cast<const PendHead *>(W + H.dwd + 8 * (H.nl - H.nroad)), P, T, lane);
+             reinterpret_cast<const PendHead *>(W + H.dwd + kExtWords * (H.nl - H.nroad)), P, T, lane);
   View C;
   PState K;
   if (!GM) {
@@ -971,7 +994,7 @@ __device__ __forceinline__ void run_tile(const StepArgs &A, StepSmem &M, const H
   } else {
     const size_t o = (size_t)H.base;
     C.st = H.cap + H.icap;
-    C.p = A.scratch + 7 * o;
+    C.p = A.scratch + 8 * o;
     const size_t o2 = o + 4 * (size_t)H.tile;       // 4 slots of slack per tile: 16-B strides
     K = pstate_at(reinterpret_cast<unsigned char *>(A.pscratch + 10 * o2), (C.st + 3) & ~3);
   }
@@ -983,6 +1006,7 @@ __device__ __forceinline__ void run_tile(const StepArgs &A, StepSmem &M, const H
     C.nxt(pos) = x.nxt;
     C.nxt2(pos) = x.nxt2;
     C.wait(pos) = x.wait;
+    C.ends(pos) = x.end_s;
   };
   // ---- merge stayers + sorted inbox into the snapshot (a1) --------------------------
   // stayers (in order, L23 keeps them so) at own index + #inbox keys below;
@@ -1096,9 +1120,13 @@ __device__ __forceinline__ void consumer(const StepArgs &A, StepSmem &M, const P
   TileSh &T = M.T[warp];
   KP_DECL
 #ifndef KS_FREERUN
+#ifndef KS_ROUND_TILES
+#define KS_ROUND_TILES 1
+#endif
   bool done = false;
   for (;;) {
-    if (!done) {
+#pragma unroll 1
+    for (int rt = 0; rt < KS_ROUND_TILES && !done; ++rt) {
       int seq = 0;
       if (lane == 0) seq = atomicAdd(&M.next_seq, 1);
       seq = __shfl_sync(0xffffffffu, seq, 0);
@@ -1109,8 +1137,19 @@ __device__ __forceinline__ void consumer(const StepArgs &A, StepSmem &M, const P
       if (H.done) {
         done = true;
       } else {
+#ifdef KS_PROF
+        const long long t0 = clock64();
+#endif
         if (H.gm) run_tile_gm<EXACT>(A, M, H, T, P, lane);
         else run_tile<EXACT, false>(A, M, H, T, P, lane);
+#ifdef KS_PROF
+        if (lane == 0 && H.tile < 65536) {
+          g_tile_cyc[H.tile][0] = (unsigned)(clock64() - t0);
+          g_tile_cyc[H.tile][1] = (unsigned)(H.n_st + H.n_in);
+          g_tile_cyc[H.tile][2] = (unsigned)T.c_lc + ((unsigned)T.c_hand << 16);
+          g_tile_cyc[H.tile][3] = (unsigned)H.nl;
+        }
+#endif
         KP(10, lane == 0);
         KPN(20, lane == 0, 1);
         if (lane == 0) mbar_arrive(&H.empty);       // the slot can be reused
@@ -1178,6 +1217,17 @@ int step_smem_bytes() { return (int)sizeof(StepSmem); }
 }  // namespace sim
 
 // dev builds (-DKS_PROF): per-phase clock totals of k_step since the last call
+extern "C" int sim_debug_tile_cycles(unsigned int *out) {
+#ifdef KS_PROF
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, sim::g_tile_cyc, sizeof(sim::g_tile_cyc));
+  return 65536;
+#else
+  (void)out;
+  return 0;
+#endif
+}
+
 extern "C" int sim_debug_kstep_prof(unsigned long long *out) {
 #ifdef KS_PROF
   cudaDeviceSynchronize();

@@ -120,10 +120,10 @@ struct TileSh {
   unsigned long long c_delay;
 };
 
-// Snapshot of a batch of tiles at time t (shared memory; the tile's global
-// scratch for a tile larger than a batch): seven word arrays of stride st —
-// the fields other vehicles read (s, v, vid, meta) and the fields only the
-// vehicle itself uses (nxt, nxt2, wait), all merged once per step (a1).
+// Snapshot of a tile at time t (shared memory; the tile's global scratch for
+// a tile in global mode): eight word arrays of stride st — the fields other
+// vehicles read (s, v, vid, meta) and the fields only the vehicle itself uses
+// (nxt, nxt2, wait, end_s), all merged once per step (a1).
 struct View {
   uint32_t *p;
   int st;
@@ -134,6 +134,7 @@ struct View {
   __device__ __forceinline__ int32_t &nxt(int i) const { return reinterpret_cast<int32_t *>(p)[4 * st + i]; }
   __device__ __forceinline__ int32_t &nxt2(int i) const { return reinterpret_cast<int32_t *>(p)[5 * st + i]; }
   __device__ __forceinline__ int32_t &wait(int i) const { return reinterpret_cast<int32_t *>(p)[6 * st + i]; }
+  __device__ __forceinline__ float &ends(int i) const { return reinterpret_cast<float *>(p)[7 * st + i]; }
 };
 
 __device__ __forceinline__ int m_lane(uint32_t m) { return (int)(m & 0xffu); }
@@ -318,11 +319,13 @@ template <typename R> struct LEv {
   R a, gap, vlead, lim, vlim;
   R limrel;                          // lim - s computed without cancellation (fp32 path)
   int leader, hops, next1;
+  int nl1;                           // next1 as a junction lane of this tile (tile-local), else -1
   bool has_leader, phantom, has_lim;
 };
 
 struct Me {                          // the ego vehicle's identity / route cache
   int vid, cur, nxt, nxt2;
+  float ends;                        // end position on the destination road
   int k;                             // index of nxt in the tile's target roads (TileSh::troad)
 };
 
@@ -348,6 +351,7 @@ __device__ __forceinline__ LEv<R> eval_lane(const StepArgs &A, const TileSh &T, 
     ext = l;
   }
   e.next1 = nx.j;
+  e.nl1 = road ? nx.hint : -1;
   const R vmax_l = (R)T.vmax[l];
   const R v0 = (p.vmax < vmax_l) ? p.vmax : vmax_l;
   const R L = (R)T.len[l];
@@ -449,6 +453,8 @@ struct Res {
   float s1, v1, acc;
   int nxt, nxt2;                     // route[c+1], route[c+2] of the snapshot (cursor c)
   int lane_g, cursor;
+  int cl, cx;                        // lane_g as a lane of this tile (local index), else -1; if
+                                     // lane_g is the exit lane of junction lane cx of this tile, cx
   int lc, hand;
   bool fin;
   int wait1;
@@ -466,7 +472,7 @@ __device__ __forceinline__ int upper_bound_s(const View &C, int a, int b, float 
 template <typename R> struct SideRes {
   int choice;                        // -1 stay, 0 left, 1 right
   R a, lim, limrel, vlim;
-  int next1;
+  int next1, nl1;
   bool has_lim, hit;
 };
 
@@ -549,6 +555,7 @@ __device__ __noinline__ SideRes<R> lane_change(const StepArgs &A, const TileSh &
   o.limrel = best.limrel;
   o.vlim = best.vlim;
   o.next1 = best.next1;
+  o.nl1 = best.nl1;
   o.has_lim = best.has_lim;
   o.hit = g.hit;
   return o;
@@ -789,17 +796,26 @@ __device__ __forceinline__ void integrate(const StepArgs &A, const TileSh &T, R 
       else { s1 = use.lim; adv = use.limrel; v1 = (use.vlim < v1) ? use.vlim : v1; }
     }
   }
-  // O9 hand-off and arrival (ledger L26, L31); position = pb + pa
+  // O9 hand-off and arrival (ledger L26, L31); position = pb + pa.
+  // The lanes a vehicle reaches in the common case are resolved from the
+  // tile's own tables: its road lane -> a junction lane of the tile (the
+  // next1 hint) -> that junction lane's exit lane (length, inbox, staged by
+  // k_prep); only a vehicle crossing further reads the global graph.  The
+  // next lane after the exit lane is looked up only when it can matter (the
+  // vehicle reaches the exit lane's end, or is within the guard band of it).
   R pb = M::fp64 ? s1 : s;
   R pa = M::fp64 ? (R)0 : adv;
   int curg = T.glob[new_l], ri = me.cur, n = use.next1, hand = 0;
-  bool croad = T.isroad[new_l];                          // current lane: tile-local until a hand-off
+  int cl = new_l, cx = -1;                              // current lane: local index / via exit of cx
+  int nl = use.nl1;                                     // n as a local junction lane (-1 unknown)
+  bool croad = T.isroad[new_l];
   R Lc = (R)T.len[new_l];
   bool fin = false;
+  constexpr int kUnknown = -100;
   for (;;) {
     const bool dest_road = croad && route_at(A, me.vid, me.cur, me.nxt, me.nxt2, ri + 1) < 0;
     if (dest_road) {
-      const R es = (R)__ldg(A.end_s + me.vid);
+      const R es = (R)me.ends;
       const R rem = M::sub(es, pb);
       if (GUARD && !(adv_zero && hand == 0) &&
           fabsf((float)(pa - rem)) <= kEpsPos * (float)(fabs(pa) + fabs(rem) + (R)1e-3))
@@ -807,23 +823,55 @@ __device__ __forceinline__ void integrate(const StepArgs &A, const TileSh &T, R 
       if (pa >= rem) { fin = true; break; }
     }
     const R rem = M::sub(Lc, pb);
-    if (GUARD && n >= 0 && !(adv_zero && hand == 0) &&
-        fabsf((float)(pa - rem)) <= kEpsPos * (float)(fabs(pa) + fabs(rem) + (R)1e-3))
-      g.hit = true;
+    const bool close = GUARD && !(adv_zero && hand == 0) &&
+                       fabsf((float)(pa - rem)) <= kEpsPos * (float)(fabs(pa) + fabs(rem) + (R)1e-3);
+    if (n == kUnknown && (pa > rem || close)) {           // next lane of a road lane beyond the tile
+      const int R1 = route_at(A, me.vid, me.cur, me.nxt, me.nxt2, ri + 1);
+      const int R2 = route_at(A, me.vid, me.cur, me.nxt, me.nxt2, ri + 2);
+      n = next_from_road_any(A, T, curg, R1, R2);
+      nl = -1;
+    }
+    if (close && n >= 0) g.hit = true;
     if (pa > rem && n >= 0) {
       pb = M::sub(pb, Lc);
-      curg = n;
-      const bool nroad = __ldg(A.lane_road + curg) >= 0;
-      croad = nroad;
-      Lc = (R)__ldg(A.lane_len + curg);
-      if (nroad) ri += 1;
       hand += 1;
-      if (nroad) {
-        int R1 = route_at(A, me.vid, me.cur, me.nxt, me.nxt2, ri + 1);
-        int R2 = route_at(A, me.vid, me.cur, me.nxt, me.nxt2, ri + 2);
-        n = next_from_road_any(A, T, curg, R1, R2);
-      } else {
-        n = __ldg(A.exit_lane + curg);
+      if (cl >= 0 && croad && nl >= 0) {                  // own road lane -> own junction lane
+        curg = n;
+        cl = nl;
+        cx = -1;
+        croad = false;
+        Lc = (R)T.len[nl];
+        n = xl_of(T, nl);
+        nl = -1;
+      } else if (cl >= 0 && !croad) {                    // own junction lane -> its exit lane
+        const ExtFirst &x = T.ext[cl - T.nroad];
+        curg = n;
+        cx = cl;
+        cl = x.dtile == T.tile ? x.dlocal : -1;
+        croad = true;
+        Lc = (R)x.Lb;
+        ri += 1;
+        n = kUnknown;
+      } else {                                            // elsewhere: the global graph
+        curg = n;
+        cx = -1;
+        cl = __ldg(A.lane_tile + curg) == T.tile ? (int)A.lane_local[curg] : -1;
+        croad = __ldg(A.lane_road + curg) >= 0;
+        Lc = (R)__ldg(A.lane_len + curg);
+        if (croad) {
+          ri += 1;
+          n = kUnknown;
+        } else {
+          n = __ldg(A.exit_lane + curg);
+        }
+        nl = -1;
+      }
+      if (cl >= 0 && croad && n == kUnknown) {            // back on a road lane of this tile
+        const int R1 = route_at(A, me.vid, me.cur, me.nxt, me.nxt2, ri + 1);
+        const int R2 = route_at(A, me.vid, me.cur, me.nxt, me.nxt2, ri + 2);
+        const Next nx = R1 < 0 ? Next{kLaneDest, false, -1} : next1_t(A, T, cl, R1, R2);
+        n = nx.j;
+        nl = nx.hint;
       }
       continue;
     }
@@ -838,6 +886,8 @@ __device__ __forceinline__ void integrate(const StepArgs &A, const TileSh &T, R 
   o.acc = (float)a;
   o.lane_g = curg;
   o.cursor = ri;
+  o.cl = cl;
+  o.cx = cx;
   o.lc = lc;
   o.hand = hand;
   o.fin = fin;
@@ -853,6 +903,7 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
   me.cur = m_cursor(meta);
   me.nxt = C.nxt(i);                                     // ego-only fields
   me.nxt2 = C.nxt2(i);
+  me.ends = C.ends(i);
   const int wait0 = C.wait(i);
   const PV<R> p = pvals(T.P[pr], (R)0);
   const R s = (R)C.s(i), v = (R)C.v(i);
@@ -886,6 +937,7 @@ __device__ void veh_update(const StepArgs &A, const TileSh &T, const View &C, in
       use.limrel = sr.limrel;
       use.vlim = sr.vlim;
       use.next1 = sr.next1;
+      use.nl1 = sr.nl1;
       lc = sr.choice == 0 ? -1 : 1;
       new_l = sr.choice == 0 ? E.sl0 : E.sl1;
     }

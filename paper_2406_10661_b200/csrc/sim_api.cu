@@ -362,10 +362,10 @@ void build_desc(sim_s *h) {
     }
     while (w.size() % 4) w.push_back(0);
     // then room for what k_prep stages per step: an ExtFirst per
-    // junction lane and a PendHead per road lane (8 words each), so that the
-    // tile's whole block is one bulk copy
+    // junction lane and a PendHead per road lane, so that the tile's whole
+    // block is one bulk copy
     h->desc_words[T] = (int)w.size();
-    w.insert(w.end(), (size_t)8 * nl, 0);
+    w.insert(w.end(), (size_t)kExtWords * (nl - nroad) + (size_t)8 * nroad, 0);
     h->desc.insert(h->desc.end(), w.begin(), w.end());
     h->desc_off[T + 1] = (int)h->desc.size();
   }
@@ -860,7 +860,7 @@ sim_status upload_state(sim_s *h, const HostState &S) {
       r.nxt2 = route_at(h, k, S.cursor[k] + 2);
       r.meta = pack_meta(h->lane_local[S.lane[k]], h->vprof[k], S.cursor[k]);
       r.wait = S.wait[k];
-      r.pad = 0;
+      r.end_s = h->end_s[k];
       unsigned long long key = ((unsigned long long)*(const uint32_t *)&r.s << 32) | (unsigned)k;
       int l = S.lane[k];
       if (key < summ[l]) summ[l] = key;
@@ -1005,7 +1005,7 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
     CK(h, cudaMemset(P.pubv[b], 0, nv * 4));
   }
   const int64_t sc = h->n_slots;
-  AL(A.scratch, 7 * sc);
+  AL(A.scratch, 8 * sc);
   AL(A.bsort_scratch, sc);
   AL(A.pscratch, 10 * (sc + 4 * (int64_t)nt));
   {

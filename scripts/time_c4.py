@@ -51,6 +51,19 @@ try:
             tot = tot_p if i < 8 else tot_c
             print(f"  {nm:18s} {pb[i]/max(tot,1)*100:5.1f}%  ({pb[i]/1e6:.1f} Mcyc)")
         print(f"  tiles {pb[20]/10:.0f}/step  gmode {pb[21]/10:.0f}")
+        tc = np.zeros(65536 * 4, np.uint32)
+        if L.sim_debug_tile_cycles(tc.ctypes.data_as(ctypes.c_void_p)) > 0:
+            tc = tc.reshape(-1, 4)[:scen.graph["road_lane_offsets"].shape[0] - 1]
+            cyc, nv = tc[:, 0].astype(float), tc[:, 1].astype(float)
+            ok = nv > 0
+            print(f"  tile cycles: mean {cyc[ok].mean():.0f} median {np.median(cyc[ok]):.0f} p90 {np.percentile(cyc[ok], 90):.0f} p99 {np.percentile(cyc[ok], 99):.0f}")
+            per = cyc[ok] / nv[ok]
+            print(f"  cycles/vehicle: mean {per.mean():.0f} median {np.median(per):.0f} p90 {np.percentile(per, 90):.0f} p99 {np.percentile(per, 99):.0f}")
+            lc, hd = (tc[:, 2] & 0xffff)[ok], (tc[:, 2] >> 16)[ok]
+            A_ = np.vstack([nv[ok], lc, hd, tc[ok, 3], np.ones(ok.sum())]).T
+            coef = np.linalg.lstsq(A_, cyc[ok], rcond=None)[0]
+            pred = A_ @ coef
+            print("  fit cycles = %.0f*veh + %.0f*lc + %.0f*handoff + %.0f*lanes + %.0f ; R2 %.2f" % (*coef, 1 - ((cyc[ok]-pred)**2).sum()/((cyc[ok]-cyc[ok].mean())**2).sum()))
 except AttributeError:
     pass
 buf = (ctypes.c_ulonglong * 32)()
