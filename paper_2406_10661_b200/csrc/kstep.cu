@@ -1097,12 +1097,18 @@ __device__ __noinline__ void run_tile_gm(const StepArgs &A, StepSmem &M, const H
   run_tile<EXACT, true>(A, M, H, T, P, lane);
 }
 
-// Named barrier of the consumer warps with a count of the threads whose
-// predicate is true (bar.red.popc).
-__device__ __forceinline__ int cons_bar_count(bool pred) {
+// Named barrier of a group of consumer warps with a count of the threads
+// whose predicate is true (bar.red.popc); barrier id 1 + group.
+#ifndef KS_GROUPS
+#define KS_GROUPS 1
+#endif
+constexpr int kGroups = KS_GROUPS;                  // consumer warp groups with their own rounds
+static_assert(kCW % kGroups == 0, "equal groups");
+constexpr int kGW = kCW / kGroups;                  // warps per group
+__device__ __forceinline__ int cons_bar_count(bool pred, int group) {
   int r;
-  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\tbar.red.popc.u32 %0, 1, %1, p;\n\t}"
-               : "=r"(r) : "r"(kCW * 32), "r"((int)pred) : "memory");
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\tbar.red.popc.u32 %0, %1, %2, p;\n\t}"
+               : "=r"(r) : "r"(1 + group), "r"(kGW * 32), "r"((int)pred) : "memory");
   return r;
 }
 
@@ -1124,7 +1130,15 @@ __device__ __forceinline__ void consumer(const StepArgs &A, StepSmem &M, const P
 #define KS_ROUND_TILES 1
 #endif
   bool done = false;
+#ifdef KS_PROF
+  __shared__ unsigned long long rt_cyc[kCW];
+  __shared__ int rt_n[kCW];
+#endif
   for (;;) {
+#ifdef KS_PROF
+    long long rt0 = clock64();
+    if (lane == 0) { rt_cyc[warp] = 0; rt_n[warp] = 0; }
+#endif
 #pragma unroll 1
     for (int rt = 0; rt < KS_ROUND_TILES && !done; ++rt) {
       int seq = 0;
@@ -1152,12 +1166,35 @@ __device__ __forceinline__ void consumer(const StepArgs &A, StepSmem &M, const P
 #endif
         KP(10, lane == 0);
         KPN(20, lane == 0, 1);
+#ifdef KS_PROF
+        if (lane == 0) { rt_cyc[warp] = (unsigned long long)(clock64() - rt0); rt_n[warp] = H.n_st + H.n_in; }
+#endif
         if (lane == 0) mbar_arrive(&H.empty);       // the slot can be reused
       }
     }
-    const int nd = cons_bar_count(done);
+    const int nd = cons_bar_count(done, warp / kGW);
     KP(11, lane == 0);
-    if (nd == kCW * 32) break;
+#ifdef KS_PROF
+    if (warp == 0 && lane == 0) {
+      unsigned long long mx = 0, sm = 0; int nmx = 0, nmin = 1 << 30, cnt = 0;
+      for (int w = 0; w < kCW; ++w) {
+        if (rt_cyc[w] == 0) continue;
+        cnt++; sm += rt_cyc[w];
+        if (rt_cyc[w] > mx) { mx = rt_cyc[w]; nmx = rt_n[w]; }
+        nmin = min(nmin, rt_n[w]);
+      }
+      if (cnt == kCW) {
+        atomicAdd(&g_ks_prof[12], mx);
+        atomicAdd(&g_ks_prof[13], sm / kCW);
+        atomicAdd(&g_ks_prof[14], 1ull);
+        int nmean = 0; for (int w = 0; w < kCW; ++w) nmean += rt_n[w];
+        atomicAdd(&g_ks_prof[15], (unsigned long long)nmx);
+        atomicAdd(&g_ks_prof[16], (unsigned long long)(nmean / kCW));
+      }
+    }
+    cons_bar_count(false, warp / kGW);
+#endif
+    if (nd == kGW * 32) break;
   }
   return;
 #endif

@@ -51,6 +51,8 @@ try:
             tot = tot_p if i < 8 else tot_c
             print(f"  {nm:18s} {pb[i]/max(tot,1)*100:5.1f}%  ({pb[i]/1e6:.1f} Mcyc)")
         print(f"  tiles {pb[20]/10:.0f}/step  gmode {pb[21]/10:.0f}")
+        if pb[14]:
+            print(f"  rounds {pb[14]}: slowest tile / mean tile = {pb[12]/max(pb[13],1):.2f}; vehicles of the slowest {pb[15]/pb[14]:.0f} vs mean {pb[16]/pb[14]:.0f}")
         tc = np.zeros(65536 * 4, np.uint32)
         if L.sim_debug_tile_cycles(tc.ctypes.data_as(ctypes.c_void_p)) > 0:
             tc = tc.reshape(-1, 4)[:scen.graph["road_lane_offsets"].shape[0] - 1]
