@@ -187,6 +187,10 @@ typedef struct {
   int64_t sum_travel_steps, sum_wait_steps_finished, sum_depart_delay;
   int64_t n_lane_changes, n_handoffs, n_inserted, n_guard_hits;
   double att_finished;               /* sum_travel_steps / n_finished */
+  int64_t sum_time_driving;          /* sum over DRIVING vehicles of (t - insert_time) */
+  double att_all;                    /* ATT over all vehicles (ledger L27): (sum_travel_steps +
+                                        sum_time_driving) / (n_finished + n_driving), trips in
+                                        progress counted with their time so far */
   int32_t *lane_count;               /* optional caller buffer [n_lanes] or NULL */
   int32_t *lane_waiting_at_end;      /* optional [n_lanes]: v < v_wait within queue_zone_m */
   float *road_avg_speed;             /* optional [n_roads]: mean speed of the vehicles on the road's
@@ -308,6 +312,13 @@ sim_status sim_read_group_metrics(sim_handle h, int32_t n_groups, sim_metrics *o
  * rebuilt from status; all fields except lane_signal/lane_offsets/lane_order
  * are required. */
 sim_status sim_load_state(sim_handle h, const sim_state *in);
+/* Test hook of sim_load_state: the DRIVING vehicles with to_inbox[vid] = 1 are
+ * placed, unsorted, in their tile's inbox (as if they had entered the tile or
+ * changed lane in the last step) instead of among its sorted stayers,
+ * so a one-step parity test exercises the step kernel's merge (a1)
+ * with populated inboxes.  to_inbox: host array [n_vehicles] or NULL (=
+ * sim_load_state).  The state itself is the same. */
+sim_status sim_load_state_inbox(sim_handle h, const sim_state *in, const uint8_t *to_inbox);
 /* Device timing (measurement hook): enable = 1 opens a new window
  * in which every sim_step launch is bracketed by CUDA events on the handle's
  * stream (and resets the launch counter); sim_read_timing (synchronising)

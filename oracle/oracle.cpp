@@ -828,10 +828,12 @@ void or_read_decisions(void *h, or_decisions *o) {
 void or_read_metrics(void *h, or_metrics *m) {
   Sim *S = (Sim *)h;
   m->t = S->t;
-  int64_t pend = 0, drv = 0, fin = 0;
+  int64_t pend = 0, drv = 0, fin = 0, tdrv = 0;
   for (auto &v : S->V) {
     pend += v.status == PENDING; drv += v.status == DRIVING; fin += v.status == FINISHED;
+    if (v.status == DRIVING) tdrv += S->t - v.insert_time;   // time so far of a trip in progress
   }
+  m->sum_time_driving = tdrv;
   m->n_pending = pend; m->n_driving = drv; m->n_finished = fin;
   m->vehicle_steps = S->vehicle_steps; m->sum_travel_steps = S->sum_travel;
   m->sum_wait_steps_finished = S->sum_wait_fin; m->sum_depart_delay = S->sum_delay;

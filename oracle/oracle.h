@@ -89,6 +89,7 @@ typedef struct {
   int64_t n_pending, n_driving, n_finished;
   int64_t vehicle_steps, sum_travel_steps, sum_wait_steps_finished;
   int64_t sum_depart_delay, n_lane_changes, n_handoffs, n_inserted;
+  int64_t sum_time_driving;          /* sum over DRIVING vehicles of (t - insert_time) */
 } or_metrics;
 
 /* returns NULL on invalid input, with a message in err */

@@ -118,7 +118,7 @@ class _Metrics(C.Structure):
     _fields_ = [("t", C.c_int32)] + [(n, C.c_int64) for n in (
         "n_pending", "n_driving", "n_finished", "vehicle_steps", "sum_travel_steps",
         "sum_wait_steps_finished", "sum_depart_delay", "n_lane_changes", "n_handoffs",
-        "n_inserted")]
+        "n_inserted", "sum_time_driving")]
 
 
 _GRAPH_DT = dict(lane_length=np.float32, lane_max_speed=np.float32, lane_road=np.int32,
@@ -228,6 +228,10 @@ class Oracle:
         self.lib.or_read_metrics(self.h, C.byref(m))
         out = {n: getattr(m, n) for n, _ in _Metrics._fields_}
         out["att_finished"] = out["sum_travel_steps"] / out["n_finished"] if out["n_finished"] else 0.0
+        # ATT over all vehicles ("the average time taken by all vehicles"; ledger L27):
+        # finished trips' travel times and the time so far of the trips in progress
+        n_all = out["n_finished"] + out["n_driving"]
+        out["att_all"] = (out["sum_travel_steps"] + out["sum_time_driving"]) / n_all if n_all else 0.0
         return out
 
     def lane_stats(self):

@@ -247,12 +247,14 @@ struct SignalArgs {
 void launch_signal(const SignalArgs &a, void *stream);
 void launch_step(const StepArgs &a, void *stream, int smem_bytes);
 void launch_prep(const StepArgs &a, void *stream);
+void launch_lane_order(const StepArgs &a, int32_t *out_vid, uint8_t *out_lane, void *stream);
 int step_smem_bytes();
 void launch_apply_requests(int32_t *request, const int32_t *junc, const int32_t *phase, int m,
                            void *stream);
 void launch_reduce_acc(const long long *tacc, int n_tiles, const int32_t *cnt,
                        const int32_t *icnt, const uint8_t *status, int nv, long long *out,
                        void *stream);
+void launch_sum_insert(const StepArgs &a, long long *out, void *stream);
 void launch_lane_stats(const StepArgs &a, int32_t *lane_count, int32_t *lane_wait,
                        float *road_speed, float queue_zone, void *stream);
 void launch_fill_u64(unsigned long long *p, unsigned long long v, int64_t n, void *stream);
@@ -262,7 +264,7 @@ void launch_scatter_i32(int32_t *dst, const int32_t *idx, const int32_t *val, in
                         void *stream);
 void launch_scatter_f32(float *dst, const int32_t *idx, const float *val, int m, void *stream);
 void launch_gather_u8(const uint8_t *src, const int32_t *idx, uint8_t *out, int m, void *stream);
-void launch_reduce_groups(const long long *tacc, const int32_t *tiles, int n_own,
+void launch_reduce_groups(const long long *tacc, int n_tiles, const int32_t *tiles, int n_own,
                           const int32_t *tile_group, const int32_t *cnt, const int32_t *icnt,
                           int n_groups, long long *out, void *stream);
 void launch_mig_header(MigRec *out_buf, const int32_t *out_off, const int32_t *out_cap,

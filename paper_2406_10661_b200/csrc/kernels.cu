@@ -137,6 +137,8 @@ __global__ void k_reduce_acc(const long long *tacc, int n_tiles, const int32_t *
                              const int32_t *icnt, const uint8_t *status, int nv, long long *out) {
   // out (zeroed by the caller): [0, kNAcc) per-tile counters, kNAcc: driving
   // (stayers + inbox), kNAcc+1 / +2: PENDING / FINISHED vehicles from status
+  // (nv > 0; the library passes 0 and uses kNAcc+1 for the driving vehicles'
+  // insert-time sum, k_sum_insert)
   __shared__ unsigned long long sh[kNAcc + 3];
   if (threadIdx.x < kNAcc + 3) sh[threadIdx.x] = 0;
   __syncthreads();
@@ -164,21 +166,26 @@ __global__ void k_reduce_acc(const long long *tacc, int n_tiles, const int32_t *
     atomicAdd(reinterpret_cast<unsigned long long *>(&out[threadIdx.x]), sh[threadIdx.x]);
 }
 
-// Per-group metrics (batched environments): the counters and driving counts
-// of the own tiles, per group.  out [n_groups][kNAcc + 1] (zeroed by the caller).
-__global__ void k_reduce_groups(const long long *tacc, const int32_t *tiles, int n_own,
+// Per-group metrics (batched environments), per group: the counters of every
+// tile (a tile's rows stay with the partition that accumulated them, also
+// after sim_repartition — as in k_reduce_acc) and the driving counts of the
+// own tiles.  out [n_groups][kNAcc + 1] (zeroed by the caller).
+__global__ void k_reduce_groups(const long long *tacc, int n_tiles, const int32_t *tiles, int n_own,
                                 const int32_t *tile_group, const int32_t *cnt,
                                 const int32_t *icnt, long long *out) {
   const int stride = gridDim.x * blockDim.x;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_own; i += stride) {
-    const int t = tiles[i];
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_tiles; t += stride) {
     long long *o = out + (size_t)tile_group[t] * (kNAcc + 1);
     for (int c = 0; c < kNAcc; ++c) {
       const long long x = tacc[(size_t)t * kNAcc + c];
       if (x) atomicAdd(reinterpret_cast<unsigned long long *>(o + c), (unsigned long long)x);
     }
+  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_own; i += stride) {
+    const int t = tiles[i];
     const int d = cnt[t] + icnt[t];
-    if (d) atomicAdd(reinterpret_cast<unsigned long long *>(o + kNAcc), (unsigned long long)d);
+    if (d) atomicAdd(reinterpret_cast<unsigned long long *>(out + (size_t)tile_group[t] * (kNAcc + 1) + kNAcc),
+                     (unsigned long long)d);
   }
 }
 
@@ -387,8 +394,10 @@ __global__ void k_rehome(StepArgs A, const int32_t *new_owner) {
   if (threadIdx.x == 0) {
     Q.cnt[par][T] = n;
     Q.icnt[par][T] = m;
-    A.cnt_in[T] = 0;
-    A.icnt_in[T] = 0;
+    A.cnt_in[T] = 0;                               // the old owner's counts of T at both parities,
+    A.icnt_in[T] = 0;                              // so no later read sums a stale count of T
+    A.cnt_out[T] = 0;
+    A.icnt_out[T] = 0;
   }
 }
 
@@ -436,18 +445,35 @@ void launch_reduce_acc(const long long *tacc, int n_tiles, const int32_t *cnt,
   k_reduce_acc<<<296, 256, 0, (cudaStream_t)stream>>>(tacc, n_tiles, cnt, icnt, status, nv, out);
 }
 
+// sum of insert_time over the DRIVING vehicles of the own tiles (stayers +
+// inbox) -> *out (added; ATT over all vehicles)
+__global__ void k_sum_insert(const StepArgs A, long long *out) {
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (w >= A.n_own) return;
+  const int T = A.tiles[w];
+  const int n = A.cnt_in[T] + A.icnt_in[T];
+  const InboxRec *rec = tile_recs(A, T, A.cnt_in[T]);
+  long long x = 0;
+  for (int i = lane; i < n; i += 32) x += A.insert_time[rec[i].vid];
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+  if (lane == 0 && x) atomicAdd(reinterpret_cast<unsigned long long *>(out), (unsigned long long)x);
+}
+void launch_sum_insert(const StepArgs &a, long long *out, void *stream) {
+  if (a.n_own > 0) k_sum_insert<<<(a.n_own + 7) / 8, 256, 0, (cudaStream_t)stream>>>(a, out);
+}
+
 void launch_lane_stats(const StepArgs &a, int32_t *lane_count, int32_t *lane_wait,
                        float *road_speed, float zone, void *stream) {
   if (a.n_own > 0)
     k_lane_stats<<<(a.n_own + 3) / 4, 128, 0, (cudaStream_t)stream>>>(a, lane_count, lane_wait, road_speed, zone);
 }
 
-void launch_reduce_groups(const long long *tacc, const int32_t *tiles, int n_own,
+void launch_reduce_groups(const long long *tacc, int n_tiles, const int32_t *tiles, int n_own,
                           const int32_t *tile_group, const int32_t *cnt, const int32_t *icnt,
                           int n_groups, long long *out, void *stream) {
   cudaMemsetAsync(out, 0, (size_t)n_groups * (kNAcc + 1) * sizeof(long long), (cudaStream_t)stream);
-  if (n_own > 0)
-    k_reduce_groups<<<296, 256, 0, (cudaStream_t)stream>>>(tacc, tiles, n_own, tile_group, cnt, icnt, out);
+  k_reduce_groups<<<296, 256, 0, (cudaStream_t)stream>>>(tacc, n_tiles, tiles, n_own, tile_group, cnt,
+                                                         icnt, out);
 }
 
 // set_vehicle_route: every DRIVING vehicle with patch[vid] >= 0

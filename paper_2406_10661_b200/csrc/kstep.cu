@@ -418,6 +418,45 @@ __global__ void __launch_bounds__(128) k_prep(const __grid_constant__ StepArgs A
   }
 }
 
+// ---- per-lane order of the vehicles at t, as the step kernel merges them ---------------
+// (a1): read side of sim_read_state.  One warp per own tile:
+// the same merge as k_step's (stayers at own index + inbox keys below, inbox
+// records at rank + stayers below, key (lane_local, s, vid)), written to
+// vid[tile_base + position] / lane_local[tile_base + position].
+__global__ void k_lane_order(const StepArgs A, int32_t *out_vid, uint8_t *out_lane) {
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (w >= A.n_own) return;
+  const int T = A.tiles[w];
+  const int ns = A.cnt_in[T], ni = A.icnt_in[T], base = A.tile_base[T];
+  const InboxRec *stay = tile_recs(A, T, ns);
+  const InboxRec *inb = stay + ns;
+  for (int i = lane; i < ns; i += 32) {
+    const InboxRec x = stay[i];
+    const unsigned long long h = hikey(m_lane(x.meta), x.s);
+    int below = 0;
+    for (int q = 0; q < ni; ++q) below += key_less(hikey(m_lane(inb[q].meta), inb[q].s), inb[q].vid, h, x.vid);
+    out_vid[base + i + below] = x.vid;
+    out_lane[base + i + below] = (uint8_t)m_lane(x.meta);
+  }
+  for (int r = lane; r < ni; r += 32) {
+    const InboxRec x = inb[r];
+    const unsigned long long h = hikey(m_lane(x.meta), x.s);
+    int rank = 0;
+    for (int q = 0; q < ni; ++q) rank += key_less(hikey(m_lane(inb[q].meta), inb[q].s), inb[q].vid, h, x.vid);
+    int lo = 0, hi = ns;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      const InboxRec &y = stay[mid];
+      if (key_less(hikey(m_lane(y.meta), y.s), y.vid, h, x.vid)) lo = mid + 1; else hi = mid;
+    }
+    out_vid[base + rank + lo] = x.vid;
+    out_lane[base + rank + lo] = (uint8_t)m_lane(x.meta);
+  }
+}
+void launch_lane_order(const StepArgs &a, int32_t *out_vid, uint8_t *out_lane, void *stream) {
+  if (a.n_own > 0) k_lane_order<<<(a.n_own + 7) / 8, 256, 0, (cudaStream_t)stream>>>(a, out_vid, out_lane);
+}
+
 void launch_prep(const StepArgs &a, void *stream) {
   if (a.n_own <= 0) return;
   k_prep<<<(a.n_own + 3) / 4, 128, 0, (cudaStream_t)stream>>>(a);

@@ -50,6 +50,7 @@ struct HostState {                  // vid / junction / lane indexed state
   std::vector<uint8_t> jpol;
   std::vector<int> jphase, jel, jy, jpend, jrem;
   std::vector<uint8_t> dir;
+  std::vector<uint8_t> to_inbox;     // test hook: 1 = place this DRIVING vehicle in its tile's inbox
 };
 
 // ---- minimal NCCL binding (dlopen; only the partitioned NCCL mode needs it) --
@@ -126,6 +127,8 @@ struct Part {
   PeerView *peers_d = nullptr;
   int32_t *tiles_cap_d = nullptr;               // sim_repartition: own-tile list (capacity n_tiles)
   int32_t *xch_d = nullptr;                     // multi-process: host-call exchange, 3 x n_veh
+  int32_t *lo_vid_d = nullptr;                  // sim_read_state lane order (k_lane_order), n_slots
+  uint8_t *lo_lane_d = nullptr;
 };
 
 struct sim_s {
@@ -821,22 +824,26 @@ sim_status push_staging(sim_s *h, const void *src, size_t bytes, void *dst) {
 // Upload a full state (canonical: stayer slabs sorted per lane, empty inboxes)
 // into every partition; each keeps the vehicles of its own tiles, all other
 // state (summaries, cold arrays, signals, queues) is replicated.
+sim_status read_counters(sim_s *h, std::vector<long long> &out);
+sim_status read_group_counters(sim_s *h, std::vector<long long> &c);
+
 sim_status upload_state(sim_s *h, const HostState &S) {
   const int nv = h->nv, nt = h->nt, t = S.t;
   const int par = t & 1;
   h->t = t;
   h->dir = S.dir;
   compute_usable(h);
-  std::vector<std::vector<int>> per_tile(nt);
+  std::vector<std::vector<int>> per_tile(nt), in_tile(nt);
   for (int k = 0; k < nv; ++k)
     if (S.status[k] == ST_DRIVING) {
       int l = S.lane[k];
       if (l < 0 || l >= h->nl) return fail(h, SIM_E_RANGE, "lane out of range for driving vehicle " + std::to_string(k));
-      per_tile[h->lane_tile[l]].push_back(k);
+      if (!S.to_inbox.empty() && S.to_inbox[k]) in_tile[h->lane_tile[l]].push_back(k);
+      else per_tile[h->lane_tile[l]].push_back(k);
     }
   std::vector<InboxRec> rec(h->n_slots);
   std::memset(rec.data(), 0, rec.size() * sizeof(InboxRec));
-  std::vector<int> cnt(nt, 0);
+  std::vector<int> cnt(nt, 0), icnt(nt, 0);
   std::vector<unsigned long long> summ(h->nl, kEmptyKey);
   std::vector<float> pubv(nv, 0.f);
   for (int T = 0; T < nt; ++T) {
@@ -867,6 +874,29 @@ sim_status upload_state(sim_s *h, const HostState &S) {
       pubv[k] = S.v[k];
     }
     cnt[T] = (int)ks.size();
+    // test hook: the rest of the tile's vehicles as unsorted inbox records
+    // (reverse vid order), as if they had entered or changed lane in step t-1
+    auto &ib = in_tile[T];
+    std::sort(ib.rbegin(), ib.rend());
+    if ((int)ib.size() > h->tile_icap[T])
+      return fail(h, SIM_E_CAPACITY, "state exceeds the inbox capacity of road tile " + std::to_string(T));
+    for (size_t i = 0; i < ib.size(); ++i) {
+      const int k = ib[i];
+      InboxRec &r = rec[(size_t)h->tile_ibase[T] + i];
+      r.s = S.s[k] == 0.0f ? 0.0f : S.s[k];
+      r.v = S.v[k];
+      r.vid = k;
+      r.nxt = route_at(h, k, S.cursor[k] + 1);
+      r.nxt2 = route_at(h, k, S.cursor[k] + 2);
+      r.meta = pack_meta(h->lane_local[S.lane[k]], h->vprof[k], S.cursor[k]);
+      r.wait = S.wait[k];
+      r.end_s = h->end_s[k];
+      unsigned long long key = ((unsigned long long)*(const uint32_t *)&r.s << 32) | (unsigned)k;
+      int l = S.lane[k];
+      if (key < summ[l]) summ[l] = key;
+      pubv[k] = S.v[k];
+    }
+    icnt[T] = (int)ib.size();
   }
   std::vector<int> wfin(nv, 0);
   h->fin0 = 0;
@@ -901,15 +931,15 @@ sim_status upload_state(sim_s *h, const HostState &S) {
   }
   for (Part &P : h->parts) {
     cudaStream_t st = h->stream;
-    std::vector<int> pc(nt, 0);
-    for (int T : P.tiles) pc[T] = cnt[T];
+    std::vector<int> pc(nt, 0), pic(nt, 0);
+    for (int T : P.tiles) { pc[T] = cnt[T]; pic[T] = icnt[T]; }
     CK(h, cudaMemcpyAsync(P.usable_d, h->usable.data(), h->nl, cudaMemcpyHostToDevice, st));
     CK(h, cudaMemcpyAsync(P.outroads_d, h->outroads.data(), h->outroads.size() * 4, cudaMemcpyHostToDevice, st));
     CK(h, cudaMemcpyAsync(P.desc_d, h->desc.data(), h->desc.size() * 4, cudaMemcpyHostToDevice, st));
     CK(h, cudaMemcpyAsync(P.inbox[par], rec.data(), rec.size() * sizeof(InboxRec), cudaMemcpyHostToDevice, st));
     CK(h, cudaMemcpyAsync(P.cnt[par], pc.data(), nt * 4, cudaMemcpyHostToDevice, st));
-    CK(h, cudaMemsetAsync(P.icnt[0], 0, nt * 4, st));
-    CK(h, cudaMemsetAsync(P.icnt[1], 0, nt * 4, st));
+    CK(h, cudaMemsetAsync(P.icnt[par ^ 1], 0, nt * 4, st));
+    CK(h, cudaMemcpyAsync(P.icnt[par], pic.data(), nt * 4, cudaMemcpyHostToDevice, st));
     CK(h, cudaMemcpyAsync(P.summ[t % 3], summ.data(), h->nl * 8, cudaMemcpyHostToDevice, st));
     launch_fill_u64(P.summ[(t + 1) % 3], kEmptyKey, h->nl, st);
     launch_fill_u64(P.summ[(t + 2) % 3], kEmptyKey, h->nl, st);
@@ -936,17 +966,23 @@ sim_status upload_state(sim_s *h, const HostState &S) {
     if (P.out_cnt) CK(h, cudaMemsetAsync(P.out_cnt, 0, h->world * 4, st));
   }
   CK(h, cudaStreamSynchronize(h->stream));   // host vectors die at return
-  // counters keep accumulating across loads: remember the finished baseline
+  // counters keep accumulating across loads: remember the finished baseline,
+  // reduced exactly as sim_read_metrics / sim_read_group_metrics reduce them
+  // (all tiles of every partition, summed across processes), so that
+  // n_finished stays the loaded count plus the arrivals since on every rank
   h->acc_fin0 = 0;
   h->grp_fin0.assign(h->n_groups, 0);
   h->grp_acc_fin0.assign(h->n_groups, 0);
   for (int k = 0; k < nv && h->n_groups; ++k) h->grp_fin0[h->veh_group[k]] += S.status[k] == ST_FINISHED;
-  for (Part &P : h->parts) {
-    std::vector<long long> ta((size_t)nt * kNAcc);
-    CK(h, cudaMemcpy(ta.data(), P.A.tacc, ta.size() * 8, cudaMemcpyDeviceToHost));
-    for (int T : P.tiles) {
-      h->acc_fin0 += ta[(size_t)T * kNAcc + ACC_FINISHED];
-      if (h->n_groups) h->grp_acc_fin0[h->road_group[T]] += ta[(size_t)T * kNAcc + ACC_FINISHED];
+  if (!(h->ipc && !h->connected)) {                // (before sim_ipc_connect every counter is 0)
+    std::vector<long long> c;
+    sim_status st = read_counters(h, c);
+    if (st) return st;
+    h->acc_fin0 = c[ACC_FINISHED];
+    if (h->n_groups) {
+      st = read_group_counters(h, c);
+      if (st) return st;
+      for (int g = 0; g < h->n_groups; ++g) h->grp_acc_fin0[g] = c[(size_t)g * (kNAcc + 1) + ACC_FINISHED];
     }
   }
   return SIM_OK;
@@ -1269,7 +1305,8 @@ sim_status read_counters(sim_s *h, std::vector<long long> &out) {
   for (Part &P : h->parts) {
     StepArgs a = step_args(P, h->t);
     launch_reduce_acc(P.A.tacc, h->nt, a.cnt_in, a.icnt_in, P.A.status, 0, P.red_d, h->stream);
-    h->n_launch += 1;
+    launch_sum_insert(a, P.red_d + kNAcc + 1, h->stream);
+    h->n_launch += 2;
   }
   if (h->comm || h->ipc) {
     sim_status st = allreduce_sum(h, 0, 0, 0, kNAcc + 3);
@@ -1285,6 +1322,32 @@ sim_status read_counters(sim_s *h, std::vector<long long> &out) {
   if (out[ACC_OVERFLOW] > 0) {
     h->sticky = SIM_E_CAPACITY;
     return fail(h, SIM_E_CAPACITY, "a road-tile inbox or a migration buffer overflowed its capacity");
+  }
+  return SIM_OK;
+}
+
+// Per-group counters [n_groups][kNAcc + 1], summed over the partitions the
+// same way as read_counters (collective across processes).
+sim_status read_group_counters(sim_s *h, std::vector<long long> &c) {
+  const size_t w = (size_t)h->n_groups * (kNAcc + 1);
+  c.assign(w, 0);
+  std::vector<long long> tmp(w);
+  for (Part &P : h->parts) {
+    StepArgs a = step_args(P, h->t);
+    launch_reduce_groups(P.A.tacc, h->nt, P.A.tiles, P.A.n_own, P.tile_group_d, a.cnt_in, a.icnt_in,
+                         h->n_groups, P.grp_d, h->stream);
+    h->n_launch += 1;
+  }
+  if (h->comm || h->ipc) {
+    sim_status st = allreduce_sum(h, 2, 0, 0, (int64_t)w);
+    if (st) return st;
+  }
+  for (size_t q = 0; q < h->parts.size(); ++q) {
+    CK(h, cudaMemcpyAsync(tmp.data(), h->parts[q].grp_d, w * 8, cudaMemcpyDeviceToHost, h->stream));
+    sim_status st = device_check(h);
+    if (st) return st;
+    for (size_t i = 0; i < w; ++i) c[i] += tmp[i];
+    if (h->comm || h->ipc) break;                     // allreduced: one copy holds the total
   }
   return SIM_OK;
 }
@@ -2183,12 +2246,41 @@ static sim_status read_state_impl(sim_s *h, sim_state *o, bool global) {
   if (o->lane_signal) CK(h, cudaMemcpy(o->lane_signal, P0.A.lane_sig, h->nl, cudaMemcpyDeviceToHost));
   if (o->lane_offsets && o->lane_order) {
     std::vector<std::vector<int>> per(h->nl);
-    for (int k = 0; k < nv; ++k) if (status[k] == ST_DRIVING) per[lane[k]].push_back(k);
+    if (!(global && h->ipc)) {
+      // the order the step kernel itself merges (k_lane_order: stayers in
+      // their record order + the inbox placed by rank), per partition
+      std::vector<int32_t> ov(h->n_slots);
+      std::vector<uint8_t> ol(h->n_slots);
+      for (Part &P : h->parts) {
+        if (!P.lo_vid_d) {
+          sim_status sa = dalloc(h, &P.lo_vid_d, (size_t)h->n_slots);
+          if (!sa) sa = dalloc(h, &P.lo_lane_d, (size_t)h->n_slots);
+          if (sa) return sa;
+        }
+        launch_lane_order(step_args(P, h->t), P.lo_vid_d, P.lo_lane_d, h->stream);
+        h->n_launch += 1;
+        CK(h, cudaMemcpyAsync(ov.data(), P.lo_vid_d, ov.size() * 4, cudaMemcpyDeviceToHost, h->stream));
+        CK(h, cudaMemcpyAsync(ol.data(), P.lo_lane_d, ol.size(), cudaMemcpyDeviceToHost, h->stream));
+        CK(h, cudaStreamSynchronize(h->stream));
+        std::vector<int> cnt(nt), icnt(nt);
+        CK(h, cudaMemcpy(cnt.data(), P.cnt[par], nt * 4, cudaMemcpyDeviceToHost));
+        CK(h, cudaMemcpy(icnt.data(), P.icnt[par], nt * 4, cudaMemcpyDeviceToHost));
+        for (int T : P.tiles)
+          for (int i = 0; i < cnt[T] + icnt[T]; ++i) {
+            const size_t p = (size_t)h->tile_base[T] + i;
+            per[h->tile_lanes[h->tile_lane_off[T] + ol[p]]].push_back(ov[p]);
+          }
+      }
+    } else {
+      // global view across processes: the (s, vid) order of the gathered state
+      for (int k = 0; k < nv; ++k) if (status[k] == ST_DRIVING) per[lane[k]].push_back(k);
+      for (int l = 0; l < h->nl; ++l)
+        std::sort(per[l].begin(), per[l].end(), [&](int a, int b) {
+          return vs[a] != vs[b] ? vs[a] < vs[b] : a < b;
+        });
+    }
     int off = 0;
     for (int l = 0; l < h->nl; ++l) {
-      std::sort(per[l].begin(), per[l].end(), [&](int a, int b) {
-        return vs[a] != vs[b] ? vs[a] < vs[b] : a < b;
-      });
       o->lane_offsets[l] = off;
       for (int k : per[l]) o->lane_order[off++] = k;
     }
@@ -2273,7 +2365,8 @@ sim_status sim_read_metrics(sim_handle h, sim_metrics *m) {
   for (Part &P : h->parts) {
     StepArgs a = step_args(P, h->t);
     launch_reduce_acc(P.A.tacc, h->nt, a.cnt_in, a.icnt_in, P.A.status, 0, P.red_d, h->stream);
-    h->n_launch += 1;
+    launch_sum_insert(a, P.red_d + kNAcc + 1, h->stream);
+    h->n_launch += 2;
   }
   if (h->comm || h->ipc) {
     sim_status st = allreduce_sum(h, 0, 0, 0, kNAcc + 3);
@@ -2337,6 +2430,13 @@ sim_status sim_read_metrics(sim_handle h, sim_metrics *m) {
   m->n_inserted = c[ACC_INSERTED];
   m->n_guard_hits = c[ACC_GUARD];
   m->att_finished = c[ACC_FINISHED] ? (double)c[ACC_SUM_TRAVEL] / (double)c[ACC_FINISHED] : 0.0;
+  // ATT over all vehicles (ledger L27): c[kNAcc + 1] = sum of insert_time
+  // over the DRIVING vehicles (k_sum_insert)
+  m->sum_time_driving = (int64_t)h->t * m->n_driving - c[kNAcc + 1];
+  {
+    const long long n_all = c[ACC_FINISHED] + m->n_driving;
+    m->att_all = n_all ? (double)(c[ACC_SUM_TRAVEL] + m->sum_time_driving) / (double)n_all : 0.0;
+  }
   if (m->lane_count && !lane_direct[0]) std::memcpy(m->lane_count, hl, h->nl * 4);
   if (m->lane_waiting_at_end && !lane_direct[1]) std::memcpy(m->lane_waiting_at_end, hl + h->nl, h->nl * 4);
   if (m->road_avg_speed && !lane_direct[2]) std::memcpy(m->road_avg_speed, hl + 2 * (size_t)h->nl, h->nr * 4);
@@ -2349,25 +2449,9 @@ sim_status sim_read_group_metrics(sim_handle h, int32_t n_groups, sim_metrics *o
   if (!out) return fail(h, SIM_E_INVALID, "out is NULL");
   if (!h->n_groups || n_groups != h->n_groups)
     return fail(h, SIM_E_INVALID, "the handle has no road_group or a different n_groups");
-  const size_t w = (size_t)h->n_groups * (kNAcc + 1);
-  std::vector<long long> c(w, 0), tmp(w);
-  for (Part &P : h->parts) {
-    StepArgs a = step_args(P, h->t);
-    launch_reduce_groups(P.A.tacc, P.A.tiles, P.A.n_own, P.tile_group_d, a.cnt_in, a.icnt_in,
-                         h->n_groups, P.grp_d, h->stream);
-    h->n_launch += 1;
-  }
-  if (h->comm || h->ipc) {
-    st = allreduce_sum(h, 2, 0, 0, (int64_t)w);
-    if (st) return st;
-  }
-  for (size_t q = 0; q < h->parts.size(); ++q) {
-    CK(h, cudaMemcpyAsync(tmp.data(), h->parts[q].grp_d, w * 8, cudaMemcpyDeviceToHost, h->stream));
-    st = device_check(h);
-    if (st) return st;
-    for (size_t i = 0; i < w; ++i) c[i] += tmp[i];
-    if (h->comm || h->ipc) break;                     // allreduced: one copy holds the total
-  }
+  std::vector<long long> c;
+  st = read_group_counters(h, c);
+  if (st) return st;
   for (int g = 0; g < h->n_groups; ++g) {
     const long long *x = c.data() + (size_t)g * (kNAcc + 1);
     sim_metrics &m = out[g];
@@ -2384,6 +2468,8 @@ sim_status sim_read_group_metrics(sim_handle h, int32_t n_groups, sim_metrics *o
     m.n_inserted = x[ACC_INSERTED];
     m.n_guard_hits = x[ACC_GUARD];
     m.att_finished = x[ACC_FINISHED] ? (double)x[ACC_SUM_TRAVEL] / (double)x[ACC_FINISHED] : 0.0;
+    m.sum_time_driving = 0;                         // per-group trips in progress: not reduced
+    m.att_all = 0.0;
   }
   return SIM_OK;
 }
@@ -2419,6 +2505,10 @@ sim_status sim_read_timing(sim_handle h, double *step_ms, double *signal_ms, int
 }
 
 sim_status sim_load_state(sim_handle h, const sim_state *in) {
+  return sim_load_state_inbox(h, in, nullptr);
+}
+
+sim_status sim_load_state_inbox(sim_handle h, const sim_state *in, const uint8_t *to_inbox) {
   sim_status st = check(h);
   if (st) return st;
   if (!in || !in->status || !in->lane || !in->cursor || !in->wait_steps || !in->insert_time ||
@@ -2459,6 +2549,7 @@ sim_status sim_load_state(sim_handle h, const sim_state *in) {
   if (in->junc_remaining) S.jrem.assign(in->junc_remaining, in->junc_remaining + h->nj);
   else S.jrem.assign(h->nj, -1);
   S.dir.assign(in->lane_dir, in->lane_dir + h->nl);
+  if (to_inbox) S.to_inbox.assign(to_inbox, to_inbox + nv);
   return upload_state(h, S);
 }
 

@@ -79,15 +79,17 @@ class sim_metrics(C.Structure):
     _fields_ = [("t", C.c_int32)] + [(n, C.c_int64) for n in (
         "n_pending", "n_driving", "n_finished", "vehicle_steps", "sum_travel_steps",
         "sum_wait_steps_finished", "sum_depart_delay", "n_lane_changes", "n_handoffs",
-        "n_inserted", "n_guard_hits")] + [("att_finished", C.c_double), ("lane_count", P),
-                                          ("lane_waiting_at_end", P), ("road_avg_speed", P)]
+        "n_inserted", "n_guard_hits")] + [("att_finished", C.c_double),
+                                          ("sum_time_driving", C.c_int64), ("att_all", C.c_double),
+                                          ("lane_count", P), ("lane_waiting_at_end", P),
+                                          ("road_avg_speed", P)]
 
 
 ABI_FUNCTIONS = ["sim_create", "sim_get_nccl_unique_id", "sim_ipc_export", "sim_ipc_connect",
                  "sim_repartition", "sim_read_state_global", "sim_partition", "sim_step", "sim_sync", "sim_set_signal_phase",
                  "sim_set_signal_phase_batch", "sim_set_lane_direction",
                  "sim_set_lane_direction_batch", "sim_query_sizes", "sim_read_state",
-                 "sim_read_decisions", "sim_read_metrics", "sim_read_group_metrics", "sim_set_signal_policy", "sim_set_signal_policy_batch", "sim_set_signal_duration", "sim_set_signal_duration_batch", "sim_set_vehicle_route", "sim_set_vehicle_route_batch", "sim_set_lane_max_speed", "sim_set_lane_max_speed_batch", "sim_set_lane_restriction", "sim_set_lane_restriction_batch", "sim_load_state",
+                 "sim_read_decisions", "sim_read_metrics", "sim_read_group_metrics", "sim_set_signal_policy", "sim_set_signal_policy_batch", "sim_set_signal_duration", "sim_set_signal_duration_batch", "sim_set_vehicle_route", "sim_set_vehicle_route_batch", "sim_set_lane_max_speed", "sim_set_lane_max_speed_batch", "sim_set_lane_restriction", "sim_set_lane_restriction_batch", "sim_load_state", "sim_load_state_inbox",
                  "sim_enable_timing", "sim_read_timing", "sim_destroy", "sim_last_error"]
 
 _lib = None
@@ -119,7 +121,7 @@ def load_library(path=LIB):
         "sim_set_vehicle_route_batch": [h, i32, P, P, P, P],
         "sim_set_lane_max_speed": [h, i32, C.c_float], "sim_set_lane_max_speed_batch": [h, i32, P, P],
         "sim_set_lane_restriction": [h, i32, i32], "sim_set_lane_restriction_batch": [h, i32, P, P],
-        "sim_load_state": [h, P], "sim_destroy": [h],
+        "sim_load_state": [h, P], "sim_load_state_inbox": [h, P, P], "sim_destroy": [h],
         "sim_enable_timing": [h, i32], "sim_read_timing": [h, P, P, P],
     }
     for name, args in sig.items():
@@ -351,7 +353,7 @@ class Sim:
             b["lane_order"] = b["lane_order"][:b["lane_offsets"][-1]]
         return b
 
-    def load_state(self, state):
+    def load_state(self, state, to_inbox=None):
         n, nj, nl = self.n, self.n_junctions, self.n_lanes
         conv = dict(status=np.uint8, lane=np.int32, cursor=np.int32, wait_steps=np.int32,
                     insert_time=np.int32, arrive_time=np.int32, s=np.float32, v=np.float32,
@@ -362,7 +364,12 @@ class Sim:
             b["junc_remaining"] = np.ascontiguousarray(state["junc_remaining"], dtype=np.int32)
         st = sim_state(int(state["t"]), *[_ptr(b[nm]) if nm in b else None
                                           for nm, _ in sim_state._fields_[1:]])
-        self._chk(self.lib.sim_load_state(self.h, C.byref(st)))
+        if to_inbox is None:
+            self._chk(self.lib.sim_load_state(self.h, C.byref(st)))
+        else:
+            ti = np.ascontiguousarray(to_inbox, np.uint8)
+            assert ti.shape == (n,)
+            self._chk(self.lib.sim_load_state_inbox(self.h, C.byref(st), _ptr(ti)))
 
     def read_decisions(self):
         n = self.n

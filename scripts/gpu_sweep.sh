@@ -1,4 +1,4 @@
 set -x
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
-timeout 120 python scripts/time_c4.py variants/prof.so > gpurun_out/sweep26.log 2>&1
-cat gpurun_out/sweep26.log
+timeout 1200 python -m pytest tests/test_gpu_merge.py tests/test_gpu_capacity.py tests/test_gpu_partition.py tests/test_gpu_parity.py -x -q -m gpu > gpurun_out/gputests27.log 2>&1
+tail -30 gpurun_out/gputests27.log

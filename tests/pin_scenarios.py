@@ -11,7 +11,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from synth import NetBuilder, Scenario, default_profiles, default_params
+from synth import NetBuilder, Scenario, default_profiles, default_params  # noqa: F401 (re-exported)
 from synth.networks import POLICY_FIXED, POLICY_NONE, TURN_LEFT, TURN_RIGHT, TURN_STRAIGHT
 
 VMAX = 16.667

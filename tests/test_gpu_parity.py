@@ -80,8 +80,9 @@ def test_exact_mode_full_run_bit_identical(simlib, oracle_lib, name):
         mg, mo = gsim.read_metrics(), orc.metrics()
         for k in ("n_finished", "n_driving", "n_pending", "vehicle_steps", "sum_travel_steps",
                   "sum_wait_steps_finished", "sum_depart_delay", "n_lane_changes",
-                  "n_handoffs", "n_inserted"):
+                  "n_handoffs", "n_inserted", "sum_time_driving"):
             assert mg[k] == mo[k], (chunk, k)
+        assert mg["att_all"] == mo["att_all"], chunk
 
 
 def test_full_run_aggregates_c2(simlib, oracle_lib):

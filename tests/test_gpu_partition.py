@@ -158,3 +158,66 @@ def test_full_size_c4_direct_partitions(simlib):
     for k in MKEYS:
         assert m1[k] == mw[k], (k, m1[k], mw[k])
     assert m1["n_handoffs"] > 50_000
+
+
+def test_repartition_metrics_every_step(simlib):
+    """after sim_repartition the old owner must not keep a
+    stale stayer count of a moved tile in its other-parity buffer; reads on
+    odd and even steps after the move equal one partition."""
+    scen = synth.grid(rows=4, cols=4, road_len=250.0, lanes=2, n_trips=3000, seed=12, depart_window=400)
+    world = 3
+    a = simlib.Sim.from_scenario(scen)
+    b = simlib.Sim.from_scenario(scen, world=world, loopback=True, direct=True)
+    nr = len(scen.graph["road_lane_offsets"]) - 1
+    for sim in (a, b):
+        sim.step(41)
+    assert b.repartition((np.arange(nr) * 5 + 1) % world) > 0
+    for k in range(5):
+        for sim in (a, b):
+            sim.step(1)
+        m1, mw = a.read_metrics(), b.read_metrics()
+        for key in MKEYS:
+            assert m1[key] == mw[key], (k, key, m1[key], mw[key])
+
+
+def test_repartition_group_metrics(simlib):
+    """per-group counters (batched environments) keep the rows a
+    tile accumulated before it changed owner."""
+    envs = [synth.grid(rows=3, cols=3, road_len=200.0, lanes=2, n_trips=800, seed=71),
+            synth.grid(rows=3, cols=2, road_len=200.0, lanes=2, n_trips=700, seed=73)]
+    B = synth.batch(envs)
+    a = simlib.Sim.from_scenario(B)
+    b = simlib.Sim.from_scenario(B, world=2, loopback=True, direct=True)
+    nr = len(B.graph["road_lane_offsets"]) - 1
+    for sim in (a, b):
+        sim.step(80)
+    assert b.repartition((np.arange(nr) * 3) % 2) > 0
+    for sim in (a, b):
+        sim.step(57)
+    ga, gb = a.read_group_metrics(len(envs)), b.read_group_metrics(len(envs))
+    for e in range(len(envs)):
+        for key in MKEYS:
+            assert ga[e][key] == gb[e][key], (e, key, ga[e][key], gb[e][key])
+
+
+def test_load_state_after_repartition(simlib):
+    """the finished-count baseline of a load uses the same
+    reduction as the reads (all tiles of all partitions), so n_finished stays
+    right after a load that follows a repartition."""
+    scen = synth.grid(rows=4, cols=4, road_len=250.0, lanes=2, n_trips=3000, seed=12, depart_window=400)
+    a = simlib.Sim.from_scenario(scen)
+    b = simlib.Sim.from_scenario(scen, world=3, loopback=True, direct=True)
+    nr = len(scen.graph["road_lane_offsets"]) - 1
+    for sim in (a, b):
+        sim.step(300)
+    assert b.repartition((np.arange(nr) * 2) % 3) > 0
+    for sim in (a, b):
+        sim.step(101)
+    st = a.read_state()
+    for sim in (a, b):
+        sim.load_state(st)
+        sim.step(33)
+    m1, mw = a.read_metrics(), b.read_metrics()
+    assert m1["n_finished"] > 0
+    for key in ("n_pending", "n_driving", "n_finished"):
+        assert m1[key] == mw[key], (key, m1[key], mw[key])

@@ -183,3 +183,26 @@ def test_two_lane_crossing_in_one_step(oracle_lib):
     assert d["handoffs"][0] == g["expect_handoffs"]
     assert st["lane"][0] == b0 and st["cursor"][0] == g["expect_cursor"]
     assert abs(st["s"][0] - s1) <= 1e-12 * 100
+
+
+# ---- ATT over all vehicles (ledger L27) ---------------------------------------
+def test_att_all_counts_trips_in_progress(oracle_lib):
+    """P:876 'the average time taken by all vehicles': a finished trip counts
+    its travel time, a trip in progress its time so far.  Two unconnected
+    roads: vid 0 drives 1000 m at v0 from t = 0 (travel 60 steps, P-FF of
+    oracle_pins.json); vid 1 departs at t = 0 on a 5000 m road (inserted at
+    t = 1).  At t = 70: ATT_all = (60 + (70 - 1)) / 2."""
+    import json, os
+    ff = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "oracle_pins.json")))["P-FF"]
+    L1, travel = ff["at_speed"][0]
+    b = PS.NetBuilder()
+    A = b.add_road(1, L1, PS.VMAX)
+    B = b.add_road(1, 5000.0, PS.VMAX)
+    rows = [dict(route=[A], lane=b.road_lanes[A][0], s=0.0, v=V0, end_s=L1),
+            dict(route=[B], lane=b.road_lanes[B][0], s=30.0, v=0.0, depart=0, on_net=0, end_s=5000.0)]
+    o = run(oracle_lib, PS.scenario("att", b, rows), 70)
+    m = o.metrics()
+    assert m["n_finished"] == 1 and m["n_driving"] == 1
+    assert m["att_finished"] == travel
+    assert m["sum_time_driving"] == 70 - 1
+    assert m["att_all"] == (travel + (70 - 1)) / 2
