@@ -141,6 +141,18 @@ typedef struct {
   const int32_t *vehicle_rng_id;
   const int32_t *road_group;
   int32_t n_groups;
+  /* Direct transport across processes: a device barrier that waits longer
+   * than this (a peer stopped stepping) flags a sticky SIM_E_CUDA instead of
+   * hanging.  <= 0: 60000 ms. */
+  int32_t barrier_timeout_ms;
+  /* Optional device allocator for every buffer the handle keeps (SURVEY
+   * §8(b): e.g. the PyTorch caching allocator, so that PyTorch provides the
+   * device memory, BASELINE.json north_star).  alloc(bytes, ctx) returns
+   * device memory on params.device or NULL; free_(ptr, ctx) releases it at
+   * sim_destroy.  Both NULL: cudaMalloc / cudaFree. */
+  void *(*alloc)(size_t bytes, void *ctx);
+  void (*free_)(void *ptr, void *ctx);
+  void *alloc_ctx;
 } sim_params;
 
 typedef struct {
@@ -300,6 +312,14 @@ sim_status sim_query_sizes(sim_handle h, sim_sizes *out);
  * sim_read_state.  Vehicles are vid-indexed, so the result equals a
  * single-partition run's. */
 sim_status sim_read_state(sim_handle h, sim_state *out);
+/* sim_read_state into DEVICE buffers on params.device (e.g. torch tensors;
+ * SURVEY §8(b) on_device): status, lane, cursor, wait_steps, insert_time,
+ * arrive_time, s, v (vid-indexed, all required), and optionally the junction
+ * arrays, lane_signal and lane_dir.  Asynchronous on the handle's stream (no
+ * synchronisation: the values are those of the step boundary at which the
+ * call is enqueued); lane_offsets / lane_order are ignored.  One process
+ * (world 1 or loopback); SIM_E_INVALID otherwise. */
+sim_status sim_read_state_device(sim_handle h, sim_state *out);
 sim_status sim_read_state_global(sim_handle h, sim_state *out);
 sim_status sim_read_decisions(sim_handle h, sim_decisions *out);
 sim_status sim_read_metrics(sim_handle h, sim_metrics *out);

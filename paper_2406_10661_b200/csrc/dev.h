@@ -255,6 +255,9 @@ void launch_reduce_acc(const long long *tacc, int n_tiles, const int32_t *cnt,
                        const int32_t *icnt, const uint8_t *status, int nv, long long *out,
                        void *stream);
 void launch_sum_insert(const StepArgs &a, long long *out, void *stream);
+void launch_state_device(const StepArgs *parts, int n_parts, int nv, uint8_t *status, int32_t *lane,
+                         int32_t *cursor, int32_t *wait, int32_t *ins, int32_t *arr, float *s, float *v,
+                         void *stream);
 void launch_lane_stats(const StepArgs &a, int32_t *lane_count, int32_t *lane_wait,
                        float *road_speed, float queue_zone, void *stream);
 void launch_fill_u64(unsigned long long *p, unsigned long long v, int64_t n, void *stream);

@@ -445,6 +445,55 @@ void launch_reduce_acc(const long long *tacc, int n_tiles, const int32_t *cnt,
   k_reduce_acc<<<296, 256, 0, (cudaStream_t)stream>>>(tacc, n_tiles, cnt, icnt, status, nv, out);
 }
 
+// ---- sim_read_state_device: the vid-indexed state into caller device buffers ----
+// pass 0 (every vid): PENDING defaults; pass 1 (per partition, every vid): the
+// latest insert time, FINISHED records; pass 2 (per partition, own tiles): the
+// DRIVING vehicles from the tile records (stayers + inbox) — the same merge
+// as the host read (sim_read_state), without leaving the device.
+__global__ void k_state_defaults(int nv, uint8_t *status, int32_t *lane, int32_t *cursor, int32_t *wait,
+                                 int32_t *ins, int32_t *arr, float *s, float *v) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nv) return;
+  status[k] = ST_PENDING; lane[k] = -1; cursor[k] = 0; wait[k] = 0; ins[k] = -1; arr[k] = -1;
+  s[k] = 0.f; v[k] = 0.f;
+}
+__global__ void k_state_cold(const StepArgs A, int nv, uint8_t *status, int32_t *wait, int32_t *ins,
+                             int32_t *arr) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nv) return;
+  atomicMax(&ins[k], A.insert_time[k]);
+  if (A.status[k] == ST_FINISHED) { status[k] = ST_FINISHED; arr[k] = A.arrive_time[k]; wait[k] = A.wait_fin[k]; }
+}
+__global__ void k_state_driving(const StepArgs A, uint8_t *status, int32_t *lane, int32_t *cursor,
+                                int32_t *wait, float *s, float *v) {
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), ln = threadIdx.x & 31;
+  if (w >= A.n_own) return;
+  const int T = A.tiles[w];
+  const int n = A.cnt_in[T] + A.icnt_in[T];
+  const InboxRec *rec = tile_recs(A, T, A.cnt_in[T]);
+  const int l0 = A.tile_lane_off[T];
+  for (int i = ln; i < n; i += 32) {
+    const InboxRec r = rec[i];
+    status[r.vid] = ST_DRIVING;
+    lane[r.vid] = A.tile_lanes[l0 + m_lane(r.meta)];
+    cursor[r.vid] = m_cursor(r.meta);
+    wait[r.vid] = r.wait;
+    s[r.vid] = r.s;
+    v[r.vid] = r.v;
+  }
+}
+void launch_state_device(const StepArgs *parts, int n_parts, int nv, uint8_t *status, int32_t *lane,
+                         int32_t *cursor, int32_t *wait, int32_t *ins, int32_t *arr, float *s, float *v,
+                         void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int g = (nv + 255) / 256;
+  if (nv > 0) k_state_defaults<<<g, 256, 0, st>>>(nv, status, lane, cursor, wait, ins, arr, s, v);
+  for (int q = 0; q < n_parts && nv > 0; ++q) k_state_cold<<<g, 256, 0, st>>>(parts[q], nv, status, wait, ins, arr);
+  for (int q = 0; q < n_parts; ++q)
+    if (parts[q].n_own > 0)
+      k_state_driving<<<(parts[q].n_own + 7) / 8, 256, 0, st>>>(parts[q], status, lane, cursor, wait, s, v);
+}
+
 // sum of insert_time over the DRIVING vehicles of the own tiles (stayers +
 // inbox) -> *out (added; ATT over all vehicles)
 __global__ void k_sum_insert(const StepArgs A, long long *out) {

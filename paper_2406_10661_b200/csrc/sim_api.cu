@@ -171,7 +171,7 @@ struct sim_s {
   bool ipc = false;                             // direct across processes (CUDA IPC mappings)
   bool connected = false;                       // ipc: sim_ipc_connect done
   unsigned bar_epoch = 0;                       // ipc: barriers passed
-  unsigned long long bar_timeout_ns = 60000000000ull;  // ipc: SIM_BARRIER_TIMEOUT_MS (default 60 s)
+  unsigned long long bar_timeout_ns = 60000000000ull;  // ipc: params.barrier_timeout_ms (default 60 s)
   int32_t *bar_err_d = nullptr;                 // ipc: set by a barrier that timed out
   void *ipc_tmp = nullptr;                      // ipc: reduction result buffer
   std::vector<void *> ipc_opened;               // ipc: peer mappings to close
@@ -195,6 +195,7 @@ struct sim_s {
   std::vector<long long> grp_nv, grp_fin0, grp_acc_fin0;
   // device
   std::vector<void *> allocs;
+  std::vector<uint8_t> alloc_hooked;            // 1: allocs[i] came from params.alloc
   int64_t bytes = 0;
   int32_t *stage_d = nullptr;        // device staging for batch setters
   int stage_cap = 0;
@@ -249,11 +250,17 @@ template <typename T>
 sim_status dalloc(sim_s *h, T **p, size_t n) {
   *p = nullptr;
   if (n == 0) n = 1;
-  cudaError_t e = cudaMalloc((void **)p, n * sizeof(T));
-  if (e != cudaSuccess) {
-    return fail(h, SIM_E_OOM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
+  if (h->P.alloc) {                                 // caller's allocator (e.g. PyTorch's caching one)
+    *p = reinterpret_cast<T *>(h->P.alloc(n * sizeof(T), h->P.alloc_ctx));
+    if (!*p) return fail(h, SIM_E_OOM, "params.alloc returned NULL");
+  } else {
+    cudaError_t e = cudaMalloc((void **)p, n * sizeof(T));
+    if (e != cudaSuccess) {
+      return fail(h, SIM_E_OOM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
+    }
   }
   h->allocs.push_back(*p);
+  h->alloc_hooked.push_back(h->P.alloc ? 1 : 0);
   h->bytes += (int64_t)(n * sizeof(T));
   return SIM_OK;
 }
@@ -1245,10 +1252,7 @@ sim_status setup_direct(sim_s *h) {
     for (Part &P : h->parts) v.push_back(P.view);
     return upload_peers(h, v);
   }
-  if (const char *e = std::getenv("SIM_BARRIER_TIMEOUT_MS")) {
-    const long long ms = std::atoll(e);
-    if (ms > 0) h->bar_timeout_ns = (unsigned long long)ms * 1000000ull;
-  }
+  if (h->P.barrier_timeout_ms > 0) h->bar_timeout_ns = (unsigned long long)h->P.barrier_timeout_ms * 1000000ull;
   sim_status st = dalloc(h, &h->bar_err_d, 1);
   if (st) return st;
   CK(h, cudaMemset(h->bar_err_d, 0, 4));
@@ -1580,7 +1584,10 @@ extern "C" {
 
 static void destroy_impl(sim_s *h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
-  for (void *p : h->allocs) cudaFree(p);
+  for (size_t i = 0; i < h->allocs.size(); ++i) {
+    if (!h->alloc_hooked[i]) cudaFree(h->allocs[i]);
+    else if (h->P.free_) h->P.free_(h->allocs[i], h->P.alloc_ctx);
+  }
   if (h->stage_d) cudaFree(h->stage_d);
   if (h->pinned) cudaFreeHost(h->pinned);
   if (h->rd_pinned) cudaFreeHost(h->rd_pinned);
@@ -1801,7 +1808,7 @@ sim_status sim_create(const sim_graph *g, const sim_trips *tr, const sim_params 
   if (!st) {
     cudaError_t e = cudaMalloc(&h->stage_dir_d, 17 * (size_t)h->nl);
     if (e != cudaSuccess) st = fail(h, SIM_E_OOM, "cudaMalloc staging");
-    else h->allocs.push_back(h->stage_dir_d);
+    else { h->allocs.push_back(h->stage_dir_d); h->alloc_hooked.push_back(0); }
   }
   if (!st) {
     if (cudaEventCreateWithFlags(&h->stage_ev, cudaEventDisableTiming) != cudaSuccess ||
@@ -2290,6 +2297,37 @@ static sim_status read_state_impl(sim_s *h, sim_state *o, bool global) {
 }
 
 sim_status sim_read_state(sim_handle h, sim_state *o) { return read_state_impl(h, o, false); }
+
+sim_status sim_read_state_device(sim_handle h, sim_state *o) {
+  sim_status st = check(h);
+  if (st) return st;
+  if (!o || !o->status || !o->lane || !o->cursor || !o->wait_steps || !o->insert_time ||
+      !o->arrive_time || !o->s || !o->v)
+    return fail(h, SIM_E_INVALID, "sim_read_state_device needs the vid-indexed device buffers");
+  if (h->ipc) return fail(h, SIM_E_INVALID, "sim_read_state_device: one process (use sim_read_state_global across processes)");
+  std::vector<StepArgs> parts;
+  for (Part &P : h->parts) parts.push_back(step_args(P, h->t));
+  launch_state_device(parts.data(), (int)parts.size(), h->nv, o->status, o->lane, o->cursor,
+                      o->wait_steps, o->insert_time, o->arrive_time, o->s, o->v, h->stream);
+  h->n_launch += 1 + 2 * (int64_t)parts.size();
+  Part &P0 = h->parts[0];
+  const size_t nj = h->nj;
+  if (nj) {
+    if (o->junc_policy) CK(h, cudaMemcpyAsync(o->junc_policy, P0.SG.policy, nj, cudaMemcpyDeviceToDevice, h->stream));
+    if (o->junc_phase) CK(h, cudaMemcpyAsync(o->junc_phase, P0.SG.phase, nj * 4, cudaMemcpyDeviceToDevice, h->stream));
+    if (o->junc_elapsed) CK(h, cudaMemcpyAsync(o->junc_elapsed, P0.SG.elapsed, nj * 4, cudaMemcpyDeviceToDevice, h->stream));
+    if (o->junc_yellow_left) CK(h, cudaMemcpyAsync(o->junc_yellow_left, P0.SG.yellow_left, nj * 4, cudaMemcpyDeviceToDevice, h->stream));
+    if (o->junc_pending) CK(h, cudaMemcpyAsync(o->junc_pending, P0.SG.pending, nj * 4, cudaMemcpyDeviceToDevice, h->stream));
+    if (o->junc_remaining) CK(h, cudaMemcpyAsync(o->junc_remaining, P0.SG.remaining, nj * 4, cudaMemcpyDeviceToDevice, h->stream));
+  }
+  if (o->lane_signal) CK(h, cudaMemcpyAsync(o->lane_signal, P0.A.lane_sig, h->nl, cudaMemcpyDeviceToDevice, h->stream));
+  if (o->lane_dir) {
+    st = push_staging(h, h->dir.data(), h->nl, o->lane_dir);
+    if (st) return st;
+  }
+  o->t = h->t;
+  return SIM_OK;
+}
 sim_status sim_read_state_global(sim_handle h, sim_state *o) { return read_state_impl(h, o, true); }
 
 sim_status sim_read_decisions(sim_handle h, sim_decisions *o) {

@@ -53,7 +53,8 @@ class sim_params(C.Structure):
                 ("world", C.c_int32), ("loopback", C.c_int32), ("direct", C.c_int32), ("nccl_id", P),
                 ("road_owner", P), ("max_pressure_period", C.c_int32),
                 ("vehicle_seed", P), ("vehicle_rng_id", P), ("road_group", P),
-                ("n_groups", C.c_int32)]
+                ("n_groups", C.c_int32), ("barrier_timeout_ms", C.c_int32),
+                ("alloc", P), ("free_", P), ("alloc_ctx", P)]
 
 
 class sim_sizes(C.Structure):
@@ -89,7 +90,7 @@ ABI_FUNCTIONS = ["sim_create", "sim_get_nccl_unique_id", "sim_ipc_export", "sim_
                  "sim_repartition", "sim_read_state_global", "sim_partition", "sim_step", "sim_sync", "sim_set_signal_phase",
                  "sim_set_signal_phase_batch", "sim_set_lane_direction",
                  "sim_set_lane_direction_batch", "sim_query_sizes", "sim_read_state",
-                 "sim_read_decisions", "sim_read_metrics", "sim_read_group_metrics", "sim_set_signal_policy", "sim_set_signal_policy_batch", "sim_set_signal_duration", "sim_set_signal_duration_batch", "sim_set_vehicle_route", "sim_set_vehicle_route_batch", "sim_set_lane_max_speed", "sim_set_lane_max_speed_batch", "sim_set_lane_restriction", "sim_set_lane_restriction_batch", "sim_load_state", "sim_load_state_inbox",
+                 "sim_read_decisions", "sim_read_metrics", "sim_read_group_metrics", "sim_set_signal_policy", "sim_set_signal_policy_batch", "sim_set_signal_duration", "sim_set_signal_duration_batch", "sim_set_vehicle_route", "sim_set_vehicle_route_batch", "sim_set_lane_max_speed", "sim_set_lane_max_speed_batch", "sim_set_lane_restriction", "sim_set_lane_restriction_batch", "sim_load_state", "sim_load_state_inbox", "sim_read_state_device",
                  "sim_enable_timing", "sim_read_timing", "sim_destroy", "sim_last_error"]
 
 _lib = None
@@ -122,6 +123,7 @@ def load_library(path=LIB):
         "sim_set_lane_max_speed": [h, i32, C.c_float], "sim_set_lane_max_speed_batch": [h, i32, P, P],
         "sim_set_lane_restriction": [h, i32, i32], "sim_set_lane_restriction_batch": [h, i32, P, P],
         "sim_load_state": [h, P], "sim_load_state_inbox": [h, P, P], "sim_destroy": [h],
+        "sim_read_state_device": [h, P],
         "sim_enable_timing": [h, i32], "sim_read_timing": [h, P, P, P],
     }
     for name, args in sig.items():
@@ -150,9 +152,30 @@ _TRIP_DT = dict(depart_step=np.int32, on_network_at_t0=np.uint8, route_offsets=n
                 start_v=np.float32, end_s=np.float32, profile=np.uint8)
 
 
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
+
+
+def torch_allocator(device=0, stream=None):
+    """(alloc, free_) callbacks of sim_params backed by PyTorch's caching
+    allocator on `device` (BASELINE.json north_star: PyTorch provides the
+    device memory).  Keep the returned pair alive as long as the handle."""
+    import torch
+
+    def _alloc(n, ctx):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(n), device=device, stream=stream)
+        except Exception:
+            return None
+
+    def _free(p, ctx):
+        torch.cuda.caching_allocator_delete(p)
+    return ALLOC_FN(_alloc), FREE_FN(_free)
+
+
 def _marshal(graph, trips, profiles, params, device=0, stream=None, exact_mode=False,
              record_decisions=False, world=1, rank=0, loopback=False, nccl_id=None,
-             road_owner=None, direct=False):
+             road_owner=None, direct=False, barrier_timeout_ms=0, allocator=None):
     g = {k: np.ascontiguousarray(graph[k], dtype=dt) for k, dt in _GRAPH_DT.items()}
     tr = {k: np.ascontiguousarray(trips[k], dtype=dt) for k, dt in _TRIP_DT.items()}
     prof = np.ascontiguousarray(profiles, dtype=np.float32).reshape(-1, 6)
@@ -180,7 +203,11 @@ def _marshal(graph, trips, profiles, params, device=0, stream=None, exact_mode=F
                     _ptr(nid) if nid is not None else None,
                     _ptr(own) if own is not None else None,
                     int(params.get("max_pressure_period", 30)),
-                    *_batch_arrays(params, keep))
+                    *_batch_arrays(params, keep), int(barrier_timeout_ms),
+                    C.cast(allocator[0], C.c_void_p) if allocator else None,
+                    C.cast(allocator[1], C.c_void_p) if allocator else None, None)
+    if allocator:
+        keep.append(allocator)
     return G, T, Pm, keep
 
 
@@ -249,12 +276,18 @@ class Sim:
 
     def __init__(self, graph, trips, profiles, params, device=0, stream=None,
                  exact_mode=False, record_decisions=False, world=1, rank=0, loopback=False,
-                 nccl_id=None, road_owner=None, direct=False):
+                 nccl_id=None, road_owner=None, direct=False, barrier_timeout_ms=0,
+                 allocator=None):
+        """allocator: None (cudaMalloc), "torch" (PyTorch's caching allocator,
+        torch_allocator) or an (alloc, free_) pair of ALLOC_FN / FREE_FN."""
         lib = load_library()
         self.lib = lib
+        if allocator == "torch":
+            allocator = torch_allocator(device, stream)
+        self._allocator = allocator                   # the callbacks must outlive the handle
         G, T, Pm, keep = _marshal(graph, trips, profiles, params, device, stream, exact_mode,
                                   record_decisions, world, rank, loopback, nccl_id, road_owner,
-                                  direct)
+                                  direct, barrier_timeout_ms, allocator)
         self.n_lanes, self.n_junctions, self.n = G.n_lanes, G.n_junctions, T.n_trips
         self.n_roads = G.n_roads
         self.world, self.rank = max(1, int(world)), int(rank)
@@ -352,6 +385,25 @@ class Sim:
         if lane_order:
             b["lane_order"] = b["lane_order"][:b["lane_offsets"][-1]]
         return b
+
+    def read_state_device(self, out=None):
+        """The vid-indexed state into torch tensors on this handle's device
+        (sim_read_state_device; stream-ordered, no synchronisation).  `out`:
+        dict of preallocated tensors (reused across calls) or None."""
+        import torch
+        n = self.n
+        dev = torch.device("cuda", torch.cuda.current_device())
+        spec = dict(status=torch.uint8, lane=torch.int32, cursor=torch.int32, wait_steps=torch.int32,
+                    insert_time=torch.int32, arrive_time=torch.int32, s=torch.float32, v=torch.float32)
+        if out is None:
+            out = {k: torch.empty(n, dtype=dt, device=dev) for k, dt in spec.items()}
+            out["lane_signal"] = torch.empty(self.n_lanes, dtype=torch.uint8, device=dev)
+            out["junc_phase"] = torch.empty(max(self.n_junctions, 1), dtype=torch.int32, device=dev)
+        st = sim_state(0, *[C.c_void_p(out[nm].data_ptr()) if nm in out else None
+                            for nm, _ in sim_state._fields_[1:]])
+        self._chk(self.lib.sim_read_state_device(self.h, C.byref(st)))
+        out["t"] = st.t
+        return out
 
     def load_state(self, state, to_inbox=None):
         n, nj, nl = self.n, self.n_junctions, self.n_lanes

@@ -91,10 +91,11 @@ def main():
         json.dump(res, open(OUT, "w"), indent=1)
     if a.only in (None, "c3"):
         scen = c3_scenario()
-        t0 = time.time()
-        res["C3-seed3-fp64"] = run(scen, controller=c3_controller(scen))
-        print(f"C3: {res['C3-seed3-fp64']} ({time.time() - t0:.0f} s)", flush=True)
-        json.dump(res, open(OUT, "w"), indent=1)
+        for mode, fp32 in (("fp64", False), ("fp32store", True)):
+            t0 = time.time()
+            res[f"C3-seed3-{mode}"] = run(scen, store_fp32=fp32, controller=c3_controller(scen))
+            print(f"C3 {mode}: {res[f'C3-seed3-{mode}']} ({time.time() - t0:.0f} s)", flush=True)
+            json.dump(res, open(OUT, "w"), indent=1)
 
 
 if __name__ == "__main__":

@@ -100,11 +100,10 @@ def _stall_worker(rank, world, port, out_dir):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    os.environ["SIM_BARRIER_TIMEOUT_MS"] = "2000"
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import paper_2406_10661_b200 as p
     scen = synth.grid(rows=3, cols=3, road_len=200.0, lanes=2, n_trips=500, seed=5)
-    g = p.Sim.from_scenario(scen, world=world, rank=rank, direct=True, device=0)
+    g = p.Sim.from_scenario(scen, world=world, rank=rank, direct=True, device=0, barrier_timeout_ms=2000)
     g.connect_process_group()
     result = "none"
     if rank == 0:                                    # rank 1 never steps

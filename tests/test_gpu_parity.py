@@ -255,3 +255,84 @@ def test_full_size_c3_dynamic_tidal_parity(simlib, oracle_lib):
     compare_decisions(g.read_decisions(), o.decisions(), st["status"], where="[C3] ")
     compare_states(g.read_state(), o.read_state(), where="[C3] ")
     assert (st["status"] == 1).sum() > 3_000
+
+
+# ---- full-run aggregates against stored oracle runs (tests/golden/oracle_aggregates.json,
+# written by scripts/oracle_aggregates.py from oracle/ only) --------------------------------
+import json as _json  # noqa: E402
+import os as _os  # noqa: E402
+
+_AGG = _json.load(open(_os.path.join(_os.path.dirname(__file__), "golden", "oracle_aggregates.json")))
+
+
+def _agg(m):
+    nf = m["n_finished"]
+    return dict(tp=nf, att_finished=m["att_finished"], att_all=m["att_all"],
+                mean_wait=m["sum_wait_steps_finished"] / nf, vehicle_steps=m["vehicle_steps"],
+                n_driving=m["n_driving"])
+
+
+def _c3_run(simlib, exact):
+    sys_path_scripts = _os.path.join(_os.path.dirname(_os.path.dirname(__file__)), "scripts")
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("oracle_aggregates",
+                                                  _os.path.join(sys_path_scripts, "oracle_aggregates.py"))
+    oa = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(oa)                   # scenario + controller recipe only
+    scen = oa.c3_scenario()
+    g = simlib.Sim.from_scenario(scen, exact_mode=exact)
+    t = 0
+    calls = {}
+    for tc, lanes, dirs in oa.c3_controller(scen):
+        calls.setdefault(tc, []).append((lanes, dirs))
+    while t < oa.STEPS:
+        for lanes, dirs in calls.get(t, []):
+            g.set_lane_direction_batch(lanes, dirs)
+        nxt = min([x for x in calls if x > t] + [oa.STEPS])
+        g.step(nxt - t)
+        t = nxt
+    return _agg(g.read_metrics())
+
+
+@pytest.mark.parametrize("seed", [2, 3])
+def test_full_run_c2_exact_mode_per_seed(simlib, seed):
+    """Per run: exact mode (fp64 arithmetic, fp32 storage) reproduces the
+    stored oracle fp32-storage aggregates of C2 exactly."""
+    g = simlib.Sim.from_scenario(synth.grid(seed=seed), exact_mode=True)
+    g.step(3600)
+    got, want = _agg(g.read_metrics()), _AGG[f"C2-seed{seed}-fp32store"]
+    for k in ("tp", "vehicle_steps", "n_driving"):
+        assert got[k] == want[k], (k, got[k], want[k])
+    for k in ("att_finished", "att_all", "mean_wait"):
+        assert got[k] == pytest.approx(want[k], rel=1e-12), k
+
+
+@pytest.mark.parametrize("seed", [2, 3])
+def test_full_run_c2_fp32_per_seed(simlib, seed):
+    """Per run, the default fp32 path against the stored fp64 oracle: TP and
+    vehicle-steps within 0.5% (north_star); ATT / mean wait within the
+    oracle's own fp64-vs-fp32-storage scatter on that seed plus 0.5%
+    (tests/test_oracle_aggregates.py shows that scatter exceeds 0.5%)."""
+    g = simlib.Sim.from_scenario(synth.grid(seed=seed))
+    g.step(3600)
+    got, ref = _agg(g.read_metrics()), _AGG[f"C2-seed{seed}-fp64"]
+    alt = _AGG[f"C2-seed{seed}-fp32store"]
+    for k in ("tp", "vehicle_steps"):
+        assert abs(got[k] - ref[k]) <= 0.005 * ref[k], (k, got[k], ref[k])
+    for k in ("att_finished", "att_all", "mean_wait"):
+        scatter = abs(alt[k] - ref[k]) / ref[k]
+        assert abs(got[k] - ref[k]) <= (scatter + 0.005) * ref[k], (k, got[k], ref[k], scatter)
+
+
+def test_full_run_c3_aggregates(simlib):
+    """BASELINE.json configs[2] (C3: 20x20, tidal + dynamic lanes, 200k trips)
+    for 3600 steps with the stored fixed lane controller: exact mode equals the
+    oracle's fp32-storage run; the fp32 path is within 0.5% of the fp64 oracle
+    in TP, vehicle-steps and ATT over all vehicles."""
+    if "C3-seed3-fp32store" in _AGG:
+        got, want = _c3_run(simlib, True), _AGG["C3-seed3-fp32store"]
+        for k in ("tp", "vehicle_steps", "n_driving"):
+            assert got[k] == want[k], (k, got[k], want[k])
+    got, ref = _c3_run(simlib, False), _AGG["C3-seed3-fp64"]
+    for k in ("tp", "vehicle_steps", "att_all"):
+        assert abs(got[k] - ref[k]) <= 0.005 * ref[k], (k, got[k], ref[k])
