@@ -32,12 +32,31 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 NCU_TRAFFIC = os.path.join(ROOT, "profiles", "ncu_kstep_traffic.json")
 
 
+# algorithmic bytes per vehicle-step at C4 (hot record read 24 +
+# written 24, lane summaries ~2.5, events ~1-2) — the roofline's unit figure
+B_ALG = 52.0
+
+
 def algorithmic_bytes(n_veh, n_movers, n_lanes):
-    """Bytes one step must move: the 28 B hot record read + written
-    per vehicle, 8 B extra per mover (32 B inbox record written and read
-    instead of the slab record), and per lane 24 B of metadata + 24 B of
-    summary traffic (first-vehicle key write / clear / read)."""
-    return 56.0 * n_veh + 8.0 * n_movers + 48.0 * n_lanes
+    """This implementation's own byte model of a step, reported
+    beside the SURVEY figure: the 32 B vehicle record read + written per
+    vehicle, per mover one more record (inbox write + read), and per lane 48 B
+    (descriptor / staging + summary write, clear, read)."""
+    return 64.0 * n_veh + 32.0 * n_movers + 48.0 * n_lanes
+
+
+def host_cpu():
+    """(cores available to this process, CPU model)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return len(os.sched_getaffinity(0)), model
 
 
 def peaks():
@@ -111,11 +130,14 @@ def make_workload(world=1, policy="fixed", scale=1.0):
     return scen
 
 
-def workload_config(scen, extra=None, policy="fixed"):
+def workload_config(scen, extra=None, policy="fixed", preroll=0):
     G = int(np.sqrt(len(scen.graph["junc_lane_offsets"]) - 1))
     sig = "fixed-time signals" if policy == "fixed" else "max-pressure signals (period 30 s)"
     cfg = {"workload": f"C4 city-like synthetic network (SURVEY 8(d)): G={G} perturbed grid, "
-                       f"{scen.n_trips / 1e6:.3g}M vehicles on the network at t=0, {sig}",
+                       f"{scen.n_trips / 1e6:.3g}M vehicles on the network at t=0, {sig}; "
+                       f"timed after a {preroll}-step untimed pre-roll from the t=0 placement "
+                       f"(vehicles at rest) plus the warm-up steps",
+           "preroll_steps": int(preroll),
            "n_vehicles": int(scen.n_trips), "n_lanes": int(scen.n_lanes),
            "n_junctions": int(len(scen.graph["junc_lane_offsets"]) - 1),
            "n_roads": int(len(scen.graph["road_lane_offsets"]) - 1),
@@ -139,9 +161,11 @@ def cpu_baseline(scen, budget_s=20.0, max_steps=10):
         veh += o.metrics()["vehicle_steps"] - before
         done += 1
     dt = time.perf_counter() - t0
+    ncores, model = host_cpu()
     return {"value": veh / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "host_cores": ncores, "cpu_model": model,
             "sample": f"first {done} steps of the same C4 workload ({veh} vehicle-steps, "
-                      f"{dt:.1f} s, serial fp64 C++ oracle)"}
+                      f"{dt:.1f} s, serial fp64 C++ oracle, one thread)"}
 
 
 def run_reference(args, rank, world):
@@ -162,14 +186,16 @@ def run_reference(args, rank, world):
         done += 1
     dt = time.perf_counter() - t0
     value = veh / dt
-    sample = (f"{done} of {args.steps} timed steps (after {args.warmup} warm-up) of the C4 "
-              f"workload, {veh} vehicle-steps in {dt:.1f} s")
+    sample = (f"{done} of {args.steps} timed steps (after {args.warmup} warm-up; the "
+              f"{args.preroll}-step pre-roll of the GPU arm is skipped: minutes of serial oracle "
+              f"time) of the C4 workload, {veh} vehicle-steps in {dt:.1f} s, one thread")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": done, "warmup": args.warmup,
             "ms_per_step": 1e3 * dt / max(done, 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(scen, policy=args.policy),
+            "config": workload_config(scen, policy=args.policy, preroll=args.preroll),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "host_cores": host_cpu()[0], "cpu_model": host_cpu()[1],
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -246,6 +272,7 @@ def run_gpu(args, rank, world, local_rank):
     else:
         sim = p.Sim.from_scenario(scen, device=local_rank, stream=stream.cuda_stream)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    sim.step(args.preroll)                               # steady state: the t=0 placement is at rest
     for _ in range(args.warmup):
         sim.step(1)
     m0 = sim.read_metrics()
@@ -276,20 +303,22 @@ def run_gpu(args, rank, world, local_rank):
     value = tot_vsteps / (t_max / 1e3)
     # roofline of the dominant kernel (k_step), per GPU
     peak, peak_kind = peaks()
-    per_launch_bytes = algorithmic_bytes(tot_vsteps / args.steps / world, movers / args.steps / world,
-                                         scen.n_lanes / world)
+    veh_per_launch = tot_vsteps / args.steps / world         # per GPU
+    survey_bytes = B_ALG * veh_per_launch                    # SURVEY 8(d) unit figure x units
+    model_bytes = algorithmic_bytes(veh_per_launch, movers / args.steps / world, scen.n_lanes / world)
     kstep_avg_s = kstep_ms / 1e3 / args.steps
-    achieved = per_launch_bytes / kstep_avg_s / 1e9
+    achieved = survey_bytes / kstep_avg_s / 1e9
     traffic = issue = None
-    for path in (NCU_TRAFFIC, NCU_TRAFFIC.replace(".json", "_8m.json")):
-        try:                                              # the capture of this instance, if any
-            with open(path) as f:
-                tr = json.load(f)
-            if tr.get("workload") == "C4" and tr.get("n_vehicles") == scen.n_trips:
-                traffic = tr.get("dram_bytes_per_launch")
-                issue = tr.get("issue_frac")
-        except Exception:
-            pass
+    if world == 1:                                        # the ncu capture of this very instance
+        for path in (NCU_TRAFFIC, NCU_TRAFFIC.replace(".json", "_8m.json")):
+            try:
+                with open(path) as f:
+                    tr = json.load(f)
+                if tr.get("workload") == "C4" and tr.get("n_vehicles") == scen.n_trips:
+                    traffic = tr.get("dram_bytes_per_launch")
+                    issue = tr.get("issue_frac")
+            except Exception:
+                pass
     # e2e: RL-style loop through the public API with host buffers
     nj = len(scen.graph["junc_lane_offsets"]) - 1
     jids = np.arange(nj, dtype=np.int32)
@@ -327,7 +356,7 @@ def run_gpu(args, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": workload_config(scen, policy=args.policy, extra={
+        "config": workload_config(scen, policy=args.policy, preroll=args.preroll, extra={
             "parallelism": "single GPU" if world == 1 else
             f"spatial partition over {world} GPUs (recursive coordinate bisection of road tiles), " +
             ("boundary movers stored by k_step into the owner GPU's inbox over NVLink peer memory "
@@ -337,9 +366,17 @@ def run_gpu(args, rank, world, local_rank):
             "fp64_guard_hits_per_step": (m1["n_guard_hits"] - m0["n_guard_hits"]) / args.steps}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "k_step", "kernel_ms_avg": kstep_ms / args.steps,
+                     "kernel": "k_prep + k_step (the step kernels, one CUDA-event window)",
+                     "kernel_ms_avg": kstep_ms / args.steps,
                      "signal_kernel_ms_avg": ksig_ms / args.steps,
-                     "alg_bytes_per_launch": per_launch_bytes,
+                     "alg_bytes_per_launch": survey_bytes,
+                     "alg_bytes_per_vehicle_step": B_ALG,
+                     # this implementation's own byte model (32 B records etc.)
+                     "model_bytes_per_launch": model_bytes,
+                     "frac_model": model_bytes / kstep_avg_s / 1e9 / peak,
+                     # what the kernel actually moved (ncu dram bytes of the same instance)
+                     "ncu_dram_gbs": (traffic / kstep_avg_s / 1e9) if traffic else None,
+                     "ncu_dram_over_alg": (traffic / survey_bytes) if traffic else None,
                      # k_step is latency / issue bound: warp instructions
                      # issued / (148 SMs x 4 schedulers x 1965 MHz), from the ncu capture
                      "issue_frac_ncu": issue},
@@ -347,6 +384,8 @@ def run_gpu(args, rank, world, local_rank):
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * nj if host_ctl else 0,
                 "d2h_bytes_per_step": lane_bytes + 8 * 15, "steps": e2e_steps},
         "gpu_launches": int(launches),
+        # ranks in the NCCL communicator / processes whose buffers are mapped (direct)
+        "comm": {"transport": args.transport if world > 1 else None, "ranks": world},
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
@@ -359,9 +398,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--preroll", type=int, default=200,
+                    help="untimed steps before the warm-up (steady state; the t=0 placement is at rest)")
     ap.add_argument("--policy", default="fixed", choices=["fixed", "maxpressure"])
-    ap.add_argument("--transport", default="direct", choices=["direct", "nccl"],
-                    help="N > 1: direct peer-memory stores from k_step (NEXT-2) or NCCL p2p exchange")
+    ap.add_argument("--transport", default="nccl", choices=["direct", "nccl"],
+                    help="N > 1: boundary migration + halo by NCCL p2p (north_star), or direct "
+                         "peer-memory stores from k_step over CUDA IPC (NEXT-2)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N > 1: C4 per GPU (weak) or one C4 split over the N GPUs (strong)")
     ap.add_argument("--scale", type=float, default=1.0,

@@ -302,8 +302,13 @@ sim_status sim_set_vehicle_route(sim_handle h, int32_t vid, int32_t n, const int
 sim_status sim_set_vehicle_route_batch(sim_handle h, int32_t m, const int32_t *vids,
                                        const int32_t *route_offsets, const int32_t *roads,
                                        const float *end_s);
+/* Sizes of the handle's entities and device memory, for sizing read buffers
+ * (no device work). */
 sim_status sim_query_sizes(sim_handle h, sim_sizes *out);
-/* Synchronising reads into caller-owned host buffers.  With partitions,
+/* The simulator's getters (e.g. get_vehicle_speeds; state per vehicle,
+ * junction and lane, App. A2.1; the per-lane order of the linked
+ * lists, P:803-806 — as the step kernel merges stayers and inbox, a1).
+ * Synchronising reads into caller-owned host buffers.  With partitions,
  * sim_read_state reports the vehicles of the partitions in this handle (one
  * process per rank: its own; the others read as PENDING unless they finished
  * here); sim_read_state_global (collective: every rank calls it) reports every
@@ -321,16 +326,32 @@ sim_status sim_read_state(sim_handle h, sim_state *out);
  * (world 1 or loopback); SIM_E_INVALID otherwise. */
 sim_status sim_read_state_device(sim_handle h, sim_state *out);
 sim_status sim_read_state_global(sim_handle h, sim_state *out);
+/* The decisions of the last step (record_decisions = 1; test hook of the
+ * parity gate): leader / lookahead hops, stop-line phantom
+ * (P:200), followers and side neighbours, lane change,
+ * hand-offs / arrivals, insertions, acceleration. */
 sim_status sim_read_decisions(sim_handle h, sim_decisions *out);
+/* Evaluation metrics: counts of pending / driving / finished
+ * vehicles, throughput = finished trips, ATT over finished trips
+ * and over all vehicles, waiting time, the lane
+ * queue lengths and road average speeds on request.
+ * With partitions the counters are summed over all of them, so every rank
+ * gets the global values.
+ * Collective across processes (NCCL or direct transport): every rank must
+ * call every read — sim_read_state, _global, _metrics, _group_metrics, and
+ * sim_load_state — in the same order with the same optional buffers present
+ * (lane statistics / road speeds), since the reductions are collective. */
 sim_status sim_read_metrics(sim_handle h, sim_metrics *out);
 /* Per-group metrics (params.road_group): out[n_groups], counters of the tiles
  * (roads) of each group and status counts of its vehicles; the lane buffers
  * of out[] are ignored.  SIM_E_INVALID without road_group or on a different
  * n_groups. */
 sim_status sim_read_group_metrics(sim_handle h, int32_t n_groups, sim_metrics *out);
-/* Replace the whole state (checkpoint / parity hook).  Pending queues are
- * rebuilt from status; all fields except lane_signal/lane_offsets/lane_order
- * are required. */
+/* Replace the whole state (checkpoint / parity hook; the inverse of the
+ * getters).  Pending queues are rebuilt from status (ordered by
+ * (depart, vid), ledger L25); all fields except lane_signal /
+ * lane_offsets / lane_order are required.  SIM_E_CAPACITY if a road tile
+ * would hold more vehicles than its record region. */
 sim_status sim_load_state(sim_handle h, const sim_state *in);
 /* Test hook of sim_load_state: the DRIVING vehicles with to_inbox[vid] = 1 are
  * placed, unsorted, in their tile's inbox (as if they had entered the tile or
@@ -347,6 +368,8 @@ sim_status sim_load_state_inbox(sim_handle h, const sim_state *in, const uint8_t
 sim_status sim_enable_timing(sim_handle h, int32_t enable);
 sim_status sim_read_timing(sim_handle h, double *step_kernel_ms, double *signal_kernel_ms,
                            int64_t *n_launches);
+/* Release every device buffer (through params.free_ when given); every later
+ * call on h fails with SIM_E_STATE. */
 sim_status sim_destroy(sim_handle h);
 /* Last error message of h (NULL h: the calling thread's last create error). */
 const char *sim_last_error(sim_handle h);

@@ -17,7 +17,7 @@ S.load_library(lib)
 st = torch.cuda.Stream()
 sim = S.Sim.from_scenario(scen, stream=st.cuda_stream)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-sim.step(10); sim.sync()
+sim.step(int(os.environ.get("PREROLL", "10"))); sim.sync()
 sim.enable_timing(True)
 n = 40
 m0 = sim.read_metrics()
