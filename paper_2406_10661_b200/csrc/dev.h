@@ -25,9 +25,8 @@ constexpr int kThreads = 32;         // k_step block size: one warp per road til
 constexpr int kSmemVeh = KSMEM_VEH;  // snapshot slots held in shared memory (larger tiles use global scratch)
 constexpr int kSmemInbox = 48;       // inbox keys sorted in shared memory
 constexpr int kNAcc = 12;            // per-tile int64 accumulators
-constexpr int kMaxRoadLanes = 4;     // road lanes per tile cached in the successor table
+constexpr int kMaxRoadLanes = 8;     // lanes per road (validated; 8-bit lane masks)
 constexpr int kMaxSucc = 8;          // successors per road lane cached in the table
-static_assert(kMaxRoadLanes * kMaxSucc == 32, "one warp builds the successor table");
 // tile descriptor (int32 words, 16-B padded, host-built by build_desc and
 // rebuilt after setters): [nl, nroad, ne, n_all], glob[nl], len[nl], vmax[nl],
 // flags[nl] (bit0 usable; road lanes: usable successors << 8, groups << 16),

@@ -43,7 +43,7 @@ namespace sim {
 #define KS_CONS_WARPS 12
 #endif
 #ifndef KS_RING_KB
-#define KS_RING_KB 190
+#define KS_RING_KB 180
 #endif
 #ifndef KS_MINB
 #define KS_MINB 1
@@ -628,9 +628,9 @@ __device__ __forceinline__ void tile_setup(const Hdr &H, const int *W, const Ext
   {
     const int8_t *gx = reinterpret_cast<const int8_t *>(W + to + 2 + kMaxRoadLanes * kMaxGroups +
                                                         (kMaxRoadLanes * kMaxGroups) / 4);
-    static_assert(kMaxRoadLanes * kMaxRoadLanes * kMaxGroups == 64, "two gidx bytes per lane");
-    (&T.gidx[0][0])[lane_id] = gx[lane_id];
-    (&T.gidx[0][0])[32 + lane_id] = gx[32 + lane_id];
+    static_assert(kMaxRoadLanes * kMaxGroups == 32, "one target road per lane of the warp");
+    for (int q = lane_id; q < kMaxRoadLanes * kMaxRoadLanes * kMaxGroups; q += 32)
+      (&T.gidx[0][0])[q] = gx[q];
   }
   if (lane_id < nl) {
     const int l = lane_id;
@@ -660,8 +660,8 @@ __device__ __forceinline__ void tile_setup(const Hdr &H, const int *W, const Ext
       for (int q = 0; q < kMaxGroups; ++q) T.gtroad[l][q] = gw[2 + q];
     }
   }
-  if (lane_id < ne) {
-    const int *ew = W + eo + 8 * lane_id;
+  for (int ei = lane_id; ei < ne; ei += 32) {
+    const int *ew = W + eo + 8 * ei;
     const unsigned fl = (unsigned)ew[3];
     const int jl = (int)(fl >> 24);
     SuccEnt e;

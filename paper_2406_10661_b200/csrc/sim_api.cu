@@ -261,6 +261,10 @@ sim_status dalloc(sim_s *h, T **p, size_t n) {
   }
   h->allocs.push_back(*p);
   h->alloc_hooked.push_back(h->P.alloc ? 1 : 0);
+  // zero-filled: unused slots of the record regions are read whole by the
+  // state reads (compute-sanitizer initcheck clean)
+  cudaError_t ez = cudaMemset(*p, 0, n * sizeof(T));
+  if (ez != cudaSuccess) return fail(h, SIM_E_CUDA, std::string("cudaMemset: ") + cudaGetErrorString(ez));
   h->bytes += (int64_t)(n * sizeof(T));
   return SIM_OK;
 }

@@ -627,10 +627,11 @@ def _place_on_lanes(lane_ids, lane_len, n_vehicles, prof_len, profile_of, rng,
 
 
 def city(G=72, spacing=900.0, n_vehicles=2_000_000, seed=4, route_len=40,
-         jitter=0.15, remove_frac=0.10, arterial_every=6):
+         jitter=0.15, remove_frac=0.10, arterial_every=6, arterial_lanes=3):
     """C4: city-like perturbed grid.
 
-    Arterials (every `arterial_every`-th grid line) have 3 lanes at 22.2 m/s,
+    Arterials (every `arterial_every`-th grid line) have `arterial_lanes`
+    lanes (3 in C4) at 22.2 m/s,
     other roads 1 or 2 lanes (p = 0.5) at 13.9 m/s.  All vehicles are on the
     network at t = 0, at rest, uniformly over road lanes, with biased random
     walk routes of `route_len` roads (straight 0.6, left 0.2, right 0.2).
@@ -645,7 +646,7 @@ def city(G=72, spacing=900.0, n_vehicles=2_000_000, seed=4, route_len=40,
     def lane_fn(a, c):
         key = (a, c) if a < c else (c, a)
         if key not in pair_lanes:
-            pair_lanes[key] = 3 if is_art(a, c) else int(rng.integers(1, 3))
+            pair_lanes[key] = arterial_lanes if is_art(a, c) else int(rng.integers(1, 3))
         return pair_lanes[key]
 
     def vmax_fn(a, c):

@@ -93,3 +93,14 @@ def test_user_partition(simlib):
     bad[0] = 5
     with pytest.raises(simlib.SimError):
         simlib.Sim(s.graph, s.trips, s.profiles, s.params, world=2, loopback=True, road_owner=bad)
+
+
+def test_wide_roads_accepted_host_side():
+    """Roads of up to 8 lanes pass sim_create's validation (host-only
+    partition call: same validation and tile build, no GPU)."""
+    import numpy as np
+    import synth
+    import paper_2406_10661_b200 as p
+    s = synth.city(G=8, n_vehicles=2000, seed=31, arterial_every=3, arterial_lanes=6)
+    own, mig, halo = p.partition(s.graph, s.trips, s.profiles, s.params, 1)
+    assert own.shape[0] == len(s.graph["road_lane_offsets"]) - 1

@@ -336,3 +336,30 @@ def test_full_run_c3_aggregates(simlib):
     got, ref = _c3_run(simlib, False), _AGG["C3-seed3-fp64"]
     for k in ("tp", "vehicle_steps", "att_all"):
         assert abs(got[k] - ref[k]) <= 0.005 * ref[k], (k, got[k], ref[k])
+
+
+def test_wide_arterials_parity(simlib, oracle_lib):
+    """roads of 6 lanes (arterials of a C4-recipe city; the
+    kernel takes up to 8 lanes per road, 8 successors per lane): one step from
+    random states (fp32 and exact) and 150 exact-mode steps bit-identical to
+    the oracle's fp32-storage run."""
+    scen = synth.city(G=12, n_vehicles=20000, seed=31, arterial_every=3, arterial_lanes=6)
+    assert int(np.diff(scen.graph["road_lane_offsets"]).max()) == 6
+    for exact in (False, True):
+        gsim, orc = _pair(simlib, oracle_lib, scen, exact=exact)
+        for seed in range(2):
+            st = synth.random_state(scen, seed=500 + seed)
+            gsim.load_state(st)
+            orc.load_state({k: (v.astype(np.float64) if k in ("s", "v") else v) for k, v in st.items()})
+            gsim.step(1)
+            orc.step(1)
+            where = f"[wide exact={exact} seed={seed}] "
+            compare_decisions(gsim.read_decisions(), orc.decisions(), st["status"], where=where)
+            compare_states(gsim.read_state(), orc.read_state(), where=where)
+    g, o = _pair(simlib, oracle_lib, scen, exact=True, store_fp32=True, record=False)
+    g.step(150)
+    o.step(150)
+    gs, os_ = g.read_state(), o.read_state()
+    for k in ("status", "lane", "cursor", "wait_steps", "insert_time", "arrive_time"):
+        assert np.array_equal(gs[k], os_[k]), k
+    assert g.read_metrics()["n_lane_changes"] > 0
