@@ -30,24 +30,31 @@ constexpr int kMaxSucc = 8;          // successors per road lane cached in the t
 // tile descriptor (int32 words, 16-B padded, host-built by build_desc and
 // rebuilt after setters): [nl, nroad, ne, n_all], glob[nl], len[nl], vmax[nl],
 // flags[nl] (bit0 usable; road lanes: usable successors << 8, groups << 16),
-// xl[nl] (junction lanes: exit lane, road lanes -1), per road lane 6 words (gbeg[0..3] bytes, gbeg[4], gtroad[0..3]), then the
-// ne <= 32 usable successors of the road lanes sorted by (lane, target road,
-// lane id), 8 words each: j, target road, exit lane, flags (bit0 junction lane,
-// lane_local << 8, rank k << 16), outroads(exit lane) x4, padded to n_all
-// entries; then the target-road section (kDescTroadWords)
+// xl[nl] (junction lanes: exit lane, road lanes -1), per road lane 6 words
+// (gbeg[0..3] bytes, gbeg[4], gtroad[0..3]), zero words up to a multiple of 4
+// (desc_ent_off), then the ne usable successors of the road lanes sorted by
+// (lane, target road, lane id), 8 words (16-B aligned, the layout of
+// SuccEnt) each: j, target road, exit lane, flags (bit0 junction lane, lane
+// << 8, rank k << 16, tile-local index of j << 24), outroads(exit lane) x4,
+// padded to n_all entries; then the target-road section (kDescTroadWords).
+// k_step reads the successor entries and the target-road section in place in
+// the tile's ring slot (tile_setup rewrites each entry's flags word there)
+__host__ __device__ constexpr int desc_ent_off(int nl, int nroad) { return (4 + 5 * nl + 6 * nroad + 3) & ~3; }
 constexpr int kMaxGroups = 4;        // distinct target roads per road lane in the table
 // target-road section at the end of a descriptor: ntr, umask, troad[16],
 // reach[16] (bytes), gidx[4][16] (bytes)
 constexpr int kDescTroadWords = 2 + kMaxRoadLanes * kMaxGroups + (kMaxRoadLanes * kMaxGroups) / 4 +
                                 (kMaxRoadLanes * kMaxRoadLanes * kMaxGroups) / 4;
-constexpr int kDescMaxWords = 4 + 5 * kMaxTileLanes + 6 * kMaxRoadLanes + 8 * kMaxRoadLanes * kMaxSucc +
+constexpr int kDescMaxWords = 4 + 5 * kMaxTileLanes + 6 * kMaxRoadLanes + 3 + 8 * kMaxRoadLanes * kMaxSucc +
                               kDescTroadWords + 3;
 constexpr int kSmemProf = 8;         // profiles staged in shared memory
 constexpr uint64_t kEmptyKey = ~0ull;
 
 enum Acc {
   ACC_VEH_STEPS = 0, ACC_FINISHED, ACC_SUM_TRAVEL, ACC_SUM_WAIT_FIN, ACC_SUM_DELAY,
-  ACC_LANE_CHANGES, ACC_HANDOFFS, ACC_INSERTED, ACC_GUARD, ACC_OVERFLOW, ACC_R1, ACC_R2
+  ACC_LANE_CHANGES, ACC_HANDOFFS, ACC_INSERTED, ACC_GUARD, ACC_OVERFLOW,
+  ACC_SUM_INSERT,   // sum of insert_time added at insertion, subtracted at arrival (att_all)
+  ACC_R2
 };
 enum { ST_PENDING = 0, ST_DRIVING = 1, ST_FINISHED = 2 };
 enum { SIG_GREEN = 0, SIG_YELLOW = 1, SIG_RED = 2 };
@@ -253,7 +260,6 @@ void launch_apply_requests(int32_t *request, const int32_t *junc, const int32_t 
 void launch_reduce_acc(const long long *tacc, int n_tiles, const int32_t *cnt,
                        const int32_t *icnt, const uint8_t *status, int nv, long long *out,
                        void *stream);
-void launch_sum_insert(const StepArgs &a, long long *out, void *stream);
 void launch_state_device(const StepArgs *parts, int n_parts, int nv, uint8_t *status, int32_t *lane,
                          int32_t *cursor, int32_t *wait, int32_t *ins, int32_t *arr, float *s, float *v,
                          void *stream);

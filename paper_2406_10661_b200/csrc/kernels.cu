@@ -137,8 +137,7 @@ __global__ void k_reduce_acc(const long long *tacc, int n_tiles, const int32_t *
                              const int32_t *icnt, const uint8_t *status, int nv, long long *out) {
   // out (zeroed by the caller): [0, kNAcc) per-tile counters, kNAcc: driving
   // (stayers + inbox), kNAcc+1 / +2: PENDING / FINISHED vehicles from status
-  // (nv > 0; the library passes 0 and uses kNAcc+1 for the driving vehicles'
-  // insert-time sum, k_sum_insert)
+  // (nv > 0; the library passes 0)
   __shared__ unsigned long long sh[kNAcc + 3];
   if (threadIdx.x < kNAcc + 3) sh[threadIdx.x] = 0;
   __syncthreads();
@@ -492,23 +491,6 @@ void launch_state_device(const StepArgs *parts, int n_parts, int nv, uint8_t *st
   for (int q = 0; q < n_parts; ++q)
     if (parts[q].n_own > 0)
       k_state_driving<<<(parts[q].n_own + 7) / 8, 256, 0, st>>>(parts[q], status, lane, cursor, wait, s, v);
-}
-
-// sum of insert_time over the DRIVING vehicles of the own tiles (stayers +
-// inbox) -> *out (added; ATT over all vehicles)
-__global__ void k_sum_insert(const StepArgs A, long long *out) {
-  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (w >= A.n_own) return;
-  const int T = A.tiles[w];
-  const int n = A.cnt_in[T] + A.icnt_in[T];
-  const InboxRec *rec = tile_recs(A, T, A.cnt_in[T]);
-  long long x = 0;
-  for (int i = lane; i < n; i += 32) x += A.insert_time[rec[i].vid];
-  for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
-  if (lane == 0 && x) atomicAdd(reinterpret_cast<unsigned long long *>(out), (unsigned long long)x);
-}
-void launch_sum_insert(const StepArgs &a, long long *out, void *stream) {
-  if (a.n_own > 0) k_sum_insert<<<(a.n_own + 7) / 8, 256, 0, (cudaStream_t)stream>>>(a, out);
 }
 
 void launch_lane_stats(const StepArgs &a, int32_t *lane_count, int32_t *lane_wait,

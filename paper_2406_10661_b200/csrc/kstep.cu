@@ -40,10 +40,10 @@
 namespace sim {
 
 #ifndef KS_CONS_WARPS
-#define KS_CONS_WARPS 12
+#define KS_CONS_WARPS 14
 #endif
 #ifndef KS_RING_KB
-#define KS_RING_KB 180
+#define KS_RING_KB 208
 #endif
 #ifndef KS_MINB
 #define KS_MINB 1
@@ -112,8 +112,14 @@ __device__ __forceinline__ PState pstate_at(unsigned char *p, int n4) {
   return S;
 }
 
+#ifdef KS_SKEW
+constexpr int kSkew = KS_SKEW;                // rounds a consumer warp may run ahead
+#else
+constexpr int kSkew = 0;
+#endif
 struct __align__(128) StepSmem {
   Hdr H[kNH];
+  unsigned long long rb[kSkew + 1];             // round barriers (KS_SKEW builds)
   int next_seq;
   __align__(16) Prof prof[kSmemProf];
   TileSh T[kCW];
@@ -300,7 +306,9 @@ __device__ __noinline__ void emit_moved(const StepArgs &A, const View &C, int i,
     A.wait_fin[vid] = r.wait1;
     atomicAdd(&T.c_fin, 1);
     long long *ta = A.tacc + (size_t)T.tile * kNAcc;
-    red_add(ta + ACC_SUM_TRAVEL, (long long)(A.t + 1 - A.insert_time[vid]));
+    const int ins = A.insert_time[vid];
+    red_add(ta + ACC_SUM_TRAVEL, (long long)(A.t + 1 - ins));
+    red_add(ta + ACC_SUM_INSERT, -(long long)ins);
     red_add(ta + ACC_SUM_WAIT_FIN, (long long)r.wait1);
     return;
   }
@@ -600,7 +608,7 @@ __device__ __forceinline__ void tile_setup(const Hdr &H, const int *W, const Ext
                                            int lane_id) {
   const int nl = H.nl, nroad = H.nroad;
   const int ne = W[2], n_all = W[3];
-  const int eo = 4 + 5 * nl + 6 * nroad;
+  const int eo = desc_ent_off(nl, nroad);
   const int to = eo + 8 * n_all;                     // target-road section
   if (lane_id == 0) {
     T.nl = nl;
@@ -620,17 +628,8 @@ __device__ __forceinline__ void tile_setup(const Hdr &H, const int *W, const Ext
     T.c_delay = 0ull;
     T.ntr = W[to];
     T.umask = (uint32_t)W[to + 1];
-  }
-  if (lane_id < kMaxRoadLanes * kMaxGroups) {
-    T.troad[lane_id] = W[to + 2 + lane_id];
-    T.reach[lane_id] = reinterpret_cast<const uint8_t *>(W + to + 2 + kMaxRoadLanes * kMaxGroups)[lane_id];
-  }
-  {
-    const int8_t *gx = reinterpret_cast<const int8_t *>(W + to + 2 + kMaxRoadLanes * kMaxGroups +
-                                                        (kMaxRoadLanes * kMaxGroups) / 4);
-    static_assert(kMaxRoadLanes * kMaxGroups == 32, "one target road per lane of the warp");
-    for (int q = lane_id; q < kMaxRoadLanes * kMaxRoadLanes * kMaxGroups; q += 32)
-      (&T.gidx[0][0])[q] = gx[q];
+    T.se_o = (uint32_t)(reinterpret_cast<const unsigned char *>(W + eo) - ks_smem);
+    T.tr_o = (uint32_t)(reinterpret_cast<const unsigned char *>(W + to + 2) - ks_smem);
   }
   if (lane_id < nl) {
     const int l = lane_id;
@@ -647,6 +646,9 @@ __device__ __forceinline__ void tile_setup(const Hdr &H, const int *W, const Ext
     T.left[l] = (l < nroad && l > 0) ? (int8_t)(l - 1) : (int8_t)-1;
     T.right[l] = (l < nroad - 1) ? (int8_t)(l + 1) : (int8_t)-1;
     if (l < nroad) {
+      int e0 = 0;                                    // entries of the road lanes before l
+      for (int q = 0; q < l; ++q) e0 += (W[4 + 3 * nl + q] >> 8) & 0xff;
+      T.se0[l] = (uint8_t)e0;
       const int *gw = W + 4 + 5 * nl + 6 * l;
       T.sn[l] = (uint8_t)((fl >> 8) & 0xff);
       T.ng[l] = (uint8_t)((fl >> 16) & 0xff);
@@ -660,18 +662,12 @@ __device__ __forceinline__ void tile_setup(const Hdr &H, const int *W, const Ext
       for (int q = 0; q < kMaxGroups; ++q) T.gtroad[l][q] = gw[2 + q];
     }
   }
-  for (int ei = lane_id; ei < ne; ei += 32) {
-    const int *ew = W + eo + 8 * ei;
+  for (int ei = lane_id; ei < ne; ei += 32) {        // flags word -> SuccEnt::fl, in place
+    int *ew = const_cast<int *>(W) + eo + 8 * ei;
     const unsigned fl = (unsigned)ew[3];
     const int jl = (int)(fl >> 24);
-    SuccEnt e;
-    e.j = ew[0];
-    e.troad = ew[1];
-    e.b = ew[2];
-    e.outr = make_int4(ew[4], ew[5], ew[6], ew[7]);
     const bool stop = (fl & 1u) && ext[jl - nroad].sig != SIG_GREEN;
-    e.fl = (stop ? 1 : 0) | ((int)(jl & 0xff) << 8);
-    T.se[(fl >> 8) & 0xff][(fl >> 16) & 0xff] = e;
+    ew[3] = (stop ? 1 : 0) | ((int)(jl & 0xff) << 8);
   }
   __syncwarp();
 }
@@ -837,6 +833,7 @@ __device__ __forceinline__ int push_list(bool pred, uint16_t *list, int count, i
 template <bool EXACT>
 __device__ __forceinline__ void run_passes(const StepArgs &A, const PState &K, const View &C,
                                            TileSh &T, int n, int lane) {
+  KP_DECL
   int nd = 0;
   if constexpr (!EXACT) {
     int nc = 0;
@@ -851,8 +848,10 @@ __device__ __forceinline__ void run_passes(const StepArgs &A, const PState &K, c
       nc = push_list(cand, K.cand, nc, q, lane);
     }
     __syncwarp();
+    KP(25, lane == 0);
     for (int q = lane; q < nc; q += 32) pass2(A, K, C, K.cand[q], T);   // pass 2 (compacted)
     __syncwarp();
+    KP(26, lane == 0);
     for (int q0 = 0; q0 < n; q0 += 32) {             // pass 3 (every vehicle)
       const int q = q0 + lane;
       bool def = false;
@@ -860,6 +859,7 @@ __device__ __forceinline__ void run_passes(const StepArgs &A, const PState &K, c
       nd = push_list(def, K.defl, nd, q, lane);
     }
     __syncwarp();
+    KP(27, lane == 0);
   } else {
     for (int q = lane; q < n; q += 32) K.defl[q] = (uint16_t)q;
     nd = n;
@@ -870,6 +870,7 @@ __device__ __forceinline__ void run_passes(const StepArgs &A, const PState &K, c
     if (!EXACT) atomicAdd(&T.c_guard, 1);
   }
   __syncwarp();
+  KP(28, lane == 0);
 }
 
 // In-order compaction of the tile's stayers into its record region for t+1,
@@ -1000,6 +1001,7 @@ __device__ __forceinline__ void tile_finish(const StepArgs &A, const PState &K, 
     if (T.c_ins) {
       red_add(ta + ACC_INSERTED, T.c_ins);
       red_add(ta + ACC_SUM_DELAY, (long long)T.c_delay);
+      red_add(ta + ACC_SUM_INSERT, (long long)T.c_ins * (A.t + 1));   // insert_time = t + 1
     }
     if (T.c_lc) red_add(ta + ACC_LANE_CHANGES, T.c_lc);
     if (T.c_hand) red_add(ta + ACC_HANDOFFS, T.c_hand);
@@ -1018,12 +1020,14 @@ __device__ __forceinline__ void tile_finish(const StepArgs &A, const PState &K, 
 template <bool EXACT, bool GM>
 __device__ __forceinline__ void run_tile(const StepArgs &A, StepSmem &M, const Hdr &H, TileSh &T,
                                          const Prof *P, int lane) {
+  KP_DECL
   const int ns = H.n_st, ni = H.n_in, n = ns + ni;
   const SlotLayout L = GM ? slot_layout(0, 0, H.dw) : slot_layout(ns, ni, H.dw);
   unsigned char *slot = M.ring + H.off;
   const int *W = reinterpret_cast<const int *>(slot + L.desc);
   tile_setup(H, W, reinterpret_cast<const ExtFirst *>(W + H.dwd),
              reinterpret_cast<const PendHead *>(W + H.dwd + kExtWords * (H.nl - H.nroad)), P, T, lane);
+  KP(22, lane == 0);
   View C;
   PState K;
   if (!GM) {
@@ -1116,6 +1120,7 @@ __device__ __forceinline__ void run_tile(const StepArgs &A, StepSmem &M, const H
     }
   }
   __syncwarp();
+  KP(23, lane == 0);
   // ---- lane segments of the snapshot -------------------------------------------------
   for (int i = lane; i < n; i += 32) {
     const int l = m_lane(C.meta(i));
@@ -1123,9 +1128,15 @@ __device__ __forceinline__ void run_tile(const StepArgs &A, StepSmem &M, const H
     if (i == n - 1 || m_lane(C.meta(i + 1)) != l) T.seg_end[l] = (int16_t)(i + 1);
   }
   __syncwarp();
+  KP(24, lane == 0);
   run_passes<EXACT>(A, K, C, T, n, lane);
+#ifdef KS_PROF
+  kp_last = clock64();
+#endif
   compact(A, K, C, T, n, lane);
+  KP(29, lane == 0);
   tile_finish(A, K, C, T, lane);
+  KP(30, lane == 0);
 }
 
 // global-mode tiles (rare), out of line so their copy of the passes stays out
@@ -1164,6 +1175,35 @@ __device__ __forceinline__ void consumer(const StepArgs &A, StepSmem &M, const P
                                          int lane) {
   TileSh &T = M.T[warp];
   KP_DECL
+#ifdef KS_SKEW
+  // bounded skew: round r starts once round r - 1 - kSkew is complete (every
+  // warp arrived on rb[(r - 1 - kSkew) % (kSkew + 1)]); a warp that meets the
+  // sentinel at round r arrives for r and leaves (no warp waits for a later
+  // round: all tiles are claimed)
+  for (int r = 0;; ++r) {
+    const int rw = r - 1 - kSkew;
+    if (rw >= 0) mbar_wait(&M.rb[rw % (kSkew + 1)], (unsigned)(rw / (kSkew + 1)) & 1u);
+    KP(11, lane == 0);
+    int seq = 0;
+    if (lane == 0) seq = atomicAdd(&M.next_seq, 1);
+    seq = __shfl_sync(0xffffffffu, seq, 0);
+    Hdr &H = M.H[seq % kNH];
+    KP(9, lane == 0);
+    mbar_wait(&H.full, (unsigned)(seq / kNH) & 1u);
+    KP(8, lane == 0);
+    const bool done = H.done;
+    if (!done) {
+      if (H.gm) run_tile_gm<EXACT>(A, M, H, T, P, lane);
+      else run_tile<EXACT, false>(A, M, H, T, P, lane);
+      KP(10, lane == 0);
+      KPN(20, lane == 0, 1);
+      if (lane == 0) mbar_arrive(&H.empty);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&M.rb[r % (kSkew + 1)]);
+    if (done) return;
+  }
+#endif
 #ifndef KS_FREERUN
 #ifndef KS_ROUND_TILES
 #define KS_ROUND_TILES 1
@@ -1257,8 +1297,7 @@ __device__ __forceinline__ void consumer(const StepArgs &A, StepSmem &M, const P
 
 template <bool EXACT>
 __global__ void __launch_bounds__(kStepThreads, KS_MINB) k_step(const __grid_constant__ StepArgs A) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  StepSmem &M = *reinterpret_cast<StepSmem *>(smem_raw);
+  StepSmem &M = *reinterpret_cast<StepSmem *>(ks_smem);
   const int tid = threadIdx.x;
   const Prof *P = A.prof;
   if (A.n_prof <= kSmemProf) {                      // profiles as int4 words (Prof is 96 B)
@@ -1273,6 +1312,7 @@ __global__ void __launch_bounds__(kStepThreads, KS_MINB) k_step(const __grid_con
       mbar_init(&M.H[e].empty, 1);
     }
     M.next_seq = 0;
+    for (int b = 0; b <= kSkew; ++b) mbar_init(&M.rb[b], kCW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();

@@ -87,6 +87,10 @@ __device__ IDM_INLINE R idm(R v, R v0, bool lead, R gap, R dv, const PV<R> &p, R
 struct SuccEnt { int j, troad, b, fl; int4 outr; };
 
 // Tile-local lane metadata staged in shared memory.
+// the dynamic shared memory of k_step (StepSmem); tile tables inside a ring
+// slot are addressed as offsets from it
+extern __shared__ __align__(128) unsigned char ks_smem[];
+
 struct TileSh {
   int nl, nroad, tile, base, ibase, cap, icap;
   int snap0, n;                      // snapshot range [snap0, snap0 + n) of the tile's vehicles
@@ -97,7 +101,11 @@ struct TileSh {
   uint8_t ng[kMaxRoadLanes];         // groups (distinct target roads) per road lane
   uint8_t gbeg[kMaxRoadLanes][kMaxGroups + 1];
   int gtroad[kMaxRoadLanes][kMaxGroups];
-  SuccEnt se[kMaxRoadLanes][kMaxSucc];   // sorted by (target road, lane id)
+  // successor table and target-road section: read in place in the tile's
+  // descriptor in the ring slot (byte offsets from ks_smem, so that every
+  // access stays a shared-memory load); se0[l] = first entry of road lane l
+  uint32_t se_o, tr_o;
+  uint8_t se0[kMaxRoadLanes];
   int glob[kMaxTileLanes];
   float len[kMaxTileLanes], vmax[kMaxTileLanes];
   int16_t seg_start[kMaxTileLanes], seg_end[kMaxTileLanes];   // lane segments of the snapshot
@@ -111,14 +119,26 @@ struct TileSh {
   // road" test is then one bit
   int ntr;
   uint32_t umask;
-  int troad[kMaxRoadLanes * kMaxGroups];
-  uint8_t reach[kMaxRoadLanes * kMaxGroups];
-  int8_t gidx[kMaxRoadLanes][kMaxRoadLanes * kMaxGroups];
   // per-tile outputs of the step
   int run;                           // stayers written (compaction, in snapshot order)
   int c_fin, c_lc, c_hand, c_guard, c_ovf, c_ins;
   unsigned long long c_delay;
 };
+
+__device__ __forceinline__ const SuccEnt &t_se(const TileSh &T, int l, int k) {
+  return reinterpret_cast<const SuccEnt *>(ks_smem + T.se_o)[T.se0[l] + k];
+}
+// target-road section: troad[32] (int), reach[32] (bytes), gidx[8][32] (bytes)
+__device__ __forceinline__ int t_troad(const TileSh &T, int k) {
+  return reinterpret_cast<const int *>(ks_smem + T.tr_o)[k];
+}
+__device__ __forceinline__ uint32_t t_reach(const TileSh &T, int k) {
+  return (ks_smem + T.tr_o + 4 * kMaxRoadLanes * kMaxGroups)[k];
+}
+__device__ __forceinline__ int t_gidx(const TileSh &T, int l, int k) {
+  return reinterpret_cast<const int8_t *>(ks_smem + T.tr_o + 5 * kMaxRoadLanes * kMaxGroups)
+      [l * (kMaxRoadLanes * kMaxGroups) + k];
+}
 
 // Snapshot of a tile at time t (shared memory; the tile's global scratch for
 // a tile in global mode): eight word arrays of stride st — the fields other
@@ -207,28 +227,28 @@ __device__ __forceinline__ Next next1_t(const StepArgs &A, const TileSh &T, int 
     // entries sorted by lane id: the first is the lowest candidate, the first
     // whose exit lane continues toward R2 is the preferred one (ledger L24)
     for (int k = b; k < e; ++k) {
-      const SuccEnt &x = T.se[l][k];
+      const SuccEnt &x = t_se(T, l, k);
       if (pref_ok(x.outr, R2)) return ent_next(x);
     }
-    return ent_next(T.se[l][b]);
+    return ent_next(t_se(T, l, b));
   }
   return Next{kLaneBlocked, false, -1};
 }
 // next1_t for the vehicle's own next road, known as troad[k] (k < 0: no road
 // lane of the tile leads there)
 __device__ __forceinline__ Next next1_k(const TileSh &T, int l, int k, int R2) {
-  const int g = k >= 0 ? T.gidx[l][k] : -1;
+  const int g = k >= 0 ? t_gidx(T, l, k) : -1;
   if (g < 0) return Next{kLaneBlocked, false, -1};
   const int b = T.gbeg[l][g], e = T.gbeg[l][g + 1];
   for (int q = b; q < e; ++q) {
-    const SuccEnt &x = T.se[l][q];
+    const SuccEnt &x = t_se(T, l, q);
     if (pref_ok(x.outr, R2)) return ent_next(x);
   }
-  return ent_next(T.se[l][b]);
+  return ent_next(t_se(T, l, b));
 }
 __device__ __forceinline__ int troad_index(const TileSh &T, int R) {
   for (int k = 0; k < T.ntr; ++k)
-    if (T.troad[k] == R) return k;
+    if (t_troad(T, k) == R) return k;
   return -1;
 }
 __device__ __forceinline__ int next_from_road_t(const StepArgs &A, const TileSh &T, int l, int R1,
@@ -587,7 +607,7 @@ __device__ __forceinline__ Elig lc_elig(const StepArgs &A, const TileSh &T, int 
     uint32_t G = T.umask;                                // destination road: every usable lane
     if (!dest) {
       me.k = troad_index(T, me.nxt);
-      G = me.k >= 0 ? T.reach[me.k] : 0u;
+      G = me.k >= 0 ? t_reach(T, me.k) : 0u;
     }
     inG = dest || ((G >> l) & 1u);                       // l in G <=> next1 != BLOCKED
     if (!inG) {                                          // ledger L18, L37

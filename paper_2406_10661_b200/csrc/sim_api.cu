@@ -188,6 +188,8 @@ struct sim_s {
   std::vector<int32_t> desc_words;       // per tile: words of the descriptor part
   int64_t fin0 = 0;                  // FINISHED vehicles in the last loaded state
   long long acc_fin0 = 0;            // finished counter at the last load
+  int64_t ins0 = 0;                  // sum of insert_time over the DRIVING vehicles loaded
+  long long acc_ins0 = 0;            // ACC_SUM_INSERT at the last load
   // batched environments (NEXT-3)
   std::vector<uint64_t> vseed;
   std::vector<int32_t> rngid, road_group, veh_group;
@@ -339,6 +341,7 @@ void build_desc(sim_s *h) {
     // first vehicle at t); road lanes: -1
     for (int l = 0; l < nl; ++l) w.push_back(l < nroad ? -1 : h->exit_lane[h->tile_lanes[l0 + l]]);
     w.insert(w.end(), grp.begin(), grp.end());
+    w.resize(desc_ent_off(nl, nroad), 0);            // 16-B aligned entries (read in place)
     w.insert(w.end(), ent.begin(), ent.end());
     // pad to all successors so setters (which change the usable set) never
     // change the descriptor's size or offsets
@@ -911,9 +914,11 @@ sim_status upload_state(sim_s *h, const HostState &S) {
   }
   std::vector<int> wfin(nv, 0);
   h->fin0 = 0;
+  h->ins0 = 0;
   for (int k = 0; k < nv; ++k) {
     wfin[k] = S.status[k] == ST_FINISHED ? S.wait[k] : 0;
     h->fin0 += S.status[k] == ST_FINISHED;
+    if (S.status[k] == ST_DRIVING) h->ins0 += S.insert_time[k];
   }
   // pending queues per start lane sorted by (depart, vid) (ledger L25)
   std::vector<std::vector<int>> pq(h->nl);
@@ -982,6 +987,7 @@ sim_status upload_state(sim_s *h, const HostState &S) {
   // (all tiles of every partition, summed across processes), so that
   // n_finished stays the loaded count plus the arrivals since on every rank
   h->acc_fin0 = 0;
+  h->acc_ins0 = 0;
   h->grp_fin0.assign(h->n_groups, 0);
   h->grp_acc_fin0.assign(h->n_groups, 0);
   for (int k = 0; k < nv && h->n_groups; ++k) h->grp_fin0[h->veh_group[k]] += S.status[k] == ST_FINISHED;
@@ -990,6 +996,7 @@ sim_status upload_state(sim_s *h, const HostState &S) {
     sim_status st = read_counters(h, c);
     if (st) return st;
     h->acc_fin0 = c[ACC_FINISHED];
+    h->acc_ins0 = c[ACC_SUM_INSERT];
     if (h->n_groups) {
       st = read_group_counters(h, c);
       if (st) return st;
@@ -1313,8 +1320,7 @@ sim_status read_counters(sim_s *h, std::vector<long long> &out) {
   for (Part &P : h->parts) {
     StepArgs a = step_args(P, h->t);
     launch_reduce_acc(P.A.tacc, h->nt, a.cnt_in, a.icnt_in, P.A.status, 0, P.red_d, h->stream);
-    launch_sum_insert(a, P.red_d + kNAcc + 1, h->stream);
-    h->n_launch += 2;
+    h->n_launch += 1;
   }
   if (h->comm || h->ipc) {
     sim_status st = allreduce_sum(h, 0, 0, 0, kNAcc + 3);
@@ -2407,8 +2413,7 @@ sim_status sim_read_metrics(sim_handle h, sim_metrics *m) {
   for (Part &P : h->parts) {
     StepArgs a = step_args(P, h->t);
     launch_reduce_acc(P.A.tacc, h->nt, a.cnt_in, a.icnt_in, P.A.status, 0, P.red_d, h->stream);
-    launch_sum_insert(a, P.red_d + kNAcc + 1, h->stream);
-    h->n_launch += 2;
+    h->n_launch += 1;
   }
   if (h->comm || h->ipc) {
     sim_status st = allreduce_sum(h, 0, 0, 0, kNAcc + 3);
@@ -2472,9 +2477,10 @@ sim_status sim_read_metrics(sim_handle h, sim_metrics *m) {
   m->n_inserted = c[ACC_INSERTED];
   m->n_guard_hits = c[ACC_GUARD];
   m->att_finished = c[ACC_FINISHED] ? (double)c[ACC_SUM_TRAVEL] / (double)c[ACC_FINISHED] : 0.0;
-  // ATT over all vehicles (ledger L27): c[kNAcc + 1] = sum of insert_time
-  // over the DRIVING vehicles (k_sum_insert)
-  m->sum_time_driving = (int64_t)h->t * m->n_driving - c[kNAcc + 1];
+  // ATT over all vehicles (ledger L27): the sum of insert_time over the
+  // DRIVING vehicles is the loaded sum plus ACC_SUM_INSERT since (+insert_time
+  // at every insertion, -insert_time at every arrival)
+  m->sum_time_driving = (int64_t)h->t * m->n_driving - (h->ins0 + (c[ACC_SUM_INSERT] - h->acc_ins0));
   {
     const long long n_all = c[ACC_FINISHED] + m->n_driving;
     m->att_all = n_all ? (double)(c[ACC_SUM_TRAVEL] + m->sum_time_driving) / (double)n_all : 0.0;

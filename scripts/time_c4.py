@@ -51,11 +51,17 @@ try:
             tot = tot_p if i < 8 else tot_c
             print(f"  {nm:18s} {pb[i]/max(tot,1)*100:5.1f}%  ({pb[i]/1e6:.1f} Mcyc)")
         print(f"  tiles {pb[20]/10:.0f}/step  gmode {pb[21]/10:.0f}")
+        ph = {22: "setup", 23: "merge", 24: "segs", 25: "pass1", 26: "pass2", 27: "pass3", 28: "fp64",
+              29: "compact", 30: "finish"}
+        tot = sum(pb[i] for i in ph) or 1
+        print("  in tile: " + "  ".join(f"{nm} {pb[i]/tot*100:.1f}%" for i, nm in ph.items()))
         if pb[14]:
             print(f"  rounds {pb[14]}: slowest tile / mean tile = {pb[12]/max(pb[13],1):.2f}; vehicles of the slowest {pb[15]/pb[14]:.0f} vs mean {pb[16]/pb[14]:.0f}")
         tc = np.zeros(65536 * 4, np.uint32)
         if L.sim_debug_tile_cycles(tc.ctypes.data_as(ctypes.c_void_p)) > 0:
             tc = tc.reshape(-1, 4)[:scen.graph["road_lane_offsets"].shape[0] - 1]
+            if os.environ.get("DUMP"):
+                np.savez(os.environ["DUMP"], tc=tc)
             cyc, nv = tc[:, 0].astype(float), tc[:, 1].astype(float)
             ok = nv > 0
             print(f"  tile cycles: mean {cyc[ok].mean():.0f} median {np.median(cyc[ok]):.0f} p90 {np.percentile(cyc[ok], 90):.0f} p99 {np.percentile(cyc[ok], 99):.0f}")
