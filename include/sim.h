@@ -153,6 +153,13 @@ typedef struct {
   void *(*alloc)(size_t bytes, void *ctx);
   void (*free_)(void *ptr, void *ctx);
   void *alloc_ctx;
+  /* sim_step(n) with n >= 12 replays a CUDA graph of 6 captured steps
+   * (launch cost once per 6 steps, programmatic dependent launches between
+   * the step kernels); results are identical to stepping one by
+   * one.  Nonzero: always launch step by step.  Graphs are never used with
+   * the multi-process transports (IPC barrier, NCCL) or while sim_enable_timing
+   * is on. */
+  int32_t no_step_graphs;
 } sim_params;
 
 typedef struct {

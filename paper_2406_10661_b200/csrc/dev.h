@@ -15,6 +15,10 @@
 #pragma once
 #include <stdint.h>
 
+#include <utility>
+
+#include <cuda_runtime.h>
+
 namespace sim {
 
 constexpr int kMaxTileLanes = 32;    // lanes per tile (road lanes + outgoing junction lanes)
@@ -143,7 +147,11 @@ __host__ __device__ inline uint32_t pack_meta(int lane_local, int prof, int curs
 }
 
 struct StepArgs {
+  // the step t this launch computes (t -> t+1) is t + *t_base when t_base is
+  // set (a step of a captured CUDA graph: t is the step's offset in the graph,
+  // *t_base the graph's first step, written before every replay), else t
   int32_t t, n_tiles, n_lanes, n_veh;
+  const int32_t *t_base;
   uint64_t seed;
   // model constants (fp32 inputs; fp64 copies are their exact promotions)
   float polite, b_hard, b_safe, v_wait;
@@ -220,6 +228,20 @@ struct StepArgs {
   uint8_t *r_guard, *r_mark;        // r_mark: processed by this partition in the last step
 };
 
+#ifdef __CUDACC__
+__device__ __forceinline__ int step_t(const StepArgs &A) {
+  return A.t_base ? A.t + __ldg(A.t_base) : A.t;
+}
+// Programmatic dependent launch (the step kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): wait until the previous
+// kernel of the stream has completed and its writes are visible; then let the
+// next one be scheduled.  Both are no-ops without a programmatic dependency.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+#endif
+
 // the vehicles of tile T at t, stayers (sorted) then inbox records, contiguous
 __host__ __device__ inline const InboxRec *tile_recs(const StepArgs &A, int T, int n_st) {
   return A.vin + A.tile_base[T] + A.tile_cap[T] - n_st;
@@ -249,9 +271,30 @@ struct SignalArgs {
   int32_t mp_period;
 };
 
+// A kernel launch that may begin while the previous kernel of the stream is
+// still running (programmatic dependent launch): the kernel
+// calls pdl_wait() before it reads what that kernel wrote.
+template <typename... K, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(K...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // kernel launchers (kernels.cu)
+void launch_set_i32(int32_t *p, int32_t v, void *stream);
 void launch_signal(const SignalArgs &a, void *stream);
 void launch_step(const StepArgs &a, void *stream, int smem_bytes);
+void init_step_launch(int smem_bytes);             // function attributes / occupancy, once
 void launch_prep(const StepArgs &a, void *stream);
 void launch_lane_order(const StepArgs &a, int32_t *out_vid, uint8_t *out_lane, void *stream);
 int step_smem_bytes();

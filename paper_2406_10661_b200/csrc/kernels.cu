@@ -32,6 +32,8 @@ __device__ __forceinline__ int sig_count(const SignalArgs &a, int lane) {
 }
 
 __global__ void k_signal(SignalArgs a) {
+  pdl_wait();                                       // the lane counts of t (previous k_step)
+  pdl_trigger();
   const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (j >= a.n_junctions) return;
@@ -365,7 +367,7 @@ __global__ void k_rehome(StepArgs A, const int32_t *new_owner) {
   if (q == A.rank) return;
   const PeerView &Q = A.peers[q];
   const PeerView &P = A.peers[A.rank];
-  const int par = A.t & 1, s3 = A.t % 3;
+  const int par = step_t(A) & 1, s3 = step_t(A) % 3;
   const int n = A.cnt_in[T], m = A.icnt_in[T];
   const int base = A.tile_base[T];
   // stayers and inbox records: one contiguous range at the same positions
@@ -429,8 +431,12 @@ void launch_peer_sum(const PeerView *peers, int world, int kind, int dtype, int6
 // ---- launchers ---------------------------------------------------------------
 void launch_signal(const SignalArgs &a, void *stream) {
   if (a.n_junctions > 0)
-    k_signal<<<(a.n_junctions + 3) / 4, 128, 0, (cudaStream_t)stream>>>(a);
+    launch_pdl(k_signal, dim3((a.n_junctions + 3) / 4), dim3(128), 0, (cudaStream_t)stream, a);
 }
+
+// the first step of a captured step graph, written before each replay
+__global__ void k_set_i32(int32_t *p, int32_t v) { *p = v; }
+void launch_set_i32(int32_t *p, int32_t v, void *stream) { k_set_i32<<<1, 1, 0, (cudaStream_t)stream>>>(p, v); }
 
 void launch_apply_requests(int32_t *request, const int32_t *junc, const int32_t *phase, int m,
                            void *stream) {

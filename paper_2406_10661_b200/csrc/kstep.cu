@@ -279,7 +279,7 @@ __device__ __noinline__ int lower_bound_inbox_global(const InboxRec *inb, const 
 __device__ __noinline__ int emit_peer(const StepArgs &A, const InboxRec &rec, int owner, int dt,
                                       int lane_g) {
   const PeerView &Q = A.peers[owner];
-  const int nb = (A.t + 1) & 1, ns = (A.t + 1) % 3;
+  const int nb = (step_t(A) + 1) & 1, ns = (step_t(A) + 1) % 3;
   const int vid = rec.vid;
   const int slot = atomicAdd(&Q.icnt[nb][dt], 1);
   int ovf = 0;
@@ -302,12 +302,12 @@ __device__ __noinline__ void emit_moved(const StepArgs &A, const View &C, int i,
   if (r.hand) atomicAdd(&T.c_hand, r.hand);
   if (kind == 3) {
     A.status[vid] = ST_FINISHED;
-    A.arrive_time[vid] = A.t + 1;
+    A.arrive_time[vid] = step_t(A) + 1;
     A.wait_fin[vid] = r.wait1;
     atomicAdd(&T.c_fin, 1);
     long long *ta = A.tacc + (size_t)T.tile * kNAcc;
     const int ins = A.insert_time[vid];
-    red_add(ta + ACC_SUM_TRAVEL, (long long)(A.t + 1 - ins));
+    red_add(ta + ACC_SUM_TRAVEL, (long long)(step_t(A) + 1 - ins));
     red_add(ta + ACC_SUM_INSERT, -(long long)ins);
     red_add(ta + ACC_SUM_WAIT_FIN, (long long)r.wait1);
     return;
@@ -366,6 +366,8 @@ __device__ __noinline__ void emit_moved(const StepArgs &A, const View &C, int i,
 // producer warp bulk-copies them with the descriptor.  Runs after k_signal (the
 // signals of t) and reads only state(t).
 __global__ void __launch_bounds__(128) k_prep(const __grid_constant__ StepArgs A) {
+  pdl_wait();                                       // the signals of t (k_signal)
+  pdl_trigger();
   const int w = blockIdx.x * 4 + (threadIdx.x >> 5), l = threadIdx.x & 31;
   if (w >= A.n_own) return;
   const int T = A.tiles[w];
@@ -415,7 +417,7 @@ __global__ void __launch_bounds__(128) k_prep(const __grid_constant__ StepArgs A
     if (h < A.pend_off[g + 1]) {
       const int vk = A.pend_vid[h];
       const int dep = A.depart[vk];
-      if (dep <= A.t) {
+      if (dep <= step_t(A)) {
         ph.k = vk;
         ph.depart = dep;
         ph.start_s = A.start_s[vk];
@@ -467,7 +469,7 @@ void launch_lane_order(const StepArgs &a, int32_t *out_vid, uint8_t *out_lane, v
 
 void launch_prep(const StepArgs &a, void *stream) {
   if (a.n_own <= 0) return;
-  k_prep<<<(a.n_own + 3) / 4, 128, 0, (cudaStream_t)stream>>>(a);
+  launch_pdl(k_prep, dim3((a.n_own + 3) / 4), dim3(128), 0, (cudaStream_t)stream, a);
 }
 
 // ---- producer warp --------------------------------------------------------------------
@@ -963,10 +965,10 @@ __device__ __noinline__ void depart(const StepArgs &A, const View &C, TileSh &T,
   if (A.lane_cnt_next) atomicAdd(&A.lane_cnt_next[g], 1);
   A.pend_head[g] = ph.h + 1;
   A.status[k] = ST_DRIVING;
-  A.insert_time[k] = A.t + 1;
+  A.insert_time[k] = step_t(A) + 1;
   if (A.record) A.r_ins[k] = 1;
   atomicAdd(&T.c_ins, 1);
-  atomicAdd(&T.c_delay, (unsigned long long)(long long)(A.t + 1 - ph.depart));
+  atomicAdd(&T.c_delay, (unsigned long long)(long long)(step_t(A) + 1 - ph.depart));
 }
 
 // Lane summaries for t+1, departures (K11; L25) and counters (a6) of
@@ -1001,7 +1003,7 @@ __device__ __forceinline__ void tile_finish(const StepArgs &A, const PState &K, 
     if (T.c_ins) {
       red_add(ta + ACC_INSERTED, T.c_ins);
       red_add(ta + ACC_SUM_DELAY, (long long)T.c_delay);
-      red_add(ta + ACC_SUM_INSERT, (long long)T.c_ins * (A.t + 1));   // insert_time = t + 1
+      red_add(ta + ACC_SUM_INSERT, (long long)T.c_ins * (step_t(A) + 1));   // insert_time = t + 1
     }
     if (T.c_lc) red_add(ta + ACC_LANE_CHANGES, T.c_lc);
     if (T.c_hand) red_add(ta + ACC_HANDOFFS, T.c_hand);
@@ -1315,6 +1317,8 @@ __global__ void __launch_bounds__(kStepThreads, KS_MINB) k_step(const __grid_con
     for (int b = 0; b <= kSkew; ++b) mbar_init(&M.rb[b], kCW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  pdl_wait();                                       // k_prep's staging (the prologue above overlaps it)
+  pdl_trigger();
   __syncthreads();
   if (tid >= kCW * 32) producer(A, M, tid & 31);
   else consumer<EXACT>(A, M, P, tid >> 5, tid & 31);
@@ -1359,8 +1363,8 @@ extern "C" int sim_debug_kstep_prof(unsigned long long *out) {
 
 namespace sim {
 
-void launch_step(const StepArgs &a, void *stream, int smem_bytes) {
-  static int resident[2] = {0, 0};                  // resident blocks per GPU, per instantiation
+static int resident[2] = {0, 0};                    // resident blocks per GPU, per instantiation
+void init_step_launch(int smem_bytes) {
   if (!resident[0]) {
     cudaFuncSetAttribute(k_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     cudaFuncSetAttribute(k_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
@@ -1372,13 +1376,17 @@ void launch_step(const StepArgs &a, void *stream, int smem_bytes) {
     resident[0] = std::max(1, b0) * std::max(1, nsm);
     resident[1] = std::max(1, b1) * std::max(1, nsm);
   }
+}
+
+void launch_step(const StepArgs &a, void *stream, int smem_bytes) {
+  init_step_launch(smem_bytes);
   if (a.n_own <= 0) return;
   const int ex = a.exact_mode ? 1 : 0;
   // enough CTAs for the work (a producer claims kGroup tiles at a time), at
   // most the resident capacity (persistent)
   const int grid = std::min((a.n_own + kGroup - 1) / kGroup, resident[ex]);
-  if (ex) k_step<true><<<grid, kStepThreads, smem_bytes, (cudaStream_t)stream>>>(a);
-  else k_step<false><<<grid, kStepThreads, smem_bytes, (cudaStream_t)stream>>>(a);
+  if (ex) launch_pdl(k_step<true>, dim3(grid), dim3(kStepThreads), smem_bytes, (cudaStream_t)stream, a);
+  else launch_pdl(k_step<false>, dim3(grid), dim3(kStepThreads), smem_bytes, (cudaStream_t)stream, a);
 }
 
 }  // namespace sim

@@ -272,8 +272,8 @@ struct First { bool found; float s, v, len; int vid; };
 static __device__ __noinline__ unsigned long long peer_summary(const StepArgs &A, int mt, int m,
                                                         const float *&pv) {
   const PeerView &Q = A.peers[__ldg(A.tile_owner + mt)];
-  pv = Q.pubv[A.t & 1];
-  return Q.summ[A.t % 3][m];
+  pv = Q.pubv[step_t(A) & 1];
+  return Q.summ[step_t(A) % 3][m];
 }
 
 // first vehicle of lane m at time t: from the tile snapshot if m is ours, else
@@ -748,7 +748,7 @@ __device__ __forceinline__ SideRes<R> lc_decide(const StepArgs &A, const TileSh 
         // U53 of Philox4x32-10(seed; vid, t) (ledger L16)
         const uint64_t sd = A.veh_seed ? A.veh_seed[me.vid] : A.seed;
         uint32_t c0 = A.rng_id ? (uint32_t)A.rng_id[me.vid] : (uint32_t)me.vid;
-        uint32_t c1 = (uint32_t)A.t, c2 = 0u, c3 = 0u;
+        uint32_t c1 = (uint32_t)step_t(A), c2 = 0u, c3 = 0u;
         uint32_t k0 = (uint32_t)(sd & 0xffffffffull), k1 = (uint32_t)(sd >> 32);
 #pragma unroll
         for (int rr = 0; rr < 10; ++rr) {

@@ -219,6 +219,13 @@ struct sim_s {
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   int64_t n_launch = 0;
+  // sim_step(n) as replays of a captured CUDA graph of kGraphSteps steps
+  // (DESIGN §3.2): the graph's kernels read the absolute step from t_dev
+  int32_t *t_dev = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  std::vector<unsigned char> g_fp;              // host state the graph was captured from
+  int64_t g_launches = 0;                       // kernels per replay
+  bool g_off = false;                           // capture unavailable on this stream
 };
 
 namespace {
@@ -1367,9 +1374,19 @@ sim_status read_group_counters(sim_s *h, std::vector<long long> &c) {
 }
 
 // One step of every partition + the exchanges.
-sim_status step_once(sim_s *h) {
+// t_base != NULL: the step is being captured into a step graph whose first
+// step is t0; its kernels read t0 from *t_base (StepArgs::t_base)
+sim_status step_once(sim_s *h, const int32_t *t_base = nullptr, int t0 = 0) {
   const int t = h->t, W = h->world;
   cudaStream_t st = h->stream;
+  auto step_args = [&](const Part &P, int tt) {
+    StepArgs a = ::step_args(P, tt);
+    if (t_base) {
+      a.t = tt - t0;
+      a.t_base = t_base;
+    }
+    return a;
+  };
   for (Part &P : h->parts) {
     if (h->P.record_decisions) {
       CK(h, cudaMemsetAsync(P.A.r_ins, 0, h->nv, st));
@@ -1605,6 +1622,7 @@ static void destroy_impl(sim_s *h) {
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   if (h->comm) g_nccl.CommDestroy(h->comm);
   for (void *q : h->ipc_opened) cudaIpcCloseMemHandle(q);
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
@@ -1854,6 +1872,85 @@ sim_status sim_create(const sim_graph *g, const sim_trips *tr, const sim_params 
   return SIM_OK;
 }
 
+// Step graphs: kGraphSteps steps captured once into a CUDA
+// graph (k_signal -> k_prep -> k_step per step, chained by programmatic
+// dependent launches) and replayed, so a long sim_step(n) costs one launch per
+// kGraphSteps steps instead of three per step.  kGraphSteps = 6 is the period
+// of the double- and triple-buffered step buffers, so the baked buffer
+// pointers are those of the replay's steps whenever it starts at the same
+// t mod 6; the absolute t comes from t_dev.  The graph is re-captured when any
+// host-side launch argument changed since the capture (fingerprint below).
+constexpr int kGraphSteps = 6;
+
+void step_fingerprint(sim_s *h, std::vector<unsigned char> &fp) {
+  fp.clear();
+  auto put = [&](const void *p, size_t n) {
+    const unsigned char *c = reinterpret_cast<const unsigned char *>(p);
+    fp.insert(fp.end(), c, c + n);
+  };
+  const int hdr[8] = {h->t % kGraphSteps, h->P.record_decisions, h->any_maxp ? 1 : 0, h->world,
+                      h->direct ? 1 : 0, h->loopback ? 1 : 0, h->smem, (int)h->parts.size()};
+  put(hdr, sizeof hdr);
+  for (const Part &P : h->parts) {
+    put(&P.A, sizeof(StepArgs));
+    put(&P.SG, sizeof(SignalArgs));
+  }
+}
+
+bool graphs_usable(sim_s *h) {
+  // not with the per-step host-side barrier (IPC) or NCCL calls, nor while
+  // per-kernel timing events are recorded
+  return !h->P.no_step_graphs && !h->g_off && !h->timing && !h->ipc && !h->comm;
+}
+
+// the graph for the current t mod 6 and host state; false: use eager steps
+sim_status ensure_graph(sim_s *h, bool *ok) {
+  *ok = false;
+  std::vector<unsigned char> fp;
+  step_fingerprint(h, fp);
+  if (h->gexec && fp == h->g_fp) { *ok = true; return SIM_OK; }
+  if (h->gexec) {
+    CK(h, cudaGraphExecDestroy(h->gexec));
+    h->gexec = nullptr;
+  }
+  if (!h->t_dev) {
+    sim_status s = dalloc(h, &h->t_dev, 1);
+    if (s) return s;
+  }
+  init_step_launch(h->smem);
+  if (cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();                             // e.g. the legacy default stream: stay eager
+    h->g_off = true;
+    return SIM_OK;
+  }
+  const int t0 = h->t;
+  const int64_t nl0 = h->n_launch;
+  sim_status s = SIM_OK;
+  for (int k = 0; k < kGraphSteps && s == SIM_OK; ++k) s = step_once(h, h->t_dev, t0);
+  cudaGraph_t g = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+  h->t = t0;
+  const int64_t per = h->n_launch - nl0;
+  h->n_launch = nl0;
+  if (s != SIM_OK || e != cudaSuccess) {
+    if (g) cudaGraphDestroy(g);
+    if (s != SIM_OK) return s;
+    h->sticky = SIM_E_CUDA;
+    return fail(h, SIM_E_CUDA, std::string("step graph capture: ") + cudaGetErrorString(e));
+  }
+  const cudaError_t ei = cudaGraphInstantiate(&h->gexec, g, 0);
+  cudaGraphDestroy(g);
+  if (ei != cudaSuccess) {
+    h->gexec = nullptr;
+    h->sticky = SIM_E_CUDA;
+    return fail(h, SIM_E_CUDA, std::string("step graph instantiate: ") + cudaGetErrorString(ei));
+  }
+  h->g_fp.swap(fp);
+  h->g_launches = per;
+  *ok = true;
+  return SIM_OK;
+}
+
 sim_status sim_step(sim_handle h, int32_t n) {
   sim_status st = check(h);
   if (st) return st;
@@ -1862,7 +1959,19 @@ sim_status sim_step(sim_handle h, int32_t n) {
     st = barrier(h);                                // the first peer write of this call
     if (st) return st;
   }
-  for (int i = 0; i < n; ++i) {
+  int i = 0;
+  if (n >= 2 * kGraphSteps && graphs_usable(h)) {
+    bool ok = false;
+    st = ensure_graph(h, &ok);
+    if (st) return st;
+    for (; ok && n - i >= kGraphSteps; i += kGraphSteps) {
+      launch_set_i32(h->t_dev, h->t, h->stream);
+      CK(h, cudaGraphLaunch(h->gexec, h->stream));
+      h->t += kGraphSteps;
+      h->n_launch += h->g_launches + 1;
+    }
+  }
+  for (; i < n; ++i) {
     st = step_once(h);
     if (st) return st;
   }

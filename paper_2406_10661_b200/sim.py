@@ -54,7 +54,7 @@ class sim_params(C.Structure):
                 ("road_owner", P), ("max_pressure_period", C.c_int32),
                 ("vehicle_seed", P), ("vehicle_rng_id", P), ("road_group", P),
                 ("n_groups", C.c_int32), ("barrier_timeout_ms", C.c_int32),
-                ("alloc", P), ("free_", P), ("alloc_ctx", P)]
+                ("alloc", P), ("free_", P), ("alloc_ctx", P), ("no_step_graphs", C.c_int32)]
 
 
 class sim_sizes(C.Structure):
@@ -175,7 +175,8 @@ def torch_allocator(device=0, stream=None):
 
 def _marshal(graph, trips, profiles, params, device=0, stream=None, exact_mode=False,
              record_decisions=False, world=1, rank=0, loopback=False, nccl_id=None,
-             road_owner=None, direct=False, barrier_timeout_ms=0, allocator=None):
+             road_owner=None, direct=False, barrier_timeout_ms=0, allocator=None,
+             step_graphs=True):
     g = {k: np.ascontiguousarray(graph[k], dtype=dt) for k, dt in _GRAPH_DT.items()}
     tr = {k: np.ascontiguousarray(trips[k], dtype=dt) for k, dt in _TRIP_DT.items()}
     prof = np.ascontiguousarray(profiles, dtype=np.float32).reshape(-1, 6)
@@ -205,7 +206,8 @@ def _marshal(graph, trips, profiles, params, device=0, stream=None, exact_mode=F
                     int(params.get("max_pressure_period", 30)),
                     *_batch_arrays(params, keep), int(barrier_timeout_ms),
                     C.cast(allocator[0], C.c_void_p) if allocator else None,
-                    C.cast(allocator[1], C.c_void_p) if allocator else None, None)
+                    C.cast(allocator[1], C.c_void_p) if allocator else None, None,
+                    int(not step_graphs))
     if allocator:
         keep.append(allocator)
     return G, T, Pm, keep
@@ -277,9 +279,11 @@ class Sim:
     def __init__(self, graph, trips, profiles, params, device=0, stream=None,
                  exact_mode=False, record_decisions=False, world=1, rank=0, loopback=False,
                  nccl_id=None, road_owner=None, direct=False, barrier_timeout_ms=0,
-                 allocator=None):
+                 allocator=None, step_graphs=True):
         """allocator: None (cudaMalloc), "torch" (PyTorch's caching allocator,
-        torch_allocator) or an (alloc, free_) pair of ALLOC_FN / FREE_FN."""
+        torch_allocator) or an (alloc, free_) pair of ALLOC_FN / FREE_FN.
+        step_graphs: sim_step(n >= 12) replays a captured 6-step CUDA graph
+        (sim_params.no_step_graphs = 0)."""
         lib = load_library()
         self.lib = lib
         if allocator == "torch":
@@ -287,7 +291,7 @@ class Sim:
         self._allocator = allocator                   # the callbacks must outlive the handle
         G, T, Pm, keep = _marshal(graph, trips, profiles, params, device, stream, exact_mode,
                                   record_decisions, world, rank, loopback, nccl_id, road_owner,
-                                  direct, barrier_timeout_ms, allocator)
+                                  direct, barrier_timeout_ms, allocator, step_graphs)
         self.n_lanes, self.n_junctions, self.n = G.n_lanes, G.n_junctions, T.n_trips
         self.n_roads = G.n_roads
         self.world, self.rank = max(1, int(world)), int(rank)
