@@ -40,13 +40,16 @@
 namespace sim {
 
 #ifndef KS_CONS_WARPS
-#define KS_CONS_WARPS 14
+#define KS_CONS_WARPS 15
 #endif
 #ifndef KS_RING_KB
-#define KS_RING_KB 208
+#define KS_RING_KB 206
 #endif
 #ifndef KS_MINB
 #define KS_MINB 1
+#endif
+#ifndef KS_PSLEEP
+#define KS_PSLEEP 64                          // producer back-off (ns) while the ring is full
 #endif
 constexpr int kCW = KS_CONS_WARPS;            // consumer warps
 constexpr int kStepThreads = (kCW + 1) * 32;  // + the producer warp (the last warp)
@@ -192,7 +195,7 @@ __device__ __forceinline__ void mbar_wait_sleep(unsigned long long *b, unsigned 
         : "r"(smem_u32(b)), "r"(parity)
         : "memory");
     if (ok) return;
-    __nanosleep(64);
+    __nanosleep(KS_PSLEEP);
   }
 }
 

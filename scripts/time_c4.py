@@ -30,7 +30,9 @@ ks, sg, nl = sim.read_timing()
 m1 = sim.read_metrics()
 vs = m1["vehicle_steps"] - m0["vehicle_steps"]
 print(f"{os.path.basename(lib)}: k_step {ks/n*1e3:.1f} us  k_signal {sg/n*1e3:.1f} us  "
-      f"veh-steps/s(kstep) {vs/(ks/1e3):.3e}  guard/step {(m1['n_guard_hits']-m0['n_guard_hits'])/n:.0f}", flush=True)
+      f"veh-steps/s(kstep) {vs/(ks/1e3):.3e}  guard/step {(m1['n_guard_hits']-m0['n_guard_hits'])/n:.0f}  "
+      f"lc/step {(m1['n_lane_changes']-m0['n_lane_changes'])/n:.0f}  handoffs/step {(m1['n_handoffs']-m0['n_handoffs'])/n:.0f}  "
+      f"driving {m1['n_driving']}", flush=True)
 import ctypes
 L = S.load_library(lib)
 pb = (ctypes.c_ulonglong * 32)()
@@ -63,7 +65,9 @@ try:
             if os.environ.get("DUMP"):
                 np.savez(os.environ["DUMP"], tc=tc)
             cyc, nv = tc[:, 0].astype(float), tc[:, 1].astype(float)
-            ok = nv > 0
+            ok = (nv > 0) & (cyc > 0)
+            if not ok.any():
+                raise AttributeError("no per-tile cycles in this build")
             print(f"  tile cycles: mean {cyc[ok].mean():.0f} median {np.median(cyc[ok]):.0f} p90 {np.percentile(cyc[ok], 90):.0f} p99 {np.percentile(cyc[ok], 99):.0f}")
             per = cyc[ok] / nv[ok]
             print(f"  cycles/vehicle: mean {per.mean():.0f} median {np.median(per):.0f} p90 {np.percentile(per, 90):.0f} p99 {np.percentile(per, 99):.0f}")
