@@ -1301,7 +1301,12 @@ __device__ __forceinline__ void consumer(const StepArgs &A, StepSmem &M, const P
 }
 
 template <bool EXACT>
-__global__ void __launch_bounds__(kStepThreads, KS_MINB) k_step(const __grid_constant__ StepArgs A) {
+#ifdef KS_MAXNREG
+#define KS_STEP_BOUNDS __maxnreg__(KS_MAXNREG)
+#else
+#define KS_STEP_BOUNDS __launch_bounds__(kStepThreads, KS_MINB)
+#endif
+__global__ void KS_STEP_BOUNDS k_step(const __grid_constant__ StepArgs A) {
   StepSmem &M = *reinterpret_cast<StepSmem *>(ks_smem);
   const int tid = threadIdx.x;
   const Prof *P = A.prof;
