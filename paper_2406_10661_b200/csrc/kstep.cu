@@ -48,6 +48,9 @@ namespace sim {
 #ifndef KS_MINB
 #define KS_MINB 1
 #endif
+#ifndef KS_ALL_GM
+#define KS_ALL_GM 0                           // experiment: every tile in global mode
+#endif
 #ifndef KS_PSLEEP
 #define KS_PSLEEP 64                          // producer back-off (ns) while the ring is full
 #endif
@@ -95,23 +98,25 @@ struct __align__(16) Hdr {          // one ring entry
 // stayer results rs1 / rv1 share pa / plim: both are written by the thread
 // that has just read a / lim of the same vehicle (pass 3, fp64 path).
 struct PState {
-  float *pa, *plim, *plimrel, *pvlim, *rs1, *rv1;
-  int *pnext1;
-  uint32_t *pfl;
-  uint8_t *kind, *pnl;                // pnl: next1 as a local junction lane (0xff none)
-  uint16_t *cand, *defl;
+  unsigned char *p;                  // base of the tile's pass state
+  int n4;                            // stride (slots, multiple of 4)
+  __device__ __forceinline__ float &pa(int i) const { return reinterpret_cast<float *>(p)[i]; }
+  __device__ __forceinline__ float &plim(int i) const { return reinterpret_cast<float *>(p)[n4 + i]; }
+  __device__ __forceinline__ float &plimrel(int i) const { return reinterpret_cast<float *>(p)[2 * n4 + i]; }
+  __device__ __forceinline__ float &pvlim(int i) const { return reinterpret_cast<float *>(p)[3 * n4 + i]; }
+  __device__ __forceinline__ float &rs1(int i) const { return pa(i); }
+  __device__ __forceinline__ float &rv1(int i) const { return plim(i); }
+  __device__ __forceinline__ int &pnext1(int i) const { return reinterpret_cast<int *>(p)[4 * n4 + i]; }
+  __device__ __forceinline__ uint32_t &pfl(int i) const { return reinterpret_cast<uint32_t *>(p)[5 * n4 + i]; }
+  __device__ __forceinline__ uint8_t &kind(int i) const { return p[24 * n4 + i]; }
+  __device__ __forceinline__ uint16_t *cand() const { return reinterpret_cast<uint16_t *>(p + 25 * n4); }
+  __device__ __forceinline__ uint16_t *defl() const { return reinterpret_cast<uint16_t *>(p + 27 * n4); }
+  __device__ __forceinline__ uint8_t &pnl(int i) const { return p[29 * n4 + i]; }
 };
 __device__ __forceinline__ PState pstate_at(unsigned char *p, int n4) {
   PState S;
-  float *f = reinterpret_cast<float *>(p);
-  S.pa = f; S.plim = f + n4; S.plimrel = f + 2 * n4; S.pvlim = f + 3 * n4;
-  S.rs1 = S.pa; S.rv1 = S.plim;
-  S.pnext1 = reinterpret_cast<int *>(f + 4 * n4);
-  S.pfl = reinterpret_cast<uint32_t *>(f + 5 * n4);
-  S.kind = reinterpret_cast<uint8_t *>(f + 6 * n4);
-  S.cand = reinterpret_cast<uint16_t *>(S.kind + n4);
-  S.defl = S.cand + n4;
-  S.pnl = reinterpret_cast<uint8_t *>(S.defl + n4);
+  S.p = p;
+  S.n4 = n4;
   return S;
 }
 
@@ -203,6 +208,11 @@ __device__ __forceinline__ void mbar_wait_sleep(unsigned long long *b, unsigned 
 #ifdef KS_PROF
 __device__ unsigned long long g_ks_prof[32];
 __device__ unsigned int g_tile_cyc[65536][4];       // per tile: cycles, vehicles, candidates, round slowest
+#ifdef KS_PROF_TILE                                 // per-tile cycles only (no per-phase probes)
+#define KP_DECL
+#define KP(idx, on) do {} while (0)
+#define KPN(idx, on, n) do {} while (0)
+#else
 #define KP_DECL long long kp_last = clock64();
 #define KP(idx, on)                                                    \
   do {                                                                 \
@@ -213,6 +223,7 @@ __device__ unsigned int g_tile_cyc[65536][4];       // per tile: cycles, vehicle
     }                                                                  \
   } while (0)
 #define KPN(idx, on, n) do { if (on) atomicAdd(&g_ks_prof[idx], (unsigned long long)(n)); } while (0)
+#endif
 #else
 #define KP_DECL
 #define KP(idx, on) do {} while (0)
@@ -549,7 +560,7 @@ __device__ __noinline__ void producer(const StepArgs &A, StepSmem &M, int lane) 
     bool gm = false;
     if (sentinel) {
       L.size = 0;
-    } else if (L.size > (uint32_t)(kRing / 2)) {     // too large for the ring: global mode
+    } else if (KS_ALL_GM || L.size > (uint32_t)(kRing / 2)) {   // too large for the ring: global mode
       gm = true;
       L = slot_layout(0, 0, dw);
     }
@@ -685,15 +696,15 @@ __device__ __forceinline__ void settle(const StepArgs &A, const PState &K, const
   const int l = m_lane(C.meta(i));
   if (r.fin) {
     emit_moved(A, C, i, r, 3, T);
-    K.kind[i] = 3;
+    K.kind(i) = 3;
   } else if (r.lc == 0 && r.hand == 0 && r.lane_g == T.glob[l]) {
-    K.rs1[i] = r.s1;
-    K.rv1[i] = r.v1;
+    K.rs1(i) = r.s1;
+    K.rv1(i) = r.v1;
     C.wait(i) = r.wait1;
-    K.kind[i] = 1;
+    K.kind(i) = 1;
   } else {
     emit_moved(A, C, i, r, 2, T);
-    K.kind[i] = 2;
+    K.kind(i) = 2;
   }
 }
 
@@ -731,13 +742,13 @@ __device__ __forceinline__ void pass1(const StepArgs &A, const PState &K, const 
     A.r_hops[me.vid] = (int8_t)use.hops;
     A.r_phantom[me.vid] = (int8_t)use.phantom;
   }
-  K.pa[i] = use.a;
-  K.plim[i] = use.lim;
-  K.plimrel[i] = use.limrel;
-  K.pvlim[i] = use.vlim;
-  K.pnext1[i] = use.next1;
-  K.pnl[i] = (uint8_t)(use.nl1 < 0 ? 0xff : use.nl1);
-  K.pfl[i] = (use.has_lim ? F_LIM : 0u) | (g.hit ? F_HIT : 0u) | (E.inG ? F_ING : 0u) |
+  K.pa(i) = use.a;
+  K.plim(i) = use.lim;
+  K.plimrel(i) = use.limrel;
+  K.pvlim(i) = use.vlim;
+  K.pnext1(i) = use.next1;
+  K.pnl(i) = (uint8_t)(use.nl1 < 0 ? 0xff : use.nl1);
+  K.pfl(i) = (use.has_lim ? F_LIM : 0u) | (g.hit ? F_HIT : 0u) | (E.inG ? F_ING : 0u) |
              (E.want0 ? F_W0 : 0u) | (E.want1 ? F_W1 : 0u) | ((uint32_t)(E.mand + 1) << F_MAND_SH) |
              ((uint32_t)(me.k + 1) << F_K_SH) | ((uint32_t)l << F_NL_SH) | (1u << F_LC_SH);
 }
@@ -747,7 +758,7 @@ __device__ __forceinline__ void pass2(const StepArgs &A, const PState &K, const 
                                       const TileSh &T) {
   const uint32_t meta = C.meta(i);
   const int l = m_lane(meta);
-  const uint32_t fl = K.pfl[i];
+  const uint32_t fl = K.pfl(i);
   Me me;
   me.vid = C.vid(i);
   me.cur = m_cursor(meta);
@@ -766,19 +777,19 @@ __device__ __forceinline__ void pass2(const StepArgs &A, const PState &K, const 
   E.want1 = (fl & F_W1) != 0;
   Guard g;
   g.hit = false;
-  const SideRes<float> sr = lc_decide<float, kGuard>(A, T, C, i, l, s, v, p, me, E, K.pa[i], g);
+  const SideRes<float> sr = lc_decide<float, kGuard>(A, T, C, i, l, s, v, p, me, E, K.pa(i), g);
   if (g.hit) {
-    K.pfl[i] = fl | F_HIT;
+    K.pfl(i) = fl | F_HIT;
   } else if (sr.choice >= 0) {
-    K.pa[i] = sr.a;
-    K.plim[i] = sr.lim;
-    K.plimrel[i] = sr.limrel;
-    K.pvlim[i] = sr.vlim;
-    K.pnext1[i] = sr.next1;
-    K.pnl[i] = (uint8_t)(sr.nl1 < 0 ? 0xff : sr.nl1);
+    K.pa(i) = sr.a;
+    K.plim(i) = sr.lim;
+    K.plimrel(i) = sr.limrel;
+    K.pvlim(i) = sr.vlim;
+    K.pnext1(i) = sr.next1;
+    K.pnl(i) = (uint8_t)(sr.nl1 < 0 ? 0xff : sr.nl1);
     const int nl = sr.choice == 0 ? E.sl0 : E.sl1;
     const int lc = sr.choice == 0 ? -1 : 1;
-    K.pfl[i] = (fl & ~(F_LIM | (0xffu << F_NL_SH) | (3u << F_LC_SH))) | (sr.has_lim ? F_LIM : 0u) |
+    K.pfl(i) = (fl & ~(F_LIM | (0xffu << F_NL_SH) | (3u << F_LC_SH))) | (sr.has_lim ? F_LIM : 0u) |
                ((uint32_t)nl << F_NL_SH) | ((uint32_t)(lc + 1) << F_LC_SH);
   }
 }
@@ -786,7 +797,7 @@ __device__ __forceinline__ void pass2(const StepArgs &A, const PState &K, const 
 // pass 3: O8-O9 (fp32).  Returns false if the vehicle must be recomputed.
 __device__ __forceinline__ bool pass3(const StepArgs &A, const PState &K, const View &C, int i,
                                       TileSh &T) {
-  const uint32_t fl = K.pfl[i];
+  const uint32_t fl = K.pfl(i);
   if (fl & F_HIT) return false;
   const uint32_t meta = C.meta(i);
   Me me;
@@ -797,12 +808,12 @@ __device__ __forceinline__ bool pass3(const StepArgs &A, const PState &K, const 
   me.ends = C.ends(i);
   me.k = -1;
   LEv<float> use;
-  use.a = K.pa[i];
-  use.lim = K.plim[i];
-  use.limrel = K.plimrel[i];
-  use.vlim = K.pvlim[i];
-  use.next1 = K.pnext1[i];
-  use.nl1 = K.pnl[i] == 0xff ? -1 : (int)K.pnl[i];
+  use.a = K.pa(i);
+  use.lim = K.plim(i);
+  use.limrel = K.plimrel(i);
+  use.vlim = K.pvlim(i);
+  use.next1 = K.pnext1(i);
+  use.nl1 = K.pnl(i) == 0xff ? -1 : (int)K.pnl(i);
   use.has_lim = (fl & F_LIM) != 0;
   const int new_l = (int)((fl >> F_NL_SH) & 0xffu);
   const int lc = (int)((fl >> F_LC_SH) & 3u) - 1;
@@ -840,6 +851,27 @@ __device__ __forceinline__ void run_passes(const StepArgs &A, const PState &K, c
                                            TileSh &T, int n, int lane) {
   KP_DECL
   int nd = 0;
+#ifdef KS_MONO
+  if constexpr (!EXACT) {                            // experiment: one fused per-vehicle pass
+    for (int q0 = 0; q0 < n; q0 += 32) {
+      const int q = q0 + lane;
+      bool def = false;
+      if (q < n) {
+        Res r;
+        Guard g;
+        g.hit = false;
+        veh_update<float, kGuard>(A, T, C, q, r, g);
+        if (g.hit) def = true;
+        else {
+          if (A.record) record(A, C.vid(q), r, false);
+          settle(A, K, C, q, r, T);
+        }
+      }
+      nd = push_list(def, K.defl(), nd, q, lane);
+    }
+    __syncwarp();
+  } else
+#endif
   if constexpr (!EXACT) {
     int nc = 0;
     for (int q0 = 0; q0 < n; q0 += 32) {             // pass 1 (every vehicle)
@@ -847,31 +879,31 @@ __device__ __forceinline__ void run_passes(const StepArgs &A, const PState &K, c
       bool cand = false;
       if (q < n) {
         pass1(A, K, C, q, T);
-        const uint32_t fl = K.pfl[q];
+        const uint32_t fl = K.pfl(q);
         cand = !(fl & F_HIT) && ((fl & (F_W0 | F_W1)) || (A.record && T.isroad[m_lane(C.meta(q))]));
       }
-      nc = push_list(cand, K.cand, nc, q, lane);
+      nc = push_list(cand, K.cand(), nc, q, lane);
     }
     __syncwarp();
     KP(25, lane == 0);
-    for (int q = lane; q < nc; q += 32) pass2(A, K, C, K.cand[q], T);   // pass 2 (compacted)
+    for (int q = lane; q < nc; q += 32) pass2(A, K, C, K.cand()[q], T);   // pass 2 (compacted)
     __syncwarp();
     KP(26, lane == 0);
     for (int q0 = 0; q0 < n; q0 += 32) {             // pass 3 (every vehicle)
       const int q = q0 + lane;
       bool def = false;
       if (q < n) def = !pass3(A, K, C, q, T);
-      nd = push_list(def, K.defl, nd, q, lane);
+      nd = push_list(def, K.defl(), nd, q, lane);
     }
     __syncwarp();
     KP(27, lane == 0);
   } else {
-    for (int q = lane; q < n; q += 32) K.defl[q] = (uint16_t)q;
+    for (int q = lane; q < n; q += 32) K.defl()[q] = (uint16_t)q;
     nd = n;
     __syncwarp();
   }
   for (int q = lane; q < nd; q += 32) {              // fp64 canonical path
-    pass_fp64(A, K, C, K.defl[q], T);
+    pass_fp64(A, K, C, K.defl()[q], T);
     if (!EXACT) atomicAdd(&T.c_guard, 1);
   }
   __syncwarp();
@@ -888,7 +920,7 @@ __device__ __forceinline__ void compact(const StepArgs &A, const PState &K, cons
   int cnt = 0;
   for (int i0 = 0; i0 < n; i0 += 32) {
     const int i = i0 + lane_id;
-    cnt += __popc(__ballot_sync(0xffffffffu, i < n && K.kind[i] == 1));
+    cnt += __popc(__ballot_sync(0xffffffffu, i < n && K.kind(i) == 1));
   }
   if (cnt > T.cap) {                                // slab capacity exceeded: sticky SIM_E_CAPACITY
     if (lane_id == 0) atomicAdd(&T.c_ovf, cnt - T.cap);
@@ -898,15 +930,15 @@ __device__ __forceinline__ void compact(const StepArgs &A, const PState &K, cons
   int run = 0;
   for (int i0 = 0; i0 < n; i0 += 32) {
     const int i = i0 + lane_id;
-    const bool st = i < n && K.kind[i] == 1;
+    const bool st = i < n && K.kind(i) == 1;
     const unsigned ball = __ballot_sync(0xffffffffu, st);
     if (st) {
       const int rank = run + __popc(ball & ((1u << lane_id) - 1u));
       if (rank < cnt) {
         const uint32_t meta = C.meta(i);
         InboxRec r;
-        r.s = K.rs1[i];
-        r.v = K.rv1[i];
+        r.s = K.rs1(i);
+        r.v = K.rv1(i);
         r.vid = C.vid(i);
         r.nxt = C.nxt(i);
         r.nxt2 = C.nxt2(i);
@@ -986,8 +1018,8 @@ __device__ __forceinline__ void tile_finish(const StepArgs &A, const PState &K, 
     if (fo != 0x7fffffff) {
       const int rank = fo >> 15, idx = fo & 0x7fff;
       const int vid = C.vid(idx);
-      atomicMin(&A.summ_next[g], vkey(K.rs1[idx], vid));
-      A.pubv_next[vid] = K.rv1[idx];
+      atomicMin(&A.summ_next[g], vkey(K.rs1(idx), vid));
+      A.pubv_next[vid] = K.rv1(idx);
       if (A.lane_cnt_next) {                          // stayers of lane l: [rank, next lane's first)
         int end = run;
         for (int q = l + 1; q < nl; ++q)
@@ -1135,7 +1167,7 @@ __device__ __forceinline__ void run_tile(const StepArgs &A, StepSmem &M, const H
   __syncwarp();
   KP(24, lane == 0);
   run_passes<EXACT>(A, K, C, T, n, lane);
-#ifdef KS_PROF
+#if defined(KS_PROF) && !defined(KS_PROF_TILE)
   kp_last = clock64();
 #endif
   compact(A, K, C, T, n, lane);
