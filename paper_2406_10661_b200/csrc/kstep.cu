@@ -48,9 +48,6 @@ namespace sim {
 #ifndef KS_MINB
 #define KS_MINB 1
 #endif
-#ifndef KS_ALL_GM
-#define KS_ALL_GM 0                           // experiment: every tile in global mode
-#endif
 #ifndef KS_PSLEEP
 #define KS_PSLEEP 64                          // producer back-off (ns) while the ring is full
 #endif
@@ -120,14 +117,8 @@ __device__ __forceinline__ PState pstate_at(unsigned char *p, int n4) {
   return S;
 }
 
-#ifdef KS_SKEW
-constexpr int kSkew = KS_SKEW;                // rounds a consumer warp may run ahead
-#else
-constexpr int kSkew = 0;
-#endif
 struct __align__(128) StepSmem {
   Hdr H[kNH];
-  unsigned long long rb[kSkew + 1];             // round barriers (KS_SKEW builds)
   int next_seq;
   __align__(16) Prof prof[kSmemProf];
   TileSh T[kCW];
@@ -560,7 +551,7 @@ __device__ __noinline__ void producer(const StepArgs &A, StepSmem &M, int lane) 
     bool gm = false;
     if (sentinel) {
       L.size = 0;
-    } else if (KS_ALL_GM || L.size > (uint32_t)(kRing / 2)) {   // too large for the ring: global mode
+    } else if (L.size > (uint32_t)(kRing / 2)) {     // too large for the ring: global mode
       gm = true;
       L = slot_layout(0, 0, dw);
     }
@@ -851,27 +842,6 @@ __device__ __forceinline__ void run_passes(const StepArgs &A, const PState &K, c
                                            TileSh &T, int n, int lane) {
   KP_DECL
   int nd = 0;
-#ifdef KS_MONO
-  if constexpr (!EXACT) {                            // experiment: one fused per-vehicle pass
-    for (int q0 = 0; q0 < n; q0 += 32) {
-      const int q = q0 + lane;
-      bool def = false;
-      if (q < n) {
-        Res r;
-        Guard g;
-        g.hit = false;
-        veh_update<float, kGuard>(A, T, C, q, r, g);
-        if (g.hit) def = true;
-        else {
-          if (A.record) record(A, C.vid(q), r, false);
-          settle(A, K, C, q, r, T);
-        }
-      }
-      nd = push_list(def, K.defl(), nd, q, lane);
-    }
-    __syncwarp();
-  } else
-#endif
   if constexpr (!EXACT) {
     int nc = 0;
     for (int q0 = 0; q0 < n; q0 += 32) {             // pass 1 (every vehicle)
@@ -1184,18 +1154,12 @@ __device__ __noinline__ void run_tile_gm(const StepArgs &A, StepSmem &M, const H
   run_tile<EXACT, true>(A, M, H, T, P, lane);
 }
 
-// Named barrier of a group of consumer warps with a count of the threads
-// whose predicate is true (bar.red.popc); barrier id 1 + group.
-#ifndef KS_GROUPS
-#define KS_GROUPS 1
-#endif
-constexpr int kGroups = KS_GROUPS;                  // consumer warp groups with their own rounds
-static_assert(kCW % kGroups == 0, "equal groups");
-constexpr int kGW = kCW / kGroups;                  // warps per group
-__device__ __forceinline__ int cons_bar_count(bool pred, int group) {
+// Named barrier 1 of the consumer warps (the producer never joins it), with
+// the number of consumer threads whose predicate is true (bar.red.popc).
+__device__ __forceinline__ int cons_bar_count(bool pred) {
   int r;
-  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\tbar.red.popc.u32 %0, %1, %2, p;\n\t}"
-               : "=r"(r) : "r"(1 + group), "r"(kGW * 32), "r"((int)pred) : "memory");
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\tbar.red.popc.u32 %0, 1, %1, p;\n\t}"
+               : "=r"(r) : "r"(kCW * 32), "r"((int)pred) : "memory");
   return r;
 }
 
@@ -1204,47 +1168,15 @@ __device__ __forceinline__ int cons_bar_count(bool pred, int group) {
 // warp has finished its tile.  Tiles come in LPT order, so the tiles of a
 // round are of similar size, and the warps run the same pass of the model at
 // about the same time: the instruction cache then holds one pass rather than
-// all of them (ncu: icc hit rate 68% free-running, 94% in rounds; 426 -> 364
-// us on C4).  Warps that met the end-of-work sentinel keep joining the
-// barrier until all have.
+// all of them (ncu: free-running warps lose 44% of their samples to "no
+// instruction"; rounds are worth ~25%, which lists the measured
+// alternatives — skew, several tiles per round, cooperative rounds).  Warps
+// that met the end-of-work sentinel keep joining the barrier until all have.
 template <bool EXACT>
 __device__ __forceinline__ void consumer(const StepArgs &A, StepSmem &M, const Prof *P, int warp,
                                          int lane) {
   TileSh &T = M.T[warp];
   KP_DECL
-#ifdef KS_SKEW
-  // bounded skew: round r starts once round r - 1 - kSkew is complete (every
-  // warp arrived on rb[(r - 1 - kSkew) % (kSkew + 1)]); a warp that meets the
-  // sentinel at round r arrives for r and leaves (no warp waits for a later
-  // round: all tiles are claimed)
-  for (int r = 0;; ++r) {
-    const int rw = r - 1 - kSkew;
-    if (rw >= 0) mbar_wait(&M.rb[rw % (kSkew + 1)], (unsigned)(rw / (kSkew + 1)) & 1u);
-    KP(11, lane == 0);
-    int seq = 0;
-    if (lane == 0) seq = atomicAdd(&M.next_seq, 1);
-    seq = __shfl_sync(0xffffffffu, seq, 0);
-    Hdr &H = M.H[seq % kNH];
-    KP(9, lane == 0);
-    mbar_wait(&H.full, (unsigned)(seq / kNH) & 1u);
-    KP(8, lane == 0);
-    const bool done = H.done;
-    if (!done) {
-      if (H.gm) run_tile_gm<EXACT>(A, M, H, T, P, lane);
-      else run_tile<EXACT, false>(A, M, H, T, P, lane);
-      KP(10, lane == 0);
-      KPN(20, lane == 0, 1);
-      if (lane == 0) mbar_arrive(&H.empty);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&M.rb[r % (kSkew + 1)]);
-    if (done) return;
-  }
-#endif
-#ifndef KS_FREERUN
-#ifndef KS_ROUND_TILES
-#define KS_ROUND_TILES 1
-#endif
   bool done = false;
 #ifdef KS_PROF
   __shared__ unsigned long long rt_cyc[kCW];
@@ -1255,8 +1187,7 @@ __device__ __forceinline__ void consumer(const StepArgs &A, StepSmem &M, const P
     long long rt0 = clock64();
     if (lane == 0) { rt_cyc[warp] = 0; rt_n[warp] = 0; }
 #endif
-#pragma unroll 1
-    for (int rt = 0; rt < KS_ROUND_TILES && !done; ++rt) {
+    if (!done) {
       int seq = 0;
       if (lane == 0) seq = atomicAdd(&M.next_seq, 1);
       seq = __shfl_sync(0xffffffffu, seq, 0);
@@ -1288,47 +1219,30 @@ __device__ __forceinline__ void consumer(const StepArgs &A, StepSmem &M, const P
         if (lane == 0) mbar_arrive(&H.empty);       // the slot can be reused
       }
     }
-    const int nd = cons_bar_count(done, warp / kGW);
+    const int nd = cons_bar_count(done);
     KP(11, lane == 0);
 #ifdef KS_PROF
-    if (warp == 0 && lane == 0) {
-      unsigned long long mx = 0, sm = 0; int nmx = 0, nmin = 1 << 30, cnt = 0;
+    if (warp == 0 && lane == 0) {                   // round imbalance (dev builds)
+      unsigned long long mx = 0, sm = 0;
+      int nmx = 0, cnt = 0, nmean = 0;
       for (int w = 0; w < kCW; ++w) {
         if (rt_cyc[w] == 0) continue;
-        cnt++; sm += rt_cyc[w];
+        cnt++;
+        sm += rt_cyc[w];
+        nmean += rt_n[w];
         if (rt_cyc[w] > mx) { mx = rt_cyc[w]; nmx = rt_n[w]; }
-        nmin = min(nmin, rt_n[w]);
       }
       if (cnt == kCW) {
         atomicAdd(&g_ks_prof[12], mx);
         atomicAdd(&g_ks_prof[13], sm / kCW);
         atomicAdd(&g_ks_prof[14], 1ull);
-        int nmean = 0; for (int w = 0; w < kCW; ++w) nmean += rt_n[w];
         atomicAdd(&g_ks_prof[15], (unsigned long long)nmx);
         atomicAdd(&g_ks_prof[16], (unsigned long long)(nmean / kCW));
       }
     }
-    cons_bar_count(false, warp / kGW);
+    cons_bar_count(false);
 #endif
-    if (nd == kGW * 32) break;
-  }
-  return;
-#endif
-  for (;;) {
-    int seq = 0;
-    if (lane == 0) seq = atomicAdd(&M.next_seq, 1);
-    seq = __shfl_sync(0xffffffffu, seq, 0);
-    Hdr &H = M.H[seq % kNH];
-    KP(9, lane == 0);
-    mbar_wait(&H.full, (unsigned)(seq / kNH) & 1u);
-    KP(8, lane == 0);
-    if (H.done) break;
-    if (H.gm) run_tile_gm<EXACT>(A, M, H, T, P, lane);
-    else run_tile<EXACT, false>(A, M, H, T, P, lane);
-    KP(10, lane == 0);
-    KPN(20, lane == 0, 1);
-    KPN(21, lane == 0, H.gm);
-    if (lane == 0) mbar_arrive(&H.empty);           // the slot can be reused
+    if (nd == kCW * 32) break;
   }
 }
 
@@ -1354,7 +1268,6 @@ __global__ void KS_STEP_BOUNDS k_step(const __grid_constant__ StepArgs A) {
       mbar_init(&M.H[e].empty, 1);
     }
     M.next_seq = 0;
-    for (int b = 0; b <= kSkew; ++b) mbar_init(&M.rb[b], kCW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   pdl_wait();                                       // k_prep's staging (the prologue above overlaps it)
