@@ -307,12 +307,12 @@ __device__ __noinline__ void emit_moved(const StepArgs &A, const View &C, int i,
   if (r.hand) atomicAdd(&T.c_hand, r.hand);
   if (kind == 3) {
     A.status[vid] = ST_FINISHED;
-    A.arrive_time[vid] = step_t(A) + 1;
+    A.arrive_time[vid] = T.t + 1;
     A.wait_fin[vid] = r.wait1;
     atomicAdd(&T.c_fin, 1);
     long long *ta = A.tacc + (size_t)T.tile * kNAcc;
     const int ins = A.insert_time[vid];
-    red_add(ta + ACC_SUM_TRAVEL, (long long)(step_t(A) + 1 - ins));
+    red_add(ta + ACC_SUM_TRAVEL, (long long)(T.t + 1 - ins));
     red_add(ta + ACC_SUM_INSERT, -(long long)ins);
     red_add(ta + ACC_SUM_WAIT_FIN, (long long)r.wait1);
     return;
@@ -970,10 +970,10 @@ __device__ __noinline__ void depart(const StepArgs &A, const View &C, TileSh &T,
   if (A.lane_cnt_next) atomicAdd(&A.lane_cnt_next[g], 1);
   A.pend_head[g] = ph.h + 1;
   A.status[k] = ST_DRIVING;
-  A.insert_time[k] = step_t(A) + 1;
+  A.insert_time[k] = T.t + 1;
   if (A.record) A.r_ins[k] = 1;
   atomicAdd(&T.c_ins, 1);
-  atomicAdd(&T.c_delay, (unsigned long long)(long long)(step_t(A) + 1 - ph.depart));
+  atomicAdd(&T.c_delay, (unsigned long long)(long long)(T.t + 1 - ph.depart));
 }
 
 // Lane summaries for t+1, departures (K11; L25) and counters (a6) of
@@ -1008,7 +1008,7 @@ __device__ __forceinline__ void tile_finish(const StepArgs &A, const PState &K, 
     if (T.c_ins) {
       red_add(ta + ACC_INSERTED, T.c_ins);
       red_add(ta + ACC_SUM_DELAY, (long long)T.c_delay);
-      red_add(ta + ACC_SUM_INSERT, (long long)T.c_ins * (step_t(A) + 1));   // insert_time = t + 1
+      red_add(ta + ACC_SUM_INSERT, (long long)T.c_ins * (T.t + 1));   // insert_time = t + 1
     }
     if (T.c_lc) red_add(ta + ACC_LANE_CHANGES, T.c_lc);
     if (T.c_hand) red_add(ta + ACC_HANDOFFS, T.c_hand);
@@ -1032,6 +1032,7 @@ __device__ __forceinline__ void run_tile(const StepArgs &A, StepSmem &M, const H
   const SlotLayout L = GM ? slot_layout(0, 0, H.dw) : slot_layout(ns, ni, H.dw);
   unsigned char *slot = M.ring + H.off;
   const int *W = reinterpret_cast<const int *>(slot + L.desc);
+  if (lane == 0) T.t = step_t(A);                   // tile_setup ends with __syncwarp
   tile_setup(H, W, reinterpret_cast<const ExtFirst *>(W + H.dwd),
              reinterpret_cast<const PendHead *>(W + H.dwd + kExtWords * (H.nl - H.nroad)), P, T, lane);
   KP(22, lane == 0);

@@ -94,6 +94,7 @@ extern __shared__ __align__(128) unsigned char ks_smem[];
 struct TileSh {
   int nl, nroad, tile, base, ibase, cap, icap;
   int snap0, n;                      // snapshot range [snap0, snap0 + n) of the tile's vehicles
+  int t;                             // the step (step_t(A), read once per tile)
   const Prof *P;                     // profile table (shared-memory copy when small)
   const ExtFirst *ext;               // [nl - nroad]: first vehicle of each junction lane's exit lane
   const PendHead *pend;              // [nroad]: heads of the pending-departure queues
@@ -748,7 +749,7 @@ __device__ __forceinline__ SideRes<R> lc_decide(const StepArgs &A, const TileSh 
         // U53 of Philox4x32-10(seed; vid, t) (ledger L16)
         const uint64_t sd = A.veh_seed ? A.veh_seed[me.vid] : A.seed;
         uint32_t c0 = A.rng_id ? (uint32_t)A.rng_id[me.vid] : (uint32_t)me.vid;
-        uint32_t c1 = (uint32_t)step_t(A), c2 = 0u, c3 = 0u;
+        uint32_t c1 = (uint32_t)T.t, c2 = 0u, c3 = 0u;
         uint32_t k0 = (uint32_t)(sd & 0xffffffffull), k1 = (uint32_t)(sd >> 32);
 #pragma unroll
         for (int rr = 0; rr < 10; ++rr) {

@@ -18,11 +18,17 @@ scen = synth.city()                       # (not the npz cache: the partitioner 
 W = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 own = synth.rcb_partition(scen, W)
 out = {"workload": "C4", "partitions": W}
-for name, kw in (("single", {}), ("copy", dict(world=W, loopback=True, road_owner=own)),
-                 ("direct", dict(world=W, loopback=True, direct=True, road_owner=own))):
+PRE = int(os.environ.get("PREROLL", "200"))
+out["preroll_steps"] = PRE
+out["note"] = "sim_step(40) timed with CUDA events: step graphs (6 steps per replay, PDL) unless *_eager"
+for name, kw in (("single", {}), ("single_eager", dict(step_graphs=False)),
+                 ("copy", dict(world=W, loopback=True, road_owner=own)),
+                 ("direct", dict(world=W, loopback=True, direct=True, road_owner=own)),
+                 ("direct_eager", dict(world=W, loopback=True, direct=True, road_owner=own,
+                                       step_graphs=False))):
     st = torch.cuda.Stream()
     sim = p.Sim.from_scenario(scen, stream=st.cuda_stream, **kw)
-    sim.step(10)
+    sim.step(PRE)
     sim.sync()
     m0 = sim.read_metrics()
     n = 40

@@ -33,6 +33,16 @@ print(f"{os.path.basename(lib)}: k_step {ks/n*1e3:.1f} us  k_signal {sg/n*1e3:.1
       f"veh-steps/s(kstep) {vs/(ks/1e3):.3e}  guard/step {(m1['n_guard_hits']-m0['n_guard_hits'])/n:.0f}  "
       f"lc/step {(m1['n_lane_changes']-m0['n_lane_changes'])/n:.0f}  handoffs/step {(m1['n_handoffs']-m0['n_handoffs'])/n:.0f}  "
       f"driving {m1['n_driving']}", flush=True)
+# sim_step(36): step graphs (6 steps per replay) with PDL, no flush between steps
+sim.enable_timing(False)
+with torch.cuda.stream(st):
+    sim.step(36)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    sim.step(72)
+    e1.record(st)
+torch.cuda.synchronize()
+print(f"  sim_step(72) (graphs): {e0.elapsed_time(e1) / 72 * 1e3:.1f} us per step", flush=True)
 import ctypes
 L = S.load_library(lib)
 pb = (ctypes.c_ulonglong * 32)()
@@ -64,6 +74,12 @@ try:
             tc = tc.reshape(-1, 4)[:scen.graph["road_lane_offsets"].shape[0] - 1]
             if os.environ.get("DUMP"):
                 np.savez(os.environ["DUMP"], tc=tc)
+                # a later step's per-tile cycles too (is the per-tile cost persistent?)
+                sim.step(int(os.environ.get("DUMP_GAP", "1")))
+                tc2 = np.zeros(65536 * 4, np.uint32)
+                L.sim_debug_tile_cycles(tc2.ctypes.data_as(ctypes.c_void_p))
+                np.savez(os.environ["DUMP"].replace(".npz", "_next.npz"),
+                         tc=tc2.reshape(-1, 4)[:scen.graph["road_lane_offsets"].shape[0] - 1])
             cyc, nv = tc[:, 0].astype(float), tc[:, 1].astype(float)
             ok = (nv > 0) & (cyc > 0)
             if not ok.any():
