@@ -682,7 +682,8 @@ __device__ __forceinline__ void tile_setup(const Hdr &H, const int *W, const Ext
 // the vehicle at snapshot slot i has been updated (fp32 path or fp64
 // canonical path): stayer results stay in the pass state for the in-order
 // compaction, movers and arrivals leave now
-__device__ __forceinline__ void settle(const StepArgs &A, const PState &K, const View &C, int i,
+template <class PS>
+__device__ __forceinline__ void settle(const StepArgs &A, const PS &K, const View &C, int i,
                                        const Res &r, TileSh &T) {
   const int l = m_lane(C.meta(i));
   if (r.fin) {
@@ -819,7 +820,8 @@ __device__ __forceinline__ bool pass3(const StepArgs &A, const PState &K, const 
 }
 
 // the fp64 canonical recomputation of one vehicle
-__device__ __noinline__ void pass_fp64(const StepArgs &A, const PState &K, const View &C, int i,
+template <class PS>
+__device__ __noinline__ void pass_fp64(const StepArgs &A, const PS &K, const View &C, int i,
                                        TileSh &T) {
   Res r;
   Guard g;
@@ -885,7 +887,8 @@ __device__ __forceinline__ void run_passes(const StepArgs &A, const PState &K, c
 // contiguous range): the stayer count first, then each stayer
 // to base + cap - count + rank as one 32-B record (coalesced); the first
 // stayer of each lane is remembered for the t+1 summary.
-__device__ __forceinline__ void compact(const StepArgs &A, const PState &K, const View &C, TileSh &T,
+template <class PS>
+__device__ __forceinline__ void compact(const StepArgs &A, const PS &K, const View &C, TileSh &T,
                                         int n, int lane_id) {
   int cnt = 0;
   for (int i0 = 0; i0 < n; i0 += 32) {
@@ -978,7 +981,8 @@ __device__ __noinline__ void depart(const StepArgs &A, const View &C, TileSh &T,
 
 // Lane summaries for t+1, departures (K11; L25) and counters (a6) of
 // the tile, after all its vehicles are settled.
-__device__ __forceinline__ void tile_finish(const StepArgs &A, const PState &K, const View &C,
+template <class PS>
+__device__ __forceinline__ void tile_finish(const StepArgs &A, const PS &K, const View &C,
                                             TileSh &T, int lane_id) {
   const int nl = T.nl, nroad = T.nroad, tile = T.tile;
   const int run = T.run < T.cap ? T.run : T.cap;
@@ -1025,12 +1029,11 @@ __device__ __forceinline__ void tile_finish(const StepArgs &A, const PState &K, 
 // common one every snapshot / pass-state access is provably to shared memory
 // (LDS/STS instead of generic loads).
 template <bool EXACT, bool GM>
-__device__ __forceinline__ void run_tile(const StepArgs &A, StepSmem &M, const Hdr &H, TileSh &T,
+__device__ __forceinline__ void run_tile(const StepArgs &A, unsigned char *slot, const Hdr &H, TileSh &T,
                                          const Prof *P, int lane) {
   KP_DECL
   const int ns = H.n_st, ni = H.n_in, n = ns + ni;
   const SlotLayout L = GM ? slot_layout(0, 0, H.dw) : slot_layout(ns, ni, H.dw);
-  unsigned char *slot = M.ring + H.off;
   const int *W = reinterpret_cast<const int *>(slot + L.desc);
   if (lane == 0) T.t = step_t(A);                   // tile_setup ends with __syncwarp
   tile_setup(H, W, reinterpret_cast<const ExtFirst *>(W + H.dwd),
@@ -1150,9 +1153,9 @@ __device__ __forceinline__ void run_tile(const StepArgs &A, StepSmem &M, const H
 // global-mode tiles (rare), out of line so their copy of the passes stays out
 // of the hot code
 template <bool EXACT>
-__device__ __noinline__ void run_tile_gm(const StepArgs &A, StepSmem &M, const Hdr &H, TileSh &T,
+__device__ __noinline__ void run_tile_gm(const StepArgs &A, unsigned char *slot, const Hdr &H, TileSh &T,
                                          const Prof *P, int lane) {
-  run_tile<EXACT, true>(A, M, H, T, P, lane);
+  run_tile<EXACT, true>(A, slot, H, T, P, lane);
 }
 
 // Named barrier 1 of the consumer warps (the producer never joins it), with
@@ -1202,8 +1205,8 @@ __device__ __forceinline__ void consumer(const StepArgs &A, StepSmem &M, const P
 #ifdef KS_PROF
         const long long t0 = clock64();
 #endif
-        if (H.gm) run_tile_gm<EXACT>(A, M, H, T, P, lane);
-        else run_tile<EXACT, false>(A, M, H, T, P, lane);
+        if (H.gm) run_tile_gm<EXACT>(A, M.ring + H.off, H, T, P, lane);
+        else run_tile<EXACT, false>(A, M.ring + H.off, H, T, P, lane);
 #ifdef KS_PROF
         if (lane == 0 && H.tile < 65536) {
           g_tile_cyc[H.tile][0] = (unsigned)(clock64() - t0);
@@ -1286,7 +1289,209 @@ __global__ void KS_STEP_BOUNDS k_step(const __grid_constant__ StepArgs A) {
   }
 }
 
-int step_smem_bytes() { return (int)sizeof(StepSmem); }
+// ---- warp-autonomous step kernel (KS_WARP builds) ---------------------
+// The round-1 execution model on this round's data layout and model code: one
+// warp per CTA, many CTAs per SM, no producer, no rounds.  Each warp claims a
+// tile, bulk-copies its block (descriptor + k_prep staging) into its own
+// shared area, merges the tile's records from global memory into a shared
+// snapshot, runs the fused per-vehicle update (veh_update: O4-O9 in one pass)
+// and the fp64 recomputation of guard hits, compacts and finishes the tile.
+// Tiles whose snapshot does not fit the area run in global mode.
+#ifndef KW_BLOCKS
+#define KW_BLOCKS 16
+#endif
+constexpr int kWB = KW_BLOCKS;                       // one-warp CTAs per SM
+// pass state of the fused path: the stayer results and the fp64 list only
+struct PStateM {
+  unsigned char *p;
+  int n4;
+  __device__ __forceinline__ float &rs1(int i) const { return reinterpret_cast<float *>(p)[i]; }
+  __device__ __forceinline__ float &rv1(int i) const { return reinterpret_cast<float *>(p)[n4 + i]; }
+  __device__ __forceinline__ uint8_t &kind(int i) const { return p[8 * n4 + i]; }
+  __device__ __forceinline__ uint16_t *defl() const { return reinterpret_cast<uint16_t *>(p + 9 * n4); }
+};
+struct WHead {
+  unsigned long long bar;                           // the block copy's mbarrier
+  Hdr H;
+  TileSh T;
+};
+constexpr int kWBlockSmem = (228 * 1024) / kWB - 1024;   // per CTA (1 KB reserved per CTA)
+constexpr int kWHead = ((int)sizeof(WHead) + 127) & ~127;
+constexpr int kWArea = (kWBlockSmem - kWHead) & ~127;
+struct __align__(128) WSmem {
+  WHead h;
+  __align__(128) unsigned char area[kWArea];
+};
+static_assert(sizeof(WSmem) <= kWBlockSmem, "WSmem fits the per-CTA budget");
+
+template <bool EXACT>
+__device__ __forceinline__ void wtile(const StepArgs &A, WSmem &M, int tile, unsigned &phase,
+                                      int lane) {
+  TileSh &T = M.h.T;
+  Hdr &H = M.h.H;
+  const int4 t0 = A.tinfo[3 * tile], t1 = A.tinfo[3 * tile + 1], t2 = A.tinfo[3 * tile + 2];
+  const int ns = A.cnt_in[tile], ni = A.icnt_in[tile], n = ns + ni;
+  const int dw = t1.y;
+  const int n4 = (n + 3) & ~3;
+  // area: block (4 dw B) | snapshot (32 n4 B) | pass state (11 n4 B, 16-B rounded) | inbox keys (16 ni B)
+  const uint32_t o_snap = 4u * (uint32_t)dw;
+  const uint32_t o_pass = o_snap + 32u * (uint32_t)n4;
+  const uint32_t o_sk = o_pass + ((11u * (uint32_t)n4 + 15u) & ~15u);
+  const bool gm = o_sk + 16u * (uint32_t)ni > (uint32_t)kWArea;
+  if (lane == 0) {
+    H.tile = tile; H.n_st = ns; H.n_in = ni; H.base = t0.x; H.ibase = t0.y; H.cap = t0.z;
+    H.icap = t0.w; H.nl = t1.z; H.nroad = t1.w; H.dw = dw; H.dwd = t2.x; H.gm = gm ? 1 : 0;
+    H.done = 0; H.off = 0;
+    fence_proxy_async();                            // the area's generic writes of the last tile
+    mbar_arrive_tx(&M.h.bar, 4u * (unsigned)dw);
+    bulk_g2s(M.area, A.desc + t1.x, 4u * (unsigned)dw, &M.h.bar);
+  }
+  mbar_wait(&M.h.bar, phase);
+  phase ^= 1u;
+  __syncwarp();
+  if (gm) {                                         // block at offset 0 = slot_layout(0, 0, dw).desc
+    run_tile_gm<EXACT>(A, M.area, H, T, A.prof, lane);
+    return;
+  }
+  const int *W = reinterpret_cast<const int *>(M.area);
+  if (lane == 0) T.t = step_t(A);
+  tile_setup(H, W, reinterpret_cast<const ExtFirst *>(W + H.dwd),
+             reinterpret_cast<const PendHead *>(W + H.dwd + kExtWords * (H.nl - H.nroad)), A.prof, T,
+             lane);
+  View C;
+  C.p = reinterpret_cast<uint32_t *>(M.area + o_snap);
+  C.st = n4;
+  PStateM K;
+  K.p = M.area + o_pass;
+  K.n4 = n4;
+  auto put = [&](int pos, const InboxRec &x) {
+    C.s(pos) = x.s;
+    C.v(pos) = x.v;
+    C.vid(pos) = x.vid;
+    C.meta(pos) = x.meta;
+    C.nxt(pos) = x.nxt;
+    C.nxt2(pos) = x.nxt2;
+    C.wait(pos) = x.wait;
+    C.ends(pos) = x.end_s;
+  };
+  // merge (a1) from the records in global memory: inbox keys ranked into
+  // shared memory, stayers at own index + #inbox keys below, inbox records at
+  // rank + #stayers below
+  const InboxRec *stay = tile_recs(A, tile, ns);
+  const InboxRec *inb = stay + ns;
+  unsigned long long *skh = reinterpret_cast<unsigned long long *>(M.area + o_sk);
+  int *skv = reinterpret_cast<int *>(skh + ni);
+  int *bs = skv + ni;
+  for (int r = lane; r < ni; r += 32) {
+    const InboxRec x = inb[r];
+    const unsigned long long h = hikey(m_lane(x.meta), x.s);
+    int rank = 0;
+    for (int q = 0; q < ni; ++q) {
+      const InboxRec o = inb[q];
+      rank += key_less(hikey(m_lane(o.meta), o.s), o.vid, h, x.vid);
+    }
+    skh[rank] = h;
+    skv[rank] = x.vid;
+    bs[rank] = r;
+  }
+  __syncwarp();
+  for (int i = lane; i < ns; i += 32) {
+    const InboxRec x = stay[i];
+    int lo = 0, hi = ni;
+    if (ni > 0) {
+      const unsigned long long h = hikey(m_lane(x.meta), x.s);
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (key_less(skh[mid], skv[mid], h, x.vid)) lo = mid + 1; else hi = mid;
+      }
+    }
+    put(i + lo, x);
+  }
+  for (int r = lane; r < ni; r += 32) {
+    const InboxRec x = inb[bs[r]];
+    const unsigned long long h = skh[r];
+    int lo = 0, hi = ns;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      const InboxRec &y = stay[mid];
+      if (key_less(hikey(m_lane(y.meta), y.s), y.vid, h, x.vid)) lo = mid + 1; else hi = mid;
+    }
+    put(r + lo, x);
+  }
+  __syncwarp();
+  for (int i = lane; i < n; i += 32) {              // lane segments of the snapshot
+    const int l = m_lane(C.meta(i));
+    if (i == 0 || m_lane(C.meta(i - 1)) != l) T.seg_start[l] = (int16_t)i;
+    if (i == n - 1 || m_lane(C.meta(i + 1)) != l) T.seg_end[l] = (int16_t)(i + 1);
+  }
+  __syncwarp();
+  // the fused per-vehicle update; guard hits and exact mode go to the fp64 path
+  int nd = 0;
+  if constexpr (!EXACT) {
+    for (int q0 = 0; q0 < n; q0 += 32) {
+      const int q = q0 + lane;
+      bool def = false;
+      if (q < n) {
+        Res r;
+        Guard g;
+        g.hit = false;
+        veh_update<float, kGuard>(A, T, C, q, r, g);
+        if (g.hit) {
+          def = true;
+        } else {
+          if (A.record) record(A, C.vid(q), r, false);
+          settle(A, K, C, q, r, T);
+        }
+      }
+      nd = push_list(def, K.defl(), nd, q, lane);
+    }
+  } else {
+    for (int q = lane; q < n; q += 32) K.defl()[q] = (uint16_t)q;
+    nd = n;
+  }
+  __syncwarp();
+  for (int q = lane; q < nd; q += 32) {
+    pass_fp64(A, K, C, K.defl()[q], T);
+    if (!EXACT) atomicAdd(&T.c_guard, 1);
+  }
+  __syncwarp();
+  compact(A, K, C, T, n, lane);
+  tile_finish(A, K, C, T, lane);
+}
+
+template <bool EXACT>
+__global__ void __launch_bounds__(32, kWB) k_step_w(const __grid_constant__ StepArgs A) {
+  WSmem &M = *reinterpret_cast<WSmem *>(ks_smem);
+  const int lane = threadIdx.x;
+  if (lane == 0) {
+    mbar_init(&M.h.bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  pdl_wait();
+  pdl_trigger();
+  unsigned phase = 0;
+  for (;;) {
+    int c = 0;
+    if (lane == 0) c = atomicAdd(&A.work[0], 1);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= A.n_own) break;
+    wtile<EXACT>(A, M, A.tiles[c], phase, lane);
+    __syncwarp();
+  }
+  if (lane == 0) {
+    __threadfence();
+    if (atomicAdd(&A.work[1], 1) == (int)gridDim.x - 1) {
+      A.work[0] = 0;
+      A.work[1] = 0;
+    }
+  }
+}
+
+#ifndef KS_WARP
+#define KS_WARP 1
+#endif
+int step_smem_bytes() { return KS_WARP ? (int)sizeof(WSmem) : (int)sizeof(StepSmem); }
 
 }  // namespace sim
 
@@ -1320,13 +1525,20 @@ namespace sim {
 static int resident[2] = {0, 0};                    // resident blocks per GPU, per instantiation
 void init_step_launch(int smem_bytes) {
   if (!resident[0]) {
-    cudaFuncSetAttribute(k_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
-    cudaFuncSetAttribute(k_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     int dev = 0, nsm = 0, b0 = 0, b1 = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b0, k_step<false>, kStepThreads, smem_bytes);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_step<true>, kStepThreads, smem_bytes);
+    if (KS_WARP) {
+      cudaFuncSetAttribute(k_step_w<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+      cudaFuncSetAttribute(k_step_w<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b0, k_step_w<false>, 32, smem_bytes);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_step_w<true>, 32, smem_bytes);
+    } else {
+      cudaFuncSetAttribute(k_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+      cudaFuncSetAttribute(k_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b0, k_step<false>, kStepThreads, smem_bytes);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_step<true>, kStepThreads, smem_bytes);
+    }
     resident[0] = std::max(1, b0) * std::max(1, nsm);
     resident[1] = std::max(1, b1) * std::max(1, nsm);
   }
@@ -1336,6 +1548,12 @@ void launch_step(const StepArgs &a, void *stream, int smem_bytes) {
   init_step_launch(smem_bytes);
   if (a.n_own <= 0) return;
   const int ex = a.exact_mode ? 1 : 0;
+  if (KS_WARP) {                                    // one warp per CTA, persistent
+    const int grid = std::min(a.n_own, resident[ex]);
+    if (ex) launch_pdl(k_step_w<true>, dim3(grid), dim3(32), smem_bytes, (cudaStream_t)stream, a);
+    else launch_pdl(k_step_w<false>, dim3(grid), dim3(32), smem_bytes, (cudaStream_t)stream, a);
+    return;
+  }
   // enough CTAs for the work (a producer claims kGroup tiles at a time), at
   // most the resident capacity (persistent)
   const int grid = std::min((a.n_own + kGroup - 1) / kGroup, resident[ex]);
