@@ -366,7 +366,7 @@ def run_gpu(args, rank, world, local_rank):
             "fp64_guard_hits_per_step": (m1["n_guard_hits"] - m0["n_guard_hits"]) / args.steps}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "k_prep + k_step (the step kernels, one CUDA-event window)",
+                     "kernel": "k_prep + k_step_w (the step kernels, one CUDA-event window)",
                      "kernel_ms_avg": kstep_ms / args.steps,
                      "signal_kernel_ms_avg": ksig_ms / args.steps,
                      "alg_bytes_per_launch": survey_bytes,
