@@ -1300,6 +1300,9 @@ __global__ void KS_STEP_BOUNDS k_step(const __grid_constant__ StepArgs A) {
 #ifndef KW_BLOCKS
 #define KW_BLOCKS 16
 #endif
+#ifndef KW_MINB
+#define KW_MINB KW_BLOCKS                            // launch-bounds CTAs per SM (register cap)
+#endif
 constexpr int kWB = KW_BLOCKS;                       // one-warp CTAs per SM
 // pass state of the fused path: the stayer results and the fp64 list only
 struct PStateM {
@@ -1460,7 +1463,7 @@ __device__ __forceinline__ void wtile(const StepArgs &A, WSmem &M, int tile, uns
 }
 
 template <bool EXACT>
-__global__ void __launch_bounds__(32, kWB) k_step_w(const __grid_constant__ StepArgs A) {
+__global__ void __launch_bounds__(32, KW_MINB) k_step_w(const __grid_constant__ StepArgs A) {
   WSmem &M = *reinterpret_cast<WSmem *>(ks_smem);
   const int lane = threadIdx.x;
   if (lane == 0) {
