@@ -323,7 +323,7 @@ def run_gpu(args, rank, world, local_rank):
     nj = len(scen.graph["junc_lane_offsets"]) - 1
     jids = np.arange(nj, dtype=np.int32)
     offs = scen.graph["junc_offset_steps"].astype(np.int64)
-    e2e_steps = max(10, min(args.steps, 50))
+    e2e_steps = max(10, min(4 * args.steps, 200))          # >= 200 steps at the default: host jitter
     lane_bytes = 8 * scen.n_lanes
     host_ctl = args.policy == "fixed"                     # max pressure runs on the device
     # host fixed-time controller (C = 102 s: NS 30+3, NS-left 15+3, EW 30+3,
