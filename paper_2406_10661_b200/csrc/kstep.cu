@@ -1,6 +1,15 @@
-// kstep.cu — the fused step kernel k_step (rows a0-a4, a6).
+// kstep.cu — the step kernels (rows a0-a4, a6) and k_prep.
 //
-// A warp-specialised persistent kernel, one CTA per SM.  One PRODUCER warp
+// Two interchangeable step kernels over the same data layout and model code:
+//   k_step_w (the default, KS_WARP=1, at the end of this file): one warp per
+//             CTA, many CTAs per SM; each warp takes a tile, bulk-copies its
+//             block into its own shared area, merges the tile's records from
+//             global memory into a shared snapshot and runs the fused
+//             per-vehicle update (veh_update), the fp64 list, the compaction
+//             and the finish.  Measured faster on C4.
+//   k_step   (KS_WARP=0): the warp-specialised ring kernel described below.
+//
+// k_step: a warp-specialised persistent kernel, one CTA per SM.  One PRODUCER warp
 // feeds kCW autonomous CONSUMER warps through a ring of tile slots in shared
 // memory (a tile = one road's lanes + the junction lanes leaving it, dev.h):
 //
