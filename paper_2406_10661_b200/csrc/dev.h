@@ -174,6 +174,11 @@ struct StepArgs {
   int32_t rank, n_own;
   const int32_t *tiles, *tile_owner;  // tiles: own tiles, largest slot capacity first
   int32_t *work;                    // [2] persistent-kernel work counter + finished warps (zero between launches)
+  // k_step_w's tile order, rebuilt by k_prep every step: own tiles bucketed
+  // by their vehicle count at t, largest first (kNBucket buckets of
+  // 2^kBucketShift vehicles); bucket d's tiles at bk_list[d * n_tiles ...];
+  // bk_cnt is zero between steps (k_step_w's last CTA clears it)
+  int32_t *bk_cnt, *bk_list;
   const int32_t *tile_lane_off, *tile_lanes, *tile_nroad;
   int32_t *desc;                    // tile blocks: descriptor words, then the k_prep staging
   const int32_t *desc_off;          // (ExtFirst per junction lane, PendHead per road lane)
@@ -270,6 +275,8 @@ struct SignalArgs {
   int32_t cnt_buf;                  // index of the lcnt buffer of state(t)
   int32_t mp_period;
 };
+
+constexpr int kNBucket = 64, kBucketShift = 3;
 
 // A kernel launch that may begin while the previous kernel of the stream is
 // still running (programmatic dependent launch): the kernel

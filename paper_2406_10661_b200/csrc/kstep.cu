@@ -57,6 +57,12 @@ namespace sim {
 #ifndef KS_MINB
 #define KS_MINB 1
 #endif
+#ifndef KS_WARP
+#define KS_WARP 1                                   // the step kernel: k_step_w (1) or the ring k_step (0)
+#endif
+#ifndef KW_ORDER
+#define KW_ORDER 1                                  // k_step_w takes tiles by vehicle count (k_prep buckets)
+#endif
 #ifndef KS_PSLEEP
 #define KS_PSLEEP 64                          // producer back-off (ns) while the ring is full
 #endif
@@ -385,6 +391,12 @@ __global__ void __launch_bounds__(128) k_prep(const __grid_constant__ StepArgs A
   const int w = blockIdx.x * 4 + (threadIdx.x >> 5), l = threadIdx.x & 31;
   if (w >= A.n_own) return;
   const int T = A.tiles[w];
+  if (KS_WARP && KW_ORDER && l == 0) {              // k_step_w's order: by vehicles at t, largest first
+    const int n = A.cnt_in[T] + A.icnt_in[T];
+    const int d = kNBucket - 1 - min(n >> kBucketShift, kNBucket - 1);
+    const int slot = atomicAdd(&A.bk_cnt[d], 1);
+    A.bk_list[(size_t)d * A.n_tiles + slot] = T;
+  }
   const int4 t1 = A.tinfo[3 * T + 1], t2 = A.tinfo[3 * T + 2];
   const int nl = t1.z, nroad = t1.w;
   int32_t *stage = A.desc + t1.x + t2.x;            // after the tile's descriptor words
@@ -1483,12 +1495,37 @@ __global__ void __launch_bounds__(32, KW_MINB) k_step_w(const __grid_constant__ 
   pdl_wait();
   pdl_trigger();
   unsigned phase = 0;
+  // this step's tile order (KW_ORDER): exclusive prefix of the bucket counts,
+  // buckets lane and 32 + lane in this lane
+  int e0 = 0, e1 = 0;
+  if (KW_ORDER) {
+    static_assert(kNBucket == 64, "two buckets per lane");
+    const int c0 = A.bk_cnt[lane], c1 = A.bk_cnt[32 + lane];
+    int i0 = c0, i1 = c1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y0 = __shfl_up_sync(0xffffffffu, i0, o), y1 = __shfl_up_sync(0xffffffffu, i1, o);
+      if (lane >= o) { i0 += y0; i1 += y1; }
+    }
+    const int t0 = __shfl_sync(0xffffffffu, i0, 31);
+    e0 = i0 - c0;
+    e1 = t0 + i1 - c1;
+  }
   for (;;) {
     int c = 0;
     if (lane == 0) c = atomicAdd(&A.work[0], 1);
     c = __shfl_sync(0xffffffffu, c, 0);
     if (c >= A.n_own) break;
-    wtile<EXACT>(A, M, A.tiles[c], phase, lane);
+    int tile;
+    if (KW_ORDER) {                                 // the last bucket d with prefix[d] <= c
+      const unsigned m0 = __ballot_sync(0xffffffffu, e0 <= c), m1 = __ballot_sync(0xffffffffu, e1 <= c);
+      const int d = m1 ? 32 + (31 - __clz(m1)) : 31 - __clz(m0);
+      const int pre = __shfl_sync(0xffffffffu, d >= 32 ? e1 : e0, d & 31);
+      tile = A.bk_list[(size_t)d * A.n_tiles + (c - pre)];
+    } else {
+      tile = A.tiles[c];
+    }
+    wtile<EXACT>(A, M, tile, phase, lane);
     __syncwarp();
   }
   if (lane == 0) {
@@ -1496,13 +1533,12 @@ __global__ void __launch_bounds__(32, KW_MINB) k_step_w(const __grid_constant__ 
     if (atomicAdd(&A.work[1], 1) == (int)gridDim.x - 1) {
       A.work[0] = 0;
       A.work[1] = 0;
+      if (KW_ORDER)
+        for (int d = 0; d < kNBucket; ++d) A.bk_cnt[d] = 0;   // for the next step's k_prep
     }
   }
 }
 
-#ifndef KS_WARP
-#define KS_WARP 1
-#endif
 int step_smem_bytes() { return KS_WARP ? (int)sizeof(WSmem) : (int)sizeof(StepSmem); }
 
 }  // namespace sim

@@ -1055,6 +1055,9 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   }
   AL(A.work, 2);
   CK(h, cudaMemset(A.work, 0, 8));
+  AL(A.bk_cnt, kNBucket);
+  CK(h, cudaMemset(A.bk_cnt, 0, kNBucket * 4));
+  AL(A.bk_list, (size_t)kNBucket * nt);
   A.n_own = (int)P.tiles.size();
   A.rank = P.rank;
   for (int b = 0; b < 2; ++b) {
