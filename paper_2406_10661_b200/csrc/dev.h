@@ -175,8 +175,9 @@ struct StepArgs {
   const int32_t *tiles, *tile_owner;  // tiles: own tiles, largest slot capacity first
   int32_t *work;                    // [2] persistent-kernel work counter + finished warps (zero between launches)
   // k_step_w's tile order, rebuilt by k_prep every step: own tiles bucketed
-  // by their vehicle count at t, largest first (kNBucket buckets of
-  // 2^kBucketShift vehicles); bucket d's tiles at bk_list[d * n_tiles ...];
+  // by an estimate of their work at t (vehicles + 4 x lanes),
+  // largest first (kNBucket buckets of 2^kBucketShift); bucket d's tiles at
+  // bk_list[d * n_tiles ...];
   // bk_cnt is zero between steps (k_step_w's last CTA clears it)
   int32_t *bk_cnt, *bk_list;
   const int32_t *tile_lane_off, *tile_lanes, *tile_nroad;

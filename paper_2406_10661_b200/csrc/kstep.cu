@@ -61,7 +61,10 @@ namespace sim {
 #define KS_WARP 1                                   // the step kernel: k_step_w (1) or the ring k_step (0)
 #endif
 #ifndef KW_ORDER
-#define KW_ORDER 1                                  // k_step_w takes tiles by vehicle count (k_prep buckets)
+#define KW_ORDER 2                                  // k_step_w tile order: 1 vehicles, 2 vehicles + 4 x lanes (k_prep buckets)
+#endif
+#ifndef KW_BSHIFT
+#define KW_BSHIFT kBucketShift
 #endif
 #ifndef KS_PSLEEP
 #define KS_PSLEEP 64                          // producer back-off (ns) while the ring is full
@@ -392,8 +395,12 @@ __global__ void __launch_bounds__(128) k_prep(const __grid_constant__ StepArgs A
   if (w >= A.n_own) return;
   const int T = A.tiles[w];
   if (KS_WARP && KW_ORDER && l == 0) {              // k_step_w's order: by vehicles at t, largest first
+#if KW_ORDER == 2
+    const int n = A.cnt_in[T] + A.icnt_in[T] + 4 * A.tinfo[3 * T + 1].z;   // + per-lane cost (DESIGN §5 fit)
+#else
     const int n = A.cnt_in[T] + A.icnt_in[T];
-    const int d = kNBucket - 1 - min(n >> kBucketShift, kNBucket - 1);
+#endif
+    const int d = kNBucket - 1 - min(n >> KW_BSHIFT, kNBucket - 1);
     const int slot = atomicAdd(&A.bk_cnt[d], 1);
     A.bk_list[(size_t)d * A.n_tiles + slot] = T;
   }
