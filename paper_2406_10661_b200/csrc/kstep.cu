@@ -1490,6 +1490,9 @@ __device__ __forceinline__ void wtile(const StepArgs &A, WSmem &M, int tile, uns
   tile_finish(A, K, C, T, lane);
 }
 
+#ifdef KW_TAIL
+__device__ unsigned long long g_kw_fin[4096];
+#endif
 template <bool EXACT>
 __global__ void __launch_bounds__(32, KW_MINB) k_step_w(const __grid_constant__ StepArgs A) {
   WSmem &M = *reinterpret_cast<WSmem *>(ks_smem);
@@ -1535,6 +1538,13 @@ __global__ void __launch_bounds__(32, KW_MINB) k_step_w(const __grid_constant__ 
     wtile<EXACT>(A, M, tile, phase, lane);
     __syncwarp();
   }
+#ifdef KW_TAIL
+  if (lane == 0 && blockIdx.x < 4096) {             // dev builds: per-CTA finish time
+    unsigned long long tnow;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+    g_kw_fin[blockIdx.x] = tnow;
+  }
+#endif
   if (lane == 0) {
     __threadfence();
     if (atomicAdd(&A.work[1], 1) == (int)gridDim.x - 1) {
@@ -1551,6 +1561,17 @@ int step_smem_bytes() { return KS_WARP ? (int)sizeof(WSmem) : (int)sizeof(StepSm
 }  // namespace sim
 
 // dev builds (-DKS_PROF): per-phase clock totals of k_step since the last call
+extern "C" int sim_debug_kw_finish(unsigned long long *out) {
+#ifdef KW_TAIL
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, sim::g_kw_fin, sizeof(sim::g_kw_fin));
+  return 4096;
+#else
+  (void)out;
+  return 0;
+#endif
+}
+
 extern "C" int sim_debug_tile_cycles(unsigned int *out) {
 #ifdef KS_PROF
   cudaDeviceSynchronize();
