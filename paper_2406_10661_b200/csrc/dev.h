@@ -294,7 +294,11 @@ inline cudaError_t launch_pdl(void (*kern)(K...), dim3 grid, dim3 block, size_t 
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
+#ifdef KS_NO_PDL
+  cfg.numAttrs = 0;                                 // dev builds: plain stream order
+#else
   cfg.numAttrs = 1;
+#endif
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
