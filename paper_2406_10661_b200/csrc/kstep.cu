@@ -1,40 +1,22 @@
-// kstep.cu — the step kernels (rows a0-a4, a6) and k_prep.
+// kstep.cu — the step kernel k_step_w (rows a0-a4, a6) and k_prep.
 //
-// Two interchangeable step kernels over the same data layout and model code:
-//   k_step_w (the default, KS_WARP=1, at the end of this file): one warp per
-//             CTA, many CTAs per SM; each warp takes a tile, bulk-copies its
-//             block into its own shared area, merges the tile's records from
-//             global memory into a shared snapshot and runs the fused
-//             per-vehicle update (veh_update), the fp64 list, the compaction
-//             and the finish.  Measured faster on C4.
-//   k_step   (KS_WARP=0): the warp-specialised ring kernel described below.
-//
-// k_step: a warp-specialised persistent kernel, one CTA per SM.  One PRODUCER warp
-// feeds kCW autonomous CONSUMER warps through a ring of tile slots in shared
-// memory (a tile = one road's lanes + the junction lanes leaving it, dev.h):
-//
-//   producer  claims tiles from a global work counter (largest first), gives
-//             each a variable-size slot in a byte ring (ring entries with full /
-//             empty mbarriers, freed in order) and streams the tile's stayer
-//             slab segment, inbox records and descriptor into it with 1-D bulk
-//             copies (cp.async.bulk + mbarrier complete_tx), together with
-//             what k_prep staged for it from other tiles — the first vehicle
-//             of every junction lane's exit lane at t (the P:168-169 lookahead
-//             target), the junction lanes' signals, the heads of the
-//             pending-departure queues — so the consumers' common path has no
-//             global loads.
-//   consumers each take the next slot in order and run the whole tile alone,
-//             with no block-wide barrier: tile metadata; merge of in-order
-//             stayers + sorted inbox into the snapshot (a1);
-//             pass 1 = eligibility + leader / lookahead + IDM on the current
-//             lane for every vehicle (a2, a3); pass 2 = MOBIL for the compacted
-//             list of vehicles that may change lane; pass 3 =
-//             integrate / hand-off / arrival (a4) with movers emitted to their
-//             destination inbox; the fp64 canonical recomputation of vehicles
-//             whose fp32 margins fell inside the guard band; the
-//             in-order compaction of stayers, lane summaries for t+1,
-//             departures (K11) and counters (a6).  The snapshot and the
-//             per-vehicle pass state live in the tile's own slot.
+// k_step_w: one warp per CTA, 16 CTAs per SM, persistent.  Each warp claims a
+// tile (a road's lanes + the junction lanes leaving it, dev.h) from a global
+// counter in an order k_prep builds (largest estimated work first),
+// bulk-copies the tile's block — descriptor + what k_prep staged from other
+// tiles: the first vehicle of every junction lane's exit lane at t (the
+// P:168-169 lookahead target), the junction lanes' signals, the heads of the
+// pending-departure queues — into its own shared area (cp.async.bulk +
+// mbarrier), merges the tile's in-order stayers and its inbox from global
+// memory into a shared snapshot (a1), runs the fused
+// per-vehicle update (eligibility, leader / lookahead, IDM, MOBIL, integrate,
+// hand-off, arrival: a2-a4), recomputes the vehicles whose fp32
+// margins fell inside the guard band on the canonical fp64 path,
+// and compacts the stayers / writes the lane summaries for t+1 / inserts
+// departures (K11) / adds the counters (a6).  Tiles too large for the
+// area run whole in global mode (snapshot and pass state in global scratch,
+// passes 1-3 below).  (The warp-specialised ring kernel of earlier in round 2
+// — producer warp + consumer rounds — is in git history.)
 //
 // Every decision reads only state(t) (the snapshot) and all
 // cross-tile outputs are integer atomics into the t+1 buffers, so the result
@@ -48,42 +30,15 @@
 
 namespace sim {
 
-#ifndef KS_CONS_WARPS
-#define KS_CONS_WARPS 15
-#endif
-#ifndef KS_RING_KB
-#define KS_RING_KB 206
-#endif
-#ifndef KS_MINB
-#define KS_MINB 1
-#endif
-#ifndef KS_WARP
-#define KS_WARP 1                                   // the step kernel: k_step_w (1) or the ring k_step (0)
-#endif
 #ifndef KW_ORDER
 #define KW_ORDER 2                                  // k_step_w tile order: 1 vehicles, 2 vehicles + 4 x lanes (k_prep buckets)
 #endif
 #ifndef KW_BSHIFT
 #define KW_BSHIFT kBucketShift
 #endif
-#ifndef KS_PSLEEP
-#define KS_PSLEEP 64                          // producer back-off (ns) while the ring is full
-#endif
-constexpr int kCW = KS_CONS_WARPS;            // consumer warps
-constexpr int kStepThreads = (kCW + 1) * 32;  // + the producer warp (the last warp)
-constexpr int kRing = KS_RING_KB * 1024;      // slot ring bytes
-constexpr int kNH = 32;                       // ring entries (slot headers)
-constexpr int kGroup = 16;                    // tiles claimed from the work counter at a time
-static_assert(kCW <= kNH, "ring entries");
-static_assert(kGroup * 2 <= 32, "the producer warp holds two groups");
-
-// Byte layout of one tile slot (all offsets 16-B aligned): the tile's vehicle
-// records at t (stayers then inbox, one contiguous bulk copy; once merged
-// into the snapshot their space holds the per-vehicle pass state), its block
-// (descriptor + the k_prep staging, one bulk copy), the merged snapshot and
-// the sorted inbox keys.  A tile too large for the ring (> kRing / 2) runs in global
-// mode: its slot holds only the block, the snapshot and pass state live in
-// the global scratch arrays.
+// Byte layout of a tile's slot in global mode (run_tile<EXACT, true>): only
+// the block (descriptor + the k_prep staging) at offset 0; the snapshot and
+// the pass state live in the global scratch arrays.
 struct SlotLayout {
   uint32_t veh, desc, snap, sortk, size;
   int n4;
@@ -100,8 +55,7 @@ __device__ __forceinline__ SlotLayout slot_layout(int n_st, int n_in, int dw) {
   return L;
 }
 
-struct __align__(16) Hdr {          // one ring entry
-  unsigned long long full, empty;   // mbarriers
+struct __align__(16) Hdr {          // a tile's fields (from its static record and counts)
   int tile, n_st, n_in, base, ibase, cap, icap, nl, nroad, dw, dwd;
   int gm, done;                     // global mode / end-of-work sentinel
   uint32_t off;                     // slot byte offset in the ring
@@ -135,16 +89,6 @@ __device__ __forceinline__ PState pstate_at(unsigned char *p, int n4) {
   return S;
 }
 
-struct __align__(128) StepSmem {
-  Hdr H[kNH];
-  int next_seq;
-  __align__(16) Prof prof[kSmemProf];
-  TileSh T[kCW];
-  __align__(128) unsigned char ring[kRing];
-};
-
-static_assert(sizeof(StepSmem) <= 227 * 1024, "one CTA per SM: at most 227 KB of shared memory");
-
 #ifdef KS_NOGUARD
 constexpr bool kGuard = false;                // timing experiment only (no fp64 fallback)
 #else
@@ -166,10 +110,6 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
 }
 __device__ __forceinline__ void mbar_init(unsigned long long *b, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long *b) {
-  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(b))
-               : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_tx(unsigned long long *b, unsigned tx) {
   asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
@@ -196,48 +136,10 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-// producer-side wait on an `empty` barrier: back off instead of spinning so
-// the waiting producer does not take issue slots from the consumers
-__device__ __forceinline__ void mbar_wait_sleep(unsigned long long *b, unsigned parity) {
-  unsigned ok = 0;
-  for (;;) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(b)), "r"(parity)
-        : "memory");
-    if (ok) return;
-    __nanosleep(KS_PSLEEP);
-  }
-}
-
-// ---- phase profiling (dev builds with -DKS_PROF; sim_debug_kstep_prof) ----------
-#ifdef KS_PROF
-__device__ unsigned long long g_ks_prof[32];
-__device__ unsigned int g_tile_cyc[65536][4];       // per tile: cycles, vehicles, candidates, round slowest
-#ifdef KS_PROF_TILE                                 // per-tile cycles only (no per-phase probes)
+// profiling probes of earlier builds (no-ops)
 #define KP_DECL
 #define KP(idx, on) do {} while (0)
 #define KPN(idx, on, n) do {} while (0)
-#else
-#define KP_DECL long long kp_last = clock64();
-#define KP(idx, on)                                                    \
-  do {                                                                 \
-    if (on) {                                                          \
-      const long long kp_now = clock64();                              \
-      atomicAdd(&g_ks_prof[idx], (unsigned long long)(kp_now - kp_last)); \
-      kp_last = kp_now;                                                \
-    }                                                                  \
-  } while (0)
-#define KPN(idx, on, n) do { if (on) atomicAdd(&g_ks_prof[idx], (unsigned long long)(n)); } while (0)
-#endif
-#else
-#define KP_DECL
-#define KP(idx, on) do {} while (0)
-#define KPN(idx, on, n) do {} while (0)
-#endif
 
 // ---- small helpers -----------------------------------------------------------
 __device__ __forceinline__ unsigned long long vkey(float s, int vid) {
@@ -380,21 +282,22 @@ __device__ __noinline__ void emit_moved(const StepArgs &A, const View &C, int i,
   }
 }
 
-// ---- k_prep: what k_step reads from other tiles, staged per tile -----------------------
+// ---- k_prep: what the step kernel reads from other tiles, staged per tile -----------------------
 // One warp per own tile, one lane per tile lane (<= 32).  Junction lane: its
 // signal at t and the first vehicle of its exit lane at t (the P:168-169
 // lookahead target one lane beyond the tile: summary key, speed, length);
 // road lane: the head of its pending-departure queue at t (K11).
-// Written into the tile's block after its descriptor words, from where k_step's
-// producer warp bulk-copies them with the descriptor.  Runs after k_signal (the
-// signals of t) and reads only state(t).
+// Written into the tile's block after its descriptor words, from where the
+// step kernel bulk-copies them with the descriptor.  Also files the tile in
+// the step kernel's work order.  Runs after k_signal (the signals of t) and
+// reads only state(t).
 __global__ void __launch_bounds__(128) k_prep(const __grid_constant__ StepArgs A) {
   pdl_wait();                                       // the signals of t (k_signal)
   pdl_trigger();
   const int w = blockIdx.x * 4 + (threadIdx.x >> 5), l = threadIdx.x & 31;
   if (w >= A.n_own) return;
   const int T = A.tiles[w];
-  if (KS_WARP && KW_ORDER && l == 0) {              // k_step_w's order: by vehicles at t, largest first
+  if (KW_ORDER && l == 0) {              // k_step_w's order: by vehicles at t, largest first
 #if KW_ORDER == 2
     const int n = A.cnt_in[T] + A.icnt_in[T] + 4 * A.tinfo[3 * T + 1].z;   // + per-lane cost (DESIGN §5 fit)
 #else
@@ -505,138 +408,7 @@ void launch_prep(const StepArgs &a, void *stream) {
   launch_pdl(k_prep, dim3((a.n_own + 3) / 4), dim3(128), 0, (cudaStream_t)stream, a);
 }
 
-// ---- producer warp --------------------------------------------------------------------
-// The tiles this CTA will take, claimed kGroup at a time from the work counter
-// and prefetched: `cur` is being published, `nxt` has its fields in flight,
-// `ids` holds the tile ids of the group after (lane q < kGroup: tile q).
-struct TInfo { int tile, n_st, n_in; int4 t0, t1, t2; };
-__device__ __forceinline__ int claim_ids(const StepArgs &A, int lane) {
-  int c = 0;
-  if (lane == 0) c = atomicAdd(&A.work[0], kGroup);
-  c = __shfl_sync(0xffffffffu, c, 0) + (lane & (kGroup - 1));
-  return (lane < kGroup && c < A.n_own) ? A.tiles[c] : -1;
-}
-__device__ __forceinline__ TInfo load_fields(const StepArgs &A, int t) {
-  TInfo x;
-  x.tile = t;
-  x.n_st = x.n_in = 0;
-  x.t0 = x.t1 = x.t2 = make_int4(0, 0, 0, 0);
-  if (t >= 0) {
-    x.n_st = A.cnt_in[t];
-    x.n_in = A.icnt_in[t];
-    x.t0 = A.tinfo[3 * t];
-    x.t1 = A.tinfo[3 * t + 1];
-    x.t2 = A.tinfo[3 * t + 2];
-  }
-  return x;
-}
-__device__ __forceinline__ int4 shfl4(const int4 &v, int src) {
-  return make_int4(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
-                   __shfl_sync(0xffffffffu, v.z, src), __shfl_sync(0xffffffffu, v.w, src));
-}
-__device__ __forceinline__ TInfo shfl_tinfo(const TInfo &x, int src) {
-  TInfo y;
-  y.tile = __shfl_sync(0xffffffffu, x.tile, src);
-  y.n_st = __shfl_sync(0xffffffffu, x.n_st, src);
-  y.n_in = __shfl_sync(0xffffffffu, x.n_in, src);
-  y.t0 = shfl4(x.t0, src);
-  y.t1 = shfl4(x.t1, src);
-  y.t2 = shfl4(x.t2, src);
-  return y;
-}
-
-__device__ __noinline__ void producer(const StepArgs &A, StepSmem &M, int lane) {
-  TInfo cur = load_fields(A, claim_ids(A, lane));
-  int ids = claim_ids(A, lane);
-  TInfo nxt = load_fields(A, ids);
-  ids = claim_ids(A, lane);
-  int pos = 0;
-  bool exhausted = false;
-  int n_sent = 0;                                   // end-of-work sentinels published
-  unsigned long long head = 0, tail = 0;            // ring bytes allocated / freed (monotonic)
-  unsigned long long ent_end = 0;                   // lane e: end (head) of entry e's slot
-  bool fenced = true;                               // no bytes freed since the last proxy fence
-  int seq = 0, tail_seq = 0;
-  KP_DECL
-  for (;;) {
-    TInfo x;
-    x.tile = -1;
-    if (!exhausted) {
-      if (pos == kGroup) {                           // next group
-        cur = nxt;
-        nxt = load_fields(A, ids);
-        ids = claim_ids(A, lane);
-        pos = 0;
-      }
-      x = shfl_tinfo(cur, pos);
-      if (x.tile < 0) exhausted = true;
-    }
-    const bool sentinel = exhausted;
-    if (sentinel && n_sent == kCW) break;
-    const int base = x.t0.x, ibase = x.t0.y, cap = x.t0.z, icap = x.t0.w;
-    const int doff = x.t1.x, dw = x.t1.y, nl = x.t1.z, nroad = x.t1.w;
-    SlotLayout L = slot_layout(x.n_st, x.n_in, dw);
-    bool gm = false;
-    if (sentinel) {
-      L.size = 0;
-    } else if (L.size > (uint32_t)(kRing / 2)) {     // too large for the ring: global mode
-      gm = true;
-      L = slot_layout(0, 0, dw);
-    }
-    const unsigned long long size = L.size;
-    // an entry and contiguous bytes; the oldest slots are freed in order
-    KP(1, lane == 0);
-    for (;;) {
-      const unsigned long long p = head % kRing;
-      const unsigned long long waste = (p + size > (unsigned long long)kRing) ? kRing - p : 0;
-      if (seq - tail_seq < kNH && head + waste + size - tail <= (unsigned long long)kRing) break;
-      const int e = tail_seq % kNH;
-      mbar_wait_sleep(&M.H[e].empty, (unsigned)(tail_seq / kNH) & 1u);
-      tail = __shfl_sync(0xffffffffu, ent_end, e);
-      tail_seq += 1;
-      fenced = false;
-    }
-    KP(0, lane == 0);
-    {
-      const unsigned long long p = head % kRing;
-      if (p + size > (unsigned long long)kRing) head += kRing - p;
-    }
-    const uint32_t off = (uint32_t)(head % kRing);
-    head += size;
-    const int e = seq % kNH;
-    if (lane == e) ent_end = head;
-    Hdr &H = M.H[e];
-    if (lane == 0) {
-      H.tile = x.tile; H.n_st = x.n_st; H.n_in = x.n_in; H.base = base; H.ibase = ibase;
-      H.cap = cap; H.icap = icap; H.nl = nl; H.nroad = nroad; H.dw = dw; H.dwd = x.t2.x;
-      H.gm = gm ? 1 : 0;
-      H.done = sentinel ? 1 : 0;
-      H.off = off;
-      unsigned tx = 0;
-      if (!sentinel) {
-        tx = 4u * (unsigned)dw;
-        if (!gm) tx += 32u * (unsigned)(x.n_st + x.n_in);
-        if (!fenced) fence_proxy_async();            // generic writes of the freed slots' last use
-      }
-      mbar_arrive_tx(&H.full, tx);                   // the single arrival; copies complete the phase
-    }
-    if (!sentinel) fenced = true;
-    __syncwarp();
-    if (!sentinel) {                                 // two bulk copies
-      unsigned char *slot = M.ring + off;
-      if (!gm && x.n_st + x.n_in > 0 && lane == 0)
-        bulk_g2s(slot + L.veh, A.vin + base + cap - x.n_st, 32u * (unsigned)(x.n_st + x.n_in), &H.full);
-      if (lane == 1) bulk_g2s(slot + L.desc, A.desc + doff, 4u * (unsigned)dw, &H.full);
-      pos += 1;
-    } else {
-      n_sent += 1;
-    }
-    seq += 1;
-    KP(2, lane == 0);
-  }
-}
-
-// ---- consumer: one tile, one warp ----------------------------------------------------
+// ---- one tile ----------------------------------------------------
 // Tile metadata from its descriptor into the warp's TileSh.
 __device__ __forceinline__ void tile_setup(const Hdr &H, const int *W, const ExtFirst *ext,
                                            const PendHead *pend, const Prof *P, TileSh &T,
@@ -1169,9 +941,6 @@ __device__ __forceinline__ void run_tile(const StepArgs &A, unsigned char *slot,
   __syncwarp();
   KP(24, lane == 0);
   run_passes<EXACT>(A, K, C, T, n, lane);
-#if defined(KS_PROF) && !defined(KS_PROF_TILE)
-  kp_last = clock64();
-#endif
   compact(A, K, C, T, n, lane);
   KP(29, lane == 0);
   tile_finish(A, K, C, T, lane);
@@ -1186,138 +955,7 @@ __device__ __noinline__ void run_tile_gm(const StepArgs &A, unsigned char *slot,
   run_tile<EXACT, true>(A, slot, H, T, P, lane);
 }
 
-// Named barrier 1 of the consumer warps (the producer never joins it), with
-// the number of consumer threads whose predicate is true (bar.red.popc).
-__device__ __forceinline__ int cons_bar_count(bool pred) {
-  int r;
-  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\tbar.red.popc.u32 %0, 1, %1, p;\n\t}"
-               : "=r"(r) : "r"(kCW * 32), "r"((int)pred) : "memory");
-  return r;
-}
-
-// The consumer warps take their tiles in rounds: each warp claims the next
-// ring entry, runs that tile, and waits at a consumer barrier until every
-// warp has finished its tile.  Tiles come in LPT order, so the tiles of a
-// round are of similar size, and the warps run the same pass of the model at
-// about the same time: the instruction cache then holds one pass rather than
-// all of them (ncu: free-running warps lose 44% of their samples to "no
-// instruction"; rounds are worth ~25%, which lists the measured
-// alternatives — skew, several tiles per round, cooperative rounds).  Warps
-// that met the end-of-work sentinel keep joining the barrier until all have.
-template <bool EXACT>
-__device__ __forceinline__ void consumer(const StepArgs &A, StepSmem &M, const Prof *P, int warp,
-                                         int lane) {
-  TileSh &T = M.T[warp];
-  KP_DECL
-  bool done = false;
-#ifdef KS_PROF
-  __shared__ unsigned long long rt_cyc[kCW];
-  __shared__ int rt_n[kCW];
-#endif
-  for (;;) {
-#ifdef KS_PROF
-    long long rt0 = clock64();
-    if (lane == 0) { rt_cyc[warp] = 0; rt_n[warp] = 0; }
-#endif
-    if (!done) {
-      int seq = 0;
-      if (lane == 0) seq = atomicAdd(&M.next_seq, 1);
-      seq = __shfl_sync(0xffffffffu, seq, 0);
-      Hdr &H = M.H[seq % kNH];
-      KP(9, lane == 0);
-      mbar_wait(&H.full, (unsigned)(seq / kNH) & 1u);
-      KP(8, lane == 0);
-      if (H.done) {
-        done = true;
-      } else {
-#ifdef KS_PROF
-        const long long t0 = clock64();
-#endif
-        if (H.gm) run_tile_gm<EXACT>(A, M.ring + H.off, H, T, P, lane);
-        else run_tile<EXACT, false>(A, M.ring + H.off, H, T, P, lane);
-#ifdef KS_PROF
-        if (lane == 0 && H.tile < 65536) {
-          g_tile_cyc[H.tile][0] = (unsigned)(clock64() - t0);
-          g_tile_cyc[H.tile][1] = (unsigned)(H.n_st + H.n_in);
-          g_tile_cyc[H.tile][2] = (unsigned)T.c_lc + ((unsigned)T.c_hand << 16);
-          g_tile_cyc[H.tile][3] = (unsigned)H.nl;
-        }
-#endif
-        KP(10, lane == 0);
-        KPN(20, lane == 0, 1);
-#ifdef KS_PROF
-        if (lane == 0) { rt_cyc[warp] = (unsigned long long)(clock64() - rt0); rt_n[warp] = H.n_st + H.n_in; }
-#endif
-        if (lane == 0) mbar_arrive(&H.empty);       // the slot can be reused
-      }
-    }
-    const int nd = cons_bar_count(done);
-    KP(11, lane == 0);
-#ifdef KS_PROF
-    if (warp == 0 && lane == 0) {                   // round imbalance (dev builds)
-      unsigned long long mx = 0, sm = 0;
-      int nmx = 0, cnt = 0, nmean = 0;
-      for (int w = 0; w < kCW; ++w) {
-        if (rt_cyc[w] == 0) continue;
-        cnt++;
-        sm += rt_cyc[w];
-        nmean += rt_n[w];
-        if (rt_cyc[w] > mx) { mx = rt_cyc[w]; nmx = rt_n[w]; }
-      }
-      if (cnt == kCW) {
-        atomicAdd(&g_ks_prof[12], mx);
-        atomicAdd(&g_ks_prof[13], sm / kCW);
-        atomicAdd(&g_ks_prof[14], 1ull);
-        atomicAdd(&g_ks_prof[15], (unsigned long long)nmx);
-        atomicAdd(&g_ks_prof[16], (unsigned long long)(nmean / kCW));
-      }
-    }
-    cons_bar_count(false);
-#endif
-    if (nd == kCW * 32) break;
-  }
-}
-
-template <bool EXACT>
-#ifdef KS_MAXNREG
-#define KS_STEP_BOUNDS __maxnreg__(KS_MAXNREG)
-#else
-#define KS_STEP_BOUNDS __launch_bounds__(kStepThreads, KS_MINB)
-#endif
-__global__ void KS_STEP_BOUNDS k_step(const __grid_constant__ StepArgs A) {
-  StepSmem &M = *reinterpret_cast<StepSmem *>(ks_smem);
-  const int tid = threadIdx.x;
-  const Prof *P = A.prof;
-  if (A.n_prof <= kSmemProf) {                      // profiles as int4 words (Prof is 96 B)
-    const int nw = A.n_prof * (int)(sizeof(Prof) / 16);
-    for (int q = tid; q < nw; q += blockDim.x)
-      reinterpret_cast<int4 *>(M.prof)[q] = reinterpret_cast<const int4 *>(A.prof)[q];
-    P = M.prof;
-  }
-  if (tid == 0) {
-    for (int e = 0; e < kNH; ++e) {
-      mbar_init(&M.H[e].full, 1);
-      mbar_init(&M.H[e].empty, 1);
-    }
-    M.next_seq = 0;
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  pdl_wait();                                       // k_prep's staging (the prologue above overlaps it)
-  pdl_trigger();
-  __syncthreads();
-  if (tid >= kCW * 32) producer(A, M, tid & 31);
-  else consumer<EXACT>(A, M, P, tid >> 5, tid & 31);
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    if (atomicAdd(&A.work[1], 1) == (int)gridDim.x - 1) {
-      A.work[0] = 0;
-      A.work[1] = 0;
-    }
-  }
-}
-
-// ---- warp-autonomous step kernel (KS_WARP builds) ---------------------
+// ---- the step kernel k_step_w ---------------------
 // The round-1 execution model on this round's data layout and model code: one
 // warp per CTA, many CTAs per SM, no producer, no rounds.  Each warp claims a
 // tile, bulk-copies its block (descriptor + k_prep staging) into its own
@@ -1556,11 +1194,11 @@ __global__ void __launch_bounds__(32, KW_MINB) k_step_w(const __grid_constant__ 
   }
 }
 
-int step_smem_bytes() { return KS_WARP ? (int)sizeof(WSmem) : (int)sizeof(StepSmem); }
+int step_smem_bytes() { return (int)sizeof(WSmem); }
 
 }  // namespace sim
 
-// dev builds (-DKS_PROF): per-phase clock totals of k_step since the last call
+// dev builds (-DKW_TAIL): per-CTA finish times of the last k_step_w
 extern "C" int sim_debug_kw_finish(unsigned long long *out) {
 #ifdef KW_TAIL
   cudaDeviceSynchronize();
@@ -1572,49 +1210,18 @@ extern "C" int sim_debug_kw_finish(unsigned long long *out) {
 #endif
 }
 
-extern "C" int sim_debug_tile_cycles(unsigned int *out) {
-#ifdef KS_PROF
-  cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out, sim::g_tile_cyc, sizeof(sim::g_tile_cyc));
-  return 65536;
-#else
-  (void)out;
-  return 0;
-#endif
-}
-
-extern "C" int sim_debug_kstep_prof(unsigned long long *out) {
-#ifdef KS_PROF
-  cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out, sim::g_ks_prof, sizeof(sim::g_ks_prof));
-  static const unsigned long long z[32] = {0};
-  cudaMemcpyToSymbol(sim::g_ks_prof, z, sizeof(z));
-  return 32;
-#else
-  (void)out;
-  return 0;
-#endif
-}
-
 namespace sim {
 
-static int resident[2] = {0, 0};                    // resident blocks per GPU, per instantiation
+static int resident[2] = {0, 0};                    // resident CTAs per GPU, per instantiation
 void init_step_launch(int smem_bytes) {
   if (!resident[0]) {
     int dev = 0, nsm = 0, b0 = 0, b1 = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (KS_WARP) {
-      cudaFuncSetAttribute(k_step_w<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
-      cudaFuncSetAttribute(k_step_w<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b0, k_step_w<false>, 32, smem_bytes);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_step_w<true>, 32, smem_bytes);
-    } else {
-      cudaFuncSetAttribute(k_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
-      cudaFuncSetAttribute(k_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b0, k_step<false>, kStepThreads, smem_bytes);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_step<true>, kStepThreads, smem_bytes);
-    }
+    cudaFuncSetAttribute(k_step_w<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    cudaFuncSetAttribute(k_step_w<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b0, k_step_w<false>, 32, smem_bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_step_w<true>, 32, smem_bytes);
     resident[0] = std::max(1, b0) * std::max(1, nsm);
     resident[1] = std::max(1, b1) * std::max(1, nsm);
   }
@@ -1624,17 +1231,9 @@ void launch_step(const StepArgs &a, void *stream, int smem_bytes) {
   init_step_launch(smem_bytes);
   if (a.n_own <= 0) return;
   const int ex = a.exact_mode ? 1 : 0;
-  if (KS_WARP) {                                    // one warp per CTA, persistent
-    const int grid = std::min(a.n_own, resident[ex]);
-    if (ex) launch_pdl(k_step_w<true>, dim3(grid), dim3(32), smem_bytes, (cudaStream_t)stream, a);
-    else launch_pdl(k_step_w<false>, dim3(grid), dim3(32), smem_bytes, (cudaStream_t)stream, a);
-    return;
-  }
-  // enough CTAs for the work (a producer claims kGroup tiles at a time), at
-  // most the resident capacity (persistent)
-  const int grid = std::min((a.n_own + kGroup - 1) / kGroup, resident[ex]);
-  if (ex) launch_pdl(k_step<true>, dim3(grid), dim3(kStepThreads), smem_bytes, (cudaStream_t)stream, a);
-  else launch_pdl(k_step<false>, dim3(grid), dim3(kStepThreads), smem_bytes, (cudaStream_t)stream, a);
+  const int grid = std::min(a.n_own, resident[ex]);  // one warp per CTA, persistent
+  if (ex) launch_pdl(k_step_w<true>, dim3(grid), dim3(32), smem_bytes, (cudaStream_t)stream, a);
+  else launch_pdl(k_step_w<false>, dim3(grid), dim3(32), smem_bytes, (cudaStream_t)stream, a);
 }
 
 }  // namespace sim
