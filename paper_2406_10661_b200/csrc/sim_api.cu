@@ -255,6 +255,15 @@ sim_status fail(sim_s *h, sim_status st, const std::string &m) {
     }                                                                               \
   } while (0)
 
+// cudaMemset on the handle's stream, completed before returning: the legacy
+// default stream is not ordered with a non-blocking handle stream, so a plain
+// cudaMemset could land after (or before) the stream work that follows it
+cudaError_t dmemset(sim_s *h, void *p, int v, size_t bytes) {
+  cudaError_t e = cudaMemsetAsync(p, v, bytes, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  return e;
+}
+
 template <typename T>
 sim_status dalloc(sim_s *h, T **p, size_t n) {
   *p = nullptr;
@@ -271,8 +280,13 @@ sim_status dalloc(sim_s *h, T **p, size_t n) {
   h->allocs.push_back(*p);
   h->alloc_hooked.push_back(h->P.alloc ? 1 : 0);
   // zero-filled: unused slots of the record regions are read whole by the
-  // state reads (compute-sanitizer initcheck clean)
-  cudaError_t ez = cudaMemset(*p, 0, n * sizeof(T));
+  // state reads (compute-sanitizer initcheck clean).  On the handle's stream
+  // and completed here: a cudaMemset on the legacy default stream is not
+  // ordered with a non-blocking handle stream, so a buffer allocated lazily
+  // (the lane-order buffers of sim_read_state, the step-graph t word) could
+  // be zeroed after the kernel that filled it had run
+  cudaError_t ez = cudaMemsetAsync(*p, 0, n * sizeof(T), h->stream);
+  if (ez == cudaSuccess) ez = cudaStreamSynchronize(h->stream);
   if (ez != cudaSuccess) return fail(h, SIM_E_CUDA, std::string("cudaMemset: ") + cudaGetErrorString(ez));
   h->bytes += (int64_t)(n * sizeof(T));
   return SIM_OK;
@@ -1034,7 +1048,7 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   AL(P.desc_d, h->desc.size()); A.desc = P.desc_d;
   UP(i32, h->desc_off); A.desc_off = i32;
   uint8_t *sig; AL(sig, nl);
-  CK(h, cudaMemset(sig, 0, nl));
+  CK(h, dmemset(h, sig, 0, nl));
   A.lane_sig = sig;
   UP(i32, h->lane_tile); A.lane_tile = i32;
   uint8_t *u8; UP(u8, h->lane_local); A.lane_local = u8;
@@ -1054,9 +1068,9 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
     UP(i32, order); A.tiles = i32;
   }
   AL(A.work, 2);
-  CK(h, cudaMemset(A.work, 0, 8));
+  CK(h, dmemset(h, A.work, 0, 8));
   AL(A.bk_cnt, kNBucket);
-  CK(h, cudaMemset(A.bk_cnt, 0, kNBucket * 4));
+  CK(h, dmemset(h, A.bk_cnt, 0, kNBucket * 4));
   AL(A.bk_list, (size_t)kNBucket * nt);
   A.n_own = (int)P.tiles.size();
   A.rank = P.rank;
@@ -1064,9 +1078,9 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
     AL(P.inbox[b], h->n_slots);                   // vehicle records: stayers + inboxes
     AL(P.cnt[b], nt); AL(P.icnt[b], nt);
     AL(P.pubv[b], nv);
-    CK(h, cudaMemset(P.cnt[b], 0, nt * 4));
-    CK(h, cudaMemset(P.icnt[b], 0, nt * 4));
-    CK(h, cudaMemset(P.pubv[b], 0, nv * 4));
+    CK(h, dmemset(h, P.cnt[b], 0, nt * 4));
+    CK(h, dmemset(h, P.icnt[b], 0, nt * 4));
+    CK(h, dmemset(h, P.pubv[b], 0, nv * 4));
   }
   const int64_t sc = h->n_slots;
   AL(A.scratch, 8 * sc);
@@ -1091,7 +1105,7 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   CK(h, cudaMemcpy(P.route_d, h->route.data(), h->route.size() * 4, cudaMemcpyHostToDevice));
   UP(f, h->end_s); A.end_s = f; P.end_s_d = f;
   AL(P.patch_d, nv);
-  CK(h, cudaMemset(P.patch_d, 0xff, (size_t)nv * 4));
+  CK(h, dmemset(h, P.patch_d, 0xff, (size_t)nv * 4));
   UP(u8, h->vprof); A.veh_prof = u8;
   AL(A.insert_time, nv); AL(A.arrive_time, nv); AL(A.wait_fin, nv); AL(A.status, nv);
   UP(i32, h->depart); A.depart = i32;
@@ -1108,7 +1122,7 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
     AL(P.grp_d, (size_t)h->n_groups * (kNAcc + 1));
   }
   AL(A.tacc, (size_t)nt * kNAcc);
-  CK(h, cudaMemset(A.tacc, 0, (size_t)nt * kNAcc * 8));
+  CK(h, dmemset(h, A.tacc, 0, (size_t)nt * kNAcc * 8));
   AL(P.red_d, kNAcc + 3);
   AL(P.lanestat_d, 2 * (size_t)nl + h->nr);           // lane counts, waiting, road speeds
   if (h->world > 1 && !h->loopback) AL(P.xch_d, 3 * (size_t)nv + 8);   // one process per rank
@@ -1130,8 +1144,8 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
     }
     P.out_n = P.out_off[W]; P.in_n = P.in_off[W];
     AL(P.out_buf, P.out_n); AL(P.in_buf, P.in_n); AL(P.out_cnt, W);
-    CK(h, cudaMemset(P.out_cnt, 0, W * 4));
-    CK(h, cudaMemset(P.in_buf, 0, std::max<int64_t>(P.in_n, 1) * sizeof(MigRec)));
+    CK(h, dmemset(h, P.out_cnt, 0, W * 4));
+    CK(h, dmemset(h, P.in_buf, 0, std::max<int64_t>(P.in_n, 1) * sizeof(MigRec)));
     std::vector<int> off(P.out_off.begin(), P.out_off.end() - 1);
     UP(i32, off); A.out_off = i32;
     UP(i32, P.out_cap); A.out_cap = i32;
@@ -1155,7 +1169,7 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   }
   if (h->direct) {
     AL(P.bar_d, 1);
-    CK(h, cudaMemset(P.bar_d, 0, 4));
+    CK(h, dmemset(h, P.bar_d, 0, 4));
   }
   // signals (replicated: every partition runs every junction's controller)
   SignalArgs &G = P.SG;
@@ -1174,7 +1188,7 @@ sim_status alloc_part(sim_s *h, Part &P, const Plan *plan) {
   UP(i32, h->jl_succ); G.jl_succ = i32;
   G.mp_period = h->P.max_pressure_period > 0 ? h->P.max_pressure_period : 30;
   if (!h->lcnt[0])                                  // shared by loopback partitions
-    for (int b = 0; b < 3; ++b) { AL(h->lcnt[b], nl); CK(h, cudaMemset(h->lcnt[b], 0, nl * 4)); }
+    for (int b = 0; b < 3; ++b) { AL(h->lcnt[b], nl); CK(h, dmemset(h, h->lcnt[b], 0, nl * 4)); }
   // constants
   A.n_tiles = nt; A.n_lanes = nl; A.n_veh = nv;
   A.seed = h->P.seed;
@@ -1276,7 +1290,7 @@ sim_status setup_direct(sim_s *h) {
   if (h->P.barrier_timeout_ms > 0) h->bar_timeout_ns = (unsigned long long)h->P.barrier_timeout_ms * 1000000ull;
   sim_status st = dalloc(h, &h->bar_err_d, 1);
   if (st) return st;
-  CK(h, cudaMemset(h->bar_err_d, 0, 4));
+  CK(h, dmemset(h, h->bar_err_d, 0, 4));
   const size_t tmp = std::max<size_t>({(size_t)(kNAcc + 3) * 8, (2 * (size_t)h->nl + h->nr) * 4,
                                        (size_t)h->n_groups * (kNAcc + 1) * 8});
   char *t = nullptr;
@@ -2162,7 +2176,7 @@ sim_status sim_set_vehicle_route_batch(sim_handle h, int32_t m, const int32_t *v
   int32_t *d_vid = d, *d_idx = d + u, *d_out = d + 2 * u;
   CK(h, cudaMemcpy(d_vid, hv.data(), u * 4, cudaMemcpyHostToDevice));
   CK(h, cudaMemcpy(d_idx, hb.data(), u * 4, cudaMemcpyHostToDevice));
-  CK(h, cudaMemset(d_out, 0xff, 2 * (size_t)u * 4));
+  CK(h, dmemset(h, d_out, 0xff, 2 * (size_t)u * 4));
   for (size_t pi = 0; pi < h->parts.size(); ++pi) {
     Part &P = h->parts[pi];
     StepArgs a = step_args(P, h->t);
